@@ -1,0 +1,17 @@
+# TEST INFRASTRUCTURE ONLY.  Compiles the reference's own hot-path sources IN
+# PLACE from /root/reference (nothing is copied into this repo) together with
+# oracle/ref_shim.cpp into oracle/_ref/libhegmm_ref.so.  oracle/_ref/ is
+# git-ignored but travels to the GPU box with the gpurun snapshot.
+CXX ?= g++
+REF ?= /root/reference/proj
+HERE := $(dir $(abspath $(lastword $(MAKEFILE_LIST))))
+OUT := $(HERE)_ref
+SRCS := $(REF)/src/matrix.cpp $(REF)/src/backend.cpp $(REF)/src/lintrans.cpp $(REF)/src/algorithms.cpp
+
+all: $(OUT)/libhegmm_ref.so
+
+$(OUT)/libhegmm_ref.so: $(SRCS) $(HERE)ref_shim.cpp $(HERE)bfv_oracle.cpp $(HERE)bfv_oracle.h
+	mkdir -p $(OUT)
+	$(CXX) -O2 -std=c++20 -fPIC -shared -I$(REF)/include -I$(HERE) -o $@ \
+	    $(SRCS) $(HERE)ref_shim.cpp $(HERE)bfv_oracle.cpp -lpthread
+.PHONY: all
