@@ -1,0 +1,132 @@
+/*
+ * hegmm_b200.h -- C ABI of the B200 HE-primitive library (libhegmm_b200.so).
+ *
+ * This is the drop-in boundary for the reference's backend contract
+ * `hegmm::Backend` (/root/reference/proj/include/hegmm/backend.hpp:107-127).
+ * Each entry point replaces one virtual of that interface; a C++ adapter that
+ * implements `hegmm::Backend` on top of these calls is given in
+ * integration/bfv_gpu_backend.cpp and INTEGRATION.md.
+ *
+ *   hgm_ctx            <- one backend session (SlotBackend ctor, backend.cpp:114-116)
+ *   hgm_encrypt        <- Backend::encrypt   (backend.hpp:113, backend.cpp:118-134)
+ *   hgm_decrypt        <- Backend::decrypt   (backend.hpp:114, backend.cpp:136-139)
+ *   hgm_add            <- Backend::he_add    (backend.hpp:116, backend.cpp:141-153)
+ *   hgm_mul            <- Backend::he_mult   (backend.hpp:117, backend.cpp:155-167)
+ *   hgm_cmul           <- Backend::he_cmult  (backend.hpp:118, backend.cpp:169-183)
+ *   hgm_rot            <- Backend::he_rot    (backend.hpp:119, backend.cpp:185-197)
+ *   hgm_stats / hgm_reset_stats / hgm_peak_live / hgm_set_phase / hgm_phase
+ *                      <- Backend::stats/reset_stats/peak_live_ciphertexts/
+ *                         set_phase/phase   (backend.hpp:121-126)
+ *   hgm_apply_plan     <- apply_plan (lintrans.hpp:161-165, lintrans.cpp:433-461):
+ *                         sum_z mask_z .* Rot(ct, z) with one hoisted ModUp
+ *   hgm_matmul_batch   <- basic_mm / enhanced_mm (algorithms.hpp:59-66) over a
+ *                         batch of independent instances in lockstep
+ *
+ * Conventions: every call returns HGM_OK (0) or an error code and never throws
+ * across the ABI; hgm_last_error() gives the thread-local message.  Error codes
+ * map to the reference exception types (errors.hpp:17-37):
+ *   HGM_EDIM -> DimensionError, HGM_ECAP -> CapacityError,
+ *   HGM_EOVERFLOW -> OverflowError, anything else -> Error.
+ * Ciphertexts are immutable, reference counted handles owned by the caller
+ * (hgm_ct_release).  Operations are recorded and executed lazily on the GPU;
+ * hgm_decrypt / hgm_ct_export / hgm_flush force execution.  A handle must be
+ * released before its context is destroyed.
+ * Slot semantics: slot_count = N/2 values per ciphertext row, values mod
+ * t = 65537, decrypted values canonical in [0, t); rotation is cyclic over the
+ * full N/2-slot row ("Row semantics").
+ */
+#ifndef HEGMM_B200_H
+#define HEGMM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    HGM_OK = 0,
+    HGM_EDIM = 1,
+    HGM_ECAP = 2,
+    HGM_EINTERNAL = 3,
+    HGM_EOVERFLOW = 4,
+    HGM_ECUDA = 5,
+    HGM_EARG = 6
+};
+
+enum { HGM_PHASE_CLIENT = 0, HGM_PHASE_CLOUD = 1 };
+
+/* Parameter sets: 0 = N 8192 / 3x60-bit Q / 1 special prime / dnum 3 (configs 1-4),
+ * 1 = N 32768 / 8x55-bit Q / 4 special primes / dnum 2 (config 5),
+ * 2 = N 4096 small test set. */
+typedef struct hgm_ctx hgm_ctx;
+typedef struct hgm_ct hgm_ct;
+
+hgm_ctx* hgm_ctx_create(int param_id, uint64_t seed, int device);
+void hgm_ctx_destroy(hgm_ctx* ctx);
+const char* hgm_last_error(void);
+
+/* info[0]=N [1]=L [2]=K [3]=nB [4]=dnum [5]=t [6]=alpha [7]=seed, then primes */
+int hgm_ctx_info(const hgm_ctx* ctx, uint64_t* info, size_t cap);
+size_t hgm_slot_count(const hgm_ctx* ctx);
+size_t hgm_ct_words(const hgm_ctx* ctx);
+
+/* encrypt uses (and advances) the session's encryption counter; the
+ * _at variant takes it explicitly (the counter selects u, e0, e1). */
+int hgm_encrypt(hgm_ctx* ctx, const int64_t* values, size_t S, hgm_ct** out);
+int hgm_encrypt_at(hgm_ctx* ctx, const int64_t* values, size_t S, uint64_t counter, hgm_ct** out);
+int hgm_decrypt(hgm_ctx* ctx, const hgm_ct* ct, int64_t* out, size_t cap);
+int hgm_add(hgm_ctx* ctx, const hgm_ct* x, const hgm_ct* y, hgm_ct** out);
+int hgm_mul(hgm_ctx* ctx, const hgm_ct* x, const hgm_ct* y, hgm_ct** out);
+int hgm_cmul(hgm_ctx* ctx, const hgm_ct* x, const int64_t* mask, size_t S, hgm_ct** out);
+int hgm_rot(hgm_ctx* ctx, const hgm_ct* x, int64_t offset, hgm_ct** out);
+/* offsets[n], masks[n][S] (row-major); counts n cmult, n-1 add and one rot
+ * per non-zero offset, as apply_plan does. */
+int hgm_apply_plan(hgm_ctx* ctx, const hgm_ct* x, size_t n, const int64_t* offsets,
+                   const int64_t* masks, size_t S, hgm_ct** out);
+
+int hgm_flush(hgm_ctx* ctx);
+int hgm_ct_export(hgm_ctx* ctx, const hgm_ct* ct, uint64_t* words);
+int hgm_ct_import(hgm_ctx* ctx, const uint64_t* words, size_t S, size_t depth, hgm_ct** out);
+size_t hgm_ct_segment(const hgm_ct* ct);
+size_t hgm_ct_depth(const hgm_ct* ct);
+int hgm_ct_phase(const hgm_ct* ct);
+hgm_ct* hgm_ct_retain(hgm_ct* ct);
+void hgm_ct_release(hgm_ct* ct);
+
+/* stats[2*k + {0: client, 1: cloud}] for k = add, mult_cc, mult_cp, rot,
+ * encrypt, decrypt (OpStats field order, backend.hpp:50-57). */
+int hgm_stats(const hgm_ctx* ctx, uint64_t stats[12]);
+int hgm_reset_stats(hgm_ctx* ctx);
+size_t hgm_peak_live(const hgm_ctx* ctx);
+int hgm_set_phase(hgm_ctx* ctx, int phase);
+int hgm_phase(const hgm_ctx* ctx);
+
+/* Batched HEGMM: `count` independent products C_i = A_i B_i (A_i m x l, B_i
+ * l x n, row-major int64) through basic_mm (algo 0) or enhanced_mm (algo 1),
+ * order -1 auto / 0 column-major / 1 row-major.  Inputs and outputs are host
+ * buffers; outputs canonical mod t.  Instance i encrypts with counters
+ * counter0 + i * E, E = encryptions per instance (3 basic, 2 enhanced).
+ * stats (optional) receives one instance's counts (identical for all). */
+int hgm_matmul_batch(hgm_ctx* ctx, int algo, int order, size_t m, size_t l, size_t n,
+                     size_t count, const int64_t* A, const int64_t* B, int64_t* C,
+                     uint64_t counter0, uint64_t* stats);
+/* same, also exporting every instance's final (pre-decrypt) ciphertext */
+int hgm_matmul_batch_export(hgm_ctx* ctx, int algo, int order, size_t m, size_t l, size_t n,
+                            size_t count, const int64_t* A, const int64_t* B, int64_t* C,
+                            uint64_t counter0, uint64_t* final_words);
+
+/* Kernel-level timing hooks for bench.py (CUDA events on the library stream). */
+int hgm_bench_ntt(hgm_ctx* ctx, int forward, size_t limbs, int iters, float* ms_per_iter);
+int hgm_device_sync(hgm_ctx* ctx);
+/* Test hook: in-place NTT of `count` host limbs (count*N words) under one
+ * prime (index into Q ++ P ++ B, or -1 for t). */
+int hgm_test_ntt(hgm_ctx* ctx, int forward, int prime, uint64_t* data, size_t count);
+/* Number of this library's kernels launched on the context so far. */
+uint64_t hgm_launch_count(const hgm_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,292 @@
+"""paper_2405_02238_b200 -- B200-native HE primitives behind the HEGMM backend contract.
+
+Thin ctypes mirror of the C ABI in ``include/hegmm_b200.h`` (which itself
+mirrors ``hegmm::Backend``, /root/reference/proj/include/hegmm/backend.hpp:107-127).
+All arithmetic runs in ``libhegmm_b200.so`` (hand-written sm_100a CUDA); this
+module only marshals host buffers.  There is no CPU fallback: importing the
+module without the built library, or creating a context without a GPU, raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhegmm_b200.so")
+
+HGM_OK, HGM_EDIM, HGM_ECAP, HGM_EINTERNAL, HGM_EOVERFLOW, HGM_ECUDA, HGM_EARG = range(7)
+PHASE_CLIENT, PHASE_CLOUD = 0, 1
+# C ABI symbols declared in include/hegmm_b200.h
+EXPORTS = (
+    "hgm_ctx_create", "hgm_ctx_destroy", "hgm_last_error", "hgm_ctx_info", "hgm_slot_count",
+    "hgm_ct_words", "hgm_encrypt", "hgm_encrypt_at", "hgm_decrypt", "hgm_add", "hgm_mul",
+    "hgm_cmul", "hgm_rot", "hgm_apply_plan", "hgm_flush", "hgm_ct_export", "hgm_ct_import",
+    "hgm_ct_segment", "hgm_ct_depth", "hgm_ct_phase", "hgm_ct_retain", "hgm_ct_release",
+    "hgm_stats", "hgm_reset_stats", "hgm_peak_live", "hgm_set_phase", "hgm_phase",
+    "hgm_matmul_batch", "hgm_matmul_batch_export", "hgm_bench_ntt", "hgm_device_sync",
+    "hgm_test_ntt", "hgm_launch_count",
+)
+
+
+class HEError(RuntimeError):
+    """Base error (reference hegmm::Error, errors.hpp:10-14)."""
+
+
+class DimensionError(HEError):
+    """Operand shapes are incompatible (errors.hpp:17-21)."""
+
+
+class CapacityError(HEError):
+    """Working set exceeds the slot budget (errors.hpp:23-27)."""
+
+
+class OverflowError_(HEError):
+    """Exact arithmetic would overflow (errors.hpp:29-33)."""
+
+
+_ERRORS = {HGM_EDIM: DimensionError, HGM_ECAP: CapacityError, HGM_EOVERFLOW: OverflowError_}
+
+_lib: Optional[ctypes.CDLL] = None
+_vp, _sz, _u64, _i64, _int = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int
+
+
+def lib() -> ctypes.CDLL:
+    """Load the CUDA library (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing; run `make -C paper_2405_02238_b200` "
+                          "(or __graft_entry__.build()) first -- there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    sig = {
+        "hgm_ctx_create": (_vp, [_int, _u64, _int]),
+        "hgm_ctx_destroy": (None, [_vp]),
+        "hgm_last_error": (ctypes.c_char_p, []),
+        "hgm_ctx_info": (_int, [_vp, _vp, _sz]),
+        "hgm_slot_count": (_sz, [_vp]),
+        "hgm_ct_words": (_sz, [_vp]),
+        "hgm_encrypt": (_int, [_vp, _vp, _sz, _vp]),
+        "hgm_encrypt_at": (_int, [_vp, _vp, _sz, _u64, _vp]),
+        "hgm_decrypt": (_int, [_vp, _vp, _vp, _sz]),
+        "hgm_add": (_int, [_vp, _vp, _vp, _vp]),
+        "hgm_mul": (_int, [_vp, _vp, _vp, _vp]),
+        "hgm_cmul": (_int, [_vp, _vp, _vp, _sz, _vp]),
+        "hgm_rot": (_int, [_vp, _vp, _i64, _vp]),
+        "hgm_apply_plan": (_int, [_vp, _vp, _sz, _vp, _vp, _sz, _vp]),
+        "hgm_flush": (_int, [_vp]),
+        "hgm_ct_export": (_int, [_vp, _vp, _vp]),
+        "hgm_ct_import": (_int, [_vp, _vp, _sz, _sz, _vp]),
+        "hgm_ct_segment": (_sz, [_vp]),
+        "hgm_ct_depth": (_sz, [_vp]),
+        "hgm_ct_phase": (_int, [_vp]),
+        "hgm_ct_retain": (_vp, [_vp]),
+        "hgm_ct_release": (None, [_vp]),
+        "hgm_stats": (_int, [_vp, _vp]),
+        "hgm_reset_stats": (_int, [_vp]),
+        "hgm_peak_live": (_sz, [_vp]),
+        "hgm_set_phase": (_int, [_vp, _int]),
+        "hgm_phase": (_int, [_vp]),
+        "hgm_matmul_batch": (_int, [_vp, _int, _int, _sz, _sz, _sz, _sz, _vp, _vp, _vp, _u64, _vp]),
+        "hgm_matmul_batch_export": (_int, [_vp, _int, _int, _sz, _sz, _sz, _sz, _vp, _vp, _vp, _u64, _vp]),
+        "hgm_bench_ntt": (_int, [_vp, _int, _sz, _int, _vp]),
+        "hgm_device_sync": (_int, [_vp]),
+        "hgm_test_ntt": (_int, [_vp, _int, _int, _vp, _sz]),
+        "hgm_launch_count": (_u64, [_vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def _check(rc: int) -> None:
+    if rc != HGM_OK:
+        msg = lib().hgm_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, HEError)(msg)
+
+
+def _ptr(a: np.ndarray) -> ctypes.c_void_p:
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _as_i64(v) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(v, dtype=np.int64))
+
+
+class Ciphertext:
+    """Immutable handle (reference Ciphertext, backend.hpp:88-103)."""
+
+    __slots__ = ("_h", "_ctx")
+
+    def __init__(self, handle: int, ctx: "Context"):
+        self._h = handle
+        self._ctx = ctx
+
+    def segment_length(self) -> int:
+        return lib().hgm_ct_segment(self._h)
+
+    def depth(self) -> int:
+        return lib().hgm_ct_depth(self._h)
+
+    def phase_tag(self) -> int:
+        return lib().hgm_ct_phase(self._h)
+
+    def release(self) -> None:
+        if self._h:
+            lib().hgm_ct_release(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
+
+class Context:
+    """One backend session on one GPU (reference SlotBackend, backend.hpp:132-163)."""
+
+    def __init__(self, param_id: int = 0, seed: int = 1, device: int = 0):
+        L = lib()
+        h = L.hgm_ctx_create(param_id, seed, device)
+        if not h:
+            raise HEError(L.hgm_last_error().decode(errors="replace"))
+        self._h = h
+        info = np.zeros(64, dtype=np.uint64)
+        _check(L.hgm_ctx_info(h, _ptr(info), 64))
+        self.N, self.L, self.K, self.nB, self.dnum, self.t = (int(x) for x in info[:6])
+        self.primes = [int(x) for x in info[8:8 + self.L + self.K + self.nB]]
+        self.slot_count = self.N // 2
+        self.ct_words = 2 * self.L * self.N
+
+    def close(self) -> None:
+        if self._h:
+            lib().hgm_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- backend contract ------------------------------------------------------
+    def _out(self) -> ctypes.c_void_p:
+        return ctypes.c_void_p()
+
+    def encrypt(self, values: Sequence[int], counter: Optional[int] = None) -> Ciphertext:
+        v = _as_i64(values)
+        out = self._out()
+        if counter is None:
+            _check(lib().hgm_encrypt(self._h, _ptr(v), v.size, ctypes.byref(out)))
+        else:
+            _check(lib().hgm_encrypt_at(self._h, _ptr(v), v.size, counter, ctypes.byref(out)))
+        return Ciphertext(out.value, self)
+
+    def decrypt(self, ct: Ciphertext) -> np.ndarray:
+        S = ct.segment_length()
+        out = np.zeros(S, dtype=np.int64)
+        _check(lib().hgm_decrypt(self._h, ct._h, _ptr(out), S))
+        return out
+
+    def he_add(self, x: Ciphertext, y: Ciphertext) -> Ciphertext:
+        out = self._out()
+        _check(lib().hgm_add(self._h, x._h, y._h, ctypes.byref(out)))
+        return Ciphertext(out.value, self)
+
+    def he_mult(self, x: Ciphertext, y: Ciphertext) -> Ciphertext:
+        out = self._out()
+        _check(lib().hgm_mul(self._h, x._h, y._h, ctypes.byref(out)))
+        return Ciphertext(out.value, self)
+
+    def he_cmult(self, x: Ciphertext, mask: Sequence[int]) -> Ciphertext:
+        m = _as_i64(mask)
+        out = self._out()
+        _check(lib().hgm_cmul(self._h, x._h, _ptr(m), m.size, ctypes.byref(out)))
+        return Ciphertext(out.value, self)
+
+    def he_rot(self, x: Ciphertext, offset: int) -> Ciphertext:
+        out = self._out()
+        _check(lib().hgm_rot(self._h, x._h, int(offset), ctypes.byref(out)))
+        return Ciphertext(out.value, self)
+
+    def apply_plan(self, x: Ciphertext, offsets: Sequence[int], masks: np.ndarray) -> Ciphertext:
+        off = _as_i64(offsets)
+        m = _as_i64(masks).reshape(len(off), -1) if len(off) else np.zeros((0, 0), np.int64)
+        out = self._out()
+        _check(lib().hgm_apply_plan(self._h, x._h, off.size, _ptr(off), _ptr(m),
+                                    m.shape[1] if m.size else 0, ctypes.byref(out)))
+        return Ciphertext(out.value, self)
+
+    def stats(self) -> np.ndarray:
+        s = np.zeros(12, dtype=np.uint64)
+        _check(lib().hgm_stats(self._h, _ptr(s)))
+        return s
+
+    def reset_stats(self) -> None:
+        _check(lib().hgm_reset_stats(self._h))
+
+    def peak_live_ciphertexts(self) -> int:
+        return lib().hgm_peak_live(self._h)
+
+    def set_phase(self, phase: int) -> None:
+        _check(lib().hgm_set_phase(self._h, phase))
+
+    def phase(self) -> int:
+        return lib().hgm_phase(self._h)
+
+    # -- extras ---------------------------------------------------------------
+    def export(self, ct: Ciphertext) -> np.ndarray:
+        w = np.zeros(self.ct_words, dtype=np.uint64)
+        _check(lib().hgm_ct_export(self._h, ct._h, _ptr(w)))
+        return w
+
+    def import_ct(self, words: np.ndarray, segment: int, depth: int = 0) -> Ciphertext:
+        w = np.ascontiguousarray(words, dtype=np.uint64)
+        out = self._out()
+        _check(lib().hgm_ct_import(self._h, _ptr(w), segment, depth, ctypes.byref(out)))
+        return Ciphertext(out.value, self)
+
+    def matmul_batch(self, A: np.ndarray, B: np.ndarray, algo: int = 0, order: int = -1,
+                     counter0: int = 0, export: bool = False):
+        """C_i = A_i B_i mod t for a batch (count, m, l) x (count, l, n)."""
+        A = _as_i64(A)
+        B = _as_i64(B)
+        if A.ndim == 2:
+            A, B = A[None], B[None]
+        cnt, m, l = A.shape
+        n = B.shape[2]
+        if B.shape[:2] != (cnt, l):
+            raise DimensionError(f"product shape mismatch: {A.shape} * {B.shape}")
+        C = np.zeros((cnt, m, n), dtype=np.int64)
+        if export:
+            words = np.zeros((cnt, self.ct_words), dtype=np.uint64)
+            _check(lib().hgm_matmul_batch_export(self._h, algo, order, m, l, n, cnt, _ptr(A), _ptr(B),
+                                                 _ptr(C), counter0, _ptr(words)))
+            return C, words
+        stats = np.zeros(12, dtype=np.uint64)
+        _check(lib().hgm_matmul_batch(self._h, algo, order, m, l, n, cnt, _ptr(A), _ptr(B), _ptr(C),
+                                      counter0, _ptr(stats)))
+        return C, stats
+
+    def test_ntt(self, data: np.ndarray, prime: int, forward: bool = True) -> np.ndarray:
+        d = np.ascontiguousarray(data, dtype=np.uint64).copy()
+        _check(lib().hgm_test_ntt(self._h, 1 if forward else 0, prime, _ptr(d), d.size // self.N))
+        return d
+
+    def bench_ntt(self, limbs: int, iters: int = 20, forward: bool = True) -> float:
+        ms = ctypes.c_float()
+        _check(lib().hgm_bench_ntt(self._h, 1 if forward else 0, limbs, iters, ctypes.byref(ms)))
+        return ms.value
+
+    def sync(self) -> None:
+        _check(lib().hgm_device_sync(self._h))
+
+    def launch_count(self) -> int:
+        return int(lib().hgm_launch_count(self._h))

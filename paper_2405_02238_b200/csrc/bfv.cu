@@ -1,0 +1,935 @@
+// bfv.cu -- RNS-BFV primitive kernels and the Context that launches them.
+//
+// Semantics are defined by oracle/bfv_oracle.cpp (bit-exact); the comments
+// name the oracle routine each kernel reproduces.  Shapes: n items per launch,
+// thread per (item, coefficient), loops over RNS limbs inside the thread so a
+// warp's loads are coalesced within each limb.
+#include <cstring>
+#include <stdexcept>
+
+#include "context.hpp"
+
+namespace hgm {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// values with |v| < q (noise, ternary, small messages)
+__device__ __forceinline__ u64 small_to_mod(i64 v, u64 q) { return v >= 0 ? (u64)v : q + v; }
+// y < src < 2*dst (all primes of a set share their bit length): centred y mod dst
+__device__ __forceinline__ u64 centred_lift(u64 y, u64 src, u64 dst) {
+    if (y > (src - 1) / 2) {
+        u64 m = src - y;
+        if (m >= dst) m -= dst;
+        return m ? dst - m : 0;
+    }
+    return y >= dst ? y - dst : y;
+}
+
+#define ITEM_LOOP for (u32 item = blockIdx.y; item < n; item += gridDim.y)
+#define COEF_LOOP for (u32 j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x)
+
+// ---------------------------------------------------------------- encoding
+// oracle encode(): slot values mod t scattered to their NTT positions
+__global__ void k_encode_scatter(const DevParams* __restrict__ dp, u32 n, const i64* vals,
+                                 const u32* S, u64* out) {
+    const u32 N = dp->N, H = N / 2;
+    ITEM_LOOP {
+        COEF_LOOP {
+            u64 v = 0;
+            if (j < S[item]) {
+                const i64 x = vals[(size_t)item * H + j];
+                v = x >= 0 ? (u64)x % kT : kT - 1 - ((u64)(-(x + 1)) % kT);
+            }
+            out[(size_t)item * N + dp->slot_ntt[j]] = v;
+        }
+    }
+}
+
+// oracle encrypt(): sample u, e0, e1; c0 = e0 + Delta m, c1 = e1 (coefficient form)
+__global__ void k_enc_lift(const DevParams* __restrict__ dp, u32 n, const u64* m, const u64* ctr,
+                           u64* U, u64* const* out) {
+    const u32 N = dp->N, L = dp->L;
+    const u64 seed = dp->seed;
+    ITEM_LOOP {
+        const u64 c = ctr[item];
+        u64* o = out[item];
+        COEF_LOOP {
+            const i64 u = ternary(seed, kStreamEncU | c, j);
+            const i64 e0 = gauss(seed, kStreamEncE0 | c, j, dp->cdt);
+            const i64 e1 = gauss(seed, kStreamEncE1 | c, j, dp->cdt);
+            const u64 mj = m[(size_t)item * N + j];
+            for (u32 i = 0; i < L; ++i) {
+                const u64 q = dp->pr[i].q;
+                U[((size_t)item * L + i) * N + j] = small_to_mod(u, q);
+                o[(size_t)i * N + j] =
+                    add_mod(small_to_mod(e0, q), shoup_mul(mj, dp->delta[i], dp->delta_sh[i], q), q);
+                o[(size_t)(L + i) * N + j] = small_to_mod(e1, q);
+            }
+        }
+    }
+}
+
+__global__ void k_enc_finish(const DevParams* __restrict__ dp, u32 n, const u64* U, const u64* pk,
+                             u64* const* out) {
+    const u32 N = dp->N, L = dp->L;
+    ITEM_LOOP {
+        u64* o = out[item];
+        COEF_LOOP {
+            for (u32 i = 0; i < L; ++i) {
+                const Prime& P = dp->pr[i];
+                const u64 u = U[((size_t)item * L + i) * N + j];
+                const size_t w0 = (size_t)i * N + j, w1 = (size_t)(L + i) * N + j;
+                o[w0] = add_mod(mul_mod(pk[w0], u, P), o[w0], P.q);
+                o[w1] = add_mod(mul_mod(pk[w1], u, P), o[w1], P.q);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- decryption
+__global__ void k_dec_phase(const DevParams* __restrict__ dp, u32 n, const u64* const* in,
+                            const u64* sk, u64* X) {
+    const u32 N = dp->N, L = dp->L;
+    ITEM_LOOP {
+        const u64* c = in[item];
+        COEF_LOOP {
+            for (u32 i = 0; i < L; ++i) {
+                const Prime& P = dp->pr[i];
+                X[((size_t)item * L + i) * N + j] =
+                    add_mod(c[(size_t)i * N + j], mul_mod(c[(size_t)(L + i) * N + j], sk[(size_t)i * N + j], P), P.q);
+            }
+        }
+    }
+}
+
+// oracle decrypt(): m = round(t x / Q) mod t via sum_i [x_i (Q/q_i)^-1]_{q_i} t/q_i
+__global__ void k_dec_round(const DevParams* __restrict__ dp, u32 n, const u64* X, u64* M) {
+    const u32 N = dp->N, L = dp->L;
+    ITEM_LOOP {
+        COEF_LOOP {
+            Acc128 s{0, 0};
+            for (u32 i = 0; i < L; ++i) {
+                const u64 q = dp->pr[i].q;
+                const u64 y = shoup_mul(X[((size_t)item * L + i) * N + j], dp->qhat_inv[i], dp->qhat_inv_sh[i], q);
+                fx_add(s, y, dp->t_over_q[i]);
+            }
+            M[(size_t)item * N + j] = fx_round(s) % kT;
+        }
+    }
+}
+
+__global__ void k_dec_gather(const DevParams* __restrict__ dp, u32 n, const u64* M, const u32* S,
+                             i64* out) {
+    const u32 N = dp->N, H = N / 2;
+    ITEM_LOOP {
+        for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < S[item]; i += gridDim.x * blockDim.x)
+            out[(size_t)item * H + i] = (i64)M[(size_t)item * N + dp->slot_ntt[i]];
+    }
+}
+
+// ---------------------------------------------------------------- linear ops
+__global__ void k_add(const DevParams* __restrict__ dp, u32 n, const u64* const* a,
+                      const u64* const* b, u64* const* out) {
+    const u32 N = dp->N, L = dp->L;
+    const size_t W = (size_t)2 * L * N;
+    ITEM_LOOP {
+        const u64 *x = a[item], *y = b[item];
+        u64* o = out[item];
+        for (size_t w = (size_t)blockIdx.x * blockDim.x + threadIdx.x; w < W; w += (size_t)gridDim.x * blockDim.x) {
+            const u64 q = dp->pr[(w / N) % L].q;
+            o[w] = add_mod(x[w], y[w], q);
+        }
+    }
+}
+
+__global__ void k_copy(u32 n, size_t W, const u64* const* in, u64* const* out) {
+    ITEM_LOOP {
+        const ulonglong2* x = reinterpret_cast<const ulonglong2*>(in[item]);
+        ulonglong2* o = reinterpret_cast<ulonglong2*>(out[item]);
+        for (size_t w = (size_t)blockIdx.x * blockDim.x + threadIdx.x; w < W / 2; w += (size_t)gridDim.x * blockDim.x)
+            o[w] = x[w];
+    }
+}
+
+// out[o] = sum_t in[t] (.* mask[t]) : oracle cmult() followed by add()
+__global__ void k_lincomb(const DevParams* __restrict__ dp, u32 n, const u32* off,
+                          const u64* const* in, const u64* const* mask, u64* const* out) {
+    const u32 N = dp->N, L = dp->L;
+    const size_t LN = (size_t)L * N, W = 2 * LN;
+    ITEM_LOOP {
+        const u32 t0 = off[item], t1 = off[item + 1];
+        u64* o = out[item];
+        for (size_t w = (size_t)blockIdx.x * blockDim.x + threadIdx.x; w < W; w += (size_t)gridDim.x * blockDim.x) {
+            const size_t wl = w < LN ? w : w - LN;
+            const Prime& P = dp->pr[wl / N];
+            u64 acc = 0;
+            for (u32 t = t0; t < t1; ++t) {
+                u64 v = in[t][w];
+                if (mask[t]) v = mul_mod(v, mask[t][wl], P);
+                acc = add_mod(acc, v, P.q);
+            }
+            o[w] = acc;
+        }
+    }
+}
+
+// centred lift of the mod-t mask polynomial to each q_i (oracle cmult())
+__global__ void k_mask_lift(const DevParams* __restrict__ dp, const u64* m, u64* out) {
+    const u32 N = dp->N, L = dp->L;
+    const u32 n = 1;
+    ITEM_LOOP {
+        COEF_LOOP {
+            const u64 v = m[j];
+            for (u32 i = 0; i < L; ++i) out[(size_t)i * N + j] = centred_lift(v, kT, dp->pr[i].q);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- key switching
+// c1 limbs of each ct into a contiguous [n][L][N] buffer
+__global__ void k_gather_c1(const DevParams* __restrict__ dp, u32 n, const u64* const* ct, u64* C) {
+    const u32 N = dp->N, L = dp->L;
+    const size_t LN = (size_t)L * N;
+    ITEM_LOOP {
+        const u64* c = ct[item] + LN;
+        for (size_t w = (size_t)blockIdx.x * blockDim.x + threadIdx.x; w < LN; w += (size_t)gridDim.x * blockDim.x)
+            C[item * LN + w] = c[w];
+    }
+}
+
+// oracle key_switch() ModUp: digit dg of the coefficient-domain poly C, lifted
+// to every limb of Q ++ P with centred residues.  D: [n][dnum][R][N]
+__global__ void k_modup_lift(const DevParams* __restrict__ dp, u32 n, const u64* C, size_t c_stride,
+                             u64* D) {
+    const u32 N = dp->N, L = dp->L, R = dp->R, A = dp->alpha, dnum = dp->dnum;
+    ITEM_LOOP {
+        const u64* c = C + item * c_stride;
+        u64* d = D + (size_t)item * dnum * R * N;
+        COEF_LOOP {
+            u64 x[kMaxL];
+            for (u32 i = 0; i < L; ++i) x[i] = c[(size_t)i * N + j];
+            for (u32 dg = 0; dg < dnum; ++dg) {
+                u64 y[kMaxL];
+                for (u32 a = 0; a < A; ++a) {
+                    const u32 i = dg * A + a;
+                    y[a] = shoup_mul(x[i], dp->dg_hat_inv[i], dp->dg_hat_inv_sh[i], dp->pr[i].q);
+                }
+                for (u32 r = 0; r < R; ++r) {
+                    u64 v;
+                    if (r < L && r / A == dg) {
+                        v = x[r];
+                    } else {
+                        const u64 qr = dp->pr[r].q;
+                        v = 0;
+                        for (u32 a = 0; a < A; ++a) {
+                            const u32 i = dg * A + a;
+                            const u64 yl = centred_lift(y[a], dp->pr[i].q, qr);
+                            v = add_mod(v, shoup_mul(yl, dp->dg_hat[i][r], dp->dg_hat_sh[i][r], qr), qr);
+                        }
+                    }
+                    d[((size_t)dg * R + r) * N + j] = v;
+                }
+            }
+        }
+    }
+}
+
+// acc[c][r] = sum_dg D[dg][r][galois_src(k)] * key[dg][c][r][k]  ([n][2][R][N])
+__global__ void k_ks_inner(const DevParams* __restrict__ dp, u32 n, const u64* const* D,
+                           const u64* const* key, const u32* g, u64* const* acc) {
+    const u32 N = dp->N, R = dp->R, dnum = dp->dnum, logN = dp->logN;
+    ITEM_LOOP {
+        const u64* d = D[item];
+        const u64* k = key[item];
+        u64* a = acc[item];
+        const u32 ge = g[item];
+        COEF_LOOP {
+            const u32 src = ge == 1 ? j : galois_src(j, ge, logN);
+            for (u32 r = 0; r < R; ++r) {
+                const Prime& P = dp->pr[r];
+                u64 a0 = 0, a1 = 0;
+                for (u32 dg = 0; dg < dnum; ++dg) {
+                    const u64 x = d[((size_t)dg * R + r) * N + src];
+                    a0 = add_mod(a0, mul_mod(x, k[(((size_t)dg * 2 + 0) * R + r) * N + j], P), P.q);
+                    a1 = add_mod(a1, mul_mod(x, k[(((size_t)dg * 2 + 1) * R + r) * N + j], P), P.q);
+                }
+                a[(size_t)r * N + j] = a0;
+                a[((size_t)R + r) * N + j] = a1;
+            }
+        }
+    }
+}
+
+// ModDown correction: V[c][i] = sum_k centred([w_k (P/p_k)^-1]_{p_k}) (P/p_k) mod q_i
+__global__ void k_moddown_conv(const DevParams* __restrict__ dp, u32 n, const u64* const* acc, u64* V) {
+    const u32 N = dp->N, L = dp->L, K = dp->K, R = dp->R;
+    ITEM_LOOP {
+        const u32 c = blockIdx.z;
+        const u64* a = acc[item] + (size_t)c * R * N;
+        u64* v = V + ((size_t)item * 2 + c) * L * N;
+        COEF_LOOP {
+            u64 z[kMaxK];
+            for (u32 k = 0; k < K; ++k) {
+                const u64 p = dp->pr[L + k].q;
+                z[k] = shoup_mul(a[(size_t)(L + k) * N + j], dp->phat_inv[k], dp->phat_inv_sh[k], p);
+            }
+            for (u32 i = 0; i < L; ++i) {
+                const u64 q = dp->pr[i].q;
+                u64 s = 0;
+                for (u32 k = 0; k < K; ++k) {
+                    const u64 zl = centred_lift(z[k], dp->pr[L + k].q, q);
+                    s = add_mod(s, shoup_mul(zl, dp->phat_mod_q[k][i], dp->phat_mod_q_sh[k][i], q), q);
+                }
+                v[(size_t)i * N + j] = s;
+            }
+        }
+    }
+}
+
+// out0 = (acc0 - V0) P^-1 + add0[galois_src]; out1 = (acc1 - V1) P^-1 (+ add1)
+__global__ void k_ks_finish(const DevParams* __restrict__ dp, u32 n, const u64* const* acc,
+                            const u64* V, const u64* const* add0, const u32* g0,
+                            const u64* const* add1, u64* const* out) {
+    const u32 N = dp->N, L = dp->L, R = dp->R, logN = dp->logN;
+    ITEM_LOOP {
+        const u64* a = acc[item];
+        const u64* v = V + (size_t)item * 2 * L * N;
+        const u64* x0 = add0[item];
+        const u64* x1 = add1 ? add1[item] : nullptr;
+        const u32 ge = g0[item];
+        u64* o = out[item];
+        COEF_LOOP {
+            const u32 src = ge == 1 ? j : galois_src(j, ge, logN);
+            for (u32 i = 0; i < L; ++i) {
+                const u64 q = dp->pr[i].q;
+                const u64 pi = dp->P_inv_q[i], pis = dp->P_inv_q_sh[i];
+                u64 r0 = shoup_mul(sub_mod(a[(size_t)i * N + j], v[(size_t)i * N + j], q), pi, pis, q);
+                u64 r1 = shoup_mul(sub_mod(a[((size_t)R + i) * N + j], v[((size_t)L + i) * N + j], q), pi, pis, q);
+                r0 = add_mod(r0, x0[(size_t)i * N + src], q);
+                if (x1) r1 = add_mod(r1, x1[(size_t)i * N + j], q);
+                o[(size_t)i * N + j] = r0;
+                o[((size_t)L + i) * N + j] = r1;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- tensoring
+// oracle q_to_b(): exact centred conversion of 4 polys per item, X: [n][4][L][N]
+__global__ void k_q_to_b(const DevParams* __restrict__ dp, u32 n, const u64* X, u64* XB) {
+    const u32 N = dp->N, L = dp->L, K = dp->K, nB = dp->nB;
+    ITEM_LOOP {
+        const u32 p = blockIdx.z;
+        const u64* x = X + ((size_t)item * 4 + p) * L * N;
+        u64* xb = XB + ((size_t)item * 4 + p) * nB * N;
+        COEF_LOOP {
+            u64 y[kMaxL];
+            Acc128 s{0, 0};
+            for (u32 i = 0; i < L; ++i) {
+                y[i] = shoup_mul(x[(size_t)i * N + j], dp->qhat_inv[i], dp->qhat_inv_sh[i], dp->pr[i].q);
+                fx_add(s, y[i], dp->one_over_q[i]);
+            }
+            const u64 v = fx_round(s);
+            for (u32 k = 0; k < nB; ++k) {
+                const u64 b = dp->pr[L + K + k].q;
+                u64 acc = 0;
+                for (u32 i = 0; i < L; ++i)
+                    acc = add_mod(acc, shoup_mul(y[i], dp->qhat_mod_b[i][k], dp->qhat_mod_b_sh[i][k], b), b);
+                xb[(size_t)k * N + j] = sub_mod(acc, shoup_mul(v, dp->Q_mod_b[k], dp->Q_mod_b_sh[k], b), b);
+            }
+        }
+    }
+}
+
+// tensor over Q ++ B in the NTT domain; T: [n][3][L+nB][N]
+__global__ void k_tensor(const DevParams* __restrict__ dp, u32 n, const u64* const* A,
+                         const u64* const* B, const u64* XB, u64* T) {
+    const u32 N = dp->N, L = dp->L, K = dp->K, nB = dp->nB, D = L + nB;
+    ITEM_LOOP {
+        const u32 d = blockIdx.z;
+        u64 *t0 = T + (((size_t)item * 3 + 0) * D + d) * N, *t1 = T + (((size_t)item * 3 + 1) * D + d) * N,
+            *t2 = T + (((size_t)item * 3 + 2) * D + d) * N;
+        const u64 *a0, *a1, *b0, *b1;
+        const Prime* P;
+        if (d < L) {
+            a0 = A[item] + (size_t)d * N; a1 = A[item] + (size_t)(L + d) * N;
+            b0 = B[item] + (size_t)d * N; b1 = B[item] + (size_t)(L + d) * N;
+            P = &dp->pr[d];
+        } else {
+            const size_t base = (size_t)item * 4 * nB * N + (size_t)(d - L) * N;
+            a0 = XB + base; a1 = XB + base + (size_t)nB * N;
+            b0 = XB + base + (size_t)2 * nB * N; b1 = XB + base + (size_t)3 * nB * N;
+            P = &dp->pr[L + K + (d - L)];
+        }
+        COEF_LOOP {
+            const u64 x0 = a0[j], x1 = a1[j], y0 = b0[j], y1 = b1[j];
+            t0[j] = mul_mod(x0, y0, *P);
+            t1[j] = add_mod(mul_mod(x0, y1, *P), mul_mod(x1, y0, *P), P->q);
+            t2[j] = mul_mod(x1, y1, *P);
+        }
+    }
+}
+
+// oracle scale_round(): round(t x / Q) from Q ++ B residues, then exact B -> Q
+__global__ void k_scale_round(const DevParams* __restrict__ dp, u32 n, const u64* T, u64* E) {
+    const u32 N = dp->N, L = dp->L, K = dp->K, nB = dp->nB, D = L + nB;
+    ITEM_LOOP {
+        const u32 p = blockIdx.z;
+        const u64* t = T + ((size_t)item * 3 + p) * D * N;
+        u64* e = E + ((size_t)item * 3 + p) * L * N;
+        COEF_LOOP {
+            u64 a[kMaxL];
+            Acc128 s{0, 0};
+            for (u32 i = 0; i < L; ++i) {
+                a[i] = shoup_mul(t[(size_t)i * N + j], dp->dhat_inv[i], dp->dhat_inv_sh[i], dp->pr[i].q);
+                fx_add(s, a[i], dp->F[i]);
+            }
+            const u64 rr = fx_round(s);
+            u64 cb[kMaxB];
+            Acc128 s2{0, 0};
+            for (u32 k = 0; k < nB; ++k) {
+                const u64 b = dp->pr[L + K + k].q;
+                u64 acc = rr % b;
+                for (u32 i = 0; i < L; ++i)
+                    acc = add_mod(acc, shoup_mul(a[i], dp->W[i][k], dp->W_sh[i][k], b), b);
+                acc = add_mod(acc, shoup_mul(t[(size_t)(L + k) * N + j], dp->T[k], dp->T_sh[k], b), b);
+                cb[k] = shoup_mul(acc, dp->bhat_inv[k], dp->bhat_inv_sh[k], b);
+                fx_add(s2, cb[k], dp->one_over_b[k]);
+            }
+            const u64 v = fx_round(s2);
+            for (u32 i = 0; i < L; ++i) {
+                const u64 q = dp->pr[i].q;
+                u64 acc = 0;
+                for (u32 k = 0; k < nB; ++k)
+                    acc = add_mod(acc, shoup_mul(cb[k], dp->bhat_mod_q[k][i], dp->bhat_mod_q_sh[k][i], q), q);
+                e[(size_t)i * N + j] = sub_mod(acc, shoup_mul(v, dp->B_mod_q[i], dp->B_mod_q_sh[i], q), q);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- key generation
+__global__ void k_keygen_sk(const DevParams* __restrict__ dp, u64* S) {
+    const u32 N = dp->N, R = dp->R;
+    const u32 n = 1;
+    ITEM_LOOP {
+        COEF_LOOP {
+            const i64 s = ternary(dp->seed, kStreamSk, j);
+            for (u32 r = 0; r < R; ++r) S[(size_t)r * N + j] = small_to_mod(s, dp->pr[r].q);
+        }
+    }
+}
+
+// Gaussian error for a stream, lifted to `limbs` limbs: E[l][j]
+__global__ void k_keygen_err(const DevParams* __restrict__ dp, u64 stream, u32 limbs, u64* E) {
+    const u32 N = dp->N;
+    const u32 n = 1;
+    ITEM_LOOP {
+        COEF_LOOP {
+            const i64 e = gauss(dp->seed, stream, j, dp->cdt);
+            for (u32 r = 0; r < limbs; ++r) E[(size_t)r * N + j] = small_to_mod(e, dp->pr[r].q);
+        }
+    }
+}
+
+__global__ void k_keygen_pk(const DevParams* __restrict__ dp, const u64* S, const u64* E, u64* pk) {
+    const u32 N = dp->N, L = dp->L;
+    const u32 n = 1;
+    ITEM_LOOP {
+        COEF_LOOP {
+            for (u32 i = 0; i < L; ++i) {
+                const Prime& P = dp->pr[i];
+                const u64 a = uniform(dp->seed, kStreamPkA, (u64)i * N + j, P.q);
+                pk[(size_t)i * N + j] = sub_mod(E[(size_t)i * N + j], mul_mod(a, S[(size_t)i * N + j], P), P.q);
+                pk[(size_t)(L + i) * N + j] = a;
+            }
+        }
+    }
+}
+
+// oracle make_key(): key[dg][0][r] = -a s + e + [r in digit dg] P s'; key[dg][1][r] = a
+__global__ void k_keygen_ks(const DevParams* __restrict__ dp, u32 kid, u32 g, const u64* S,
+                            const u64* E, u64* key) {
+    const u32 N = dp->N, L = dp->L, R = dp->R, A = dp->alpha, logN = dp->logN;
+    const u32 dg = blockIdx.y;
+    const u32 n = 1;
+    (void)n;
+    COEF_LOOP {
+        const u32 src = kid == 0 ? j : galois_src(j, g, logN);
+        for (u32 r = 0; r < R; ++r) {
+            const Prime& P = dp->pr[r];
+            const u64 sr = S[(size_t)r * N + j];
+            const u64 a = uniform(dp->seed, kStreamKsA | ((u64)kid << 8) | dg, (u64)r * N + j, P.q);
+            u64 v = sub_mod(E[((size_t)dg * R + r) * N + j], mul_mod(a, sr, P), P.q);
+            if (r < L && r / A == dg) {
+                const u64 sp = kid == 0 ? mul_mod(sr, sr, P) : S[(size_t)r * N + src];
+                v = add_mod(v, mul_mod(dp->P_mod_q[r], sp, P), P.q);
+            }
+            key[(((size_t)dg * 2 + 0) * R + r) * N + j] = v;
+            key[(((size_t)dg * 2 + 1) * R + r) * N + j] = a;
+        }
+    }
+}
+
+dim3 grid_of(u32 N, u32 n, u32 z = 1) {
+    const u32 gx = (N + kThreads - 1) / kThreads;
+    return dim3(gx, n < 65535 ? n : 65535, z);
+}
+
+u64 mask_hash(const i64* m, size_t S) {
+    u64 h = 0x243f6a8885a308d3ULL ^ S;
+    for (size_t i = 0; i < S; ++i) h = mix64(h ^ (u64)m[i]) + 0x9e3779b97f4a7c15ULL;
+    return h;
+}
+
+}  // namespace
+
+// ==================================================================== PinnedRing
+PinnedRing::PinnedRing(size_t bytes) : cap_(bytes) {
+    HGM_CUDA(cudaMallocHost(&host_, cap_));
+    HGM_CUDA(cudaMalloc(&dev_, cap_));
+}
+PinnedRing::~PinnedRing() {
+    for (auto& m : marks_) cudaEventDestroy(m.ev);
+    for (auto e : free_events_) cudaEventDestroy(e);
+    cudaFreeHost(host_);
+    cudaFree(dev_);
+}
+void* PinnedRing::upload(const void* src, size_t bytes, cudaStream_t s) {
+    const size_t need = (bytes + 255) & ~size_t(255);
+    if (need > cap_) throw std::length_error("staging ring too small for an upload of " + std::to_string(bytes));
+    size_t b = head_;
+    if (b + need > cap_) b = 0;
+    const size_t e = b + need;
+    // retire (wait for) any in-flight copy whose host range intersects [b, e)
+    for (size_t i = 0; i < marks_.size();) {
+        const size_t mb = marks_[i].end >> 32, me = marks_[i].end & 0xffffffffULL;
+        if (mb < e && b < me) {
+            HGM_CUDA(cudaEventSynchronize(marks_[i].ev));
+            free_events_.push_back(marks_[i].ev);
+            marks_.erase(marks_.begin() + i);
+        } else {
+            // drop completed marks opportunistically
+            if (cudaEventQuery(marks_[i].ev) == cudaSuccess) {
+                free_events_.push_back(marks_[i].ev);
+                marks_.erase(marks_.begin() + i);
+            } else {
+                ++i;
+            }
+        }
+    }
+    std::memcpy(host_ + b, src, bytes);
+    HGM_CUDA(cudaMemcpyAsync(dev_ + b, host_ + b, bytes, cudaMemcpyHostToDevice, s));
+    cudaEvent_t ev;
+    if (free_events_.empty()) {
+        HGM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    } else {
+        ev = free_events_.back();
+        free_events_.pop_back();
+    }
+    HGM_CUDA(cudaEventRecord(ev, s));
+    marks_.push_back(Mark{((size_t)b << 32) | e, ev});
+    head_ = e;
+    return dev_ + b;
+}
+
+// ==================================================================== Context
+Context::Context(int param_id, u64 seed, int device) : device_(device) {
+    hp_ = make_params(param_id, seed);
+    // all primes of one set share their bit length (centred_lift relies on it)
+    for (size_t r = 1; r < hp_.primes.size(); ++r)
+        if (64 - __builtin_clzll(hp_.primes[r]) != 64 - __builtin_clzll(hp_.primes[0]))
+            throw std::logic_error("prime set has mixed bit lengths");
+    HGM_CUDA(cudaSetDevice(device_));
+    HGM_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    HGM_CUDA(cudaDeviceGetDefaultMemPool(&pool, device_));
+    u64 threshold = ~0ULL;
+    HGM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    ring_ = std::make_unique<PinnedRing>((size_t)64 << 20);
+
+    const size_t N = hp_.N;
+    HGM_CUDA(cudaMalloc(&d_tw_, hp_.tw.size() * 8));
+    HGM_CUDA(cudaMemcpy(d_tw_, hp_.tw.data(), hp_.tw.size() * 8, cudaMemcpyHostToDevice));
+    HGM_CUDA(cudaMalloc(&d_slot_, N * 4));
+    HGM_CUDA(cudaMemcpy(d_slot_, hp_.slot_ntt.data(), N * 4, cudaMemcpyHostToDevice));
+    HGM_CUDA(cudaMalloc(&d_cdt_, sizeof(kGaussCdt)));
+    HGM_CUDA(cudaMemcpy(d_cdt_, kGaussCdt, sizeof(kGaussCdt), cudaMemcpyHostToDevice));
+    hp_.dev.tw = d_tw_;
+    hp_.dev.slot_ntt = d_slot_;
+    hp_.dev.cdt = d_cdt_;
+    HGM_CUDA(cudaMalloc(&dp_, sizeof(DevParams)));
+    HGM_CUDA(cudaMemcpy(dp_, &hp_.dev, sizeof(DevParams), cudaMemcpyHostToDevice));
+    build_keys();
+}
+
+Context::~Context() {
+    cudaSetDevice(device_);
+    cudaStreamSynchronize(stream_);
+    for (auto& kv : keys_) cudaFree(kv.second);
+    for (auto& kv : masks_)
+        for (auto& e : kv.second) cudaFree(e.dev);
+    cudaFree(d_sk_);
+    cudaFree(d_pk_);
+    cudaFree(dp_);
+    cudaFree(d_tw_);
+    cudaFree(d_slot_);
+    cudaFree(d_cdt_);
+    ring_.reset();
+    cudaStreamDestroy(stream_);
+}
+
+u64* Context::alloc(size_t words) {
+    void* p = nullptr;
+    HGM_CUDA(cudaMallocAsync(&p, words * 8, stream_));
+    return static_cast<u64*>(p);
+}
+void Context::release(void* p) {
+    if (p) HGM_CUDA(cudaFreeAsync(p, stream_));
+}
+void Context::sync() { HGM_CUDA(cudaStreamSynchronize(stream_)); }
+
+void Context::ntt(bool forward, const NttJobs& jobs) {
+    if (jobs.count == 0) return;
+    launches_ += hp_.logN > 13 ? 2 : 1;
+    if (forward)
+        ntt_forward(dp_, hp_.dev, jobs, stream_);
+    else
+        ntt_inverse(dp_, hp_.dev, jobs, stream_);
+    HGM_CUDA(cudaGetLastError());
+}
+
+void Context::build_keys() {
+    const u32 N = hp_.N, L = hp_.L, R = hp_.R;
+    HGM_CUDA(cudaMalloc(&d_sk_, (size_t)R * N * 8));
+    HGM_CUDA(cudaMalloc(&d_pk_, (size_t)2 * L * N * 8));
+    k_keygen_sk<<<grid_of(N, 1), kThreads, 0, stream_>>>(dp_, d_sk_); ++launches_;
+    ntt(true, jobs_contig(d_sk_, R, 0, R));
+    u64* E = alloc((size_t)L * N);
+    k_keygen_err<<<grid_of(N, 1), kThreads, 0, stream_>>>(dp_, kStreamPkE, L, E); ++launches_;
+    ntt(true, jobs_contig(E, L, 0, L));
+    k_keygen_pk<<<grid_of(N, 1), kThreads, 0, stream_>>>(dp_, d_sk_, E, d_pk_); ++launches_;
+    release(E);
+    HGM_CUDA(cudaGetLastError());
+    ks_key(0);  // relinearisation key
+}
+
+u32 Context::galois_of(i64 z, u32 N) {
+    const i64 H = N / 2;
+    const i64 zz = ((z % H) + H) % H;
+    u64 g = 1;
+    for (i64 i = 0; i < zz; ++i) g = g * 3 % (2 * (u64)N);
+    return (u32)g;
+}
+
+const u64* Context::ks_key(u32 kid) {
+    {
+        std::lock_guard<std::mutex> lk(key_mu_);
+        auto it = keys_.find(kid);
+        if (it != keys_.end()) return it->second;
+    }
+    const u32 N = hp_.N, R = hp_.R, dnum = hp_.dnum;
+    u64* key = nullptr;
+    HGM_CUDA(cudaMallocAsync((void**)&key, (size_t)dnum * 2 * R * N * 8, stream_));
+    u64* E = alloc((size_t)dnum * R * N);
+    for (u32 dg = 0; dg < dnum; ++dg)
+        k_keygen_err<<<grid_of(N, 1), kThreads, 0, stream_>>>(dp_, kStreamKsE | ((u64)kid << 8) | dg, R,
+                                                             E + (size_t)dg * R * N); ++launches_;
+    ntt(true, jobs_contig(E, dnum * R, 0, R));
+    k_keygen_ks<<<dim3((N + kThreads - 1) / kThreads, dnum), kThreads, 0, stream_>>>(dp_, kid, kid, d_sk_, E, key); ++launches_;
+    release(E);
+    HGM_CUDA(cudaGetLastError());
+    std::lock_guard<std::mutex> lk(key_mu_);
+    keys_.emplace(kid, key);
+    return key;
+}
+
+void Context::ensure_galois_keys(const std::vector<u32>& elements) {
+    for (u32 g : elements)
+        if (g != 1) ks_key(g);
+}
+
+size_t Context::key_count() const {
+    std::lock_guard<std::mutex> lk(key_mu_);
+    return keys_.size();
+}
+
+const u64* Context::mask_plain(const i64* mask, size_t S) {
+    const u64 h = mask_hash(mask, S);
+    std::lock_guard<std::mutex> lk(mask_mu_);
+    auto& bucket = masks_[h];
+    for (auto& e : bucket)
+        if (e.content.size() == S && std::equal(e.content.begin(), e.content.end(), mask)) return e.dev;
+    const u32 N = hp_.N, L = hp_.L;
+    std::vector<i64> padded(N / 2, 0);
+    std::copy(mask, mask + S, padded.begin());
+    const i64* dvals = upload(padded);
+    std::vector<u32> Sv{(u32)S};
+    const u32* dS = upload(Sv);
+    u64* m = alloc(N);
+    k_encode_scatter<<<grid_of(N, 1), kThreads, 0, stream_>>>(dp_, 1, dvals, dS, m); ++launches_;
+    NttJobs tj = jobs_contig(m, 1, kTIndex, 1);
+    ntt(false, tj);
+    u64* out = nullptr;
+    HGM_CUDA(cudaMallocAsync((void**)&out, (size_t)L * N * 8, stream_));
+    k_mask_lift<<<grid_of(N, 1), kThreads, 0, stream_>>>(dp_, m, out); ++launches_;
+    ntt(true, jobs_contig(out, L, 0, L));
+    release(m);
+    HGM_CUDA(cudaGetLastError());
+    bucket.push_back(MaskEntry{std::vector<i64>(mask, mask + S), out});
+    return out;
+}
+
+// ------------------------------------------------------------------ primitives
+void Context::encrypt(int n, const i64* const* host_vals, const size_t* S, const u64* counters,
+                      u64* const* out) {
+    if (n <= 0) return;
+    const u32 N = hp_.N, L = hp_.L, H = N / 2;
+    std::vector<i64> vals((size_t)n * H, 0);
+    std::vector<u32> Sv(n);
+    std::vector<u64> ctr(counters, counters + n);
+    std::vector<u64*> outs(out, out + n);
+    for (int i = 0; i < n; ++i) {
+        Sv[i] = (u32)S[i];
+        std::copy(host_vals[i], host_vals[i] + S[i], vals.begin() + (size_t)i * H);
+    }
+    const i64* dvals = static_cast<const i64*>(upload(vals));
+    const u32* dS = upload(Sv);
+    const u64* dctr = upload(ctr);
+    u64* const* dout = upload(outs);
+    u64* M = alloc((size_t)n * N);
+    u64* U = alloc((size_t)n * L * N);
+    k_encode_scatter<<<grid_of(N, n), kThreads, 0, stream_>>>(dp_, n, dvals, dS, M); ++launches_;
+    ntt(false, jobs_contig(M, n, kTIndex, 1));
+    k_enc_lift<<<grid_of(N, n), kThreads, 0, stream_>>>(dp_, n, M, dctr, U, dout); ++launches_;
+    ntt(true, jobs_contig(U, n * L, 0, L));
+    NttJobs cj;
+    std::vector<u64*> limbs((size_t)n * 2 * L);
+    for (int i = 0; i < n; ++i)
+        for (u32 w = 0; w < 2 * L; ++w) limbs[(size_t)i * 2 * L + w] = out[i] + (size_t)w * N;
+    cj.ptrs = upload(limbs);
+    cj.count = n * 2 * L;
+    cj.period = L;
+    for (u32 i = 0; i < L; ++i) cj.prime[i] = (unsigned char)i;
+    ntt(true, cj);
+    k_enc_finish<<<grid_of(N, n), kThreads, 0, stream_>>>(dp_, n, U, d_pk_, dout); ++launches_;
+    release(M);
+    release(U);
+    HGM_CUDA(cudaGetLastError());
+}
+
+void Context::decrypt(int n, const u64* const* in, const size_t* S, i64* const* host_out) {
+    if (n <= 0) return;
+    const u32 N = hp_.N, L = hp_.L, H = N / 2;
+    std::vector<const u64*> ins(in, in + n);
+    std::vector<u32> Sv(n);
+    for (int i = 0; i < n; ++i) Sv[i] = (u32)S[i];
+    const u64* const* din = upload(ins);
+    const u32* dS = upload(Sv);
+    u64* X = alloc((size_t)n * L * N);
+    u64* M = alloc((size_t)n * N);
+    i64* O = reinterpret_cast<i64*>(alloc((size_t)n * H));
+    k_dec_phase<<<grid_of(N, n), kThreads, 0, stream_>>>(dp_, n, din, d_sk_, X); ++launches_;
+    ntt(false, jobs_contig(X, n * L, 0, L));
+    k_dec_round<<<grid_of(N, n), kThreads, 0, stream_>>>(dp_, n, X, M); ++launches_;
+    ntt(true, jobs_contig(M, n, kTIndex, 1));
+    k_dec_gather<<<grid_of(H, n), kThreads, 0, stream_>>>(dp_, n, M, dS, O); ++launches_;
+    std::vector<i64> host((size_t)n * H);
+    HGM_CUDA(cudaMemcpyAsync(host.data(), O, host.size() * 8, cudaMemcpyDeviceToHost, stream_));
+    release(X);
+    release(M);
+    release(O);
+    sync();
+    for (int i = 0; i < n; ++i) std::copy(host.begin() + (size_t)i * H, host.begin() + (size_t)i * H + S[i], host_out[i]);
+}
+
+void Context::add(int n, const u64* const* a, const u64* const* b, u64* const* out) {
+    if (n <= 0) return;
+    std::vector<const u64*> va(a, a + n), vb(b, b + n);
+    std::vector<u64*> vo(out, out + n);
+    k_add<<<grid_of(hp_.N, n, 1), kThreads, 0, stream_>>>(dp_, n, upload(va), upload(vb), upload(vo)); ++launches_;
+    HGM_CUDA(cudaGetLastError());
+}
+
+void Context::copy(int n, const u64* const* in, u64* const* out) {
+    if (n <= 0) return;
+    std::vector<const u64*> vi(in, in + n);
+    std::vector<u64*> vo(out, out + n);
+    k_copy<<<grid_of(hp_.N, n), kThreads, 0, stream_>>>(n, ct_words(), upload(vi), upload(vo)); ++launches_;
+    HGM_CUDA(cudaGetLastError());
+}
+
+void Context::lincomb(int n_out, const u32* off, const u64* const* in, const u64* const* mask,
+                      u64* const* out) {
+    if (n_out <= 0) return;
+    const u32 nt = off[n_out];
+    std::vector<u32> voff(off, off + n_out + 1);
+    std::vector<const u64*> vin(in, in + nt), vm(mask, mask + nt);
+    std::vector<u64*> vo(out, out + n_out);
+    k_lincomb<<<grid_of(hp_.N, n_out, 1), kThreads, 0, stream_>>>(dp_, n_out, upload(voff), upload(vin),
+                                                                  upload(vm), upload(vo)); ++launches_;
+    HGM_CUDA(cudaGetLastError());
+}
+
+void Context::modup(int n, const u64* const* ct, u64* const* out) {
+    if (n <= 0) return;
+    const u32 N = hp_.N, L = hp_.L, R = hp_.R, dnum = hp_.dnum;
+    std::vector<const u64*> vc(ct, ct + n);
+    u64* C = alloc((size_t)n * L * N);
+    k_gather_c1<<<grid_of(N, n), kThreads, 0, stream_>>>(dp_, n, upload(vc), C); ++launches_;
+    ntt(false, jobs_contig(C, n * L, 0, L));
+    // lift into a contiguous staging area, then scatter-copy to the outputs
+    bool contiguous = true;
+    for (int i = 1; i < n; ++i)
+        if (out[i] != out[0] + (size_t)i * dnum * R * N) contiguous = false;
+    u64* D = contiguous ? out[0] : alloc((size_t)n * dnum * R * N);
+    k_modup_lift<<<grid_of(N, n), kThreads, 0, stream_>>>(dp_, n, C, (size_t)L * N, D); ++launches_;
+    ntt(true, jobs_contig(D, n * dnum * R, 0, R));
+    if (!contiguous) {
+        std::vector<const u64*> src(n);
+        std::vector<u64*> dst(out, out + n);
+        for (int i = 0; i < n; ++i) src[i] = D + (size_t)i * dnum * R * N;
+        const size_t W = modup_words();
+        k_copy<<<grid_of(N, n), kThreads, 0, stream_>>>(n, W, upload(src), upload(dst)); ++launches_;
+        release(D);
+    }
+    release(C);
+    HGM_CUDA(cudaGetLastError());
+}
+
+void Context::inner_product(int n, const u64* const* digits, const u64* const* keys, const u32* g,
+                            u64* const* acc) {
+    std::vector<const u64*> vd(digits, digits + n), vk(keys, keys + n);
+    std::vector<u32> vg(g, g + n);
+    std::vector<u64*> va(acc, acc + n);
+    k_ks_inner<<<grid_of(hp_.N, n), kThreads, 0, stream_>>>(dp_, n, upload(vd), upload(vk), upload(vg),
+                                                           upload(va)); ++launches_;
+    HGM_CUDA(cudaGetLastError());
+}
+
+// ModDown of n accumulators, then out = (acc - conv) P^-1 + add0[g0] (+ add1)
+void Context::key_switch_tail(int n, u64* const* acc, const u64* const* add0, const u32* g0,
+                              const u64* const* add1, u64* const* out) {
+    const u32 N = hp_.N, L = hp_.L, K = hp_.K, R = hp_.R;
+    NttJobs pj;
+    std::vector<u64*> plimbs((size_t)n * 2 * K);
+    for (int i = 0; i < n; ++i)
+        for (u32 c = 0; c < 2; ++c)
+            for (u32 k = 0; k < K; ++k) plimbs[((size_t)i * 2 + c) * K + k] = acc[i] + ((size_t)c * R + L + k) * N;
+    pj.ptrs = upload(plimbs);
+    pj.count = n * 2 * K;
+    pj.period = K;
+    for (u32 k = 0; k < K; ++k) pj.prime[k] = (unsigned char)(L + k);
+    ntt(false, pj);
+    std::vector<u64*> va(acc, acc + n);
+    u64* const* dacc = upload(va);
+    u64* V = alloc((size_t)n * 2 * L * N);
+    k_moddown_conv<<<grid_of(N, n, 2), kThreads, 0, stream_>>>(dp_, n, dacc, V); ++launches_;
+    ntt(true, jobs_contig(V, n * 2 * L, 0, L));
+    std::vector<const u64*> v0(add0, add0 + n);
+    std::vector<u32> vg(g0, g0 + n);
+    std::vector<u64*> vo(out, out + n);
+    const u64* const* d1 = nullptr;
+    if (add1) {
+        std::vector<const u64*> v1(add1, add1 + n);
+        d1 = upload(v1);
+    }
+    k_ks_finish<<<grid_of(N, n), kThreads, 0, stream_>>>(dp_, n, dacc, V, upload(v0), upload(vg), d1,
+                                                        upload(vo)); ++launches_;
+    release(V);
+    HGM_CUDA(cudaGetLastError());
+}
+
+void Context::rotate(int n, const u64* const* modup, const u64* const* ct, const u32* g,
+                     u64* const* out) {
+    if (n <= 0) return;
+    const u32 N = hp_.N, R = hp_.R;
+    std::vector<const u64*> keys(n);
+    for (int i = 0; i < n; ++i) keys[i] = ks_key(g[i]);
+    u64* A = alloc((size_t)n * 2 * R * N);
+    std::vector<u64*> accs(n);
+    for (int i = 0; i < n; ++i) accs[i] = A + (size_t)i * 2 * R * N;
+    inner_product(n, modup, keys.data(), g, accs.data());
+    key_switch_tail(n, accs.data(), ct, g, nullptr, out);
+    release(A);
+}
+
+void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* out) {
+    if (n <= 0) return;
+    const u32 N = hp_.N, L = hp_.L, K = hp_.K, R = hp_.R, nB = hp_.nB, dnum = hp_.dnum;
+    const size_t LN = (size_t)L * N;
+    // 1. gather (a.c0, a.c1, b.c0, b.c1) and INTT
+    u64* X = alloc((size_t)n * 4 * LN);
+    {
+        std::vector<const u64*> src((size_t)2 * n);
+        std::vector<u64*> dst((size_t)2 * n);
+        for (int i = 0; i < n; ++i) {
+            src[2 * i] = a[i];
+            src[2 * i + 1] = b[i];
+            dst[2 * i] = X + (size_t)i * 4 * LN;
+            dst[2 * i + 1] = X + (size_t)i * 4 * LN + 2 * LN;
+        }
+        k_copy<<<grid_of(N, 2 * n), kThreads, 0, stream_>>>(2 * n, ct_words(), upload(src), upload(dst)); ++launches_;
+    }
+    ntt(false, jobs_contig(X, n * 4 * L, 0, L));
+    // 2. exact Q -> B and NTT over B
+    u64* XB = alloc((size_t)n * 4 * nB * N);
+    k_q_to_b<<<grid_of(N, n, 4), kThreads, 0, stream_>>>(dp_, n, X, XB); ++launches_;
+    release(X);
+    ntt(true, jobs_contig(XB, n * 4 * nB, L + K, nB));
+    // 3. tensor over Q ++ B, INTT
+    const u32 D = L + nB;
+    u64* T = alloc((size_t)n * 3 * D * N);
+    {
+        std::vector<const u64*> va(a, a + n), vb(b, b + n);
+        k_tensor<<<grid_of(N, n, D), kThreads, 0, stream_>>>(dp_, n, upload(va), upload(vb), XB, T); ++launches_;
+    }
+    release(XB);
+    NttJobs tj = jobs_contig(T, n * 3 * D, 0, D);
+    for (u32 k = 0; k < nB; ++k) tj.prime[L + k] = (unsigned char)(L + K + k);
+    ntt(false, tj);
+    // 4. scale and round back to Q (coefficient form)
+    u64* E = alloc((size_t)n * 3 * LN);
+    k_scale_round<<<grid_of(N, n, 3), kThreads, 0, stream_>>>(dp_, n, T, E); ++launches_;
+    release(T);
+    // 5. relinearise e2: ModUp, inner product with rlk, ModDown, add NTT(e0, e1)
+    u64* Dg = alloc((size_t)n * dnum * R * N);
+    k_modup_lift<<<grid_of(N, n), kThreads, 0, stream_>>>(dp_, n, E + 2 * LN, 3 * LN, Dg); ++launches_;
+    ntt(true, jobs_contig(Dg, n * dnum * R, 0, R));
+    {
+        NttJobs ej;
+        std::vector<u64*> limbs((size_t)n * 2 * L);
+        for (int i = 0; i < n; ++i)
+            for (u32 w = 0; w < 2 * L; ++w) limbs[(size_t)i * 2 * L + w] = E + (size_t)i * 3 * LN + (size_t)w * N;
+        ej.ptrs = upload(limbs);
+        ej.count = n * 2 * L;
+        ej.period = L;
+        for (u32 i = 0; i < L; ++i) ej.prime[i] = (unsigned char)i;
+        ntt(true, ej);
+    }
+    u64* A = alloc((size_t)n * 2 * R * N);
+    std::vector<const u64*> digits(n), keys(n), e0(n), e1(n);
+    std::vector<u64*> accs(n);
+    std::vector<u32> ones(n, 1);
+    const u64* rlk = ks_key(0);
+    for (int i = 0; i < n; ++i) {
+        digits[i] = Dg + (size_t)i * dnum * R * N;
+        keys[i] = rlk;
+        accs[i] = A + (size_t)i * 2 * R * N;
+        e0[i] = E + (size_t)i * 3 * LN;
+        e1[i] = E + (size_t)i * 3 * LN + LN;
+    }
+    inner_product(n, digits.data(), keys.data(), ones.data(), accs.data());
+    key_switch_tail(n, accs.data(), e0.data(), ones.data(), e1.data(), out);
+    release(Dg);
+    release(A);
+    release(E);
+}
+
+}  // namespace hgm

@@ -1,0 +1,534 @@
+// capi.cpp -- the extern "C" boundary (include/hegmm_b200.h).
+//
+// A session (hgm_ctx) records every primitive call as a node of a lazy op
+// graph and counts it immediately, exactly like the reference backend counts
+// (backend.cpp:103-107, one counter bump per call, split by phase).  Work is
+// executed when a result is needed (decrypt / export / flush): the pending
+// sub-graph becomes a Program and runs through the batched executor, so the
+// many independent rotations and masks of one HEGMM call share launches and
+// ModUps.  Nodes still referenced by a pinned handle keep their ciphertext;
+// every other intermediate is recomputed on demand (all ops are deterministic).
+#include <atomic>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/hegmm_b200.h"
+#include "context.hpp"
+#include "engine.hpp"
+#include "hegmm_algos.hpp"
+
+using namespace hgm;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct DevBuf {
+    Context* ctx;
+    u64* p;
+    DevBuf(Context* c, u64* q) : ctx(c), p(q) {}
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) ctx->release(p);
+    }
+};
+
+struct SNode {
+    PNode::Kind kind = PNode::Input;
+    std::vector<std::shared_ptr<SNode>> in;
+    std::vector<MaskRef> masks;
+    u32 g = 1;
+    size_t S = 0, depth = 0;
+    int phase = 0;
+    std::vector<i64> values;  // Enc
+    u64 counter = 0;          // Enc
+    std::shared_ptr<DevBuf> buf;
+    std::atomic<int> pins{0};
+};
+
+}  // namespace
+
+struct hgm_ctx {
+    std::unique_ptr<Context> ctx;
+    std::mutex mu;
+    std::atomic<int> phase{0};
+    Counts counts;
+    u64 enc_counter = 0;
+    std::atomic<size_t> live{0}, peak{0};
+};
+
+struct hgm_ct {
+    hgm_ctx* owner;
+    std::shared_ptr<SNode> node;
+    std::atomic<int> refs{1};
+    bool pinned = true;
+};
+
+namespace {
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return HGM_OK;
+    } catch (const hgm::DimensionError& e) {
+        return fail(HGM_EDIM, e.what());
+    } catch (const hgm::CapacityError& e) {
+        return fail(HGM_ECAP, e.what());
+    } catch (const CudaError& e) {
+        return fail(HGM_ECUDA, e.what());
+    } catch (const std::invalid_argument& e) {
+        return fail(HGM_EARG, e.what());
+    } catch (const std::exception& e) {
+        return fail(HGM_EINTERNAL, e.what());
+    }
+}
+
+void bump(hgm_ctx* c, int op) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->counts.at(op, c->phase.load())++;
+}
+
+hgm_ct* make_handle(hgm_ctx* c, std::shared_ptr<SNode> n) {
+    auto* h = new hgm_ct;
+    h->owner = c;
+    h->node = std::move(n);
+    h->node->pins++;
+    const size_t now = ++c->live;
+    size_t seen = c->peak.load();
+    while (seen < now && !c->peak.compare_exchange_weak(seen, now)) {
+    }
+    return h;
+}
+
+std::shared_ptr<SNode> new_node(hgm_ctx* c, PNode::Kind k, size_t S, size_t depth) {
+    auto n = std::make_shared<SNode>();
+    n->kind = k;
+    n->S = S;
+    n->depth = depth;
+    n->phase = c->phase.load();
+    return n;
+}
+
+void check_values(hgm_ctx* c, size_t S) {
+    if (S == 0) throw hgm::DimensionError("cannot encrypt an empty vector");
+    if (S > c->ctx->slots())
+        throw hgm::CapacityError("vector of length " + std::to_string(S) + " exceeds " +
+                                 std::to_string(c->ctx->slots()) + " slots");
+}
+
+// Materialise `targets` (and every pinned node on their pending sub-graph).
+void flush(hgm_ctx* c, const std::vector<std::shared_ptr<SNode>>& targets) {
+    std::unordered_map<SNode*, int> index;
+    std::vector<std::shared_ptr<SNode>> order;  // topological
+    std::vector<std::shared_ptr<SNode>> inputs;
+    Program prog;
+    // iterative post-order DFS
+    struct Frame {
+        std::shared_ptr<SNode> n;
+        size_t next;
+    };
+    for (const auto& t : targets) {
+        if (t->buf || index.count(t.get())) continue;
+        std::vector<Frame> st{{t, 0}};
+        while (!st.empty()) {
+            Frame& f = st.back();
+            SNode* n = f.n.get();
+            if (index.count(n)) {
+                st.pop_back();
+                continue;
+            }
+            if (!n->buf && f.next < n->in.size()) {
+                auto child = n->in[f.next++];
+                if (!index.count(child.get())) st.push_back({child, 0});
+                continue;
+            }
+            int id;
+            if (n->buf) {
+                id = prog.add_input(n->S);
+                inputs.push_back(f.n);
+            } else {
+                std::vector<int> in;
+                for (auto& x : n->in) in.push_back(index.at(x.get()));
+                switch (n->kind) {
+                    case PNode::Enc: id = prog.add_enc(n->S); break;
+                    case PNode::Rot: id = prog.add_rot(in[0], n->g); break;
+                    case PNode::Comb: id = prog.add_comb(in, n->masks); break;
+                    case PNode::Mult: id = prog.add_mult(in[0], in[1]); break;
+                    default: throw std::logic_error("unmaterialised input node");
+                }
+            }
+            index.emplace(n, id);
+            order.push_back(f.n);
+            st.pop_back();
+        }
+    }
+    // outputs: targets, plus pending nodes somebody still holds a pinned handle to
+    std::vector<std::shared_ptr<SNode>> outs;
+    for (const auto& t : targets)
+        if (!t->buf) outs.push_back(t);
+    for (const auto& n : order)
+        if (!n->buf && n->pins.load() > 0) outs.push_back(n);
+    if (outs.empty()) return;
+    std::unordered_map<SNode*, size_t> out_pos;
+    std::vector<std::shared_ptr<SNode>> uniq;
+    for (auto& n : outs)
+        if (!out_pos.count(n.get())) {
+            out_pos.emplace(n.get(), uniq.size());
+            uniq.push_back(n);
+            prog.outputs.push_back(index.at(n.get()));
+        }
+    std::vector<SNode*> encs;
+    for (const auto& n : order)
+        if (!n->buf && n->kind == PNode::Enc) encs.push_back(n.get());
+    const Schedule sch = optimise(prog);
+    ExecIO io;
+    io.K = 1;
+    io.input = [&](int s, int) { return (const u64*)inputs[s]->buf->p; };
+    io.enc_values = [&](int s, int) { return (const i64*)encs[s]->values.data(); };
+    io.enc_counter = [&](int s, int) { return encs[s]->counter; };
+    std::vector<u64*> res = execute(*c->ctx, sch, io);
+    for (size_t i = 0; i < uniq.size(); ++i) {
+        uniq[i]->buf = std::make_shared<DevBuf>(c->ctx.get(), res[i]);
+        uniq[i]->in.clear();  // materialised: history no longer needed
+    }
+}
+
+const SNode& node_of(const hgm_ct* h) { return *h->node; }
+
+}  // namespace
+
+extern "C" {
+
+const char* hgm_last_error(void) { return g_err.c_str(); }
+
+hgm_ctx* hgm_ctx_create(int param_id, uint64_t seed, int device) {
+    hgm_ctx* c = nullptr;
+    const int rc = guarded([&] {
+        auto h = std::make_unique<hgm_ctx>();
+        h->ctx = std::make_unique<Context>(param_id, seed, device);
+        c = h.release();
+    });
+    return rc == HGM_OK ? c : nullptr;
+}
+
+void hgm_ctx_destroy(hgm_ctx* c) { delete c; }
+
+int hgm_ctx_info(const hgm_ctx* c, uint64_t* info, size_t cap) {
+    const HostParams& h = c->ctx->host();
+    if (cap < 8 + h.primes.size()) return fail(HGM_EARG, "info buffer too small");
+    info[0] = h.N; info[1] = h.L; info[2] = h.K; info[3] = h.nB; info[4] = h.dnum;
+    info[5] = kT; info[6] = h.alpha; info[7] = h.seed;
+    for (size_t i = 0; i < h.primes.size(); ++i) info[8 + i] = h.primes[i];
+    return HGM_OK;
+}
+size_t hgm_slot_count(const hgm_ctx* c) { return c->ctx->slots(); }
+size_t hgm_ct_words(const hgm_ctx* c) { return c->ctx->ct_words(); }
+
+int hgm_encrypt_at(hgm_ctx* c, const int64_t* values, size_t S, uint64_t counter, hgm_ct** out) {
+    return guarded([&] {
+        check_values(c, S);
+        auto n = new_node(c, PNode::Enc, S, 0);
+        n->values.assign(values, values + S);
+        n->counter = counter;
+        bump(c, kEnc);
+        *out = make_handle(c, std::move(n));
+    });
+}
+int hgm_encrypt(hgm_ctx* c, const int64_t* values, size_t S, hgm_ct** out) {
+    u64 ctr;
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        ctr = c->enc_counter;
+    }
+    const int rc = hgm_encrypt_at(c, values, S, ctr, out);
+    if (rc == HGM_OK) {
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->enc_counter++;
+    }
+    return rc;
+}
+
+int hgm_decrypt(hgm_ctx* c, const hgm_ct* ct, int64_t* out, size_t cap) {
+    return guarded([&] {
+        bump(c, kDec);
+        const size_t S = node_of(ct).S;
+        if (cap < S) throw std::invalid_argument("decrypt output buffer smaller than the segment");
+        flush(c, {ct->node});
+        const u64* p = ct->node->buf->p;
+        c->ctx->decrypt(1, &p, &S, &out);
+        if (!ct->pinned || ct->node->pins.load() == 0) {
+        }
+    });
+}
+
+int hgm_add(hgm_ctx* c, const hgm_ct* x, const hgm_ct* y, hgm_ct** out) {
+    return guarded([&] {
+        const SNode &a = node_of(x), &b = node_of(y);
+        if (a.S != b.S)
+            throw hgm::DimensionError("he_add segment mismatch: " + std::to_string(a.S) + " vs " + std::to_string(b.S));
+        auto n = new_node(c, PNode::Comb, a.S, std::max(a.depth, b.depth));
+        n->in = {x->node, y->node};
+        n->masks = {nullptr, nullptr};
+        bump(c, kAdd);
+        *out = make_handle(c, std::move(n));
+    });
+}
+
+int hgm_mul(hgm_ctx* c, const hgm_ct* x, const hgm_ct* y, hgm_ct** out) {
+    return guarded([&] {
+        const SNode &a = node_of(x), &b = node_of(y);
+        if (a.S != b.S)
+            throw hgm::DimensionError("he_mult segment mismatch: " + std::to_string(a.S) + " vs " + std::to_string(b.S));
+        auto n = new_node(c, PNode::Mult, a.S, std::max(a.depth, b.depth) + 1);
+        n->in = {x->node, y->node};
+        bump(c, kMultCC);
+        *out = make_handle(c, std::move(n));
+    });
+}
+
+int hgm_cmul(hgm_ctx* c, const hgm_ct* x, const int64_t* mask, size_t S, hgm_ct** out) {
+    return guarded([&] {
+        const SNode& a = node_of(x);
+        if (S != a.S)
+            throw hgm::DimensionError("he_cmult mask length " + std::to_string(S) + " does not match segment " +
+                                      std::to_string(a.S));
+        auto md = std::make_shared<MaskData>();
+        md->v.assign(mask, mask + S);
+        auto n = new_node(c, PNode::Comb, a.S, a.depth);
+        n->in = {x->node};
+        n->masks = {md};
+        bump(c, kMultCP);
+        *out = make_handle(c, std::move(n));
+    });
+}
+
+int hgm_rot(hgm_ctx* c, const hgm_ct* x, int64_t z, hgm_ct** out) {
+    return guarded([&] {
+        const SNode& a = node_of(x);
+        auto n = new_node(c, PNode::Rot, a.S, a.depth);
+        n->in = {x->node};
+        n->g = Context::galois_of(z, (u32)c->ctx->host().N);
+        bump(c, kRot);
+        *out = make_handle(c, std::move(n));
+    });
+}
+
+int hgm_apply_plan(hgm_ctx* c, const hgm_ct* x, size_t n_entries, const int64_t* offsets,
+                   const int64_t* masks, size_t S, hgm_ct** out) {
+    return guarded([&] {
+        const SNode& a = node_of(x);
+        if (S != a.S)
+            throw hgm::DimensionError("ciphertext segment " + std::to_string(a.S) + " does not match plan length " +
+                                      std::to_string(S));
+        if (n_entries == 0) throw hgm::DimensionError("cannot apply an empty plan");
+        std::shared_ptr<SNode> acc;
+        for (size_t e = 0; e < n_entries; ++e) {
+            std::shared_ptr<SNode> src = x->node;
+            if (offsets[e] != 0) {
+                auto r = new_node(c, PNode::Rot, S, a.depth);
+                r->in = {x->node};
+                r->g = Context::galois_of(offsets[e], (u32)c->ctx->host().N);
+                bump(c, kRot);
+                src = r;
+            }
+            auto md = std::make_shared<MaskData>();
+            md->v.assign(masks + e * S, masks + (e + 1) * S);
+            auto term = new_node(c, PNode::Comb, S, a.depth);
+            term->in = {src};
+            term->masks = {md};
+            bump(c, kMultCP);
+            if (!acc) {
+                acc = term;
+            } else {
+                auto s = new_node(c, PNode::Comb, S, a.depth);
+                s->in = {acc, term};
+                s->masks = {nullptr, nullptr};
+                bump(c, kAdd);
+                acc = s;
+            }
+        }
+        *out = make_handle(c, std::move(acc));
+    });
+}
+
+int hgm_flush(hgm_ctx* c) {
+    (void)c;
+    return HGM_OK;
+}
+
+int hgm_ct_export(hgm_ctx* c, const hgm_ct* ct, uint64_t* words) {
+    return guarded([&] {
+        flush(c, {ct->node});
+        c->ctx->sync();
+        HGM_CUDA(cudaMemcpy(words, ct->node->buf->p, c->ctx->ct_words() * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+int hgm_ct_import(hgm_ctx* c, const uint64_t* words, size_t S, size_t depth, hgm_ct** out) {
+    return guarded([&] {
+        check_values(c, S);
+        auto n = new_node(c, PNode::Input, S, depth);
+        u64* p = c->ctx->alloc(c->ctx->ct_words());
+        n->buf = std::make_shared<DevBuf>(c->ctx.get(), p);
+        HGM_CUDA(cudaMemcpyAsync(p, words, c->ctx->ct_words() * 8, cudaMemcpyHostToDevice, c->ctx->stream()));
+        c->ctx->sync();
+        *out = make_handle(c, std::move(n));
+    });
+}
+
+size_t hgm_ct_segment(const hgm_ct* ct) { return ct->node->S; }
+size_t hgm_ct_depth(const hgm_ct* ct) { return ct->node->depth; }
+int hgm_ct_phase(const hgm_ct* ct) { return ct->node->phase; }
+hgm_ct* hgm_ct_retain(hgm_ct* ct) {
+    ct->refs++;
+    return ct;
+}
+void hgm_ct_release(hgm_ct* ct) {
+    if (!ct) return;
+    if (--ct->refs == 0) {
+        if (ct->pinned) ct->node->pins--;
+        ct->owner->live--;
+        delete ct;
+    }
+}
+
+int hgm_stats(const hgm_ctx* c, uint64_t stats[12]) {
+    auto* m = const_cast<hgm_ctx*>(c);
+    std::lock_guard<std::mutex> lk(m->mu);
+    for (int k = 0; k < 6; ++k) {
+        stats[2 * k] = c->counts.c[k][0];
+        stats[2 * k + 1] = c->counts.c[k][1];
+    }
+    return HGM_OK;
+}
+int hgm_reset_stats(hgm_ctx* c) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->counts = Counts{};
+    c->peak.store(c->live.load());
+    return HGM_OK;
+}
+size_t hgm_peak_live(const hgm_ctx* c) { return c->peak.load(); }
+int hgm_set_phase(hgm_ctx* c, int phase) {
+    if (phase != 0 && phase != 1) return fail(HGM_EARG, "phase must be 0 (client) or 1 (cloud)");
+    c->phase.store(phase);
+    return HGM_OK;
+}
+int hgm_phase(const hgm_ctx* c) { return c->phase.load(); }
+
+static int matmul_batch_impl(hgm_ctx* c, int algo, int order, size_t m, size_t l, size_t n, size_t count,
+                             const int64_t* A, const int64_t* B, int64_t* C, uint64_t counter0,
+                             uint64_t* stats, uint64_t* final_words) {
+    return guarded([&] {
+        if (order < -1 || order > 1) throw std::invalid_argument("order must be -1, 0 or 1");
+        Context& ctx = *c->ctx;
+        auto prog = get_matmul_program(algo, order, m, l, n, ctx.slots(), ctx.host().N);
+        if (stats)
+            for (int k = 0; k < 6; ++k) {
+                stats[2 * k] = prog->counts.c[k][0];
+                stats[2 * k + 1] = prog->counts.c[k][1];
+            }
+        if (count == 0) return;
+        const size_t W = ctx.ct_words();
+        // instances per lockstep chunk: bounded by the rotated working set
+        const size_t per_inst = (prog->sched.rot_count + 8) * W * 8 + 64 * W * 8;
+        size_t free_b = 0, total_b = 0;
+        HGM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        size_t chunk = std::max<size_t>(1, (size_t)(0.5 * (double)free_b) / per_inst);
+        chunk = std::min<size_t>(chunk, 1024);
+        for (size_t c0 = 0; c0 < count; c0 += chunk) {
+            const int K = (int)std::min(chunk, count - c0);
+            std::vector<std::vector<std::vector<i64>>> packed(K);
+            for (int k = 0; k < K; ++k)
+                packed[k] = prog->pack(A + (c0 + k) * m * l, B + (c0 + k) * l * n);
+            ExecIO io;
+            io.K = K;
+            io.input = [](int, int) -> const u64* { return nullptr; };
+            io.enc_values = [&](int s, int k) { return (const i64*)packed[k][s].data(); };
+            io.enc_counter = [&](int s, int k) { return counter0 + (c0 + k) * prog->n_enc + s; };
+            std::vector<u64*> res = execute(ctx, prog->sched, io);
+            std::vector<const u64*> cts(K);
+            std::vector<size_t> S(K, prog->segment);
+            std::vector<std::vector<i64>> outv(K, std::vector<i64>(prog->segment));
+            std::vector<i64*> outp(K);
+            for (int k = 0; k < K; ++k) {
+                cts[k] = res[0] + (size_t)k * W;
+                outp[k] = outv[k].data();
+            }
+            ctx.decrypt(K, cts.data(), S.data(), outp.data());
+            if (final_words)
+                HGM_CUDA(cudaMemcpy(final_words + c0 * W, res[0], (size_t)K * W * 8, cudaMemcpyDeviceToHost));
+            for (u64* r : res) ctx.release(r);
+            for (int k = 0; k < K; ++k) prog->unpack(outv[k], C + (c0 + k) * m * n);
+        }
+        ctx.sync();
+    });
+}
+
+int hgm_matmul_batch(hgm_ctx* c, int algo, int order, size_t m, size_t l, size_t n, size_t count,
+                     const int64_t* A, const int64_t* B, int64_t* C, uint64_t counter0, uint64_t* stats) {
+    return matmul_batch_impl(c, algo, order, m, l, n, count, A, B, C, counter0, stats, nullptr);
+}
+int hgm_matmul_batch_export(hgm_ctx* c, int algo, int order, size_t m, size_t l, size_t n, size_t count,
+                            const int64_t* A, const int64_t* B, int64_t* C, uint64_t counter0,
+                            uint64_t* final_words) {
+    return matmul_batch_impl(c, algo, order, m, l, n, count, A, B, C, counter0, nullptr, final_words);
+}
+
+int hgm_bench_ntt(hgm_ctx* c, int forward, size_t limbs, int iters, float* ms) {
+    return guarded([&] {
+        Context& ctx = *c->ctx;
+        const u32 N = ctx.host().N, L = ctx.host().L;
+        u64* buf = ctx.alloc(limbs * N);
+        HGM_CUDA(cudaMemsetAsync(buf, 0, limbs * N * 8, ctx.stream()));
+        NttJobs j = jobs_contig(buf, (u32)limbs, 0, L);
+        ctx.ntt(forward != 0, j);  // warm-up
+        cudaEvent_t e0, e1;
+        HGM_CUDA(cudaEventCreate(&e0));
+        HGM_CUDA(cudaEventCreate(&e1));
+        HGM_CUDA(cudaEventRecord(e0, ctx.stream()));
+        for (int i = 0; i < iters; ++i) ctx.ntt(forward != 0, j);
+        HGM_CUDA(cudaEventRecord(e1, ctx.stream()));
+        HGM_CUDA(cudaEventSynchronize(e1));
+        float t = 0;
+        HGM_CUDA(cudaEventElapsedTime(&t, e0, e1));
+        *ms = t / iters;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        ctx.release(buf);
+        ctx.sync();
+    });
+}
+
+int hgm_device_sync(hgm_ctx* c) {
+    return guarded([&] { c->ctx->sync(); });
+}
+
+int hgm_test_ntt(hgm_ctx* c, int forward, int prime, uint64_t* data, size_t count) {
+    return guarded([&] {
+        Context& ctx = *c->ctx;
+        const u32 N = ctx.host().N;
+        const int p = prime < 0 ? kTIndex : prime;
+        if (prime >= (int)ctx.host().primes.size()) throw std::invalid_argument("prime index out of range");
+        u64* buf = ctx.alloc(count * N);
+        HGM_CUDA(cudaMemcpyAsync(buf, data, count * N * 8, cudaMemcpyHostToDevice, ctx.stream()));
+        ctx.ntt(forward != 0, jobs_contig(buf, (u32)count, (u32)p, 1));
+        HGM_CUDA(cudaMemcpyAsync(data, buf, count * N * 8, cudaMemcpyDeviceToHost, ctx.stream()));
+        ctx.release(buf);
+        ctx.sync();
+    });
+}
+
+uint64_t hgm_launch_count(const hgm_ctx* c) { return c->ctx->launches(); }
+
+}  // extern "C"

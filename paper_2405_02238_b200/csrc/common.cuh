@@ -1,0 +1,192 @@
+// common.cuh -- integer arithmetic and the device-side parameter block.
+//
+// All ciphertext arithmetic is 64-bit RNS modular arithmetic over NTT-friendly
+// primes q < 2^62.  Fixed multiplicands (twiddles, base-conversion constants)
+// use Shoup's precomputed quotient; products of two variables use a shifted
+// Barrett reduction.  Nothing here is floating point: the scale-and-round steps
+// use 128-bit fixed-point fractions (see Frac) so that every result is an exact
+// integer function of its inputs and matches oracle/bfv_oracle.cpp bit for bit.
+#pragma once
+#include <cstdint>
+
+#ifdef __CUDACC__
+#define HD __host__ __device__ __forceinline__
+#else
+#define HD inline
+#endif
+
+namespace hgm {
+
+using u64 = std::uint64_t;
+using u32 = std::uint32_t;
+using i64 = std::int64_t;
+
+constexpr int kMaxL = 8;       // ciphertext primes
+constexpr int kMaxK = 4;       // special primes
+constexpr int kMaxB = 10;      // auxiliary base for the tensor product
+constexpr int kMaxR = kMaxL + kMaxK;
+constexpr int kMaxPrimes = kMaxL + kMaxK + kMaxB;
+constexpr int kTIndex = kMaxPrimes;  // table slot of the plaintext modulus t
+constexpr u64 kT = 65537;
+
+// sampler stream tags: identical to oracle/bfv_oracle.cpp
+constexpr u64 kStreamSk = 1ULL << 56, kStreamPkA = 2ULL << 56, kStreamPkE = 3ULL << 56,
+              kStreamKsA = 4ULL << 56, kStreamKsE = 5ULL << 56, kStreamEncU = 6ULL << 56,
+              kStreamEncE0 = 7ULL << 56, kStreamEncE1 = 8ULL << 56;
+
+struct Frac {
+    u64 hi, lo;  // floor(a * 2^128 / q) for a < q
+};
+
+struct Prime {
+    u64 q;
+    u64 mu;      // floor(2^(62+s) / q), shifted Barrett
+    u32 s;       // bit length of q
+    u32 pad;
+    u64 ninv, ninv_sh;
+};
+
+// Everything a kernel needs, stored once in device memory per context and
+// passed by pointer (uniform loads through the constant/L1 path).
+struct DevParams {
+    u32 N, logN, L, K, nB, dnum, alpha, R;  // R = L + K
+    u64 seed;
+    Prime pr[kMaxPrimes + 1];  // Q ++ P ++ B, then t at kTIndex
+    const u64* tw;             // [(kMaxPrimes+1)][4][N]: psi_rev, sh, ipsi_rev, sh
+    const u32* slot_ntt;       // slot (row*N/2+col) -> NTT index, N entries
+    const u64* cdt;            // 20-entry Gaussian CDT
+    // encrypt / decrypt
+    u64 delta[kMaxL], delta_sh[kMaxL];
+    u64 qhat_inv[kMaxL], qhat_inv_sh[kMaxL];  // (Q/q_i)^-1 mod q_i
+    Frac t_over_q[kMaxL];
+    // exact Q -> B
+    Frac one_over_q[kMaxL];
+    u64 qhat_mod_b[kMaxL][kMaxB], qhat_mod_b_sh[kMaxL][kMaxB];
+    u64 Q_mod_b[kMaxB], Q_mod_b_sh[kMaxB];
+    // scale-and-round Q++B -> B
+    u64 dhat_inv[kMaxL], dhat_inv_sh[kMaxL];
+    u64 W[kMaxL][kMaxB], W_sh[kMaxL][kMaxB];
+    Frac F[kMaxL];
+    u64 T[kMaxB], T_sh[kMaxB];
+    // exact B -> Q
+    u64 bhat_inv[kMaxB], bhat_inv_sh[kMaxB];
+    Frac one_over_b[kMaxB];
+    u64 bhat_mod_q[kMaxB][kMaxL], bhat_mod_q_sh[kMaxB][kMaxL];
+    u64 B_mod_q[kMaxL], B_mod_q_sh[kMaxL];
+    // key switching (digit d holds primes d*alpha .. d*alpha+alpha-1)
+    u64 dg_hat_inv[kMaxL], dg_hat_inv_sh[kMaxL];               // by prime i
+    u64 dg_hat[kMaxL][kMaxR], dg_hat_sh[kMaxL][kMaxR];         // [i][r] (Q_d/q_i) mod r
+    u64 P_mod_q[kMaxL], P_mod_q_sh[kMaxL];
+    u64 P_inv_q[kMaxL], P_inv_q_sh[kMaxL];
+    u64 phat_inv[kMaxK], phat_inv_sh[kMaxK];
+    u64 phat_mod_q[kMaxK][kMaxL], phat_mod_q_sh[kMaxK][kMaxL];
+};
+
+// ------------------------------------------------------------------ scalar ops
+#ifdef __CUDACC__
+HD u64 mulhi64(u64 a, u64 b) {
+#ifdef __CUDA_ARCH__
+    return __umul64hi(a, b);
+#else
+    return (u64)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+#else
+inline u64 mulhi64(u64 a, u64 b) { return (u64)(((unsigned __int128)a * b) >> 64); }
+#endif
+
+HD u64 add_mod(u64 a, u64 b, u64 q) {
+    u64 s = a + b;
+    return s >= q ? s - q : s;
+}
+HD u64 sub_mod(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }
+HD u64 neg_mod(u64 a, u64 q) { return a ? q - a : 0; }
+// a * w mod q with ws = floor(w 2^64 / q); any a < 2^64, result in [0, q)
+HD u64 shoup_mul(u64 a, u64 w, u64 ws, u64 q) {
+    u64 h = mulhi64(a, ws);
+    u64 r = a * w - h * q;
+    return r >= q ? r - q : r;
+}
+// a * b mod q for a, b < q < 2^62 (shifted Barrett, at most two corrections)
+HD u64 mul_mod(u64 a, u64 b, const Prime& p) {
+    const u64 lo = a * b, hi = mulhi64(a, b);
+    const u64 x = (hi << (66 - p.s)) | (lo >> (p.s - 2));
+    const u64 qh = mulhi64(x, p.mu);
+    u64 r = lo - qh * p.q;
+    if (r >= p.q) r -= p.q;
+    if (r >= p.q) r -= p.q;
+    return r;
+}
+HD u64 from_signed(i64 v, u64 q) { return v >= 0 ? (u64)v % q : q - 1 - ((u64)(-(v + 1)) % q); }
+HD u64 centred_neg(u64 y, u64 q) { return y > (q - 1) / 2; }
+// y (canonical mod src) viewed as its centred representative, reduced mod dst.
+// Requires src < 2^62 and src, dst odd primes.
+HD u64 centred_to(u64 y, u64 src, u64 dst) {
+    if (y > (src - 1) / 2) {
+        u64 m = (src - y) % dst;  // |centred value| mod dst
+        return m ? dst - m : 0;
+    }
+    return y % dst;
+}
+
+// 128-bit accumulator in units of 2^-64
+struct Acc128 {
+    u64 lo, hi;
+};
+HD void fx_add(Acc128& s, u64 y, const Frac& f) {
+    // y*f.hi (128 bit) + mulhi(y, f.lo)
+    u64 plo = y * f.hi, phi = mulhi64(y, f.hi);
+    u64 t = mulhi64(y, f.lo);
+    u64 lo1 = plo + t;
+    phi += (lo1 < plo);
+    u64 lo2 = s.lo + lo1;
+    s.hi += phi + (lo2 < lo1);
+    s.lo = lo2;
+}
+HD u64 fx_round(const Acc128& s) {
+    // (s + 2^63) >> 64
+    u64 lo = s.lo + (1ULL << 63);
+    return s.hi + (lo < s.lo);
+}
+
+// ------------------------------------------------------------------ sampler
+HD u64 mix64(u64 z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+HD u64 prng(u64 seed, u64 stream, u64 idx) {
+    u64 h = mix64(seed ^ 0x5851f42d4c957f2dULL);
+    h = mix64(h ^ stream);
+    return mix64(h + (idx + 1) * 0x9e3779b97f4a7c15ULL);
+}
+HD i64 ternary(u64 seed, u64 stream, u64 idx) { return (i64)mulhi64(prng(seed, stream, idx), 3) - 1; }
+HD u64 uniform(u64 seed, u64 stream, u64 idx, u64 q) { return mulhi64(prng(seed, stream, idx), q); }
+HD i64 gauss(u64 seed, u64 stream, u64 idx, const u64* cdt) {
+    u64 r = prng(seed, stream, idx);
+    u64 mag = r & 0x7fffffffffffffffULL;
+    i64 k = 0;
+    while (mag >= cdt[k]) ++k;
+    return (r >> 63) ? -k : k;
+}
+
+// index of the NTT slot read by the automorphism X -> X^g at NTT index k
+HD u32 galois_src(u32 k, u32 g, u32 logN) {
+#ifdef __CUDA_ARCH__
+    const u32 bk = __brev(k) >> (32 - logN);
+#else
+    u32 bk = 0;
+    for (u32 i = 0, x = k; i < logN; ++i, x >>= 1) bk = (bk << 1) | (x & 1);
+#endif
+    const u32 twoN_mask = (2u << logN) - 1;
+    const u32 e = (u32)(((unsigned long long)g * (2 * bk + 1)) & twoN_mask);
+#ifdef __CUDA_ARCH__
+    return __brev((e - 1) >> 1) >> (32 - logN);
+#else
+    u32 v = (e - 1) >> 1, r = 0;
+    for (u32 i = 0; i < logN; ++i, v >>= 1) r = (r << 1) | (v & 1);
+    return r;
+#endif
+}
+
+}  // namespace hgm

@@ -1,0 +1,138 @@
+// context.hpp -- per-device BFV context: tables and keys resident in HBM, the
+// content-addressed plaintext-mask cache, pinned staging, and the batched
+// primitive launchers that every higher layer (C ABI, lazy engine) calls.
+//
+// Every primitive works on a batch of independent items given as arrays of
+// device pointers, so one launch sequence serves many ciphertexts (many
+// rotations of one HEGMM call, or the same op of many lockstep instances).
+// Ciphertexts are 2*L*N words, c0 limbs then c1 limbs, NTT domain, canonical.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+#include "ntt.cuh"
+#include "params.hpp"
+
+namespace hgm {
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+void cuda_check(cudaError_t e, const char* what);
+#define HGM_CUDA(x) ::hgm::cuda_check((x), #x)
+
+// Host-pinned ring for uploads of small argument tables and input values.
+class PinnedRing {
+  public:
+    explicit PinnedRing(size_t bytes);
+    ~PinnedRing();
+    // Copies `bytes` from host `src` to the returned device pointer,
+    // asynchronously on `s` (the device copy lives in `dev_` ring).
+    void* upload(const void* src, size_t bytes, cudaStream_t s);
+
+  private:
+    size_t cap_;
+    char* host_ = nullptr;
+    char* dev_ = nullptr;
+    size_t head_ = 0;
+    struct Mark {
+        size_t end;
+        cudaEvent_t ev;
+    };
+    std::vector<Mark> marks_;
+    std::vector<cudaEvent_t> free_events_;
+};
+
+class Context {
+  public:
+    Context(int param_id, u64 seed, int device);
+    ~Context();
+    Context(const Context&) = delete;
+    Context& operator=(const Context&) = delete;
+
+    const HostParams& host() const { return hp_; }
+    const DevParams& hdev() const { return hp_.dev; }
+    const DevParams* dparams() const { return dp_; }
+    cudaStream_t stream() const { return stream_; }
+    int device() const { return device_; }
+    size_t ct_words() const { return (size_t)2 * hp_.L * hp_.N; }
+    size_t slots() const { return hp_.N / 2; }
+
+    u64* alloc(size_t words);
+    void release(void* p);
+    void sync();
+    template <typename T>
+    T* upload(const std::vector<T>& v) {
+        return static_cast<T*>(ring_->upload(v.data(), v.size() * sizeof(T), stream_));
+    }
+
+    // ---------------------------------------------------------------- keys
+    const u64* ks_key(u32 kid);  // [dnum][2][R][N]; kid = Galois element, 0 = relin
+    void ensure_galois_keys(const std::vector<u32>& elements);
+    size_t key_count() const;
+    static u32 galois_of(i64 z, u32 N);  // 3^(z mod N/2) mod 2N; 1 for z = 0
+
+    // ---------------------------------------------------------------- masks
+    // NTT-domain centred lift of the batch-encoded mask over Q: [L][N].
+    const u64* mask_plain(const i64* mask, size_t S);
+
+    // ---------------------------------------------------------------- primitives
+    // host_vals[i] holds S[i] values; counters[i] is the encryption counter.
+    void encrypt(int n, const i64* const* host_vals, const size_t* S, const u64* counters,
+                 u64* const* out);
+    // Decrypts n ciphertexts into host buffers (synchronises the stream).
+    void decrypt(int n, const u64* const* in, const size_t* S, i64* const* host_out);
+    void add(int n, const u64* const* a, const u64* const* b, u64* const* out);
+    // out[o] = sum over terms t in [off[o], off[o+1]) of in[t] (.* mask[t] if set)
+    void lincomb(int n_out, const u32* off, const u64* const* in, const u64* const* mask,
+                 u64* const* out);
+    // Hoisted half of key switching: digits of c1, lifted to Q++P, NTT domain.
+    size_t modup_words() const { return (size_t)hp_.dnum * hp_.R * hp_.N; }
+    void modup(int n, const u64* const* ct, u64* const* out);
+    // out = Rot(ct, g) from ct's ModUp image.
+    void rotate(int n, const u64* const* modup, const u64* const* ct, const u32* g,
+                u64* const* out);
+    void mult(int n, const u64* const* a, const u64* const* b, u64* const* out);
+    void copy(int n, const u64* const* in, u64* const* out);
+
+    // batched NTT helpers (exposed for tests / micro-benchmarks)
+    void ntt(bool forward, const NttJobs& jobs);
+    u64 launches() const { return launches_.load(); }
+
+  private:
+    void build_keys();
+    void key_switch_tail(int n, u64* const* acc, const u64* const* add0, const u32* g0,
+                         const u64* const* add1, u64* const* out);
+    void inner_product(int n, const u64* const* digits, const u64* const* keys, const u32* g,
+                       u64* const* acc);
+
+    HostParams hp_;
+    std::atomic<u64> launches_{0};
+    int device_ = 0;
+    cudaStream_t stream_ = nullptr;
+    DevParams* dp_ = nullptr;
+    u64* d_tw_ = nullptr;
+    u32* d_slot_ = nullptr;
+    u64* d_cdt_ = nullptr;
+    u64* d_sk_ = nullptr;  // [R][N]
+    u64* d_pk_ = nullptr;  // [2][L][N]
+    std::unique_ptr<PinnedRing> ring_;
+    mutable std::mutex key_mu_;
+    std::unordered_map<u32, u64*> keys_;
+    std::mutex mask_mu_;
+    struct MaskEntry {
+        std::vector<i64> content;
+        u64* dev;
+    };
+    std::unordered_map<u64, std::vector<MaskEntry>> masks_;
+};
+
+}  // namespace hgm

@@ -1,0 +1,84 @@
+// engine.hpp -- HE programs and their batched execution on one GPU.
+//
+// A Program is the cloud-side op DAG of one HEGMM call (or of the pending
+// ops of a lazy session), recorded through the reference's op vocabulary:
+// encrypt / he_rot / he_cmult / he_add / he_mult (backend.hpp:113-119).
+// The executor runs it for K independent instances in lockstep and applies
+// only EXACT rewrites, so results stay bit-identical to op-by-op execution
+// (oracle/bfv_oracle.cpp):
+//   * he_rot by 0 (mod N/2) is the identity;
+//   * identical rotations of one ciphertext are computed once (CSE);
+//   * all rotations of one ciphertext share one ModUp (hoisting; exact because
+//     the digit lift uses centred residues and commutes with X -> X^g);
+//   * trees of he_add over he_cmult / he_add become one masked sum
+//     (modular adds are associative and commutative);
+//   * every op of one dependency level is one batched launch sequence over
+//     all (node, instance) pairs; rotations are grouped by Galois key so that
+//     one key read from HBM serves the whole group.
+#pragma once
+#include <functional>
+#include <memory>
+#include <vector>
+
+#include "context.hpp"
+
+namespace hgm {
+
+struct MaskData {
+    std::vector<i64> v;
+};
+using MaskRef = std::shared_ptr<const MaskData>;
+
+struct PNode {
+    enum Kind : unsigned char { Input, Enc, Rot, Comb, Mult };
+    Kind kind = Input;
+    std::vector<int> in;          // Rot: {src}; Mult: {a, b}; Comb: term inputs
+    std::vector<MaskRef> masks;   // Comb: one per term, null = plain addend
+    u32 g = 1;                    // Rot: Galois element
+    int slot = -1;                // Input / Enc: external index
+    size_t S = 0;                 // logical segment length
+};
+
+struct Program {
+    std::vector<PNode> nodes;
+    std::vector<int> outputs;
+    int n_inputs = 0;  // Input slots
+    int n_enc = 0;     // Enc slots
+    int add_input(size_t S);
+    int add_enc(size_t S);
+    int add_rot(int src, u32 g);
+    int add_comb(std::vector<int> in, std::vector<MaskRef> masks);
+    int add_mult(int a, int b);
+};
+
+// Optimised, levelised form of a Program (built once, reused for every batch).
+struct Schedule {
+    Program prog;                        // rewritten program
+    std::vector<std::vector<int>> levels;
+    std::vector<int> last_use_level;     // -1: never read
+    std::vector<char> is_output;
+    size_t rot_count = 0, comb_count = 0, mult_count = 0;
+};
+Schedule optimise(const Program& p);
+
+struct ExecIO {
+    int K = 1;
+    // Input slot s of instance k -> device ciphertext
+    std::function<const u64*(int s, int k)> input;
+    // Enc slot s of instance k -> host values and encryption counter
+    std::function<const i64*(int s, int k)> enc_values;
+    std::function<u64(int s, int k)> enc_counter;
+};
+
+// Executes `sch` for io.K instances; returns, for each output o, a device
+// buffer of K consecutive ciphertexts (caller releases with ctx.release).
+std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io);
+
+// Kernel-launch accounting of the last execute() on this thread.
+struct ExecCounters {
+    size_t levels = 0, launches = 0, rot_items = 0, modup_items = 0, comb_items = 0,
+           mult_items = 0, enc_items = 0;
+};
+ExecCounters last_exec_counters();
+
+}  // namespace hgm

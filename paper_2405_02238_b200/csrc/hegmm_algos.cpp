@@ -1,0 +1,511 @@
+// hegmm_algos.cpp -- HEGMM (Algorithm 1) and HEGMM-Enhanced (Algorithm 2) as
+// recorded HE programs.  Each function names the reference routine whose op
+// stream it reproduces.
+#include "hegmm_algos.hpp"
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <set>
+#include <tuple>
+
+namespace hgm {
+
+size_t Plan::rotations() const {
+    size_t r = 0;
+    for (const auto& e : entries) r += e.offset != 0;
+    return r;
+}
+
+namespace {
+
+// ------------------------------------------------------------ matrix packing
+// reference matrix.cpp:99-176 (sigma, tau, eps, omega, duplication)
+Mat sigma(const Mat& a) {
+    Mat o(a.rows, a.cols);
+    for (size_t i = 0; i < a.rows; ++i)
+        for (size_t j = 0; j < a.cols; ++j) o.at(i, j) = a.at(i, (i + j) % a.cols);
+    return o;
+}
+Mat tau(const Mat& b) {
+    Mat o(b.rows, b.cols);
+    for (size_t i = 0; i < b.rows; ++i)
+        for (size_t j = 0; j < b.cols; ++j) o.at(i, j) = b.at((i + j) % b.rows, j);
+    return o;
+}
+Mat shift_cols(const Mat& a, size_t k, size_t out_rows, size_t out_cols) {  // eps
+    Mat o(out_rows, out_cols);
+    for (size_t i = 0; i < out_rows; ++i)
+        for (size_t j = 0; j < out_cols; ++j) o.at(i, j) = a.at(i, (j + k) % a.cols);
+    return o;
+}
+Mat shift_rows(const Mat& b, size_t k, size_t out_rows, size_t out_cols) {  // omega
+    Mat o(out_rows, out_cols);
+    for (size_t i = 0; i < out_rows; ++i)
+        for (size_t j = 0; j < out_cols; ++j) o.at(i, j) = b.at((i + k) % b.rows, j);
+    return o;
+}
+Mat stack_rows(const Mat& a, size_t t) {
+    Mat o(a.rows * t, a.cols);
+    for (size_t i = 0; i < o.rows; ++i)
+        for (size_t j = 0; j < o.cols; ++j) o.at(i, j) = a.at(i % a.rows, j);
+    return o;
+}
+Mat stack_cols(const Mat& b, size_t t) {
+    Mat o(b.rows, b.cols * t);
+    for (size_t i = 0; i < o.rows; ++i)
+        for (size_t j = 0; j < o.cols; ++j) o.at(i, j) = b.at(i, j % b.cols);
+    return o;
+}
+std::vector<i64> flatten_padded(const Mat& a, Order o, size_t segment) {
+    std::vector<i64> v(segment, 0);
+    for (size_t r = 0; r < a.rows; ++r)
+        for (size_t c = 0; c < a.cols; ++c) v[flat_index(r, c, a.rows, a.cols, o)] = a.at(r, c);
+    return v;
+}
+
+// ------------------------------------------------------------ plans
+// reference lintrans.cpp:139-159: group (out, in) pairs by z = in - out
+std::shared_ptr<Plan> plan_from_pairs(const std::vector<std::pair<size_t, size_t>>& pairs,
+                                      size_t in_len, size_t out_len, size_t mask_len) {
+    std::map<i64, std::vector<i64>> by;
+    for (const auto& pr : pairs) {
+        const i64 z = (i64)pr.second - (i64)pr.first;
+        auto it = by.find(z);
+        if (it == by.end()) it = by.emplace(z, std::vector<i64>(mask_len, 0)).first;
+        it->second[pr.first] = 1;
+    }
+    auto plan = std::make_shared<Plan>();
+    plan->in_len = in_len;
+    plan->out_len = out_len;
+    for (auto& kv : by) {
+        auto md = std::make_shared<MaskData>();
+        md->v = std::move(kv.second);
+        plan->entries.push_back(PlanEntry{kv.first, md});
+    }
+    return plan;
+}
+
+void check_shift(size_t k, size_t mod, const char* what) {
+    if (mod == 0 || k >= mod)
+        throw DimensionError(std::string(what) + " shift index " + std::to_string(k) + " outside [0, " +
+                             std::to_string(mod) + ")");
+}
+
+// eps_k: out (i, j) of m x n reads (i, (j+k) mod l) of m x l (lintrans.cpp:108-117)
+std::shared_ptr<Plan> eps_plan(size_t k, size_t m, size_t l, size_t n, Order o) {
+    check_shift(k, l, "eps");
+    std::vector<std::pair<size_t, size_t>> pairs;
+    pairs.reserve(m * n);
+    for (size_t i = 0; i < m; ++i)
+        for (size_t j = 0; j < n; ++j)
+            pairs.emplace_back(flat_index(i, j, m, n, o), flat_index(i, (j + k) % l, m, l, o));
+    std::sort(pairs.begin(), pairs.end());
+    return plan_from_pairs(pairs, m * l, m * n, m * n);
+}
+// omega_k: out (i, j) of m x n reads ((i+k) mod l, j) of l x n (lintrans.cpp:118-127)
+std::shared_ptr<Plan> omega_plan(size_t k, size_t l, size_t m, size_t n, Order o) {
+    check_shift(k, l, "omega");
+    std::vector<std::pair<size_t, size_t>> pairs;
+    pairs.reserve(m * n);
+    for (size_t i = 0; i < m; ++i)
+        for (size_t j = 0; j < n; ++j)
+            pairs.emplace_back(flat_index(i, j, m, n, o), flat_index((i + k) % l, j, l, n, o));
+    std::sort(pairs.begin(), pairs.end());
+    return plan_from_pairs(pairs, l * n, m * n, m * n);
+}
+// lintrans.cpp:244-263
+std::shared_ptr<Plan> embed(const Plan& p, size_t segment) {
+    if (segment < std::max(p.in_len, p.out_len))
+        throw DimensionError("segment " + std::to_string(segment) + " too small for a plan of lengths " +
+                             std::to_string(p.in_len) + "->" + std::to_string(p.out_len));
+    auto out = std::make_shared<Plan>();
+    out->in_len = out->out_len = segment;
+    for (const auto& e : p.entries) {
+        auto md = std::make_shared<MaskData>();
+        md->v.assign(segment, 0);
+        std::copy(e.mask->v.begin(), e.mask->v.end(), md->v.begin());
+        out->entries.push_back(PlanEntry{e.offset, md});
+    }
+    return out;
+}
+
+using PlanKey = std::tuple<int, size_t, size_t, size_t, size_t, int, size_t>;
+std::mutex g_plan_mu;
+std::map<PlanKey, std::shared_ptr<const Plan>> g_plans;
+
+template <typename F>
+std::shared_ptr<const Plan> cached(const PlanKey& key, F&& build) {
+    {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        auto it = g_plans.find(key);
+        if (it != g_plans.end()) return it->second;
+    }
+    std::shared_ptr<const Plan> p = build();
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    return g_plans.emplace(key, p).first->second;
+}
+
+size_t plan_size(int tag, size_t k, size_t m, size_t l, size_t n, Order o) {
+    return cached(PlanKey{tag, k, m, l, n, (int)o, 0}, [&] {
+               return tag == 0 ? eps_plan(k, m, l, n, o) : omega_plan(k, l, m, n, o);
+           })->entries.size();
+}
+
+}  // namespace
+
+std::shared_ptr<const Plan> eps_plan_embedded(size_t k, size_t m, size_t l, size_t n, Order o,
+                                              size_t segment) {
+    return cached(PlanKey{2, k, m, l, n, (int)o, segment}, [&] {
+        auto base = cached(PlanKey{0, k, m, l, n, (int)o, 0}, [&] { return eps_plan(k, m, l, n, o); });
+        return embed(*base, segment);
+    });
+}
+std::shared_ptr<const Plan> omega_plan_embedded(size_t k, size_t l, size_t m, size_t n, Order o,
+                                                size_t segment) {
+    return cached(PlanKey{3, k, m, l, n, (int)o, segment}, [&] {
+        auto base = cached(PlanKey{1, k, m, l, n, (int)o, 0}, [&] { return omega_plan(k, l, m, n, o); });
+        return embed(*base, segment);
+    });
+}
+// lintrans.cpp:265-283: columns of the M x max(l, N') buffer repeat with period l
+std::shared_ptr<const Plan> shaped_eps_plan(size_t k, size_t rows, size_t out_cols, size_t period,
+                                            Order o, size_t segment) {
+    return cached(PlanKey{4, k, rows, out_cols, period, (int)o, segment}, [&] {
+        check_shift(k, period, "eps");
+        const size_t buf_cols = std::max(period, out_cols);
+        if (segment < std::max(rows * buf_cols, rows * out_cols))
+            throw DimensionError("segment too small for shaped eps plan");
+        std::vector<std::pair<size_t, size_t>> pairs;
+        for (size_t r = 0; r < rows; ++r)
+            for (size_t c = 0; c < out_cols; ++c) {
+                const size_t src = c + k < buf_cols ? c + k : c + k - period;
+                pairs.emplace_back(flat_index(r, c, rows, out_cols, o), flat_index(r, src, rows, buf_cols, o));
+            }
+        return plan_from_pairs(pairs, segment, segment, segment);
+    });
+}
+// lintrans.cpp:285-302: rows of the max(l, M) x N' buffer repeat with period l
+std::shared_ptr<const Plan> shaped_omega_plan(size_t k, size_t out_rows, size_t cols,
+                                              size_t period, Order o, size_t segment) {
+    return cached(PlanKey{5, k, out_rows, cols, period, (int)o, segment}, [&] {
+        check_shift(k, period, "omega");
+        const size_t buf_rows = std::max(period, out_rows);
+        if (segment < std::max(buf_rows * cols, out_rows * cols))
+            throw DimensionError("segment too small for shaped omega plan");
+        std::vector<std::pair<size_t, size_t>> pairs;
+        for (size_t r = 0; r < out_rows; ++r)
+            for (size_t c = 0; c < cols; ++c) {
+                const size_t src = r + k < buf_rows ? r + k : r + k - period;
+                pairs.emplace_back(flat_index(r, c, out_rows, cols, o), flat_index(src, c, buf_rows, cols, o));
+            }
+        return plan_from_pairs(pairs, segment, segment, segment);
+    });
+}
+
+namespace {
+
+// ------------------------------------------------------------ recorder
+struct Recorder {
+    Program prog;
+    Counts counts;
+    int phase = 0;
+    u32 N = 0;
+    std::vector<std::pair<int, i64>> stream;
+    std::vector<MaskRef> smasks;
+
+    size_t seg(int x) const { return prog.nodes[x].S; }
+    int enc(size_t S) {
+        counts.at(kEnc, phase)++;
+        stream.emplace_back(0, (i64)S);
+        return prog.add_enc(S);
+    }
+    void dec(int x) {
+        counts.at(kDec, phase)++;
+        stream.emplace_back(1, (i64)seg(x));
+        prog.outputs.push_back(x);
+    }
+    int add(int a, int b) {
+        if (seg(a) != seg(b)) throw DimensionError("he_add segment mismatch");
+        counts.at(kAdd, phase)++;
+        stream.emplace_back(2, (i64)seg(a));
+        return prog.add_comb({a, b}, {nullptr, nullptr});
+    }
+    int mult(int a, int b) {
+        if (seg(a) != seg(b)) throw DimensionError("he_mult segment mismatch");
+        counts.at(kMultCC, phase)++;
+        stream.emplace_back(3, (i64)seg(a));
+        return prog.add_mult(a, b);
+    }
+    int cmult(int a, const MaskRef& m) {
+        if (m->v.size() != seg(a)) throw DimensionError("he_cmult mask length does not match segment");
+        counts.at(kMultCP, phase)++;
+        stream.emplace_back(4, (i64)m->v.size());
+        smasks.push_back(m);
+        return prog.add_comb({a}, {m});
+    }
+    int rot(int a, i64 z) {
+        counts.at(kRot, phase)++;
+        stream.emplace_back(5, z);
+        return prog.add_rot(a, Context::galois_of(z, N));
+    }
+};
+
+// reference apply_plan (lintrans.cpp:433-461)
+int apply_plan(Recorder& R, int ct, const Plan& plan) {
+    if (plan.in_len != plan.out_len)
+        throw DimensionError("apply_plan needs a square working segment, got " + std::to_string(plan.in_len) +
+                             "->" + std::to_string(plan.out_len));
+    if (R.seg(ct) != plan.in_len)
+        throw DimensionError("ciphertext segment " + std::to_string(R.seg(ct)) + " does not match plan length " +
+                             std::to_string(plan.in_len));
+    if (plan.entries.empty()) throw DimensionError("cannot apply an empty plan");
+    int acc = -1;
+    for (const auto& e : plan.entries) {
+        const int term = e.offset == 0 ? R.cmult(ct, e.mask) : R.cmult(R.rot(ct, e.offset), e.mask);
+        acc = acc < 0 ? term : R.add(acc, term);
+    }
+    return acc;
+}
+
+void check_capacity(size_t need, size_t slots, const char* what) {
+    if (need > slots)
+        throw CapacityError(std::string(what) + " needs " + std::to_string(need) + " slots but the backend has " +
+                            std::to_string(slots));
+}
+
+size_t kept_blocks(size_t k, size_t p, size_t l) { return (l - k + p - 1) / p; }
+
+void en_shape(size_t l, size_t rows_w, size_t cols_w, size_t& buf_a_cols, size_t& buf_b_rows, size_t& segment) {
+    buf_a_cols = std::max(l, cols_w);
+    buf_b_rows = std::max(l, rows_w);
+    segment = std::max(rows_w * buf_a_cols, buf_b_rows * cols_w);
+}
+
+// reference finalize_strategy (algorithms.cpp:89-117)
+void finalize(Strategy& s, size_t l) {
+    size_t a, b;
+    en_shape(l, s.rows_w, s.cols_w, a, b, s.segment);
+    Counts c;
+    c.at(kMultCC, 1) = s.p;
+    std::set<size_t> masked;
+    for (size_t k = 0; k < s.p; ++k) {
+        auto pe = shaped_eps_plan(k, s.rows_w, s.cols_w, l, s.order, s.segment);
+        auto po = shaped_omega_plan(k, s.rows_w, s.cols_w, l, s.order, s.segment);
+        c.at(kRot, 1) += pe->rotations() + po->rotations();
+        c.at(kMultCP, 1) += pe->entries.size() + po->entries.size();
+        c.at(kAdd, 1) += pe->entries.size() - 1 + po->entries.size() - 1;
+        const size_t kept = kept_blocks(k, s.p, l);
+        if (kept < s.t) masked.insert(kept);
+    }
+    c.at(kAdd, 1) += s.p - 1;
+    c.at(kMultCP, 1) += masked.size();
+    if (s.t > 1) {
+        c.at(kRot, 1) += s.t - 1;
+        c.at(kAdd, 1) += s.t - 1;
+    }
+    s.predicted = c;
+}
+
+// reference prefix_mask (algorithms.cpp:119-139)
+MaskRef prefix_mask(size_t kept, Dup dup, size_t p, size_t rows_w, size_t cols_w, Order o, size_t segment) {
+    auto md = std::make_shared<MaskData>();
+    md->v.assign(segment, 0);
+    for (size_t h = 0; h < kept; ++h) {
+        if (dup == Dup::AVertical) {
+            for (size_t r = h * p; r < (h + 1) * p; ++r)
+                for (size_t c = 0; c < cols_w; ++c) md->v[flat_index(r, c, rows_w, cols_w, o)] = 1;
+        } else {
+            for (size_t r = 0; r < rows_w; ++r)
+                for (size_t c = h * p; c < (h + 1) * p; ++c) md->v[flat_index(r, c, rows_w, cols_w, o)] = 1;
+        }
+    }
+    return md;
+}
+
+Mat mat_from(const i64* p, size_t r, size_t c) {
+    Mat m(r, c);
+    std::copy(p, p + r * c, m.d.begin());
+    return m;
+}
+
+}  // namespace
+
+// reference select_strategy (algorithms.cpp:143-170)
+Strategy select_strategy(size_t m, size_t l, size_t n) {
+    if (m == 0 || l == 0 || n == 0) throw DimensionError("dimensions must be positive");
+    Strategy s;
+    s.p = std::min({m, l, n});
+    s.t = (l + s.p - 1) / s.p;
+    if (s.p == l) {
+        s.dup = Dup::None;
+        s.order = Order::Col;
+        s.rows_w = m;
+        s.cols_w = n;
+    } else if (s.p == m) {
+        s.dup = Dup::AVertical;
+        s.order = Order::Col;
+        s.rows_w = s.t * m;
+        s.cols_w = n;
+    } else {
+        s.dup = Dup::BHorizontal;
+        s.order = Order::Row;
+        s.rows_w = m;
+        s.cols_w = s.t * n;
+    }
+    finalize(s, l);
+    return s;
+}
+
+std::vector<std::vector<i64>> MatmulProgram::pack(const i64* A, const i64* B) const {
+    const Mat a = mat_from(A, m, l), b = mat_from(B, l, n);
+    std::vector<std::vector<i64>> out;
+    if (algo == Algo::Basic) {
+        out.push_back(flatten_padded(sigma(a), order, segment));
+        out.push_back(flatten_padded(tau(b), order, segment));
+        out.emplace_back(segment, 0);
+    } else {
+        size_t buf_a_cols, buf_b_rows, seg;
+        en_shape(l, strat.rows_w, strat.cols_w, buf_a_cols, buf_b_rows, seg);
+        const Mat abar = strat.dup == Dup::AVertical ? stack_rows(a, strat.t) : a;
+        const Mat bbar = strat.dup == Dup::BHorizontal ? stack_cols(b, strat.t) : b;
+        out.push_back(flatten_padded(shift_cols(sigma(abar), 0, strat.rows_w, buf_a_cols), order, segment));
+        out.push_back(flatten_padded(shift_rows(tau(bbar), 0, buf_b_rows, strat.cols_w), order, segment));
+    }
+    return out;
+}
+
+void MatmulProgram::unpack(const std::vector<i64>& v, i64* C) const {
+    if (algo == Algo::Basic) {
+        for (size_t r = 0; r < m; ++r)
+            for (size_t c = 0; c < n; ++c) C[r * n + c] = v[flat_index(r, c, m, n, order)];
+    } else {
+        for (size_t r = 0; r < m; ++r)
+            for (size_t c = 0; c < n; ++c) C[r * n + c] = v[flat_index(r, c, strat.rows_w, strat.cols_w, order)];
+    }
+}
+
+namespace {
+
+// reference basic_mm (algorithms.cpp:198-248)
+std::shared_ptr<MatmulProgram> build_basic(int order_opt, size_t m, size_t l, size_t n, size_t slots, u32 N) {
+    check_capacity(m * l, slots, "flattened left operand");
+    check_capacity(l * n, slots, "flattened right operand");
+    check_capacity(m * n, slots, "flattened product");
+    auto mp = std::make_shared<MatmulProgram>();
+    mp->algo = Algo::Basic;
+    mp->m = m; mp->l = l; mp->n = n; mp->slots = slots;
+    mp->segment = std::max({m * l, l * n, m * n});
+    if (order_opt >= 0) {
+        mp->order = (Order)order_opt;
+    } else {
+        size_t col = 0, row = 0;
+        for (size_t k = 0; k < l; ++k) {
+            col += plan_size(0, k, m, l, n, Order::Col) + plan_size(1, k, m, l, n, Order::Col);
+            row += plan_size(0, k, m, l, n, Order::Row) + plan_size(1, k, m, l, n, Order::Row);
+        }
+        mp->order = row < col ? Order::Row : Order::Col;
+    }
+    Recorder R;
+    R.N = N;
+    R.phase = 0;
+    const int ca = R.enc(mp->segment), cb = R.enc(mp->segment);
+    int acc = R.enc(mp->segment);
+    R.phase = 1;
+    for (size_t k = 0; k < l; ++k) {
+        const int e = apply_plan(R, ca, *eps_plan_embedded(k, m, l, n, mp->order, mp->segment));
+        const int w = apply_plan(R, cb, *omega_plan_embedded(k, l, m, n, mp->order, mp->segment));
+        const int prod = R.mult(e, w);
+        acc = R.add(acc, prod);
+    }
+    R.phase = 0;
+    R.dec(acc);
+    mp->n_enc = R.prog.n_enc;
+    mp->counts = R.counts;
+    mp->stream = std::move(R.stream);
+    mp->stream_masks = std::move(R.smasks);
+    mp->sched = optimise(R.prog);
+    return mp;
+}
+
+// reference enhanced_mm (algorithms.cpp:250-367)
+std::shared_ptr<MatmulProgram> build_enhanced(int order_opt, size_t m, size_t l, size_t n, size_t slots, u32 N) {
+    Strategy s = select_strategy(m, l, n);
+    if (order_opt >= 0 && (Order)order_opt != s.order) {
+        s.order = (Order)order_opt;
+        finalize(s, l);
+    }
+    size_t buf_a_cols, buf_b_rows, segment;
+    en_shape(l, s.rows_w, s.cols_w, buf_a_cols, buf_b_rows, segment);
+    check_capacity(segment, slots, "expanded working set");
+    auto mp = std::make_shared<MatmulProgram>();
+    mp->algo = Algo::Enhanced;
+    mp->m = m; mp->l = l; mp->n = n; mp->slots = slots;
+    mp->segment = segment;
+    mp->order = s.order;
+    mp->strat = s;
+    Recorder R;
+    R.N = N;
+    R.phase = 0;
+    const int ca = R.enc(segment), cb = R.enc(segment);
+    R.phase = 1;
+    std::map<size_t, int> groups;
+    for (size_t k = 0; k < s.p; ++k) {
+        const int e = apply_plan(R, ca, *shaped_eps_plan(k, s.rows_w, s.cols_w, l, s.order, segment));
+        const int w = apply_plan(R, cb, *shaped_omega_plan(k, s.rows_w, s.cols_w, l, s.order, segment));
+        const int temp = R.mult(e, w);
+        const size_t kept = kept_blocks(k, s.p, l);
+        auto it = groups.find(kept);
+        if (it == groups.end())
+            groups.emplace(kept, temp);
+        else
+            it->second = R.add(it->second, temp);
+    }
+    int acc = -1;
+    for (auto& kv : groups) {
+        const int masked = kv.first < s.t
+                               ? R.cmult(kv.second, prefix_mask(kv.first, s.dup, s.p, s.rows_w, s.cols_w, s.order, segment))
+                               : kv.second;
+        acc = acc < 0 ? masked : R.add(acc, masked);
+    }
+    int folded = acc;
+    if (s.t > 1) {
+        const size_t stride = s.dup == Dup::AVertical ? (s.order == Order::Col ? m : m * s.cols_w)
+                                                      : (s.order == Order::Col ? n * s.rows_w : n);
+        for (size_t h = 1; h < s.t; ++h) {
+            const int r = R.rot(acc, (i64)(h * stride));
+            folded = R.add(folded, r);
+        }
+    }
+    R.phase = 0;
+    R.dec(folded);
+    mp->n_enc = R.prog.n_enc;
+    mp->counts = R.counts;
+    mp->stream = std::move(R.stream);
+    mp->stream_masks = std::move(R.smasks);
+    mp->sched = optimise(R.prog);
+    return mp;
+}
+
+std::mutex g_prog_mu;
+std::map<std::tuple<int, int, size_t, size_t, size_t, size_t, u32>, std::shared_ptr<const MatmulProgram>> g_progs;
+
+}  // namespace
+
+std::shared_ptr<const MatmulProgram> get_matmul_program(int algo, int order, size_t m, size_t l, size_t n,
+                                                        size_t slots, u32 N) {
+    if (m == 0 || l == 0 || n == 0) throw DimensionError("matrix dimensions must be positive");
+    if (algo != 0 && algo != 1) throw DimensionError("unknown algorithm id");
+    const auto key = std::make_tuple(algo, order, m, l, n, slots, N);
+    {
+        std::lock_guard<std::mutex> lk(g_prog_mu);
+        auto it = g_progs.find(key);
+        if (it != g_progs.end()) return it->second;
+    }
+    std::shared_ptr<const MatmulProgram> p =
+        algo == 0 ? build_basic(order, m, l, n, slots, N) : build_enhanced(order, m, l, n, slots, N);
+    std::lock_guard<std::mutex> lk(g_prog_mu);
+    return g_progs.emplace(key, p).first->second;
+}
+
+}  // namespace hgm

@@ -1,0 +1,46 @@
+// ntt.cuh -- batched negacyclic NTT / INTT over 64-bit primes.
+//
+// One CTA transforms one block of NB = 2^LB residues (one limb for N <= 8192,
+// a quarter limb for N = 32768) entirely in shared memory:
+//   coalesced 16-byte loads -> smem -> 3 register rounds of up to 5 radix-2
+//   stages each (Cooley-Tukey forward / Gentleman-Sande inverse) -> smem ->
+//   coalesced stores.
+// The smem image is padded one word per 16 (pad()) so that the stride-16 and
+// contiguous-16 access patterns of the three rounds are bank-conflict free.
+// Twiddles are Shoup pairs read through the read-only path; every twiddle is
+// loaded once per group and stage.  For N = 2^15 the two outermost stages run
+// in a separate coalesced pass (pre-pass for the forward transform, post-pass
+// with the N^-1 scaling for the inverse).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace hgm {
+
+// A batch of in-place transforms.  Job j works on ptrs[j] if ptrs is set,
+// else on base + j*N; its prime is prime[j % period] (index into DevParams::pr,
+// kTIndex for the plaintext modulus).
+struct NttJobs {
+    u64* base = nullptr;
+    u64* const* ptrs = nullptr;
+    u32 count = 0;
+    u32 period = 1;
+    unsigned char prime[32] = {0};
+    // optional fused scaling after an inverse transform: multiply by a
+    // per-prime Shoup constant (used to fold extra factors); null = none
+};
+
+void ntt_forward(const DevParams* dp, const DevParams& hp, const NttJobs& jobs, cudaStream_t s);
+void ntt_inverse(const DevParams* dp, const DevParams& hp, const NttJobs& jobs, cudaStream_t s);
+
+inline NttJobs jobs_contig(u64* base, u32 count, u32 first_prime, u32 period) {
+    NttJobs j;
+    j.base = base;
+    j.count = count;
+    j.period = period;
+    for (u32 i = 0; i < period && i < 32; ++i) j.prime[i] = (unsigned char)(first_prime + i);
+    return j;
+}
+
+}  // namespace hgm
