@@ -117,6 +117,41 @@ int hgm_matmul_batch_export(hgm_ctx* ctx, int algo, int order, size_t m, size_t 
                             size_t count, const int64_t* A, const int64_t* B, int64_t* C,
                             uint64_t counter0, uint64_t* final_words);
 
+/* The same pipeline split at the reference's phase boundaries
+ * (algorithms.cpp:216-247: Client encrypt / Cloud loop / Client decrypt):
+ *   hgm_batch_encrypt  packs and encrypts `count` instances (ciphertexts stay in HBM)
+ *   hgm_batch_cloud    runs the cloud program on them; *device_ms = CUDA-event time
+ *   hgm_batch_output   device pointer of instance i's result ciphertext (for gathers)
+ *   hgm_batch_decrypt  decrypts and unpacks every result into host C */
+typedef struct hgm_batch hgm_batch;
+int hgm_batch_encrypt(hgm_ctx* ctx, int algo, int order, size_t m, size_t l, size_t n, size_t count,
+                      const int64_t* A, const int64_t* B, uint64_t counter0, hgm_batch** out);
+int hgm_batch_cloud(hgm_ctx* ctx, hgm_batch* b, float* device_ms);
+uint64_t* hgm_batch_output(hgm_batch* b, size_t i);
+int hgm_batch_decrypt(hgm_ctx* ctx, hgm_batch* b, int64_t* C);
+int hgm_batch_decrypt_words(hgm_ctx* ctx, const uint64_t* dev_words, size_t count, size_t S,
+                            int64_t* out);
+void hgm_batch_free(hgm_batch* b);
+/* Program facts of a product shape (no GPU needed): stats[12] as hgm_stats,
+ * facts[0]=segment [1]=encryptions [2]=rotations after CSE [3]=masked sums
+ * [4]=CC-mults [5]=levels [6]=flatten order used. */
+int hgm_program_info(int algo, int order, size_t m, size_t l, size_t n, size_t slots, uint32_t N,
+                     uint64_t* stats, uint64_t* facts);
+/* Op stream of a product shape in call order (no GPU needed), same layout as
+ * the reference trace: hdr[3*i] = kind (0 enc 1 dec 2 add 3 mult 4 cmult 5 rot),
+ * hdr[3*i+1] = rotation offset / segment, hdr[3*i+2] = data length; data = the
+ * cmult masks concatenated.  Returns the op count (or -error). */
+long hgm_program_stream(int algo, int order, size_t m, size_t l, size_t n, size_t slots, uint32_t N,
+                        int64_t* hdr, size_t hdr_cap, int64_t* data, size_t data_cap,
+                        size_t* data_len);
+
+/* Diagonal plan introspection (no GPU): kind 0 = eps_k (a=m, b=l, c=n),
+ * 1 = omega_k (a=l, b=m, c=n) embedded in `segment`; 4 / 5 = the shaped
+ * eps / omega plans of enhanced_mm (a=rows, b=cols, c=period).  Writes up to
+ * cap (offset, weight) pairs; returns the entry count or -error. */
+long hgm_plan_info(int kind, size_t k, size_t a, size_t b, size_t c, int order, size_t segment,
+                   int64_t* offsets, uint64_t* weights, size_t cap);
+
 /* Kernel-level timing hooks for bench.py (CUDA events on the library stream). */
 int hgm_bench_ntt(hgm_ctx* ctx, int forward, size_t limbs, int iters, float* ms_per_iter);
 int hgm_device_sync(hgm_ctx* ctx);

@@ -167,6 +167,11 @@ class RefLib:
             L.ref_trace.argtypes = [_int, _int, _vp, _sz, _sz, _vp, _sz, _sz, _vp, _sz, _vp, _sz, _vp]
             L.ref_mm_oracle.restype = ctypes.c_long
             L.ref_mm_oracle.argtypes = [_int, _u64, _u64, _int, _int, _vp, _sz, _sz, _vp, _sz, _vp, _vp, _vp]
+            L.ref_oracle_session_create.restype = _vp
+            L.ref_oracle_session_create.argtypes = [_int, _u64]
+            L.ref_oracle_session_destroy.argtypes = [_vp]
+            L.ref_oracle_session_mm.restype = ctypes.c_long
+            L.ref_oracle_session_mm.argtypes = [_vp, _u64, _int, _int, _vp, _sz, _sz, _vp, _sz, _vp]
             cls._lib = L
         return cls._lib
 
@@ -228,3 +233,35 @@ class RefLib:
         if nxt < 0:
             raise OracleError(f"rc={nxt}: {cls._err()}")
         return C, st, ct, nxt
+
+
+class OracleSession:
+    """Reference algorithms over a persistent CPU-BFV oracle context (one per thread).
+    The ctypes calls release the GIL, so threads run truly in parallel."""
+
+    def __init__(self, param_id: int = 0, seed: int = 1):
+        self._h = RefLib.lib().ref_oracle_session_create(param_id, seed)
+        if not self._h:
+            raise OracleError(RefLib._err())
+
+    def mm(self, A, B, algo="basic", order=-1, counter0=0):
+        A = np.ascontiguousarray(A, dtype=np.int64)
+        B = np.ascontiguousarray(B, dtype=np.int64)
+        m, l = A.shape
+        n = B.shape[1]
+        C = np.zeros((m, n), dtype=np.int64)
+        nxt = RefLib.lib().ref_oracle_session_mm(self._h, counter0, ALGO[algo], order, _p(A), m, l, _p(B), n, _p(C))
+        if nxt < 0:
+            raise OracleError(f"rc={nxt}: {RefLib._err()}")
+        return C
+
+    def close(self):
+        if self._h:
+            RefLib.lib().ref_oracle_session_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -345,4 +345,27 @@ long ref_mm_oracle(int param_id, std::uint64_t seed, std::uint64_t counter0, int
     }
 }
 
+// Persistent oracle session (keys and tables built once, reused across products);
+// one session per thread.
+void* ref_oracle_session_create(int param_id, std::uint64_t seed) {
+    orc_ctx* ctx = orc_create(param_id, seed);
+    if (!ctx) g_err = orc_last_error();
+    return ctx;
+}
+void ref_oracle_session_destroy(void* s) { orc_destroy(static_cast<orc_ctx*>(s)); }
+long ref_oracle_session_mm(void* s, std::uint64_t counter0, int algo, int order, const std::int64_t* A,
+                           std::size_t m, std::size_t l, const std::int64_t* B, std::size_t n,
+                           std::int64_t* C) {
+    try {
+        Matrix a(m, l, std::vector<value_t>(A, A + m * l));
+        Matrix b(l, n, std::vector<value_t>(B, B + l * n));
+        OracleBackend be(static_cast<orc_ctx*>(s), counter0);
+        const Matrix c = run(algo, order, a, b, be);
+        std::memcpy(C, c.data().data(), m * n * 8);
+        return (long)be.counter();
+    } catch (const std::exception& e) {
+        return -rc_of(e);
+    }
+}
+
 }  // extern "C"

@@ -27,8 +27,88 @@ EXPORTS = (
     "hgm_ct_segment", "hgm_ct_depth", "hgm_ct_phase", "hgm_ct_retain", "hgm_ct_release",
     "hgm_stats", "hgm_reset_stats", "hgm_peak_live", "hgm_set_phase", "hgm_phase",
     "hgm_matmul_batch", "hgm_matmul_batch_export", "hgm_bench_ntt", "hgm_device_sync",
-    "hgm_test_ntt", "hgm_launch_count",
+    "hgm_test_ntt", "hgm_launch_count", "hgm_batch_encrypt", "hgm_batch_cloud", "hgm_batch_output",
+    "hgm_batch_decrypt", "hgm_batch_decrypt_words", "hgm_batch_free", "hgm_program_info",
+    "hgm_program_stream", "hgm_plan_info",
 )
+ALGOS = {"basic": 0, "enhanced": 1}
+
+
+def plan_info(kind: int, k: int, a: int, b: int, c: int, order: int, segment: int):
+    """(offsets, weights) of a diagonal plan (CPU only); see hgm_plan_info."""
+    off = np.zeros(4096, dtype=np.int64)
+    w = np.zeros(4096, dtype=np.uint64)
+    cnt = lib().hgm_plan_info(kind, k, a, b, c, order, segment, _ptr(off), _ptr(w), off.size)
+    if cnt < 0:
+        _check(-cnt)
+    return off[:cnt].tolist(), w[:cnt].astype(int).tolist()
+
+
+def program_info(algo: int, m: int, l: int, n: int, slots: int = 4096, N: int = 8192, order: int = -1):
+    """Op counts (stats[12]) and facts of a compiled HEGMM program (CPU only)."""
+    st = np.zeros(12, dtype=np.uint64)
+    facts = np.zeros(7, dtype=np.uint64)
+    _check(lib().hgm_program_info(algo, order, m, l, n, slots, N, _ptr(st), _ptr(facts)))
+    keys = ("segment", "encryptions", "rotations", "masked_sums", "cc_mults", "levels", "order")
+    return st, dict(zip(keys, (int(x) for x in facts)))
+
+
+def program_stream(algo: int, m: int, l: int, n: int, slots: int = 4096, N: int = 8192, order: int = -1):
+    """The recorded op stream (reference trace layout): (hdr[k,3], mask data)."""
+    dl = ctypes.c_size_t()
+    cnt = lib().hgm_program_stream(algo, order, m, l, n, slots, N, None, 0, None, 0, ctypes.byref(dl))
+    if cnt < 0:
+        _check(-cnt)
+    hdr = np.zeros(3 * cnt, dtype=np.int64)
+    data = np.zeros(max(1, dl.value), dtype=np.int64)
+    cnt2 = lib().hgm_program_stream(algo, order, m, l, n, slots, N, _ptr(hdr), hdr.size, _ptr(data), data.size,
+                                    ctypes.byref(dl))
+    if cnt2 < 0:
+        _check(-cnt2)
+    return hdr.reshape(-1, 3), data[:dl.value]
+
+
+class Batch:
+    """Encrypted inputs of `count` instances resident in HBM (client phase done)."""
+
+    def __init__(self, ctx: "Context", A: np.ndarray, B: np.ndarray, algo: int = 0, order: int = -1,
+                 counter0: int = 0):
+        A = _as_i64(A)
+        B = _as_i64(B)
+        if A.ndim == 2:
+            A, B = A[None], B[None]
+        self.ctx = ctx
+        self.count, self.m, self.l = A.shape
+        self.n = B.shape[2]
+        h = ctypes.c_void_p()
+        _check(lib().hgm_batch_encrypt(ctx._h, algo, order, self.m, self.l, self.n, self.count, _ptr(A),
+                                       _ptr(B), counter0, ctypes.byref(h)))
+        self._h = h.value
+
+    def cloud(self) -> float:
+        """Run the cloud phase; returns its CUDA-event time in ms."""
+        ms = ctypes.c_float()
+        _check(lib().hgm_batch_cloud(self.ctx._h, self._h, ctypes.byref(ms)))
+        return ms.value
+
+    def output_ptr(self, i: int) -> int:
+        return lib().hgm_batch_output(self._h, i)
+
+    def decrypt(self) -> np.ndarray:
+        C = np.zeros((self.count, self.m, self.n), dtype=np.int64)
+        _check(lib().hgm_batch_decrypt(self.ctx._h, self._h, _ptr(C)))
+        return C
+
+    def free(self) -> None:
+        if self._h:
+            lib().hgm_batch_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 class HEError(RuntimeError):
@@ -96,6 +176,16 @@ def lib() -> ctypes.CDLL:
         "hgm_device_sync": (_int, [_vp]),
         "hgm_test_ntt": (_int, [_vp, _int, _int, _vp, _sz]),
         "hgm_launch_count": (_u64, [_vp]),
+        "hgm_batch_encrypt": (_int, [_vp, _int, _int, _sz, _sz, _sz, _sz, _vp, _vp, _u64, _vp]),
+        "hgm_batch_cloud": (_int, [_vp, _vp, _vp]),
+        "hgm_batch_output": (_vp, [_vp, _sz]),
+        "hgm_batch_decrypt": (_int, [_vp, _vp, _vp]),
+        "hgm_batch_decrypt_words": (_int, [_vp, _vp, _sz, _sz, _vp]),
+        "hgm_batch_free": (None, [_vp]),
+        "hgm_program_info": (_int, [_int, _int, _sz, _sz, _sz, _sz, ctypes.c_uint32, _vp, _vp]),
+        "hgm_program_stream": (ctypes.c_long, [_int, _int, _sz, _sz, _sz, _sz, ctypes.c_uint32, _vp, _sz,
+                                               _vp, _sz, _vp]),
+        "hgm_plan_info": (ctypes.c_long, [_int, _sz, _sz, _sz, _sz, _int, _sz, _vp, _vp, _sz]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

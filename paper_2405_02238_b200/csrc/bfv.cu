@@ -4,6 +4,7 @@
 // name the oracle routine each kernel reproduces.  Shapes: n items per launch,
 // thread per (item, coefficient), loops over RNS limbs inside the thread so a
 // warp's loads are coalesced within each limb.
+#include <algorithm>
 #include <cstring>
 #include <stdexcept>
 
@@ -18,6 +19,8 @@ void cuda_check(cudaError_t e, const char* what) {
 namespace {
 
 constexpr int kThreads = 256;
+// items per launch sequence: bounds temporaries and staging uploads
+constexpr int kChunkEnc = 256, kChunkDec = 1024, kChunkLin = 8192, kChunkKs = 1024, kChunkMult = 128;
 
 // values with |v| < q (noise, ternary, small messages)
 __device__ __forceinline__ u64 small_to_mod(i64 v, u64 q) { return v >= 0 ? (u64)v : q + v; }
@@ -690,6 +693,13 @@ const u64* Context::mask_plain(const i64* mask, size_t S) {
 void Context::encrypt(int n, const i64* const* host_vals, const size_t* S, const u64* counters,
                       u64* const* out) {
     if (n <= 0) return;
+    if (n > kChunkEnc) {
+        for (int c0 = 0; c0 < n; c0 += kChunkEnc) {
+            const int cn = std::min(kChunkEnc, n - c0);
+            encrypt(cn, host_vals + c0, S + c0, counters + c0, out + c0);
+        }
+        return;
+    }
     const u32 N = hp_.N, L = hp_.L, H = N / 2;
     std::vector<i64> vals((size_t)n * H, 0);
     std::vector<u32> Sv(n);
@@ -726,6 +736,13 @@ void Context::encrypt(int n, const i64* const* host_vals, const size_t* S, const
 
 void Context::decrypt(int n, const u64* const* in, const size_t* S, i64* const* host_out) {
     if (n <= 0) return;
+    if (n > kChunkDec) {
+        for (int c0 = 0; c0 < n; c0 += kChunkDec) {
+            const int cn = std::min(kChunkDec, n - c0);
+            decrypt(cn, in + c0, S + c0, host_out + c0);
+        }
+        return;
+    }
     const u32 N = hp_.N, L = hp_.L, H = N / 2;
     std::vector<const u64*> ins(in, in + n);
     std::vector<u32> Sv(n);
@@ -751,6 +768,13 @@ void Context::decrypt(int n, const u64* const* in, const size_t* S, i64* const* 
 
 void Context::add(int n, const u64* const* a, const u64* const* b, u64* const* out) {
     if (n <= 0) return;
+    if (n > kChunkLin) {
+        for (int c0 = 0; c0 < n; c0 += kChunkLin) {
+            const int cn = std::min(kChunkLin, n - c0);
+            add(cn, a + c0, b + c0, out + c0);
+        }
+        return;
+    }
     std::vector<const u64*> va(a, a + n), vb(b, b + n);
     std::vector<u64*> vo(out, out + n);
     k_add<<<grid_of(hp_.N, n, 1), kThreads, 0, stream_>>>(dp_, n, upload(va), upload(vb), upload(vo)); ++launches_;
@@ -759,6 +783,13 @@ void Context::add(int n, const u64* const* a, const u64* const* b, u64* const* o
 
 void Context::copy(int n, const u64* const* in, u64* const* out) {
     if (n <= 0) return;
+    if (n > kChunkLin) {
+        for (int c0 = 0; c0 < n; c0 += kChunkLin) {
+            const int cn = std::min(kChunkLin, n - c0);
+            copy(cn, in + c0, out + c0);
+        }
+        return;
+    }
     std::vector<const u64*> vi(in, in + n);
     std::vector<u64*> vo(out, out + n);
     k_copy<<<grid_of(hp_.N, n), kThreads, 0, stream_>>>(n, ct_words(), upload(vi), upload(vo)); ++launches_;
@@ -768,6 +799,15 @@ void Context::copy(int n, const u64* const* in, u64* const* out) {
 void Context::lincomb(int n_out, const u32* off, const u64* const* in, const u64* const* mask,
                       u64* const* out) {
     if (n_out <= 0) return;
+    if (n_out > kChunkLin) {
+        for (int c0 = 0; c0 < n_out; c0 += kChunkLin) {
+            const int cn = std::min(kChunkLin, n_out - c0);
+            std::vector<u32> sub(cn + 1);
+            for (int i = 0; i <= cn; ++i) sub[i] = off[c0 + i] - off[c0];
+            lincomb(cn, sub.data(), in + off[c0], mask + off[c0], out + c0);
+        }
+        return;
+    }
     const u32 nt = off[n_out];
     std::vector<u32> voff(off, off + n_out + 1);
     std::vector<const u64*> vin(in, in + nt), vm(mask, mask + nt);
@@ -779,6 +819,13 @@ void Context::lincomb(int n_out, const u32* off, const u64* const* in, const u64
 
 void Context::modup(int n, const u64* const* ct, u64* const* out) {
     if (n <= 0) return;
+    if (n > kChunkKs) {
+        for (int c0 = 0; c0 < n; c0 += kChunkKs) {
+            const int cn = std::min(kChunkKs, n - c0);
+            modup(cn, ct + c0, out + c0);
+        }
+        return;
+    }
     const u32 N = hp_.N, L = hp_.L, R = hp_.R, dnum = hp_.dnum;
     std::vector<const u64*> vc(ct, ct + n);
     u64* C = alloc((size_t)n * L * N);
@@ -849,6 +896,13 @@ void Context::key_switch_tail(int n, u64* const* acc, const u64* const* add0, co
 void Context::rotate(int n, const u64* const* modup, const u64* const* ct, const u32* g,
                      u64* const* out) {
     if (n <= 0) return;
+    if (n > kChunkKs) {
+        for (int c0 = 0; c0 < n; c0 += kChunkKs) {
+            const int cn = std::min(kChunkKs, n - c0);
+            rotate(cn, modup + c0, ct + c0, g + c0, out + c0);
+        }
+        return;
+    }
     const u32 N = hp_.N, R = hp_.R;
     std::vector<const u64*> keys(n);
     for (int i = 0; i < n; ++i) keys[i] = ks_key(g[i]);
@@ -862,6 +916,13 @@ void Context::rotate(int n, const u64* const* modup, const u64* const* ct, const
 
 void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* out) {
     if (n <= 0) return;
+    if (n > kChunkMult) {
+        for (int c0 = 0; c0 < n; c0 += kChunkMult) {
+            const int cn = std::min(kChunkMult, n - c0);
+            mult(cn, a + c0, b + c0, out + c0);
+        }
+        return;
+    }
     const u32 N = hp_.N, L = hp_.L, K = hp_.K, R = hp_.R, nB = hp_.nB, dnum = hp_.dnum;
     const size_t LN = (size_t)L * N;
     // 1. gather (a.c0, a.c1, b.c0, b.c1) and INTT

@@ -475,6 +475,219 @@ static int matmul_batch_impl(hgm_ctx* c, int algo, int order, size_t m, size_t l
     });
 }
 
+}  // extern "C"
+
+struct hgm_batch {
+    hgm_ctx* owner = nullptr;
+    std::shared_ptr<const MatmulProgram> prog;
+    size_t count = 0;
+    u64* in = nullptr;   // [count][n_enc][W]
+    u64* out = nullptr;  // [count][W]
+};
+
+namespace {
+
+size_t lockstep_chunk(Context& ctx, const MatmulProgram& prog) {
+    const size_t W = ctx.ct_words();
+    const size_t per_inst = (prog.cloud_sched.rot_count + prog.cloud_sched.comb_count / 2 + 8) * W * 8;
+    size_t free_b = 0, total_b = 0;
+    HGM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    size_t chunk = std::max<size_t>(1, (size_t)(0.45 * (double)free_b) / per_inst);
+    return std::min<size_t>(chunk, 1024);
+}
+
+}  // namespace
+
+extern "C" {
+
+int hgm_batch_encrypt(hgm_ctx* c, int algo, int order, size_t m, size_t l, size_t n, size_t count,
+                      const int64_t* A, const int64_t* B, uint64_t counter0, hgm_batch** out) {
+    return guarded([&] {
+        if (order < -1 || order > 1) throw std::invalid_argument("order must be -1, 0 or 1");
+        Context& ctx = *c->ctx;
+        auto b = std::make_unique<hgm_batch>();
+        b->owner = c;
+        b->prog = get_matmul_program(algo, order, m, l, n, ctx.slots(), ctx.host().N);
+        b->count = count;
+        const size_t W = ctx.ct_words(), E = b->prog->n_enc;
+        b->in = ctx.alloc(std::max<size_t>(1, count * E) * W);
+        b->out = ctx.alloc(std::max<size_t>(1, count) * W);
+        const size_t chunk = 1024;
+        for (size_t c0 = 0; c0 < count; c0 += chunk) {
+            const size_t K = std::min(chunk, count - c0);
+            std::vector<std::vector<std::vector<i64>>> packed(K);
+            std::vector<const i64*> vals;
+            std::vector<size_t> S;
+            std::vector<u64> ctr;
+            std::vector<u64*> dst;
+            for (size_t k = 0; k < K; ++k) {
+                packed[k] = b->prog->pack(A + (c0 + k) * m * l, B + (c0 + k) * l * n);
+                for (size_t s = 0; s < E; ++s) {
+                    vals.push_back(packed[k][s].data());
+                    S.push_back(b->prog->segment);
+                    ctr.push_back(counter0 + (c0 + k) * E + s);
+                    dst.push_back(b->in + ((c0 + k) * E + s) * W);
+                }
+            }
+            ctx.encrypt((int)vals.size(), vals.data(), S.data(), ctr.data(), dst.data());
+            ctx.sync();  // `packed` is host staging for this chunk
+        }
+        *out = b.release();
+    });
+}
+
+int hgm_batch_cloud(hgm_ctx* c, hgm_batch* b, float* device_ms) {
+    return guarded([&] {
+        Context& ctx = *c->ctx;
+        const MatmulProgram& prog = *b->prog;
+        const size_t W = ctx.ct_words(), E = prog.n_enc;
+        const size_t chunk = lockstep_chunk(ctx, prog);
+        cudaEvent_t e0, e1;
+        HGM_CUDA(cudaEventCreate(&e0));
+        HGM_CUDA(cudaEventCreate(&e1));
+        HGM_CUDA(cudaEventRecord(e0, ctx.stream()));
+        for (size_t c0 = 0; c0 < b->count; c0 += chunk) {
+            const int K = (int)std::min(chunk, b->count - c0);
+            ExecIO io;
+            io.K = K;
+            io.input = [&](int s, int k) -> const u64* { return b->in + ((c0 + k) * E + s) * W; };
+            io.enc_values = [](int, int) -> const i64* { throw std::logic_error("cloud program encrypts"); };
+            io.enc_counter = [](int, int) -> u64 { return 0; };
+            std::vector<u64*> res = execute(ctx, prog.cloud_sched, io);
+            HGM_CUDA(cudaMemcpyAsync(b->out + c0 * W, res[0], (size_t)K * W * 8, cudaMemcpyDeviceToDevice,
+                                     ctx.stream()));
+            for (u64* r : res) ctx.release(r);
+        }
+        HGM_CUDA(cudaEventRecord(e1, ctx.stream()));
+        HGM_CUDA(cudaEventSynchronize(e1));
+        float ms = 0;
+        HGM_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        if (device_ms) *device_ms = ms;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    });
+}
+
+uint64_t* hgm_batch_output(hgm_batch* b, size_t i) {
+    if (!b || i >= b->count) return nullptr;
+    return b->out + i * b->owner->ctx->ct_words();
+}
+
+int hgm_batch_decrypt_words(hgm_ctx* c, const uint64_t* dev_words, size_t count, size_t S, int64_t* out) {
+    return guarded([&] {
+        Context& ctx = *c->ctx;
+        if (S == 0 || S > ctx.slots()) throw hgm::DimensionError("bad segment");
+        const size_t W = ctx.ct_words();
+        const size_t chunk = 1024;
+        for (size_t c0 = 0; c0 < count; c0 += chunk) {
+            const size_t K = std::min(chunk, count - c0);
+            std::vector<const u64*> cts(K);
+            std::vector<size_t> Sv(K, S);
+            std::vector<i64*> outp(K);
+            for (size_t k = 0; k < K; ++k) {
+                cts[k] = dev_words + (c0 + k) * W;
+                outp[k] = out + (c0 + k) * S;
+            }
+            ctx.decrypt((int)K, cts.data(), Sv.data(), outp.data());
+        }
+    });
+}
+
+int hgm_batch_decrypt(hgm_ctx* c, hgm_batch* b, int64_t* C) {
+    return guarded([&] {
+        const MatmulProgram& prog = *b->prog;
+        std::vector<i64> slots(b->count * prog.segment);
+        const int rc = hgm_batch_decrypt_words(c, b->out, b->count, prog.segment, slots.data());
+        if (rc != HGM_OK) throw std::runtime_error(g_err);
+        std::vector<i64> v(prog.segment);
+        for (size_t k = 0; k < b->count; ++k) {
+            std::copy(slots.begin() + k * prog.segment, slots.begin() + (k + 1) * prog.segment, v.begin());
+            prog.unpack(v, C + k * prog.m * prog.n);
+        }
+    });
+}
+
+void hgm_batch_free(hgm_batch* b) {
+    if (!b) return;
+    b->owner->ctx->release(b->in);
+    b->owner->ctx->release(b->out);
+    b->owner->ctx->sync();
+    delete b;
+}
+
+int hgm_program_info(int algo, int order, size_t m, size_t l, size_t n, size_t slots, uint32_t N,
+                     uint64_t* stats, uint64_t* facts) {
+    return guarded([&] {
+        auto p = get_matmul_program(algo, order, m, l, n, slots, N);
+        if (stats)
+            for (int k = 0; k < 6; ++k) {
+                stats[2 * k] = p->counts.c[k][0];
+                stats[2 * k + 1] = p->counts.c[k][1];
+            }
+        if (facts) {
+            facts[0] = p->segment;
+            facts[1] = p->n_enc;
+            facts[2] = p->cloud_sched.rot_count;
+            facts[3] = p->cloud_sched.comb_count;
+            facts[4] = p->cloud_sched.mult_count;
+            facts[5] = p->cloud_sched.levels.size();
+            facts[6] = (u64)p->order;
+        }
+    });
+}
+
+long hgm_program_stream(int algo, int order, size_t m, size_t l, size_t n, size_t slots, uint32_t N,
+                        int64_t* hdr, size_t hdr_cap, int64_t* data, size_t data_cap, size_t* data_len) {
+    long result = 0;
+    const int rc = guarded([&] {
+        auto p = get_matmul_program(algo, order, m, l, n, slots, N);
+        size_t dl = 0;
+        for (const auto& mk : p->stream_masks) dl += mk->v.size();
+        if (data_len) *data_len = dl;
+        result = (long)p->stream.size();
+        if (!hdr) return;
+        if (hdr_cap < p->stream.size() * 3 || data_cap < dl) throw std::invalid_argument("buffers too small");
+        size_t off = 0, mi = 0;
+        for (size_t i = 0; i < p->stream.size(); ++i) {
+            hdr[3 * i] = p->stream[i].first;
+            hdr[3 * i + 1] = p->stream[i].second;
+            hdr[3 * i + 2] = 0;
+            if (p->stream[i].first == 4) {
+                const auto& v = p->stream_masks[mi++]->v;
+                hdr[3 * i + 2] = (int64_t)v.size();
+                std::copy(v.begin(), v.end(), data + off);
+                off += v.size();
+            }
+        }
+    });
+    return rc == HGM_OK ? result : -rc;
+}
+
+long hgm_plan_info(int kind, size_t k, size_t a, size_t b, size_t c, int order, size_t segment,
+                   int64_t* offsets, uint64_t* weights, size_t cap) {
+    long result = 0;
+    const int rc = guarded([&] {
+        if (order != 0 && order != 1) throw std::invalid_argument("order must be 0 or 1");
+        const Order o = (Order)order;
+        std::shared_ptr<const Plan> p;
+        switch (kind) {
+            case 0: p = eps_plan_embedded(k, a, b, c, o, segment); break;
+            case 1: p = omega_plan_embedded(k, a, b, c, o, segment); break;
+            case 4: p = shaped_eps_plan(k, a, b, c, o, segment); break;
+            case 5: p = shaped_omega_plan(k, a, b, c, o, segment); break;
+            default: throw std::invalid_argument("unknown plan kind");
+        }
+        result = (long)p->entries.size();
+        for (size_t i = 0; i < p->entries.size() && i < cap; ++i) {
+            offsets[i] = p->entries[i].offset;
+            u64 w = 0;
+            for (i64 v : p->entries[i].mask->v) w += v != 0;
+            weights[i] = w;
+        }
+    });
+    return rc == HGM_OK ? result : -rc;
+}
+
 int hgm_matmul_batch(hgm_ctx* c, int algo, int order, size_t m, size_t l, size_t n, size_t count,
                      const int64_t* A, const int64_t* B, int64_t* C, uint64_t counter0, uint64_t* stats) {
     return matmul_batch_impl(c, algo, order, m, l, n, count, A, B, C, counter0, stats, nullptr);

@@ -387,6 +387,16 @@ void MatmulProgram::unpack(const std::vector<i64>& v, i64* C) const {
 
 namespace {
 
+// the cloud phase alone: encryptions become pre-materialised inputs (same slots)
+Program cloud_only(const Program& p) {
+    Program q = p;
+    for (PNode& nd : q.nodes)
+        if (nd.kind == PNode::Enc) nd.kind = PNode::Input;
+    q.n_inputs = q.n_enc;
+    q.n_enc = 0;
+    return q;
+}
+
 // reference basic_mm (algorithms.cpp:198-248)
 std::shared_ptr<MatmulProgram> build_basic(int order_opt, size_t m, size_t l, size_t n, size_t slots, u32 N) {
     check_capacity(m * l, slots, "flattened left operand");
@@ -425,6 +435,7 @@ std::shared_ptr<MatmulProgram> build_basic(int order_opt, size_t m, size_t l, si
     mp->stream = std::move(R.stream);
     mp->stream_masks = std::move(R.smasks);
     mp->sched = optimise(R.prog);
+    mp->cloud_sched = optimise(cloud_only(R.prog));
     return mp;
 }
 
@@ -484,6 +495,7 @@ std::shared_ptr<MatmulProgram> build_enhanced(int order_opt, size_t m, size_t l,
     mp->stream = std::move(R.stream);
     mp->stream_masks = std::move(R.smasks);
     mp->sched = optimise(R.prog);
+    mp->cloud_sched = optimise(cloud_only(R.prog));
     return mp;
 }
 

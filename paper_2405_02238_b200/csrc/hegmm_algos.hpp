@@ -73,7 +73,8 @@ struct MatmulProgram {
     size_t m = 0, l = 0, n = 0, segment = 0, slots = 0;
     Order order = Order::Col;
     Strategy strat;
-    Schedule sched;
+    Schedule sched;        // client encrypt + cloud (encryptions are level 0)
+    Schedule cloud_sched;  // cloud only: the encrypted inputs are Input slots
     int n_enc = 0;
     Counts counts;  // per instance, by phase
     // op stream in call order: (kind, arg) with kind 0 enc 1 dec 2 add 3 mult 4 cmult 5 rot

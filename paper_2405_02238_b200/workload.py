@@ -38,9 +38,18 @@ def splitmix_matrices(seed: int, index: int, m: int, l: int, n: int, lo: int, hi
 
 
 def batch(seed: int, first: int, count: int, m: int, l: int, n: int, lo: int, hi: int):
-    """Instances first..first+count-1 stacked as (count, m, l), (count, l, n)."""
-    A = np.empty((count, m, l), dtype=np.int64)
-    B = np.empty((count, l, n), dtype=np.int64)
-    for i in range(count):
-        A[i], B[i] = splitmix_matrices(seed, first + i, m, l, n, lo, hi)
+    """Instances first..first+count-1 stacked as (count, m, l), (count, l, n);
+    the same draws as splitmix_matrices, vectorised (uint64 arithmetic wraps)."""
+    total = m * l + l * n
+    g = np.uint64(GOLDEN)
+    with np.errstate(over="ignore"):
+        base = (np.uint64(seed % (1 << 64)) * g + np.arange(first, first + count, dtype=np.uint64)
+                + np.uint64(1))
+        z = base[:, None] + g * np.arange(1, total + 1, dtype=np.uint64)[None, :]
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z ^= z >> np.uint64(31)
+    vals = (np.int64(lo) + (z % np.uint64(hi - lo + 1)).astype(np.int64))
+    A = np.ascontiguousarray(vals[:, : m * l].reshape(count, m, l))
+    B = np.ascontiguousarray(vals[:, m * l:].reshape(count, l, n))
     return A, B

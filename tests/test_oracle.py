@@ -1,0 +1,112 @@
+"""CPU: pins the BFV oracle (oracle/bfv_oracle.cpp) before it is trusted.
+
+* its NTT against the definition  out[k] = sum_j a_j psi^(j (2 brv(k) + 1));
+* its primitives against plain modular arithmetic on the slots, including
+  the reference's left-rotation semantics (backend.cpp:185-197, row-wide);
+* the reference's own algorithms running on it against the reference's
+  golden vectors (test_cli.cpp KATs, seeded config outputs) and against the
+  reference SlotBackend{N/2, 65537} on random shapes."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2405_02238_b200.workload import CONFIGS, splitmix_matrices
+
+T = 65537
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_golden.json")))
+
+
+def brv(x, bits):
+    return int(f"{x:0{bits}b}"[::-1], 2)
+
+
+def test_ntt_matches_definition(oracle_factory):
+    o = oracle_factory(2)
+    N, logN = o.N, o.N.bit_length() - 1
+    rng = np.random.default_rng(1)
+    for prime in (0, len(o.primes) - 1, -1):
+        q = T if prime < 0 else o.primes[prime]
+        a = [int(x) % q for x in rng.integers(0, 2**62, N)]
+        out = o.ntt(np.array(a, dtype=np.uint64), prime)
+        # psi: the primitive 2N-th root the oracle uses is out[0] of X = (0, 1, 0, ...)
+        x = np.zeros(N, dtype=np.uint64)
+        x[1] = 1
+        psi = int(o.ntt(x, prime)[0])
+        assert pow(psi, N, q) == q - 1
+        for k in rng.integers(0, N, 6):
+            e = 2 * brv(int(k), logN) + 1
+            want = sum(aj * pow(psi, j * e, q) for j, aj in enumerate(a)) % q
+            assert int(out[k]) == want
+        assert np.array_equal(o.ntt(out, prime, forward=False), np.array(a, dtype=np.uint64))
+
+
+def test_primitives_decrypt_correctly(oracle_factory):
+    o = oracle_factory(2)
+    H = o.N // 2
+    rng = np.random.default_rng(2)
+    S = 200
+    a = rng.integers(-8, 8, S)
+    b = rng.integers(-8, 8, S)
+    ca, cb = o.encrypt(a, 0), o.encrypt(b, 1)
+    assert np.array_equal(o.decrypt(ca, S), a % T)
+    assert np.array_equal(o.decrypt(o.add(ca, cb), S), (a + b) % T)
+    m = rng.integers(0, 2, S)
+    assert np.array_equal(o.decrypt(o.cmult(ca, m), S), (a * m) % T)
+    assert np.array_equal(o.decrypt(o.mult(ca, cb), S), (a * b) % T)
+    full = np.zeros(H, dtype=np.int64)
+    full[:S] = a
+    for z in (1, -1, 17, H - 1, 0, H + 3):
+        assert np.array_equal(o.decrypt(o.rot(ca, z), S), np.roll(full, -z)[:S] % T)
+    # the rotation composes additively over the row (test_backend.cpp:102-115, row-wide)
+    assert np.array_equal(o.decrypt(o.rot(o.rot(ca, 5), 7), S), o.decrypt(o.rot(ca, 12), S))
+
+
+def test_noise_budget_after_mult(oracle_factory):
+    o = oracle_factory(0)
+    rng = np.random.default_rng(3)
+    a, b = rng.integers(-8, 8, 64), rng.integers(-8, 8, 64)
+    p = o.mult(o.encrypt(a, 0), o.encrypt(b, 1))
+    assert o.noise_budget(p) > 20  # fixed-point measure saturates near 61 bits
+
+
+def test_error_conventions(oracle_factory):
+    from oracle.bindings import OracleError
+
+    o = oracle_factory(2)
+    with pytest.raises(OracleError, match="DimensionError"):
+        o.encrypt(np.zeros(0, np.int64), 0)
+    with pytest.raises(OracleError, match="CapacityError"):
+        o.encrypt(np.zeros(o.N // 2 + 1, np.int64), 0)
+
+
+def test_reference_kats_through_oracle(ref):
+    for kat in GOLD["kats"]:
+        A, B = np.array(kat["A"]), np.array(kat["B"])
+        C, st, _, _ = ref.mm_oracle(A, B, param_id=2, algo=kat["algo"])
+        assert C.tolist() == kat["C"], kat["source"]
+        assert st[:12].astype(int).tolist() == kat["stats"]
+
+
+def test_cfg1_through_oracle_matches_golden(ref):
+    g = GOLD["configs"]["cfg1"]
+    A, B = splitmix_matrices(GOLD["seed"], 0, g["m"], g["l"], g["n"], g["lo"], g["hi"])
+    for algo in ("enhanced", "basic"):
+        C, st, _, _ = ref.mm_oracle(A, B, param_id=0, algo=algo)
+        rec = g["algos"][algo]
+        assert hashlib.sha256(C.astype(np.int64).tobytes()).hexdigest() == rec["C_sha256"]
+        assert st[:12].astype(int).tolist() == rec["stats"]
+
+
+def test_random_shapes_oracle_vs_slotbackend(ref):
+    rng = np.random.default_rng(4)
+    for _ in range(6):
+        m, l, n = (int(x) for x in rng.integers(1, 9, 3))
+        A = rng.integers(-9, 10, (m, l))
+        B = rng.integers(-9, 10, (l, n))
+        for algo in ("basic", "enhanced"):
+            C, _, _, _ = ref.mm_oracle(A, B, param_id=2, algo=algo)
+            Cref, _ = ref.mm(A, B, algo, slots=2048)
+            assert np.array_equal(C, Cref), (m, l, n, algo)
