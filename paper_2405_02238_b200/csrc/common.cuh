@@ -107,6 +107,19 @@ HD u64 shoup_mul(u64 a, u64 w, u64 ws, u64 q) {
     u64 r = a * w - h * q;
     return r >= q ? r - q : r;
 }
+// Harvey's lazy Shoup product: a * w mod q in [0, 2q), any a < 2^64
+HD u64 shoup_lazy(u64 a, u64 w, u64 ws, u64 q) { return a * w - mulhi64(a, ws) * q; }
+// Shoup product with a 3-multiply quotient: the a_lo*ws_lo partial product is
+// dropped, so the quotient is low by at most 1 and the result lies in [0, 3q).
+// (The NTT is bound by the wide-multiply pipe; this saves 1 of ~6 per butterfly.)
+HD u64 shoup_lazy3(u64 a, u64 w, u64 ws, u64 q) {
+    const u64 a_lo = (u32)a, a_hi = a >> 32, b_lo = (u32)ws, b_hi = ws >> 32;
+    const u64 m1 = a_hi * b_lo, m2 = a_lo * b_hi;
+    const u64 qh = a_hi * b_hi + (m1 >> 32) + (m2 >> 32) + (((m1 & 0xffffffffULL) + (m2 & 0xffffffffULL)) >> 32);
+    return a * w - qh * q;
+}
+// x in [0, 2m) -> [0, m)   (m = q or 2q)
+HD u64 reduce_once(u64 x, u64 m) { return x >= m ? x - m : x; }
 // a * b mod q for a, b < q < 2^62 (shifted Barrett, at most two corrections)
 HD u64 mul_mod(u64 a, u64 b, const Prime& p) {
     const u64 lo = a * b, hi = mulhi64(a, b);

@@ -26,9 +26,14 @@ struct NttJobs {
     u64* const* ptrs = nullptr;
     u32 count = 0;
     u32 period = 1;
-    unsigned char prime[32] = {0};
-    // optional fused scaling after an inverse transform: multiply by a
-    // per-prime Shoup constant (used to fold extra factors); null = none
+    unsigned char prime[32] = {0};  // host-side pattern
+    u64 packed[4] = {0, 0, 0, 0};   // the same pattern, packed for the kernel
+    void pack() {
+        for (int w = 0; w < 4; ++w) {
+            packed[w] = 0;
+            for (int b = 0; b < 8; ++b) packed[w] |= (u64)prime[8 * w + b] << (8 * b);
+        }
+    }
 };
 
 void ntt_forward(const DevParams* dp, const DevParams& hp, const NttJobs& jobs, cudaStream_t s);
