@@ -94,6 +94,12 @@ size_t hgm_ct_depth(const hgm_ct* ct);
 int hgm_ct_phase(const hgm_ct* ct);
 hgm_ct* hgm_ct_retain(hgm_ct* ct);
 void hgm_ct_release(hgm_ct* ct);
+/* A pinned handle (the default) keeps its ciphertext materialised after a
+ * flush.  An unpinned handle only keeps the recipe: the value is recomputed
+ * (bit-identically) if it is needed again, and it never blocks the fusion of
+ * its node into a consumer.  Adapters that cannot observe when the caller
+ * drops a handle (integration/bfv_gpu_backend.cpp) unpin everything. */
+int hgm_ct_set_pinned(hgm_ct* ct, int pinned);
 
 /* stats[2*k + {0: client, 1: cloud}] for k = add, mult_cc, mult_cp, rot,
  * encrypt, decrypt (OpStats field order, backend.hpp:50-57). */

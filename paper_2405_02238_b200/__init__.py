@@ -24,7 +24,7 @@ EXPORTS = (
     "hgm_ctx_create", "hgm_ctx_destroy", "hgm_last_error", "hgm_ctx_info", "hgm_slot_count",
     "hgm_ct_words", "hgm_encrypt", "hgm_encrypt_at", "hgm_decrypt", "hgm_add", "hgm_mul",
     "hgm_cmul", "hgm_rot", "hgm_apply_plan", "hgm_flush", "hgm_ct_export", "hgm_ct_import",
-    "hgm_ct_segment", "hgm_ct_depth", "hgm_ct_phase", "hgm_ct_retain", "hgm_ct_release",
+    "hgm_ct_segment", "hgm_ct_depth", "hgm_ct_phase", "hgm_ct_retain", "hgm_ct_release", "hgm_ct_set_pinned",
     "hgm_stats", "hgm_reset_stats", "hgm_peak_live", "hgm_set_phase", "hgm_phase",
     "hgm_matmul_batch", "hgm_matmul_batch_export", "hgm_bench_ntt", "hgm_device_sync",
     "hgm_test_ntt", "hgm_launch_count", "hgm_batch_encrypt", "hgm_batch_cloud", "hgm_batch_output",
@@ -165,6 +165,7 @@ def lib() -> ctypes.CDLL:
         "hgm_ct_phase": (_int, [_vp]),
         "hgm_ct_retain": (_vp, [_vp]),
         "hgm_ct_release": (None, [_vp]),
+        "hgm_ct_set_pinned": (_int, [_vp, _int]),
         "hgm_stats": (_int, [_vp, _vp]),
         "hgm_reset_stats": (_int, [_vp]),
         "hgm_peak_live": (_sz, [_vp]),

@@ -394,6 +394,19 @@ hgm_ct* hgm_ct_retain(hgm_ct* ct) {
     ct->refs++;
     return ct;
 }
+int hgm_ct_set_pinned(hgm_ct* ct, int pinned) {
+    if (!ct) return fail(HGM_EARG, "null handle");
+    const bool p = pinned != 0;
+    if (p != ct->pinned) {
+        if (p)
+            ct->node->pins++;
+        else
+            ct->node->pins--;
+        ct->pinned = p;
+    }
+    return HGM_OK;
+}
+
 void hgm_ct_release(hgm_ct* ct) {
     if (!ct) return;
     if (--ct->refs == 0) {

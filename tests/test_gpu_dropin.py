@@ -1,0 +1,80 @@
+"""GPU: the reference's OWN algorithms (basic_mm / enhanced_mm / square_pad_mm,
+compiled from /root/reference sources) drive the B200 through
+hegmm::BfvGpuBackend (integration/), built against the unmodified reference
+header.  Results, per-phase op counts and final ciphertext words must equal
+the library's batched path and the CPU oracle."""
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+from paper_2405_02238_b200.workload import CONFIGS, splitmix_matrices
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SO = os.path.join(ROOT, "integration", "_build", "libhegmm_dropin.so")
+T = 65537
+
+
+@pytest.fixture(scope="module")
+def dropin():
+    if not os.path.exists(SO):
+        pytest.skip("integration/_build/libhegmm_dropin.so not built (needs the reference headers)")
+    L = ctypes.CDLL(SO)
+    vp, sz = ctypes.c_void_p, ctypes.c_size_t
+    L.dropin_mm.restype = ctypes.c_int
+    L.dropin_mm.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, vp, sz, sz, vp, sz, vp, vp, vp]
+    L.dropin_last_error.restype = ctypes.c_char_p
+
+    def run(A, B, param_id=0, algo=0, order=-1, words=None):
+        A = np.ascontiguousarray(A, dtype=np.int64)
+        B = np.ascontiguousarray(B, dtype=np.int64)
+        m, l = A.shape
+        n = B.shape[1]
+        C = np.zeros((m, n), dtype=np.int64)
+        st = np.zeros(13, dtype=np.uint64)
+        w = np.zeros(words, dtype=np.uint64) if words else None
+        rc = L.dropin_mm(param_id, 1, algo, order, A.ctypes.data, m, l, B.ctypes.data, n, C.ctypes.data,
+                         st.ctypes.data, w.ctypes.data if w is not None else None)
+        if rc != 0:
+            raise RuntimeError(f"rc={rc}: {L.dropin_last_error().decode()}")
+        return C, st, w
+
+    return run
+
+
+@pytest.mark.parametrize("algo,aid", [("enhanced", 1), ("basic", 0)])
+def test_reference_algorithms_on_gpu_cfg1(algo, aid, dropin, ref, gpu_factory):
+    m, l, n, lo, hi, pid, _, _ = CONFIGS["cfg1"]
+    A, B = splitmix_matrices(20240101, 0, m, l, n, lo, hi)
+    g = gpu_factory(pid)
+    C, st, words = dropin(A, B, pid, aid, words=g.ct_words)
+    Cref, st_ref = ref.mm(A, B, algo, slots=g.slot_count)
+    assert np.array_equal(C, Cref)
+    assert st[:12].astype(int).tolist() == st_ref[:12].astype(int).tolist()
+    # the same op stream through the library's batched program: identical words
+    Cb, wb = g.matmul_batch(A, B, algo=aid, counter0=0, export=True)
+    assert np.array_equal(words, wb[0])
+    _, _, ct_o, _ = ref.mm_oracle(A, B, param_id=pid, seed=1, counter0=0, algo=algo, words=g.ct_words)
+    assert np.array_equal(words, ct_o)
+
+
+def test_reference_algorithms_random_shapes(dropin, ref):
+    rng = np.random.default_rng(8)
+    for _ in range(6):
+        m, l, n = (int(x) for x in rng.integers(1, 11, 3))
+        A = rng.integers(-9, 10, (m, l))
+        B = rng.integers(-9, 10, (l, n))
+        for aid, algo in [(0, "basic"), (1, "enhanced"), (2, "square_pad")]:
+            C, st, _ = dropin(A, B, 2, aid)
+            Cref, st_ref = ref.mm(A, B, algo, slots=2048)
+            assert np.array_equal(C, Cref), (m, l, n, algo)
+            assert st[:12].astype(int).tolist() == st_ref[:12].astype(int).tolist()
+
+
+def test_capacity_error_propagates(dropin):
+    A = np.ones((36, 64), dtype=np.int64)
+    B = np.ones((64, 64), dtype=np.int64)
+    with pytest.raises(RuntimeError, match="rc=2"):
+        dropin(A, B, 0, 1)
