@@ -109,10 +109,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def shard(rank, world, total):
-    lo = rank * total // world
-    hi = (rank + 1) * total // world
-    return lo, hi - lo
+from paper_2405_02238_b200.dist import counter_base, gather_ciphertexts, shard  # noqa: E402
 
 
 def cpu_baseline(seconds_budget: float = 20.0):
@@ -258,7 +255,7 @@ def main():
         return float(t.item())
 
     # ---------------------------------------------------------------- value: cloud phase
-    bt = hb.Batch(ctx, A, B, algo=algo, counter0=first * E)  # client phase (not timed)
+    bt = hb.Batch(ctx, A, B, algo=algo, counter0=counter_base(first, E))  # client phase (not timed)
     for _ in range(args.warmup):
         bt.cloud()
     barrier()
@@ -291,15 +288,23 @@ def main():
                                                  "version": 3}
 
         mine = torch.as_tensor(_View(bt.output_ptr(0), count * W), device="cuda")
-        maxc = max(shard(r, world, args.instances)[1] for r in range(world))
-        send = torch.zeros(maxc * W, dtype=torch.int64, device="cuda")
-        send[: count * W] = mine
+        ctx.sync()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        outs = [torch.empty_like(send) for _ in range(world)] if rank == 0 else None
-        dist.gather(send, outs, dst=0)
+        got = gather_ciphertexts(dist, mine, count, W, args.instances, world, rank, device="cuda")
         torch.cuda.synchronize()
         gather_ms = 1e3 * (time.perf_counter() - t0)
+        if rank == 0:  # rank 0 (the client side) decrypts a sample of every shard
+            for r, part in enumerate(got):
+                f, c = shard(r, world, args.instances)
+                if c:  # check the shard's first product from its gathered ciphertext
+                    slots = ctx.decrypt_words(part[: W], facts["segment"])[0]
+                    Ar, Br = batch(SEED, f, 1, M, L_, N_, LO, HI)
+                    col = facts["order"] == 0
+                    C0 = np.array([[slots[(i + j * M) if col else (i * N_ + j)] for j in range(N_)]
+                                   for i in range(M)])
+                    if not np.array_equal(C0, (Ar[0] @ Br[0]) % 65537):
+                        raise RuntimeError(f"gathered ciphertext of rank {r} decrypts wrongly")
     bt.free()
 
     # ---------------------------------------------------------------- e2e through the C ABI

@@ -366,6 +366,17 @@ class Context:
                                       counter0, _ptr(stats)))
         return C, stats
 
+    def decrypt_words(self, words, segment: int) -> np.ndarray:
+        """Decrypts ciphertexts held in a device buffer (a torch CUDA tensor, e.g.
+        one gathered over NCCL, or a raw device pointer for one ciphertext)."""
+        if hasattr(words, "data_ptr"):
+            ptr, n = words.data_ptr(), words.numel() // self.ct_words
+        else:
+            ptr, n = int(words), 1
+        out = np.zeros((n, segment), dtype=np.int64)
+        _check(lib().hgm_batch_decrypt_words(self._h, ptr, n, segment, _ptr(out)))
+        return out
+
     def test_ntt(self, data: np.ndarray, prime: int, forward: bool = True) -> np.ndarray:
         d = np.ascontiguousarray(data, dtype=np.uint64).copy()
         _check(lib().hgm_test_ntt(self._h, 1 if forward else 0, prime, _ptr(d), d.size // self.N))
