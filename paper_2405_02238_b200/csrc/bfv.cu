@@ -18,6 +18,8 @@ void cuda_check(cudaError_t e, const char* what) {
 
 namespace {
 
+__constant__ DevParams c_dp[kParamSets];
+
 constexpr int kThreads = 256;
 // items per launch sequence: bounds temporaries and staging uploads
 constexpr int kChunkEnc = 256, kChunkDec = 1024, kChunkLin = 8192, kChunkKs = 1024, kChunkMult = 128;
@@ -39,8 +41,9 @@ __device__ __forceinline__ u64 centred_lift(u64 y, u64 src, u64 dst) {
 
 // ---------------------------------------------------------------- encoding
 // oracle encode(): slot values mod t scattered to their NTT positions
-__global__ void k_encode_scatter(const DevParams* __restrict__ dp, u32 n, const i64* vals,
+__global__ void k_encode_scatter(DevCtx cx, u32 n, const i64* vals,
                                  const u32* S, u64* out) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, H = N / 2;
     ITEM_LOOP {
         COEF_LOOP {
@@ -49,23 +52,24 @@ __global__ void k_encode_scatter(const DevParams* __restrict__ dp, u32 n, const 
                 const i64 x = vals[(size_t)item * H + j];
                 v = x >= 0 ? (u64)x % kT : kT - 1 - ((u64)(-(x + 1)) % kT);
             }
-            out[(size_t)item * N + dp->slot_ntt[j]] = v;
+            out[(size_t)item * N + cx.slot_ntt[j]] = v;
         }
     }
 }
 
 // oracle encrypt(): sample u, e0, e1; c0 = e0 + Delta m, c1 = e1 (coefficient form)
-__global__ void k_enc_lift(const DevParams* __restrict__ dp, u32 n, const u64* m, const u64* ctr,
+__global__ void k_enc_lift(DevCtx cx, u32 n, const u64* m, const u64* ctr,
                            u64* U, u64* const* out) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = dp->L;
-    const u64 seed = dp->seed;
+    const u64 seed = cx.seed;
     ITEM_LOOP {
         const u64 c = ctr[item];
         u64* o = out[item];
         COEF_LOOP {
             const i64 u = ternary(seed, kStreamEncU | c, j);
-            const i64 e0 = gauss(seed, kStreamEncE0 | c, j, dp->cdt);
-            const i64 e1 = gauss(seed, kStreamEncE1 | c, j, dp->cdt);
+            const i64 e0 = gauss(seed, kStreamEncE0 | c, j, cx.cdt);
+            const i64 e1 = gauss(seed, kStreamEncE1 | c, j, cx.cdt);
             const u64 mj = m[(size_t)item * N + j];
             for (u32 i = 0; i < L; ++i) {
                 const u64 q = dp->pr[i].q;
@@ -78,8 +82,9 @@ __global__ void k_enc_lift(const DevParams* __restrict__ dp, u32 n, const u64* m
     }
 }
 
-__global__ void k_enc_finish(const DevParams* __restrict__ dp, u32 n, const u64* U, const u64* pk,
+__global__ void k_enc_finish(DevCtx cx, u32 n, const u64* U, const u64* pk,
                              u64* const* out) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = dp->L;
     ITEM_LOOP {
         u64* o = out[item];
@@ -96,8 +101,9 @@ __global__ void k_enc_finish(const DevParams* __restrict__ dp, u32 n, const u64*
 }
 
 // ---------------------------------------------------------------- decryption
-__global__ void k_dec_phase(const DevParams* __restrict__ dp, u32 n, const u64* const* in,
+__global__ void k_dec_phase(DevCtx cx, u32 n, const u64* const* in,
                             const u64* sk, u64* X) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = dp->L;
     ITEM_LOOP {
         const u64* c = in[item];
@@ -112,7 +118,8 @@ __global__ void k_dec_phase(const DevParams* __restrict__ dp, u32 n, const u64* 
 }
 
 // oracle decrypt(): m = round(t x / Q) mod t via sum_i [x_i (Q/q_i)^-1]_{q_i} t/q_i
-__global__ void k_dec_round(const DevParams* __restrict__ dp, u32 n, const u64* X, u64* M) {
+__global__ void k_dec_round(DevCtx cx, u32 n, const u64* X, u64* M) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = dp->L;
     ITEM_LOOP {
         COEF_LOOP {
@@ -127,18 +134,20 @@ __global__ void k_dec_round(const DevParams* __restrict__ dp, u32 n, const u64* 
     }
 }
 
-__global__ void k_dec_gather(const DevParams* __restrict__ dp, u32 n, const u64* M, const u32* S,
+__global__ void k_dec_gather(DevCtx cx, u32 n, const u64* M, const u32* S,
                              i64* out) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, H = N / 2;
     ITEM_LOOP {
         for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < S[item]; i += gridDim.x * blockDim.x)
-            out[(size_t)item * H + i] = (i64)M[(size_t)item * N + dp->slot_ntt[i]];
+            out[(size_t)item * H + i] = (i64)M[(size_t)item * N + cx.slot_ntt[i]];
     }
 }
 
 // ---------------------------------------------------------------- linear ops
-__global__ void k_add(const DevParams* __restrict__ dp, u32 n, const u64* const* a,
+__global__ void k_add(DevCtx cx, u32 n, const u64* const* a,
                       const u64* const* b, u64* const* out) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = dp->L;
     const size_t W = (size_t)2 * L * N;
     ITEM_LOOP {
@@ -161,8 +170,9 @@ __global__ void k_copy(u32 n, size_t W, const u64* const* in, u64* const* out) {
 }
 
 // out[o] = sum_t in[t] (.* mask[t]) : oracle cmult() followed by add()
-__global__ void k_lincomb(const DevParams* __restrict__ dp, u32 n, const u32* off,
+__global__ void k_lincomb(DevCtx cx, u32 n, const u32* off,
                           const u64* const* in, const u64* const* mask, u64* const* out) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = dp->L;
     const size_t LN = (size_t)L * N, W = 2 * LN;
     ITEM_LOOP {
@@ -183,7 +193,8 @@ __global__ void k_lincomb(const DevParams* __restrict__ dp, u32 n, const u32* of
 }
 
 // centred lift of the mod-t mask polynomial to each q_i (oracle cmult())
-__global__ void k_mask_lift(const DevParams* __restrict__ dp, const u64* m, u64* out) {
+__global__ void k_mask_lift(DevCtx cx, const u64* m, u64* out) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = dp->L;
     const u32 n = 1;
     ITEM_LOOP {
@@ -196,7 +207,8 @@ __global__ void k_mask_lift(const DevParams* __restrict__ dp, const u64* m, u64*
 
 // ---------------------------------------------------------------- key switching
 // c1 limbs of each ct into a contiguous [n][L][N] buffer
-__global__ void k_gather_c1(const DevParams* __restrict__ dp, u32 n, const u64* const* ct, u64* C) {
+__global__ void k_gather_c1(DevCtx cx, u32 n, const u64* const* ct, u64* C) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = dp->L;
     const size_t LN = (size_t)L * N;
     ITEM_LOOP {
@@ -208,8 +220,9 @@ __global__ void k_gather_c1(const DevParams* __restrict__ dp, u32 n, const u64* 
 
 // oracle key_switch() ModUp: digit dg of the coefficient-domain poly C, lifted
 // to every limb of Q ++ P with centred residues.  D: [n][dnum][R][N]
-__global__ void k_modup_lift(const DevParams* __restrict__ dp, u32 n, const u64* C, size_t c_stride,
+__global__ void k_modup_lift(DevCtx cx, u32 n, const u64* C, size_t c_stride,
                              u64* D) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = dp->L, R = dp->R, A = dp->alpha, dnum = dp->dnum;
     ITEM_LOOP {
         const u64* c = C + item * c_stride;
@@ -244,8 +257,9 @@ __global__ void k_modup_lift(const DevParams* __restrict__ dp, u32 n, const u64*
 }
 
 // acc[c][r] = sum_dg D[dg][r][galois_src(k)] * key[dg][c][r][k]  ([n][2][R][N])
-__global__ void k_ks_inner(const DevParams* __restrict__ dp, u32 n, const u64* const* D,
+__global__ void k_ks_inner(DevCtx cx, u32 n, const u64* const* D,
                            const u64* const* key, const u32* g, u64* const* acc) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, R = dp->R, dnum = dp->dnum, logN = dp->logN;
     ITEM_LOOP {
         const u64* d = D[item];
@@ -256,21 +270,23 @@ __global__ void k_ks_inner(const DevParams* __restrict__ dp, u32 n, const u64* c
             const u32 src = ge == 1 ? j : galois_src(j, ge, logN);
             for (u32 r = 0; r < R; ++r) {
                 const Prime& P = dp->pr[r];
-                u64 a0 = 0, a1 = 0;
+                // 128-bit lazy accumulation, one reduction per output (dnum <= 4)
+                Acc a0, a1;
                 for (u32 dg = 0; dg < dnum; ++dg) {
                     const u64 x = d[((size_t)dg * R + r) * N + src];
-                    a0 = add_mod(a0, mul_mod(x, k[(((size_t)dg * 2 + 0) * R + r) * N + j], P), P.q);
-                    a1 = add_mod(a1, mul_mod(x, k[(((size_t)dg * 2 + 1) * R + r) * N + j], P), P.q);
+                    a0.mac(x, __ldg(k + (((size_t)dg * 2 + 0) * R + r) * N + j));
+                    a1.mac(x, __ldg(k + (((size_t)dg * 2 + 1) * R + r) * N + j));
                 }
-                a[(size_t)r * N + j] = a0;
-                a[((size_t)R + r) * N + j] = a1;
+                a[(size_t)r * N + j] = reduce_acc(a0, P);
+                a[((size_t)R + r) * N + j] = reduce_acc(a1, P);
             }
         }
     }
 }
 
 // ModDown correction: V[c][i] = sum_k centred([w_k (P/p_k)^-1]_{p_k}) (P/p_k) mod q_i
-__global__ void k_moddown_conv(const DevParams* __restrict__ dp, u32 n, const u64* const* acc, u64* V) {
+__global__ void k_moddown_conv(DevCtx cx, u32 n, const u64* const* acc, u64* V) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = dp->L, K = dp->K, R = dp->R;
     ITEM_LOOP {
         const u32 c = blockIdx.z;
@@ -296,9 +312,10 @@ __global__ void k_moddown_conv(const DevParams* __restrict__ dp, u32 n, const u6
 }
 
 // out0 = (acc0 - V0) P^-1 + add0[galois_src]; out1 = (acc1 - V1) P^-1 (+ add1)
-__global__ void k_ks_finish(const DevParams* __restrict__ dp, u32 n, const u64* const* acc,
+__global__ void k_ks_finish(DevCtx cx, u32 n, const u64* const* acc,
                             const u64* V, const u64* const* add0, const u32* g0,
                             const u64* const* add1, u64* const* out) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = dp->L, R = dp->R, logN = dp->logN;
     ITEM_LOOP {
         const u64* a = acc[item];
@@ -325,7 +342,8 @@ __global__ void k_ks_finish(const DevParams* __restrict__ dp, u32 n, const u64* 
 
 // ---------------------------------------------------------------- tensoring
 // oracle q_to_b(): exact centred conversion of 4 polys per item, X: [n][4][L][N]
-__global__ void k_q_to_b(const DevParams* __restrict__ dp, u32 n, const u64* X, u64* XB) {
+__global__ void k_q_to_b(DevCtx cx, u32 n, const u64* X, u64* XB) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = dp->L, K = dp->K, nB = dp->nB;
     ITEM_LOOP {
         const u32 p = blockIdx.z;
@@ -351,8 +369,9 @@ __global__ void k_q_to_b(const DevParams* __restrict__ dp, u32 n, const u64* X, 
 }
 
 // tensor over Q ++ B in the NTT domain; T: [n][3][L+nB][N]
-__global__ void k_tensor(const DevParams* __restrict__ dp, u32 n, const u64* const* A,
+__global__ void k_tensor(DevCtx cx, u32 n, const u64* const* A,
                          const u64* const* B, const u64* XB, u64* T) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = dp->L, K = dp->K, nB = dp->nB, D = L + nB;
     ITEM_LOOP {
         const u32 d = blockIdx.z;
@@ -380,7 +399,8 @@ __global__ void k_tensor(const DevParams* __restrict__ dp, u32 n, const u64* con
 }
 
 // oracle scale_round(): round(t x / Q) from Q ++ B residues, then exact B -> Q
-__global__ void k_scale_round(const DevParams* __restrict__ dp, u32 n, const u64* T, u64* E) {
+__global__ void k_scale_round(DevCtx cx, u32 n, const u64* T, u64* E) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = dp->L, K = dp->K, nB = dp->nB, D = L + nB;
     ITEM_LOOP {
         const u32 p = blockIdx.z;
@@ -398,7 +418,9 @@ __global__ void k_scale_round(const DevParams* __restrict__ dp, u32 n, const u64
             Acc128 s2{0, 0};
             for (u32 k = 0; k < nB; ++k) {
                 const u64 b = dp->pr[L + K + k].q;
-                u64 acc = rr % b;
+                Acc rra;
+                rra.lo = rr;  // rr < L * 2^60: one Barrett step instead of a 64-bit division
+                u64 acc = reduce_acc(rra, dp->pr[L + K + k]);
                 for (u32 i = 0; i < L; ++i)
                     acc = add_mod(acc, shoup_mul(a[i], dp->W[i][k], dp->W_sh[i][k], b), b);
                 acc = add_mod(acc, shoup_mul(t[(size_t)(L + k) * N + j], dp->T[k], dp->T_sh[k], b), b);
@@ -418,37 +440,40 @@ __global__ void k_scale_round(const DevParams* __restrict__ dp, u32 n, const u64
 }
 
 // ---------------------------------------------------------------- key generation
-__global__ void k_keygen_sk(const DevParams* __restrict__ dp, u64* S) {
+__global__ void k_keygen_sk(DevCtx cx, u64* S) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, R = dp->R;
     const u32 n = 1;
     ITEM_LOOP {
         COEF_LOOP {
-            const i64 s = ternary(dp->seed, kStreamSk, j);
+            const i64 s = ternary(cx.seed, kStreamSk, j);
             for (u32 r = 0; r < R; ++r) S[(size_t)r * N + j] = small_to_mod(s, dp->pr[r].q);
         }
     }
 }
 
 // Gaussian error for a stream, lifted to `limbs` limbs: E[l][j]
-__global__ void k_keygen_err(const DevParams* __restrict__ dp, u64 stream, u32 limbs, u64* E) {
+__global__ void k_keygen_err(DevCtx cx, u64 stream, u32 limbs, u64* E) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N;
     const u32 n = 1;
     ITEM_LOOP {
         COEF_LOOP {
-            const i64 e = gauss(dp->seed, stream, j, dp->cdt);
+            const i64 e = gauss(cx.seed, stream, j, cx.cdt);
             for (u32 r = 0; r < limbs; ++r) E[(size_t)r * N + j] = small_to_mod(e, dp->pr[r].q);
         }
     }
 }
 
-__global__ void k_keygen_pk(const DevParams* __restrict__ dp, const u64* S, const u64* E, u64* pk) {
+__global__ void k_keygen_pk(DevCtx cx, const u64* S, const u64* E, u64* pk) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = dp->L;
     const u32 n = 1;
     ITEM_LOOP {
         COEF_LOOP {
             for (u32 i = 0; i < L; ++i) {
                 const Prime& P = dp->pr[i];
-                const u64 a = uniform(dp->seed, kStreamPkA, (u64)i * N + j, P.q);
+                const u64 a = uniform(cx.seed, kStreamPkA, (u64)i * N + j, P.q);
                 pk[(size_t)i * N + j] = sub_mod(E[(size_t)i * N + j], mul_mod(a, S[(size_t)i * N + j], P), P.q);
                 pk[(size_t)(L + i) * N + j] = a;
             }
@@ -457,8 +482,9 @@ __global__ void k_keygen_pk(const DevParams* __restrict__ dp, const u64* S, cons
 }
 
 // oracle make_key(): key[dg][0][r] = -a s + e + [r in digit dg] P s'; key[dg][1][r] = a
-__global__ void k_keygen_ks(const DevParams* __restrict__ dp, u32 kid, u32 g, const u64* S,
+__global__ void k_keygen_ks(DevCtx cx, u32 kid, u32 g, const u64* S,
                             const u64* E, u64* key) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = dp->L, R = dp->R, A = dp->alpha, logN = dp->logN;
     const u32 dg = blockIdx.y;
     const u32 n = 1;
@@ -468,7 +494,7 @@ __global__ void k_keygen_ks(const DevParams* __restrict__ dp, u32 kid, u32 g, co
         for (u32 r = 0; r < R; ++r) {
             const Prime& P = dp->pr[r];
             const u64 sr = S[(size_t)r * N + j];
-            const u64 a = uniform(dp->seed, kStreamKsA | ((u64)kid << 8) | dg, (u64)r * N + j, P.q);
+            const u64 a = uniform(cx.seed, kStreamKsA | ((u64)kid << 8) | dg, (u64)r * N + j, P.q);
             u64 v = sub_mod(E[((size_t)dg * R + r) * N + j], mul_mod(a, sr, P), P.q);
             if (r < L && r / A == dg) {
                 const u64 sp = kid == 0 ? mul_mod(sr, sr, P) : S[(size_t)r * N + src];
@@ -569,6 +595,15 @@ Context::Context(int param_id, u64 seed, int device) : device_(device) {
     hp_.dev.cdt = d_cdt_;
     HGM_CUDA(cudaMalloc(&dp_, sizeof(DevParams)));
     HGM_CUDA(cudaMemcpy(dp_, &hp_.dev, sizeof(DevParams), cudaMemcpyHostToDevice));
+    // parameter-set constants -> __constant__ (identical for every context of the set)
+    HGM_CUDA(cudaMemcpyToSymbol(c_dp, &hp_.dev, sizeof(DevParams), (size_t)param_id * sizeof(DevParams)));
+    ntt_upload_params(param_id, hp_.dev);
+    HGM_CUDA(cudaGetLastError());
+    cx_.tw = d_tw_;
+    cx_.slot_ntt = d_slot_;
+    cx_.cdt = d_cdt_;
+    cx_.seed = seed;
+    cx_.pid = (u32)param_id;
     build_keys();
 }
 
@@ -602,9 +637,9 @@ void Context::ntt(bool forward, const NttJobs& jobs) {
     if (jobs.count == 0) return;
     launches_ += hp_.logN > 13 ? 2 : 1;
     if (forward)
-        ntt_forward(dp_, hp_.dev, jobs, stream_);
+        ntt_forward(cx_, hp_.dev, jobs, stream_);
     else
-        ntt_inverse(dp_, hp_.dev, jobs, stream_);
+        ntt_inverse(cx_, hp_.dev, jobs, stream_);
     HGM_CUDA(cudaGetLastError());
 }
 
@@ -612,12 +647,12 @@ void Context::build_keys() {
     const u32 N = hp_.N, L = hp_.L, R = hp_.R;
     HGM_CUDA(cudaMalloc(&d_sk_, (size_t)R * N * 8));
     HGM_CUDA(cudaMalloc(&d_pk_, (size_t)2 * L * N * 8));
-    k_keygen_sk<<<grid_of(N, 1), kThreads, 0, stream_>>>(dp_, d_sk_); ++launches_;
+    k_keygen_sk<<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, d_sk_); ++launches_;
     ntt(true, jobs_contig(d_sk_, R, 0, R));
     u64* E = alloc((size_t)L * N);
-    k_keygen_err<<<grid_of(N, 1), kThreads, 0, stream_>>>(dp_, kStreamPkE, L, E); ++launches_;
+    k_keygen_err<<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, kStreamPkE, L, E); ++launches_;
     ntt(true, jobs_contig(E, L, 0, L));
-    k_keygen_pk<<<grid_of(N, 1), kThreads, 0, stream_>>>(dp_, d_sk_, E, d_pk_); ++launches_;
+    k_keygen_pk<<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, d_sk_, E, d_pk_); ++launches_;
     release(E);
     HGM_CUDA(cudaGetLastError());
     ks_key(0);  // relinearisation key
@@ -642,10 +677,10 @@ const u64* Context::ks_key(u32 kid) {
     HGM_CUDA(cudaMallocAsync((void**)&key, (size_t)dnum * 2 * R * N * 8, stream_));
     u64* E = alloc((size_t)dnum * R * N);
     for (u32 dg = 0; dg < dnum; ++dg)
-        k_keygen_err<<<grid_of(N, 1), kThreads, 0, stream_>>>(dp_, kStreamKsE | ((u64)kid << 8) | dg, R,
+        k_keygen_err<<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, kStreamKsE | ((u64)kid << 8) | dg, R,
                                                              E + (size_t)dg * R * N); ++launches_;
     ntt(true, jobs_contig(E, dnum * R, 0, R));
-    k_keygen_ks<<<dim3((N + kThreads - 1) / kThreads, dnum), kThreads, 0, stream_>>>(dp_, kid, kid, d_sk_, E, key); ++launches_;
+    k_keygen_ks<<<dim3((N + kThreads - 1) / kThreads, dnum), kThreads, 0, stream_>>>(cx_, kid, kid, d_sk_, E, key); ++launches_;
     release(E);
     HGM_CUDA(cudaGetLastError());
     std::lock_guard<std::mutex> lk(key_mu_);
@@ -676,12 +711,12 @@ const u64* Context::mask_plain(const i64* mask, size_t S) {
     std::vector<u32> Sv{(u32)S};
     const u32* dS = upload(Sv);
     u64* m = alloc(N);
-    k_encode_scatter<<<grid_of(N, 1), kThreads, 0, stream_>>>(dp_, 1, dvals, dS, m); ++launches_;
+    k_encode_scatter<<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, 1, dvals, dS, m); ++launches_;
     NttJobs tj = jobs_contig(m, 1, kTIndex, 1);
     ntt(false, tj);
     u64* out = nullptr;
     HGM_CUDA(cudaMallocAsync((void**)&out, (size_t)L * N * 8, stream_));
-    k_mask_lift<<<grid_of(N, 1), kThreads, 0, stream_>>>(dp_, m, out); ++launches_;
+    k_mask_lift<<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, m, out); ++launches_;
     ntt(true, jobs_contig(out, L, 0, L));
     release(m);
     HGM_CUDA(cudaGetLastError());
@@ -715,9 +750,9 @@ void Context::encrypt(int n, const i64* const* host_vals, const size_t* S, const
     u64* const* dout = upload(outs);
     u64* M = alloc((size_t)n * N);
     u64* U = alloc((size_t)n * L * N);
-    k_encode_scatter<<<grid_of(N, n), kThreads, 0, stream_>>>(dp_, n, dvals, dS, M); ++launches_;
+    k_encode_scatter<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, dvals, dS, M); ++launches_;
     ntt(false, jobs_contig(M, n, kTIndex, 1));
-    k_enc_lift<<<grid_of(N, n), kThreads, 0, stream_>>>(dp_, n, M, dctr, U, dout); ++launches_;
+    k_enc_lift<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, M, dctr, U, dout); ++launches_;
     ntt(true, jobs_contig(U, n * L, 0, L));
     NttJobs cj;
     std::vector<u64*> limbs((size_t)n * 2 * L);
@@ -728,7 +763,7 @@ void Context::encrypt(int n, const i64* const* host_vals, const size_t* S, const
     cj.period = L;
     for (u32 i = 0; i < L; ++i) cj.prime[i] = (unsigned char)i;
     ntt(true, cj);
-    k_enc_finish<<<grid_of(N, n), kThreads, 0, stream_>>>(dp_, n, U, d_pk_, dout); ++launches_;
+    k_enc_finish<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, U, d_pk_, dout); ++launches_;
     release(M);
     release(U);
     HGM_CUDA(cudaGetLastError());
@@ -752,11 +787,11 @@ void Context::decrypt(int n, const u64* const* in, const size_t* S, i64* const* 
     u64* X = alloc((size_t)n * L * N);
     u64* M = alloc((size_t)n * N);
     i64* O = reinterpret_cast<i64*>(alloc((size_t)n * H));
-    k_dec_phase<<<grid_of(N, n), kThreads, 0, stream_>>>(dp_, n, din, d_sk_, X); ++launches_;
+    k_dec_phase<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, din, d_sk_, X); ++launches_;
     ntt(false, jobs_contig(X, n * L, 0, L));
-    k_dec_round<<<grid_of(N, n), kThreads, 0, stream_>>>(dp_, n, X, M); ++launches_;
+    k_dec_round<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, X, M); ++launches_;
     ntt(true, jobs_contig(M, n, kTIndex, 1));
-    k_dec_gather<<<grid_of(H, n), kThreads, 0, stream_>>>(dp_, n, M, dS, O); ++launches_;
+    k_dec_gather<<<grid_of(H, n), kThreads, 0, stream_>>>(cx_, n, M, dS, O); ++launches_;
     std::vector<i64> host((size_t)n * H);
     HGM_CUDA(cudaMemcpyAsync(host.data(), O, host.size() * 8, cudaMemcpyDeviceToHost, stream_));
     release(X);
@@ -777,7 +812,7 @@ void Context::add(int n, const u64* const* a, const u64* const* b, u64* const* o
     }
     std::vector<const u64*> va(a, a + n), vb(b, b + n);
     std::vector<u64*> vo(out, out + n);
-    k_add<<<grid_of(hp_.N, n, 1), kThreads, 0, stream_>>>(dp_, n, upload(va), upload(vb), upload(vo)); ++launches_;
+    k_add<<<grid_of(hp_.N, n, 1), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), upload(vo)); ++launches_;
     HGM_CUDA(cudaGetLastError());
 }
 
@@ -812,7 +847,7 @@ void Context::lincomb(int n_out, const u32* off, const u64* const* in, const u64
     std::vector<u32> voff(off, off + n_out + 1);
     std::vector<const u64*> vin(in, in + nt), vm(mask, mask + nt);
     std::vector<u64*> vo(out, out + n_out);
-    k_lincomb<<<grid_of(hp_.N, n_out, 1), kThreads, 0, stream_>>>(dp_, n_out, upload(voff), upload(vin),
+    k_lincomb<<<grid_of(hp_.N, n_out, 1), kThreads, 0, stream_>>>(cx_, n_out, upload(voff), upload(vin),
                                                                   upload(vm), upload(vo)); ++launches_;
     HGM_CUDA(cudaGetLastError());
 }
@@ -829,15 +864,20 @@ void Context::modup(int n, const u64* const* ct, u64* const* out) {
     const u32 N = hp_.N, L = hp_.L, R = hp_.R, dnum = hp_.dnum;
     std::vector<const u64*> vc(ct, ct + n);
     u64* C = alloc((size_t)n * L * N);
-    k_gather_c1<<<grid_of(N, n), kThreads, 0, stream_>>>(dp_, n, upload(vc), C); ++launches_;
+    k_gather_c1<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, upload(vc), C); ++launches_;
     ntt(false, jobs_contig(C, n * L, 0, L));
     // lift into a contiguous staging area, then scatter-copy to the outputs
     bool contiguous = true;
     for (int i = 1; i < n; ++i)
         if (out[i] != out[0] + (size_t)i * dnum * R * N) contiguous = false;
     u64* D = contiguous ? out[0] : alloc((size_t)n * dnum * R * N);
-    k_modup_lift<<<grid_of(N, n), kThreads, 0, stream_>>>(dp_, n, C, (size_t)L * N, D); ++launches_;
-    ntt(true, jobs_contig(D, n * dnum * R, 0, R));
+    if (ntt_fusable(hp_.dev)) {
+        ntt_modup_fused(cx_, hp_.dev, n, C, (size_t)L * N, D, stream_);
+        ++launches_;
+    } else {
+        k_modup_lift<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, C, (size_t)L * N, D); ++launches_;
+        ntt(true, jobs_contig(D, n * dnum * R, 0, R));
+    }
     if (!contiguous) {
         std::vector<const u64*> src(n);
         std::vector<u64*> dst(out, out + n);
@@ -855,14 +895,18 @@ void Context::inner_product(int n, const u64* const* digits, const u64* const* k
     std::vector<const u64*> vd(digits, digits + n), vk(keys, keys + n);
     std::vector<u32> vg(g, g + n);
     std::vector<u64*> va(acc, acc + n);
-    k_ks_inner<<<grid_of(hp_.N, n), kThreads, 0, stream_>>>(dp_, n, upload(vd), upload(vk), upload(vg),
+    k_ks_inner<<<grid_of(hp_.N, n), kThreads, 0, stream_>>>(cx_, n, upload(vd), upload(vk), upload(vg),
                                                            upload(va)); ++launches_;
     HGM_CUDA(cudaGetLastError());
 }
 
 // ModDown of n accumulators, then out = (acc - conv) P^-1 + add0[g0] (+ add1)
-void Context::key_switch_tail(int n, u64* const* acc, const u64* const* add0, const u32* g0,
-                              const u64* const* add1, u64* const* out) {
+// ModDown of n accumulators (P limbs inverse-transformed first), then
+//   out = (acc - NTT(conv)) P^-1 + NTT(ecoef) + addn[galois]   (ecoef/addn optional)
+// ecoef: per item [2][L][N] coefficient-domain addend (relinearisation's e0, e1);
+// addn: per item NTT-domain c0 limbs added to component 0 (rotation's phi(c0)).
+void Context::key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, const u64* const* addn,
+                              const u32* g, u64* const* out) {
     const u32 N = hp_.N, L = hp_.L, K = hp_.K, R = hp_.R;
     NttJobs pj;
     std::vector<u64*> plimbs((size_t)n * 2 * K);
@@ -876,19 +920,36 @@ void Context::key_switch_tail(int n, u64* const* acc, const u64* const* add0, co
     ntt(false, pj);
     std::vector<u64*> va(acc, acc + n);
     u64* const* dacc = upload(va);
-    u64* V = alloc((size_t)n * 2 * L * N);
-    k_moddown_conv<<<grid_of(N, n, 2), kThreads, 0, stream_>>>(dp_, n, dacc, V); ++launches_;
-    ntt(true, jobs_contig(V, n * 2 * L, 0, L));
-    std::vector<const u64*> v0(add0, add0 + n);
-    std::vector<u32> vg(g0, g0 + n);
+    std::vector<u32> vg(g, g + n);
     std::vector<u64*> vo(out, out + n);
-    const u64* const* d1 = nullptr;
-    if (add1) {
-        std::vector<const u64*> v1(add1, add1 + n);
-        d1 = upload(v1);
+    const u64* const* dadd = nullptr;
+    if (addn) {
+        std::vector<const u64*> v(addn, addn + n);
+        dadd = upload(v);
     }
-    k_ks_finish<<<grid_of(N, n), kThreads, 0, stream_>>>(dp_, n, dacc, V, upload(v0), upload(vg), d1,
-                                                        upload(vo)); ++launches_;
+    const u64* const* dec = nullptr;
+    if (ecoef) {
+        std::vector<const u64*> v(ecoef, ecoef + n);
+        dec = upload(v);
+    }
+    if (ntt_fusable(hp_.dev)) {
+        ntt_moddown_fused(cx_, hp_.dev, n, dacc, dec, dadd, upload(vg), upload(vo), stream_);
+        ++launches_;
+        HGM_CUDA(cudaGetLastError());
+        return;
+    }
+    // unfused (N = 32768): conversion pass, NTT, finishing pass; ecoef was
+    // already transformed by the caller and is added as NTT-domain e0 / e1
+    u64* V = alloc((size_t)n * 2 * L * N);
+    k_moddown_conv<<<grid_of(N, n, 2), kThreads, 0, stream_>>>(cx_, n, dacc, V); ++launches_;
+    ntt(true, jobs_contig(V, n * 2 * L, 0, L));
+    std::vector<const u64*> v0(n), v1(n);
+    for (int i = 0; i < n; ++i) {
+        v0[i] = ecoef ? ecoef[i] : addn[i];
+        v1[i] = ecoef ? ecoef[i] + (size_t)L * N : nullptr;
+    }
+    k_ks_finish<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, dacc, V, upload(v0), upload(vg),
+                                                        ecoef ? upload(v1) : nullptr, upload(vo)); ++launches_;
     release(V);
     HGM_CUDA(cudaGetLastError());
 }
@@ -910,7 +971,7 @@ void Context::rotate(int n, const u64* const* modup, const u64* const* ct, const
     std::vector<u64*> accs(n);
     for (int i = 0; i < n; ++i) accs[i] = A + (size_t)i * 2 * R * N;
     inner_product(n, modup, keys.data(), g, accs.data());
-    key_switch_tail(n, accs.data(), ct, g, nullptr, out);
+    key_switch_tail(n, accs.data(), nullptr, ct, g, out);
     release(A);
 }
 
@@ -941,7 +1002,7 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
     ntt(false, jobs_contig(X, n * 4 * L, 0, L));
     // 2. exact Q -> B and NTT over B
     u64* XB = alloc((size_t)n * 4 * nB * N);
-    k_q_to_b<<<grid_of(N, n, 4), kThreads, 0, stream_>>>(dp_, n, X, XB); ++launches_;
+    k_q_to_b<<<grid_of(N, n, 4), kThreads, 0, stream_>>>(cx_, n, X, XB); ++launches_;
     release(X);
     ntt(true, jobs_contig(XB, n * 4 * nB, L + K, nB));
     // 3. tensor over Q ++ B, INTT
@@ -949,7 +1010,7 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
     u64* T = alloc((size_t)n * 3 * D * N);
     {
         std::vector<const u64*> va(a, a + n), vb(b, b + n);
-        k_tensor<<<grid_of(N, n, D), kThreads, 0, stream_>>>(dp_, n, upload(va), upload(vb), XB, T); ++launches_;
+        k_tensor<<<grid_of(N, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T); ++launches_;
     }
     release(XB);
     NttJobs tj = jobs_contig(T, n * 3 * D, 0, D);
@@ -957,14 +1018,18 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
     ntt(false, tj);
     // 4. scale and round back to Q (coefficient form)
     u64* E = alloc((size_t)n * 3 * LN);
-    k_scale_round<<<grid_of(N, n, 3), kThreads, 0, stream_>>>(dp_, n, T, E); ++launches_;
+    k_scale_round<<<grid_of(N, n, 3), kThreads, 0, stream_>>>(cx_, n, T, E); ++launches_;
     release(T);
-    // 5. relinearise e2: ModUp, inner product with rlk, ModDown, add NTT(e0, e1)
+    // 5. relinearise e2: ModUp, inner product with rlk, ModDown, add (e0, e1)
+    const bool fused = ntt_fusable(hp_.dev);
     u64* Dg = alloc((size_t)n * dnum * R * N);
-    k_modup_lift<<<grid_of(N, n), kThreads, 0, stream_>>>(dp_, n, E + 2 * LN, 3 * LN, Dg); ++launches_;
-    ntt(true, jobs_contig(Dg, n * dnum * R, 0, R));
-    {
-        NttJobs ej;
+    if (fused) {
+        ntt_modup_fused(cx_, hp_.dev, n, E + 2 * LN, 3 * LN, Dg, stream_);
+        ++launches_;
+    } else {
+        k_modup_lift<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, E + 2 * LN, 3 * LN, Dg); ++launches_;
+        ntt(true, jobs_contig(Dg, n * dnum * R, 0, R));
+        NttJobs ej;  // e0, e1 to the NTT domain (the fused ModDown adds them in coefficient form)
         std::vector<u64*> limbs((size_t)n * 2 * L);
         for (int i = 0; i < n; ++i)
             for (u32 w = 0; w < 2 * L; ++w) limbs[(size_t)i * 2 * L + w] = E + (size_t)i * 3 * LN + (size_t)w * N;
@@ -975,7 +1040,7 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
         ntt(true, ej);
     }
     u64* A = alloc((size_t)n * 2 * R * N);
-    std::vector<const u64*> digits(n), keys(n), e0(n), e1(n);
+    std::vector<const u64*> digits(n), keys(n), ecoef(n);
     std::vector<u64*> accs(n);
     std::vector<u32> ones(n, 1);
     const u64* rlk = ks_key(0);
@@ -983,11 +1048,10 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
         digits[i] = Dg + (size_t)i * dnum * R * N;
         keys[i] = rlk;
         accs[i] = A + (size_t)i * 2 * R * N;
-        e0[i] = E + (size_t)i * 3 * LN;
-        e1[i] = E + (size_t)i * 3 * LN + LN;
+        ecoef[i] = E + (size_t)i * 3 * LN;  // [e0 limbs | e1 limbs]
     }
     inner_product(n, digits.data(), keys.data(), ones.data(), accs.data());
-    key_switch_tail(n, accs.data(), e0.data(), ones.data(), e1.data(), out);
+    key_switch_tail(n, accs.data(), ecoef.data(), nullptr, ones.data(), out);
     release(Dg);
     release(A);
     release(E);

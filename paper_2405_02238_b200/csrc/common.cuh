@@ -82,6 +82,17 @@ struct DevParams {
     u64 phat_mod_q[kMaxK][kMaxL], phat_mod_q_sh[kMaxK][kMaxL];
 };
 
+// Per-context values passed by value to every kernel (the parameter-set
+// constants live in __constant__ memory, one slot per set, see kParamSets).
+constexpr int kParamSets = 3;
+struct DevCtx {
+    const u64* tw;        // twiddle tables of this context
+    const u32* slot_ntt;  // slot -> NTT index
+    const u64* cdt;       // Gaussian CDT
+    u64 seed;
+    u32 pid;              // parameter-set slot in c_dp
+};
+
 // ------------------------------------------------------------------ scalar ops
 #ifdef __CUDACC__
 HD u64 mulhi64(u64 a, u64 b) {
@@ -127,6 +138,26 @@ HD u64 mul_mod(u64 a, u64 b, const Prime& p) {
     const u64 qh = mulhi64(x, p.mu);
     u64 r = lo - qh * p.q;
     if (r >= p.q) r -= p.q;
+    if (r >= p.q) r -= p.q;
+    return r;
+}
+// 128-bit lazy accumulator of products of residues (sum of <= 4 products of
+// values < q < 2^60), reduced once: x = hi:lo < 2^(2s+2).
+struct Acc {
+    u64 lo = 0, hi = 0;
+    HD void mac(u64 a, u64 b) {
+        const u64 pl = a * b, ph = mulhi64(a, b);
+        lo += pl;
+        hi += ph + (lo < pl);
+    }
+};
+// Shifted Barrett on x < 2^(2s+2) (s = bit length of q <= 60): the quotient
+// estimate is low by at most 2, so two corrections give [0, q).
+HD u64 reduce_acc(const Acc& a, const Prime& p) {
+    const u64 x = (a.hi << (66 - p.s)) | (a.lo >> (p.s - 2));
+    const u64 qh = mulhi64(x, p.mu);
+    u64 r = a.lo - qh * p.q;
+    if (r >= 2 * p.q) r -= 2 * p.q;
     if (r >= p.q) r -= p.q;
     return r;
 }

@@ -109,8 +109,8 @@ class Context {
 
   private:
     void build_keys();
-    void key_switch_tail(int n, u64* const* acc, const u64* const* add0, const u32* g0,
-                         const u64* const* add1, u64* const* out);
+    void key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, const u64* const* addn,
+                         const u32* g, u64* const* out);
     void inner_product(int n, const u64* const* digits, const u64* const* keys, const u32* g,
                        u64* const* acc);
 
@@ -119,6 +119,7 @@ class Context {
     int device_ = 0;
     cudaStream_t stream_ = nullptr;
     DevParams* dp_ = nullptr;
+    DevCtx cx_{};
     u64* d_tw_ = nullptr;
     u32* d_slot_ = nullptr;
     u64* d_cdt_ = nullptr;

@@ -1,9 +1,13 @@
 // ntt.cu -- see ntt.cuh for the design.
 #include "ntt.cuh"
 
+#include <cstdlib>
+
 namespace hgm {
 
 namespace {
+
+__constant__ DevParams c_dp[kParamSets];
 
 __device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
 
@@ -67,10 +71,14 @@ __device__ __forceinline__ void inv_stage(u64 (&x)[1 << R], u64 q, u64 q4, const
 // Forward local stages [S0, S0+R): stage s = S0 + r, twiddle
 //   2^(pre+s) + (blk << s) + (block << r) + c   (global table index)
 //   (1 << s) - 1 + (block << r) + c             (CTA cache index, s < 9)
-template <int LB, int S0, int R, bool kCached, bool kFromGlobal = false>
+struct NoLoad {
+    __device__ u64 operator()(int) const { return 0; }
+};
+
+template <int LB, int S0, int R, bool kCached, bool kFromGlobal = false, typename Ld = NoLoad>
 __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_cache,
                                           const u64* __restrict__ w_tab, const u64* __restrict__ ws_tab,
-                                          u64 q, int pre, int blk, const u64* __restrict__ gsrc = nullptr) {
+                                          u64 q, int pre, int blk, const Ld& ld = Ld()) {
     constexpr int NB = 1 << LB, T = NB / kElems, G = (NB >> R) / T;
     constexpr int LT_FIRST = LB - 1 - S0, LT_MIN = LT_FIRST - (R - 1);
     const u64 q3 = q << 1, q4 = q << 1;  // 2q (Harvey bounds)
@@ -84,7 +92,7 @@ __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_ca
         if constexpr (kCached) {
             if constexpr (kFromGlobal) {
 #pragma unroll
-                for (int k = 0; k < (1 << R); ++k) x[k] = __ldcs(gsrc + base + (k << LT_MIN));
+                for (int k = 0; k < (1 << R); ++k) x[k] = ld(base + (k << LT_MIN));
             } else {
 #pragma unroll
                 for (int k = 0; k < (1 << R); ++k) x[k] = sm[pad(base + (k << LT_MIN))];
@@ -226,6 +234,22 @@ __device__ __forceinline__ void store_last_stage(const u64* sm, u64* g, const u6
     }
 }
 
+// Same, handing each finished pair (elements 2i, 2i+1, canonical) to `st`.
+template <int LB, typename St>
+__device__ __forceinline__ void store_last_stage_io(const u64* sm, const St& st, const u64* __restrict__ w_tab,
+                                                    const u64* __restrict__ ws_tab, u64 q, int logN, int blk) {
+    constexpr int NB = 1 << LB, T = NB / kElems;
+    const int tw0 = (1 << (logN - 1)) + (blk << (LB - 1));
+    const u64 q2 = q << 1;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < NB / 2; i += T) {
+        const u64 w = __ldg(w_tab + tw0 + i), ws = __ldg(ws_tab + tw0 + i);
+        const u64 U = reduce_once(sm[pad(2 * i)], q2);
+        const u64 V = shoup_lazy(sm[pad(2 * i + 1)], w, ws, q);
+        st(i, reduce_once(reduce_once(U + V, q2), q), reduce_once(reduce_once(U - V + q2, q2), q));
+    }
+}
+
 // Inverse: the first Gentleman-Sande stage (t = 1) fused into the coalesced load.
 template <int LB>
 __device__ __forceinline__ void load_first_stage(u64* sm, const u64* g, const u64* __restrict__ w_tab,
@@ -277,7 +301,8 @@ __device__ __forceinline__ void store_block(const u64* sm, u64* g, u64 q, u64 s,
 // the first eight with CTA-cached twiddles), the last stage fused into the store.
 template <int LB>
 __global__ void __launch_bounds__((1 << LB) / kElems, 1)
-    k_ntt_fwd(const DevParams* __restrict__ dp, NttJobs jobs) {
+    k_ntt_fwd(DevCtx cx, NttJobs jobs) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     extern __shared__ u64 sm[];
     u64* cache = sm + smem_words<LB>();
     const u32 N = dp->N;
@@ -286,11 +311,12 @@ __global__ void __launch_bounds__((1 << LB) / kElems, 1)
     const int blk = blockIdx.y;
     const JobView jv = job_of(jobs, blockIdx.x, N);
     const u64 q = dp->pr[jv.prime].q;
-    const u64* w = dp->tw + (size_t)jv.prime * 4 * N;
+    const u64* w = cx.tw + (size_t)jv.prime * 4 * N;
     u64* g = jv.ptr + ((size_t)blk << LB);
     fill_tw_cache(cache, w, w + N, pre, blk);
     __syncthreads();
-    fwd_round<LB, 0, 4, true, true>(sm, cache, w, w + N, q, pre, blk, g);
+    auto ld = [g](int j) { return __ldcs(g + j); };
+    fwd_round<LB, 0, 4, true, true>(sm, cache, w, w + N, q, pre, blk, ld);
     __syncthreads();
     fwd_round<LB, 4, 4, true>(sm, cache, w, w + N, q, pre, blk);
     __syncthreads();
@@ -299,12 +325,143 @@ __global__ void __launch_bounds__((1 << LB) / kElems, 1)
     store_last_stage<LB>(sm, g, w, w + N, q, logN, blk);
 }
 
+// Forward transform of a limb whose input is COMPUTED by io.load(job, j) and
+// whose canonical NTT-domain output is CONSUMED by io.store(job, i, v0, v1)
+// (elements 2i, 2i+1): base-conversion passes fused around the NTT.
+template <int LB, typename IO>
+__global__ void __launch_bounds__((1 << LB) / kElems, 1) k_ntt_fwd_io(DevCtx cx, IO io) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
+    extern __shared__ u64 sm[];
+    u64* cache = sm + smem_words<LB>();
+    const u32 N = dp->N;
+    const int logN = (int)dp->logN;
+    const u32 job = blockIdx.x;
+    const int prime = io.prime(job);
+    const u64 q = dp->pr[prime].q;
+    const u64* w = cx.tw + (size_t)prime * 4 * N;
+    fill_tw_cache(cache, w, w + N, 0, 0);
+    __syncthreads();
+    auto ld = [&](int j) { return io.load(dp, job, (u32)j); };
+    fwd_round<LB, 0, 4, true, true>(sm, cache, w, w + N, q, 0, 0, ld);
+    __syncthreads();
+    fwd_round<LB, 4, 4, true>(sm, cache, w, w + N, q, 0, 0);
+    __syncthreads();
+    fwd_round<LB, 8, LB - 9, false>(sm, cache, w, w + N, q, 0, 0);
+    __syncthreads();
+    auto st = [&](int i, u64 v0, u64 v1) { io.store(dp, job, (u32)i, v0, v1); };
+    store_last_stage_io<LB>(sm, st, w, w + N, q, logN, 0);
+}
+
+// y < src < 2*dst (one bit length per prime set): centred y mod dst
+__device__ __forceinline__ u64 centred_lift_n(u64 y, u64 src, u64 dst) {
+    if (y > (src - 1) / 2) {
+        u64 m = src - y;
+        if (m >= dst) m -= dst;
+        return m ? dst - m : 0;
+    }
+    return y >= dst ? y - dst : y;
+}
+
+// ModUp fused into the forward NTT: job = (item, digit dg, target limb r).
+struct ModUpIO {
+    const u64* C;      // [item] c_stride words: L coefficient-domain limbs
+    size_t c_stride;
+    u64* D;            // [item][dnum][R][N]
+    u32 R, dnum, L, A, N;
+    __device__ int prime(u32 job) const { return (int)(job % R); }
+    __device__ u64 load(const DevParams* dp, u32 job, u32 j) const {
+        const u32 item = job / (dnum * R), dg = (job / R) % dnum, r = job % R;
+        const u64* c = C + item * c_stride;
+        if (r < L && r / A == dg) return c[(size_t)r * N + j];
+        const u64 qr = dp->pr[r].q;
+        u64 v = 0;
+        for (u32 a = 0; a < A; ++a) {
+            const u32 i = dg * A + a;
+            const u64 y = shoup_mul(c[(size_t)i * N + j], dp->dg_hat_inv[i], dp->dg_hat_inv_sh[i], dp->pr[i].q);
+            v = add_mod(v, shoup_mul(centred_lift_n(y, dp->pr[i].q, qr), dp->dg_hat[i][r], dp->dg_hat_sh[i][r], qr), qr);
+        }
+        return v;
+    }
+    __device__ void store(const DevParams*, u32 job, u32 i, u64 v0, u64 v1) const {
+        ulonglong2 v;
+        v.x = v0;
+        v.y = v1;
+        reinterpret_cast<ulonglong2*>(D + (size_t)job * N)[i] = v;
+    }
+};
+
+// ModDown fused into the forward NTT: job = (item, component c, limb i).
+//   out_c,i = NTT(addc_c,i - P^-1 conv_c,i) + P^-1 acc_c,i + [c = 0] addn_i[galois_src]
+// which equals the oracle's (acc - NTT(conv)) P^-1 (+ NTT(addc)) (+ phi(c0)) by
+// linearity of the NTT mod q_i -- exact.
+struct ModDownIO {
+    u64* const* acc;         // per item [2][R][N]; P limbs already inverse-transformed
+    const u64* const* addc;  // per item [2][L][N] coefficient-domain addend, or null
+    const u64* const* addn;  // per item [L][N] NTT-domain addend for c = 0, or null
+    const u32* g;            // per item Galois element for addn
+    u64* const* out;         // per item [2][L][N]
+    u32 L, K, R, N, logN;
+    __device__ int prime(u32 job) const { return (int)(job % L); }
+    __device__ u64 load(const DevParams* dp, u32 job, u32 j) const {
+        const u32 item = job / (2 * L), c = (job / L) & 1, i = job % L;
+        const u64* a = acc[item] + (size_t)c * R * N;
+        const u64 q = dp->pr[i].q;
+        u64 v = 0;
+        for (u32 k = 0; k < K; ++k) {
+            const u64 p = dp->pr[L + k].q;
+            const u64 z = shoup_mul(a[(size_t)(L + k) * N + j], dp->phat_inv[k], dp->phat_inv_sh[k], p);
+            v = add_mod(v, shoup_mul(centred_lift_n(z, p, q), dp->phat_mod_q[k][i], dp->phat_mod_q_sh[k][i], q), q);
+        }
+        const u64 base = addc ? addc[item][((size_t)c * L + i) * N + j] : 0;
+        return sub_mod(base, shoup_mul(v, dp->P_inv_q[i], dp->P_inv_q_sh[i], q), q);
+    }
+    __device__ void store(const DevParams* dp, u32 job, u32 i2, u64 v0, u64 v1) const {
+        const u32 item = job / (2 * L), c = (job / L) & 1, i = job % L;
+        const u64 q = dp->pr[i].q, pi = dp->P_inv_q[i], pis = dp->P_inv_q_sh[i];
+        const u64* a = acc[item] + ((size_t)c * R + i) * N;
+        u64 r0 = add_mod(v0, shoup_mul(a[2 * i2], pi, pis, q), q);
+        u64 r1 = add_mod(v1, shoup_mul(a[2 * i2 + 1], pi, pis, q), q);
+        if (c == 0 && addn) {
+            const u64* x = addn[item] + (size_t)i * N;
+            const u32 ge = g[item];
+            r0 = add_mod(r0, x[ge == 1 ? 2 * i2 : galois_src(2 * i2, ge, logN)], q);
+            r1 = add_mod(r1, x[ge == 1 ? 2 * i2 + 1 : galois_src(2 * i2 + 1, ge, logN)], q);
+        }
+        ulonglong2 v;
+        v.x = r0;
+        v.y = r1;
+        reinterpret_cast<ulonglong2*>(out[item] + ((size_t)c * L + i) * N)[i2] = v;
+    }
+};
+
+template <typename IO>
+void launch_fwd_io(const DevCtx& cx, const DevParams& hp, const IO& io, u32 jobs, cudaStream_t s) {
+    if (jobs == 0) return;
+    static bool configured13 = false, configured12 = false;
+    if (hp.logN == 13) {
+        const size_t smem = (smem_words<13>() + 2 * kTwCache) * sizeof(u64);
+        if (!configured13) {
+            cudaFuncSetAttribute(k_ntt_fwd_io<13, IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            configured13 = true;
+        }
+        k_ntt_fwd_io<13, IO><<<jobs, (1 << 13) / kElems, smem, s>>>(cx, io);
+    } else {
+        const size_t smem = (smem_words<12>() + 2 * kTwCache) * sizeof(u64);
+        if (!configured12) {
+            cudaFuncSetAttribute(k_ntt_fwd_io<12, IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            configured12 = true;
+        }
+        k_ntt_fwd_io<12, IO><<<jobs, (1 << 12) / kElems, smem, s>>>(cx, io);
+    }
+}
+
 // Inverse block transform: first stage fused into the load, then rounds of 4
 // (the last eight local stages with CTA-cached twiddles); N^-1 folded into the
 // store when the block is the whole limb.
 template <int LB>
 __global__ void __launch_bounds__((1 << LB) / kElems, 1)
-    k_ntt_inv(const DevParams* __restrict__ dp, NttJobs jobs) {
+    k_ntt_inv(DevCtx cx, NttJobs jobs) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     extern __shared__ u64 sm[];
     u64* cache = sm + smem_words<LB>();
     const u32 N = dp->N;
@@ -313,7 +470,7 @@ __global__ void __launch_bounds__((1 << LB) / kElems, 1)
     const JobView jv = job_of(jobs, blockIdx.x, N);
     const Prime& P = dp->pr[jv.prime];
     const u64 q = P.q;
-    const u64* w = dp->tw + (size_t)jv.prime * 4 * N;
+    const u64* w = cx.tw + (size_t)jv.prime * 4 * N;
     u64* g = jv.ptr + ((size_t)blk << LB);
     fill_tw_cache(cache, w + 2 * N, w + 3 * N, logN - LB, blk);
     load_first_stage<LB>(sm, g, w + 2 * N, w + 3 * N, q, logN, blk);
@@ -331,11 +488,12 @@ __global__ void __launch_bounds__((1 << LB) / kElems, 1)
 }
 
 // Two outermost forward stages for N = 4 * 2^LB: element j, j+N/4, j+N/2, j+3N/4.
-__global__ void k_ntt_fwd_outer2(const DevParams* __restrict__ dp, NttJobs jobs) {
+__global__ void k_ntt_fwd_outer2(DevCtx cx, NttJobs jobs) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, Q4 = N / 4;
     const JobView jv = job_of(jobs, blockIdx.y, N);
     const u64 q = dp->pr[jv.prime].q;
-    const u64* w = dp->tw + (size_t)jv.prime * 4 * N;
+    const u64* w = cx.tw + (size_t)jv.prime * 4 * N;
     const u64 w1 = w[1], w1s = w[N + 1], w2 = w[2], w2s = w[N + 2], w3 = w[3], w3s = w[N + 3];
     for (u32 j = blockIdx.x * blockDim.x + threadIdx.x; j < Q4; j += gridDim.x * blockDim.x) {
         u64* a = jv.ptr;
@@ -354,12 +512,13 @@ __global__ void k_ntt_fwd_outer2(const DevParams* __restrict__ dp, NttJobs jobs)
 }
 
 // Two outermost inverse stages (t = N/4, N/2) plus the N^-1 scaling.
-__global__ void k_ntt_inv_outer2(const DevParams* __restrict__ dp, NttJobs jobs) {
+__global__ void k_ntt_inv_outer2(DevCtx cx, NttJobs jobs) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, Q4 = N / 4;
     const JobView jv = job_of(jobs, blockIdx.y, N);
     const Prime& P = dp->pr[jv.prime];
     const u64 q = P.q;
-    const u64* w = dp->tw + (size_t)jv.prime * 4 * N + 2 * N;
+    const u64* w = cx.tw + (size_t)jv.prime * 4 * N + 2 * N;
     const u64* ws = w + N;
     const u64 w2 = w[2], w2s = ws[2], w3 = w[3], w3s = ws[3], w1 = w[1], w1s = ws[1];
     for (u32 j = blockIdx.x * blockDim.x + threadIdx.x; j < Q4; j += gridDim.x * blockDim.x) {
@@ -379,7 +538,7 @@ __global__ void k_ntt_inv_outer2(const DevParams* __restrict__ dp, NttJobs jobs)
 }
 
 template <int LB>
-void launch_block(bool fwd, const DevParams* dp, const NttJobs& jobs, int sub, cudaStream_t s) {
+void launch_block(bool fwd, const DevCtx& cx, const NttJobs& jobs, int sub, cudaStream_t s) {
     const size_t smem = (smem_words<LB>() + 2 * kTwCache) * sizeof(u64);
     static bool configured = false;
     if (!configured) {
@@ -389,38 +548,65 @@ void launch_block(bool fwd, const DevParams* dp, const NttJobs& jobs, int sub, c
     }
     dim3 grid(jobs.count, sub);
     if (fwd)
-        k_ntt_fwd<LB><<<grid, (1 << LB) / kElems, smem, s>>>(dp, jobs);
+        k_ntt_fwd<LB><<<grid, (1 << LB) / kElems, smem, s>>>(cx, jobs);
     else
-        k_ntt_inv<LB><<<grid, (1 << LB) / kElems, smem, s>>>(dp, jobs);
+        k_ntt_inv<LB><<<grid, (1 << LB) / kElems, smem, s>>>(cx, jobs);
 }
 
 }  // namespace
 
-void ntt_forward(const DevParams* dp, const DevParams& hp, const NttJobs& jobs_in, cudaStream_t s) {
+// The fused variants are exact but measured slower on B200 while the NTT is
+// integer-pipe bound (the conversions then compete with the butterflies at
+// one CTA per SM); they are opt-in via HGM_FUSED_KS=1 for experiments.
+bool ntt_fusable(const DevParams& hp) {
+    static const bool on = [] {
+        const char* e = std::getenv("HGM_FUSED_KS");
+        return e && e[0] == '1';
+    }();
+    return on && hp.logN <= 13;
+}
+
+void ntt_modup_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* C, size_t c_stride, u64* D,
+                     cudaStream_t s) {
+    ModUpIO io{C, c_stride, D, hp.R, hp.dnum, hp.L, hp.alpha, hp.N};
+    launch_fwd_io(cx, hp, io, (u32)n * hp.dnum * hp.R, s);
+}
+
+void ntt_moddown_fused(const DevCtx& cx, const DevParams& hp, int n, u64* const* acc, const u64* const* addc,
+                       const u64* const* addn, const u32* g, u64* const* out, cudaStream_t s) {
+    ModDownIO io{acc, addc, addn, g, out, hp.L, hp.K, hp.R, hp.N, hp.logN};
+    launch_fwd_io(cx, hp, io, (u32)n * 2 * hp.L, s);
+}
+
+void ntt_upload_params(int pid, const DevParams& p) {
+    cudaMemcpyToSymbol(c_dp, &p, sizeof(DevParams), (size_t)pid * sizeof(DevParams));
+}
+
+void ntt_forward(const DevCtx& cx, const DevParams& hp, const NttJobs& jobs_in, cudaStream_t s) {
     if (jobs_in.count == 0) return;
     NttJobs jobs = jobs_in;
     jobs.pack();
     if (hp.logN == 13) {
-        launch_block<13>(true, dp, jobs, 1, s);
+        launch_block<13>(true, cx, jobs, 1, s);
     } else if (hp.logN == 12) {
-        launch_block<12>(true, dp, jobs, 1, s);
+        launch_block<12>(true, cx, jobs, 1, s);
     } else {  // 2^15: two outer stages, then four 2^13 blocks
-        k_ntt_fwd_outer2<<<dim3(16, jobs.count), 512, 0, s>>>(dp, jobs);
-        launch_block<13>(true, dp, jobs, 4, s);
+        k_ntt_fwd_outer2<<<dim3(16, jobs.count), 512, 0, s>>>(cx, jobs);
+        launch_block<13>(true, cx, jobs, 4, s);
     }
 }
 
-void ntt_inverse(const DevParams* dp, const DevParams& hp, const NttJobs& jobs_in, cudaStream_t s) {
+void ntt_inverse(const DevCtx& cx, const DevParams& hp, const NttJobs& jobs_in, cudaStream_t s) {
     if (jobs_in.count == 0) return;
     NttJobs jobs = jobs_in;
     jobs.pack();
     if (hp.logN == 13) {
-        launch_block<13>(false, dp, jobs, 1, s);
+        launch_block<13>(false, cx, jobs, 1, s);
     } else if (hp.logN == 12) {
-        launch_block<12>(false, dp, jobs, 1, s);
+        launch_block<12>(false, cx, jobs, 1, s);
     } else {
-        launch_block<13>(false, dp, jobs, 4, s);
-        k_ntt_inv_outer2<<<dim3(16, jobs.count), 512, 0, s>>>(dp, jobs);
+        launch_block<13>(false, cx, jobs, 4, s);
+        k_ntt_inv_outer2<<<dim3(16, jobs.count), 512, 0, s>>>(cx, jobs);
     }
 }
 

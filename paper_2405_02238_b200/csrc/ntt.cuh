@@ -36,8 +36,20 @@ struct NttJobs {
     }
 };
 
-void ntt_forward(const DevParams* dp, const DevParams& hp, const NttJobs& jobs, cudaStream_t s);
-void ntt_inverse(const DevParams* dp, const DevParams& hp, const NttJobs& jobs, cudaStream_t s);
+void ntt_forward(const DevCtx& cx, const DevParams& hp, const NttJobs& jobs, cudaStream_t s);
+void ntt_inverse(const DevCtx& cx, const DevParams& hp, const NttJobs& jobs, cudaStream_t s);
+// Forward NTTs with fused base conversions (whole-limb transforms, N <= 8192):
+//  * ModUp: D[item][dg][r] = NTT_r(digit dg of C[item] lifted to prime r), C
+//    holding L coefficient-domain limbs per item (stride c_stride words);
+//  * ModDown: out[item] = (acc - NTT(conv(P-part))) P^-1 (+ NTT(addc)) (+ addn[galois]),
+//    acc's P limbs already inverse-transformed.  Pointer arrays live on the device.
+bool ntt_fusable(const DevParams& hp);
+void ntt_modup_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* C, size_t c_stride, u64* D,
+                     cudaStream_t s);
+void ntt_moddown_fused(const DevCtx& cx, const DevParams& hp, int n, u64* const* acc, const u64* const* addc,
+                       const u64* const* addn, const u32* g, u64* const* out, cudaStream_t s);
+// copies a parameter set's constants into this translation unit's __constant__ slot
+void ntt_upload_params(int pid, const DevParams& p);
 
 inline NttJobs jobs_contig(u64* base, u32 count, u32 first_prime, u32 period) {
     NttJobs j;
