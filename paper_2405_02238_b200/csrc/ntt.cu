@@ -1,6 +1,7 @@
 // ntt.cu -- see ntt.cuh for the design.
 #include "ntt.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace hgm {
@@ -297,32 +298,86 @@ __device__ __forceinline__ void store_block(const u64* sm, u64* g, u64 q, u64 s,
     }
 }
 
+// ---------------------------------------------------------------- persistent kernels
+// One CTA per SM loops over (limb, block) work items; the next item's residues
+// stream into the second shared-memory buffer with cp.async (8-byte granules,
+// the padded layout) while the current one is transformed, so HBM latency is
+// hidden behind the butterflies even at one CTA per SM.
+__device__ __forceinline__ void cp_async8(u64* smem_dst, const u64* gsrc) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+template <int LB>
+__device__ __forceinline__ void prefetch_block(u64* buf, const u64* g) {
+    constexpr int NB = 1 << LB, T = NB / kElems;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < NB; i += T) cp_async8(buf + pad(i), g + i);
+}
+
+struct WorkItem {
+    u64* g;
+    int prime, blk;
+};
+__device__ __forceinline__ WorkItem work_item(const NttJobs& jobs, u32 v, int sub, u32 N, int LB) {
+    const JobView jv = job_of(jobs, v / sub, N);
+    WorkItem w;
+    w.blk = (int)(v % sub);
+    w.prime = jv.prime;
+    w.g = jv.ptr + ((size_t)w.blk << LB);
+    return w;
+}
+
 // Forward block transform: rounds of 4 register stages (local stages 0..LB-2,
 // the first eight with CTA-cached twiddles), the last stage fused into the store.
 template <int LB>
 __global__ void __launch_bounds__((1 << LB) / kElems, 1)
-    k_ntt_fwd(DevCtx cx, NttJobs jobs) {
+    k_ntt_fwd(DevCtx cx, NttJobs jobs, int sub) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     extern __shared__ u64 sm[];
-    u64* cache = sm + smem_words<LB>();
+    u64* buf0 = sm;
+    u64* buf1 = sm + smem_words<LB>();
+    u64* cache = sm + 2 * smem_words<LB>();
     const u32 N = dp->N;
     const int logN = (int)dp->logN;
     const int pre = logN - LB;
-    const int blk = blockIdx.y;
-    const JobView jv = job_of(jobs, blockIdx.x, N);
-    const u64 q = dp->pr[jv.prime].q;
-    const u64* w = cx.tw + (size_t)jv.prime * 4 * N;
-    u64* g = jv.ptr + ((size_t)blk << LB);
-    fill_tw_cache(cache, w, w + N, pre, blk);
-    __syncthreads();
-    auto ld = [g](int j) { return __ldcs(g + j); };
-    fwd_round<LB, 0, 4, true, true>(sm, cache, w, w + N, q, pre, blk, ld);
-    __syncthreads();
-    fwd_round<LB, 4, 4, true>(sm, cache, w, w + N, q, pre, blk);
-    __syncthreads();
-    fwd_round<LB, 8, LB - 9, false>(sm, cache, w, w + N, q, pre, blk);
-    __syncthreads();
-    store_last_stage<LB>(sm, g, w, w + N, q, logN, blk);
+    const u32 total = jobs.count * (u32)sub;
+    u32 v = blockIdx.x;
+    if (v >= total) return;
+    WorkItem cur = work_item(jobs, v, sub, N, LB);
+    prefetch_block<LB>(buf0, cur.g);
+    cp_async_commit();
+    int cached_prime = -1, cached_blk = -1;
+    for (int slot = 0; v < total; v += gridDim.x, slot ^= 1) {
+        u64* b = slot ? buf1 : buf0;
+        const u32 vn = v + gridDim.x;
+        WorkItem nxt{nullptr, 0, 0};
+        if (vn < total) {
+            nxt = work_item(jobs, vn, sub, N, LB);
+            prefetch_block<LB>(slot ? buf0 : buf1, nxt.g);
+        }
+        cp_async_commit();
+        const u64 q = dp->pr[cur.prime].q;
+        const u64* w = cx.tw + (size_t)cur.prime * 4 * N;
+        if (cur.prime != cached_prime || cur.blk != cached_blk) {
+            fill_tw_cache(cache, w, w + N, pre, cur.blk);
+            cached_prime = cur.prime;
+            cached_blk = cur.blk;
+        }
+        cp_async_wait1();
+        __syncthreads();
+        fwd_round<LB, 0, 4, true>(b, cache, w, w + N, q, pre, cur.blk);
+        __syncthreads();
+        fwd_round<LB, 4, 4, true>(b, cache, w, w + N, q, pre, cur.blk);
+        __syncthreads();
+        fwd_round<LB, 8, LB - 9, false>(b, cache, w, w + N, q, pre, cur.blk);
+        __syncthreads();
+        store_last_stage<LB>(b, cur.g, w, w + N, q, logN, cur.blk);
+        __syncthreads();
+        cur = nxt;
+    }
 }
 
 // Forward transform of a limb whose input is COMPUTED by io.load(job, j) and
@@ -455,36 +510,72 @@ void launch_fwd_io(const DevCtx& cx, const DevParams& hp, const IO& io, u32 jobs
     }
 }
 
-// Inverse block transform: first stage fused into the load, then rounds of 4
-// (the last eight local stages with CTA-cached twiddles); N^-1 folded into the
-// store when the block is the whole limb.
+// Inverse block transform: prefetched block, first stage as an smem pass, then
+// rounds of 4 (the last eight local stages with CTA-cached twiddles); N^-1
+// folded into the store when the block is the whole limb.
 template <int LB>
 __global__ void __launch_bounds__((1 << LB) / kElems, 1)
-    k_ntt_inv(DevCtx cx, NttJobs jobs) {
+    k_ntt_inv(DevCtx cx, NttJobs jobs, int sub) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     extern __shared__ u64 sm[];
-    u64* cache = sm + smem_words<LB>();
+    constexpr int NB = 1 << LB, T = NB / kElems;
+    u64* buf0 = sm;
+    u64* buf1 = sm + smem_words<LB>();
+    u64* cache = sm + 2 * smem_words<LB>();
     const u32 N = dp->N;
     const int logN = (int)dp->logN;
-    const int blk = blockIdx.y;
-    const JobView jv = job_of(jobs, blockIdx.x, N);
-    const Prime& P = dp->pr[jv.prime];
-    const u64 q = P.q;
-    const u64* w = cx.tw + (size_t)jv.prime * 4 * N;
-    u64* g = jv.ptr + ((size_t)blk << LB);
-    fill_tw_cache(cache, w + 2 * N, w + 3 * N, logN - LB, blk);
-    load_first_stage<LB>(sm, g, w + 2 * N, w + 3 * N, q, logN, blk);
-    __syncthreads();
-    inv_round<LB, 1, LB - 9, false>(sm, cache, w + 2 * N, w + 3 * N, q, logN, blk);
-    __syncthreads();
-    inv_round<LB, LB - 8, 4, true>(sm, cache, w + 2 * N, w + 3 * N, q, logN, blk);
-    __syncthreads();
-    inv_round<LB, LB - 4, 4, true>(sm, cache, w + 2 * N, w + 3 * N, q, logN, blk);
-    __syncthreads();
-    if (logN == LB)
-        store_block<LB, true>(sm, g, q, P.ninv, P.ninv_sh);
-    else
-        store_block<LB, false>(sm, g, q, 0, 0);
+    const u32 total = jobs.count * (u32)sub;
+    u32 v = blockIdx.x;
+    if (v >= total) return;
+    WorkItem cur = work_item(jobs, v, sub, N, LB);
+    prefetch_block<LB>(buf0, cur.g);
+    cp_async_commit();
+    int cached_prime = -1, cached_blk = -1;
+    for (int slot = 0; v < total; v += gridDim.x, slot ^= 1) {
+        u64* b = slot ? buf1 : buf0;
+        const u32 vn = v + gridDim.x;
+        WorkItem nxt{nullptr, 0, 0};
+        if (vn < total) {
+            nxt = work_item(jobs, vn, sub, N, LB);
+            prefetch_block<LB>(slot ? buf0 : buf1, nxt.g);
+        }
+        cp_async_commit();
+        const Prime& P = dp->pr[cur.prime];
+        const u64 q = P.q;
+        const u64* w = cx.tw + (size_t)cur.prime * 4 * N;
+        if (cur.prime != cached_prime || cur.blk != cached_blk) {
+            fill_tw_cache(cache, w + 2 * N, w + 3 * N, logN - LB, cur.blk);
+            cached_prime = cur.prime;
+            cached_blk = cur.blk;
+        }
+        cp_async_wait1();
+        __syncthreads();
+        {  // first Gentleman-Sande stage (t = 1) on adjacent pairs
+            const int tw0 = (1 << (logN - 1)) + (cur.blk << (LB - 1));
+            const u64* wt = w + 2 * N;
+            const u64* wst = w + 3 * N;
+#pragma unroll 4
+            for (int i = threadIdx.x; i < NB / 2; i += T) {
+                const u64 x0 = b[pad(2 * i)], x1 = b[pad(2 * i + 1)];
+                const u64 tw = __ldg(wt + tw0 + i), tws = __ldg(wst + tw0 + i);
+                b[pad(2 * i)] = reduce_once(x0 + x1, q << 1);
+                b[pad(2 * i + 1)] = shoup_lazy(x0 - x1 + (q << 1), tw, tws, q);
+            }
+        }
+        __syncthreads();
+        inv_round<LB, 1, LB - 9, false>(b, cache, w + 2 * N, w + 3 * N, q, logN, cur.blk);
+        __syncthreads();
+        inv_round<LB, LB - 8, 4, true>(b, cache, w + 2 * N, w + 3 * N, q, logN, cur.blk);
+        __syncthreads();
+        inv_round<LB, LB - 4, 4, true>(b, cache, w + 2 * N, w + 3 * N, q, logN, cur.blk);
+        __syncthreads();
+        if (logN == LB)
+            store_block<LB, true>(b, cur.g, q, P.ninv, P.ninv_sh);
+        else
+            store_block<LB, false>(b, cur.g, q, 0, 0);
+        __syncthreads();
+        cur = nxt;
+    }
 }
 
 // Two outermost forward stages for N = 4 * 2^LB: element j, j+N/4, j+N/2, j+3N/4.
@@ -537,20 +628,32 @@ __global__ void k_ntt_inv_outer2(DevCtx cx, NttJobs jobs) {
     }
 }
 
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
 template <int LB>
 void launch_block(bool fwd, const DevCtx& cx, const NttJobs& jobs, int sub, cudaStream_t s) {
-    const size_t smem = (smem_words<LB>() + 2 * kTwCache) * sizeof(u64);
+    const size_t smem = (2 * smem_words<LB>() + 2 * kTwCache) * sizeof(u64);
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(k_ntt_fwd<LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_ntt_inv<LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
-    dim3 grid(jobs.count, sub);
+    const u32 items = jobs.count * (u32)sub;
+    const u32 grid = std::min<u32>(items, (u32)sm_count());
     if (fwd)
-        k_ntt_fwd<LB><<<grid, (1 << LB) / kElems, smem, s>>>(cx, jobs);
+        k_ntt_fwd<LB><<<grid, (1 << LB) / kElems, smem, s>>>(cx, jobs, sub);
     else
-        k_ntt_inv<LB><<<grid, (1 << LB) / kElems, smem, s>>>(cx, jobs);
+        k_ntt_inv<LB><<<grid, (1 << LB) / kElems, smem, s>>>(cx, jobs, sub);
 }
 
 }  // namespace
