@@ -242,11 +242,15 @@ __global__ void k_modup_lift(DevCtx cx, u32 n, const u64* C, size_t c_stride,
                         v = x[r];
                     } else {
                         const u64 qr = dp->pr[r].q;
-                        v = 0;
-                        for (u32 a = 0; a < A; ++a) {
-                            const u32 i = dg * A + a;
-                            const u64 yl = centred_lift(y[a], dp->pr[i].q, qr);
-                            v = add_mod(v, shoup_mul(yl, dp->dg_hat[i][r], dp->dg_hat_sh[i][r], qr), qr);
+                        if (A == 1) {
+                            v = centred_lift(y[0], dp->pr[dg].q, qr);  // (Q_d/q_i) = 1
+                        } else {
+                            Acc s;
+                            for (u32 a = 0; a < A; ++a) {
+                                const u32 i = dg * A + a;
+                                s.mac(centred_lift(y[a], dp->pr[i].q, qr), dp->dg_hat[i][r]);
+                            }
+                            v = reduce_acc(s, dp->pr[r]);
                         }
                     }
                     d[((size_t)dg * R + r) * N + j] = v;
@@ -257,40 +261,75 @@ __global__ void k_modup_lift(DevCtx cx, u32 n, const u64* C, size_t c_stride,
 }
 
 // acc[c][r] = sum_dg D[dg][r][galois_src(k)] * key[dg][c][r][k]  ([n][2][R][N])
+// Items are grouped by Galois key (the engine sorts rotations by element): a
+// block serves up to kKeyReuse consecutive items and reads each key element
+// once for all items of the group that share it.
+constexpr int kKeyReuse = 4;
 __global__ void k_ks_inner(DevCtx cx, u32 n, const u64* const* D,
                            const u64* const* key, const u32* g, u64* const* acc) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, R = dp->R, dnum = dp->dnum, logN = dp->logN;
-    ITEM_LOOP {
-        const u64* d = D[item];
-        const u64* k = key[item];
-        u64* a = acc[item];
-        const u32 ge = g[item];
+    for (u32 grp = blockIdx.y; grp * kKeyReuse < n; grp += gridDim.y) {
+        const u32 i0 = grp * kKeyReuse;
+        const u32 cnt = min((u32)kKeyReuse, n - i0);
+        const u64* k = key[i0];
+        const u32 ge = g[i0];
+        u32 same = 1;  // leading items that share key and element with i0
+        while (same < cnt && key[i0 + same] == k && g[i0 + same] == ge) ++same;
         COEF_LOOP {
             const u32 src = ge == 1 ? j : galois_src(j, ge, logN);
             for (u32 r = 0; r < R; ++r) {
                 const Prime& P = dp->pr[r];
-                // 128-bit lazy accumulation, one reduction per output (dnum <= 4)
-                Acc a0, a1;
+                u64 k0[4], k1[4];
                 for (u32 dg = 0; dg < dnum; ++dg) {
-                    const u64 x = d[((size_t)dg * R + r) * N + src];
-                    a0.mac(x, __ldg(k + (((size_t)dg * 2 + 0) * R + r) * N + j));
-                    a1.mac(x, __ldg(k + (((size_t)dg * 2 + 1) * R + r) * N + j));
+                    k0[dg] = __ldg(k + (((size_t)dg * 2 + 0) * R + r) * N + j);
+                    k1[dg] = __ldg(k + (((size_t)dg * 2 + 1) * R + r) * N + j);
                 }
-                a[(size_t)r * N + j] = reduce_acc(a0, P);
-                a[((size_t)R + r) * N + j] = reduce_acc(a1, P);
+                for (u32 u = 0; u < same; ++u) {
+                    const u64* d = D[i0 + u];
+                    Acc a0, a1;  // 128-bit lazy accumulation, one reduction per output
+                    for (u32 dg = 0; dg < dnum; ++dg) {
+                        const u64 x = d[((size_t)dg * R + r) * N + src];
+                        a0.mac(x, k0[dg]);
+                        a1.mac(x, k1[dg]);
+                    }
+                    u64* a = acc[i0 + u];
+                    a[(size_t)r * N + j] = reduce_acc(a0, P);
+                    a[((size_t)R + r) * N + j] = reduce_acc(a1, P);
+                }
+            }
+            for (u32 u = same; u < cnt; ++u) {  // rest of the group: own key
+                const u64* kk = key[i0 + u];
+                const u32 gu = g[i0 + u];
+                const u32 su = gu == 1 ? j : galois_src(j, gu, logN);
+                const u64* d = D[i0 + u];
+                u64* a = acc[i0 + u];
+                for (u32 r = 0; r < R; ++r) {
+                    Acc a0, a1;
+                    for (u32 dg = 0; dg < dnum; ++dg) {
+                        const u64 x = d[((size_t)dg * R + r) * N + su];
+                        a0.mac(x, __ldg(kk + (((size_t)dg * 2 + 0) * R + r) * N + j));
+                        a1.mac(x, __ldg(kk + (((size_t)dg * 2 + 1) * R + r) * N + j));
+                    }
+                    a[(size_t)r * N + j] = reduce_acc(a0, dp->pr[r]);
+                    a[((size_t)R + r) * N + j] = reduce_acc(a1, dp->pr[r]);
+                }
             }
         }
     }
 }
 
 // ModDown correction: V[c][i] = sum_k centred([w_k (P/p_k)^-1]_{p_k}) (P/p_k) mod q_i
-__global__ void k_moddown_conv(DevCtx cx, u32 n, const u64* const* acc, u64* V) {
+// V[c][i] = ecoef[c][i] - P^-1 conv[c][i]  (coefficient domain; ecoef optional)
+// so that NTT(V) + P^-1 acc = (acc - NTT(conv)) P^-1 + NTT(ecoef) exactly (the NTT
+// is linear mod q_i): relinearisation adds e0, e1 without transforming them apart.
+__global__ void k_moddown_conv(DevCtx cx, u32 n, const u64* const* acc, const u64* const* ecoef, u64* V) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = dp->L, K = dp->K, R = dp->R;
     ITEM_LOOP {
         const u32 c = blockIdx.z;
         const u64* a = acc[item] + (size_t)c * R * N;
+        const u64* ec = ecoef ? ecoef[item] + (size_t)c * L * N : nullptr;
         u64* v = V + ((size_t)item * 2 + c) * L * N;
         COEF_LOOP {
             u64 z[kMaxK];
@@ -300,39 +339,40 @@ __global__ void k_moddown_conv(DevCtx cx, u32 n, const u64* const* acc, u64* V) 
             }
             for (u32 i = 0; i < L; ++i) {
                 const u64 q = dp->pr[i].q;
-                u64 s = 0;
-                for (u32 k = 0; k < K; ++k) {
-                    const u64 zl = centred_lift(z[k], dp->pr[L + k].q, q);
-                    s = add_mod(s, shoup_mul(zl, dp->phat_mod_q[k][i], dp->phat_mod_q_sh[k][i], q), q);
+                u64 conv;
+                if (K == 1) {  // P/p_0 = 1: the conversion is the centred lift itself
+                    conv = centred_lift(z[0], dp->pr[L].q, q);
+                } else {
+                    Acc s;
+                    for (u32 k = 0; k < K; ++k) s.mac(centred_lift(z[k], dp->pr[L + k].q, q), dp->phat_mod_q[k][i]);
+                    conv = reduce_acc(s, dp->pr[i]);
                 }
-                v[(size_t)i * N + j] = s;
+                const u64 scaled = shoup_mul(conv, dp->P_inv_q[i], dp->P_inv_q_sh[i], q);
+                v[(size_t)i * N + j] = sub_mod(ec ? ec[(size_t)i * N + j] : 0, scaled, q);
             }
         }
     }
 }
 
-// out0 = (acc0 - V0) P^-1 + add0[galois_src]; out1 = (acc1 - V1) P^-1 (+ add1)
-__global__ void k_ks_finish(DevCtx cx, u32 n, const u64* const* acc,
-                            const u64* V, const u64* const* add0, const u32* g0,
-                            const u64* const* add1, u64* const* out) {
+// out_c = NTT(V_c) + P^-1 acc_c  (+ addn[galois_src] for c = 0)
+__global__ void k_ks_finish(DevCtx cx, u32 n, const u64* const* acc, const u64* V, const u64* const* addn,
+                            const u32* g, u64* const* out) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = dp->L, R = dp->R, logN = dp->logN;
     ITEM_LOOP {
         const u64* a = acc[item];
         const u64* v = V + (size_t)item * 2 * L * N;
-        const u64* x0 = add0[item];
-        const u64* x1 = add1 ? add1[item] : nullptr;
-        const u32 ge = g0[item];
+        const u64* x0 = addn ? addn[item] : nullptr;
+        const u32 ge = g[item];
         u64* o = out[item];
         COEF_LOOP {
             const u32 src = ge == 1 ? j : galois_src(j, ge, logN);
             for (u32 i = 0; i < L; ++i) {
                 const u64 q = dp->pr[i].q;
                 const u64 pi = dp->P_inv_q[i], pis = dp->P_inv_q_sh[i];
-                u64 r0 = shoup_mul(sub_mod(a[(size_t)i * N + j], v[(size_t)i * N + j], q), pi, pis, q);
-                u64 r1 = shoup_mul(sub_mod(a[((size_t)R + i) * N + j], v[((size_t)L + i) * N + j], q), pi, pis, q);
-                r0 = add_mod(r0, x0[(size_t)i * N + src], q);
-                if (x1) r1 = add_mod(r1, x1[(size_t)i * N + j], q);
+                u64 r0 = add_mod(v[(size_t)i * N + j], shoup_mul(a[(size_t)i * N + j], pi, pis, q), q);
+                const u64 r1 = add_mod(v[((size_t)L + i) * N + j], shoup_mul(a[((size_t)R + i) * N + j], pi, pis, q), q);
+                if (x0) r0 = add_mod(r0, x0[(size_t)i * N + src], q);
                 o[(size_t)i * N + j] = r0;
                 o[((size_t)L + i) * N + j] = r1;
             }
@@ -358,11 +398,11 @@ __global__ void k_q_to_b(DevCtx cx, u32 n, const u64* X, u64* XB) {
             }
             const u64 v = fx_round(s);
             for (u32 k = 0; k < nB; ++k) {
-                const u64 b = dp->pr[L + K + k].q;
-                u64 acc = 0;
-                for (u32 i = 0; i < L; ++i)
-                    acc = add_mod(acc, shoup_mul(y[i], dp->qhat_mod_b[i][k], dp->qhat_mod_b_sh[i][k], b), b);
-                xb[(size_t)k * N + j] = sub_mod(acc, shoup_mul(v, dp->Q_mod_b[k], dp->Q_mod_b_sh[k], b), b);
+                // sum_i y_i (Q/q_i) - v Q  (mod b_k), one reduction
+                Acc a;
+                for (u32 i = 0; i < L; ++i) a.mac(y[i], dp->qhat_mod_b[i][k]);
+                a.mac(v, dp->neg_Q_mod_b[k]);
+                xb[(size_t)k * N + j] = reduce_acc(a, dp->pr[L + K + k]);
             }
         }
     }
@@ -418,22 +458,21 @@ __global__ void k_scale_round(DevCtx cx, u32 n, const u64* T, u64* E) {
             Acc128 s2{0, 0};
             for (u32 k = 0; k < nB; ++k) {
                 const u64 b = dp->pr[L + K + k].q;
-                Acc rra;
-                rra.lo = rr;  // rr < L * 2^60: one Barrett step instead of a 64-bit division
-                u64 acc = reduce_acc(rra, dp->pr[L + K + k]);
-                for (u32 i = 0; i < L; ++i)
-                    acc = add_mod(acc, shoup_mul(a[i], dp->W[i][k], dp->W_sh[i][k], b), b);
-                acc = add_mod(acc, shoup_mul(t[(size_t)(L + k) * N + j], dp->T[k], dp->T_sh[k], b), b);
-                cb[k] = shoup_mul(acc, dp->bhat_inv[k], dp->bhat_inv_sh[k], b);
+                // rr + sum_i a_i floor(tB/q_i) + x_b [t/Q]  (mod b_k), one reduction
+                Acc acc;
+                acc.lo = rr;  // rr < L * 2^60
+                for (u32 i = 0; i < L; ++i) acc.mac(a[i], dp->W[i][k]);
+                acc.mac(t[(size_t)(L + k) * N + j], dp->T[k]);
+                cb[k] = shoup_mul(reduce_acc(acc, dp->pr[L + K + k]), dp->bhat_inv[k], dp->bhat_inv_sh[k], b);
                 fx_add(s2, cb[k], dp->one_over_b[k]);
             }
             const u64 v = fx_round(s2);
             for (u32 i = 0; i < L; ++i) {
-                const u64 q = dp->pr[i].q;
-                u64 acc = 0;
-                for (u32 k = 0; k < nB; ++k)
-                    acc = add_mod(acc, shoup_mul(cb[k], dp->bhat_mod_q[k][i], dp->bhat_mod_q_sh[k][i], q), q);
-                e[(size_t)i * N + j] = sub_mod(acc, shoup_mul(v, dp->B_mod_q[i], dp->B_mod_q_sh[i], q), q);
+                // sum_k c_k (B/b_k) - v B  (mod q_i), one reduction
+                Acc acc;
+                for (u32 k = 0; k < nB; ++k) acc.mac(cb[k], dp->bhat_mod_q[k][i]);
+                acc.mac(v, dp->neg_B_mod_q[i]);
+                e[(size_t)i * N + j] = reduce_acc(acc, dp->pr[i]);
             }
         }
     }
@@ -895,7 +934,7 @@ void Context::inner_product(int n, const u64* const* digits, const u64* const* k
     std::vector<const u64*> vd(digits, digits + n), vk(keys, keys + n);
     std::vector<u32> vg(g, g + n);
     std::vector<u64*> va(acc, acc + n);
-    k_ks_inner<<<grid_of(hp_.N, n), kThreads, 0, stream_>>>(cx_, n, upload(vd), upload(vk), upload(vg),
+    k_ks_inner<<<grid_of(hp_.N, (n + kKeyReuse - 1) / kKeyReuse), kThreads, 0, stream_>>>(cx_, n, upload(vd), upload(vk), upload(vg),
                                                            upload(va)); ++launches_;
     HGM_CUDA(cudaGetLastError());
 }
@@ -938,18 +977,11 @@ void Context::key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, c
         HGM_CUDA(cudaGetLastError());
         return;
     }
-    // unfused (N = 32768): conversion pass, NTT, finishing pass; ecoef was
-    // already transformed by the caller and is added as NTT-domain e0 / e1
+    // conversion pass (V = ecoef - P^-1 conv), NTT, finishing pass
     u64* V = alloc((size_t)n * 2 * L * N);
-    k_moddown_conv<<<grid_of(N, n, 2), kThreads, 0, stream_>>>(cx_, n, dacc, V); ++launches_;
+    k_moddown_conv<<<grid_of(N, n, 2), kThreads, 0, stream_>>>(cx_, n, dacc, dec, V); ++launches_;
     ntt(true, jobs_contig(V, n * 2 * L, 0, L));
-    std::vector<const u64*> v0(n), v1(n);
-    for (int i = 0; i < n; ++i) {
-        v0[i] = ecoef ? ecoef[i] : addn[i];
-        v1[i] = ecoef ? ecoef[i] + (size_t)L * N : nullptr;
-    }
-    k_ks_finish<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, dacc, V, upload(v0), upload(vg),
-                                                        ecoef ? upload(v1) : nullptr, upload(vo)); ++launches_;
+    k_ks_finish<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, dacc, V, dadd, upload(vg), upload(vo)); ++launches_;
     release(V);
     HGM_CUDA(cudaGetLastError());
 }
@@ -1029,15 +1061,6 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
     } else {
         k_modup_lift<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, E + 2 * LN, 3 * LN, Dg); ++launches_;
         ntt(true, jobs_contig(Dg, n * dnum * R, 0, R));
-        NttJobs ej;  // e0, e1 to the NTT domain (the fused ModDown adds them in coefficient form)
-        std::vector<u64*> limbs((size_t)n * 2 * L);
-        for (int i = 0; i < n; ++i)
-            for (u32 w = 0; w < 2 * L; ++w) limbs[(size_t)i * 2 * L + w] = E + (size_t)i * 3 * LN + (size_t)w * N;
-        ej.ptrs = upload(limbs);
-        ej.count = n * 2 * L;
-        ej.period = L;
-        for (u32 i = 0; i < L; ++i) ej.prime[i] = (unsigned char)i;
-        ntt(true, ej);
     }
     u64* A = alloc((size_t)n * 2 * R * N);
     std::vector<const u64*> digits(n), keys(n), ecoef(n);

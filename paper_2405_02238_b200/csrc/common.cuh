@@ -63,6 +63,7 @@ struct DevParams {
     Frac one_over_q[kMaxL];
     u64 qhat_mod_b[kMaxL][kMaxB], qhat_mod_b_sh[kMaxL][kMaxB];
     u64 Q_mod_b[kMaxB], Q_mod_b_sh[kMaxB];
+    u64 neg_Q_mod_b[kMaxB];  // b_j - (Q mod b_j)
     // scale-and-round Q++B -> B
     u64 dhat_inv[kMaxL], dhat_inv_sh[kMaxL];
     u64 W[kMaxL][kMaxB], W_sh[kMaxL][kMaxB];
@@ -73,6 +74,7 @@ struct DevParams {
     Frac one_over_b[kMaxB];
     u64 bhat_mod_q[kMaxB][kMaxL], bhat_mod_q_sh[kMaxB][kMaxL];
     u64 B_mod_q[kMaxL], B_mod_q_sh[kMaxL];
+    u64 neg_B_mod_q[kMaxL];  // q_i - (B mod q_i)
     // key switching (digit d holds primes d*alpha .. d*alpha+alpha-1)
     u64 dg_hat_inv[kMaxL], dg_hat_inv_sh[kMaxL];               // by prime i
     u64 dg_hat[kMaxL][kMaxR], dg_hat_sh[kMaxL][kMaxR];         // [i][r] (Q_d/q_i) mod r
@@ -141,8 +143,8 @@ HD u64 mul_mod(u64 a, u64 b, const Prime& p) {
     if (r >= p.q) r -= p.q;
     return r;
 }
-// 128-bit lazy accumulator of products of residues (sum of <= 4 products of
-// values < q < 2^60), reduced once: x = hi:lo < 2^(2s+2).
+// 128-bit lazy accumulator of products of residues, reduced once; valid while
+// the sum stays below 2^(s+62) (4 products of 60-bit residues, 9 of 55-bit).
 struct Acc {
     u64 lo = 0, hi = 0;
     HD void mac(u64 a, u64 b) {
@@ -151,8 +153,8 @@ struct Acc {
         hi += ph + (lo < pl);
     }
 };
-// Shifted Barrett on x < 2^(2s+2) (s = bit length of q <= 60): the quotient
-// estimate is low by at most 2, so two corrections give [0, q).
+// Shifted Barrett on x < 2^(s+62) (s = bit length of q <= 60): x >> (s-2)
+// fits 64 bits, the quotient estimate is low by at most 2, two corrections.
 HD u64 reduce_acc(const Acc& a, const Prime& p) {
     const u64 x = (a.hi << (66 - p.s)) | (a.lo >> (p.s - 2));
     const u64 qh = mulhi64(x, p.mu);

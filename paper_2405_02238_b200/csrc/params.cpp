@@ -186,6 +186,7 @@ HostParams make_params(int id, u64 seed) {
         }
         d.B_mod_q[i] = Bq;
         d.B_mod_q_sh[i] = shoup_of(Bq, q);
+        d.neg_B_mod_q[i] = (q - Bq) % q;
         const u64 Pq = prod_mod(Ps, q);
         d.P_mod_q[i] = Pq;
         d.P_mod_q_sh[i] = shoup_of(Pq, q);
@@ -196,6 +197,7 @@ HostParams make_params(int id, u64 seed) {
         const u64 b = bv(j);
         d.Q_mod_b[j] = prod_mod(Qs, b);
         d.Q_mod_b_sh[j] = shoup_of(d.Q_mod_b[j], b);
+        d.neg_Q_mod_b[j] = (b - d.Q_mod_b[j]) % b;
         d.T[j] = mulmod(kT % b, invmod(d.Q_mod_b[j], b), b);
         d.T_sh[j] = shoup_of(d.T[j], b);
         d.bhat_inv[j] = invmod(prod_mod(without(Bs, j), b), b);
