@@ -41,3 +41,32 @@ def gather_ciphertexts(dist, local, count: int, words: int, total: int, world: i
     if rank != 0:
         return None
     return [outs[r][: shard(r, world, total)[1] * words] for r in range(world)]
+
+
+def row_blocks(m: int, parts: int) -> List[Tuple[int, int]]:
+    """Row-block decomposition of an m-row product into `parts` contiguous
+    blocks (config 5: 128 rows -> 8 blocks of 16).  Every block
+    A_r (rows x l) . B is an independent product; C is their row concatenation."""
+    return [shard(r, parts, m) for r in range(parts)]
+
+
+def sharded_matmul(ctx, A, B, parts: int, algo: int = 1, rank: int = 0, world: int = 1, counter0: int = 0):
+    """Runs this rank's share of the row blocks of A.B as one lockstep batch on
+    its GPU (blocks of equal height share one compiled program).  Returns
+    {block index: C block} for the blocks this rank owns."""
+    import numpy as np
+
+    blocks = row_blocks(A.shape[0], parts)
+    first, count = shard(rank, world, parts)
+    mine = list(range(first, first + count))
+    out = {}
+    by_height = {}
+    for bi in mine:
+        by_height.setdefault(blocks[bi][1], []).append(bi)
+    for height, ids in by_height.items():
+        As = np.stack([A[blocks[bi][0]: blocks[bi][0] + height] for bi in ids])
+        Bs = np.stack([B for _ in ids])
+        C, _ = ctx.matmul_batch(As, Bs, algo=algo, counter0=counter0 + ids[0] * 2)
+        for k, bi in enumerate(ids):
+            out[bi] = C[k]
+    return out

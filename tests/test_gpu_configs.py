@@ -67,3 +67,20 @@ def test_n32768_ops_bit_exact(gpu_factory, oracle_factory):
     m = g.he_mult(ca, cb)
     assert np.array_equal(g.export(m), o.mult(oa, ob))
     assert np.array_equal(g.decrypt(m), (a * b) % T)
+
+
+def test_cfg5_row_block_sharding(gpu_factory):
+    """Config 5 split into 8 independent 16x128x128 HEGMM-Enhanced products
+    (the per-GPU unit of the 8-GPU decomposition), run as one batch here."""
+    import paper_2405_02238_b200 as hb
+    from paper_2405_02238_b200.dist import row_blocks, sharded_matmul
+
+    g = GOLD["configs"]["cfg5"]
+    A, B = splitmix_matrices(GOLD["seed"], 0, g["m"], g["l"], g["n"], g["lo"], g["hi"])
+    ctx = gpu_factory(1)
+    st, facts = hb.program_info(1, 16, 128, 128, ctx.slot_count, ctx.N)
+    assert st[3] == 16 and facts["segment"] == 16384  # p = 16 CC-mults, fits N = 32768
+    parts = sharded_matmul(ctx, A, B, 8, algo=1)
+    C = np.concatenate([parts[i] for i in range(8)])
+    assert sha(C) == g["algos"]["enhanced"]["C_sha256"]
+    assert [c for _, c in row_blocks(128, 8)] == [16] * 8
