@@ -110,18 +110,32 @@ int hgm_set_phase(hgm_ctx* ctx, int phase);
 int hgm_phase(const hgm_ctx* ctx);
 
 /* Batched HEGMM: `count` independent products C_i = A_i B_i (A_i m x l, B_i
- * l x n, row-major int64) through basic_mm (algo 0) or enhanced_mm (algo 1),
- * order -1 auto / 0 column-major / 1 row-major.  Inputs and outputs are host
- * buffers; outputs canonical mod t.  Instance i encrypts with counters
- * counter0 + i * E, E = encryptions per instance (3 basic, 2 enhanced).
- * stats (optional) receives one instance's counts (identical for all). */
-int hgm_matmul_batch(hgm_ctx* ctx, int algo, int order, size_t m, size_t l, size_t n,
+ * l x n, row-major int64) through basic_mm (algo 0), enhanced_mm (algo 1) or
+ * square_pad_mm (algo 2) (algorithms.hpp:59-71); order -1 auto / 0 column-major /
+ * 1 row-major; flags bit 0 = MultiplyOptions::encrypted_client_transforms
+ * (algorithms.hpp:21).  Inputs and outputs are host buffers; outputs canonical
+ * mod t.  Instance i encrypts with counters counter0 + i * E, E = encryptions
+ * per instance (3 basic, 2 enhanced).  stats (optional) receives one
+ * instance's counts (identical for all). */
+#define HGM_FLAG_ENCRYPTED_CLIENT_TRANSFORMS 1
+int hgm_matmul_batch(hgm_ctx* ctx, int algo, int order, int flags, size_t m, size_t l, size_t n,
                      size_t count, const int64_t* A, const int64_t* B, int64_t* C,
                      uint64_t counter0, uint64_t* stats);
 /* same, also exporting every instance's final (pre-decrypt) ciphertext */
-int hgm_matmul_batch_export(hgm_ctx* ctx, int algo, int order, size_t m, size_t l, size_t n,
+int hgm_matmul_batch_export(hgm_ctx* ctx, int algo, int order, int flags, size_t m, size_t l, size_t n,
                             size_t count, const int64_t* A, const int64_t* B, int64_t* C,
                             uint64_t counter0, uint64_t* final_words);
+/* blocked_mm (algorithms.hpp:97-98, algorithms.cpp:434-498): the product tiled by
+ * the row / mid / col partitions; every block product runs (the independent
+ * ones in lockstep batches) with `algo`, falling back from enhanced (1) to
+ * basic (0) when a block's working set exceeds the slots, and the decrypted
+ * blocks are accumulated mod t.  log (optional, 4 int32 per block in the
+ * reference loop order bi, bj, bk): algo used, fell_back, block m, l.
+ * Block b encrypts with counters counter0 + (encryptions of blocks before b). */
+int hgm_blocked_mm(hgm_ctx* ctx, int algo, size_t m, size_t l, size_t n, const size_t* row_blocks,
+                   size_t n_row, const size_t* mid_blocks, size_t n_mid, const size_t* col_blocks,
+                   size_t n_col, const int64_t* A, const int64_t* B, int64_t* C, uint64_t counter0,
+                   int32_t* log);
 
 /* The same pipeline split at the reference's phase boundaries
  * (algorithms.cpp:216-247: Client encrypt / Cloud loop / Client decrypt):
@@ -130,8 +144,9 @@ int hgm_matmul_batch_export(hgm_ctx* ctx, int algo, int order, size_t m, size_t 
  *   hgm_batch_output   device pointer of instance i's result ciphertext (for gathers)
  *   hgm_batch_decrypt  decrypts and unpacks every result into host C */
 typedef struct hgm_batch hgm_batch;
-int hgm_batch_encrypt(hgm_ctx* ctx, int algo, int order, size_t m, size_t l, size_t n, size_t count,
-                      const int64_t* A, const int64_t* B, uint64_t counter0, hgm_batch** out);
+int hgm_batch_encrypt(hgm_ctx* ctx, int algo, int order, int flags, size_t m, size_t l, size_t n,
+                      size_t count, const int64_t* A, const int64_t* B, uint64_t counter0,
+                      hgm_batch** out);
 int hgm_batch_cloud(hgm_ctx* ctx, hgm_batch* b, float* device_ms);
 uint64_t* hgm_batch_output(hgm_batch* b, size_t i);
 int hgm_batch_decrypt(hgm_ctx* ctx, hgm_batch* b, int64_t* C);
@@ -141,14 +156,14 @@ void hgm_batch_free(hgm_batch* b);
 /* Program facts of a product shape (no GPU needed): stats[12] as hgm_stats,
  * facts[0]=segment [1]=encryptions [2]=rotations after CSE [3]=masked sums
  * [4]=CC-mults [5]=levels [6]=flatten order used. */
-int hgm_program_info(int algo, int order, size_t m, size_t l, size_t n, size_t slots, uint32_t N,
-                     uint64_t* stats, uint64_t* facts);
+int hgm_program_info(int algo, int order, int flags, size_t m, size_t l, size_t n, size_t slots,
+                     uint32_t N, uint64_t* stats, uint64_t* facts);
 /* Op stream of a product shape in call order (no GPU needed), same layout as
  * the reference trace: hdr[3*i] = kind (0 enc 1 dec 2 add 3 mult 4 cmult 5 rot),
  * hdr[3*i+1] = rotation offset / segment, hdr[3*i+2] = data length; data = the
  * cmult masks concatenated.  Returns the op count (or -error). */
-long hgm_program_stream(int algo, int order, size_t m, size_t l, size_t n, size_t slots, uint32_t N,
-                        int64_t* hdr, size_t hdr_cap, int64_t* data, size_t data_cap,
+long hgm_program_stream(int algo, int order, int flags, size_t m, size_t l, size_t n, size_t slots,
+                        uint32_t N, int64_t* hdr, size_t hdr_cap, int64_t* data, size_t data_cap,
                         size_t* data_len);
 
 /* Diagonal plan introspection (no GPU): kind 0 = eps_k (a=m, b=l, c=n),

@@ -167,6 +167,13 @@ class RefLib:
             L.ref_trace.argtypes = [_int, _int, _vp, _sz, _sz, _vp, _sz, _sz, _vp, _sz, _vp, _sz, _vp]
             L.ref_mm_oracle.restype = ctypes.c_long
             L.ref_mm_oracle.argtypes = [_int, _u64, _u64, _int, _int, _vp, _sz, _sz, _vp, _sz, _vp, _vp, _vp]
+            L.ref_mm2.restype = _int
+            L.ref_mm2.argtypes = [_int, _int, _int, _vp, _sz, _sz, _vp, _sz, _sz, _i64, _vp, _vp]
+            L.ref_trace2.restype = ctypes.c_long
+            L.ref_trace2.argtypes = [_int, _int, _int, _vp, _sz, _sz, _vp, _sz, _sz, _vp, _sz, _vp, _sz, _vp]
+            L.ref_blocked.restype = _int
+            L.ref_blocked.argtypes = [_int, _vp, _sz, _vp, _sz, _vp, _sz, _vp, _sz, _sz, _vp, _sz, _sz, _i64, _vp,
+                                      _vp]
             L.ref_oracle_session_create.restype = _vp
             L.ref_oracle_session_create.argtypes = [_int, _u64]
             L.ref_oracle_session_destroy.argtypes = [_vp]
@@ -191,6 +198,51 @@ class RefLib:
         if rc != 0:
             raise OracleError(f"rc={rc}: {cls._err()}")
         return C, st
+
+    @classmethod
+    def mm2(cls, A, B, algo="basic", order=-1, flags=0, slots=4096, modulus=65537):
+        A = np.ascontiguousarray(A, dtype=np.int64)
+        B = np.ascontiguousarray(B, dtype=np.int64)
+        m, l = A.shape
+        n = B.shape[1]
+        C = np.zeros((m, n), dtype=np.int64)
+        st = np.zeros(13, dtype=np.uint64)
+        rc = cls.lib().ref_mm2(ALGO[algo], order, flags, _p(A), m, l, _p(B), n, slots, modulus, _p(C), _p(st))
+        if rc != 0:
+            raise OracleError(f"rc={rc}: {cls._err()}")
+        return C, st
+
+    @classmethod
+    def trace2(cls, A, B, algo="basic", order=-1, flags=0, slots=4096):
+        A = np.ascontiguousarray(A, dtype=np.int64)
+        B = np.ascontiguousarray(B, dtype=np.int64)
+        m, l = A.shape
+        n = B.shape[1]
+        dl = ctypes.c_size_t()
+        cnt = cls.lib().ref_trace2(ALGO[algo], order, flags, _p(A), m, l, _p(B), n, slots, None, 0, None, 0,
+                                   ctypes.byref(dl))
+        if cnt < 0:
+            raise OracleError(cls._err())
+        hdr = np.zeros(3 * cnt, dtype=np.int64)
+        data = np.zeros(max(1, dl.value), dtype=np.int64)
+        cls.lib().ref_trace2(ALGO[algo], order, flags, _p(A), m, l, _p(B), n, slots, _p(hdr), hdr.size, _p(data),
+                             data.size, ctypes.byref(dl))
+        return hdr.reshape(-1, 3), data[:dl.value]
+
+    @classmethod
+    def blocked(cls, A, B, rows, mids, cols, algo="enhanced", slots=4096, modulus=65537):
+        A = np.ascontiguousarray(A, dtype=np.int64)
+        B = np.ascontiguousarray(B, dtype=np.int64)
+        m, l = A.shape
+        n = B.shape[1]
+        r, md, c = (np.ascontiguousarray(x, dtype=np.uint64) for x in (rows, mids, cols))
+        C = np.zeros((m, n), dtype=np.int64)
+        log = np.zeros((r.size * md.size * c.size, 4), dtype=np.int32)
+        rc = cls.lib().ref_blocked(ALGO[algo], _p(r), r.size, _p(md), md.size, _p(c), c.size, _p(A), m, l, _p(B),
+                                   n, slots, modulus, _p(C), _p(log))
+        if rc != 0:
+            raise OracleError(f"rc={rc}: {cls._err()}")
+        return C, log
 
     @classmethod
     def naive_mod(cls, A, B, q=65537):

@@ -217,8 +217,9 @@ class TraceBackend final : public Backend {
     SlotBackend inner_;
 };
 
-Matrix run(int algo, int order, const Matrix& a, const Matrix& b, Backend& be) {
+Matrix run(int algo, int order, const Matrix& a, const Matrix& b, Backend& be, int flags = 0) {
     MultiplyOptions opts;
+    opts.encrypted_client_transforms = (flags & 1) != 0;
     if (order == 0) opts.order = FlattenOrder::ColumnMajor;
     if (order == 1) opts.order = FlattenOrder::RowMajor;
     switch (algo) {
@@ -264,6 +265,80 @@ int ref_mm(int algo, int order, const std::int64_t* A, std::size_t m, std::size_
         const Matrix c = run(algo, order, a, b, be);
         std::memcpy(C, c.data().data(), m * n * 8);
         put_stats(be, stats);
+        return 0;
+    } catch (const std::exception& e) {
+        return rc_of(e);
+    }
+}
+
+// Same with MultiplyOptions flags (bit 0: encrypted_client_transforms).
+int ref_mm2(int algo, int order, int flags, const std::int64_t* A, std::size_t m, std::size_t l,
+            const std::int64_t* B, std::size_t n, std::size_t slots, std::int64_t modulus, std::int64_t* C,
+            std::uint64_t* stats) {
+    try {
+        Matrix a(m, l, std::vector<value_t>(A, A + m * l));
+        Matrix b(l, n, std::vector<value_t>(B, B + l * n));
+        BackendConfig cfg{slots, modulus > 0 ? std::optional<value_t>(modulus) : std::nullopt};
+        SlotBackend be(cfg);
+        const Matrix c = run(algo, order, a, b, be, flags);
+        std::memcpy(C, c.data().data(), m * n * 8);
+        put_stats(be, stats);
+        return 0;
+    } catch (const std::exception& e) {
+        return rc_of(e);
+    }
+}
+
+long ref_trace2(int algo, int order, int flags, const std::int64_t* A, std::size_t m, std::size_t l,
+                const std::int64_t* B, std::size_t n, std::size_t slots, std::int64_t* hdr, std::size_t hdr_cap,
+                std::int64_t* data, std::size_t data_cap, std::size_t* data_len) {
+    try {
+        Matrix a(m, l, std::vector<value_t>(A, A + m * l));
+        Matrix b(l, n, std::vector<value_t>(B, B + l * n));
+        TraceBackend be(BackendConfig{slots, value_t{65537}});
+        run(algo, order, a, b, be, flags);
+        std::size_t dl = 0;
+        for (const auto& op : be.ops) dl += op.data.size();
+        if (data_len) *data_len = dl;
+        if (hdr) {
+            if (hdr_cap < be.ops.size() * 3 || data_cap < dl) return -5;
+            std::size_t off = 0;
+            for (std::size_t i = 0; i < be.ops.size(); ++i) {
+                hdr[3 * i] = be.ops[i].kind;
+                hdr[3 * i + 1] = be.ops[i].arg;
+                hdr[3 * i + 2] = (std::int64_t)be.ops[i].data.size();
+                std::memcpy(data + off, be.ops[i].data.data(), be.ops[i].data.size() * 8);
+                off += be.ops[i].data.size();
+            }
+        }
+        return (long)be.ops.size();
+    } catch (const std::exception& e) {
+        return -rc_of(e);
+    }
+}
+
+// Reference blocked_mm (algorithms.cpp:434-498) over SlotBackend; log: 4 ints per block
+int ref_blocked(int algo, const std::size_t* rows, std::size_t nr, const std::size_t* mids, std::size_t nm,
+                const std::size_t* cols, std::size_t nc, const std::int64_t* A, std::size_t m, std::size_t l,
+                const std::int64_t* B, std::size_t n, std::size_t slots, std::int64_t modulus, std::int64_t* C,
+                std::int32_t* log) {
+    try {
+        Matrix a(m, l, std::vector<value_t>(A, A + m * l));
+        Matrix b(l, n, std::vector<value_t>(B, B + l * n));
+        BlockPlan plan{std::vector<std::size_t>(rows, rows + nr), std::vector<std::size_t>(mids, mids + nm),
+                       std::vector<std::size_t>(cols, cols + nc)};
+        BackendConfig cfg{slots, modulus > 0 ? std::optional<value_t>(modulus) : std::nullopt};
+        SlotBackend be(cfg);
+        std::vector<BlockRun> runs;
+        const Algo al = algo == 0 ? Algo::Hegmm : algo == 1 ? Algo::HegmmEn : Algo::SquarePad;
+        const Matrix c = blocked_mm(a, b, plan, al, be, &runs);
+        std::memcpy(C, c.data().data(), m * n * 8);
+        for (std::size_t i = 0; log && i < runs.size(); ++i) {
+            log[4 * i] = runs[i].used == Algo::Hegmm ? 0 : runs[i].used == Algo::HegmmEn ? 1 : 2;
+            log[4 * i + 1] = runs[i].fell_back ? 1 : 0;
+            log[4 * i + 2] = (std::int32_t)runs[i].m;
+            log[4 * i + 3] = (std::int32_t)runs[i].l;
+        }
         return 0;
     } catch (const std::exception& e) {
         return rc_of(e);

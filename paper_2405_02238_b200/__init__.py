@@ -29,9 +29,10 @@ EXPORTS = (
     "hgm_matmul_batch", "hgm_matmul_batch_export", "hgm_bench_ntt", "hgm_device_sync",
     "hgm_test_ntt", "hgm_launch_count", "hgm_batch_encrypt", "hgm_batch_cloud", "hgm_batch_output",
     "hgm_batch_decrypt", "hgm_batch_decrypt_words", "hgm_batch_free", "hgm_program_info",
-    "hgm_program_stream", "hgm_plan_info",
+    "hgm_program_stream", "hgm_plan_info", "hgm_blocked_mm",
 )
-ALGOS = {"basic": 0, "enhanced": 1}
+FLAG_ENCRYPTED_CLIENT_TRANSFORMS = 1
+ALGOS = {"basic": 0, "enhanced": 1, "square_pad": 2}
 
 
 def plan_info(kind: int, k: int, a: int, b: int, c: int, order: int, segment: int):
@@ -44,25 +45,27 @@ def plan_info(kind: int, k: int, a: int, b: int, c: int, order: int, segment: in
     return off[:cnt].tolist(), w[:cnt].astype(int).tolist()
 
 
-def program_info(algo: int, m: int, l: int, n: int, slots: int = 4096, N: int = 8192, order: int = -1):
+def program_info(algo: int, m: int, l: int, n: int, slots: int = 4096, N: int = 8192, order: int = -1,
+                 flags: int = 0):
     """Op counts (stats[12]) and facts of a compiled HEGMM program (CPU only)."""
     st = np.zeros(12, dtype=np.uint64)
     facts = np.zeros(7, dtype=np.uint64)
-    _check(lib().hgm_program_info(algo, order, m, l, n, slots, N, _ptr(st), _ptr(facts)))
+    _check(lib().hgm_program_info(algo, order, flags, m, l, n, slots, N, _ptr(st), _ptr(facts)))
     keys = ("segment", "encryptions", "rotations", "masked_sums", "cc_mults", "levels", "order")
     return st, dict(zip(keys, (int(x) for x in facts)))
 
 
-def program_stream(algo: int, m: int, l: int, n: int, slots: int = 4096, N: int = 8192, order: int = -1):
+def program_stream(algo: int, m: int, l: int, n: int, slots: int = 4096, N: int = 8192, order: int = -1,
+                   flags: int = 0):
     """The recorded op stream (reference trace layout): (hdr[k,3], mask data)."""
     dl = ctypes.c_size_t()
-    cnt = lib().hgm_program_stream(algo, order, m, l, n, slots, N, None, 0, None, 0, ctypes.byref(dl))
+    cnt = lib().hgm_program_stream(algo, order, flags, m, l, n, slots, N, None, 0, None, 0, ctypes.byref(dl))
     if cnt < 0:
         _check(-cnt)
     hdr = np.zeros(3 * cnt, dtype=np.int64)
     data = np.zeros(max(1, dl.value), dtype=np.int64)
-    cnt2 = lib().hgm_program_stream(algo, order, m, l, n, slots, N, _ptr(hdr), hdr.size, _ptr(data), data.size,
-                                    ctypes.byref(dl))
+    cnt2 = lib().hgm_program_stream(algo, order, flags, m, l, n, slots, N, _ptr(hdr), hdr.size, _ptr(data),
+                                    data.size, ctypes.byref(dl))
     if cnt2 < 0:
         _check(-cnt2)
     return hdr.reshape(-1, 3), data[:dl.value]
@@ -72,7 +75,7 @@ class Batch:
     """Encrypted inputs of `count` instances resident in HBM (client phase done)."""
 
     def __init__(self, ctx: "Context", A: np.ndarray, B: np.ndarray, algo: int = 0, order: int = -1,
-                 counter0: int = 0):
+                 counter0: int = 0, flags: int = 0):
         A = _as_i64(A)
         B = _as_i64(B)
         if A.ndim == 2:
@@ -81,8 +84,8 @@ class Batch:
         self.count, self.m, self.l = A.shape
         self.n = B.shape[2]
         h = ctypes.c_void_p()
-        _check(lib().hgm_batch_encrypt(ctx._h, algo, order, self.m, self.l, self.n, self.count, _ptr(A),
-                                       _ptr(B), counter0, ctypes.byref(h)))
+        _check(lib().hgm_batch_encrypt(ctx._h, algo, order, flags, self.m, self.l, self.n, self.count,
+                                       _ptr(A), _ptr(B), counter0, ctypes.byref(h)))
         self._h = h.value
 
     def cloud(self) -> float:
@@ -171,21 +174,22 @@ def lib() -> ctypes.CDLL:
         "hgm_peak_live": (_sz, [_vp]),
         "hgm_set_phase": (_int, [_vp, _int]),
         "hgm_phase": (_int, [_vp]),
-        "hgm_matmul_batch": (_int, [_vp, _int, _int, _sz, _sz, _sz, _sz, _vp, _vp, _vp, _u64, _vp]),
-        "hgm_matmul_batch_export": (_int, [_vp, _int, _int, _sz, _sz, _sz, _sz, _vp, _vp, _vp, _u64, _vp]),
+        "hgm_matmul_batch": (_int, [_vp, _int, _int, _int, _sz, _sz, _sz, _sz, _vp, _vp, _vp, _u64, _vp]),
+        "hgm_matmul_batch_export": (_int, [_vp, _int, _int, _int, _sz, _sz, _sz, _sz, _vp, _vp, _vp, _u64, _vp]),
+        "hgm_blocked_mm": (_int, [_vp, _int, _sz, _sz, _sz, _vp, _sz, _vp, _sz, _vp, _sz, _vp, _vp, _vp, _u64, _vp]),
         "hgm_bench_ntt": (_int, [_vp, _int, _sz, _int, _vp]),
         "hgm_device_sync": (_int, [_vp]),
         "hgm_test_ntt": (_int, [_vp, _int, _int, _vp, _sz]),
         "hgm_launch_count": (_u64, [_vp]),
-        "hgm_batch_encrypt": (_int, [_vp, _int, _int, _sz, _sz, _sz, _sz, _vp, _vp, _u64, _vp]),
+        "hgm_batch_encrypt": (_int, [_vp, _int, _int, _int, _sz, _sz, _sz, _sz, _vp, _vp, _u64, _vp]),
         "hgm_batch_cloud": (_int, [_vp, _vp, _vp]),
         "hgm_batch_output": (_vp, [_vp, _sz]),
         "hgm_batch_decrypt": (_int, [_vp, _vp, _vp]),
         "hgm_batch_decrypt_words": (_int, [_vp, _vp, _sz, _sz, _vp]),
         "hgm_batch_free": (None, [_vp]),
-        "hgm_program_info": (_int, [_int, _int, _sz, _sz, _sz, _sz, ctypes.c_uint32, _vp, _vp]),
-        "hgm_program_stream": (ctypes.c_long, [_int, _int, _sz, _sz, _sz, _sz, ctypes.c_uint32, _vp, _sz,
-                                               _vp, _sz, _vp]),
+        "hgm_program_info": (_int, [_int, _int, _int, _sz, _sz, _sz, _sz, ctypes.c_uint32, _vp, _vp]),
+        "hgm_program_stream": (ctypes.c_long, [_int, _int, _int, _sz, _sz, _sz, _sz, ctypes.c_uint32, _vp,
+                                               _sz, _vp, _sz, _vp]),
         "hgm_plan_info": (ctypes.c_long, [_int, _sz, _sz, _sz, _sz, _int, _sz, _vp, _vp, _sz]),
     }
     for name, (res, args) in sig.items():
@@ -345,7 +349,7 @@ class Context:
         return Ciphertext(out.value, self)
 
     def matmul_batch(self, A: np.ndarray, B: np.ndarray, algo: int = 0, order: int = -1,
-                     counter0: int = 0, export: bool = False):
+                     counter0: int = 0, export: bool = False, flags: int = 0):
         """C_i = A_i B_i mod t for a batch (count, m, l) x (count, l, n)."""
         A = _as_i64(A)
         B = _as_i64(B)
@@ -358,13 +362,27 @@ class Context:
         C = np.zeros((cnt, m, n), dtype=np.int64)
         if export:
             words = np.zeros((cnt, self.ct_words), dtype=np.uint64)
-            _check(lib().hgm_matmul_batch_export(self._h, algo, order, m, l, n, cnt, _ptr(A), _ptr(B),
+            _check(lib().hgm_matmul_batch_export(self._h, algo, order, flags, m, l, n, cnt, _ptr(A), _ptr(B),
                                                  _ptr(C), counter0, _ptr(words)))
             return C, words
         stats = np.zeros(12, dtype=np.uint64)
-        _check(lib().hgm_matmul_batch(self._h, algo, order, m, l, n, cnt, _ptr(A), _ptr(B), _ptr(C),
+        _check(lib().hgm_matmul_batch(self._h, algo, order, flags, m, l, n, cnt, _ptr(A), _ptr(B), _ptr(C),
                                       counter0, _ptr(stats)))
         return C, stats
+
+    def blocked_mm(self, A: np.ndarray, B: np.ndarray, rows, mids, cols, algo: int = 1, counter0: int = 0):
+        """blocked_mm (algorithms.cpp:434-498): returns (C mod t, per-block log
+        rows of (algo used, fell_back, block m, block l))."""
+        A = _as_i64(A)
+        B = _as_i64(B)
+        m, l = A.shape
+        n = B.shape[1]
+        r, md, c = (np.ascontiguousarray(x, dtype=np.uint64) for x in (rows, mids, cols))
+        C = np.zeros((m, n), dtype=np.int64)
+        log = np.zeros((r.size * md.size * c.size, 4), dtype=np.int32)
+        _check(lib().hgm_blocked_mm(self._h, algo, m, l, n, _ptr(r), r.size, _ptr(md), md.size, _ptr(c), c.size,
+                                    _ptr(A), _ptr(B), _ptr(C), counter0, _ptr(log)))
+        return C, log
 
     def decrypt_words(self, words, segment: int) -> np.ndarray:
         """Decrypts ciphertexts held in a device buffer (a torch CUDA tensor, e.g.

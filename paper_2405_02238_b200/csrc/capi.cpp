@@ -9,6 +9,9 @@
 // ModUps.  Nodes still referenced by a pinned handle keep their ciphertext;
 // every other intermediate is recomputed on demand (all ops are deterministic).
 #include <atomic>
+#include <functional>
+#include <map>
+#include <tuple>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -439,52 +442,165 @@ int hgm_set_phase(hgm_ctx* c, int phase) {
 }
 int hgm_phase(const hgm_ctx* c) { return c->phase.load(); }
 
-static int matmul_batch_impl(hgm_ctx* c, int algo, int order, size_t m, size_t l, size_t n, size_t count,
-                             const int64_t* A, const int64_t* B, int64_t* C, uint64_t counter0,
-                             uint64_t* stats, uint64_t* final_words) {
+}  // extern "C"
+
+namespace {
+
+// Runs `count` instances of one compiled program in lockstep chunks: instance k
+// reads A_k / B_k, encrypts with counters base(k) + s, and writes C_k (and its
+// final ciphertext words when requested).
+void run_instances(Context& ctx, const MatmulProgram& prog, size_t count,
+                   const std::function<const i64*(size_t)>& a_of, const std::function<const i64*(size_t)>& b_of,
+                   const std::function<u64(size_t)>& base_of, const std::function<i64*(size_t)>& c_of,
+                   uint64_t* final_words) {
+    const size_t W = ctx.ct_words();
+    // instances per lockstep chunk: bounded by the rotated working set
+    const size_t per_inst = (prog.sched.rot_count + prog.sched.comb_count / 2 + 8) * W * 8;
+    size_t free_b = 0, total_b = 0;
+    HGM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    size_t chunk = std::max<size_t>(1, (size_t)(0.45 * (double)free_b) / per_inst);
+    chunk = std::min<size_t>(chunk, 1024);
+    for (size_t c0 = 0; c0 < count; c0 += chunk) {
+        const int K = (int)std::min(chunk, count - c0);
+        std::vector<std::vector<std::vector<i64>>> packed(K);
+        for (int k = 0; k < K; ++k) packed[k] = prog.pack(a_of(c0 + k), b_of(c0 + k));
+        ExecIO io;
+        io.K = K;
+        io.input = [](int, int) -> const u64* { return nullptr; };
+        io.enc_values = [&](int s, int k) { return (const i64*)packed[k][s].data(); };
+        io.enc_counter = [&](int s, int k) { return base_of(c0 + k) + (u64)s; };
+        std::vector<u64*> res = execute(ctx, prog.sched, io);
+        std::vector<const u64*> cts(K);
+        std::vector<size_t> S(K, prog.segment);
+        std::vector<std::vector<i64>> outv(K, std::vector<i64>(prog.segment));
+        std::vector<i64*> outp(K);
+        for (int k = 0; k < K; ++k) {
+            cts[k] = res[0] + (size_t)k * W;
+            outp[k] = outv[k].data();
+        }
+        ctx.decrypt(K, cts.data(), S.data(), outp.data());
+        if (final_words)
+            HGM_CUDA(cudaMemcpy(final_words + c0 * W, res[0], (size_t)K * W * 8, cudaMemcpyDeviceToHost));
+        for (u64* r : res) ctx.release(r);
+        for (int k = 0; k < K; ++k) prog.unpack(outv[k], c_of(c0 + k));
+    }
+    ctx.sync();
+}
+
+void put_counts(const MatmulProgram& prog, uint64_t* stats) {
+    if (!stats) return;
+    for (int k = 0; k < 6; ++k) {
+        stats[2 * k] = prog.counts.c[k][0];
+        stats[2 * k + 1] = prog.counts.c[k][1];
+    }
+}
+
+int matmul_batch_impl(hgm_ctx* c, int algo, int order, int flags, size_t m, size_t l, size_t n, size_t count,
+                      const int64_t* A, const int64_t* B, int64_t* C, uint64_t counter0, uint64_t* stats,
+                      uint64_t* final_words) {
     return guarded([&] {
         if (order < -1 || order > 1) throw std::invalid_argument("order must be -1, 0 or 1");
         Context& ctx = *c->ctx;
-        auto prog = get_matmul_program(algo, order, m, l, n, ctx.slots(), ctx.host().N);
-        if (stats)
-            for (int k = 0; k < 6; ++k) {
-                stats[2 * k] = prog->counts.c[k][0];
-                stats[2 * k + 1] = prog->counts.c[k][1];
-            }
+        auto prog = get_matmul_program(algo, order, m, l, n, ctx.slots(), ctx.host().N, flags);
+        put_counts(*prog, stats);
         if (count == 0) return;
-        const size_t W = ctx.ct_words();
-        // instances per lockstep chunk: bounded by the rotated working set
-        const size_t per_inst = (prog->sched.rot_count + 8) * W * 8 + 64 * W * 8;
-        size_t free_b = 0, total_b = 0;
-        HGM_CUDA(cudaMemGetInfo(&free_b, &total_b));
-        size_t chunk = std::max<size_t>(1, (size_t)(0.5 * (double)free_b) / per_inst);
-        chunk = std::min<size_t>(chunk, 1024);
-        for (size_t c0 = 0; c0 < count; c0 += chunk) {
-            const int K = (int)std::min(chunk, count - c0);
-            std::vector<std::vector<std::vector<i64>>> packed(K);
-            for (int k = 0; k < K; ++k)
-                packed[k] = prog->pack(A + (c0 + k) * m * l, B + (c0 + k) * l * n);
-            ExecIO io;
-            io.K = K;
-            io.input = [](int, int) -> const u64* { return nullptr; };
-            io.enc_values = [&](int s, int k) { return (const i64*)packed[k][s].data(); };
-            io.enc_counter = [&](int s, int k) { return counter0 + (c0 + k) * prog->n_enc + s; };
-            std::vector<u64*> res = execute(ctx, prog->sched, io);
-            std::vector<const u64*> cts(K);
-            std::vector<size_t> S(K, prog->segment);
-            std::vector<std::vector<i64>> outv(K, std::vector<i64>(prog->segment));
-            std::vector<i64*> outp(K);
-            for (int k = 0; k < K; ++k) {
-                cts[k] = res[0] + (size_t)k * W;
-                outp[k] = outv[k].data();
+        const u64 E = (u64)prog->n_enc;
+        run_instances(
+            ctx, *prog, count, [&](size_t k) { return A + k * m * l; }, [&](size_t k) { return B + k * l * n; },
+            [&](size_t k) { return counter0 + k * E; }, [&](size_t k) { return C + k * m * n; }, final_words);
+    });
+}
+
+}  // namespace
+
+extern "C" {
+
+int hgm_blocked_mm(hgm_ctx* c, int algo, size_t m, size_t l, size_t n, const size_t* rows, size_t n_row,
+                   const size_t* mids, size_t n_mid, const size_t* cols, size_t n_col, const int64_t* A,
+                   const int64_t* B, int64_t* C, uint64_t counter0, int32_t* log) {
+    return guarded([&] {
+        if (algo < 0 || algo > 2) throw hgm::DimensionError("unknown algorithm id");
+        // BlockPlan::validate (algorithms.cpp:412-432)
+        auto check = [](const size_t* p, size_t np, size_t total, const char* name) {
+            if (np == 0) throw hgm::DimensionError(std::string("empty ") + name + " partition");
+            size_t sum = 0;
+            for (size_t i = 0; i < np; ++i) {
+                if (p[i] == 0) throw hgm::DimensionError(std::string("zero-sized block in ") + name + " partition");
+                sum += p[i];
             }
-            ctx.decrypt(K, cts.data(), S.data(), outp.data());
-            if (final_words)
-                HGM_CUDA(cudaMemcpy(final_words + c0 * W, res[0], (size_t)K * W * 8, cudaMemcpyDeviceToHost));
-            for (u64* r : res) ctx.release(r);
-            for (int k = 0; k < K; ++k) prog->unpack(outv[k], C + (c0 + k) * m * n);
+            if (sum != total)
+                throw hgm::DimensionError(std::string(name) + " partition sums to " + std::to_string(sum) +
+                                          ", expected " + std::to_string(total));
+        };
+        check(rows, n_row, m, "row");
+        check(mids, n_mid, l, "mid");
+        check(cols, n_col, n, "col");
+        Context& ctx = *c->ctx;
+        const size_t slots = ctx.slots();
+        auto offs = [](const size_t* p, size_t np) {
+            std::vector<size_t> o(np + 1, 0);
+            for (size_t i = 0; i < np; ++i) o[i + 1] = o[i] + p[i];
+            return o;
+        };
+        const auto ro = offs(rows, n_row), mo = offs(mids, n_mid), co = offs(cols, n_col);
+        struct Blk {
+            size_t bi, bj, bk, mm, ll, nn;
+            int used;
+            bool fell;
+            u64 base;
+            std::vector<i64> a, b, cprod;
+        };
+        std::vector<Blk> blocks;
+        u64 ctr = counter0;
+        for (size_t bi = 0; bi < n_row; ++bi)
+            for (size_t bj = 0; bj < n_col; ++bj)
+                for (size_t bk = 0; bk < n_mid; ++bk) {  // the reference loop order (algorithms.cpp:472-492)
+                    Blk k{bi, bj, bk, rows[bi], mids[bk], cols[bj], algo, false, 0, {}, {}, {}};
+                    if (algo == 1 && !hgm::fits(1, k.mm, k.ll, k.nn, slots)) {
+                        k.used = 0;  // duplicated working set outgrows the slots (algorithms.cpp:456-466)
+                        k.fell = true;
+                    }
+                    auto prog = get_matmul_program(k.used, -1, k.mm, k.ll, k.nn, slots, ctx.host().N);
+                    k.base = ctr;
+                    ctr += (u64)prog->n_enc;
+                    k.a.resize(k.mm * k.ll);
+                    k.b.resize(k.ll * k.nn);
+                    k.cprod.resize(k.mm * k.nn);
+                    for (size_t r = 0; r < k.mm; ++r)
+                        for (size_t q = 0; q < k.ll; ++q) k.a[r * k.ll + q] = A[(ro[bi] + r) * l + mo[bk] + q];
+                    for (size_t r = 0; r < k.ll; ++r)
+                        for (size_t q = 0; q < k.nn; ++q) k.b[r * k.nn + q] = B[(mo[bk] + r) * n + co[bj] + q];
+                    blocks.push_back(std::move(k));
+                }
+        // one lockstep batch per distinct (algorithm, shape)
+        std::map<std::tuple<int, size_t, size_t, size_t>, std::vector<size_t>> groups;
+        for (size_t i = 0; i < blocks.size(); ++i)
+            groups[std::make_tuple(blocks[i].used, blocks[i].mm, blocks[i].ll, blocks[i].nn)].push_back(i);
+        for (auto& kv : groups) {
+            const auto& ids = kv.second;
+            const Blk& f = blocks[ids[0]];
+            auto prog = get_matmul_program(f.used, -1, f.mm, f.ll, f.nn, slots, ctx.host().N);
+            run_instances(
+                ctx, *prog, ids.size(), [&](size_t k) { return (const i64*)blocks[ids[k]].a.data(); },
+                [&](size_t k) { return (const i64*)blocks[ids[k]].b.data(); },
+                [&](size_t k) { return blocks[ids[k]].base; }, [&](size_t k) { return blocks[ids[k]].cprod.data(); },
+                nullptr);
         }
-        ctx.sync();
+        std::fill(C, C + m * n, 0);
+        for (size_t i = 0; i < blocks.size(); ++i) {
+            const Blk& k = blocks[i];
+            for (size_t r = 0; r < k.mm; ++r)
+                for (size_t q = 0; q < k.nn; ++q) {
+                    i64& dst = C[(ro[k.bi] + r) * n + co[k.bj] + q];
+                    dst = (dst + k.cprod[r * k.nn + q]) % (i64)kT;
+                }
+            if (log) {
+                log[4 * i] = k.used;
+                log[4 * i + 1] = k.fell ? 1 : 0;
+                log[4 * i + 2] = (int32_t)k.mm;
+                log[4 * i + 3] = (int32_t)k.ll;
+            }
+        }
     });
 }
 
@@ -513,14 +629,14 @@ size_t lockstep_chunk(Context& ctx, const MatmulProgram& prog) {
 
 extern "C" {
 
-int hgm_batch_encrypt(hgm_ctx* c, int algo, int order, size_t m, size_t l, size_t n, size_t count,
+int hgm_batch_encrypt(hgm_ctx* c, int algo, int order, int flags, size_t m, size_t l, size_t n, size_t count,
                       const int64_t* A, const int64_t* B, uint64_t counter0, hgm_batch** out) {
     return guarded([&] {
         if (order < -1 || order > 1) throw std::invalid_argument("order must be -1, 0 or 1");
         Context& ctx = *c->ctx;
         auto b = std::make_unique<hgm_batch>();
         b->owner = c;
-        b->prog = get_matmul_program(algo, order, m, l, n, ctx.slots(), ctx.host().N);
+        b->prog = get_matmul_program(algo, order, m, l, n, ctx.slots(), ctx.host().N, flags);
         b->count = count;
         const size_t W = ctx.ct_words(), E = b->prog->n_enc;
         b->in = ctx.alloc(std::max<size_t>(1, count * E) * W);
@@ -628,10 +744,10 @@ void hgm_batch_free(hgm_batch* b) {
     delete b;
 }
 
-int hgm_program_info(int algo, int order, size_t m, size_t l, size_t n, size_t slots, uint32_t N,
+int hgm_program_info(int algo, int order, int flags, size_t m, size_t l, size_t n, size_t slots, uint32_t N,
                      uint64_t* stats, uint64_t* facts) {
     return guarded([&] {
-        auto p = get_matmul_program(algo, order, m, l, n, slots, N);
+        auto p = get_matmul_program(algo, order, m, l, n, slots, N, flags);
         if (stats)
             for (int k = 0; k < 6; ++k) {
                 stats[2 * k] = p->counts.c[k][0];
@@ -649,11 +765,11 @@ int hgm_program_info(int algo, int order, size_t m, size_t l, size_t n, size_t s
     });
 }
 
-long hgm_program_stream(int algo, int order, size_t m, size_t l, size_t n, size_t slots, uint32_t N,
+long hgm_program_stream(int algo, int order, int flags, size_t m, size_t l, size_t n, size_t slots, uint32_t N,
                         int64_t* hdr, size_t hdr_cap, int64_t* data, size_t data_cap, size_t* data_len) {
     long result = 0;
     const int rc = guarded([&] {
-        auto p = get_matmul_program(algo, order, m, l, n, slots, N);
+        auto p = get_matmul_program(algo, order, m, l, n, slots, N, flags);
         size_t dl = 0;
         for (const auto& mk : p->stream_masks) dl += mk->v.size();
         if (data_len) *data_len = dl;
@@ -701,14 +817,14 @@ long hgm_plan_info(int kind, size_t k, size_t a, size_t b, size_t c, int order, 
     return rc == HGM_OK ? result : -rc;
 }
 
-int hgm_matmul_batch(hgm_ctx* c, int algo, int order, size_t m, size_t l, size_t n, size_t count,
+int hgm_matmul_batch(hgm_ctx* c, int algo, int order, int flags, size_t m, size_t l, size_t n, size_t count,
                      const int64_t* A, const int64_t* B, int64_t* C, uint64_t counter0, uint64_t* stats) {
-    return matmul_batch_impl(c, algo, order, m, l, n, count, A, B, C, counter0, stats, nullptr);
+    return matmul_batch_impl(c, algo, order, flags, m, l, n, count, A, B, C, counter0, stats, nullptr);
 }
-int hgm_matmul_batch_export(hgm_ctx* c, int algo, int order, size_t m, size_t l, size_t n, size_t count,
-                            const int64_t* A, const int64_t* B, int64_t* C, uint64_t counter0,
+int hgm_matmul_batch_export(hgm_ctx* c, int algo, int order, int flags, size_t m, size_t l, size_t n,
+                            size_t count, const int64_t* A, const int64_t* B, int64_t* C, uint64_t counter0,
                             uint64_t* final_words) {
-    return matmul_batch_impl(c, algo, order, m, l, n, count, A, B, C, counter0, nullptr, final_words);
+    return matmul_batch_impl(c, algo, order, flags, m, l, n, count, A, B, C, counter0, nullptr, final_words);
 }
 
 int hgm_bench_ntt(hgm_ctx* c, int forward, size_t limbs, int iters, float* ms) {

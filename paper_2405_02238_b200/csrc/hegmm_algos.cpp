@@ -114,6 +114,23 @@ std::shared_ptr<Plan> omega_plan(size_t k, size_t l, size_t m, size_t n, Order o
     std::sort(pairs.begin(), pairs.end());
     return plan_from_pairs(pairs, l * n, m * n, m * n);
 }
+// sigma: out (i, j) of m x l reads (i, (i+j) mod l) (lintrans.cpp:88-95)
+std::shared_ptr<Plan> sigma_plan(size_t m, size_t l, Order o) {
+    std::vector<std::pair<size_t, size_t>> pairs;
+    for (size_t i = 0; i < m; ++i)
+        for (size_t j = 0; j < l; ++j)
+            pairs.emplace_back(flat_index(i, j, m, l, o), flat_index(i, (i + j) % l, m, l, o));
+    return plan_from_pairs(pairs, m * l, m * l, m * l);
+}
+// tau: out (i, j) of l x n reads ((i+j) mod l, j) (lintrans.cpp:96-103)
+std::shared_ptr<Plan> tau_plan(size_t l, size_t n, Order o) {
+    std::vector<std::pair<size_t, size_t>> pairs;
+    for (size_t i = 0; i < l; ++i)
+        for (size_t j = 0; j < n; ++j)
+            pairs.emplace_back(flat_index(i, j, l, n, o), flat_index((i + j) % l, j, l, n, o));
+    return plan_from_pairs(pairs, l * n, l * n, l * n);
+}
+
 // lintrans.cpp:244-263
 std::shared_ptr<Plan> embed(const Plan& p, size_t segment) {
     if (segment < std::max(p.in_len, p.out_len))
@@ -158,6 +175,18 @@ std::shared_ptr<const Plan> eps_plan_embedded(size_t k, size_t m, size_t l, size
                                               size_t segment) {
     return cached(PlanKey{2, k, m, l, n, (int)o, segment}, [&] {
         auto base = cached(PlanKey{0, k, m, l, n, (int)o, 0}, [&] { return eps_plan(k, m, l, n, o); });
+        return embed(*base, segment);
+    });
+}
+std::shared_ptr<const Plan> sigma_plan_embedded(size_t m, size_t l, Order o, size_t segment) {
+    return cached(PlanKey{6, 0, m, l, 0, (int)o, segment}, [&] {
+        auto base = cached(PlanKey{6, 0, m, l, 0, (int)o, 0}, [&] { return sigma_plan(m, l, o); });
+        return embed(*base, segment);
+    });
+}
+std::shared_ptr<const Plan> tau_plan_embedded(size_t l, size_t n, Order o, size_t segment) {
+    return cached(PlanKey{7, 0, l, n, 0, (int)o, segment}, [&] {
+        auto base = cached(PlanKey{7, 0, l, n, 0, (int)o, 0}, [&] { return tau_plan(l, n, o); });
         return embed(*base, segment);
     });
 }
@@ -358,31 +387,42 @@ Strategy select_strategy(size_t m, size_t l, size_t n) {
 }
 
 std::vector<std::vector<i64>> MatmulProgram::pack(const i64* A, const i64* B) const {
-    const Mat a = mat_from(A, m, l), b = mat_from(B, l, n);
+    Mat a = mat_from(A, m0, l0), b = mat_from(B, l0, n0);
+    if (algo == Algo::SquarePad) {  // algorithms.cpp:369-388: zero-pad to d x d
+        Mat pa(m, l), pb(l, n);
+        for (size_t r = 0; r < m0; ++r)
+            for (size_t c = 0; c < l0; ++c) pa.at(r, c) = a.at(r, c);
+        for (size_t r = 0; r < l0; ++r)
+            for (size_t c = 0; c < n0; ++c) pb.at(r, c) = b.at(r, c);
+        a = pa;
+        b = pb;
+    }
     std::vector<std::vector<i64>> out;
-    if (algo == Algo::Basic) {
-        out.push_back(flatten_padded(sigma(a), order, segment));
-        out.push_back(flatten_padded(tau(b), order, segment));
+    if (algo != Algo::Enhanced) {
+        out.push_back(flatten_padded(enc_transforms ? a : sigma(a), order, segment));
+        out.push_back(flatten_padded(enc_transforms ? b : tau(b), order, segment));
         out.emplace_back(segment, 0);
     } else {
         size_t buf_a_cols, buf_b_rows, seg;
         en_shape(l, strat.rows_w, strat.cols_w, buf_a_cols, buf_b_rows, seg);
         const Mat abar = strat.dup == Dup::AVertical ? stack_rows(a, strat.t) : a;
         const Mat bbar = strat.dup == Dup::BHorizontal ? stack_cols(b, strat.t) : b;
-        out.push_back(flatten_padded(shift_cols(sigma(abar), 0, strat.rows_w, buf_a_cols), order, segment));
-        out.push_back(flatten_padded(shift_rows(tau(bbar), 0, buf_b_rows, strat.cols_w), order, segment));
+        if (enc_transforms) {
+            out.push_back(flatten_padded(abar, order, segment));
+            out.push_back(flatten_padded(bbar, order, segment));
+        } else {
+            out.push_back(flatten_padded(shift_cols(sigma(abar), 0, strat.rows_w, buf_a_cols), order, segment));
+            out.push_back(flatten_padded(shift_rows(tau(bbar), 0, buf_b_rows, strat.cols_w), order, segment));
+        }
     }
     return out;
 }
 
 void MatmulProgram::unpack(const std::vector<i64>& v, i64* C) const {
-    if (algo == Algo::Basic) {
-        for (size_t r = 0; r < m; ++r)
-            for (size_t c = 0; c < n; ++c) C[r * n + c] = v[flat_index(r, c, m, n, order)];
-    } else {
-        for (size_t r = 0; r < m; ++r)
-            for (size_t c = 0; c < n; ++c) C[r * n + c] = v[flat_index(r, c, strat.rows_w, strat.cols_w, order)];
-    }
+    const size_t rows = algo == Algo::Enhanced ? strat.rows_w : m;
+    const size_t cols = algo == Algo::Enhanced ? strat.cols_w : n;
+    for (size_t r = 0; r < m0; ++r)
+        for (size_t c = 0; c < n0; ++c) C[r * n0 + c] = v[flat_index(r, c, rows, cols, order)];
 }
 
 namespace {
@@ -398,7 +438,8 @@ Program cloud_only(const Program& p) {
 }
 
 // reference basic_mm (algorithms.cpp:198-248)
-std::shared_ptr<MatmulProgram> build_basic(int order_opt, size_t m, size_t l, size_t n, size_t slots, u32 N) {
+std::shared_ptr<MatmulProgram> build_basic(int order_opt, size_t m, size_t l, size_t n, size_t slots, u32 N,
+                                           bool enc) {
     check_capacity(m * l, slots, "flattened left operand");
     check_capacity(l * n, slots, "flattened right operand");
     check_capacity(m * n, slots, "flattened product");
@@ -416,10 +457,16 @@ std::shared_ptr<MatmulProgram> build_basic(int order_opt, size_t m, size_t l, si
         }
         mp->order = row < col ? Order::Row : Order::Col;
     }
+    mp->m0 = m; mp->l0 = l; mp->n0 = n;
+    mp->enc_transforms = enc;
     Recorder R;
     R.N = N;
     R.phase = 0;
-    const int ca = R.enc(mp->segment), cb = R.enc(mp->segment);
+    int ca = R.enc(mp->segment), cb = R.enc(mp->segment);
+    if (enc) {  // algorithms.cpp:219-227: sigma / tau as ciphertext plans (client phase)
+        ca = apply_plan(R, ca, *sigma_plan_embedded(m, l, mp->order, mp->segment));
+        cb = apply_plan(R, cb, *tau_plan_embedded(l, n, mp->order, mp->segment));
+    }
     int acc = R.enc(mp->segment);
     R.phase = 1;
     for (size_t k = 0; k < l; ++k) {
@@ -440,7 +487,8 @@ std::shared_ptr<MatmulProgram> build_basic(int order_opt, size_t m, size_t l, si
 }
 
 // reference enhanced_mm (algorithms.cpp:250-367)
-std::shared_ptr<MatmulProgram> build_enhanced(int order_opt, size_t m, size_t l, size_t n, size_t slots, u32 N) {
+std::shared_ptr<MatmulProgram> build_enhanced(int order_opt, size_t m, size_t l, size_t n, size_t slots, u32 N,
+                                              bool enc) {
     Strategy s = select_strategy(m, l, n);
     if (order_opt >= 0 && (Order)order_opt != s.order) {
         s.order = (Order)order_opt;
@@ -455,10 +503,20 @@ std::shared_ptr<MatmulProgram> build_enhanced(int order_opt, size_t m, size_t l,
     mp->segment = segment;
     mp->order = s.order;
     mp->strat = s;
+    mp->m0 = m; mp->l0 = l; mp->n0 = n;
+    mp->enc_transforms = enc;
     Recorder R;
     R.N = N;
     R.phase = 0;
-    const int ca = R.enc(segment), cb = R.enc(segment);
+    int ca = R.enc(segment), cb = R.enc(segment);
+    if (enc) {  // algorithms.cpp:279-301: sigma, tau, eps_0, omega_0 as ciphertext plans
+        const size_t a_rows = s.dup == Dup::AVertical ? s.t * m : m;
+        const size_t b_cols = s.dup == Dup::BHorizontal ? s.t * n : n;
+        ca = apply_plan(R, ca, *sigma_plan_embedded(a_rows, l, s.order, segment));
+        cb = apply_plan(R, cb, *tau_plan_embedded(l, b_cols, s.order, segment));
+        ca = apply_plan(R, ca, *eps_plan_embedded(0, s.rows_w, l, buf_a_cols, s.order, segment));
+        cb = apply_plan(R, cb, *omega_plan_embedded(0, l, buf_b_rows, s.cols_w, s.order, segment));
+    }
     R.phase = 1;
     std::map<size_t, int> groups;
     for (size_t k = 0; k < s.p; ++k) {
@@ -500,22 +558,49 @@ std::shared_ptr<MatmulProgram> build_enhanced(int order_opt, size_t m, size_t l,
 }
 
 std::mutex g_prog_mu;
-std::map<std::tuple<int, int, size_t, size_t, size_t, size_t, u32>, std::shared_ptr<const MatmulProgram>> g_progs;
+std::map<std::tuple<int, int, int, size_t, size_t, size_t, size_t, u32>, std::shared_ptr<const MatmulProgram>> g_progs;
+
+// reference square_pad_mm (algorithms.cpp:369-388): basic_mm on d x d operands
+std::shared_ptr<MatmulProgram> build_square_pad(int order, size_t m, size_t l, size_t n, size_t slots, u32 N,
+                                                bool enc) {
+    const size_t d = std::max({m, l, n});
+    check_capacity(d * d, slots, "square-padded operands");
+    auto mp = build_basic(order, d, d, d, slots, N, enc);
+    mp->algo = Algo::SquarePad;
+    mp->m0 = m; mp->l0 = l; mp->n0 = n;
+    return mp;
+}
 
 }  // namespace
 
+size_t enhanced_segment(size_t m, size_t l, size_t n) { return select_strategy(m, l, n).segment; }
+
+bool fits(int algo, size_t m, size_t l, size_t n, size_t slots) {
+    switch (algo) {
+        case 0: return std::max({m * l, l * n, m * n}) <= slots;
+        case 1: return enhanced_segment(m, l, n) <= slots;
+        case 2: {
+            const size_t d = std::max({m, l, n});
+            return d * d <= slots;
+        }
+    }
+    return false;
+}
+
 std::shared_ptr<const MatmulProgram> get_matmul_program(int algo, int order, size_t m, size_t l, size_t n,
-                                                        size_t slots, u32 N) {
+                                                        size_t slots, u32 N, int flags) {
     if (m == 0 || l == 0 || n == 0) throw DimensionError("matrix dimensions must be positive");
-    if (algo != 0 && algo != 1) throw DimensionError("unknown algorithm id");
-    const auto key = std::make_tuple(algo, order, m, l, n, slots, N);
+    if (algo < 0 || algo > 2) throw DimensionError("unknown algorithm id");
+    const bool enc = (flags & kFlagEncryptedClientTransforms) != 0;
+    const auto key = std::make_tuple(algo, order, (int)enc, m, l, n, slots, N);
     {
         std::lock_guard<std::mutex> lk(g_prog_mu);
         auto it = g_progs.find(key);
         if (it != g_progs.end()) return it->second;
     }
-    std::shared_ptr<const MatmulProgram> p =
-        algo == 0 ? build_basic(order, m, l, n, slots, N) : build_enhanced(order, m, l, n, slots, N);
+    std::shared_ptr<const MatmulProgram> p = algo == 0   ? build_basic(order, m, l, n, slots, N, enc)
+                                             : algo == 1 ? build_enhanced(order, m, l, n, slots, N, enc)
+                                                         : build_square_pad(order, m, l, n, slots, N, enc);
     std::lock_guard<std::mutex> lk(g_prog_mu);
     return g_progs.emplace(key, p).first->second;
 }

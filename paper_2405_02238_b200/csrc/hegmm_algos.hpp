@@ -19,7 +19,9 @@
 namespace hgm {
 
 enum class Order { Col = 0, Row = 1 };
-enum class Algo { Basic = 0, Enhanced = 1 };
+enum class Algo { Basic = 0, Enhanced = 1, SquarePad = 2 };
+// MultiplyOptions (algorithms.hpp:15-22) as flags
+constexpr int kFlagEncryptedClientTransforms = 1;
 enum class Dup { None, AVertical, BHorizontal };
 
 // errors raised with the reference's exception classes (errors.hpp:17-27)
@@ -70,7 +72,9 @@ Strategy select_strategy(size_t m, size_t l, size_t n);
 // A product shape compiled to a program.
 struct MatmulProgram {
     Algo algo = Algo::Basic;
-    size_t m = 0, l = 0, n = 0, segment = 0, slots = 0;
+    size_t m = 0, l = 0, n = 0, segment = 0, slots = 0;  // dims the program runs on
+    size_t m0 = 0, l0 = 0, n0 = 0;                        // caller's dims (square_pad pads)
+    bool enc_transforms = false;
     Order order = Order::Col;
     Strategy strat;
     Schedule sched;        // client encrypt + cloud (encryptions are level 0)
@@ -85,9 +89,12 @@ struct MatmulProgram {
     void unpack(const std::vector<i64>& slots_out, i64* C) const;
 };
 
-// Cached per (algo, m, l, n, order, slots, N); order: -1 auto.
+// Cached per (algo, order, flags, m, l, n, slots, N); order: -1 auto.
 std::shared_ptr<const MatmulProgram> get_matmul_program(int algo, int order, size_t m, size_t l,
-                                                        size_t n, size_t slots, u32 N);
+                                                        size_t n, size_t slots, u32 N, int flags = 0);
+// Working flattened length of each algorithm (algorithms.cpp:172-196)
+size_t enhanced_segment(size_t m, size_t l, size_t n);
+bool fits(int algo, size_t m, size_t l, size_t n, size_t slots);
 
 // Plans (exposed for tests)
 std::shared_ptr<const Plan> eps_plan_embedded(size_t k, size_t m, size_t l, size_t n, Order o,

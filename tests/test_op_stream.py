@@ -103,3 +103,25 @@ def test_golden_products_with_reference(ref):
         C, _ = ref.mm(A, B, "basic", slots=g["slots"])
         assert hashlib.sha256(C.astype(np.int64).tobytes()).hexdigest() == g["algos"]["basic"]["C_sha256"]
         assert np.array_equal(C, (A @ B) % 65537)
+
+
+def test_encrypted_client_transforms_and_square_pad_streams(ref):
+    """MultiplyOptions::encrypted_client_transforms (algorithms.cpp:219-227,
+    :279-301) and square_pad_mm (:369-388): same op stream as the reference,
+    including the client-phase rotations and masks."""
+    rng = np.random.default_rng(21)
+    for trial in range(25):
+        m, l, n = (int(x) for x in rng.integers(1, 11, 3))
+        A = rng.integers(-9, 10, (m, l))
+        B = rng.integers(-9, 10, (l, n))
+        for algo in ("basic", "enhanced", "square_pad"):
+            for flags in (0, 1):
+                order = (-1, 0, 1)[trial % 3]
+                rh, rd = ref.trace2(A, B, algo, order, flags, slots=4096)
+                mh, md = hb.program_stream(hb.ALGOS[algo], m, l, n, 4096, 8192, order, flags)
+                assert digest(rh, rd) == digest(mh, md), (m, l, n, algo, flags, order)
+                _, st_ref = ref.mm2(A, B, algo, order, flags, slots=4096)
+                st, _ = hb.program_info(hb.ALGOS[algo], m, l, n, 4096, 8192, order, flags)
+                assert st.astype(int).tolist() == st_ref[:12].astype(int).tolist()
+                if flags:
+                    assert st[4] > 0  # client-phase cmults (test_algorithms.cpp:84-94)
