@@ -21,6 +21,16 @@ namespace {
 __constant__ DevParams c_dp[kParamSets];
 
 constexpr int kThreads = 256;
+
+// RNS shapes of the parameter sets, as compile-time constants so per-thread
+// residue arrays unroll into registers (set 0 and 2: L 3 / K 1 / B 4 / dnum 3;
+// set 1: L 8 / K 4 / B 9 / dnum 2).
+struct ShapeQ3 {
+    static constexpr u32 L = 3, K = 1, nB = 4, dnum = 3, A = 1, R = 4;
+};
+struct ShapeQ8 {
+    static constexpr u32 L = 8, K = 4, nB = 9, dnum = 2, A = 4, R = 12;
+};
 // items per launch sequence: bounds temporaries and staging uploads
 constexpr int kChunkEnc = 256, kChunkDec = 1024, kChunkLin = 8192, kChunkKs = 1024, kChunkMult = 128;
 
@@ -58,10 +68,11 @@ __global__ void k_encode_scatter(DevCtx cx, u32 n, const i64* vals,
 }
 
 // oracle encrypt(): sample u, e0, e1; c0 = e0 + Delta m, c1 = e1 (coefficient form)
+template <typename SH>
 __global__ void k_enc_lift(DevCtx cx, u32 n, const u64* m, const u64* ctr,
                            u64* U, u64* const* out) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, L = dp->L;
+    const u32 N = dp->N, L = SH::L;
     const u64 seed = cx.seed;
     ITEM_LOOP {
         const u64 c = ctr[item];
@@ -82,10 +93,11 @@ __global__ void k_enc_lift(DevCtx cx, u32 n, const u64* m, const u64* ctr,
     }
 }
 
+template <typename SH>
 __global__ void k_enc_finish(DevCtx cx, u32 n, const u64* U, const u64* pk,
                              u64* const* out) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, L = dp->L;
+    const u32 N = dp->N, L = SH::L;
     ITEM_LOOP {
         u64* o = out[item];
         COEF_LOOP {
@@ -101,10 +113,11 @@ __global__ void k_enc_finish(DevCtx cx, u32 n, const u64* U, const u64* pk,
 }
 
 // ---------------------------------------------------------------- decryption
+template <typename SH>
 __global__ void k_dec_phase(DevCtx cx, u32 n, const u64* const* in,
                             const u64* sk, u64* X) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, L = dp->L;
+    const u32 N = dp->N, L = SH::L;
     ITEM_LOOP {
         const u64* c = in[item];
         COEF_LOOP {
@@ -118,9 +131,10 @@ __global__ void k_dec_phase(DevCtx cx, u32 n, const u64* const* in,
 }
 
 // oracle decrypt(): m = round(t x / Q) mod t via sum_i [x_i (Q/q_i)^-1]_{q_i} t/q_i
+template <typename SH>
 __global__ void k_dec_round(DevCtx cx, u32 n, const u64* X, u64* M) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, L = dp->L;
+    const u32 N = dp->N, L = SH::L;
     ITEM_LOOP {
         COEF_LOOP {
             Acc128 s{0, 0};
@@ -145,10 +159,11 @@ __global__ void k_dec_gather(DevCtx cx, u32 n, const u64* M, const u32* S,
 }
 
 // ---------------------------------------------------------------- linear ops
+template <typename SH>
 __global__ void k_add(DevCtx cx, u32 n, const u64* const* a,
                       const u64* const* b, u64* const* out) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, L = dp->L;
+    const u32 N = dp->N, L = SH::L;
     const size_t W = (size_t)2 * L * N;
     ITEM_LOOP {
         const u64 *x = a[item], *y = b[item];
@@ -170,10 +185,11 @@ __global__ void k_copy(u32 n, size_t W, const u64* const* in, u64* const* out) {
 }
 
 // out[o] = sum_t in[t] (.* mask[t]) : oracle cmult() followed by add()
+template <typename SH>
 __global__ void k_lincomb(DevCtx cx, u32 n, const u32* off,
                           const u64* const* in, const u64* const* mask, u64* const* out) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, L = dp->L;
+    const u32 N = dp->N, L = SH::L;
     const size_t LN = (size_t)L * N, W = 2 * LN;
     ITEM_LOOP {
         const u32 t0 = off[item], t1 = off[item + 1];
@@ -193,9 +209,10 @@ __global__ void k_lincomb(DevCtx cx, u32 n, const u32* off,
 }
 
 // centred lift of the mod-t mask polynomial to each q_i (oracle cmult())
+template <typename SH>
 __global__ void k_mask_lift(DevCtx cx, const u64* m, u64* out) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, L = dp->L;
+    const u32 N = dp->N, L = SH::L;
     const u32 n = 1;
     ITEM_LOOP {
         COEF_LOOP {
@@ -207,9 +224,10 @@ __global__ void k_mask_lift(DevCtx cx, const u64* m, u64* out) {
 
 // ---------------------------------------------------------------- key switching
 // c1 limbs of each ct into a contiguous [n][L][N] buffer
+template <typename SH>
 __global__ void k_gather_c1(DevCtx cx, u32 n, const u64* const* ct, u64* C) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, L = dp->L;
+    const u32 N = dp->N, L = SH::L;
     const size_t LN = (size_t)L * N;
     ITEM_LOOP {
         const u64* c = ct[item] + LN;
@@ -220,10 +238,11 @@ __global__ void k_gather_c1(DevCtx cx, u32 n, const u64* const* ct, u64* C) {
 
 // oracle key_switch() ModUp: digit dg of the coefficient-domain poly C, lifted
 // to every limb of Q ++ P with centred residues.  D: [n][dnum][R][N]
+template <typename SH>
 __global__ void k_modup_lift(DevCtx cx, u32 n, const u64* C, size_t c_stride,
                              u64* D) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, L = dp->L, R = dp->R, A = dp->alpha, dnum = dp->dnum;
+    const u32 N = dp->N, L = SH::L, R = SH::R, A = SH::A, dnum = SH::dnum;
     ITEM_LOOP {
         const u64* c = C + item * c_stride;
         u64* d = D + (size_t)item * dnum * R * N;
@@ -265,10 +284,11 @@ __global__ void k_modup_lift(DevCtx cx, u32 n, const u64* C, size_t c_stride,
 // block serves up to kKeyReuse consecutive items and reads each key element
 // once for all items of the group that share it.
 constexpr int kKeyReuse = 4;
+template <typename SH>
 __global__ void k_ks_inner(DevCtx cx, u32 n, const u64* const* D,
                            const u64* const* key, const u32* g, u64* const* acc) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, R = dp->R, dnum = dp->dnum, logN = dp->logN;
+    const u32 N = dp->N, R = SH::R, dnum = SH::dnum, logN = dp->logN;
     for (u32 grp = blockIdx.y; grp * kKeyReuse < n; grp += gridDim.y) {
         const u32 i0 = grp * kKeyReuse;
         const u32 cnt = min((u32)kKeyReuse, n - i0);
@@ -323,9 +343,10 @@ __global__ void k_ks_inner(DevCtx cx, u32 n, const u64* const* D,
 // V[c][i] = ecoef[c][i] - P^-1 conv[c][i]  (coefficient domain; ecoef optional)
 // so that NTT(V) + P^-1 acc = (acc - NTT(conv)) P^-1 + NTT(ecoef) exactly (the NTT
 // is linear mod q_i): relinearisation adds e0, e1 without transforming them apart.
+template <typename SH>
 __global__ void k_moddown_conv(DevCtx cx, u32 n, const u64* const* acc, const u64* const* ecoef, u64* V) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, L = dp->L, K = dp->K, R = dp->R;
+    const u32 N = dp->N, L = SH::L, K = SH::K, R = SH::R;
     ITEM_LOOP {
         const u32 c = blockIdx.z;
         const u64* a = acc[item] + (size_t)c * R * N;
@@ -355,10 +376,11 @@ __global__ void k_moddown_conv(DevCtx cx, u32 n, const u64* const* acc, const u6
 }
 
 // out_c = NTT(V_c) + P^-1 acc_c  (+ addn[galois_src] for c = 0)
+template <typename SH>
 __global__ void k_ks_finish(DevCtx cx, u32 n, const u64* const* acc, const u64* V, const u64* const* addn,
                             const u32* g, u64* const* out) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, L = dp->L, R = dp->R, logN = dp->logN;
+    const u32 N = dp->N, L = SH::L, R = SH::R, logN = dp->logN;
     ITEM_LOOP {
         const u64* a = acc[item];
         const u64* v = V + (size_t)item * 2 * L * N;
@@ -382,9 +404,10 @@ __global__ void k_ks_finish(DevCtx cx, u32 n, const u64* const* acc, const u64* 
 
 // ---------------------------------------------------------------- tensoring
 // oracle q_to_b(): exact centred conversion of 4 polys per item, X: [n][4][L][N]
+template <typename SH>
 __global__ void k_q_to_b(DevCtx cx, u32 n, const u64* X, u64* XB) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, L = dp->L, K = dp->K, nB = dp->nB;
+    const u32 N = dp->N, L = SH::L, K = SH::K, nB = SH::nB;
     ITEM_LOOP {
         const u32 p = blockIdx.z;
         const u64* x = X + ((size_t)item * 4 + p) * L * N;
@@ -409,10 +432,11 @@ __global__ void k_q_to_b(DevCtx cx, u32 n, const u64* X, u64* XB) {
 }
 
 // tensor over Q ++ B in the NTT domain; T: [n][3][L+nB][N]
+template <typename SH>
 __global__ void k_tensor(DevCtx cx, u32 n, const u64* const* A,
                          const u64* const* B, const u64* XB, u64* T) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, L = dp->L, K = dp->K, nB = dp->nB, D = L + nB;
+    const u32 N = dp->N, L = SH::L, K = SH::K, nB = SH::nB, D = L + nB;
     ITEM_LOOP {
         const u32 d = blockIdx.z;
         u64 *t0 = T + (((size_t)item * 3 + 0) * D + d) * N, *t1 = T + (((size_t)item * 3 + 1) * D + d) * N,
@@ -439,9 +463,10 @@ __global__ void k_tensor(DevCtx cx, u32 n, const u64* const* A,
 }
 
 // oracle scale_round(): round(t x / Q) from Q ++ B residues, then exact B -> Q
+template <typename SH>
 __global__ void k_scale_round(DevCtx cx, u32 n, const u64* T, u64* E) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, L = dp->L, K = dp->K, nB = dp->nB, D = L + nB;
+    const u32 N = dp->N, L = SH::L, K = SH::K, nB = SH::nB, D = L + nB;
     ITEM_LOOP {
         const u32 p = blockIdx.z;
         const u64* t = T + ((size_t)item * 3 + p) * D * N;
@@ -479,9 +504,10 @@ __global__ void k_scale_round(DevCtx cx, u32 n, const u64* T, u64* E) {
 }
 
 // ---------------------------------------------------------------- key generation
+template <typename SH>
 __global__ void k_keygen_sk(DevCtx cx, u64* S) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, R = dp->R;
+    const u32 N = dp->N, R = SH::R;
     const u32 n = 1;
     ITEM_LOOP {
         COEF_LOOP {
@@ -504,9 +530,10 @@ __global__ void k_keygen_err(DevCtx cx, u64 stream, u32 limbs, u64* E) {
     }
 }
 
+template <typename SH>
 __global__ void k_keygen_pk(DevCtx cx, const u64* S, const u64* E, u64* pk) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, L = dp->L;
+    const u32 N = dp->N, L = SH::L;
     const u32 n = 1;
     ITEM_LOOP {
         COEF_LOOP {
@@ -521,10 +548,11 @@ __global__ void k_keygen_pk(DevCtx cx, const u64* S, const u64* E, u64* pk) {
 }
 
 // oracle make_key(): key[dg][0][r] = -a s + e + [r in digit dg] P s'; key[dg][1][r] = a
+template <typename SH>
 __global__ void k_keygen_ks(DevCtx cx, u32 kid, u32 g, const u64* S,
                             const u64* E, u64* key) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, L = dp->L, R = dp->R, A = dp->alpha, logN = dp->logN;
+    const u32 N = dp->N, L = SH::L, R = SH::R, A = SH::A, logN = dp->logN;
     const u32 dg = blockIdx.y;
     const u32 n = 1;
     (void)n;
@@ -686,12 +714,12 @@ void Context::build_keys() {
     const u32 N = hp_.N, L = hp_.L, R = hp_.R;
     HGM_CUDA(cudaMalloc(&d_sk_, (size_t)R * N * 8));
     HGM_CUDA(cudaMalloc(&d_pk_, (size_t)2 * L * N * 8));
-    k_keygen_sk<<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, d_sk_); ++launches_;
+    if (hp_.L == 3) k_keygen_sk<ShapeQ3><<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, d_sk_); else k_keygen_sk<ShapeQ8><<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, d_sk_); ++launches_;
     ntt(true, jobs_contig(d_sk_, R, 0, R));
     u64* E = alloc((size_t)L * N);
     k_keygen_err<<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, kStreamPkE, L, E); ++launches_;
     ntt(true, jobs_contig(E, L, 0, L));
-    k_keygen_pk<<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, d_sk_, E, d_pk_); ++launches_;
+    if (hp_.L == 3) k_keygen_pk<ShapeQ3><<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, d_sk_, E, d_pk_); else k_keygen_pk<ShapeQ8><<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, d_sk_, E, d_pk_); ++launches_;
     release(E);
     HGM_CUDA(cudaGetLastError());
     ks_key(0);  // relinearisation key
@@ -719,7 +747,7 @@ const u64* Context::ks_key(u32 kid) {
         k_keygen_err<<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, kStreamKsE | ((u64)kid << 8) | dg, R,
                                                              E + (size_t)dg * R * N); ++launches_;
     ntt(true, jobs_contig(E, dnum * R, 0, R));
-    k_keygen_ks<<<dim3((N + kThreads - 1) / kThreads, dnum), kThreads, 0, stream_>>>(cx_, kid, kid, d_sk_, E, key); ++launches_;
+    if (hp_.L == 3) k_keygen_ks<ShapeQ3><<<dim3((N + kThreads - 1) / kThreads, dnum), kThreads, 0, stream_>>>(cx_, kid, kid, d_sk_, E, key); else k_keygen_ks<ShapeQ8><<<dim3((N + kThreads - 1) / kThreads, dnum), kThreads, 0, stream_>>>(cx_, kid, kid, d_sk_, E, key); ++launches_;
     release(E);
     HGM_CUDA(cudaGetLastError());
     std::lock_guard<std::mutex> lk(key_mu_);
@@ -755,7 +783,7 @@ const u64* Context::mask_plain(const i64* mask, size_t S) {
     ntt(false, tj);
     u64* out = nullptr;
     HGM_CUDA(cudaMallocAsync((void**)&out, (size_t)L * N * 8, stream_));
-    k_mask_lift<<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, m, out); ++launches_;
+    if (hp_.L == 3) k_mask_lift<ShapeQ3><<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, m, out); else k_mask_lift<ShapeQ8><<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, m, out); ++launches_;
     ntt(true, jobs_contig(out, L, 0, L));
     release(m);
     HGM_CUDA(cudaGetLastError());
@@ -791,7 +819,7 @@ void Context::encrypt(int n, const i64* const* host_vals, const size_t* S, const
     u64* U = alloc((size_t)n * L * N);
     k_encode_scatter<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, dvals, dS, M); ++launches_;
     ntt(false, jobs_contig(M, n, kTIndex, 1));
-    k_enc_lift<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, M, dctr, U, dout); ++launches_;
+    if (hp_.L == 3) k_enc_lift<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, M, dctr, U, dout); else k_enc_lift<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, M, dctr, U, dout); ++launches_;
     ntt(true, jobs_contig(U, n * L, 0, L));
     NttJobs cj;
     std::vector<u64*> limbs((size_t)n * 2 * L);
@@ -802,7 +830,7 @@ void Context::encrypt(int n, const i64* const* host_vals, const size_t* S, const
     cj.period = L;
     for (u32 i = 0; i < L; ++i) cj.prime[i] = (unsigned char)i;
     ntt(true, cj);
-    k_enc_finish<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, U, d_pk_, dout); ++launches_;
+    if (hp_.L == 3) k_enc_finish<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, U, d_pk_, dout); else k_enc_finish<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, U, d_pk_, dout); ++launches_;
     release(M);
     release(U);
     HGM_CUDA(cudaGetLastError());
@@ -826,9 +854,9 @@ void Context::decrypt(int n, const u64* const* in, const size_t* S, i64* const* 
     u64* X = alloc((size_t)n * L * N);
     u64* M = alloc((size_t)n * N);
     i64* O = reinterpret_cast<i64*>(alloc((size_t)n * H));
-    k_dec_phase<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, din, d_sk_, X); ++launches_;
+    if (hp_.L == 3) k_dec_phase<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, din, d_sk_, X); else k_dec_phase<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, din, d_sk_, X); ++launches_;
     ntt(false, jobs_contig(X, n * L, 0, L));
-    k_dec_round<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, X, M); ++launches_;
+    if (hp_.L == 3) k_dec_round<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, X, M); else k_dec_round<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, X, M); ++launches_;
     ntt(true, jobs_contig(M, n, kTIndex, 1));
     k_dec_gather<<<grid_of(H, n), kThreads, 0, stream_>>>(cx_, n, M, dS, O); ++launches_;
     std::vector<i64> host((size_t)n * H);
@@ -851,7 +879,7 @@ void Context::add(int n, const u64* const* a, const u64* const* b, u64* const* o
     }
     std::vector<const u64*> va(a, a + n), vb(b, b + n);
     std::vector<u64*> vo(out, out + n);
-    k_add<<<grid_of(hp_.N, n, 1), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), upload(vo)); ++launches_;
+    if (hp_.L == 3) k_add<ShapeQ3><<<grid_of(hp_.N, n, 1), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), upload(vo)); else k_add<ShapeQ8><<<grid_of(hp_.N, n, 1), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), upload(vo)); ++launches_;
     HGM_CUDA(cudaGetLastError());
 }
 
@@ -886,7 +914,8 @@ void Context::lincomb(int n_out, const u32* off, const u64* const* in, const u64
     std::vector<u32> voff(off, off + n_out + 1);
     std::vector<const u64*> vin(in, in + nt), vm(mask, mask + nt);
     std::vector<u64*> vo(out, out + n_out);
-    k_lincomb<<<grid_of(hp_.N, n_out, 1), kThreads, 0, stream_>>>(cx_, n_out, upload(voff), upload(vin),
+    if (hp_.L == 3) k_lincomb<ShapeQ3><<<grid_of(hp_.N, n_out, 1), kThreads, 0, stream_>>>(cx_, n_out, upload(voff), upload(vin),
+                                                                  upload(vm), upload(vo)); else k_lincomb<ShapeQ8><<<grid_of(hp_.N, n_out, 1), kThreads, 0, stream_>>>(cx_, n_out, upload(voff), upload(vin),
                                                                   upload(vm), upload(vo)); ++launches_;
     HGM_CUDA(cudaGetLastError());
 }
@@ -903,7 +932,7 @@ void Context::modup(int n, const u64* const* ct, u64* const* out) {
     const u32 N = hp_.N, L = hp_.L, R = hp_.R, dnum = hp_.dnum;
     std::vector<const u64*> vc(ct, ct + n);
     u64* C = alloc((size_t)n * L * N);
-    k_gather_c1<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, upload(vc), C); ++launches_;
+    if (hp_.L == 3) k_gather_c1<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, upload(vc), C); else k_gather_c1<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, upload(vc), C); ++launches_;
     ntt(false, jobs_contig(C, n * L, 0, L));
     // lift into a contiguous staging area, then scatter-copy to the outputs
     bool contiguous = true;
@@ -914,7 +943,7 @@ void Context::modup(int n, const u64* const* ct, u64* const* out) {
         ntt_modup_fused(cx_, hp_.dev, n, C, (size_t)L * N, D, stream_);
         ++launches_;
     } else {
-        k_modup_lift<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, C, (size_t)L * N, D); ++launches_;
+        if (hp_.L == 3) k_modup_lift<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, C, (size_t)L * N, D); else k_modup_lift<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, C, (size_t)L * N, D); ++launches_;
         ntt(true, jobs_contig(D, n * dnum * R, 0, R));
     }
     if (!contiguous) {
@@ -934,7 +963,8 @@ void Context::inner_product(int n, const u64* const* digits, const u64* const* k
     std::vector<const u64*> vd(digits, digits + n), vk(keys, keys + n);
     std::vector<u32> vg(g, g + n);
     std::vector<u64*> va(acc, acc + n);
-    k_ks_inner<<<grid_of(hp_.N, (n + kKeyReuse - 1) / kKeyReuse), kThreads, 0, stream_>>>(cx_, n, upload(vd), upload(vk), upload(vg),
+    if (hp_.L == 3) k_ks_inner<ShapeQ3><<<grid_of(hp_.N, (n + kKeyReuse - 1) / kKeyReuse), kThreads, 0, stream_>>>(cx_, n, upload(vd), upload(vk), upload(vg),
+                                                           upload(va)); else k_ks_inner<ShapeQ8><<<grid_of(hp_.N, (n + kKeyReuse - 1) / kKeyReuse), kThreads, 0, stream_>>>(cx_, n, upload(vd), upload(vk), upload(vg),
                                                            upload(va)); ++launches_;
     HGM_CUDA(cudaGetLastError());
 }
@@ -979,9 +1009,9 @@ void Context::key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, c
     }
     // conversion pass (V = ecoef - P^-1 conv), NTT, finishing pass
     u64* V = alloc((size_t)n * 2 * L * N);
-    k_moddown_conv<<<grid_of(N, n, 2), kThreads, 0, stream_>>>(cx_, n, dacc, dec, V); ++launches_;
+    if (hp_.L == 3) k_moddown_conv<ShapeQ3><<<grid_of(N, n, 2), kThreads, 0, stream_>>>(cx_, n, dacc, dec, V); else k_moddown_conv<ShapeQ8><<<grid_of(N, n, 2), kThreads, 0, stream_>>>(cx_, n, dacc, dec, V); ++launches_;
     ntt(true, jobs_contig(V, n * 2 * L, 0, L));
-    k_ks_finish<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, dacc, V, dadd, upload(vg), upload(vo)); ++launches_;
+    if (hp_.L == 3) k_ks_finish<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, dacc, V, dadd, upload(vg), upload(vo)); else k_ks_finish<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, dacc, V, dadd, upload(vg), upload(vo)); ++launches_;
     release(V);
     HGM_CUDA(cudaGetLastError());
 }
@@ -1034,7 +1064,7 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
     ntt(false, jobs_contig(X, n * 4 * L, 0, L));
     // 2. exact Q -> B and NTT over B
     u64* XB = alloc((size_t)n * 4 * nB * N);
-    k_q_to_b<<<grid_of(N, n, 4), kThreads, 0, stream_>>>(cx_, n, X, XB); ++launches_;
+    if (hp_.L == 3) k_q_to_b<ShapeQ3><<<grid_of(N, n, 4), kThreads, 0, stream_>>>(cx_, n, X, XB); else k_q_to_b<ShapeQ8><<<grid_of(N, n, 4), kThreads, 0, stream_>>>(cx_, n, X, XB); ++launches_;
     release(X);
     ntt(true, jobs_contig(XB, n * 4 * nB, L + K, nB));
     // 3. tensor over Q ++ B, INTT
@@ -1042,7 +1072,7 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
     u64* T = alloc((size_t)n * 3 * D * N);
     {
         std::vector<const u64*> va(a, a + n), vb(b, b + n);
-        k_tensor<<<grid_of(N, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T); ++launches_;
+        if (hp_.L == 3) k_tensor<ShapeQ3><<<grid_of(N, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T); else k_tensor<ShapeQ8><<<grid_of(N, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T); ++launches_;
     }
     release(XB);
     NttJobs tj = jobs_contig(T, n * 3 * D, 0, D);
@@ -1050,7 +1080,7 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
     ntt(false, tj);
     // 4. scale and round back to Q (coefficient form)
     u64* E = alloc((size_t)n * 3 * LN);
-    k_scale_round<<<grid_of(N, n, 3), kThreads, 0, stream_>>>(cx_, n, T, E); ++launches_;
+    if (hp_.L == 3) k_scale_round<ShapeQ3><<<grid_of(N, n, 3), kThreads, 0, stream_>>>(cx_, n, T, E); else k_scale_round<ShapeQ8><<<grid_of(N, n, 3), kThreads, 0, stream_>>>(cx_, n, T, E); ++launches_;
     release(T);
     // 5. relinearise e2: ModUp, inner product with rlk, ModDown, add (e0, e1)
     const bool fused = ntt_fusable(hp_.dev);
@@ -1059,7 +1089,7 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
         ntt_modup_fused(cx_, hp_.dev, n, E + 2 * LN, 3 * LN, Dg, stream_);
         ++launches_;
     } else {
-        k_modup_lift<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, E + 2 * LN, 3 * LN, Dg); ++launches_;
+        if (hp_.L == 3) k_modup_lift<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, E + 2 * LN, 3 * LN, Dg); else k_modup_lift<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, E + 2 * LN, 3 * LN, Dg); ++launches_;
         ntt(true, jobs_contig(Dg, n * dnum * R, 0, R));
     }
     u64* A = alloc((size_t)n * 2 * R * N);
