@@ -69,7 +69,7 @@ __global__ void k_encode_scatter(DevCtx cx, u32 n, const i64* vals,
 
 // oracle encrypt(): sample u, e0, e1; c0 = e0 + Delta m, c1 = e1 (coefficient form)
 template <typename SH>
-__global__ void k_enc_lift(DevCtx cx, u32 n, const u64* m, const u64* ctr,
+__global__ void __launch_bounds__(kThreads, 4) k_enc_lift(DevCtx cx, u32 n, const u64* m, const u64* ctr,
                            u64* U, u64* const* out) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = SH::L;
@@ -132,7 +132,7 @@ __global__ void k_dec_phase(DevCtx cx, u32 n, const u64* const* in,
 
 // oracle decrypt(): m = round(t x / Q) mod t via sum_i [x_i (Q/q_i)^-1]_{q_i} t/q_i
 template <typename SH>
-__global__ void k_dec_round(DevCtx cx, u32 n, const u64* X, u64* M) {
+__global__ void __launch_bounds__(kThreads, 4) k_dec_round(DevCtx cx, u32 n, const u64* X, u64* M) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = SH::L;
     ITEM_LOOP {
@@ -344,7 +344,7 @@ __global__ void k_ks_inner(DevCtx cx, u32 n, const u64* const* D,
 // so that NTT(V) + P^-1 acc = (acc - NTT(conv)) P^-1 + NTT(ecoef) exactly (the NTT
 // is linear mod q_i): relinearisation adds e0, e1 without transforming them apart.
 template <typename SH>
-__global__ void k_moddown_conv(DevCtx cx, u32 n, const u64* const* acc, const u64* const* ecoef, u64* V) {
+__global__ void __launch_bounds__(kThreads, 4) k_moddown_conv(DevCtx cx, u32 n, const u64* const* acc, const u64* const* ecoef, u64* V) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = SH::L, K = SH::K, R = SH::R;
     ITEM_LOOP {
@@ -405,7 +405,7 @@ __global__ void k_ks_finish(DevCtx cx, u32 n, const u64* const* acc, const u64* 
 // ---------------------------------------------------------------- tensoring
 // oracle q_to_b(): exact centred conversion of 4 polys per item, X: [n][4][L][N]
 template <typename SH>
-__global__ void k_q_to_b(DevCtx cx, u32 n, const u64* X, u64* XB) {
+__global__ void __launch_bounds__(kThreads, 4) k_q_to_b(DevCtx cx, u32 n, const u64* X, u64* XB) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = SH::L, K = SH::K, nB = SH::nB;
     ITEM_LOOP {
@@ -464,7 +464,7 @@ __global__ void k_tensor(DevCtx cx, u32 n, const u64* const* A,
 
 // oracle scale_round(): round(t x / Q) from Q ++ B residues, then exact B -> Q
 template <typename SH>
-__global__ void k_scale_round(DevCtx cx, u32 n, const u64* T, u64* E) {
+__global__ void __launch_bounds__(kThreads, 4) k_scale_round(DevCtx cx, u32 n, const u64* T, u64* E) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = SH::L, K = SH::K, nB = SH::nB, D = L + nB;
     ITEM_LOOP {
