@@ -197,13 +197,24 @@ __global__ void k_lincomb(DevCtx cx, u32 n, const u32* off,
         for (size_t w = (size_t)blockIdx.x * blockDim.x + threadIdx.x; w < W; w += (size_t)gridDim.x * blockDim.x) {
             const size_t wl = w < LN ? w : w - LN;
             const Prime& P = dp->pr[wl / N];
-            u64 acc = 0;
+            // exact 128-bit accumulation; reduced after every 3 masked products
+            // (the sum stays below 2^(s+62), reduce_acc's range)
+            Acc acc;
+            u32 pending = 0;
             for (u32 t = t0; t < t1; ++t) {
-                u64 v = in[t][w];
-                if (mask[t]) v = mul_mod(v, mask[t][wl], P);
-                acc = add_mod(acc, v, P.q);
+                const u64 v = in[t][w];
+                if (mask[t]) {
+                    acc.mac(v, mask[t][wl]);
+                    if (++pending == 3) {
+                        acc.lo = reduce_acc(acc, P);
+                        acc.hi = 0;
+                        pending = 0;
+                    }
+                } else {
+                    acc.add(v);
+                }
             }
-            o[w] = acc;
+            o[w] = reduce_acc(acc, P);
         }
     }
 }

@@ -147,6 +147,10 @@ HD u64 mul_mod(u64 a, u64 b, const Prime& p) {
 // the sum stays below 2^(s+62) (4 products of 60-bit residues, 9 of 55-bit).
 struct Acc {
     u64 lo = 0, hi = 0;
+    HD void add(u64 v) {
+        lo += v;
+        hi += (lo < v);
+    }
     HD void mac(u64 a, u64 b) {
         const u64 pl = a * b, ph = mulhi64(a, b);
         lo += pl;
