@@ -943,8 +943,17 @@ void Context::modup(int n, const u64* const* ct, u64* const* out) {
     const u32 N = hp_.N, L = hp_.L, R = hp_.R, dnum = hp_.dnum;
     std::vector<const u64*> vc(ct, ct + n);
     u64* C = alloc((size_t)n * L * N);
-    if (hp_.L == 3) k_gather_c1<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, upload(vc), C); else k_gather_c1<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, upload(vc), C); ++launches_;
-    ntt(false, jobs_contig(C, n * L, 0, L));
+    if (ntt_fusable_size(hp_.dev)) {  // out-of-place INTT of the c1 limbs
+        std::vector<const u64*> src((size_t)n * L);
+        for (int i = 0; i < n; ++i)
+            for (u32 l = 0; l < L; ++l) src[(size_t)i * L + l] = ct[i] + (size_t)(L + l) * N;
+        NttJobs cj = jobs_contig(C, n * L, 0, L);
+        cj.src = upload(src);
+        ntt(false, cj);
+    } else {
+        if (hp_.L == 3) k_gather_c1<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, upload(vc), C); else k_gather_c1<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, upload(vc), C); ++launches_;
+        ntt(false, jobs_contig(C, n * L, 0, L));
+    }
     // lift into a contiguous staging area, then scatter-copy to the outputs
     bool contiguous = true;
     for (int i = 1; i < n; ++i)
@@ -1059,9 +1068,17 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
     }
     const u32 N = hp_.N, L = hp_.L, K = hp_.K, R = hp_.R, nB = hp_.nB, dnum = hp_.dnum;
     const size_t LN = (size_t)L * N;
-    // 1. gather (a.c0, a.c1, b.c0, b.c1) and INTT
+    // 1. (a.c0, a.c1, b.c0, b.c1) to the coefficient domain (out-of-place INTT)
     u64* X = alloc((size_t)n * 4 * LN);
-    {
+    if (ntt_fusable_size(hp_.dev)) {
+        std::vector<const u64*> src((size_t)n * 4 * L);
+        for (int i = 0; i < n; ++i)
+            for (u32 w = 0; w < 4 * L; ++w)
+                src[(size_t)i * 4 * L + w] = (w < 2 * L ? a[i] + (size_t)w * N : b[i] + (size_t)(w - 2 * L) * N);
+        NttJobs xj = jobs_contig(X, n * 4 * L, 0, L);
+        xj.src = upload(src);
+        ntt(false, xj);
+    } else {
         std::vector<const u64*> src((size_t)2 * n);
         std::vector<u64*> dst((size_t)2 * n);
         for (int i = 0; i < n; ++i) {
@@ -1071,8 +1088,8 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
             dst[2 * i + 1] = X + (size_t)i * 4 * LN + 2 * LN;
         }
         k_copy<<<grid_of(N, 2 * n), kThreads, 0, stream_>>>(2 * n, ct_words(), upload(src), upload(dst)); ++launches_;
+        ntt(false, jobs_contig(X, n * 4 * L, 0, L));
     }
-    ntt(false, jobs_contig(X, n * 4 * L, 0, L));
     // 2. exact Q -> B and NTT over B
     u64* XB = alloc((size_t)n * 4 * nB * N);
     if (hp_.L == 3) k_q_to_b<ShapeQ3><<<grid_of(N, n, 4), kThreads, 0, stream_>>>(cx_, n, X, XB); else k_q_to_b<ShapeQ8><<<grid_of(N, n, 4), kThreads, 0, stream_>>>(cx_, n, X, XB); ++launches_;

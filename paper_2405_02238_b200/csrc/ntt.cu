@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <stdexcept>
 
 namespace hgm {
 
@@ -318,7 +319,8 @@ __device__ __forceinline__ void prefetch_block(u64* buf, const u64* g) {
 }
 
 struct WorkItem {
-    u64* g;
+    u64* g;        // destination block
+    const u64* s;  // source block (== g unless out of place)
     int prime, blk;
 };
 __device__ __forceinline__ WorkItem work_item(const NttJobs& jobs, u32 v, int sub, u32 N, int LB) {
@@ -327,6 +329,7 @@ __device__ __forceinline__ WorkItem work_item(const NttJobs& jobs, u32 v, int su
     w.blk = (int)(v % sub);
     w.prime = jv.prime;
     w.g = jv.ptr + ((size_t)w.blk << LB);
+    w.s = jobs.src ? jobs.src[v / sub] + ((size_t)w.blk << LB) : w.g;
     return w;
 }
 
@@ -347,16 +350,16 @@ __global__ void __launch_bounds__((1 << LB) / kElems, 1)
     u32 v = blockIdx.x;
     if (v >= total) return;
     WorkItem cur = work_item(jobs, v, sub, N, LB);
-    prefetch_block<LB>(buf0, cur.g);
+    prefetch_block<LB>(buf0, cur.s);
     cp_async_commit();
     int cached_prime = -1, cached_blk = -1;
     for (int slot = 0; v < total; v += gridDim.x, slot ^= 1) {
         u64* b = slot ? buf1 : buf0;
         const u32 vn = v + gridDim.x;
-        WorkItem nxt{nullptr, 0, 0};
+        WorkItem nxt{nullptr, nullptr, 0, 0};
         if (vn < total) {
             nxt = work_item(jobs, vn, sub, N, LB);
-            prefetch_block<LB>(slot ? buf0 : buf1, nxt.g);
+            prefetch_block<LB>(slot ? buf0 : buf1, nxt.s);
         }
         cp_async_commit();
         const u64 q = dp->pr[cur.prime].q;
@@ -528,16 +531,16 @@ __global__ void __launch_bounds__((1 << LB) / kElems, 1)
     u32 v = blockIdx.x;
     if (v >= total) return;
     WorkItem cur = work_item(jobs, v, sub, N, LB);
-    prefetch_block<LB>(buf0, cur.g);
+    prefetch_block<LB>(buf0, cur.s);
     cp_async_commit();
     int cached_prime = -1, cached_blk = -1;
     for (int slot = 0; v < total; v += gridDim.x, slot ^= 1) {
         u64* b = slot ? buf1 : buf0;
         const u32 vn = v + gridDim.x;
-        WorkItem nxt{nullptr, 0, 0};
+        WorkItem nxt{nullptr, nullptr, 0, 0};
         if (vn < total) {
             nxt = work_item(jobs, vn, sub, N, LB);
-            prefetch_block<LB>(slot ? buf0 : buf1, nxt.g);
+            prefetch_block<LB>(slot ? buf0 : buf1, nxt.s);
         }
         cp_async_commit();
         const Prime& P = dp->pr[cur.prime];
@@ -687,6 +690,7 @@ void ntt_upload_params(int pid, const DevParams& p) {
 
 void ntt_forward(const DevCtx& cx, const DevParams& hp, const NttJobs& jobs_in, cudaStream_t s) {
     if (jobs_in.count == 0) return;
+    if (jobs_in.src && hp.logN > 13) throw std::logic_error("out-of-place NTT needs whole-limb blocks");
     NttJobs jobs = jobs_in;
     jobs.pack();
     if (hp.logN == 13) {
@@ -701,6 +705,7 @@ void ntt_forward(const DevCtx& cx, const DevParams& hp, const NttJobs& jobs_in, 
 
 void ntt_inverse(const DevCtx& cx, const DevParams& hp, const NttJobs& jobs_in, cudaStream_t s) {
     if (jobs_in.count == 0) return;
+    if (jobs_in.src && hp.logN > 13) throw std::logic_error("out-of-place NTT needs whole-limb blocks");
     NttJobs jobs = jobs_in;
     jobs.pack();
     if (hp.logN == 13) {

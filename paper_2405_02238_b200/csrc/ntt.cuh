@@ -24,6 +24,9 @@ namespace hgm {
 struct NttJobs {
     u64* base = nullptr;
     u64* const* ptrs = nullptr;
+    // optional out-of-place source: job j reads src[j] and writes its ptr/base
+    // slot (whole-limb transforms only, N <= 8192)
+    const u64* const* src = nullptr;
     u32 count = 0;
     u32 period = 1;
     unsigned char prime[32] = {0};  // host-side pattern
@@ -44,6 +47,8 @@ void ntt_inverse(const DevCtx& cx, const DevParams& hp, const NttJobs& jobs, cud
 //  * ModDown: out[item] = (acc - NTT(conv(P-part))) P^-1 (+ NTT(addc)) (+ addn[galois]),
 //    acc's P limbs already inverse-transformed.  Pointer arrays live on the device.
 bool ntt_fusable(const DevParams& hp);
+// whole-limb transforms (N <= 8192): out-of-place jobs allowed
+inline bool ntt_fusable_size(const DevParams& hp) { return hp.logN <= 13; }
 void ntt_modup_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* C, size_t c_stride, u64* D,
                      cudaStream_t s);
 void ntt_moddown_fused(const DevCtx& cx, const DevParams& hp, int n, u64* const* acc, const u64* const* addc,
