@@ -77,11 +77,11 @@ struct NoLoad {
     __device__ u64 operator()(int) const { return 0; }
 };
 
-template <int LB, int S0, int R, bool kCached, bool kFromGlobal = false, typename Ld = NoLoad>
+template <int LB, int S0, int R, bool kCached, bool kFromGlobal = false, typename Ld = NoLoad, int E = kElems>
 __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_cache,
                                           const u64* __restrict__ w_tab, const u64* __restrict__ ws_tab,
                                           u64 q, int pre, int blk, const Ld& ld = Ld()) {
-    constexpr int NB = 1 << LB, T = NB / kElems, G = (NB >> R) / T;
+    constexpr int NB = 1 << LB, T = NB / E, G = (NB >> R) / T;
     constexpr int LT_FIRST = LB - 1 - S0, LT_MIN = LT_FIRST - (R - 1);
     const u64 q3 = q << 1, q4 = q << 1;  // 2q (Harvey bounds)
 #pragma unroll
@@ -131,11 +131,11 @@ __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_ca
 // Inverse local stages with half-sizes 2^(LT_LO + r), r < R; twiddle
 //   2^(logN-lt-1) + (blk << (LB-lt-1)) + (block << (R-r-1)) + c,  lt = LT_LO + r
 //   cache index (1 << (LB-lt-1)) - 1 + (block << (R-r-1)) + c     (LB-lt-1 < 9)
-template <int LB, int LT_LO, int R, bool kCached>
+template <int LB, int LT_LO, int R, bool kCached, int E = kElems>
 __device__ __forceinline__ void inv_round(u64* sm, const u64* __restrict__ tw_cache,
                                           const u64* __restrict__ w_tab, const u64* __restrict__ ws_tab,
                                           u64 q, int logN, int blk) {
-    constexpr int NB = 1 << LB, T = NB / kElems, G = (NB >> R) / T;
+    constexpr int NB = 1 << LB, T = NB / E, G = (NB >> R) / T;
     const u64 q4 = q << 1;  // 2q (Harvey bounds)
 #pragma unroll
     for (int gg = 0; gg < G; ++gg) {
@@ -184,8 +184,9 @@ __device__ __forceinline__ void inv_round(u64* sm, const u64* __restrict__ tw_ca
 // outer = pre; inverse: base(s) = 2^(logN-LB+s) + (blk << s) for the stage
 // with m-offset 2^s inside the block).
 __device__ __forceinline__ void fill_tw_cache(u64* cache, const u64* __restrict__ w_tab,
-                                              const u64* __restrict__ ws_tab, int outer, int blk) {
-    for (int i = threadIdx.x; i < kTwCache; i += blockDim.x) {
+                                              const u64* __restrict__ ws_tab, int outer, int blk,
+                                              int count = kTwCache) {
+    for (int i = threadIdx.x; i < count; i += blockDim.x) {
         const int s = 31 - __clz(i + 1);  // i + 1 in [2^s, 2^(s+1))
         const int c = i + 1 - (1 << s);
         const int g = (1 << (outer + s)) + (blk << s) + c;
@@ -217,10 +218,10 @@ __device__ __forceinline__ JobView job_of(const NttJobs& jobs, u32 j, u32 N) {
 // Forward: the last Cooley-Tukey stage (t = 1, m = N/2) pairs adjacent
 // residues, i.e. exactly the 16-byte vector each thread stores, so it is
 // fused into the coalesced store together with the reduction to [0, q).
-template <int LB>
+template <int LB, int E = kElems>
 __device__ __forceinline__ void store_last_stage(const u64* sm, u64* g, const u64* __restrict__ w_tab,
                                                  const u64* __restrict__ ws_tab, u64 q, int logN, int blk) {
-    constexpr int NB = 1 << LB, T = NB / kElems;
+    constexpr int NB = 1 << LB, T = NB / E;
     ulonglong2* g2 = reinterpret_cast<ulonglong2*>(g);
     const int tw0 = (1 << (logN - 1)) + (blk << (LB - 1));
 #pragma unroll 4
@@ -237,10 +238,10 @@ __device__ __forceinline__ void store_last_stage(const u64* sm, u64* g, const u6
 }
 
 // Same, handing each finished pair (elements 2i, 2i+1, canonical) to `st`.
-template <int LB, typename St>
+template <int LB, typename St, int E = kElems>
 __device__ __forceinline__ void store_last_stage_io(const u64* sm, const St& st, const u64* __restrict__ w_tab,
                                                     const u64* __restrict__ ws_tab, u64 q, int logN, int blk) {
-    constexpr int NB = 1 << LB, T = NB / kElems;
+    constexpr int NB = 1 << LB, T = NB / E;
     const int tw0 = (1 << (logN - 1)) + (blk << (LB - 1));
     const u64 q2 = q << 1;
 #pragma unroll 4
@@ -253,10 +254,10 @@ __device__ __forceinline__ void store_last_stage_io(const u64* sm, const St& st,
 }
 
 // Inverse: the first Gentleman-Sande stage (t = 1) fused into the coalesced load.
-template <int LB>
+template <int LB, int E = kElems>
 __device__ __forceinline__ void load_first_stage(u64* sm, const u64* g, const u64* __restrict__ w_tab,
                                                  const u64* __restrict__ ws_tab, u64 q, int logN, int blk) {
-    constexpr int NB = 1 << LB, T = NB / kElems;
+    constexpr int NB = 1 << LB, T = NB / E;
     const ulonglong2* g2 = reinterpret_cast<const ulonglong2*>(g);
     const int tw0 = (1 << (logN - 1)) + (blk << (LB - 1));
 #pragma unroll 4
@@ -268,9 +269,9 @@ __device__ __forceinline__ void load_first_stage(u64* sm, const u64* g, const u6
     }
 }
 
-template <int LB>
+template <int LB, int E = kElems>
 __device__ __forceinline__ void load_block(u64* sm, const u64* g) {
-    constexpr int NB = 1 << LB, T = NB / kElems;
+    constexpr int NB = 1 << LB, T = NB / E;
     const ulonglong2* g2 = reinterpret_cast<const ulonglong2*>(g);
 #pragma unroll 4
     for (int i = threadIdx.x; i < NB / 2; i += T) {
@@ -281,9 +282,9 @@ __device__ __forceinline__ void load_block(u64* sm, const u64* g) {
 }
 
 // stores canonical residues from smem values in [0, 2q), optionally scaled
-template <int LB, bool kScale>
+template <int LB, bool kScale, int E = kElems>
 __device__ __forceinline__ void store_block(const u64* sm, u64* g, u64 q, u64 s, u64 ssh) {
-    constexpr int NB = 1 << LB, T = NB / kElems;
+    constexpr int NB = 1 << LB, T = NB / E;
     ulonglong2* g2 = reinterpret_cast<ulonglong2*>(g);
 #pragma unroll 4
     for (int i = threadIdx.x; i < NB / 2; i += T) {
@@ -311,9 +312,9 @@ __device__ __forceinline__ void cp_async8(u64* smem_dst, const u64* gsrc) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
-template <int LB>
+template <int LB, int E = kElems>
 __device__ __forceinline__ void prefetch_block(u64* buf, const u64* g) {
-    constexpr int NB = 1 << LB, T = NB / kElems;
+    constexpr int NB = 1 << LB, T = NB / E;
 #pragma unroll 4
     for (int i = threadIdx.x; i < NB; i += T) cp_async8(buf + pad(i), g + i);
 }
@@ -659,6 +660,87 @@ void launch_block(bool fwd, const DevCtx& cx, const NttJobs& jobs, int sub, cuda
         k_ntt_inv<LB><<<grid, (1 << LB) / kElems, smem, s>>>(cx, jobs, sub);
 }
 
+
+// ---------------------------------------------------------------- 3-CTA variant
+// 256 threads x 32 residues, radix-16 rounds over two groups per thread,
+// 255 cached twiddle pairs (stages < 8), no double buffer: 72 KB of shared
+// memory and <= 85 registers, so three CTAs (24 warps) share an SM.
+constexpr int kElems3 = 32, kTwCache3 = 255;
+
+template <int LB>
+__global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_fwd3(DevCtx cx, NttJobs jobs) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
+    extern __shared__ u64 sm[];
+    u64* cache = sm + smem_words<LB>();
+    const u32 N = dp->N;
+    const int logN = (int)dp->logN;
+    const JobView jv = job_of(jobs, blockIdx.x, N);
+    const u64 q = dp->pr[jv.prime].q;
+    const u64* w = cx.tw + (size_t)jv.prime * 4 * N;
+    u64* g = jv.ptr;
+    const u64* src = jobs.src ? jobs.src[blockIdx.x] : g;
+    fill_tw_cache(cache, w, w + N, 0, 0, kTwCache3);
+    __syncthreads();
+    auto ld = [src](int j) { return __ldcs(src + j); };
+    fwd_round<LB, 0, 4, true, true, decltype(ld), kElems3>(sm, cache, w, w + N, q, 0, 0, ld);
+    __syncthreads();
+    fwd_round<LB, 4, 4, true, false, NoLoad, kElems3>(sm, cache, w, w + N, q, 0, 0);
+    __syncthreads();
+    fwd_round<LB, 8, LB - 9, false, false, NoLoad, kElems3>(sm, cache, w, w + N, q, 0, 0);
+    __syncthreads();
+    store_last_stage<LB, kElems3>(sm, g, w, w + N, q, logN, 0);
+}
+
+template <int LB>
+__global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_inv3(DevCtx cx, NttJobs jobs) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
+    extern __shared__ u64 sm[];
+    u64* cache = sm + smem_words<LB>();
+    const u32 N = dp->N;
+    const int logN = (int)dp->logN;
+    const JobView jv = job_of(jobs, blockIdx.x, N);
+    const Prime& P = dp->pr[jv.prime];
+    const u64 q = P.q;
+    const u64* w = cx.tw + (size_t)jv.prime * 4 * N;
+    u64* g = jv.ptr;
+    const u64* src = jobs.src ? jobs.src[blockIdx.x] : g;
+    fill_tw_cache(cache, w + 2 * N, w + 3 * N, 0, 0, kTwCache3);
+    load_first_stage<LB, kElems3>(sm, src, w + 2 * N, w + 3 * N, q, logN, 0);
+    __syncthreads();
+    inv_round<LB, 1, LB - 9, false, kElems3>(sm, cache, w + 2 * N, w + 3 * N, q, logN, 0);
+    __syncthreads();
+    inv_round<LB, LB - 8, 4, true, kElems3>(sm, cache, w + 2 * N, w + 3 * N, q, logN, 0);
+    __syncthreads();
+    inv_round<LB, LB - 4, 4, true, kElems3>(sm, cache, w + 2 * N, w + 3 * N, q, logN, 0);
+    __syncthreads();
+    store_block<LB, true, kElems3>(sm, g, q, P.ninv, P.ninv_sh);
+}
+
+template <int LB>
+void launch_block3(bool fwd, const DevCtx& cx, const NttJobs& jobs, cudaStream_t s) {
+    const size_t smem = (smem_words<LB>() + 2 * kTwCache3) * sizeof(u64);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_ntt_fwd3<LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_ntt_inv3<LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    if (fwd)
+        k_ntt_fwd3<LB><<<jobs.count, (1 << LB) / kElems3, smem, s>>>(cx, jobs);
+    else
+        k_ntt_inv3<LB><<<jobs.count, (1 << LB) / kElems3, smem, s>>>(cx, jobs);
+}
+
+// Default for whole 2^13 limbs (measured +15% forward, +19% inverse over the
+// persistent 512-thread kernel); HGM_NTT3=0 selects the persistent kernel.
+bool use_ntt3() {
+    static const bool on = [] {
+        const char* e = std::getenv("HGM_NTT3");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 }  // namespace
 
 // The fused variants are exact but measured slower on B200 while the NTT is
@@ -693,7 +775,9 @@ void ntt_forward(const DevCtx& cx, const DevParams& hp, const NttJobs& jobs_in, 
     if (jobs_in.src && hp.logN > 13) throw std::logic_error("out-of-place NTT needs whole-limb blocks");
     NttJobs jobs = jobs_in;
     jobs.pack();
-    if (hp.logN == 13) {
+    if (hp.logN == 13 && use_ntt3()) {
+        launch_block3<13>(true, cx, jobs, s);
+    } else if (hp.logN == 13) {
         launch_block<13>(true, cx, jobs, 1, s);
     } else if (hp.logN == 12) {
         launch_block<12>(true, cx, jobs, 1, s);
@@ -708,7 +792,9 @@ void ntt_inverse(const DevCtx& cx, const DevParams& hp, const NttJobs& jobs_in, 
     if (jobs_in.src && hp.logN > 13) throw std::logic_error("out-of-place NTT needs whole-limb blocks");
     NttJobs jobs = jobs_in;
     jobs.pack();
-    if (hp.logN == 13) {
+    if (hp.logN == 13 && use_ntt3()) {
+        launch_block3<13>(false, cx, jobs, s);
+    } else if (hp.logN == 13) {
         launch_block<13>(false, cx, jobs, 1, s);
     } else if (hp.logN == 12) {
         launch_block<12>(false, cx, jobs, 1, s);
