@@ -342,7 +342,7 @@ def main():
             traffic = None
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": "k_ntt_fwd<13> (forward NTT, N=8192, 64-bit Shoup)",
+                "kernel": "k_ntt_fwd3<13> (forward NTT, N=8192, 64-bit Shoup, 3 CTAs/SM)",
                 "algorithmic_bytes_per_launch": limbs * LIMB_BYTES, "limbs_per_launch": limbs,
                 "inverse_frac": round(limbs * LIMB_BYTES / (intt_ms / 1e3) / 1e9 / peak, 4),
                 "peak_source": peak_src}
