@@ -122,15 +122,31 @@ HD u64 shoup_mul(u64 a, u64 w, u64 ws, u64 q) {
 }
 // Harvey's lazy Shoup product: a * w mod q in [0, 2q), any a < 2^64
 HD u64 shoup_lazy(u64 a, u64 w, u64 ws, u64 q) { return a * w - mulhi64(a, ws) * q; }
-// Shoup product with a 3-multiply quotient: the a_lo*ws_lo partial product is
-// dropped, so the quotient is low by at most 1 and the result lies in [0, 3q).
-// (The NTT is bound by the wide-multiply pipe; this saves 1 of ~6 per butterfly.)
-HD u64 shoup_lazy3(u64 a, u64 w, u64 ws, u64 q) {
-    const u64 a_lo = (u32)a, a_hi = a >> 32, b_lo = (u32)ws, b_hi = ws >> 32;
+// Shoup product whose quotient drops the a_lo*ws_lo partial product: the
+// quotient is low by at most 1, so the result lies in [0, 3q) for any a < 2^64.
+// On sm_100a the quotient is 2 IMAD.WIDE + 1 IMAD.HI instead of 4 IMAD.WIDE
+// (the NTT is bound by the integer multiply pipe).
+HD u64 mulhi64_approx(u64 a, u64 b) {
+#ifdef __CUDA_ARCH__
+    const u32 a0 = (u32)a, a1 = (u32)(a >> 32), b0 = (u32)b, b1 = (u32)(b >> 32);
+    u32 x0, x1, x2, r0, r1;
+    asm("mul.lo.u32 %0, %5, %7;\n\t"
+        "mul.hi.u32 %1, %5, %7;\n\t"
+        "mad.lo.cc.u32 %0, %6, %8, %0;\n\t"
+        "madc.hi.cc.u32 %1, %6, %8, %1;\n\t"
+        "addc.u32 %2, 0, 0;\n\t"
+        "mad.lo.cc.u32 %3, %5, %8, %1;\n\t"
+        "madc.hi.u32 %4, %5, %8, %2;"
+        : "=&r"(x0), "=&r"(x1), "=&r"(x2), "=&r"(r0), "=&r"(r1)
+        : "r"(a1), "r"(a0), "r"(b0), "r"(b1));
+    return ((u64)r1 << 32) | r0;
+#else
+    const u64 a_lo = (u32)a, a_hi = a >> 32, b_lo = (u32)b, b_hi = b >> 32;
     const u64 m1 = a_hi * b_lo, m2 = a_lo * b_hi;
-    const u64 qh = a_hi * b_hi + (m1 >> 32) + (m2 >> 32) + (((m1 & 0xffffffffULL) + (m2 & 0xffffffffULL)) >> 32);
-    return a * w - qh * q;
+    return a_hi * b_hi + (m1 >> 32) + (m2 >> 32) + (((m1 & 0xffffffffULL) + (m2 & 0xffffffffULL)) >> 32);
+#endif
 }
+HD u64 shoup_lazy3(u64 a, u64 w, u64 ws, u64 q) { return a * w - mulhi64_approx(a, ws) * q; }
 // x in [0, 2m) -> [0, m)   (m = q or 2q)
 HD u64 reduce_once(u64 x, u64 m) { return x >= m ? x - m : x; }
 // a * b mod q for a, b < q < 2^62 (shifted Barrett, at most two corrections)

@@ -39,10 +39,11 @@ __device__ __forceinline__ void fwd_stage(u64 (&x)[1 << R], u64 q, u64 q3, u64 q
         tw(r, c, w, ws);
 #pragma unroll
         for (int u = 0; u < h; ++u) {
-            // Harvey butterfly: values in [0, 4q), U in [0, 2q), V in [0, 2q)
+            // lazy butterfly: values in [0, 8q), U in [0, 4q), V in [0, 3q)
+            // (q < 2^61; shoup_lazy3's quotient is low by at most 1)
             const int k = c * 2 * h + u;
-            const u64 U = reduce_once(x[k], q3);
-            const u64 V = shoup_lazy(x[k + h], w, ws, q);
+            const u64 U = reduce_once(x[k], q4);
+            const u64 V = shoup_lazy3(x[k + h], w, ws, q);
             x[k] = U + V;
             x[k + h] = U - V + q3;
         }
@@ -60,11 +61,11 @@ __device__ __forceinline__ void inv_stage(u64 (&x)[1 << R], u64 q, u64 q4, const
         tw(r, c, w, ws);
 #pragma unroll
         for (int u = 0; u < h; ++u) {
-            // Harvey butterfly: inputs and outputs in [0, 2q)
+            // lazy butterfly: inputs and outputs in [0, 4q)
             const int k = c * 2 * h + u;
             const u64 U = x[k], V = x[k + h];
             x[k] = reduce_once(U + V, q4);
-            x[k + h] = shoup_lazy(U - V + q4, w, ws, q);
+            x[k + h] = shoup_lazy3(U - V + q4, w, ws, q);
         }
     }
     if constexpr (r + 1 < R) inv_stage<R, r + 1>(x, q, q4, tw);
@@ -83,7 +84,7 @@ __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_ca
                                           u64 q, int pre, int blk, const Ld& ld = Ld()) {
     constexpr int NB = 1 << LB, T = NB / E, G = (NB >> R) / T;
     constexpr int LT_FIRST = LB - 1 - S0, LT_MIN = LT_FIRST - (R - 1);
-    const u64 q3 = q << 1, q4 = q << 1;  // 2q (Harvey bounds)
+    const u64 q3 = 3 * q, q4 = q << 2;  // lazy bounds (fwd_stage)
 #pragma unroll
     for (int gg = 0; gg < G; ++gg) {
         const int gi = threadIdx.x + gg * T;
@@ -136,7 +137,7 @@ __device__ __forceinline__ void inv_round(u64* sm, const u64* __restrict__ tw_ca
                                           const u64* __restrict__ w_tab, const u64* __restrict__ ws_tab,
                                           u64 q, int logN, int blk) {
     constexpr int NB = 1 << LB, T = NB / E, G = (NB >> R) / T;
-    const u64 q4 = q << 1;  // 2q (Harvey bounds)
+    const u64 q4 = q << 2;  // lazy bound 4q (inv_stage)
 #pragma unroll
     for (int gg = 0; gg < G; ++gg) {
         const int gi = threadIdx.x + gg * T;
@@ -227,8 +228,8 @@ __device__ __forceinline__ void store_last_stage(const u64* sm, u64* g, const u6
 #pragma unroll 4
     for (int i = threadIdx.x; i < NB / 2; i += T) {
         const u64 w = __ldg(w_tab + tw0 + i), ws = __ldg(ws_tab + tw0 + i);
-        const u64 q2 = q << 1;
-        const u64 U = reduce_once(sm[pad(2 * i)], q2);
+        const u64 q2 = q << 1, q4 = q << 2;
+        const u64 U = reduce_once(reduce_once(sm[pad(2 * i)], q4), q2);  // [0, 8q) -> [0, 2q)
         const u64 V = shoup_lazy(sm[pad(2 * i + 1)], w, ws, q);
         ulonglong2 v;
         v.x = reduce_once(reduce_once(U + V, q2), q);
@@ -243,11 +244,11 @@ __device__ __forceinline__ void store_last_stage_io(const u64* sm, const St& st,
                                                     const u64* __restrict__ ws_tab, u64 q, int logN, int blk) {
     constexpr int NB = 1 << LB, T = NB / E;
     const int tw0 = (1 << (logN - 1)) + (blk << (LB - 1));
-    const u64 q2 = q << 1;
+    const u64 q2 = q << 1, q4 = q << 2;
 #pragma unroll 4
     for (int i = threadIdx.x; i < NB / 2; i += T) {
         const u64 w = __ldg(w_tab + tw0 + i), ws = __ldg(ws_tab + tw0 + i);
-        const u64 U = reduce_once(sm[pad(2 * i)], q2);
+        const u64 U = reduce_once(reduce_once(sm[pad(2 * i)], q4), q2);  // [0, 8q) -> [0, 2q)
         const u64 V = shoup_lazy(sm[pad(2 * i + 1)], w, ws, q);
         st(i, reduce_once(reduce_once(U + V, q2), q), reduce_once(reduce_once(U - V + q2, q2), q));
     }
@@ -281,7 +282,7 @@ __device__ __forceinline__ void load_block(u64* sm, const u64* g) {
     }
 }
 
-// stores canonical residues from smem values in [0, 2q), optionally scaled
+// stores canonical residues from smem values in [0, 4q), optionally scaled
 template <int LB, bool kScale, int E = kElems>
 __device__ __forceinline__ void store_block(const u64* sm, u64* g, u64 q, u64 s, u64 ssh) {
     constexpr int NB = 1 << LB, T = NB / E;
@@ -293,8 +294,8 @@ __device__ __forceinline__ void store_block(const u64* sm, u64* g, u64 q, u64 s,
             v.x = shoup_mul(sm[pad(2 * i)], s, ssh, q);
             v.y = shoup_mul(sm[pad(2 * i + 1)], s, ssh, q);
         } else {
-            v.x = reduce_once(sm[pad(2 * i)], q);
-            v.y = reduce_once(sm[pad(2 * i + 1)], q);
+            v.x = reduce_once(reduce_once(sm[pad(2 * i)], q << 1), q);
+            v.y = reduce_once(reduce_once(sm[pad(2 * i + 1)], q << 1), q);
         }
         g2[i] = v;
     }
