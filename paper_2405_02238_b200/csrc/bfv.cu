@@ -25,11 +25,14 @@ constexpr int kThreads = 256;
 // RNS shapes of the parameter sets, as compile-time constants so per-thread
 // residue arrays unroll into registers (set 0 and 2: L 3 / K 1 / B 4 / dnum 3;
 // set 1: L 8 / K 4 / B 9 / dnum 2).
+// S: digit width of the column accumulator (residues < 2^(2S)).
 struct ShapeQ3 {
     static constexpr u32 L = 3, K = 1, nB = 4, dnum = 3, A = 1, R = 4;
+    static constexpr int S = 30;  // 60-bit primes
 };
 struct ShapeQ8 {
     static constexpr u32 L = 8, K = 4, nB = 9, dnum = 2, A = 4, R = 12;
+    static constexpr int S = 28;  // 55-bit primes
 };
 // items per launch sequence: bounds temporaries and staging uploads
 constexpr int kChunkEnc = 256, kChunkDec = 1024, kChunkLin = 8192, kChunkKs = 1024, kChunkMult = 128;
@@ -199,22 +202,22 @@ __global__ void k_lincomb(DevCtx cx, u32 n, const u32* off,
             const Prime& P = dp->pr[wl / N];
             // exact 128-bit accumulation; reduced after every 3 masked products
             // (the sum stays below 2^(s+62), reduce_acc's range)
-            Acc acc;
+            Cols acc;
             u32 pending = 0;
             for (u32 t = t0; t < t1; ++t) {
                 const u64 v = in[t][w];
                 if (mask[t]) {
-                    acc.mac(v, mask[t][wl]);
+                    acc.mac(split<SH::S>(v), split<SH::S>(mask[t][wl]));
                     if (++pending == 3) {
-                        acc.lo = reduce_acc(acc, P);
-                        acc.hi = 0;
+                        acc.c0 = reduce_acc(acc.fold<SH::S>(), P);
+                        acc.c1 = acc.c2 = 0;
                         pending = 0;
                     }
                 } else {
-                    acc.add(v);
+                    acc.add<SH::S>(v);
                 }
             }
-            o[w] = reduce_acc(acc, P);
+            o[w] = reduce_acc(acc.fold<SH::S>(), P);
         }
     }
 }
@@ -275,12 +278,12 @@ __global__ void k_modup_lift(DevCtx cx, u32 n, const u64* C, size_t c_stride,
                         if (A == 1) {
                             v = centred_lift(y[0], dp->pr[dg].q, qr);  // (Q_d/q_i) = 1
                         } else {
-                            Acc s;
+                            Cols s;
                             for (u32 a = 0; a < A; ++a) {
                                 const u32 i = dg * A + a;
-                                s.mac(centred_lift(y[a], dp->pr[i].q, qr), dp->dg_hat[i][r]);
+                                s.mac(split<SH::S>(centred_lift(y[a], dp->pr[i].q, qr)), split<SH::S>(dp->dg_hat[i][r]));
                             }
-                            v = reduce_acc(s, dp->pr[r]);
+                            v = reduce_acc(s.fold<SH::S>(), dp->pr[r]);
                         }
                     }
                     d[((size_t)dg * R + r) * N + j] = v;
@@ -311,22 +314,22 @@ __global__ void k_ks_inner(DevCtx cx, u32 n, const u64* const* D,
             const u32 src = ge == 1 ? j : galois_src(j, ge, logN);
             for (u32 r = 0; r < R; ++r) {
                 const Prime& P = dp->pr[r];
-                u64 k0[4], k1[4];
+                Dig<SH::S> k0[4], k1[4];
                 for (u32 dg = 0; dg < dnum; ++dg) {
-                    k0[dg] = __ldg(k + (((size_t)dg * 2 + 0) * R + r) * N + j);
-                    k1[dg] = __ldg(k + (((size_t)dg * 2 + 1) * R + r) * N + j);
+                    k0[dg] = split<SH::S>(__ldg(k + (((size_t)dg * 2 + 0) * R + r) * N + j));
+                    k1[dg] = split<SH::S>(__ldg(k + (((size_t)dg * 2 + 1) * R + r) * N + j));
                 }
                 for (u32 u = 0; u < same; ++u) {
                     const u64* d = D[i0 + u];
-                    Acc a0, a1;  // 128-bit lazy accumulation, one reduction per output
+                    Cols a0, a1;  // column accumulation, one reduction per output
                     for (u32 dg = 0; dg < dnum; ++dg) {
-                        const u64 x = d[((size_t)dg * R + r) * N + src];
+                        const Dig<SH::S> x = split<SH::S>(d[((size_t)dg * R + r) * N + src]);
                         a0.mac(x, k0[dg]);
                         a1.mac(x, k1[dg]);
                     }
                     u64* a = acc[i0 + u];
-                    a[(size_t)r * N + j] = reduce_acc(a0, P);
-                    a[((size_t)R + r) * N + j] = reduce_acc(a1, P);
+                    a[(size_t)r * N + j] = reduce_acc(a0.fold<SH::S>(), P);
+                    a[((size_t)R + r) * N + j] = reduce_acc(a1.fold<SH::S>(), P);
                 }
             }
             for (u32 u = same; u < cnt; ++u) {  // rest of the group: own key
@@ -336,14 +339,14 @@ __global__ void k_ks_inner(DevCtx cx, u32 n, const u64* const* D,
                 const u64* d = D[i0 + u];
                 u64* a = acc[i0 + u];
                 for (u32 r = 0; r < R; ++r) {
-                    Acc a0, a1;
+                    Cols a0, a1;
                     for (u32 dg = 0; dg < dnum; ++dg) {
-                        const u64 x = d[((size_t)dg * R + r) * N + su];
-                        a0.mac(x, __ldg(kk + (((size_t)dg * 2 + 0) * R + r) * N + j));
-                        a1.mac(x, __ldg(kk + (((size_t)dg * 2 + 1) * R + r) * N + j));
+                        const Dig<SH::S> x = split<SH::S>(d[((size_t)dg * R + r) * N + su]);
+                        a0.mac(x, split<SH::S>(__ldg(kk + (((size_t)dg * 2 + 0) * R + r) * N + j)));
+                        a1.mac(x, split<SH::S>(__ldg(kk + (((size_t)dg * 2 + 1) * R + r) * N + j)));
                     }
-                    a[(size_t)r * N + j] = reduce_acc(a0, dp->pr[r]);
-                    a[((size_t)R + r) * N + j] = reduce_acc(a1, dp->pr[r]);
+                    a[(size_t)r * N + j] = reduce_acc(a0.fold<SH::S>(), dp->pr[r]);
+                    a[((size_t)R + r) * N + j] = reduce_acc(a1.fold<SH::S>(), dp->pr[r]);
                 }
             }
         }
@@ -375,9 +378,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_moddown_conv(DevCtx cx, u32 n, 
                 if (K == 1) {  // P/p_0 = 1: the conversion is the centred lift itself
                     conv = centred_lift(z[0], dp->pr[L].q, q);
                 } else {
-                    Acc s;
-                    for (u32 k = 0; k < K; ++k) s.mac(centred_lift(z[k], dp->pr[L + k].q, q), dp->phat_mod_q[k][i]);
-                    conv = reduce_acc(s, dp->pr[i]);
+                    Cols s;
+                    for (u32 k = 0; k < K; ++k)
+                        s.mac(split<SH::S>(centred_lift(z[k], dp->pr[L + k].q, q)), split<SH::S>(dp->phat_mod_q[k][i]));
+                    conv = reduce_acc(s.fold<SH::S>(), dp->pr[i]);
                 }
                 const u64 scaled = shoup_mul(conv, dp->P_inv_q[i], dp->P_inv_q_sh[i], q);
                 v[(size_t)i * N + j] = sub_mod(ec ? ec[(size_t)i * N + j] : 0, scaled, q);
@@ -431,12 +435,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_q_to_b(DevCtx cx, u32 n, const 
                 fx_add(s, y[i], dp->one_over_q[i]);
             }
             const u64 v = fx_round(s);
+            Dig<SH::S> yd[kMaxL];
+            for (u32 i = 0; i < L; ++i) yd[i] = split<SH::S>(y[i]);
             for (u32 k = 0; k < nB; ++k) {
                 // sum_i y_i (Q/q_i) - v Q  (mod b_k), one reduction
-                Acc a;
-                for (u32 i = 0; i < L; ++i) a.mac(y[i], dp->qhat_mod_b[i][k]);
-                a.mac(v, dp->neg_Q_mod_b[k]);
-                xb[(size_t)k * N + j] = reduce_acc(a, dp->pr[L + K + k]);
+                Cols a;
+                for (u32 i = 0; i < L; ++i) a.mac(yd[i], split<SH::S>(dp->qhat_mod_b[i][k]));
+                a.mac(split<SH::S>(v), split<SH::S>(dp->neg_Q_mod_b[k]));
+                xb[(size_t)k * N + j] = reduce_acc(a.fold<SH::S>(), dp->pr[L + K + k]);
             }
         }
     }
@@ -465,10 +471,16 @@ __global__ void k_tensor(DevCtx cx, u32 n, const u64* const* A,
             P = &dp->pr[L + K + (d - L)];
         }
         COEF_LOOP {
-            const u64 x0 = a0[j], x1 = a1[j], y0 = b0[j], y1 = b1[j];
-            t0[j] = mul_mod(x0, y0, *P);
-            t1[j] = add_mod(mul_mod(x0, y1, *P), mul_mod(x1, y0, *P), P->q);
-            t2[j] = mul_mod(x1, y1, *P);
+            const Dig<SH::S> x0 = split<SH::S>(a0[j]), x1 = split<SH::S>(a1[j]), y0 = split<SH::S>(b0[j]),
+                             y1 = split<SH::S>(b1[j]);
+            Cols s0, s1, s2;
+            s0.mac(x0, y0);
+            s1.mac(x0, y1);
+            s1.mac(x1, y0);
+            s2.mac(x1, y1);
+            t0[j] = reduce_acc(s0.fold<SH::S>(), *P);
+            t1[j] = reduce_acc(s1.fold<SH::S>(), *P);
+            t2[j] = reduce_acc(s2.fold<SH::S>(), *P);
         }
     }
 }
@@ -490,25 +502,29 @@ __global__ void __launch_bounds__(kThreads, 4) k_scale_round(DevCtx cx, u32 n, c
                 fx_add(s, a[i], dp->F[i]);
             }
             const u64 rr = fx_round(s);
-            u64 cb[kMaxB];
+            Dig<SH::S> ad[kMaxL];
+            for (u32 i = 0; i < L; ++i) ad[i] = split<SH::S>(a[i]);
+            Dig<SH::S> cb[kMaxB];
             Acc128 s2{0, 0};
             for (u32 k = 0; k < nB; ++k) {
                 const u64 b = dp->pr[L + K + k].q;
                 // rr + sum_i a_i floor(tB/q_i) + x_b [t/Q]  (mod b_k), one reduction
-                Acc acc;
-                acc.lo = rr;  // rr < L * 2^60
-                for (u32 i = 0; i < L; ++i) acc.mac(a[i], dp->W[i][k]);
-                acc.mac(t[(size_t)(L + k) * N + j], dp->T[k]);
-                cb[k] = shoup_mul(reduce_acc(acc, dp->pr[L + K + k]), dp->bhat_inv[k], dp->bhat_inv_sh[k], b);
-                fx_add(s2, cb[k], dp->one_over_b[k]);
+                Cols acc;
+                acc.c0 = rr;  // rr < L * 2^60
+                for (u32 i = 0; i < L; ++i) acc.mac(ad[i], split<SH::S>(dp->W[i][k]));
+                acc.mac(split<SH::S>(t[(size_t)(L + k) * N + j]), split<SH::S>(dp->T[k]));
+                const u64 c = shoup_mul(reduce_acc(acc.fold<SH::S>(), dp->pr[L + K + k]), dp->bhat_inv[k],
+                                        dp->bhat_inv_sh[k], b);
+                cb[k] = split<SH::S>(c);
+                fx_add(s2, c, dp->one_over_b[k]);
             }
             const u64 v = fx_round(s2);
             for (u32 i = 0; i < L; ++i) {
                 // sum_k c_k (B/b_k) - v B  (mod q_i), one reduction
-                Acc acc;
-                for (u32 k = 0; k < nB; ++k) acc.mac(cb[k], dp->bhat_mod_q[k][i]);
-                acc.mac(v, dp->neg_B_mod_q[i]);
-                e[(size_t)i * N + j] = reduce_acc(acc, dp->pr[i]);
+                Cols acc;
+                for (u32 k = 0; k < nB; ++k) acc.mac(cb[k], split<SH::S>(dp->bhat_mod_q[k][i]));
+                acc.mac(split<SH::S>(v), split<SH::S>(dp->neg_B_mod_q[i]));
+                e[(size_t)i * N + j] = reduce_acc(acc.fold<SH::S>(), dp->pr[i]);
             }
         }
     }

@@ -114,12 +114,6 @@ HD u64 add_mod(u64 a, u64 b, u64 q) {
 }
 HD u64 sub_mod(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }
 HD u64 neg_mod(u64 a, u64 q) { return a ? q - a : 0; }
-// a * w mod q with ws = floor(w 2^64 / q); any a < 2^64, result in [0, q)
-HD u64 shoup_mul(u64 a, u64 w, u64 ws, u64 q) {
-    u64 h = mulhi64(a, ws);
-    u64 r = a * w - h * q;
-    return r >= q ? r - q : r;
-}
 // Harvey's lazy Shoup product: a * w mod q in [0, 2q), any a < 2^64
 HD u64 shoup_lazy(u64 a, u64 w, u64 ws, u64 q) { return a * w - mulhi64(a, ws) * q; }
 // Shoup product whose quotient drops the a_lo*ws_lo partial product: the
@@ -147,15 +141,21 @@ HD u64 mulhi64_approx(u64 a, u64 b) {
 #endif
 }
 HD u64 shoup_lazy3(u64 a, u64 w, u64 ws, u64 q) { return a * w - mulhi64_approx(a, ws) * q; }
+// a * w mod q with ws = floor(w 2^64 / q); any a < 2^64, result in [0, q)
+HD u64 shoup_mul(u64 a, u64 w, u64 ws, u64 q) {
+    u64 r = shoup_lazy3(a, w, ws, q);  // [0, 3q)
+    r = r >= q ? r - q : r;
+    return r >= q ? r - q : r;
+}
 // x in [0, 2m) -> [0, m)   (m = q or 2q)
 HD u64 reduce_once(u64 x, u64 m) { return x >= m ? x - m : x; }
-// a * b mod q for a, b < q < 2^62 (shifted Barrett, at most two corrections)
+// a * b mod q for a, b < q < 2^61 (shifted Barrett, two corrections)
 HD u64 mul_mod(u64 a, u64 b, const Prime& p) {
     const u64 lo = a * b, hi = mulhi64(a, b);
     const u64 x = (hi << (66 - p.s)) | (lo >> (p.s - 2));
-    const u64 qh = mulhi64(x, p.mu);
+    const u64 qh = mulhi64_approx(x, p.mu);  // low by at most 3: r < 4q
     u64 r = lo - qh * p.q;
-    if (r >= p.q) r -= p.q;
+    if (r >= 2 * p.q) r -= 2 * p.q;
     if (r >= p.q) r -= p.q;
     return r;
 }
@@ -174,15 +174,60 @@ struct Acc {
     }
 };
 // Shifted Barrett on x < 2^(s+62) (s = bit length of q <= 60): x >> (s-2)
-// fits 64 bits, the quotient estimate is low by at most 2, two corrections.
+// fits 64 bits; the quotient estimate is low by at most 2 (+1 for the
+// 3-partial-product high half), so r < 4q and two corrections suffice.
 HD u64 reduce_acc(const Acc& a, const Prime& p) {
     const u64 x = (a.hi << (66 - p.s)) | (a.lo >> (p.s - 2));
-    const u64 qh = mulhi64(x, p.mu);
+    const u64 qh = mulhi64_approx(x, p.mu);
     u64 r = a.lo - qh * p.q;
     if (r >= 2 * p.q) r -= 2 * p.q;
     if (r >= p.q) r -= p.q;
     return r;
 }
+// Column accumulator for sums of residue products.  Operands are split into
+// S-bit digits (residues < 2^(2S): S = 30 for 60-bit primes, 28 for 55-bit),
+// so each 32x32 partial product is < 2^(2S) and accumulates with one
+// IMAD.WIDE (multiply + 64-bit add) into its column, with no carry handling:
+// a 64x64 product costs 4 IMAD.WIDE instead of 5 IMAD.WIDE + 2 IMAD + carries.
+// Column c1 takes two partials per product: up to 2^(63-2S) products.
+template <int S>
+struct Dig {
+    u32 l, h;
+};
+template <int S>
+HD Dig<S> split(u64 a) {
+    return Dig<S>{(u32)a & ((1u << S) - 1u), (u32)(a >> S)};
+}
+struct Cols {
+    u64 c0 = 0, c1 = 0, c2 = 0;
+    template <int S>
+    HD void mac(Dig<S> a, Dig<S> b) {
+        c0 += (u64)a.l * b.l;
+        c1 += (u64)a.l * b.h;
+        c1 += (u64)a.h * b.l;
+        c2 += (u64)a.h * b.h;
+    }
+    // adds a full 64-bit value (the carry out of c0 moves to c1)
+    template <int S>
+    HD void add(u64 v) {
+        c0 += v;
+        c1 += (c0 < v) ? (1ULL << (64 - S)) : 0;
+    }
+    // c0 + c1 2^S + c2 2^(2S) as a 128-bit accumulator
+    template <int S>
+    HD Acc fold() const {
+        Acc a;
+        a.lo = c0;
+        a.hi = 0;
+        const u64 t1 = c1 << S, t2 = c2 << (2 * S);
+        a.lo += t1;
+        a.hi += (c1 >> (64 - S)) + (a.lo < t1);
+        a.lo += t2;
+        a.hi += (c2 >> (64 - 2 * S)) + (a.lo < t2);
+        return a;
+    }
+};
+
 HD u64 from_signed(i64 v, u64 q) { return v >= 0 ? (u64)v % q : q - 1 - ((u64)(-(v + 1)) % q); }
 HD u64 centred_neg(u64 y, u64 q) { return y > (q - 1) / 2; }
 // y (canonical mod src) viewed as its centred representative, reduced mod dst.
