@@ -84,7 +84,7 @@ __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_ca
                                           u64 q, int pre, int blk, const Ld& ld = Ld()) {
     constexpr int NB = 1 << LB, T = NB / E, G = (NB >> R) / T;
     constexpr int LT_FIRST = LB - 1 - S0, LT_MIN = LT_FIRST - (R - 1);
-    const u64 q3 = 3 * q, q4 = q << 2;  // lazy bounds (fwd_stage)
+    const u64 q3 = q << 2, q4 = q << 2;  // lazy bounds (fwd_stage): U - V + 4q in (q, 8q)
 #pragma unroll
     for (int gg = 0; gg < G; ++gg) {
         const int gi = threadIdx.x + gg * T;
