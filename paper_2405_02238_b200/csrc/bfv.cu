@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_moddown_conv(DevCtx cx, u32 n, 
             u64 z[kMaxK];
             for (u32 k = 0; k < K; ++k) {
                 const u64 p = dp->pr[L + k].q;
-                z[k] = shoup_mul(a[(size_t)(L + k) * N + j], dp->phat_inv[k], dp->phat_inv_sh[k], p);
+                z[k] = shoup_mul(a[(size_t)(L + k) * N + j], dp->phat_inv_n[k], dp->phat_inv_n_sh[k], p);
             }
             for (u32 i = 0; i < L; ++i) {
                 const u64 q = dp->pr[i].q;
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_q_to_b(DevCtx cx, u32 n, const 
             u64 y[kMaxL];
             Acc128 s{0, 0};
             for (u32 i = 0; i < L; ++i) {
-                y[i] = shoup_mul(x[(size_t)i * N + j], dp->qhat_inv[i], dp->qhat_inv_sh[i], dp->pr[i].q);
+                y[i] = shoup_mul(x[(size_t)i * N + j], dp->qhat_inv_n[i], dp->qhat_inv_n_sh[i], dp->pr[i].q);
                 fx_add(s, y[i], dp->one_over_q[i]);
             }
             const u64 v = fx_round(s);
@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_scale_round(DevCtx cx, u32 n, c
             u64 a[kMaxL];
             Acc128 s{0, 0};
             for (u32 i = 0; i < L; ++i) {
-                a[i] = shoup_mul(t[(size_t)i * N + j], dp->dhat_inv[i], dp->dhat_inv_sh[i], dp->pr[i].q);
+                a[i] = shoup_mul(t[(size_t)i * N + j], dp->dhat_inv_n[i], dp->dhat_inv_n_sh[i], dp->pr[i].q);
                 fx_add(s, a[i], dp->F[i]);
             }
             const u64 rr = fx_round(s);
@@ -512,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_scale_round(DevCtx cx, u32 n, c
                 Cols acc;
                 acc.c0 = rr;  // rr < L * 2^60
                 for (u32 i = 0; i < L; ++i) acc.mac(ad[i], split<SH::S>(dp->W[i][k]));
-                acc.mac(split<SH::S>(t[(size_t)(L + k) * N + j]), split<SH::S>(dp->T[k]));
+                acc.mac(split<SH::S>(t[(size_t)(L + k) * N + j]), split<SH::S>(dp->T_n[k]));
                 const u64 c = shoup_mul(reduce_acc(acc.fold<SH::S>(), dp->pr[L + K + k]), dp->bhat_inv[k],
                                         dp->bhat_inv_sh[k], b);
                 cb[k] = split<SH::S>(c);
@@ -1022,6 +1022,7 @@ void Context::key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, c
     pj.count = n * 2 * K;
     pj.period = K;
     for (u32 k = 0; k < K; ++k) pj.prime[k] = (unsigned char)(L + k);
+    pj.unscaled = 1;  // k_moddown_conv / ModDownIO fold N^-1 into phat_inv
     ntt(false, pj);
     std::vector<u64*> va(acc, acc + n);
     u64* const* dacc = upload(va);
@@ -1093,6 +1094,7 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
                 src[(size_t)i * 4 * L + w] = (w < 2 * L ? a[i] + (size_t)w * N : b[i] + (size_t)(w - 2 * L) * N);
         NttJobs xj = jobs_contig(X, n * 4 * L, 0, L);
         xj.src = upload(src);
+        xj.unscaled = 1;  // k_q_to_b folds N^-1 into qhat_inv
         ntt(false, xj);
     } else {
         std::vector<const u64*> src((size_t)2 * n);
@@ -1104,7 +1106,9 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
             dst[2 * i + 1] = X + (size_t)i * 4 * LN + 2 * LN;
         }
         k_copy<<<grid_of(N, 2 * n), kThreads, 0, stream_>>>(2 * n, ct_words(), upload(src), upload(dst)); ++launches_;
-        ntt(false, jobs_contig(X, n * 4 * L, 0, L));
+        NttJobs xj = jobs_contig(X, n * 4 * L, 0, L);
+        xj.unscaled = 1;
+        ntt(false, xj);
     }
     // 2. exact Q -> B and NTT over B
     u64* XB = alloc((size_t)n * 4 * nB * N);
@@ -1121,6 +1125,7 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
     release(XB);
     NttJobs tj = jobs_contig(T, n * 3 * D, 0, D);
     for (u32 k = 0; k < nB; ++k) tj.prime[L + k] = (unsigned char)(L + K + k);
+    tj.unscaled = 1;  // k_scale_round folds N^-1 into dhat_inv and T
     ntt(false, tj);
     // 4. scale and round back to Q (coefficient form)
     u64* E = alloc((size_t)n * 3 * LN);

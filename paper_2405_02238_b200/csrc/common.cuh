@@ -82,6 +82,11 @@ struct DevParams {
     u64 P_inv_q[kMaxL], P_inv_q_sh[kMaxL];
     u64 phat_inv[kMaxK], phat_inv_sh[kMaxK];
     u64 phat_mod_q[kMaxK][kMaxL], phat_mod_q_sh[kMaxK][kMaxL];
+    // the same with N^-1 folded in, for inputs from unscaled INTTs (NttJobs::unscaled)
+    u64 qhat_inv_n[kMaxL], qhat_inv_n_sh[kMaxL];
+    u64 dhat_inv_n[kMaxL], dhat_inv_n_sh[kMaxL];
+    u64 T_n[kMaxB];
+    u64 phat_inv_n[kMaxK], phat_inv_n_sh[kMaxK];
 };
 
 // Per-context values passed by value to every kernel (the parameter-set

@@ -469,7 +469,7 @@ struct ModDownIO {
         u64 v = 0;
         for (u32 k = 0; k < K; ++k) {
             const u64 p = dp->pr[L + k].q;
-            const u64 z = shoup_mul(a[(size_t)(L + k) * N + j], dp->phat_inv[k], dp->phat_inv_sh[k], p);
+            const u64 z = shoup_mul(a[(size_t)(L + k) * N + j], dp->phat_inv_n[k], dp->phat_inv_n_sh[k], p);
             v = add_mod(v, shoup_mul(centred_lift_n(z, p, q), dp->phat_mod_q[k][i], dp->phat_mod_q_sh[k][i], q), q);
         }
         const u64 base = addc ? addc[item][((size_t)c * L + i) * N + j] : 0;
@@ -574,7 +574,7 @@ __global__ void __launch_bounds__((1 << LB) / kElems, 1)
         __syncthreads();
         inv_round<LB, LB - 4, 4, true>(b, cache, w + 2 * N, w + 3 * N, q, logN, cur.blk);
         __syncthreads();
-        if (logN == LB)
+        if (logN == LB && !jobs.unscaled)
             store_block<LB, true>(b, cur.g, q, P.ninv, P.ninv_sh);
         else
             store_block<LB, false>(b, cur.g, q, 0, 0);
@@ -626,10 +626,17 @@ __global__ void k_ntt_inv_outer2(DevCtx cx, NttJobs jobs) {
         // t = N/2: pairs (0,2), (1,3) with m=1 -> w[1]
         u64 z0 = add_mod(y0, y2, q), z2 = shoup_mul(sub_mod(y0, y2, q), w1, w1s, q);
         u64 z1 = add_mod(y1, y3, q), z3 = shoup_mul(sub_mod(y1, y3, q), w1, w1s, q);
-        a[j] = shoup_mul(z0, P.ninv, P.ninv_sh, q);
-        a[j + Q4] = shoup_mul(z1, P.ninv, P.ninv_sh, q);
-        a[j + 2 * Q4] = shoup_mul(z2, P.ninv, P.ninv_sh, q);
-        a[j + 3 * Q4] = shoup_mul(z3, P.ninv, P.ninv_sh, q);
+        if (jobs.unscaled) {
+            a[j] = z0;
+            a[j + Q4] = z1;
+            a[j + 2 * Q4] = z2;
+            a[j + 3 * Q4] = z3;
+        } else {
+            a[j] = shoup_mul(z0, P.ninv, P.ninv_sh, q);
+            a[j + Q4] = shoup_mul(z1, P.ninv, P.ninv_sh, q);
+            a[j + 2 * Q4] = shoup_mul(z2, P.ninv, P.ninv_sh, q);
+            a[j + 3 * Q4] = shoup_mul(z3, P.ninv, P.ninv_sh, q);
+        }
     }
 }
 
@@ -717,7 +724,7 @@ __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_inv3(DevCtx cx, 
     __syncthreads();
     inv_round<LB, LB - 4, 4, true, kElems3>(sm, cache, w + 2 * N, w + 3 * N, q, logN, blk);
     __syncthreads();
-    if (logN == LB)
+    if (logN == LB && !jobs.unscaled)
         store_block<LB, true, kElems3>(sm, g, q, P.ninv, P.ninv_sh);
     else
         store_block<LB, false, kElems3>(sm, g, q, 0, 0);

@@ -29,6 +29,9 @@ struct NttJobs {
     const u64* const* src = nullptr;
     u32 count = 0;
     u32 period = 1;
+    // inverse only: leave out the N^-1 scaling (the output is N * INTT(x)); for
+    // consumers whose first step multiplies by a constant that has N^-1 folded in
+    u32 unscaled = 0;
     unsigned char prime[32] = {0};  // host-side pattern
     u64 packed[4] = {0, 0, 0, 0};   // the same pattern, packed for the kernel
     void pack() {

@@ -233,6 +233,19 @@ HostParams make_params(int id, u64 seed) {
             d.phat_mod_q_sh[k][i] = shoup_of(d.phat_mod_q[k][i], q);
         }
     }
+    // N^-1 folded into the first multiplier of each unscaled-INTT consumer
+    auto with_ninv = [&](u64 c, unsigned r) { return mulmod(c, d.pr[r].ninv, h.primes[r]); };
+    for (unsigned i = 0; i < L; ++i) {
+        d.qhat_inv_n[i] = with_ninv(d.qhat_inv[i], i);
+        d.qhat_inv_n_sh[i] = shoup_of(d.qhat_inv_n[i], qv(i));
+        d.dhat_inv_n[i] = with_ninv(d.dhat_inv[i], i);
+        d.dhat_inv_n_sh[i] = shoup_of(d.dhat_inv_n[i], qv(i));
+    }
+    for (unsigned j = 0; j < nB; ++j) d.T_n[j] = with_ninv(d.T[j], L + K + j);
+    for (unsigned k = 0; k < K; ++k) {
+        d.phat_inv_n[k] = with_ninv(d.phat_inv[k], L + k);
+        d.phat_inv_n_sh[k] = shoup_of(d.phat_inv_n[k], h.primes[L + k]);
+    }
     return h;
 }
 
