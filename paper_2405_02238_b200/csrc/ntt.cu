@@ -27,48 +27,168 @@ constexpr int kTwCache = 511;
 // residues per thread: NB / kElems threads per CTA
 constexpr int kElems = 16;
 
-// Cooley-Tukey stage r of an R-stage register round (compile-time bounds so the
-// round unrolls and x[] stays in registers).  tw(r, c) yields (w, w') for the
-// c-th twiddle of stage r within this group.
-template <int R, int r, typename Tw>
-__device__ __forceinline__ void fwd_stage(u64 (&x)[1 << R], u64 q, u64 q3, u64 q4, const Tw& tw) {
+// Forward value bounds, in units of q, before global stage s (inputs canonical).
+// A stage maps inputs < b q to outputs < (b + 4) q (U + V with V < 3q, and
+// U - V + 4q); values must stay below 16q <= 2^64 (q < 2^60), so U is reduced
+// by 8q only where b > 12: about every other stage instead of every stage.
+constexpr int fwd_bound(int s) {
+    int b = 1;
+    for (int i = 0; i < s; ++i) b = (b > 12 ? 8 : b) + 4;
+    return b;
+}
+constexpr bool fwd_reduce(int s) { return fwd_bound(s) > 12; }
+
+// Cooley-Tukey stage r (global stage SG + r) of an R-stage register round
+// (compile-time bounds so the round unrolls and x[] stays in registers).
+// tw(r, c) yields (w, w') for the c-th twiddle of stage r within this group.
+template <int R, int r, int SG, typename Tw>
+__device__ __forceinline__ void fwd_stage(u64 (&x)[1 << R], u64 q, u64 q4, u64 q8, const Tw& tw) {
     constexpr int h = 1 << (R - 1 - r);
+    constexpr bool kReduce = fwd_reduce(SG + r);
 #pragma unroll
     for (int c = 0; c < (1 << r); ++c) {
         u64 w, ws;
         tw(r, c, w, ws);
 #pragma unroll
         for (int u = 0; u < h; ++u) {
-            // lazy butterfly: values in [0, 8q), U in [0, 4q), V in [0, 3q)
-            // (q < 2^61; shoup_lazy3's quotient is low by at most 1)
+            // lazy butterfly: U < 12q, V = w x mod q in [0, 3q) (shoup_lazy3)
             const int k = c * 2 * h + u;
-            const u64 U = reduce_once(x[k], q4);
+            const u64 U = kReduce ? reduce_once(x[k], q8) : x[k];
             const u64 V = shoup_lazy3(x[k + h], w, ws, q);
             x[k] = U + V;
-            x[k + h] = U - V + q3;
+            x[k + h] = U - V + q4;
         }
     }
-    if constexpr (r + 1 < R) fwd_stage<R, r + 1>(x, q, q3, q4, tw);
+    if constexpr (r + 1 < R) fwd_stage<R, r + 1, SG>(x, q, q4, q8, tw);
 }
 
-// Gentleman-Sande stage r (half-size 2^(LT_LO + r)) of an R-stage round.
-template <int R, int r, typename Tw>
-__device__ __forceinline__ void inv_stage(u64 (&x)[1 << R], u64 q, u64 q4, const Tw& tw) {
-    constexpr int h = 1 << r;
-#pragma unroll
-    for (int c = 0; c < (1 << (R - 1 - r)); ++c) {
-        u64 w, ws;
-        tw(r, c, w, ws);
-#pragma unroll
-        for (int u = 0; u < h; ++u) {
-            // lazy butterfly: inputs and outputs in [0, 4q)
-            const int k = c * 2 * h + u;
-            const u64 U = x[k], V = x[k + h];
-            x[k] = reduce_once(U + V, q4);
-            x[k + h] = shoup_lazy3(U - V + q4, w, ws, q);
+// Gentleman-Sande rounds track a compile-time bound (units of q) per register
+// element: a butterfly's sum output is the sum of its input bounds and its
+// difference output is shoup_lazy3's 3q.  Values stay below 16q <= 2^64, a
+// sum is reduced (one conditional subtraction of a power-of-two multiple of q)
+// only above kGsT, and the round ends with every element below kGsIn, the
+// bound its inputs were assumed to have -- about 5 reductions per 8 butterflies
+// instead of 8.
+constexpr int kGsIn = 4, kGsT = 8;
+constexpr int p2ceil(int x) {
+    int m = 1;
+    while (m < x) m *= 2;
+    return m;
+}
+constexpr int red_to(int v) { return p2ceil(v) / 2; }  // reduce_once by m = p2ceil(v)/2: < m
+struct GsAct {
+    int mU, mV, off, mS;  // pre-reductions of U and V, U - V offset, sum reduction (0: none)
+};
+template <int R>
+struct GsPlan {
+    GsAct act[R][1 << R];  // [stage][top index k]
+    int fin[1 << R][2];    // round-end reductions of element k
+};
+template <int R>
+constexpr GsPlan<R> make_gs_plan() {
+    GsPlan<R> p{};
+    int b[1 << R] = {};
+    for (int k = 0; k < (1 << R); ++k) b[k] = kGsIn;
+    for (int r = 0; r < R; ++r) {
+        const int h = 1 << r;
+        int nb[1 << R] = {};
+        for (int k = 0; k < (1 << R); ++k) nb[k] = b[k];
+        for (int k = 0; k < (1 << R); ++k) {
+            if (k & h) continue;
+            GsAct a{0, 0, 0, 0};
+            int U = b[k], V = b[k + h];
+            if (U + p2ceil(V) > 16 || U + V > 16) {
+                if (U >= V) a.mU = U = red_to(U); else a.mV = V = red_to(V);
+            }
+            if (U + p2ceil(V) > 16 || U + V > 16) {
+                if (!a.mU && U > 1) a.mU = U = red_to(U);
+                else if (!a.mV && V > 1) a.mV = V = red_to(V);
+            }
+            a.off = p2ceil(V);
+            int S = U + V;
+            if (S > kGsT) a.mS = S = red_to(S);
+            nb[k] = S;
+            nb[k + h] = 3;
+            p.act[r][k] = a;
+        }
+        for (int k = 0; k < (1 << R); ++k) b[k] = nb[k];
+    }
+    for (int k = 0; k < (1 << R); ++k) {
+        for (int st = 0; st < 2; ++st) {
+            p.fin[k][st] = 0;
+            if (b[k] > kGsIn) p.fin[k][st] = b[k] = red_to(b[k]);
         }
     }
-    if constexpr (r + 1 < R) inv_stage<R, r + 1>(x, q, q4, tw);
+    return p;
+}
+template <int R>
+constexpr bool gs_plan_ok() {
+    constexpr GsPlan<R> p = make_gs_plan<R>();
+    int b[1 << R] = {};
+    for (int k = 0; k < (1 << R); ++k) b[k] = kGsIn;
+    for (int r = 0; r < R; ++r)
+        for (int k = 0; k < (1 << R); ++k) {
+            if (k & (1 << r)) continue;
+            const GsAct a = p.act[r][k];
+            int U = b[k], V = b[k + (1 << r)];
+            if (a.mU) { if (U > 2 * a.mU) return false; U = a.mU; }
+            if (a.mV) { if (V > 2 * a.mV) return false; V = a.mV; }
+            if (U + V > 16 || U + a.off > 16 || a.off < V) return false;
+            int S = U + V;
+            if (a.mS) { if (S > 2 * a.mS) return false; S = a.mS; }
+            b[k] = S;
+            b[k + (1 << r)] = 3;
+        }
+    for (int k = 0; k < (1 << R); ++k) {
+        int v = b[k];
+        for (int st = 0; st < 2; ++st)
+            if (p.fin[k][st]) { if (v > 2 * p.fin[k][st]) return false; v = p.fin[k][st]; }
+        if (v > kGsIn) return false;
+    }
+    return true;
+}
+template <int R>
+struct GsPlanOf {
+    static_assert(gs_plan_ok<R>(), "Gentleman-Sande bound plan exceeds 16q");
+    static constexpr GsPlan<R> v = make_gs_plan<R>();
+};
+constexpr int ilog2c(int m) { return m <= 1 ? 0 : 1 + ilog2c(m / 2); }
+template <int M>
+__device__ __forceinline__ u64 red_by(u64 x, u64 q) {
+    if constexpr (M == 0) return x;
+    else return reduce_once(x, q << ilog2c(M));
+}
+
+template <int R, int r, int c, int u, typename Tw>
+__device__ __forceinline__ void inv_bf(u64 (&x)[1 << R], u64 q, u64 w, u64 ws) {
+    constexpr int h = 1 << r, k = c * 2 * h + u;
+    constexpr GsAct a = GsPlanOf<R>::v.act[r][k];
+    const u64 U = red_by<a.mU>(x[k], q), V = red_by<a.mV>(x[k + h], q);
+    x[k] = red_by<a.mS>(U + V, q);
+    x[k + h] = shoup_lazy3(U - V + (q << ilog2c(a.off)), w, ws, q);
+    if constexpr (u + 1 < h) inv_bf<R, r, c, u + 1, Tw>(x, q, w, ws);
+}
+template <int R, int r, int c, typename Tw>
+__device__ __forceinline__ void inv_group(u64 (&x)[1 << R], u64 q, const Tw& tw) {
+    u64 w, ws;
+    tw(r, c, w, ws);
+    inv_bf<R, r, c, 0, Tw>(x, q, w, ws);
+    if constexpr (c + 1 < (1 << (R - 1 - r))) inv_group<R, r, c + 1>(x, q, tw);
+}
+template <int R, int k>
+__device__ __forceinline__ void inv_finish(u64 (&x)[1 << R], u64 q) {
+    x[k] = red_by<GsPlanOf<R>::v.fin[k][1]>(red_by<GsPlanOf<R>::v.fin[k][0]>(x[k], q), q);
+    if constexpr (k + 1 < (1 << R)) inv_finish<R, k + 1>(x, q);
+}
+// Gentleman-Sande stage r (half-size 2^(LT_LO + r)) of an R-stage round;
+// inputs and round outputs in [0, kGsIn q).
+template <int R, int r, typename Tw>
+__device__ __forceinline__ void inv_stage(u64 (&x)[1 << R], u64 q, u64 /*q4*/, const Tw& tw) {
+    inv_group<R, r, 0>(x, q, tw);
+    if constexpr (r + 1 < R)
+        inv_stage<R, r + 1>(x, q, 0, tw);
+    else
+        inv_finish<R, 0>(x, q);
 }
 
 // Forward local stages [S0, S0+R): stage s = S0 + r, twiddle
@@ -84,7 +204,7 @@ __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_ca
                                           u64 q, int pre, int blk, const Ld& ld = Ld()) {
     constexpr int NB = 1 << LB, T = NB / E, G = (NB >> R) / T;
     constexpr int LT_FIRST = LB - 1 - S0, LT_MIN = LT_FIRST - (R - 1);
-    const u64 q3 = q << 2, q4 = q << 2;  // lazy bounds (fwd_stage): U - V + 4q in (q, 8q)
+    const u64 q4 = q << 2, q8 = q << 3;  // lazy bounds (fwd_stage)
 #pragma unroll
     for (int gg = 0; gg < G; ++gg) {
         const int gi = threadIdx.x + gg * T;
@@ -105,7 +225,7 @@ __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_ca
                 w = tw_cache[2 * i];
                 ws = tw_cache[2 * i + 1];
             };
-            fwd_stage<R, 0>(x, q, q3, q4, tw);
+            fwd_stage<R, 0, S0>(x, q, q4, q8, tw);
         } else {
             u64 pw[(1 << R) - 1], pws[(1 << R) - 1];
 #pragma unroll
@@ -122,7 +242,7 @@ __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_ca
                 w = pw[(1 << r) - 1 + c];
                 ws = pws[(1 << r) - 1 + c];
             };
-            fwd_stage<R, 0>(x, q, q3, q4, tw);
+            fwd_stage<R, 0, S0>(x, q, q4, q8, tw);
         }
 #pragma unroll
         for (int k = 0; k < (1 << R); ++k) sm[pad(base + (k << LT_MIN))] = x[k];
@@ -229,7 +349,7 @@ __device__ __forceinline__ void store_last_stage(const u64* sm, u64* g, const u6
     for (int i = threadIdx.x; i < NB / 2; i += T) {
         const u64 w = __ldg(w_tab + tw0 + i), ws = __ldg(ws_tab + tw0 + i);
         const u64 q2 = q << 1, q4 = q << 2;
-        const u64 U = reduce_once(reduce_once(sm[pad(2 * i)], q4), q2);  // [0, 8q) -> [0, 2q)
+        const u64 U = reduce_once(reduce_once(reduce_once(sm[pad(2 * i)], q4 << 1), q4), q2);  // [0, 16q) -> [0, 2q)
         const u64 V = shoup_lazy(sm[pad(2 * i + 1)], w, ws, q);
         ulonglong2 v;
         v.x = reduce_once(reduce_once(U + V, q2), q);
@@ -248,7 +368,7 @@ __device__ __forceinline__ void store_last_stage_io(const u64* sm, const St& st,
 #pragma unroll 4
     for (int i = threadIdx.x; i < NB / 2; i += T) {
         const u64 w = __ldg(w_tab + tw0 + i), ws = __ldg(ws_tab + tw0 + i);
-        const u64 U = reduce_once(reduce_once(sm[pad(2 * i)], q4), q2);  // [0, 8q) -> [0, 2q)
+        const u64 U = reduce_once(reduce_once(reduce_once(sm[pad(2 * i)], q4 << 1), q4), q2);  // [0, 16q) -> [0, 2q)
         const u64 V = shoup_lazy(sm[pad(2 * i + 1)], w, ws, q);
         st(i, reduce_once(reduce_once(U + V, q2), q), reduce_once(reduce_once(U - V + q2, q2), q));
     }
