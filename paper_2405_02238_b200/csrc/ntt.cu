@@ -26,6 +26,8 @@ constexpr int smem_words() {
 constexpr int kTwCache = 511;
 // residues per thread: NB / kElems threads per CTA
 constexpr int kElems = 16;
+// 3-CTA/SM variant: 256 threads x 32 residues, 255 cached twiddle pairs
+constexpr int kElems3 = 32, kTwCache3 = 255;
 
 // Forward value bounds, in units of q, before global stage s (inputs canonical).
 // A stage maps inputs < b q to outputs < (b + 4) q (U + V with V < 3q, and
@@ -509,7 +511,7 @@ __global__ void __launch_bounds__((1 << LB) / kElems, 1)
 // whose canonical NTT-domain output is CONSUMED by io.store(job, i, v0, v1)
 // (elements 2i, 2i+1): base-conversion passes fused around the NTT.
 template <int LB, typename IO>
-__global__ void __launch_bounds__((1 << LB) / kElems, 1) k_ntt_fwd_io(DevCtx cx, IO io) {
+__global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_fwd_io(DevCtx cx, IO io) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     extern __shared__ u64 sm[];
     u64* cache = sm + smem_words<LB>();
@@ -519,17 +521,17 @@ __global__ void __launch_bounds__((1 << LB) / kElems, 1) k_ntt_fwd_io(DevCtx cx,
     const int prime = io.prime(job);
     const u64 q = dp->pr[prime].q;
     const u64* w = cx.tw + (size_t)prime * 4 * N;
-    fill_tw_cache(cache, w, w + N, 0, 0);
+    fill_tw_cache(cache, w, w + N, 0, 0, kTwCache3);
     __syncthreads();
     auto ld = [&](int j) { return io.load(dp, job, (u32)j); };
-    fwd_round<LB, 0, 4, true, true>(sm, cache, w, w + N, q, 0, 0, ld);
+    fwd_round<LB, 0, 4, true, true, decltype(ld), kElems3>(sm, cache, w, w + N, q, 0, 0, ld);
     __syncthreads();
-    fwd_round<LB, 4, 4, true>(sm, cache, w, w + N, q, 0, 0);
+    fwd_round<LB, 4, 4, true, false, NoLoad, kElems3>(sm, cache, w, w + N, q, 0, 0);
     __syncthreads();
-    fwd_round<LB, 8, LB - 9, false>(sm, cache, w, w + N, q, 0, 0);
+    fwd_round<LB, 8, LB - 9, false, false, NoLoad, kElems3>(sm, cache, w, w + N, q, 0, 0);
     __syncthreads();
     auto st = [&](int i, u64 v0, u64 v1) { io.store(dp, job, (u32)i, v0, v1); };
-    store_last_stage_io<LB>(sm, st, w, w + N, q, logN, 0);
+    store_last_stage_io<LB, decltype(st), kElems3>(sm, st, w, w + N, q, logN, 0);
 }
 
 // y < src < 2*dst (one bit length per prime set): centred y mod dst
@@ -619,19 +621,19 @@ void launch_fwd_io(const DevCtx& cx, const DevParams& hp, const IO& io, u32 jobs
     if (jobs == 0) return;
     static bool configured13 = false, configured12 = false;
     if (hp.logN == 13) {
-        const size_t smem = (smem_words<13>() + 2 * kTwCache) * sizeof(u64);
+        const size_t smem = (smem_words<13>() + 2 * kTwCache3) * sizeof(u64);
         if (!configured13) {
             cudaFuncSetAttribute(k_ntt_fwd_io<13, IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             configured13 = true;
         }
-        k_ntt_fwd_io<13, IO><<<jobs, (1 << 13) / kElems, smem, s>>>(cx, io);
+        k_ntt_fwd_io<13, IO><<<jobs, (1 << 13) / kElems3, smem, s>>>(cx, io);
     } else {
-        const size_t smem = (smem_words<12>() + 2 * kTwCache) * sizeof(u64);
+        const size_t smem = (smem_words<12>() + 2 * kTwCache3) * sizeof(u64);
         if (!configured12) {
             cudaFuncSetAttribute(k_ntt_fwd_io<12, IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             configured12 = true;
         }
-        k_ntt_fwd_io<12, IO><<<jobs, (1 << 12) / kElems, smem, s>>>(cx, io);
+        k_ntt_fwd_io<12, IO><<<jobs, (1 << 12) / kElems3, smem, s>>>(cx, io);
     }
 }
 
@@ -793,7 +795,6 @@ void launch_block(bool fwd, const DevCtx& cx, const NttJobs& jobs, int sub, cuda
 // 256 threads x 32 residues, radix-16 rounds over two groups per thread,
 // 255 cached twiddle pairs (stages < 8), no double buffer: 72 KB of shared
 // memory and <= 85 registers, so three CTAs (24 warps) share an SM.
-constexpr int kElems3 = 32, kTwCache3 = 255;
 
 template <int LB>
 __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_fwd3(DevCtx cx, NttJobs jobs) {
