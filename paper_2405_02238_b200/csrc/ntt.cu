@@ -383,12 +383,25 @@ __device__ __forceinline__ void load_first_stage(u64* sm, const u64* g, const u6
     constexpr int NB = 1 << LB, T = NB / E;
     const ulonglong2* g2 = reinterpret_cast<const ulonglong2*>(g);
     const int tw0 = (1 << (logN - 1)) + (blk << (LB - 1));
-#pragma unroll 4
-    for (int i = threadIdx.x; i < NB / 2; i += T) {
-        const ulonglong2 v = g2[i];
-        const u64 w = __ldg(w_tab + tw0 + i), ws = __ldg(ws_tab + tw0 + i);
-        sm[pad(2 * i)] = reduce_once(v.x + v.y, q << 1);
-        sm[pad(2 * i + 1)] = shoup_lazy(v.x - v.y + (q << 1), w, ws, q);
+    // batches of kB pairs: all loads of a batch in flight before any use
+    constexpr int kIt = NB / 2 / T, kB = kIt < 8 ? kIt : 8;
+#pragma unroll 1
+    for (int i0 = 0; i0 < kIt; i0 += kB) {
+        ulonglong2 v[kB];
+        u64 w[kB], ws[kB];
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+            const int i = threadIdx.x + (i0 + b) * T;
+            v[b] = __ldcs(g2 + i);
+            w[b] = __ldg(w_tab + tw0 + i);
+            ws[b] = __ldg(ws_tab + tw0 + i);
+        }
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+            const int i = threadIdx.x + (i0 + b) * T;
+            sm[pad(2 * i)] = reduce_once(v[b].x + v[b].y, q << 1);
+            sm[pad(2 * i + 1)] = shoup_lazy3(v[b].x - v[b].y + (q << 1), w[b], ws[b], q);
+        }
     }
 }
 
