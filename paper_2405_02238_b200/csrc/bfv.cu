@@ -1047,6 +1047,13 @@ void Context::key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, c
     // conversion pass (V = ecoef - P^-1 conv), NTT, finishing pass
     u64* V = alloc((size_t)n * 2 * L * N);
     if (hp_.L == 3) k_moddown_conv<ShapeQ3><<<grid_of(N, n, 2), kThreads, 0, stream_>>>(cx_, n, dacc, dec, V); else k_moddown_conv<ShapeQ8><<<grid_of(N, n, 2), kThreads, 0, stream_>>>(cx_, n, dacc, dec, V); ++launches_;
+    if (ntt_finish_fusable(hp_.dev)) {
+        ntt_finish_fused(cx_, hp_.dev, n, V, dacc, dadd, upload(vg), upload(vo), stream_);
+        ++launches_;
+        release(V);
+        HGM_CUDA(cudaGetLastError());
+        return;
+    }
     ntt(true, jobs_contig(V, n * 2 * L, 0, L));
     if (hp_.L == 3) k_ks_finish<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, dacc, V, dadd, upload(vg), upload(vo)); else k_ks_finish<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, dacc, V, dadd, upload(vg), upload(vo)); ++launches_;
     release(V);

@@ -629,6 +629,14 @@ struct ModDownIO {
     }
 };
 
+// ModDown's forward NTT with the finishing pass fused into its store: input is
+// V = ecoef - P^-1 conv (k_moddown_conv), job = (item, component c, limb i) over
+// the contiguous [n][2][L][N] buffer; the store is ModDownIO's.
+struct FinishIO : ModDownIO {
+    const u64* V;
+    __device__ u64 load(const DevParams*, u32 job, u32 j) const { return __ldcs(V + (size_t)job * N + j); }
+};
+
 template <typename IO>
 void launch_fwd_io(const DevCtx& cx, const DevParams& hp, const IO& io, u32 jobs, cudaStream_t s) {
     if (jobs == 0) return;
@@ -912,6 +920,22 @@ void ntt_modup_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* C,
 void ntt_moddown_fused(const DevCtx& cx, const DevParams& hp, int n, u64* const* acc, const u64* const* addc,
                        const u64* const* addn, const u32* g, u64* const* out, cudaStream_t s) {
     ModDownIO io{acc, addc, addn, g, out, hp.L, hp.K, hp.R, hp.N, hp.logN};
+    launch_fwd_io(cx, hp, io, (u32)n * 2 * hp.L, s);
+}
+
+bool ntt_finish_fusable(const DevParams& hp) {
+    static const bool on = [] {
+        const char* e = std::getenv("HGM_FUSED_FINISH");
+        return !e || e[0] != '0';
+    }();
+    return on && hp.logN <= 13;
+}
+
+void ntt_finish_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* V, u64* const* acc,
+                      const u64* const* addn, const u32* g, u64* const* out, cudaStream_t s) {
+    FinishIO io;
+    static_cast<ModDownIO&>(io) = ModDownIO{acc, nullptr, addn, g, out, hp.L, hp.K, hp.R, hp.N, hp.logN};
+    io.V = V;
     launch_fwd_io(cx, hp, io, (u32)n * 2 * hp.L, s);
 }
 

@@ -56,6 +56,12 @@ void ntt_modup_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* C,
                      cudaStream_t s);
 void ntt_moddown_fused(const DevCtx& cx, const DevParams& hp, int n, u64* const* acc, const u64* const* addc,
                        const u64* const* addn, const u32* g, u64* const* out, cudaStream_t s);
+// ModDown's forward NTT of V (k_moddown_conv's output, [n][2][L][N]) with the
+// finishing pass (P^-1 acc + phi_g(addn)) fused into the store; default on
+// (HGM_FUSED_FINISH=0 disables) for whole-limb transforms.
+bool ntt_finish_fusable(const DevParams& hp);
+void ntt_finish_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* V, u64* const* acc,
+                      const u64* const* addn, const u32* g, u64* const* out, cudaStream_t s);
 // copies a parameter set's constants into this translation unit's __constant__ slot
 void ntt_upload_params(int pid, const DevParams& p);
 
