@@ -975,7 +975,7 @@ void Context::modup(int n, const u64* const* ct, u64* const* out) {
     for (int i = 1; i < n; ++i)
         if (out[i] != out[0] + (size_t)i * dnum * R * N) contiguous = false;
     u64* D = contiguous ? out[0] : alloc((size_t)n * dnum * R * N);
-    if (ntt_fusable(hp_.dev)) {
+    if (ntt_fusable(hp_.dev, kFuseModUp)) {
         ntt_modup_fused(cx_, hp_.dev, n, C, (size_t)L * N, D, stream_);
         ++launches_;
     } else {
@@ -1038,7 +1038,7 @@ void Context::key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, c
         std::vector<const u64*> v(ecoef, ecoef + n);
         dec = upload(v);
     }
-    if (ntt_fusable(hp_.dev)) {
+    if (ntt_fusable(hp_.dev, kFuseModDown)) {
         ntt_moddown_fused(cx_, hp_.dev, n, dacc, dec, dadd, upload(vg), upload(vo), stream_);
         ++launches_;
         HGM_CUDA(cudaGetLastError());
@@ -1139,7 +1139,7 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
     if (hp_.L == 3) k_scale_round<ShapeQ3><<<grid_of(N, n, 3), kThreads, 0, stream_>>>(cx_, n, T, E); else k_scale_round<ShapeQ8><<<grid_of(N, n, 3), kThreads, 0, stream_>>>(cx_, n, T, E); ++launches_;
     release(T);
     // 5. relinearise e2: ModUp, inner product with rlk, ModDown, add (e0, e1)
-    const bool fused = ntt_fusable(hp_.dev);
+    const bool fused = ntt_fusable(hp_.dev, kFuseModUp);
     u64* Dg = alloc((size_t)n * dnum * R * N);
     if (fused) {
         ntt_modup_fused(cx_, hp_.dev, n, E + 2 * LN, 3 * LN, Dg, stream_);

@@ -903,12 +903,14 @@ bool use_ntt3() {
 // The fused variants are exact but measured slower on B200 while the NTT is
 // integer-pipe bound (the conversions then compete with the butterflies at
 // one CTA per SM); they are opt-in via HGM_FUSED_KS=1 for experiments.
-bool ntt_fusable(const DevParams& hp) {
-    static const bool on = [] {
+bool ntt_fusable(const DevParams& hp, int which) {
+    // HGM_FUSED_KS: "1" both, "u" ModUp only, "d" ModDown only
+    static const int mask = [] {
         const char* e = std::getenv("HGM_FUSED_KS");
-        return e && e[0] == '1';
+        if (!e) return 0;
+        return e[0] == '1' ? 3 : e[0] == 'u' ? 1 : e[0] == 'd' ? 2 : 0;
     }();
-    return on && hp.logN <= 13;
+    return (mask & which) && hp.logN <= 13;
 }
 
 void ntt_modup_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* C, size_t c_stride, u64* D,

@@ -49,7 +49,8 @@ void ntt_inverse(const DevCtx& cx, const DevParams& hp, const NttJobs& jobs, cud
 //    holding L coefficient-domain limbs per item (stride c_stride words);
 //  * ModDown: out[item] = (acc - NTT(conv(P-part))) P^-1 (+ NTT(addc)) (+ addn[galois]),
 //    acc's P limbs already inverse-transformed.  Pointer arrays live on the device.
-bool ntt_fusable(const DevParams& hp);
+constexpr int kFuseModUp = 1, kFuseModDown = 2;
+bool ntt_fusable(const DevParams& hp, int which);
 // whole-limb transforms (N <= 8192): out-of-place jobs allowed
 inline bool ntt_fusable_size(const DevParams& hp) { return hp.logN <= 13; }
 void ntt_modup_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* C, size_t c_stride, u64* D,
