@@ -1013,17 +1013,6 @@ void Context::inner_product(int n, const u64* const* digits, const u64* const* k
 void Context::key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, const u64* const* addn,
                               const u32* g, u64* const* out) {
     const u32 N = hp_.N, L = hp_.L, K = hp_.K, R = hp_.R;
-    NttJobs pj;
-    std::vector<u64*> plimbs((size_t)n * 2 * K);
-    for (int i = 0; i < n; ++i)
-        for (u32 c = 0; c < 2; ++c)
-            for (u32 k = 0; k < K; ++k) plimbs[((size_t)i * 2 + c) * K + k] = acc[i] + ((size_t)c * R + L + k) * N;
-    pj.ptrs = upload(plimbs);
-    pj.count = n * 2 * K;
-    pj.period = K;
-    for (u32 k = 0; k < K; ++k) pj.prime[k] = (unsigned char)(L + k);
-    pj.unscaled = 1;  // k_moddown_conv / ModDownIO fold N^-1 into phat_inv
-    ntt(false, pj);
     std::vector<u64*> va(acc, acc + n);
     u64* const* dacc = upload(va);
     std::vector<u32> vg(g, g + n);
@@ -1038,24 +1027,41 @@ void Context::key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, c
         std::vector<const u64*> v(ecoef, ecoef + n);
         dec = upload(v);
     }
+    const bool conv_fused = ntt_conv_fusable(hp_.dev) && !ntt_fusable(hp_.dev, kFuseModDown);
+    if (!conv_fused) {  // P limbs back to the coefficient domain (N^-1 left to the conversion)
+        NttJobs pj;
+        std::vector<u64*> plimbs((size_t)n * 2 * K);
+        for (int i = 0; i < n; ++i)
+            for (u32 c = 0; c < 2; ++c)
+                for (u32 k = 0; k < K; ++k) plimbs[((size_t)i * 2 + c) * K + k] = acc[i] + ((size_t)c * R + L + k) * N;
+        pj.ptrs = upload(plimbs);
+        pj.count = n * 2 * K;
+        pj.period = K;
+        for (u32 k = 0; k < K; ++k) pj.prime[k] = (unsigned char)(L + k);
+        pj.unscaled = 1;  // k_moddown_conv / ModDownIO fold N^-1 into phat_inv
+        ntt(false, pj);
+    }
     if (ntt_fusable(hp_.dev, kFuseModDown)) {
         ntt_moddown_fused(cx_, hp_.dev, n, dacc, dec, dadd, upload(vg), upload(vo), stream_);
         ++launches_;
         HGM_CUDA(cudaGetLastError());
         return;
     }
-    // conversion pass (V = ecoef - P^-1 conv), NTT, finishing pass
+    // conversion (V = ecoef - P^-1 conv), NTT of V, finishing pass
     u64* V = alloc((size_t)n * 2 * L * N);
-    if (hp_.L == 3) k_moddown_conv<ShapeQ3><<<grid_of(N, n, 2), kThreads, 0, stream_>>>(cx_, n, dacc, dec, V); else k_moddown_conv<ShapeQ8><<<grid_of(N, n, 2), kThreads, 0, stream_>>>(cx_, n, dacc, dec, V); ++launches_;
+    if (conv_fused) {
+        ntt_moddown_conv_fused(cx_, hp_.dev, n, dacc, dec, V, stream_);
+        ++launches_;
+    } else {
+        if (hp_.L == 3) k_moddown_conv<ShapeQ3><<<grid_of(N, n, 2), kThreads, 0, stream_>>>(cx_, n, dacc, dec, V); else k_moddown_conv<ShapeQ8><<<grid_of(N, n, 2), kThreads, 0, stream_>>>(cx_, n, dacc, dec, V); ++launches_;
+    }
     if (ntt_finish_fusable(hp_.dev)) {
         ntt_finish_fused(cx_, hp_.dev, n, V, dacc, dadd, upload(vg), upload(vo), stream_);
         ++launches_;
-        release(V);
-        HGM_CUDA(cudaGetLastError());
-        return;
+    } else {
+        ntt(true, jobs_contig(V, n * 2 * L, 0, L));
+        if (hp_.L == 3) k_ks_finish<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, dacc, V, dadd, upload(vg), upload(vo)); else k_ks_finish<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, dacc, V, dadd, upload(vg), upload(vo)); ++launches_;
     }
-    ntt(true, jobs_contig(V, n * 2 * L, 0, L));
-    if (hp_.L == 3) k_ks_finish<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, dacc, V, dadd, upload(vg), upload(vo)); else k_ks_finish<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, dacc, V, dadd, upload(vg), upload(vo)); ++launches_;
     release(V);
     HGM_CUDA(cudaGetLastError());
 }

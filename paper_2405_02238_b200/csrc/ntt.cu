@@ -872,6 +872,88 @@ __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_inv3(DevCtx cx, 
         store_block<LB, false, kElems3>(sm, g, q, 0, 0);
 }
 
+// Inverse transform of a whole limb read from io.src(job) whose canonical,
+// UNSCALED (N * INTT) output is consumed by io.store(job, i, v0, v1)
+// (elements 2i, 2i+1): a base conversion fused behind the INTT.
+template <int LB, typename IO>
+__global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_inv_io(DevCtx cx, IO io) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
+    extern __shared__ u64 sm[];
+    u64* cache = sm + smem_words<LB>();
+    constexpr int NB = 1 << LB, T = NB / kElems3;
+    const u32 N = dp->N;
+    const int logN = (int)dp->logN;
+    const u32 job = blockIdx.x;
+    const int prime = io.prime(job);
+    const u64 q = dp->pr[prime].q;
+    const u64* w = cx.tw + (size_t)prime * 4 * N;
+    fill_tw_cache(cache, w + 2 * N, w + 3 * N, 0, 0, kTwCache3);
+    load_first_stage<LB, kElems3>(sm, io.src(job), w + 2 * N, w + 3 * N, q, logN, 0);
+    __syncthreads();
+    inv_round<LB, 1, LB - 9, false, kElems3>(sm, cache, w + 2 * N, w + 3 * N, q, logN, 0);
+    __syncthreads();
+    inv_round<LB, LB - 8, 4, true, kElems3>(sm, cache, w + 2 * N, w + 3 * N, q, logN, 0);
+    __syncthreads();
+    inv_round<LB, LB - 4, 4, true, kElems3>(sm, cache, w + 2 * N, w + 3 * N, q, logN, 0);
+    __syncthreads();
+#pragma unroll 4
+    for (int i = threadIdx.x; i < NB / 2; i += T) {
+        const u64 v0 = reduce_once(reduce_once(sm[pad(2 * i)], q << 1), q);
+        const u64 v1 = reduce_once(reduce_once(sm[pad(2 * i + 1)], q << 1), q);
+        io.store(dp, job, (u32)i, v0, v1);
+    }
+}
+
+// ModDown conversion fused behind the INTT of acc's P limb (K = 1, so P/p = 1):
+// job = (item, component c);  V[item][c][i] = ecoef[c][i] - P^-1 centred(N^-1 * INTT_p)
+// -- k_moddown_conv's output, from the unscaled INTT (N^-1 folded into phat_inv_n).
+struct MdConvIO {
+    u64* const* acc;           // per item [2][R][N]; the P limb in the NTT domain
+    const u64* const* ecoef;   // per item [2][L][N] coefficient-domain addend, or null
+    u64* V;                    // [n][2][L][N]
+    u32 L, R, N;
+    __device__ int prime(u32) const { return (int)L; }
+    __device__ const u64* src(u32 job) const { return acc[job >> 1] + ((size_t)(job & 1) * R + L) * N; }
+    __device__ void store(const DevParams* dp, u32 job, u32 i2, u64 v0, u64 v1) const {
+        const u32 item = job >> 1, c = job & 1;
+        const u64 p = dp->pr[L].q;
+        const u64 z0 = shoup_mul(v0, dp->phat_inv_n[0], dp->phat_inv_n_sh[0], p);
+        const u64 z1 = shoup_mul(v1, dp->phat_inv_n[0], dp->phat_inv_n_sh[0], p);
+        const u64* ec = ecoef ? ecoef[item] + (size_t)c * L * N : nullptr;
+        u64* out = V + ((size_t)item * 2 + c) * L * N;
+        for (u32 i = 0; i < L; ++i) {
+            const u64 q = dp->pr[i].q, pi = dp->P_inv_q[i], pis = dp->P_inv_q_sh[i];
+            ulonglong2 b{0, 0};
+            if (ec) b = __ldcs(reinterpret_cast<const ulonglong2*>(ec + (size_t)i * N) + i2);
+            ulonglong2 v;
+            v.x = sub_mod(b.x, shoup_mul(centred_lift_n(z0, p, q), pi, pis, q), q);
+            v.y = sub_mod(b.y, shoup_mul(centred_lift_n(z1, p, q), pi, pis, q), q);
+            reinterpret_cast<ulonglong2*>(out + (size_t)i * N)[i2] = v;
+        }
+    }
+};
+
+template <typename IO>
+void launch_inv_io(const DevCtx& cx, const DevParams& hp, const IO& io, u32 jobs, cudaStream_t s) {
+    if (jobs == 0) return;
+    static bool configured13 = false, configured12 = false;
+    if (hp.logN == 13) {
+        const size_t smem = (smem_words<13>() + 2 * kTwCache3) * sizeof(u64);
+        if (!configured13) {
+            cudaFuncSetAttribute(k_ntt_inv_io<13, IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            configured13 = true;
+        }
+        k_ntt_inv_io<13, IO><<<jobs, (1 << 13) / kElems3, smem, s>>>(cx, io);
+    } else {
+        const size_t smem = (smem_words<12>() + 2 * kTwCache3) * sizeof(u64);
+        if (!configured12) {
+            cudaFuncSetAttribute(k_ntt_inv_io<12, IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            configured12 = true;
+        }
+        k_ntt_inv_io<12, IO><<<jobs, (1 << 12) / kElems3, smem, s>>>(cx, io);
+    }
+}
+
 template <int LB>
 void launch_block3(bool fwd, const DevCtx& cx, const NttJobs& jobs, int sub, cudaStream_t s) {
     const size_t smem = (smem_words<LB>() + 2 * kTwCache3) * sizeof(u64);
@@ -939,6 +1021,20 @@ void ntt_finish_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* V
     static_cast<ModDownIO&>(io) = ModDownIO{acc, nullptr, addn, g, out, hp.L, hp.K, hp.R, hp.N, hp.logN};
     io.V = V;
     launch_fwd_io(cx, hp, io, (u32)n * 2 * hp.L, s);
+}
+
+bool ntt_conv_fusable(const DevParams& hp) {
+    static const bool on = [] {
+        const char* e = std::getenv("HGM_FUSED_CONV");
+        return !e || e[0] != '0';
+    }();
+    return on && hp.logN <= 13 && hp.K == 1;
+}
+
+void ntt_moddown_conv_fused(const DevCtx& cx, const DevParams& hp, int n, u64* const* acc, const u64* const* ecoef,
+                            u64* V, cudaStream_t s) {
+    MdConvIO io{acc, ecoef, V, hp.L, hp.R, hp.N};
+    launch_inv_io(cx, hp, io, (u32)n * 2, s);
 }
 
 void ntt_upload_params(int pid, const DevParams& p) {

@@ -63,6 +63,11 @@ void ntt_moddown_fused(const DevCtx& cx, const DevParams& hp, int n, u64* const*
 bool ntt_finish_fusable(const DevParams& hp);
 void ntt_finish_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* V, u64* const* acc,
                       const u64* const* addn, const u32* g, u64* const* out, cudaStream_t s);
+// INTT of acc's P limb with k_moddown_conv fused into its store (K = 1, whole
+// limbs; default on, HGM_FUSED_CONV=0 disables): writes V = ecoef - P^-1 conv.
+bool ntt_conv_fusable(const DevParams& hp);
+void ntt_moddown_conv_fused(const DevCtx& cx, const DevParams& hp, int n, u64* const* acc, const u64* const* ecoef,
+                            u64* V, cudaStream_t s);
 // copies a parameter set's constants into this translation unit's __constant__ slot
 void ntt_upload_params(int pid, const DevParams& p);
 
