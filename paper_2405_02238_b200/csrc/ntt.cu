@@ -28,6 +28,9 @@ constexpr int kTwCache = 511;
 constexpr int kElems = 16;
 // 3-CTA/SM variant: 256 threads x 32 residues, 255 cached twiddle pairs
 constexpr int kElems3 = 32, kTwCache3 = 255;
+// Twiddle tables hold (w, w') Shoup pairs interleaved, one 16-byte load per
+// twiddle: per prime [forward pairs: N][inverse pairs: N] (params.cpp).
+__device__ __forceinline__ const ulonglong2* pairs(const u64* t) { return reinterpret_cast<const ulonglong2*>(t); }
 
 // Forward value bounds, in units of q, before global stage s (inputs canonical).
 // A stage maps inputs < b q to outputs < (b + 4) q (U + V with V < 3q, and
@@ -202,7 +205,7 @@ struct NoLoad {
 
 template <int LB, int S0, int R, bool kCached, bool kFromGlobal = false, typename Ld = NoLoad, int E = kElems>
 __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_cache,
-                                          const u64* __restrict__ w_tab, const u64* __restrict__ ws_tab,
+                                          const ulonglong2* __restrict__ tw_tab,
                                           u64 q, int pre, int blk, const Ld& ld = Ld()) {
     constexpr int NB = 1 << LB, T = NB / E, G = (NB >> R) / T;
     constexpr int LT_FIRST = LB - 1 - S0, LT_MIN = LT_FIRST - (R - 1);
@@ -235,8 +238,9 @@ __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_ca
 #pragma unroll
                 for (int c = 0; c < (1 << r); ++c) {
                     const int g = (1 << (pre + S0 + r)) + (blk << (S0 + r)) + (block << r) + c;
-                    pw[(1 << r) - 1 + c] = __ldg(w_tab + g);
-                    pws[(1 << r) - 1 + c] = __ldg(ws_tab + g);
+                    const ulonglong2 t = __ldg(tw_tab + g);
+                    pw[(1 << r) - 1 + c] = t.x;
+                    pws[(1 << r) - 1 + c] = t.y;
                 }
 #pragma unroll
             for (int k = 0; k < (1 << R); ++k) x[k] = sm[pad(base + (k << LT_MIN))];
@@ -256,7 +260,7 @@ __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_ca
 //   cache index (1 << (LB-lt-1)) - 1 + (block << (R-r-1)) + c     (LB-lt-1 < 9)
 template <int LB, int LT_LO, int R, bool kCached, int E = kElems>
 __device__ __forceinline__ void inv_round(u64* sm, const u64* __restrict__ tw_cache,
-                                          const u64* __restrict__ w_tab, const u64* __restrict__ ws_tab,
+                                          const ulonglong2* __restrict__ tw_tab,
                                           u64 q, int logN, int blk) {
     constexpr int NB = 1 << LB, T = NB / E, G = (NB >> R) / T;
     const u64 q4 = q << 2;  // lazy bound 4q (inv_stage)
@@ -285,8 +289,9 @@ __device__ __forceinline__ void inv_round(u64* sm, const u64* __restrict__ tw_ca
                     const int lt = LT_LO + r;
                     const int g = (1 << (logN - lt - 1)) + (blk << (LB - lt - 1)) + (block << (R - r - 1)) + c;
                     const int slot = (1 << R) - (1 << (R - r)) + c;  // stage r occupies 2^(R-1-r) slots
-                    pw[slot] = __ldg(w_tab + g);
-                    pws[slot] = __ldg(ws_tab + g);
+                    const ulonglong2 t = __ldg(tw_tab + g);
+                    pw[slot] = t.x;
+                    pws[slot] = t.y;
                 }
 #pragma unroll
             for (int k = 0; k < (1 << R); ++k) x[k] = sm[pad(base + (k << LT_LO))];
@@ -306,15 +311,15 @@ __device__ __forceinline__ void inv_round(u64* sm, const u64* __restrict__ tw_ca
 // global index base(s) + c with base(s) = 2^(outer+s) + (blk << s) (forward:
 // outer = pre; inverse: base(s) = 2^(logN-LB+s) + (blk << s) for the stage
 // with m-offset 2^s inside the block).
-__device__ __forceinline__ void fill_tw_cache(u64* cache, const u64* __restrict__ w_tab,
-                                              const u64* __restrict__ ws_tab, int outer, int blk,
+__device__ __forceinline__ void fill_tw_cache(u64* cache, const ulonglong2* __restrict__ tw_tab, int outer, int blk,
                                               int count = kTwCache) {
     for (int i = threadIdx.x; i < count; i += blockDim.x) {
         const int s = 31 - __clz(i + 1);  // i + 1 in [2^s, 2^(s+1))
         const int c = i + 1 - (1 << s);
         const int g = (1 << (outer + s)) + (blk << s) + c;
-        cache[2 * i] = __ldg(w_tab + g);
-        cache[2 * i + 1] = __ldg(ws_tab + g);
+        const ulonglong2 t = __ldg(tw_tab + g);
+        cache[2 * i] = t.x;
+        cache[2 * i + 1] = t.y;
     }
 }
 
@@ -342,14 +347,14 @@ __device__ __forceinline__ JobView job_of(const NttJobs& jobs, u32 j, u32 N) {
 // residues, i.e. exactly the 16-byte vector each thread stores, so it is
 // fused into the coalesced store together with the reduction to [0, q).
 template <int LB, int E = kElems>
-__device__ __forceinline__ void store_last_stage(const u64* sm, u64* g, const u64* __restrict__ w_tab,
-                                                 const u64* __restrict__ ws_tab, u64 q, int logN, int blk) {
+__device__ __forceinline__ void store_last_stage(const u64* sm, u64* g, const ulonglong2* __restrict__ tw_tab, u64 q, int logN, int blk) {
     constexpr int NB = 1 << LB, T = NB / E;
     ulonglong2* g2 = reinterpret_cast<ulonglong2*>(g);
     const int tw0 = (1 << (logN - 1)) + (blk << (LB - 1));
 #pragma unroll 4
     for (int i = threadIdx.x; i < NB / 2; i += T) {
-        const u64 w = __ldg(w_tab + tw0 + i), ws = __ldg(ws_tab + tw0 + i);
+        const ulonglong2 t = __ldg(tw_tab + tw0 + i);
+        const u64 w = t.x, ws = t.y;
         const u64 q2 = q << 1, q4 = q << 2;
         const u64 U = reduce_once(reduce_once(reduce_once(sm[pad(2 * i)], q4 << 1), q4), q2);  // [0, 16q) -> [0, 2q)
         const u64 V = shoup_lazy(sm[pad(2 * i + 1)], w, ws, q);
@@ -362,14 +367,14 @@ __device__ __forceinline__ void store_last_stage(const u64* sm, u64* g, const u6
 
 // Same, handing each finished pair (elements 2i, 2i+1, canonical) to `st`.
 template <int LB, typename St, int E = kElems>
-__device__ __forceinline__ void store_last_stage_io(const u64* sm, const St& st, const u64* __restrict__ w_tab,
-                                                    const u64* __restrict__ ws_tab, u64 q, int logN, int blk) {
+__device__ __forceinline__ void store_last_stage_io(const u64* sm, const St& st, const ulonglong2* __restrict__ tw_tab, u64 q, int logN, int blk) {
     constexpr int NB = 1 << LB, T = NB / E;
     const int tw0 = (1 << (logN - 1)) + (blk << (LB - 1));
     const u64 q2 = q << 1, q4 = q << 2;
 #pragma unroll 4
     for (int i = threadIdx.x; i < NB / 2; i += T) {
-        const u64 w = __ldg(w_tab + tw0 + i), ws = __ldg(ws_tab + tw0 + i);
+        const ulonglong2 t = __ldg(tw_tab + tw0 + i);
+        const u64 w = t.x, ws = t.y;
         const u64 U = reduce_once(reduce_once(reduce_once(sm[pad(2 * i)], q4 << 1), q4), q2);  // [0, 16q) -> [0, 2q)
         const u64 V = shoup_lazy(sm[pad(2 * i + 1)], w, ws, q);
         st(i, reduce_once(reduce_once(U + V, q2), q), reduce_once(reduce_once(U - V + q2, q2), q));
@@ -378,8 +383,7 @@ __device__ __forceinline__ void store_last_stage_io(const u64* sm, const St& st,
 
 // Inverse: the first Gentleman-Sande stage (t = 1) fused into the coalesced load.
 template <int LB, int E = kElems>
-__device__ __forceinline__ void load_first_stage(u64* sm, const u64* g, const u64* __restrict__ w_tab,
-                                                 const u64* __restrict__ ws_tab, u64 q, int logN, int blk) {
+__device__ __forceinline__ void load_first_stage(u64* sm, const u64* g, const ulonglong2* __restrict__ tw_tab, u64 q, int logN, int blk) {
     constexpr int NB = 1 << LB, T = NB / E;
     const ulonglong2* g2 = reinterpret_cast<const ulonglong2*>(g);
     const int tw0 = (1 << (logN - 1)) + (blk << (LB - 1));
@@ -393,8 +397,9 @@ __device__ __forceinline__ void load_first_stage(u64* sm, const u64* g, const u6
         for (int b = 0; b < kB; ++b) {
             const int i = threadIdx.x + (i0 + b) * T;
             v[b] = __ldcs(g2 + i);
-            w[b] = __ldg(w_tab + tw0 + i);
-            ws[b] = __ldg(ws_tab + tw0 + i);
+            const ulonglong2 t = __ldg(tw_tab + tw0 + i);
+            w[b] = t.x;
+            ws[b] = t.y;
         }
 #pragma unroll
         for (int b = 0; b < kB; ++b) {
@@ -502,19 +507,19 @@ __global__ void __launch_bounds__((1 << LB) / kElems, 1)
         const u64 q = dp->pr[cur.prime].q;
         const u64* w = cx.tw + (size_t)cur.prime * 4 * N;
         if (cur.prime != cached_prime || cur.blk != cached_blk) {
-            fill_tw_cache(cache, w, w + N, pre, cur.blk);
+            fill_tw_cache(cache, pairs(w), pre, cur.blk);
             cached_prime = cur.prime;
             cached_blk = cur.blk;
         }
         cp_async_wait1();
         __syncthreads();
-        fwd_round<LB, 0, 4, true>(b, cache, w, w + N, q, pre, cur.blk);
+        fwd_round<LB, 0, 4, true>(b, cache, pairs(w), q, pre, cur.blk);
         __syncthreads();
-        fwd_round<LB, 4, 4, true>(b, cache, w, w + N, q, pre, cur.blk);
+        fwd_round<LB, 4, 4, true>(b, cache, pairs(w), q, pre, cur.blk);
         __syncthreads();
-        fwd_round<LB, 8, LB - 9, false>(b, cache, w, w + N, q, pre, cur.blk);
+        fwd_round<LB, 8, LB - 9, false>(b, cache, pairs(w), q, pre, cur.blk);
         __syncthreads();
-        store_last_stage<LB>(b, cur.g, w, w + N, q, logN, cur.blk);
+        store_last_stage<LB>(b, cur.g, pairs(w), q, logN, cur.blk);
         __syncthreads();
         cur = nxt;
     }
@@ -534,17 +539,17 @@ __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_fwd_io(DevCtx cx
     const int prime = io.prime(job);
     const u64 q = dp->pr[prime].q;
     const u64* w = cx.tw + (size_t)prime * 4 * N;
-    fill_tw_cache(cache, w, w + N, 0, 0, kTwCache3);
+    fill_tw_cache(cache, pairs(w), 0, 0, kTwCache3);
     __syncthreads();
     auto ld = [&](int j) { return io.load(dp, job, (u32)j); };
-    fwd_round<LB, 0, 4, true, true, decltype(ld), kElems3>(sm, cache, w, w + N, q, 0, 0, ld);
+    fwd_round<LB, 0, 4, true, true, decltype(ld), kElems3>(sm, cache, pairs(w), q, 0, 0, ld);
     __syncthreads();
-    fwd_round<LB, 4, 4, true, false, NoLoad, kElems3>(sm, cache, w, w + N, q, 0, 0);
+    fwd_round<LB, 4, 4, true, false, NoLoad, kElems3>(sm, cache, pairs(w), q, 0, 0);
     __syncthreads();
-    fwd_round<LB, 8, LB - 9, false, false, NoLoad, kElems3>(sm, cache, w, w + N, q, 0, 0);
+    fwd_round<LB, 8, LB - 9, false, false, NoLoad, kElems3>(sm, cache, pairs(w), q, 0, 0);
     __syncthreads();
     auto st = [&](int i, u64 v0, u64 v1) { io.store(dp, job, (u32)i, v0, v1); };
-    store_last_stage_io<LB, decltype(st), kElems3>(sm, st, w, w + N, q, logN, 0);
+    store_last_stage_io<LB, decltype(st), kElems3>(sm, st, pairs(w), q, logN, 0);
 }
 
 // y < src < 2*dst (one bit length per prime set): centred y mod dst
@@ -692,7 +697,7 @@ __global__ void __launch_bounds__((1 << LB) / kElems, 1)
         const u64 q = P.q;
         const u64* w = cx.tw + (size_t)cur.prime * 4 * N;
         if (cur.prime != cached_prime || cur.blk != cached_blk) {
-            fill_tw_cache(cache, w + 2 * N, w + 3 * N, logN - LB, cur.blk);
+            fill_tw_cache(cache, pairs(w + 2 * N), logN - LB, cur.blk);
             cached_prime = cur.prime;
             cached_blk = cur.blk;
         }
@@ -700,22 +705,22 @@ __global__ void __launch_bounds__((1 << LB) / kElems, 1)
         __syncthreads();
         {  // first Gentleman-Sande stage (t = 1) on adjacent pairs
             const int tw0 = (1 << (logN - 1)) + (cur.blk << (LB - 1));
-            const u64* wt = w + 2 * N;
-            const u64* wst = w + 3 * N;
+            const ulonglong2* wt = pairs(w + 2 * N);
 #pragma unroll 4
             for (int i = threadIdx.x; i < NB / 2; i += T) {
                 const u64 x0 = b[pad(2 * i)], x1 = b[pad(2 * i + 1)];
-                const u64 tw = __ldg(wt + tw0 + i), tws = __ldg(wst + tw0 + i);
+                const ulonglong2 t = __ldg(wt + tw0 + i);
+                const u64 tw = t.x, tws = t.y;
                 b[pad(2 * i)] = reduce_once(x0 + x1, q << 1);
                 b[pad(2 * i + 1)] = shoup_lazy(x0 - x1 + (q << 1), tw, tws, q);
             }
         }
         __syncthreads();
-        inv_round<LB, 1, LB - 9, false>(b, cache, w + 2 * N, w + 3 * N, q, logN, cur.blk);
+        inv_round<LB, 1, LB - 9, false>(b, cache, pairs(w + 2 * N), q, logN, cur.blk);
         __syncthreads();
-        inv_round<LB, LB - 8, 4, true>(b, cache, w + 2 * N, w + 3 * N, q, logN, cur.blk);
+        inv_round<LB, LB - 8, 4, true>(b, cache, pairs(w + 2 * N), q, logN, cur.blk);
         __syncthreads();
-        inv_round<LB, LB - 4, 4, true>(b, cache, w + 2 * N, w + 3 * N, q, logN, cur.blk);
+        inv_round<LB, LB - 4, 4, true>(b, cache, pairs(w + 2 * N), q, logN, cur.blk);
         __syncthreads();
         if (logN == LB && !jobs.unscaled)
             store_block<LB, true>(b, cur.g, q, P.ninv, P.ninv_sh);
@@ -732,8 +737,8 @@ __global__ void k_ntt_fwd_outer2(DevCtx cx, NttJobs jobs) {
     const u32 N = dp->N, Q4 = N / 4;
     const JobView jv = job_of(jobs, blockIdx.y, N);
     const u64 q = dp->pr[jv.prime].q;
-    const u64* w = cx.tw + (size_t)jv.prime * 4 * N;
-    const u64 w1 = w[1], w1s = w[N + 1], w2 = w[2], w2s = w[N + 2], w3 = w[3], w3s = w[N + 3];
+    const ulonglong2* t = pairs(cx.tw + (size_t)jv.prime * 4 * N);
+    const u64 w1 = t[1].x, w1s = t[1].y, w2 = t[2].x, w2s = t[2].y, w3 = t[3].x, w3s = t[3].y;
     for (u32 j = blockIdx.x * blockDim.x + threadIdx.x; j < Q4; j += gridDim.x * blockDim.x) {
         u64* a = jv.ptr;
         u64 x0 = a[j], x1 = a[j + Q4], x2 = a[j + 2 * Q4], x3 = a[j + 3 * Q4];
@@ -757,9 +762,8 @@ __global__ void k_ntt_inv_outer2(DevCtx cx, NttJobs jobs) {
     const JobView jv = job_of(jobs, blockIdx.y, N);
     const Prime& P = dp->pr[jv.prime];
     const u64 q = P.q;
-    const u64* w = cx.tw + (size_t)jv.prime * 4 * N + 2 * N;
-    const u64* ws = w + N;
-    const u64 w2 = w[2], w2s = ws[2], w3 = w[3], w3s = ws[3], w1 = w[1], w1s = ws[1];
+    const ulonglong2* t = pairs(cx.tw + (size_t)jv.prime * 4 * N + 2 * N);
+    const u64 w2 = t[2].x, w2s = t[2].y, w3 = t[3].x, w3s = t[3].y, w1 = t[1].x, w1s = t[1].y;
     for (u32 j = blockIdx.x * blockDim.x + threadIdx.x; j < Q4; j += gridDim.x * blockDim.x) {
         u64* a = jv.ptr;
         u64 x0 = a[j], x1 = a[j + Q4], x2 = a[j + 2 * Q4], x3 = a[j + 3 * Q4];
@@ -831,16 +835,16 @@ __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_fwd3(DevCtx cx, 
     const u64* w = cx.tw + (size_t)jv.prime * 4 * N;
     u64* g = jv.ptr + ((size_t)blk << LB);
     const u64* src = jobs.src ? jobs.src[blockIdx.x] + ((size_t)blk << LB) : g;
-    fill_tw_cache(cache, w, w + N, pre, blk, kTwCache3);
+    fill_tw_cache(cache, pairs(w), pre, blk, kTwCache3);
     __syncthreads();
     auto ld = [src](int j) { return __ldcs(src + j); };
-    fwd_round<LB, 0, 4, true, true, decltype(ld), kElems3>(sm, cache, w, w + N, q, pre, blk, ld);
+    fwd_round<LB, 0, 4, true, true, decltype(ld), kElems3>(sm, cache, pairs(w), q, pre, blk, ld);
     __syncthreads();
-    fwd_round<LB, 4, 4, true, false, NoLoad, kElems3>(sm, cache, w, w + N, q, pre, blk);
+    fwd_round<LB, 4, 4, true, false, NoLoad, kElems3>(sm, cache, pairs(w), q, pre, blk);
     __syncthreads();
-    fwd_round<LB, 8, LB - 9, false, false, NoLoad, kElems3>(sm, cache, w, w + N, q, pre, blk);
+    fwd_round<LB, 8, LB - 9, false, false, NoLoad, kElems3>(sm, cache, pairs(w), q, pre, blk);
     __syncthreads();
-    store_last_stage<LB, kElems3>(sm, g, w, w + N, q, logN, blk);
+    store_last_stage<LB, kElems3>(sm, g, pairs(w), q, logN, blk);
 }
 
 template <int LB>
@@ -857,14 +861,14 @@ __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_inv3(DevCtx cx, 
     const u64* w = cx.tw + (size_t)jv.prime * 4 * N;
     u64* g = jv.ptr + ((size_t)blk << LB);
     const u64* src = jobs.src ? jobs.src[blockIdx.x] + ((size_t)blk << LB) : g;
-    fill_tw_cache(cache, w + 2 * N, w + 3 * N, logN - LB, blk, kTwCache3);
-    load_first_stage<LB, kElems3>(sm, src, w + 2 * N, w + 3 * N, q, logN, blk);
+    fill_tw_cache(cache, pairs(w + 2 * N), logN - LB, blk, kTwCache3);
+    load_first_stage<LB, kElems3>(sm, src, pairs(w + 2 * N), q, logN, blk);
     __syncthreads();
-    inv_round<LB, 1, LB - 9, false, kElems3>(sm, cache, w + 2 * N, w + 3 * N, q, logN, blk);
+    inv_round<LB, 1, LB - 9, false, kElems3>(sm, cache, pairs(w + 2 * N), q, logN, blk);
     __syncthreads();
-    inv_round<LB, LB - 8, 4, true, kElems3>(sm, cache, w + 2 * N, w + 3 * N, q, logN, blk);
+    inv_round<LB, LB - 8, 4, true, kElems3>(sm, cache, pairs(w + 2 * N), q, logN, blk);
     __syncthreads();
-    inv_round<LB, LB - 4, 4, true, kElems3>(sm, cache, w + 2 * N, w + 3 * N, q, logN, blk);
+    inv_round<LB, LB - 4, 4, true, kElems3>(sm, cache, pairs(w + 2 * N), q, logN, blk);
     __syncthreads();
     if (logN == LB && !jobs.unscaled)
         store_block<LB, true, kElems3>(sm, g, q, P.ninv, P.ninv_sh);
@@ -887,14 +891,14 @@ __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_inv_io(DevCtx cx
     const int prime = io.prime(job);
     const u64 q = dp->pr[prime].q;
     const u64* w = cx.tw + (size_t)prime * 4 * N;
-    fill_tw_cache(cache, w + 2 * N, w + 3 * N, 0, 0, kTwCache3);
-    load_first_stage<LB, kElems3>(sm, io.src(job), w + 2 * N, w + 3 * N, q, logN, 0);
+    fill_tw_cache(cache, pairs(w + 2 * N), 0, 0, kTwCache3);
+    load_first_stage<LB, kElems3>(sm, io.src(job), pairs(w + 2 * N), q, logN, 0);
     __syncthreads();
-    inv_round<LB, 1, LB - 9, false, kElems3>(sm, cache, w + 2 * N, w + 3 * N, q, logN, 0);
+    inv_round<LB, 1, LB - 9, false, kElems3>(sm, cache, pairs(w + 2 * N), q, logN, 0);
     __syncthreads();
-    inv_round<LB, LB - 8, 4, true, kElems3>(sm, cache, w + 2 * N, w + 3 * N, q, logN, 0);
+    inv_round<LB, LB - 8, 4, true, kElems3>(sm, cache, pairs(w + 2 * N), q, logN, 0);
     __syncthreads();
-    inv_round<LB, LB - 4, 4, true, kElems3>(sm, cache, w + 2 * N, w + 3 * N, q, logN, 0);
+    inv_round<LB, LB - 4, 4, true, kElems3>(sm, cache, pairs(w + 2 * N), q, logN, 0);
     __syncthreads();
 #pragma unroll 4
     for (int i = threadIdx.x; i < NB / 2; i += T) {

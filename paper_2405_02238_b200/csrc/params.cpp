@@ -124,12 +124,13 @@ HostParams make_params(int id, u64 seed) {
         h.psi.push_back(psi);
         const u64 ipsi = invmod(psi, q);
         u64* base = h.tw.data() + (size_t)slot * 4 * N;
+        // interleaved Shoup pairs: [2i] = w, [2i+1] = w' (forward), then the inverse at +2N
         for (u32 i = 0; i < N; ++i) {
             const u32 e = bitrev(i, h.logN);
-            base[i] = powmod(psi, e, q);
-            base[N + i] = shoup_of(base[i], q);
-            base[2 * N + i] = powmod(ipsi, e, q);
-            base[3 * N + i] = shoup_of(base[2 * N + i], q);
+            base[2 * i] = powmod(psi, e, q);
+            base[2 * i + 1] = shoup_of(base[2 * i], q);
+            base[2 * N + 2 * i] = powmod(ipsi, e, q);
+            base[2 * N + 2 * i + 1] = shoup_of(base[2 * N + 2 * i], q);
         }
     };
     for (unsigned r = 0; r < total; ++r) fill(r, h.primes[r]);

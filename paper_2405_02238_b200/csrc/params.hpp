@@ -23,7 +23,7 @@ struct HostParams {
     u64 seed = 0;
     std::vector<u64> primes;          // Q ++ P ++ B
     std::vector<u64> psi;             // primitive 2N-th roots, same order, then t's
-    std::vector<u64> tw;              // [(kMaxPrimes+1)][4][N]
+    std::vector<u64> tw;              // [(kMaxPrimes+1)][fwd, inv][N][w, w'] interleaved Shoup pairs
     std::vector<u32> slot_ntt;        // N
     DevParams dev{};                  // scalar part (pointers filled on upload)
 };
