@@ -209,8 +209,9 @@ __global__ void k_lincomb(DevCtx cx, u32 n, const u32* off,
                 if (mask[t]) {
                     acc.mac(split<SH::S>(v), split<SH::S>(mask[t][wl]));
                     if (++pending == 3) {
-                        acc.c0 = reduce_acc(acc.fold<SH::S>(), P);
-                        acc.c1 = acc.c2 = 0;
+                        const u64 r = reduce_acc(acc.fold<SH::S>(), P);
+                        acc = Cols{};
+                        acc.x = r;
                         pending = 0;
                     }
                 } else {
@@ -441,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_q_to_b(DevCtx cx, u32 n, const 
                 // sum_i y_i (Q/q_i) - v Q  (mod b_k), one reduction
                 Cols a;
                 for (u32 i = 0; i < L; ++i) a.mac(yd[i], split<SH::S>(dp->qhat_mod_b[i][k]));
-                a.mac(split<SH::S>(v), split<SH::S>(dp->neg_Q_mod_b[k]));
+                a.add<SH::S>(v * dp->neg_Q_mod_b[k]);  // v <= L: < 2^63, a plain addend
                 xb[(size_t)k * N + j] = reduce_acc(a.fold<SH::S>(), dp->pr[L + K + k]);
             }
         }
@@ -510,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_scale_round(DevCtx cx, u32 n, c
                 const u64 b = dp->pr[L + K + k].q;
                 // rr + sum_i a_i floor(tB/q_i) + x_b [t/Q]  (mod b_k), one reduction
                 Cols acc;
-                acc.c0 = rr;  // rr < L * 2^60
+                acc.x = rr;  // rr < L * 2^60
                 for (u32 i = 0; i < L; ++i) acc.mac(ad[i], split<SH::S>(dp->W[i][k]));
                 acc.mac(split<SH::S>(t[(size_t)(L + k) * N + j]), split<SH::S>(dp->T_n[k]));
                 const u64 c = shoup_mul(reduce_acc(acc.fold<SH::S>(), dp->pr[L + K + k]), dp->bhat_inv[k],
@@ -523,7 +524,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_scale_round(DevCtx cx, u32 n, c
                 // sum_k c_k (B/b_k) - v B  (mod q_i), one reduction
                 Cols acc;
                 for (u32 k = 0; k < nB; ++k) acc.mac(cb[k], split<SH::S>(dp->bhat_mod_q[k][i]));
-                acc.mac(split<SH::S>(v), split<SH::S>(dp->neg_B_mod_q[i]));
+                acc.add<SH::S>(v * dp->neg_B_mod_q[i]);  // v <= nB: < 2^64, a plain addend
                 e[(size_t)i * N + j] = reduce_acc(acc.fold<SH::S>(), dp->pr[i]);
             }
         }

@@ -190,43 +190,47 @@ HD u64 reduce_acc(const Acc& a, const Prime& p) {
     return r;
 }
 // Column accumulator for sums of residue products.  Operands are split into
-// S-bit digits (residues < 2^(2S): S = 30 for 60-bit primes, 28 for 55-bit),
-// so each 32x32 partial product is < 2^(2S) and accumulates with one
-// IMAD.WIDE (multiply + 64-bit add) into its column, with no carry handling:
-// a 64x64 product costs 4 IMAD.WIDE instead of 5 IMAD.WIDE + 2 IMAD + carries.
-// Column c1 takes two partials per product: up to 2^(63-2S) products.
+// S-bit digits (residues < 2^(2S): S = 30 for 60-bit primes, 28 for 55-bit)
+// and multiplied Karatsuba-style: c0 += a_l b_l, c2 += a_h b_h,
+// c1 += (a_l + a_h)(b_l + b_h), the middle column being c1 - c0 - c2 at fold
+// time.  Each partial product accumulates with one IMAD.WIDE (multiply + 64-bit
+// add) and no carry handling, so a 64x64 product costs 3 IMAD.WIDE instead of
+// 5 IMAD.WIDE + 2 IMAD + carries.  Digit sums are < 2^(S+1): c1 holds up to
+// 2^(62-2S) products between folds (4 at S = 30, 64 at S = 28).  Plain
+// additions go to a separate 128-bit word (x, xh), outside the columns.
 template <int S>
 struct Dig {
-    u32 l, h;
+    u32 l, h, s;  // s = l + h
 };
 template <int S>
 HD Dig<S> split(u64 a) {
-    return Dig<S>{(u32)a & ((1u << S) - 1u), (u32)(a >> S)};
+    const u32 l = (u32)a & ((1u << S) - 1u), h = (u32)(a >> S);
+    return Dig<S>{l, h, l + h};
 }
 struct Cols {
-    u64 c0 = 0, c1 = 0, c2 = 0;
+    u64 c0 = 0, c1 = 0, c2 = 0, x = 0, xh = 0;
     template <int S>
     HD void mac(Dig<S> a, Dig<S> b) {
         c0 += (u64)a.l * b.l;
-        c1 += (u64)a.l * b.h;
-        c1 += (u64)a.h * b.l;
+        c1 += (u64)a.s * b.s;
         c2 += (u64)a.h * b.h;
     }
-    // adds a full 64-bit value (the carry out of c0 moves to c1)
+    // adds a full 64-bit value
     template <int S>
     HD void add(u64 v) {
-        c0 += v;
-        c1 += (c0 < v) ? (1ULL << (64 - S)) : 0;
+        x += v;
+        xh += (x < v);
     }
-    // c0 + c1 2^S + c2 2^(2S) as a 128-bit accumulator
+    // x + c0 + (c1 - c0 - c2) 2^S + c2 2^(2S) as a 128-bit accumulator
     template <int S>
     HD Acc fold() const {
+        const u64 mid = c1 - c0 - c2;
         Acc a;
-        a.lo = c0;
-        a.hi = 0;
-        const u64 t1 = c1 << S, t2 = c2 << (2 * S);
+        a.lo = c0 + x;
+        a.hi = xh + (a.lo < x);
+        const u64 t1 = mid << S, t2 = c2 << (2 * S);
         a.lo += t1;
-        a.hi += (c1 >> (64 - S)) + (a.lo < t1);
+        a.hi += (mid >> (64 - S)) + (a.lo < t1);
         a.lo += t2;
         a.hi += (c2 >> (64 - 2 * S)) + (a.lo < t2);
         return a;
