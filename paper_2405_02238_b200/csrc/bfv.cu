@@ -35,7 +35,14 @@ struct ShapeQ8 {
     static constexpr int S = 28;  // 55-bit primes
 };
 // items per launch sequence: bounds temporaries and staging uploads
-constexpr int kChunkEnc = 256, kChunkDec = 1024, kChunkLin = 8192, kChunkKs = 1024, kChunkMult = 128;
+constexpr int kChunkEnc = 256, kChunkDec = 1024, kChunkLin = 8192, kChunkKs = 8192, kChunkMult = 4096;
+// key-switch and multiplication batches are also capped by their temporaries:
+// large batches fill the GPU (3 NTT CTAs per SM, >= 1 wave of limbs per launch)
+constexpr size_t kChunkBytes = (size_t)24 << 30;
+int chunk_for(size_t words_per_item, int cap) {
+    const size_t n = kChunkBytes / (words_per_item * 8);
+    return (int)std::max<size_t>(1, std::min<size_t>(n, (size_t)cap));
+}
 
 // values with |v| < q (noise, ternary, small messages)
 __device__ __forceinline__ u64 small_to_mod(i64 v, u64 q) { return v >= 0 ? (u64)v : q + v; }
@@ -950,9 +957,10 @@ void Context::lincomb(int n_out, const u32* off, const u64* const* in, const u64
 
 void Context::modup(int n, const u64* const* ct, u64* const* out) {
     if (n <= 0) return;
-    if (n > kChunkKs) {
-        for (int c0 = 0; c0 < n; c0 += kChunkKs) {
-            const int cn = std::min(kChunkKs, n - c0);
+    const int chunk = chunk_for((size_t)(hp_.dnum * hp_.R + 2 * hp_.R + 2 * hp_.L) * hp_.N, kChunkKs);
+    if (n > chunk) {
+        for (int c0 = 0; c0 < n; c0 += chunk) {
+            const int cn = std::min(chunk, n - c0);
             modup(cn, ct + c0, out + c0);
         }
         return;
@@ -1070,9 +1078,10 @@ void Context::key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, c
 void Context::rotate(int n, const u64* const* modup, const u64* const* ct, const u32* g,
                      u64* const* out) {
     if (n <= 0) return;
-    if (n > kChunkKs) {
-        for (int c0 = 0; c0 < n; c0 += kChunkKs) {
-            const int cn = std::min(kChunkKs, n - c0);
+    const int chunk = chunk_for((size_t)(hp_.dnum * hp_.R + 2 * hp_.R + 2 * hp_.L) * hp_.N, kChunkKs);
+    if (n > chunk) {
+        for (int c0 = 0; c0 < n; c0 += chunk) {
+            const int cn = std::min(chunk, n - c0);
             rotate(cn, modup + c0, ct + c0, g + c0, out + c0);
         }
         return;
@@ -1090,9 +1099,11 @@ void Context::rotate(int n, const u64* const* modup, const u64* const* ct, const
 
 void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* out) {
     if (n <= 0) return;
-    if (n > kChunkMult) {
-        for (int c0 = 0; c0 < n; c0 += kChunkMult) {
-            const int cn = std::min(kChunkMult, n - c0);
+    const u32 Lm = hp_.L, Rm = hp_.R, Dm = hp_.L + hp_.nB;
+    const int chunk = chunk_for((size_t)(7 * Lm + 4 * hp_.nB + 3 * Dm + hp_.dnum * Rm + 2 * Rm) * hp_.N, kChunkMult);
+    if (n > chunk) {
+        for (int c0 = 0; c0 < n; c0 += chunk) {
+            const int cn = std::min(chunk, n - c0);
             mult(cn, a + c0, b + c0, out + c0);
         }
         return;
