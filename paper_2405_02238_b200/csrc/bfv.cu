@@ -9,6 +9,7 @@
 #include <stdexcept>
 
 #include "context.hpp"
+#include "parallel.hpp"
 
 namespace hgm {
 
@@ -61,20 +62,23 @@ __device__ __forceinline__ u64 centred_lift(u64 y, u64 src, u64 dst) {
 
 // ---------------------------------------------------------------- encoding
 // oracle encode(): slot values mod t scattered to their NTT positions
-__global__ void k_encode_scatter(DevCtx cx, u32 n, const i64* vals,
+// vals: slot values already reduced to [0, t) on the host (to_slot_residue),
+// stride H per item
+__global__ void k_encode_scatter(DevCtx cx, u32 n, const u32* vals,
                                  const u32* S, u64* out) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, H = N / 2;
     ITEM_LOOP {
         COEF_LOOP {
             u64 v = 0;
-            if (j < S[item]) {
-                const i64 x = vals[(size_t)item * H + j];
-                v = x >= 0 ? (u64)x % kT : kT - 1 - ((u64)(-(x + 1)) % kT);
-            }
+            if (j < S[item]) v = vals[(size_t)item * H + j];
             out[(size_t)item * N + cx.slot_ntt[j]] = v;
         }
     }
+}
+// canonical residue mod t of a signed slot value (SlotBackend semantics)
+inline u32 to_slot_residue(i64 x) {
+    return (u32)(x >= 0 ? (u64)x % kT : kT - 1 - ((u64)(-(x + 1)) % kT));
 }
 
 // oracle encrypt(): sample u, e0, e1; c0 = e0 + Delta m, c1 = e1 (coefficient form)
@@ -158,13 +162,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_dec_round(DevCtx cx, u32 n, con
     }
 }
 
+// out: decrypted slots in [0, t) as u32, stride H per item
 __global__ void k_dec_gather(DevCtx cx, u32 n, const u64* M, const u32* S,
-                             i64* out) {
+                             u32* out) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, H = N / 2;
     ITEM_LOOP {
         for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < S[item]; i += gridDim.x * blockDim.x)
-            out[(size_t)item * H + i] = (i64)M[(size_t)item * N + cx.slot_ntt[i]];
+            out[(size_t)item * H + i] = (u32)M[(size_t)item * N + cx.slot_ntt[i]];
     }
 }
 
@@ -632,7 +637,7 @@ PinnedRing::~PinnedRing() {
     cudaFreeHost(host_);
     cudaFree(dev_);
 }
-void* PinnedRing::upload(const void* src, size_t bytes, cudaStream_t s) {
+char* PinnedRing::reserve(size_t bytes) {
     const size_t need = (bytes + 255) & ~size_t(255);
     if (need > cap_) throw std::length_error("staging ring too small for an upload of " + std::to_string(bytes));
     size_t b = head_;
@@ -655,8 +660,13 @@ void* PinnedRing::upload(const void* src, size_t bytes, cudaStream_t s) {
             }
         }
     }
-    std::memcpy(host_ + b, src, bytes);
-    HGM_CUDA(cudaMemcpyAsync(dev_ + b, host_ + b, bytes, cudaMemcpyHostToDevice, s));
+    head_ = e;
+    return host_ + b;
+}
+
+void* PinnedRing::commit(char* host, size_t bytes, cudaStream_t s) {
+    const size_t b = (size_t)(host - host_), e = b + ((bytes + 255) & ~size_t(255));
+    HGM_CUDA(cudaMemcpyAsync(dev_ + b, host, bytes, cudaMemcpyHostToDevice, s));
     cudaEvent_t ev;
     if (free_events_.empty()) {
         HGM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -666,8 +676,13 @@ void* PinnedRing::upload(const void* src, size_t bytes, cudaStream_t s) {
     }
     HGM_CUDA(cudaEventRecord(ev, s));
     marks_.push_back(Mark{((size_t)b << 32) | e, ev});
-    head_ = e;
     return dev_ + b;
+}
+
+void* PinnedRing::upload(const void* src, size_t bytes, cudaStream_t s) {
+    char* h = reserve(bytes);
+    std::memcpy(h, src, bytes);
+    return commit(h, bytes, s);
 }
 
 // ==================================================================== Context
@@ -722,6 +737,7 @@ Context::~Context() {
     cudaFree(d_slot_);
     cudaFree(d_cdt_);
     ring_.reset();
+    if (dl_host_) cudaFreeHost(dl_host_);
     cudaStreamDestroy(stream_);
 }
 
@@ -807,9 +823,9 @@ const u64* Context::mask_plain(const i64* mask, size_t S) {
     for (auto& e : bucket)
         if (e.content.size() == S && std::equal(e.content.begin(), e.content.end(), mask)) return e.dev;
     const u32 N = hp_.N, L = hp_.L;
-    std::vector<i64> padded(N / 2, 0);
-    std::copy(mask, mask + S, padded.begin());
-    const i64* dvals = upload(padded);
+    std::vector<u32> padded(N / 2, 0);
+    for (size_t j = 0; j < S; ++j) padded[j] = to_slot_residue(mask[j]);
+    const u32* dvals = upload(padded);
     std::vector<u32> Sv{(u32)S};
     const u32* dS = upload(Sv);
     u64* m = alloc(N);
@@ -838,15 +854,19 @@ void Context::encrypt(int n, const i64* const* host_vals, const size_t* S, const
         return;
     }
     const u32 N = hp_.N, L = hp_.L, H = N / 2;
-    std::vector<i64> vals((size_t)n * H, 0);
     std::vector<u32> Sv(n);
     std::vector<u64> ctr(counters, counters + n);
     std::vector<u64*> outs(out, out + n);
-    for (int i = 0; i < n; ++i) {
-        Sv[i] = (u32)S[i];
-        std::copy(host_vals[i], host_vals[i] + S[i], vals.begin() + (size_t)i * H);
-    }
-    const i64* dvals = static_cast<const i64*>(upload(vals));
+    for (int i = 0; i < n; ++i) Sv[i] = (u32)S[i];
+    // slot values -> residues mod t, written straight into pinned staging
+    const size_t vbytes = (size_t)n * H * sizeof(u32);
+    u32* hv = reinterpret_cast<u32*>(ring_->reserve(vbytes));
+    parallel_for((size_t)n, [&](size_t i) {
+        const i64* src = host_vals[i];
+        u32* dst = hv + i * H;
+        for (size_t j = 0; j < S[i]; ++j) dst[j] = to_slot_residue(src[j]);
+    });
+    const u32* dvals = static_cast<const u32*>(ring_->commit(reinterpret_cast<char*>(hv), vbytes, stream_));
     const u32* dS = upload(Sv);
     const u64* dctr = upload(ctr);
     u64* const* dout = upload(outs);
@@ -888,19 +908,33 @@ void Context::decrypt(int n, const u64* const* in, const size_t* S, i64* const* 
     const u32* dS = upload(Sv);
     u64* X = alloc((size_t)n * L * N);
     u64* M = alloc((size_t)n * N);
-    i64* O = reinterpret_cast<i64*>(alloc((size_t)n * H));
+    u32* O = reinterpret_cast<u32*>(alloc(((size_t)n * H + 1) / 2));
     if (hp_.L == 3) k_dec_phase<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, din, d_sk_, X); else k_dec_phase<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, din, d_sk_, X); ++launches_;
     ntt(false, jobs_contig(X, n * L, 0, L));
     if (hp_.L == 3) k_dec_round<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, X, M); else k_dec_round<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, X, M); ++launches_;
     ntt(true, jobs_contig(M, n, kTIndex, 1));
     k_dec_gather<<<grid_of(H, n), kThreads, 0, stream_>>>(cx_, n, M, dS, O); ++launches_;
-    std::vector<i64> host((size_t)n * H);
-    HGM_CUDA(cudaMemcpyAsync(host.data(), O, host.size() * 8, cudaMemcpyDeviceToHost, stream_));
+    const u32* host = static_cast<const u32*>(download_buffer((size_t)n * H * sizeof(u32)));
+    HGM_CUDA(cudaMemcpyAsync((void*)host, O, (size_t)n * H * sizeof(u32), cudaMemcpyDeviceToHost, stream_));
     release(X);
     release(M);
     release(O);
     sync();
-    for (int i = 0; i < n; ++i) std::copy(host.begin() + (size_t)i * H, host.begin() + (size_t)i * H + S[i], host_out[i]);
+    parallel_for((size_t)n, [&](size_t i) {
+        const u32* src = host + i * H;
+        i64* dst = host_out[i];
+        for (size_t j = 0; j < S[i]; ++j) dst[j] = (i64)src[j];
+    });
+}
+
+void* Context::download_buffer(size_t bytes) {
+    if (bytes > dl_cap_) {
+        if (dl_host_) HGM_CUDA(cudaFreeHost(dl_host_));
+        dl_host_ = nullptr;
+        HGM_CUDA(cudaMallocHost(&dl_host_, bytes));
+        dl_cap_ = bytes;
+    }
+    return dl_host_;
 }
 
 void Context::add(int n, const u64* const* a, const u64* const* b, u64* const* out) {

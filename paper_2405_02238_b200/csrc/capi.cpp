@@ -22,6 +22,7 @@
 #include "../../include/hegmm_b200.h"
 #include "context.hpp"
 #include "engine.hpp"
+#include "parallel.hpp"
 #include "hegmm_algos.hpp"
 
 using namespace hgm;
@@ -463,7 +464,7 @@ void run_instances(Context& ctx, const MatmulProgram& prog, size_t count,
     for (size_t c0 = 0; c0 < count; c0 += chunk) {
         const int K = (int)std::min(chunk, count - c0);
         std::vector<std::vector<std::vector<i64>>> packed(K);
-        for (int k = 0; k < K; ++k) packed[k] = prog.pack(a_of(c0 + k), b_of(c0 + k));
+        parallel_for((size_t)K, [&](size_t k) { packed[k] = prog.pack(a_of(c0 + k), b_of(c0 + k)); }, 4);
         ExecIO io;
         io.K = K;
         io.input = [](int, int) -> const u64* { return nullptr; };
@@ -482,7 +483,7 @@ void run_instances(Context& ctx, const MatmulProgram& prog, size_t count,
         if (final_words)
             HGM_CUDA(cudaMemcpy(final_words + c0 * W, res[0], (size_t)K * W * 8, cudaMemcpyDeviceToHost));
         for (u64* r : res) ctx.release(r);
-        for (int k = 0; k < K; ++k) prog.unpack(outv[k], c_of(c0 + k));
+        parallel_for((size_t)K, [&](size_t k) { prog.unpack(outv[k], c_of(c0 + k)); }, 4);
     }
     ctx.sync();
 }
@@ -649,8 +650,8 @@ int hgm_batch_encrypt(hgm_ctx* c, int algo, int order, int flags, size_t m, size
             std::vector<size_t> S;
             std::vector<u64> ctr;
             std::vector<u64*> dst;
+            parallel_for(K, [&](size_t k) { packed[k] = b->prog->pack(A + (c0 + k) * m * l, B + (c0 + k) * l * n); }, 4);
             for (size_t k = 0; k < K; ++k) {
-                packed[k] = b->prog->pack(A + (c0 + k) * m * l, B + (c0 + k) * l * n);
                 for (size_t s = 0; s < E; ++s) {
                     vals.push_back(packed[k][s].data());
                     S.push_back(b->prog->segment);
@@ -728,11 +729,10 @@ int hgm_batch_decrypt(hgm_ctx* c, hgm_batch* b, int64_t* C) {
         std::vector<i64> slots(b->count * prog.segment);
         const int rc = hgm_batch_decrypt_words(c, b->out, b->count, prog.segment, slots.data());
         if (rc != HGM_OK) throw std::runtime_error(g_err);
-        std::vector<i64> v(prog.segment);
-        for (size_t k = 0; k < b->count; ++k) {
-            std::copy(slots.begin() + k * prog.segment, slots.begin() + (k + 1) * prog.segment, v.begin());
+        parallel_for(b->count, [&](size_t k) {
+            std::vector<i64> v(slots.begin() + k * prog.segment, slots.begin() + (k + 1) * prog.segment);
             prog.unpack(v, C + k * prog.m * prog.n);
-        }
+        });
     });
 }
 

@@ -37,6 +37,10 @@ class PinnedRing {
     // Copies `bytes` from host `src` to the returned device pointer,
     // asynchronously on `s` (the device copy lives in `dev_` ring).
     void* upload(const void* src, size_t bytes, cudaStream_t s);
+    // Two-step form: reserve() returns the pinned host range to fill, commit()
+    // issues its copy and returns the device pointer.
+    char* reserve(size_t bytes);
+    void* commit(char* host, size_t bytes, cudaStream_t s);
 
   private:
     size_t cap_;
@@ -73,6 +77,8 @@ class Context {
     T* upload(const std::vector<T>& v) {
         return static_cast<T*>(ring_->upload(v.data(), v.size() * sizeof(T), stream_));
     }
+    // pinned host buffer for result downloads (grown on demand, reused)
+    void* download_buffer(size_t bytes);
 
     // ---------------------------------------------------------------- keys
     const u64* ks_key(u32 kid);  // [dnum][2][R][N]; kid = Galois element, 0 = relin
@@ -126,6 +132,8 @@ class Context {
     u64* d_sk_ = nullptr;  // [R][N]
     u64* d_pk_ = nullptr;  // [2][L][N]
     std::unique_ptr<PinnedRing> ring_;
+    void* dl_host_ = nullptr;
+    size_t dl_cap_ = 0;
     mutable std::mutex key_mu_;
     std::unordered_map<u32, u64*> keys_;
     std::mutex mask_mu_;
