@@ -10,6 +10,7 @@
 // every other intermediate is recomputed on demand (all ops are deterministic).
 #include <atomic>
 #include <functional>
+#include <future>
 #include <map>
 #include <tuple>
 #include <cstring>
@@ -461,10 +462,20 @@ void run_instances(Context& ctx, const MatmulProgram& prog, size_t count,
     HGM_CUDA(cudaMemGetInfo(&free_b, &total_b));
     size_t chunk = std::max<size_t>(1, (size_t)(0.45 * (double)free_b) / per_inst);
     chunk = std::min<size_t>(chunk, 1024);
+    // host packing of chunk i+1 and unpacking of chunk i-1 overlap chunk i's GPU work
+    using Packed = std::vector<std::vector<std::vector<i64>>>;
+    auto pack_chunk = [&](size_t c0) {
+        const size_t K = std::min(chunk, count - c0);
+        Packed p(K);
+        parallel_for(K, [&](size_t k) { p[k] = prog.pack(a_of(c0 + k), b_of(c0 + k)); }, 4);
+        return p;
+    };
+    std::future<Packed> next = std::async(std::launch::async, pack_chunk, (size_t)0);
+    std::future<void> unpacking;
     for (size_t c0 = 0; c0 < count; c0 += chunk) {
         const int K = (int)std::min(chunk, count - c0);
-        std::vector<std::vector<std::vector<i64>>> packed(K);
-        parallel_for((size_t)K, [&](size_t k) { packed[k] = prog.pack(a_of(c0 + k), b_of(c0 + k)); }, 4);
+        Packed packed = next.get();
+        if (c0 + chunk < count) next = std::async(std::launch::async, pack_chunk, c0 + chunk);
         ExecIO io;
         io.K = K;
         io.input = [](int, int) -> const u64* { return nullptr; };
@@ -483,8 +494,12 @@ void run_instances(Context& ctx, const MatmulProgram& prog, size_t count,
         if (final_words)
             HGM_CUDA(cudaMemcpy(final_words + c0 * W, res[0], (size_t)K * W * 8, cudaMemcpyDeviceToHost));
         for (u64* r : res) ctx.release(r);
-        parallel_for((size_t)K, [&](size_t k) { prog.unpack(outv[k], c_of(c0 + k)); }, 4);
+        if (unpacking.valid()) unpacking.get();
+        unpacking = std::async(std::launch::async, [&prog, &c_of, c0, K, outv = std::move(outv)]() {
+            parallel_for((size_t)K, [&](size_t k) { prog.unpack(outv[k], c_of(c0 + k)); }, 4);
+        });
     }
+    if (unpacking.valid()) unpacking.get();
     ctx.sync();
 }
 
