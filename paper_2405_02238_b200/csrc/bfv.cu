@@ -794,9 +794,11 @@ const u64* Context::ks_key(u32 kid) {
     u64* key = nullptr;
     HGM_CUDA(cudaMallocAsync((void**)&key, (size_t)dnum * 2 * R * N * 8, stream_));
     u64* E = alloc((size_t)dnum * R * N);
-    for (u32 dg = 0; dg < dnum; ++dg)
+    for (u32 dg = 0; dg < dnum; ++dg) {
         k_keygen_err<<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, kStreamKsE | ((u64)kid << 8) | dg, R,
-                                                             E + (size_t)dg * R * N); ++launches_;
+                                                             E + (size_t)dg * R * N);
+        ++launches_;
+    }
     ntt(true, jobs_contig(E, dnum * R, 0, R));
     if (hp_.L == 3) k_keygen_ks<ShapeQ3><<<dim3((N + kThreads - 1) / kThreads, dnum), kThreads, 0, stream_>>>(cx_, kid, kid, d_sk_, E, key); else k_keygen_ks<ShapeQ8><<<dim3((N + kThreads - 1) / kThreads, dnum), kThreads, 0, stream_>>>(cx_, kid, kid, d_sk_, E, key); ++launches_;
     release(E);
