@@ -525,7 +525,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_scale_round(DevCtx cx, u32 n, c
                 Cols acc;
                 acc.x = rr;  // rr < L * 2^60
                 for (u32 i = 0; i < L; ++i) acc.mac(ad[i], split<SH::S>(dp->W[i][k]));
-                acc.mac(split<SH::S>(t[(size_t)(L + k) * N + j]), split<SH::S>(dp->T_n[k]));
+                const u64 tb = reduce_once(reduce_once(t[(size_t)(L + k) * N + j], b << 1), b);  // [0, 4b) -> [0, b)
+                acc.mac(split<SH::S>(tb), split<SH::S>(dp->T_n[k]));
                 const u64 c = shoup_mul(reduce_acc(acc.fold<SH::S>(), dp->pr[L + K + k]), dp->bhat_inv[k],
                                         dp->bhat_inv_sh[k], b);
                 cb[k] = split<SH::S>(c);
@@ -1083,7 +1084,7 @@ void Context::key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, c
         pj.count = n * 2 * K;
         pj.period = K;
         for (u32 k = 0; k < K; ++k) pj.prime[k] = (unsigned char)(L + k);
-        pj.unscaled = 1;  // k_moddown_conv / ModDownIO fold N^-1 into phat_inv
+        pj.unscaled = kLazyOut;  // k_moddown_conv / ModDownIO: Shoup by phat_inv_n (N^-1 folded in)
         ntt(false, pj);
     }
     if (ntt_fusable(hp_.dev, kFuseModDown)) {
@@ -1155,7 +1156,7 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
                 src[(size_t)i * 4 * L + w] = (w < 2 * L ? a[i] + (size_t)w * N : b[i] + (size_t)(w - 2 * L) * N);
         NttJobs xj = jobs_contig(X, n * 4 * L, 0, L);
         xj.src = upload(src);
-        xj.unscaled = 1;  // k_q_to_b folds N^-1 into qhat_inv
+        xj.unscaled = kLazyOut;  // k_q_to_b: Shoup by qhat_inv_n (N^-1 folded in)
         ntt(false, xj);
     } else {
         std::vector<const u64*> src((size_t)2 * n);
@@ -1186,7 +1187,7 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
     release(XB);
     NttJobs tj = jobs_contig(T, n * 3 * D, 0, D);
     for (u32 k = 0; k < nB; ++k) tj.prime[L + k] = (unsigned char)(L + K + k);
-    tj.unscaled = 1;  // k_scale_round folds N^-1 into dhat_inv and T
+    tj.unscaled = kLazyOut;  // k_scale_round: Shoup by dhat_inv_n; B limbs reduced, times T_n
     ntt(false, tj);
     // 4. scale and round back to Q (coefficient form)
     u64* E = alloc((size_t)n * 3 * LN);

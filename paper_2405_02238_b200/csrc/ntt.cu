@@ -422,6 +422,20 @@ __device__ __forceinline__ void load_block(u64* sm, const u64* g) {
     }
 }
 
+// stores the smem values as they are (in [0, 4q): NttJobs::kLazyOut)
+template <int LB, int E = kElems>
+__device__ __forceinline__ void store_block_raw(const u64* sm, u64* g) {
+    constexpr int NB = 1 << LB, T = NB / E;
+    ulonglong2* g2 = reinterpret_cast<ulonglong2*>(g);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < NB / 2; i += T) {
+        ulonglong2 v;
+        v.x = sm[pad(2 * i)];
+        v.y = sm[pad(2 * i + 1)];
+        __stcs(g2 + i, v);
+    }
+}
+
 // stores canonical residues from smem values in [0, 4q), optionally scaled
 template <int LB, bool kScale, int E = kElems>
 __device__ __forceinline__ void store_block(const u64* sm, u64* g, u64 q, u64 s, u64 ssh) {
@@ -872,12 +886,14 @@ __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_inv3(DevCtx cx, 
     __syncthreads();
     if (logN == LB && !jobs.unscaled)
         store_block<LB, true, kElems3>(sm, g, q, P.ninv, P.ninv_sh);
+    else if (logN == LB && jobs.unscaled == kLazyOut)
+        store_block_raw<LB, kElems3>(sm, g);
     else
         store_block<LB, false, kElems3>(sm, g, q, 0, 0);
 }
 
-// Inverse transform of a whole limb read from io.src(job) whose canonical,
-// UNSCALED (N * INTT) output is consumed by io.store(job, i, v0, v1)
+// Inverse transform of a whole limb read from io.src(job) whose UNSCALED
+// (N * INTT) output, in [0, 4q), is consumed by io.store(job, i, v0, v1)
 // (elements 2i, 2i+1): a base conversion fused behind the INTT.
 template <int LB, typename IO>
 __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_inv_io(DevCtx cx, IO io) {
@@ -901,11 +917,8 @@ __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_inv_io(DevCtx cx
     inv_round<LB, LB - 4, 4, true, kElems3>(sm, cache, pairs(w + 2 * N), q, logN, 0);
     __syncthreads();
 #pragma unroll 4
-    for (int i = threadIdx.x; i < NB / 2; i += T) {
-        const u64 v0 = reduce_once(reduce_once(sm[pad(2 * i)], q << 1), q);
-        const u64 v1 = reduce_once(reduce_once(sm[pad(2 * i + 1)], q << 1), q);
-        io.store(dp, job, (u32)i, v0, v1);
-    }
+    for (int i = threadIdx.x; i < NB / 2; i += T)  // values in [0, 4q): io.store takes any 64-bit input
+        io.store(dp, job, (u32)i, sm[pad(2 * i)], sm[pad(2 * i + 1)]);
 }
 
 // ModDown conversion fused behind the INTT of acc's P limb (K = 1, so P/p = 1):

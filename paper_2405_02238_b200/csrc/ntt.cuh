@@ -30,7 +30,10 @@ struct NttJobs {
     u32 count = 0;
     u32 period = 1;
     // inverse only: leave out the N^-1 scaling (the output is N * INTT(x)); for
-    // consumers whose first step multiplies by a constant that has N^-1 folded in
+    // consumers whose first step multiplies by a constant that has N^-1 folded in.
+    // 1: canonical residues; 2 (kLazyOut): residues in [0, 4q), not reduced
+    // (whole-limb transforms; for consumers whose Shoup product takes any
+    // 64-bit input -- others get canonical output)
     u32 unscaled = 0;
     unsigned char prime[32] = {0};  // host-side pattern
     u64 packed[4] = {0, 0, 0, 0};   // the same pattern, packed for the kernel
@@ -70,6 +73,8 @@ void ntt_moddown_conv_fused(const DevCtx& cx, const DevParams& hp, int n, u64* c
                             u64* V, cudaStream_t s);
 // copies a parameter set's constants into this translation unit's __constant__ slot
 void ntt_upload_params(int pid, const DevParams& p);
+
+constexpr u32 kLazyOut = 2;
 
 inline NttJobs jobs_contig(u64* base, u32 count, u32 first_prime, u32 period) {
     NttJobs j;
