@@ -299,7 +299,7 @@ HD u32 galois_src(u32 k, u32 g, u32 logN) {
     for (u32 i = 0, x = k; i < logN; ++i, x >>= 1) bk = (bk << 1) | (x & 1);
 #endif
     const u32 twoN_mask = (2u << logN) - 1;
-    const u32 e = (u32)(((unsigned long long)g * (2 * bk + 1)) & twoN_mask);
+    const u32 e = (g * (2 * bk + 1)) & twoN_mask;  // mod 2^32 then mod 2N (2N | 2^32)
 #ifdef __CUDA_ARCH__
     return __brev((e - 1) >> 1) >> (32 - logN);
 #else

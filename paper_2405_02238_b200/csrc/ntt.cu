@@ -632,9 +632,9 @@ struct ModDownIO {
     __device__ void store(const DevParams* dp, u32 job, u32 i2, u64 v0, u64 v1) const {
         const u32 item = job / (2 * L), c = (job / L) & 1, i = job % L;
         const u64 q = dp->pr[i].q, pi = dp->P_inv_q[i], pis = dp->P_inv_q_sh[i];
-        const u64* a = acc[item] + ((size_t)c * R + i) * N;
-        u64 r0 = add_mod(v0, shoup_mul(a[2 * i2], pi, pis, q), q);
-        u64 r1 = add_mod(v1, shoup_mul(a[2 * i2 + 1], pi, pis, q), q);
+        const ulonglong2 av = __ldcs(reinterpret_cast<const ulonglong2*>(acc[item] + ((size_t)c * R + i) * N) + i2);
+        u64 r0 = add_mod(v0, shoup_mul(av.x, pi, pis, q), q);
+        u64 r1 = add_mod(v1, shoup_mul(av.y, pi, pis, q), q);
         if (c == 0 && addn) {
             const u64* x = addn[item] + (size_t)i * N;
             const u32 ge = g[item];
