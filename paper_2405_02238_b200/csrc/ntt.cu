@@ -365,7 +365,7 @@ __device__ __forceinline__ void store_last_stage(const u64* sm, u64* g, const ul
     }
 }
 
-// Same, handing each finished pair (elements 2i, 2i+1, canonical) to `st`.
+// Same, handing each finished pair (elements 2i, 2i+1, in [0, 4q)) to `st`.
 template <int LB, typename St, int E = kElems>
 __device__ __forceinline__ void store_last_stage_io(const u64* sm, const St& st, const ulonglong2* __restrict__ tw_tab, u64 q, int logN, int blk) {
     constexpr int NB = 1 << LB, T = NB / E;
@@ -377,7 +377,7 @@ __device__ __forceinline__ void store_last_stage_io(const u64* sm, const St& st,
         const u64 w = t.x, ws = t.y;
         const u64 U = reduce_once(reduce_once(reduce_once(sm[pad(2 * i)], q4 << 1), q4), q2);  // [0, 16q) -> [0, 2q)
         const u64 V = shoup_lazy(sm[pad(2 * i + 1)], w, ws, q);
-        st(i, reduce_once(reduce_once(U + V, q2), q), reduce_once(reduce_once(U - V + q2, q2), q));
+        st(i, U + V, U - V + q2);  // lazy, in [0, 4q): the consumer reduces
     }
 }
 
@@ -596,10 +596,11 @@ struct ModUpIO {
         }
         return v;
     }
-    __device__ void store(const DevParams*, u32 job, u32 i, u64 v0, u64 v1) const {
+    __device__ void store(const DevParams* dp, u32 job, u32 i, u64 v0, u64 v1) const {
+        const u64 q = dp->pr[job % R].q;
         ulonglong2 v;
-        v.x = v0;
-        v.y = v1;
+        v.x = reduce_once(reduce_once(v0, q << 1), q);
+        v.y = reduce_once(reduce_once(v1, q << 1), q);
         reinterpret_cast<ulonglong2*>(D + (size_t)job * N)[i] = v;
     }
 };
@@ -633,17 +634,19 @@ struct ModDownIO {
         const u32 item = job / (2 * L), c = (job / L) & 1, i = job % L;
         const u64 q = dp->pr[i].q, pi = dp->P_inv_q[i], pis = dp->P_inv_q_sh[i];
         const ulonglong2 av = __ldcs(reinterpret_cast<const ulonglong2*>(acc[item] + ((size_t)c * R + i) * N) + i2);
-        u64 r0 = add_mod(v0, shoup_mul(av.x, pi, pis, q), q);
-        u64 r1 = add_mod(v1, shoup_mul(av.y, pi, pis, q), q);
+        // lazy sums (v < 4q, Shoup < 3q, addend < q), one reduction chain from [0, 8q)
+        u64 r0 = v0 + shoup_lazy3(av.x, pi, pis, q);
+        u64 r1 = v1 + shoup_lazy3(av.y, pi, pis, q);
         if (c == 0 && addn) {
             const u64* x = addn[item] + (size_t)i * N;
             const u32 ge = g[item];
-            r0 = add_mod(r0, x[ge == 1 ? 2 * i2 : galois_src(2 * i2, ge, logN)], q);
-            r1 = add_mod(r1, x[ge == 1 ? 2 * i2 + 1 : galois_src(2 * i2 + 1, ge, logN)], q);
+            r0 += x[ge == 1 ? 2 * i2 : galois_src(2 * i2, ge, logN)];
+            r1 += x[ge == 1 ? 2 * i2 + 1 : galois_src(2 * i2 + 1, ge, logN)];
         }
+        const u64 q2 = q << 1, q4 = q << 2;
         ulonglong2 v;
-        v.x = r0;
-        v.y = r1;
+        v.x = reduce_once(reduce_once(reduce_once(r0, q4), q2), q);
+        v.y = reduce_once(reduce_once(reduce_once(r1, q4), q2), q);
         reinterpret_cast<ulonglong2*>(out[item] + ((size_t)c * L + i) * N)[i2] = v;
     }
 };
