@@ -200,38 +200,58 @@ __global__ void k_copy(u32 n, size_t W, const u64* const* in, u64* const* out) {
 }
 
 // out[o] = sum_t in[t] (.* mask[t]) : oracle cmult() followed by add()
+// Masks are stored in packed digit form (mask_digits: l | h << 32).  Each
+// thread takes two adjacent words (16-byte loads) of one limb.
 template <typename SH>
 __global__ void k_lincomb(DevCtx cx, u32 n, const u32* off,
                           const u64* const* in, const u64* const* mask, u64* const* out) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, L = SH::L;
-    const size_t LN = (size_t)L * N, W = 2 * LN;
+    const u32 N = dp->N, logN = dp->logN, L = SH::L;
+    const size_t LN = (size_t)L * N, W2 = LN;  // word pairs per ciphertext
     ITEM_LOOP {
         const u32 t0 = off[item], t1 = off[item + 1];
-        u64* o = out[item];
-        for (size_t w = (size_t)blockIdx.x * blockDim.x + threadIdx.x; w < W; w += (size_t)gridDim.x * blockDim.x) {
-            const size_t wl = w < LN ? w : w - LN;
-            const Prime& P = dp->pr[wl / N];
-            // exact 128-bit accumulation; reduced after every 3 masked products
+        ulonglong2* o = reinterpret_cast<ulonglong2*>(out[item]);
+        for (size_t w2 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; w2 < W2; w2 += (size_t)gridDim.x * blockDim.x) {
+            const size_t wl2 = w2 < LN / 2 ? w2 : w2 - LN / 2;  // pair index within the component
+            const Prime& P = dp->pr[(wl2 * 2) >> logN];
+            // exact accumulation; reduced after every 3 masked products
             // (the sum stays below 2^(s+62), reduce_acc's range)
-            Cols acc;
+            Cols a0, a1;
             u32 pending = 0;
             for (u32 t = t0; t < t1; ++t) {
-                const u64 v = in[t][w];
-                if (mask[t]) {
-                    acc.mac(split<SH::S>(v), split<SH::S>(mask[t][wl]));
+                const ulonglong2 v = reinterpret_cast<const ulonglong2*>(in[t])[w2];
+                const u64* mt = mask[t];
+                if (mt) {
+                    const ulonglong2 m = __ldg(reinterpret_cast<const ulonglong2*>(mt) + wl2);
+                    a0.mac(split<SH::S>(v.x), packed_dig<SH::S>(m.x));
+                    a1.mac(split<SH::S>(v.y), packed_dig<SH::S>(m.y));
                     if (++pending == 3) {
-                        const u64 r = reduce_acc(acc.fold<SH::S>(), P);
-                        acc = Cols{};
-                        acc.x = r;
+                        const u64 r0 = reduce_acc(a0.fold<SH::S>(), P), r1 = reduce_acc(a1.fold<SH::S>(), P);
+                        a0 = Cols{};
+                        a1 = Cols{};
+                        a0.x = r0;
+                        a1.x = r1;
                         pending = 0;
                     }
                 } else {
-                    acc.add<SH::S>(v);
+                    a0.add<SH::S>(v.x);
+                    a1.add<SH::S>(v.y);
                 }
             }
-            o[w] = reduce_acc(acc.fold<SH::S>(), P);
+            ulonglong2 r;
+            r.x = reduce_acc(a0.fold<SH::S>(), P);
+            r.y = reduce_acc(a1.fold<SH::S>(), P);
+            o[w2] = r;
         }
+    }
+}
+
+// canonical mask residues -> packed digit form (l | h << 32) for k_lincomb
+template <typename SH>
+__global__ void k_mask_digits(u64* m, size_t words) {
+    for (size_t w = (size_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (size_t)gridDim.x * blockDim.x) {
+        const Dig<SH::S> d = split<SH::S>(m[w]);
+        m[w] = (u64)d.l | ((u64)d.h << 32);
     }
 }
 
@@ -839,6 +859,8 @@ const u64* Context::mask_plain(const i64* mask, size_t S) {
     HGM_CUDA(cudaMallocAsync((void**)&out, (size_t)L * N * 8, stream_));
     if (hp_.L == 3) k_mask_lift<ShapeQ3><<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, m, out); else k_mask_lift<ShapeQ8><<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, m, out); ++launches_;
     ntt(true, jobs_contig(out, L, 0, L));
+    if (hp_.L == 3) k_mask_digits<ShapeQ3><<<grid_of(N, 1), kThreads, 0, stream_>>>(out, (size_t)L * N); else k_mask_digits<ShapeQ8><<<grid_of(N, 1), kThreads, 0, stream_>>>(out, (size_t)L * N);
+    ++launches_;
     release(m);
     HGM_CUDA(cudaGetLastError());
     bucket.push_back(MaskEntry{std::vector<i64>(mask, mask + S), out});

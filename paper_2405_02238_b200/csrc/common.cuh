@@ -207,6 +207,12 @@ HD Dig<S> split(u64 a) {
     const u32 l = (u32)a & ((1u << S) - 1u), h = (u32)(a >> S);
     return Dig<S>{l, h, l + h};
 }
+// digits of a value stored packed as l | h << 32 (k_mask_digits)
+template <int S>
+HD Dig<S> packed_dig(u64 p) {
+    const u32 l = (u32)p, h = (u32)(p >> 32);
+    return Dig<S>{l, h, l + h};
+}
 struct Cols {
     u64 c0 = 0, c1 = 0, c2 = 0, x = 0, xh = 0;
     template <int S>
