@@ -1202,15 +1202,19 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
     // 3. tensor over Q ++ B, INTT
     const u32 D = L + nB;
     u64* T = alloc((size_t)n * 3 * D * N);
-    {
-        std::vector<const u64*> va(a, a + n), vb(b, b + n);
+    std::vector<const u64*> va(a, a + n), vb(b, b + n);
+    if (ntt_tensor_fusable(hp_.dev)) {  // tensor computed inside its INTT's load
+        ntt_tensor_fused(cx_, hp_.dev, n, upload(va), upload(vb), XB, T, stream_);
+        ++launches_;
+        release(XB);
+    } else {
         if (hp_.L == 3) k_tensor<ShapeQ3><<<grid_of(N, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T); else k_tensor<ShapeQ8><<<grid_of(N, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T); ++launches_;
+        release(XB);
+        NttJobs tj = jobs_contig(T, n * 3 * D, 0, D);
+        for (u32 k = 0; k < nB; ++k) tj.prime[L + k] = (unsigned char)(L + K + k);
+        tj.unscaled = kLazyOut;  // k_scale_round: Shoup by dhat_inv_n; B limbs reduced, times T_n
+        ntt(false, tj);
     }
-    release(XB);
-    NttJobs tj = jobs_contig(T, n * 3 * D, 0, D);
-    for (u32 k = 0; k < nB; ++k) tj.prime[L + k] = (unsigned char)(L + K + k);
-    tj.unscaled = kLazyOut;  // k_scale_round: Shoup by dhat_inv_n; B limbs reduced, times T_n
-    ntt(false, tj);
     // 4. scale and round back to Q (coefficient form)
     u64* E = alloc((size_t)n * 3 * LN);
     if (hp_.L == 3) k_scale_round<ShapeQ3><<<grid_of(N, n, 3), kThreads, 0, stream_>>>(cx_, n, T, E); else k_scale_round<ShapeQ8><<<grid_of(N, n, 3), kThreads, 0, stream_>>>(cx_, n, T, E); ++launches_;

@@ -381,11 +381,10 @@ __device__ __forceinline__ void store_last_stage_io(const u64* sm, const St& st,
     }
 }
 
-// Inverse: the first Gentleman-Sande stage (t = 1) fused into the coalesced load.
-template <int LB, int E = kElems>
-__device__ __forceinline__ void load_first_stage(u64* sm, const u64* g, const ulonglong2* __restrict__ tw_tab, u64 q, int logN, int blk) {
+template <int LB, int E, typename Ld2>
+__device__ __forceinline__ void load_first_stage_fn(u64* sm, const Ld2& ld2, const ulonglong2* __restrict__ tw_tab,
+                                                    u64 q, int logN, int blk) {
     constexpr int NB = 1 << LB, T = NB / E;
-    const ulonglong2* g2 = reinterpret_cast<const ulonglong2*>(g);
     const int tw0 = (1 << (logN - 1)) + (blk << (LB - 1));
     // batches of kB pairs: all loads of a batch in flight before any use
     constexpr int kIt = NB / 2 / T, kB = kIt < 8 ? kIt : 8;
@@ -396,7 +395,7 @@ __device__ __forceinline__ void load_first_stage(u64* sm, const u64* g, const ul
 #pragma unroll
         for (int b = 0; b < kB; ++b) {
             const int i = threadIdx.x + (i0 + b) * T;
-            v[b] = __ldcs(g2 + i);
+            v[b] = ld2(i);
             const ulonglong2 t = __ldg(tw_tab + tw0 + i);
             w[b] = t.x;
             ws[b] = t.y;
@@ -408,6 +407,15 @@ __device__ __forceinline__ void load_first_stage(u64* sm, const u64* g, const ul
             sm[pad(2 * i + 1)] = shoup_lazy3(v[b].x - v[b].y + (q << 1), w[b], ws[b], q);
         }
     }
+}
+
+// Inverse: the first Gentleman-Sande stage (t = 1) fused into the coalesced load
+// (inputs canonical, or below 2q).
+template <int LB, int E = kElems>
+__device__ __forceinline__ void load_first_stage(u64* sm, const u64* g, const ulonglong2* __restrict__ tw_tab, u64 q,
+                                                 int logN, int blk) {
+    const ulonglong2* g2 = reinterpret_cast<const ulonglong2*>(g);
+    load_first_stage_fn<LB, E>(sm, [g2](int i) { return __ldcs(g2 + i); }, tw_tab, q, logN, blk);
 }
 
 template <int LB, int E = kElems>
@@ -895,7 +903,8 @@ __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_inv3(DevCtx cx, 
         store_block<LB, false, kElems3>(sm, g, q, 0, 0);
 }
 
-// Inverse transform of a whole limb read from io.src(job) whose UNSCALED
+// Inverse transform of a whole limb read as pairs from io.load2(job, i) (values
+// below 2q) whose UNSCALED
 // (N * INTT) output, in [0, 4q), is consumed by io.store(job, i, v0, v1)
 // (elements 2i, 2i+1): a base conversion fused behind the INTT.
 template <int LB, typename IO>
@@ -911,7 +920,7 @@ __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_inv_io(DevCtx cx
     const u64 q = dp->pr[prime].q;
     const u64* w = cx.tw + (size_t)prime * 4 * N;
     fill_tw_cache(cache, pairs(w + 2 * N), 0, 0, kTwCache3);
-    load_first_stage<LB, kElems3>(sm, io.src(job), pairs(w + 2 * N), q, logN, 0);
+    load_first_stage_fn<LB, kElems3>(sm, [&](int i) { return io.load2(dp, job, (u32)i); }, pairs(w + 2 * N), q, logN, 0);
     __syncthreads();
     inv_round<LB, 1, LB - 9, false, kElems3>(sm, cache, pairs(w + 2 * N), q, logN, 0);
     __syncthreads();
@@ -933,7 +942,9 @@ struct MdConvIO {
     u64* V;                    // [n][2][L][N]
     u32 L, R, N;
     __device__ int prime(u32) const { return (int)L; }
-    __device__ const u64* src(u32 job) const { return acc[job >> 1] + ((size_t)(job & 1) * R + L) * N; }
+    __device__ ulonglong2 load2(const DevParams*, u32 job, u32 i) const {
+        return __ldcs(reinterpret_cast<const ulonglong2*>(acc[job >> 1] + ((size_t)(job & 1) * R + L) * N) + i);
+    }
     __device__ void store(const DevParams* dp, u32 job, u32 i2, u64 v0, u64 v1) const {
         const u32 item = job >> 1, c = job & 1;
         const u64 p = dp->pr[L].q;
@@ -950,6 +961,61 @@ struct MdConvIO {
             v.y = sub_mod(b.y, shoup_mul(centred_lift_n(z1, p, q), pi, pis, q), q);
             reinterpret_cast<ulonglong2*>(out + (size_t)i * N)[i2] = v;
         }
+    }
+};
+
+// The BFV tensor product fused into the INTT that brings it back to the
+// coefficient domain: job = (item, component p, limb d of Q ++ B); the INTT
+// input pair is computed from the NTT-domain operands (Q limbs of a, b; B limbs
+// of their extension XB) and the output, N * INTT in [0, 4q), is stored to
+// T[item][p][d] (k_scale_round's input, kLazyOut).
+template <int S>
+struct TensorIO {
+    const u64* const* A;
+    const u64* const* B;
+    const u64* XB;  // [n][4][nB][N]: a.c0, a.c1, b.c0, b.c1 over B
+    u64* T;         // [n][3][D][N]
+    u32 L, K, nB, D, N;
+    __device__ int prime(u32 job) const {
+        const u32 d = job % D;
+        return (int)(d < L ? d : L + K + (d - L));
+    }
+    __device__ ulonglong2 load2(const DevParams* dp, u32 job, u32 i) const {
+        const u32 item = job / (3 * D), p = (job / D) % 3, d = job % D;
+        const ulonglong2 *a0, *a1, *b0, *b1;
+        if (d < L) {
+            a0 = reinterpret_cast<const ulonglong2*>(A[item] + (size_t)d * N);
+            a1 = reinterpret_cast<const ulonglong2*>(A[item] + (size_t)(L + d) * N);
+            b0 = reinterpret_cast<const ulonglong2*>(B[item] + (size_t)d * N);
+            b1 = reinterpret_cast<const ulonglong2*>(B[item] + (size_t)(L + d) * N);
+        } else {
+            const u64* base = XB + (size_t)item * 4 * nB * N + (size_t)(d - L) * N;
+            a0 = reinterpret_cast<const ulonglong2*>(base);
+            a1 = reinterpret_cast<const ulonglong2*>(base + (size_t)nB * N);
+            b0 = reinterpret_cast<const ulonglong2*>(base + (size_t)2 * nB * N);
+            b1 = reinterpret_cast<const ulonglong2*>(base + (size_t)3 * nB * N);
+        }
+        const Prime& P = dp->pr[d < L ? d : L + K + (d - L)];
+        Cols s0, s1;
+        if (p == 0) {
+            const ulonglong2 x = a0[i], y = b0[i];
+            s0.mac(split<S>(x.x), split<S>(y.x));
+            s1.mac(split<S>(x.y), split<S>(y.y));
+        } else if (p == 2) {
+            const ulonglong2 x = a1[i], y = b1[i];
+            s0.mac(split<S>(x.x), split<S>(y.x));
+            s1.mac(split<S>(x.y), split<S>(y.y));
+        } else {
+            const ulonglong2 x0 = a0[i], x1 = a1[i], y0 = b0[i], y1 = b1[i];
+            s0.mac(split<S>(x0.x), split<S>(y1.x));
+            s0.mac(split<S>(x1.x), split<S>(y0.x));
+            s1.mac(split<S>(x0.y), split<S>(y1.y));
+            s1.mac(split<S>(x1.y), split<S>(y0.y));
+        }
+        return make_ulonglong2(reduce_acc(s0.fold<S>(), P), reduce_acc(s1.fold<S>(), P));
+    }
+    __device__ void store(const DevParams*, u32 job, u32 i, u64 v0, u64 v1) const {
+        __stcs(reinterpret_cast<ulonglong2*>(T + (size_t)job * N) + i, make_ulonglong2(v0, v1));
     }
 };
 
@@ -1055,6 +1121,28 @@ void ntt_moddown_conv_fused(const DevCtx& cx, const DevParams& hp, int n, u64* c
                             u64* V, cudaStream_t s) {
     MdConvIO io{acc, ecoef, V, hp.L, hp.R, hp.N};
     launch_inv_io(cx, hp, io, (u32)n * 2, s);
+}
+
+bool ntt_tensor_fusable(const DevParams& hp) {
+    static const bool on = [] {
+        const char* e = std::getenv("HGM_FUSED_TENSOR");
+        return e && e[0] == '1';  // opt-in: measured 1% slower than k_tensor + INTT
+    }();
+    return on && hp.logN <= 13;
+}
+
+void ntt_tensor_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* const* A, const u64* const* B,
+                      const u64* XB, u64* T, cudaStream_t s) {
+    const u32 D = hp.L + hp.nB;
+    if (hp.logN == 13 || hp.logN == 12) {
+        if (hp.L == 3) {
+            TensorIO<30> io{A, B, XB, T, hp.L, hp.K, hp.nB, D, hp.N};
+            launch_inv_io(cx, hp, io, (u32)n * 3 * D, s);
+        } else {
+            TensorIO<28> io{A, B, XB, T, hp.L, hp.K, hp.nB, D, hp.N};
+            launch_inv_io(cx, hp, io, (u32)n * 3 * D, s);
+        }
+    }
 }
 
 void ntt_upload_params(int pid, const DevParams& p) {

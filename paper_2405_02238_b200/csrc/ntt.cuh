@@ -71,6 +71,12 @@ void ntt_finish_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* V
 bool ntt_conv_fusable(const DevParams& hp);
 void ntt_moddown_conv_fused(const DevCtx& cx, const DevParams& hp, int n, u64* const* acc, const u64* const* ecoef,
                             u64* V, cudaStream_t s);
+// The tensor product over Q ++ B fused into its INTT (whole limbs; opt-in,
+// HGM_FUSED_TENSOR=1): T[item][p][d] = N * INTT(tensor_p) in [0, 4q),
+// A/B per item NTT-domain ciphertexts, XB [n][4][nB][N] their B extension.
+bool ntt_tensor_fusable(const DevParams& hp);
+void ntt_tensor_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* const* A, const u64* const* B,
+                      const u64* XB, u64* T, cudaStream_t s);
 // copies a parameter set's constants into this translation unit's __constant__ slot
 void ntt_upload_params(int pid, const DevParams& p);
 
