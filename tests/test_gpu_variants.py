@@ -1,0 +1,34 @@
+"""GPU: the alternative kernel paths stay bit-exact.
+
+The library picks its NTT layout and kernel fusions once per process from the
+environment (csrc/ntt.cu: HGM_NTT3, HGM_FUSED_KS, HGM_FUSED_CONV,
+HGM_FUSED_FINISH, HGM_FUSED_TENSOR).  Each variant re-runs the primitive
+parity tests (every op against the CPU oracle, ciphertext words bit-exact) and
+the HEGMM product tests in a fresh process with that environment."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+VARIANTS = {
+    "one-cta-ntt": {"HGM_NTT3": "0"},
+    "fused-modup-moddown": {"HGM_FUSED_KS": "1"},
+    "fused-modup": {"HGM_FUSED_KS": "u"},
+    "unfused-conv-finish": {"HGM_FUSED_CONV": "0", "HGM_FUSED_FINISH": "0"},
+    "fused-tensor": {"HGM_FUSED_TENSOR": "1"},
+}
+
+
+@pytest.mark.parametrize("name", sorted(VARIANTS))
+def test_variant_parity(name):
+    env = dict(os.environ)
+    env.update(VARIANTS[name])
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        "tests/test_gpu_parity.py", "tests/test_gpu_hegmm.py"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, f"{name}: {VARIANTS[name]}\n{r.stdout[-3000:]}\n{r.stderr[-2000:]}"
