@@ -285,11 +285,16 @@ __global__ void k_gather_c1(DevCtx cx, u32 n, const u64* const* ct, u64* C) {
 
 // oracle key_switch() ModUp: digit dg of the coefficient-domain poly C, lifted
 // to every limb of Q ++ P with centred residues.  D: [n][dnum][R][N]
+// from_intt: C is an unscaled, lazy INTT (N * c1 in [0, 4q)); N^-1 is folded
+// into dg_hat_inv_n and the digit's own limbs are not written (the caller
+// copies them from the NTT-domain ciphertext, so they need no forward NTT).
 template <typename SH>
 __global__ void k_modup_lift(DevCtx cx, u32 n, const u64* C, size_t c_stride,
-                             u64* D) {
+                             u64* D, int from_intt) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = SH::L, R = SH::R, A = SH::A, dnum = SH::dnum;
+    const u64* ghi = from_intt ? dp->dg_hat_inv_n : dp->dg_hat_inv;
+    const u64* ghs = from_intt ? dp->dg_hat_inv_n_sh : dp->dg_hat_inv_sh;
     ITEM_LOOP {
         const u64* c = C + item * c_stride;
         u64* d = D + (size_t)item * dnum * R * N;
@@ -300,11 +305,12 @@ __global__ void k_modup_lift(DevCtx cx, u32 n, const u64* C, size_t c_stride,
                 u64 y[kMaxL];
                 for (u32 a = 0; a < A; ++a) {
                     const u32 i = dg * A + a;
-                    y[a] = shoup_mul(x[i], dp->dg_hat_inv[i], dp->dg_hat_inv_sh[i], dp->pr[i].q);
+                    y[a] = shoup_mul(x[i], ghi[i], ghs[i], dp->pr[i].q);
                 }
                 for (u32 r = 0; r < R; ++r) {
                     u64 v;
                     if (r < L && r / A == dg) {
+                        if (from_intt) continue;
                         v = x[r];
                     } else {
                         const u64 qr = dp->pr[r].q;
@@ -1027,12 +1033,16 @@ void Context::modup(int n, const u64* const* ct, u64* const* out) {
     const u32 N = hp_.N, L = hp_.L, R = hp_.R, dnum = hp_.dnum;
     std::vector<const u64*> vc(ct, ct + n);
     u64* C = alloc((size_t)n * L * N);
+    // own_copy: a digit's own limbs are the ciphertext's NTT-domain c1 limbs, copied
+    // instead of lifted and transformed back; then the c1 INTT can stay unscaled
+    const bool own_copy = ntt_fusable_size(hp_.dev) && !ntt_fusable(hp_.dev, kFuseModUp);
     if (ntt_fusable_size(hp_.dev)) {  // out-of-place INTT of the c1 limbs
         std::vector<const u64*> src((size_t)n * L);
         for (int i = 0; i < n; ++i)
             for (u32 l = 0; l < L; ++l) src[(size_t)i * L + l] = ct[i] + (size_t)(L + l) * N;
         NttJobs cj = jobs_contig(C, n * L, 0, L);
         cj.src = upload(src);
+        if (own_copy) cj.unscaled = kLazyOut;  // k_modup_lift: Shoup by dg_hat_inv_n
         ntt(false, cj);
     } else {
         if (hp_.L == 3) k_gather_c1<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, upload(vc), C); else k_gather_c1<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, upload(vc), C); ++launches_;
@@ -1046,8 +1056,39 @@ void Context::modup(int n, const u64* const* ct, u64* const* out) {
     if (ntt_fusable(hp_.dev, kFuseModUp)) {
         ntt_modup_fused(cx_, hp_.dev, n, C, (size_t)L * N, D, stream_);
         ++launches_;
+    } else if (own_copy) {
+        if (hp_.L == 3) k_modup_lift<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, C, (size_t)L * N, D, 1); else k_modup_lift<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, C, (size_t)L * N, D, 1); ++launches_;
+        // forward NTT of the lifted (non-own) limbs only; own limbs copied from c1
+        const u32 A = hp_.alpha, per = dnum * R - L;
+        NttJobs dj;
+        std::vector<u64*> dl((size_t)n * per);
+        std::vector<const u64*> csrc((size_t)n * L);
+        std::vector<u64*> cdst((size_t)n * L);
+        u32 k = 0;
+        for (u32 dg = 0; dg < dnum; ++dg)
+            for (u32 r = 0; r < R; ++r)
+                if (!(r < L && r / A == dg)) dj.prime[k++] = (unsigned char)r;
+        for (int i = 0; i < n; ++i) {
+            u64* base = D + (size_t)i * dnum * R * N;
+            u32 t = 0;
+            for (u32 dg = 0; dg < dnum; ++dg)
+                for (u32 r = 0; r < R; ++r) {
+                    u64* limb = base + ((size_t)dg * R + r) * N;
+                    if (r < L && r / A == dg) {
+                        csrc[(size_t)i * L + r] = ct[i] + (size_t)(L + r) * N;
+                        cdst[(size_t)i * L + r] = limb;
+                    } else {
+                        dl[(size_t)i * per + t++] = limb;
+                    }
+                }
+        }
+        dj.ptrs = upload(dl);
+        dj.count = n * per;
+        dj.period = per;
+        ntt(true, dj);
+        k_copy<<<grid_of(N, n * L), kThreads, 0, stream_>>>(n * L, N, upload(csrc), upload(cdst)); ++launches_;
     } else {
-        if (hp_.L == 3) k_modup_lift<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, C, (size_t)L * N, D); else k_modup_lift<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, C, (size_t)L * N, D); ++launches_;
+        if (hp_.L == 3) k_modup_lift<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, C, (size_t)L * N, D, 0); else k_modup_lift<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, C, (size_t)L * N, D, 0); ++launches_;
         ntt(true, jobs_contig(D, n * dnum * R, 0, R));
     }
     if (!contiguous) {
@@ -1226,7 +1267,7 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
         ntt_modup_fused(cx_, hp_.dev, n, E + 2 * LN, 3 * LN, Dg, stream_);
         ++launches_;
     } else {
-        if (hp_.L == 3) k_modup_lift<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, E + 2 * LN, 3 * LN, Dg); else k_modup_lift<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, E + 2 * LN, 3 * LN, Dg); ++launches_;
+        if (hp_.L == 3) k_modup_lift<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, E + 2 * LN, 3 * LN, Dg, 0); else k_modup_lift<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, E + 2 * LN, 3 * LN, Dg, 0); ++launches_;
         ntt(true, jobs_contig(Dg, n * dnum * R, 0, R));
     }
     u64* A = alloc((size_t)n * 2 * R * N);

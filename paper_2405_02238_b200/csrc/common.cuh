@@ -87,6 +87,7 @@ struct DevParams {
     u64 dhat_inv_n[kMaxL], dhat_inv_n_sh[kMaxL];
     u64 T_n[kMaxB];
     u64 phat_inv_n[kMaxK], phat_inv_n_sh[kMaxK];
+    u64 dg_hat_inv_n[kMaxL], dg_hat_inv_n_sh[kMaxL];
 };
 
 // Per-context values passed by value to every kernel (the parameter-set

@@ -243,6 +243,10 @@ HostParams make_params(int id, u64 seed) {
         d.dhat_inv_n_sh[i] = shoup_of(d.dhat_inv_n[i], qv(i));
     }
     for (unsigned j = 0; j < nB; ++j) d.T_n[j] = with_ninv(d.T[j], L + K + j);
+    for (unsigned i = 0; i < L; ++i) {
+        d.dg_hat_inv_n[i] = with_ninv(d.dg_hat_inv[i], i);
+        d.dg_hat_inv_n_sh[i] = shoup_of(d.dg_hat_inv_n[i], qv(i));
+    }
     for (unsigned k = 0; k < K; ++k) {
         d.phat_inv_n[k] = with_ninv(d.phat_inv[k], L + k);
         d.phat_inv_n_sh[k] = shoup_of(d.phat_inv_n[k], h.primes[L + k]);
