@@ -846,8 +846,8 @@ void launch_block(bool fwd, const DevCtx& cx, const NttJobs& jobs, int sub, cuda
 // 255 cached twiddle pairs (stages < 8), no double buffer: 72 KB of shared
 // memory and <= 85 registers, so three CTAs (24 warps) share an SM.
 
-template <int LB>
-__global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_fwd3(DevCtx cx, NttJobs jobs) {
+template <int LB, int E = kElems3, int MINB = 3>
+__global__ void __launch_bounds__((1 << LB) / E, MINB) k_ntt_fwd3(DevCtx cx, NttJobs jobs) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     extern __shared__ u64 sm[];
     u64* cache = sm + smem_words<LB>();
@@ -863,17 +863,17 @@ __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_fwd3(DevCtx cx, 
     fill_tw_cache(cache, pairs(w), pre, blk, kTwCache3);
     __syncthreads();
     auto ld = [src](int j) { return __ldcs(src + j); };
-    fwd_round<LB, 0, 4, true, true, decltype(ld), kElems3>(sm, cache, pairs(w), q, pre, blk, ld);
+    fwd_round<LB, 0, 4, true, true, decltype(ld), E>(sm, cache, pairs(w), q, pre, blk, ld);
     __syncthreads();
-    fwd_round<LB, 4, 4, true, false, NoLoad, kElems3>(sm, cache, pairs(w), q, pre, blk);
+    fwd_round<LB, 4, 4, true, false, NoLoad, E>(sm, cache, pairs(w), q, pre, blk);
     __syncthreads();
-    fwd_round<LB, 8, LB - 9, false, false, NoLoad, kElems3>(sm, cache, pairs(w), q, pre, blk);
+    fwd_round<LB, 8, LB - 9, false, false, NoLoad, E>(sm, cache, pairs(w), q, pre, blk);
     __syncthreads();
-    store_last_stage<LB, kElems3>(sm, g, pairs(w), q, logN, blk);
+    store_last_stage<LB, E>(sm, g, pairs(w), q, logN, blk);
 }
 
-template <int LB>
-__global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_inv3(DevCtx cx, NttJobs jobs) {
+template <int LB, int E = kElems3, int MINB = 3>
+__global__ void __launch_bounds__((1 << LB) / E, MINB) k_ntt_inv3(DevCtx cx, NttJobs jobs) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     extern __shared__ u64 sm[];
     u64* cache = sm + smem_words<LB>();
@@ -887,20 +887,20 @@ __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_inv3(DevCtx cx, 
     u64* g = jv.ptr + ((size_t)blk << LB);
     const u64* src = jobs.src ? jobs.src[blockIdx.x] + ((size_t)blk << LB) : g;
     fill_tw_cache(cache, pairs(w + 2 * N), logN - LB, blk, kTwCache3);
-    load_first_stage<LB, kElems3>(sm, src, pairs(w + 2 * N), q, logN, blk);
+    load_first_stage<LB, E>(sm, src, pairs(w + 2 * N), q, logN, blk);
     __syncthreads();
-    inv_round<LB, 1, LB - 9, false, kElems3>(sm, cache, pairs(w + 2 * N), q, logN, blk);
+    inv_round<LB, 1, LB - 9, false, E>(sm, cache, pairs(w + 2 * N), q, logN, blk);
     __syncthreads();
-    inv_round<LB, LB - 8, 4, true, kElems3>(sm, cache, pairs(w + 2 * N), q, logN, blk);
+    inv_round<LB, LB - 8, 4, true, E>(sm, cache, pairs(w + 2 * N), q, logN, blk);
     __syncthreads();
-    inv_round<LB, LB - 4, 4, true, kElems3>(sm, cache, pairs(w + 2 * N), q, logN, blk);
+    inv_round<LB, LB - 4, 4, true, E>(sm, cache, pairs(w + 2 * N), q, logN, blk);
     __syncthreads();
     if (logN == LB && !jobs.unscaled)
-        store_block<LB, true, kElems3>(sm, g, q, P.ninv, P.ninv_sh);
+        store_block<LB, true, E>(sm, g, q, P.ninv, P.ninv_sh);
     else if (logN == LB && jobs.unscaled == kLazyOut)
-        store_block_raw<LB, kElems3>(sm, g);
+        store_block_raw<LB, E>(sm, g);
     else
-        store_block<LB, false, kElems3>(sm, g, q, 0, 0);
+        store_block<LB, false, E>(sm, g, q, 0, 0);
 }
 
 // Inverse transform of a whole limb read as pairs from io.load2(job, i) (values
@@ -1040,24 +1040,44 @@ void launch_inv_io(const DevCtx& cx, const DevParams& hp, const IO& io, u32 jobs
     }
 }
 
-template <int LB>
-void launch_block3(bool fwd, const DevCtx& cx, const NttJobs& jobs, int sub, cudaStream_t s) {
+int ntt_elems() {
+    static const int e = [] {
+        const char* v = std::getenv("HGM_NTT_E");
+        const int x = v ? std::atoi(v) : 32;
+        return x == 16 || x == 322 ? x : 32;
+    }();
+    return e;
+}
+
+template <int LB, int E, int MINB>
+void launch_block_e(bool fwd, const DevCtx& cx, const NttJobs& jobs, int sub, cudaStream_t s) {
     const size_t smem = (smem_words<LB>() + 2 * kTwCache3) * sizeof(u64);
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_ntt_fwd3<LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_ntt_inv3<LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_ntt_fwd3<LB, E, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_ntt_inv3<LB, E, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
     const dim3 grid(jobs.count, sub);
     if (fwd)
-        k_ntt_fwd3<LB><<<grid, (1 << LB) / kElems3, smem, s>>>(cx, jobs);
+        k_ntt_fwd3<LB, E, MINB><<<grid, (1 << LB) / E, smem, s>>>(cx, jobs);
     else
-        k_ntt_inv3<LB><<<grid, (1 << LB) / kElems3, smem, s>>>(cx, jobs);
+        k_ntt_inv3<LB, E, MINB><<<grid, (1 << LB) / E, smem, s>>>(cx, jobs);
 }
 
-// Default for whole 2^13 limbs (measured +15% forward, +19% inverse over the
-// persistent 512-thread kernel); HGM_NTT3=0 selects the persistent kernel.
+// shared-memory resident block kernels: 256 threads x 32 residues, 3 CTAs/SM
+// (default), 512 x 16 at 2 CTAs/SM (HGM_NTT_E=16: spills, -8%), or 256 x 32 at
+// 2 CTAs/SM (HGM_NTT_E=322: no spills, forward -4%, inverse +2%)
+template <int LB>
+void launch_block3(bool fwd, const DevCtx& cx, const NttJobs& jobs, int sub, cudaStream_t s) {
+    if (ntt_elems() == 16)
+        launch_block_e<LB, 16, 2>(fwd, cx, jobs, sub, s);
+    else if (ntt_elems() == 322)  // 2 CTAs/SM, 128 registers
+        launch_block_e<LB, kElems3, 2>(fwd, cx, jobs, sub, s);
+    else
+        launch_block_e<LB, kElems3, 3>(fwd, cx, jobs, sub, s);
+}
+
 bool use_ntt3() {
     static const bool on = [] {
         const char* e = std::getenv("HGM_NTT3");
