@@ -45,6 +45,7 @@ TOTAL_INSTANCES = 4096
 SEED = 20240404
 PARAM_ID = 0  # N 8192 / Q 3x60-bit / P 1x60-bit / dnum 3
 LIMB_BYTES = 2 * 8 * 8192  # algorithmic bytes of one N=8192 limb NTT (read + write)
+OP_BYTES_PER_MATMUL = 1.2445e9  # SURVEY.md 8(d), cfg2/cfg4 basic_mm
 
 
 def env_int(name, default):
@@ -345,7 +346,15 @@ def main():
                 "kernel": "k_ntt_fwd3<13> (forward NTT, N=8192, 64-bit Shoup, 3 CTAs/SM)",
                 "algorithmic_bytes_per_launch": limbs * LIMB_BYTES, "limbs_per_launch": limbs,
                 "inverse_frac": round(limbs * LIMB_BYTES / (intt_ms / 1e3) / 1e9 / peak, 4),
-                "peak_source": peak_src}
+                "peak_source": peak_src,
+                "frac_vs_spec_8tbs": round(achieved / 8000.0, 4),
+                # op-level bytes of one cfg2/cfg4 basic_mm matmul
+                # (every primitive's compulsory ciphertext/key/mask traffic x the reference op
+                # counts); fused, deduplicated execution may move fewer, so frac may exceed 1
+                "op_level": {"bytes_per_matmul": OP_BYTES_PER_MATMUL,
+                             "achieved": round(value * OP_BYTES_PER_MATMUL / 1e9 / world, 1),
+                             "unit": "GB/s per GPU",
+                             "frac": round(value * OP_BYTES_PER_MATMUL / 1e9 / world / peak, 4)}}
 
     if rank == 0:
         clocks = clk.summary()
