@@ -526,7 +526,10 @@ __global__ void k_tensor(DevCtx cx, u32 n, const u64* const* A,
 
 // oracle scale_round(): round(t x / Q) from Q ++ B residues, then exact B -> Q
 template <typename SH>
-__global__ void __launch_bounds__(kThreads, 4) k_scale_round(DevCtx cx, u32 n, const u64* T, u64* E) {
+// Dg (optional, alpha = 1): component 2 is not stored in E but lifted straight
+// into the relinearisation digits [n][dnum][R][N] (k_modup_lift's output: digit
+// dg = limb dg, centred into every other limb).
+__global__ void __launch_bounds__(kThreads, 4) k_scale_round(DevCtx cx, u32 n, const u64* T, u64* E, u64* Dg) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = SH::L, K = SH::K, nB = SH::nB, D = L + nB;
     ITEM_LOOP {
@@ -564,7 +567,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_scale_round(DevCtx cx, u32 n, c
                 Cols acc;
                 for (u32 k = 0; k < nB; ++k) acc.mac(cb[k], split<SH::S>(dp->bhat_mod_q[k][i]));
                 acc.add<SH::S>(v * dp->neg_B_mod_q[i]);  // v <= nB: < 2^64, a plain addend
-                e[(size_t)i * N + j] = reduce_acc(acc.fold<SH::S>(), dp->pr[i]);
+                const u64 r = reduce_acc(acc.fold<SH::S>(), dp->pr[i]);
+                if (SH::A == 1 && Dg && p == 2) {
+                    u64* dgi = Dg + ((size_t)item * SH::dnum + i) * SH::R * N;
+                    for (u32 rr2 = 0; rr2 < SH::R; ++rr2)
+                        dgi[(size_t)rr2 * N + j] = rr2 == i ? r : centred_lift(r, dp->pr[i].q, dp->pr[rr2].q);
+                } else {
+                    e[(size_t)i * N + j] = r;
+                }
             }
         }
     }
@@ -1258,12 +1268,16 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
     }
     // 4. scale and round back to Q (coefficient form)
     u64* E = alloc((size_t)n * 3 * LN);
-    if (hp_.L == 3) k_scale_round<ShapeQ3><<<grid_of(N, n, 3), kThreads, 0, stream_>>>(cx_, n, T, E); else k_scale_round<ShapeQ8><<<grid_of(N, n, 3), kThreads, 0, stream_>>>(cx_, n, T, E); ++launches_;
-    release(T);
-    // 5. relinearise e2: ModUp, inner product with rlk, ModDown, add (e0, e1)
     const bool fused = ntt_fusable(hp_.dev, kFuseModUp);
     u64* Dg = alloc((size_t)n * dnum * R * N);
-    if (fused) {
+    // alpha = 1: scale-and-round writes e2's ModUp digits itself
+    const bool lift_in_sr = hp_.alpha == 1 && !fused;
+    if (hp_.L == 3) k_scale_round<ShapeQ3><<<grid_of(N, n, 3), kThreads, 0, stream_>>>(cx_, n, T, E, lift_in_sr ? Dg : nullptr); else k_scale_round<ShapeQ8><<<grid_of(N, n, 3), kThreads, 0, stream_>>>(cx_, n, T, E, nullptr); ++launches_;
+    release(T);
+    // 5. relinearise e2: ModUp, inner product with rlk, ModDown, add (e0, e1)
+    if (lift_in_sr) {
+        ntt(true, jobs_contig(Dg, n * dnum * R, 0, R));
+    } else if (fused) {
         ntt_modup_fused(cx_, hp_.dev, n, E + 2 * LN, 3 * LN, Dg, stream_);
         ++launches_;
     } else {
