@@ -113,6 +113,10 @@ HostParams make_params(int id, u64 seed) {
         const u64 c = (1ULL << h.spec.qbits) - k * 2 * N + 1;
         if (is_prime(c)) h.primes.push_back(c);
     }
+    // the lazy NTT butterflies keep values below 16q and the column accumulator
+    // splits residues into two digits of at most 30 bits: both need q < 2^60
+    for (u64 q : h.primes)
+        if (q >> 60) throw std::logic_error("prime above 2^60 breaks the lazy NTT / digit bounds");
     // tables: slot t lives at kTIndex
     h.tw.assign((size_t)(kMaxPrimes + 1) * 4 * N, 0);
     auto fill = [&](unsigned slot, u64 q) {
