@@ -12,6 +12,10 @@ namespace {
 __constant__ DevParams c_dp[kParamSets];
 
 __device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
+// pad() of a compile-time offset.  For base = (block << b) + o with b >= 4 and an
+// offset k * 2^s whose bits lie above o's (o < 2^s), pad(base + off) =
+// pad(base) + padc(off): one runtime pad per group, immediates for the rest.
+constexpr int padc(int i) { return i + (i >> 4); }
 
 template <int LB>
 constexpr int smem_words() {
@@ -270,10 +274,11 @@ __device__ __forceinline__ void inv_round(u64* sm, const u64* __restrict__ tw_ca
         const int o = gi & ((1 << LT_LO) - 1);
         const int block = gi >> LT_LO;
         const int base = (block << (LT_LO + R)) + o;
+        const int pb = pad(base);
         u64 x[1 << R];
         if constexpr (kCached) {
 #pragma unroll
-            for (int k = 0; k < (1 << R); ++k) x[k] = sm[pad(base + (k << LT_LO))];
+            for (int k = 0; k < (1 << R); ++k) x[k] = sm[pb + padc(k << LT_LO)];
             auto tw = [&](int r, int c, u64& w, u64& ws) {
                 const int i = (1 << (LB - LT_LO - r - 1)) - 1 + (block << (R - r - 1)) + c;
                 w = tw_cache[2 * i];
@@ -294,7 +299,7 @@ __device__ __forceinline__ void inv_round(u64* sm, const u64* __restrict__ tw_ca
                     pws[slot] = t.y;
                 }
 #pragma unroll
-            for (int k = 0; k < (1 << R); ++k) x[k] = sm[pad(base + (k << LT_LO))];
+            for (int k = 0; k < (1 << R); ++k) x[k] = sm[pb + padc(k << LT_LO)];
             auto tw = [&](int r, int c, u64& w, u64& ws) {
                 const int slot = (1 << R) - (1 << (R - r)) + c;
                 w = pw[slot];
@@ -303,7 +308,7 @@ __device__ __forceinline__ void inv_round(u64* sm, const u64* __restrict__ tw_ca
             inv_stage<R, 0>(x, q, q4, tw);
         }
 #pragma unroll
-        for (int k = 0; k < (1 << R); ++k) sm[pad(base + (k << LT_LO))] = x[k];
+        for (int k = 0; k < (1 << R); ++k) sm[pb + padc(k << LT_LO)] = x[k];
     }
 }
 
@@ -402,9 +407,9 @@ __device__ __forceinline__ void load_first_stage_fn(u64* sm, const Ld2& ld2, con
         }
 #pragma unroll
         for (int b = 0; b < kB; ++b) {
-            const int i = threadIdx.x + (i0 + b) * T;
-            sm[pad(2 * i)] = reduce_once(v[b].x + v[b].y, q << 1);
-            sm[pad(2 * i + 1)] = shoup_lazy3(v[b].x - v[b].y + (q << 1), w[b], ws[b], q);
+            const int p = pad(2 * (int)threadIdx.x) + padc(2 * (i0 + b) * T);
+            sm[p] = reduce_once(v[b].x + v[b].y, q << 1);
+            sm[p + 1] = shoup_lazy3(v[b].x - v[b].y + (q << 1), w[b], ws[b], q);
         }
     }
 }
@@ -422,11 +427,12 @@ template <int LB, int E = kElems>
 __device__ __forceinline__ void load_block(u64* sm, const u64* g) {
     constexpr int NB = 1 << LB, T = NB / E;
     const ulonglong2* g2 = reinterpret_cast<const ulonglong2*>(g);
+    const int p0 = pad(2 * (int)threadIdx.x);
 #pragma unroll 4
-    for (int i = threadIdx.x; i < NB / 2; i += T) {
-        const ulonglong2 v = g2[i];
-        sm[pad(2 * i)] = v.x;
-        sm[pad(2 * i + 1)] = v.y;
+    for (int j = 0; j < NB / 2 / T; ++j) {
+        const ulonglong2 v = g2[threadIdx.x + j * T];
+        sm[p0 + padc(2 * j * T)] = v.x;
+        sm[p0 + padc(2 * j * T) + 1] = v.y;
     }
 }
 
@@ -435,12 +441,14 @@ template <int LB, int E = kElems>
 __device__ __forceinline__ void store_block_raw(const u64* sm, u64* g) {
     constexpr int NB = 1 << LB, T = NB / E;
     ulonglong2* g2 = reinterpret_cast<ulonglong2*>(g);
+    const int p0 = pad(2 * (int)threadIdx.x);
 #pragma unroll 4
-    for (int i = threadIdx.x; i < NB / 2; i += T) {
+    for (int j = 0; j < NB / 2 / T; ++j) {
+        const int p = p0 + padc(2 * j * T);
         ulonglong2 v;
-        v.x = sm[pad(2 * i)];
-        v.y = sm[pad(2 * i + 1)];
-        __stcs(g2 + i, v);
+        v.x = sm[p];
+        v.y = sm[p + 1];
+        __stcs(g2 + threadIdx.x + j * T, v);
     }
 }
 
@@ -449,17 +457,19 @@ template <int LB, bool kScale, int E = kElems>
 __device__ __forceinline__ void store_block(const u64* sm, u64* g, u64 q, u64 s, u64 ssh) {
     constexpr int NB = 1 << LB, T = NB / E;
     ulonglong2* g2 = reinterpret_cast<ulonglong2*>(g);
+    const int p0 = pad(2 * (int)threadIdx.x);
 #pragma unroll 4
-    for (int i = threadIdx.x; i < NB / 2; i += T) {
+    for (int j = 0; j < NB / 2 / T; ++j) {
+        const int p = p0 + padc(2 * j * T);
         ulonglong2 v;
         if constexpr (kScale) {
-            v.x = shoup_mul(sm[pad(2 * i)], s, ssh, q);
-            v.y = shoup_mul(sm[pad(2 * i + 1)], s, ssh, q);
+            v.x = shoup_mul(sm[p], s, ssh, q);
+            v.y = shoup_mul(sm[p + 1], s, ssh, q);
         } else {
-            v.x = reduce_once(reduce_once(sm[pad(2 * i)], q << 1), q);
-            v.y = reduce_once(reduce_once(sm[pad(2 * i + 1)], q << 1), q);
+            v.x = reduce_once(reduce_once(sm[p], q << 1), q);
+            v.y = reduce_once(reduce_once(sm[p + 1], q << 1), q);
         }
-        g2[i] = v;
+        g2[threadIdx.x + j * T] = v;
     }
 }
 
@@ -928,9 +938,12 @@ __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_inv_io(DevCtx cx
     __syncthreads();
     inv_round<LB, LB - 4, 4, true, kElems3>(sm, cache, pairs(w + 2 * N), q, logN, 0);
     __syncthreads();
+    const int p0 = pad(2 * (int)threadIdx.x);
 #pragma unroll 4
-    for (int i = threadIdx.x; i < NB / 2; i += T)  // values in [0, 4q): io.store takes any 64-bit input
-        io.store(dp, job, (u32)i, sm[pad(2 * i)], sm[pad(2 * i + 1)]);
+    for (int j = 0; j < NB / 2 / T; ++j) {  // values in [0, 4q): io.store takes any 64-bit input
+        const int p = p0 + padc(2 * j * T);
+        io.store(dp, job, (u32)(threadIdx.x + j * T), sm[p], sm[p + 1]);
+    }
 }
 
 // ModDown conversion fused behind the INTT of acc's P limb (K = 1, so P/p = 1):
