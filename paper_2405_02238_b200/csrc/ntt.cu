@@ -220,6 +220,9 @@ __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_ca
         const int o = gi & ((1 << LT_MIN) - 1);
         const int block = gi >> LT_MIN;
         const int base = (block << (LT_FIRST + 1)) + o;
+        constexpr bool kFold = !kFromGlobal;  // measured: folding in the global-load round costs registers
+        const int pb = pad(base);
+        auto at = [&](int k) { return kFold ? pb + padc(k << LT_MIN) : pad(base + (k << LT_MIN)); };
         u64 x[1 << R];
         if constexpr (kCached) {
             if constexpr (kFromGlobal) {
@@ -227,7 +230,7 @@ __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_ca
                 for (int k = 0; k < (1 << R); ++k) x[k] = ld(base + (k << LT_MIN));
             } else {
 #pragma unroll
-                for (int k = 0; k < (1 << R); ++k) x[k] = sm[pad(base + (k << LT_MIN))];
+                for (int k = 0; k < (1 << R); ++k) x[k] = sm[at(k)];
             }
             auto tw = [&](int r, int c, u64& w, u64& ws) {
                 const int i = (1 << (S0 + r)) - 1 + (block << r) + c;
@@ -247,7 +250,7 @@ __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_ca
                     pws[(1 << r) - 1 + c] = t.y;
                 }
 #pragma unroll
-            for (int k = 0; k < (1 << R); ++k) x[k] = sm[pad(base + (k << LT_MIN))];
+            for (int k = 0; k < (1 << R); ++k) x[k] = sm[at(k)];
             auto tw = [&](int r, int c, u64& w, u64& ws) {
                 w = pw[(1 << r) - 1 + c];
                 ws = pws[(1 << r) - 1 + c];
@@ -255,7 +258,7 @@ __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_ca
             fwd_stage<R, 0, S0>(x, q, q4, q8, tw);
         }
 #pragma unroll
-        for (int k = 0; k < (1 << R); ++k) sm[pad(base + (k << LT_MIN))] = x[k];
+        for (int k = 0; k < (1 << R); ++k) sm[at(k)] = x[k];
     }
 }
 
