@@ -246,7 +246,8 @@ __global__ void k_lincomb(DevCtx cx, u32 n, const u32* off,
     }
 }
 
-// canonical mask residues -> packed digit form (l | h << 32) for k_lincomb
+// canonical residues -> packed digit form (l | h << 32) for k_lincomb (masks) and
+// k_ks_inner (keys); launch on a 1-D grid (every word converted exactly once)
 template <typename SH>
 __global__ void k_mask_digits(u64* m, size_t words) {
     for (size_t w = (size_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (size_t)gridDim.x * blockDim.x) {
@@ -332,7 +333,8 @@ __global__ void k_modup_lift(DevCtx cx, u32 n, const u64* C, size_t c_stride,
     }
 }
 
-// acc[c][r] = sum_dg D[dg][r][galois_src(k)] * key[dg][c][r][k]  ([n][2][R][N])
+// acc[c][r] = sum_dg D[dg][r][galois_src(k)] * key[dg][c][r][k]  ([n][2][R][N];
+// keys stored in packed digit form, k_mask_digits)
 // Items are grouped by Galois key (the engine sorts rotations by element): a
 // block serves up to kKeyReuse consecutive items and reads each key element
 // once for all items of the group that share it.
@@ -355,8 +357,8 @@ __global__ void k_ks_inner(DevCtx cx, u32 n, const u64* const* D,
                 const Prime& P = dp->pr[r];
                 Dig<SH::S> k0[4], k1[4];
                 for (u32 dg = 0; dg < dnum; ++dg) {
-                    k0[dg] = split<SH::S>(__ldg(k + (((size_t)dg * 2 + 0) * R + r) * N + j));
-                    k1[dg] = split<SH::S>(__ldg(k + (((size_t)dg * 2 + 1) * R + r) * N + j));
+                    k0[dg] = packed_dig<SH::S>(__ldg(k + (((size_t)dg * 2 + 0) * R + r) * N + j));
+                    k1[dg] = packed_dig<SH::S>(__ldg(k + (((size_t)dg * 2 + 1) * R + r) * N + j));
                 }
                 for (u32 u = 0; u < same; ++u) {
                     const u64* d = D[i0 + u];
@@ -381,8 +383,8 @@ __global__ void k_ks_inner(DevCtx cx, u32 n, const u64* const* D,
                     Cols a0, a1;
                     for (u32 dg = 0; dg < dnum; ++dg) {
                         const Dig<SH::S> x = split<SH::S>(d[((size_t)dg * R + r) * N + su]);
-                        a0.mac(x, split<SH::S>(__ldg(kk + (((size_t)dg * 2 + 0) * R + r) * N + j)));
-                        a1.mac(x, split<SH::S>(__ldg(kk + (((size_t)dg * 2 + 1) * R + r) * N + j)));
+                        a0.mac(x, packed_dig<SH::S>(__ldg(kk + (((size_t)dg * 2 + 0) * R + r) * N + j)));
+                        a1.mac(x, packed_dig<SH::S>(__ldg(kk + (((size_t)dg * 2 + 1) * R + r) * N + j)));
                     }
                     a[(size_t)r * N + j] = reduce_acc(a0.fold<SH::S>(), dp->pr[r]);
                     a[((size_t)R + r) * N + j] = reduce_acc(a1.fold<SH::S>(), dp->pr[r]);
@@ -838,6 +840,11 @@ const u64* Context::ks_key(u32 kid) {
     }
     ntt(true, jobs_contig(E, dnum * R, 0, R));
     if (hp_.L == 3) k_keygen_ks<ShapeQ3><<<dim3((N + kThreads - 1) / kThreads, dnum), kThreads, 0, stream_>>>(cx_, kid, kid, d_sk_, E, key); else k_keygen_ks<ShapeQ8><<<dim3((N + kThreads - 1) / kThreads, dnum), kThreads, 0, stream_>>>(cx_, kid, kid, d_sk_, E, key); ++launches_;
+    // k_ks_inner (the only reader) takes the key in packed digit form
+    const size_t kw = (size_t)dnum * 2 * R * N;
+    const dim3 kg((unsigned)((kw + 4 * kThreads - 1) / (4 * kThreads)));  // 1-D: each word converted once
+    if (hp_.L == 3) k_mask_digits<ShapeQ3><<<kg, kThreads, 0, stream_>>>(key, kw); else k_mask_digits<ShapeQ8><<<kg, kThreads, 0, stream_>>>(key, kw);
+    ++launches_;
     release(E);
     HGM_CUDA(cudaGetLastError());
     std::lock_guard<std::mutex> lk(key_mu_);
