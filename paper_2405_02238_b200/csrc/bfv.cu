@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_q_to_b(DevCtx cx, u32 n, const 
             Acc128 s{0, 0};
             for (u32 i = 0; i < L; ++i) {
                 y[i] = shoup_mul(x[(size_t)i * N + j], dp->qhat_inv_n[i], dp->qhat_inv_n_sh[i], dp->pr[i].q);
-                fx_add(s, y[i], dp->one_over_q[i]);
+                fx_add_small(s, y[i], dp->one_over_q[i]);  // 1/q_i: integer part < 2^32
             }
             const u64 v = fx_round(s);
             Dig<SH::S> yd[kMaxL];
@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_scale_round(DevCtx cx, u32 n, c
                 const u64 c = shoup_mul(reduce_acc(acc.fold<SH::S>(), dp->pr[L + K + k]), dp->bhat_inv[k],
                                         dp->bhat_inv_sh[k], b);
                 cb[k] = split<SH::S>(c);
-                fx_add(s2, c, dp->one_over_b[k]);
+                fx_add_small(s2, c, dp->one_over_b[k]);  // 1/b_k: integer part < 2^32
             }
             const u64 v = fx_round(s2);
             for (u32 i = 0; i < L; ++i) {

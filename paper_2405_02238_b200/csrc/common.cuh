@@ -270,6 +270,19 @@ HD void fx_add(Acc128& s, u64 y, const Frac& f) {
     s.hi += phi + (lo2 < lo1);
     s.lo = lo2;
 }
+// fx_add for a fraction whose integer part f.hi < 2^32 (1/q, 1/b: f.hi = 2^64/q):
+// y * f.hi from two 32x32 products instead of a full 64x64 one; same sum exactly
+HD void fx_add_small(Acc128& s, u64 y, const Frac& f) {
+    const u64 p0 = (u64)(u32)y * f.hi, p1 = (y >> 32) * f.hi;  // f.hi < 2^32
+    const u64 plo = p0 + (p1 << 32);
+    u64 phi = (p1 >> 32) + (plo < p0);
+    const u64 t = mulhi64(y, f.lo);
+    const u64 lo1 = plo + t;
+    phi += (lo1 < plo);
+    const u64 lo2 = s.lo + lo1;
+    s.hi += phi + (lo2 < lo1);
+    s.lo = lo2;
+}
 HD u64 fx_round(const Acc128& s) {
     // (s + 2^63) >> 64
     u64 lo = s.lo + (1ULL << 63);

@@ -238,6 +238,11 @@ HostParams make_params(int id, u64 seed) {
             d.phat_mod_q_sh[k][i] = shoup_of(d.phat_mod_q[k][i], q);
         }
     }
+    // fx_add_small: the reciprocals' integer parts fit 32 bits
+    for (unsigned i = 0; i < L; ++i)
+        if (d.one_over_q[i].hi >> 32) throw std::logic_error("1/q integer part above 2^32");
+    for (unsigned j = 0; j < nB; ++j)
+        if (d.one_over_b[j].hi >> 32) throw std::logic_error("1/b integer part above 2^32");
     // N^-1 folded into the first multiplier of each unscaled-INTT consumer
     auto with_ninv = [&](u64 c, unsigned r) { return mulmod(c, d.pr[r].ninv, h.primes[r]); };
     for (unsigned i = 0; i < L; ++i) {
