@@ -389,13 +389,13 @@ __device__ __forceinline__ void store_last_stage_io(const u64* sm, const St& st,
     }
 }
 
-template <int LB, int E, typename Ld2>
+template <int LB, int E, typename Ld2, int kLoadBatch = 8>
 __device__ __forceinline__ void load_first_stage_fn(u64* sm, const Ld2& ld2, const ulonglong2* __restrict__ tw_tab,
                                                     u64 q, int logN, int blk) {
     constexpr int NB = 1 << LB, T = NB / E;
     const int tw0 = (1 << (logN - 1)) + (blk << (LB - 1));
     // batches of kB pairs: all loads of a batch in flight before any use
-    constexpr int kIt = NB / 2 / T, kB = kIt < 8 ? kIt : 8;
+    constexpr int kIt = NB / 2 / T, kB = kIt < kLoadBatch ? kIt : kLoadBatch;
 #pragma unroll 1
     for (int i0 = 0; i0 < kIt; i0 += kB) {
         ulonglong2 v[kB];
@@ -419,11 +419,12 @@ __device__ __forceinline__ void load_first_stage_fn(u64* sm, const Ld2& ld2, con
 
 // Inverse: the first Gentleman-Sande stage (t = 1) fused into the coalesced load
 // (inputs canonical, or below 2q).
-template <int LB, int E = kElems>
+template <int LB, int E = kElems, int kLoadBatch = 8>
 __device__ __forceinline__ void load_first_stage(u64* sm, const u64* g, const ulonglong2* __restrict__ tw_tab, u64 q,
                                                  int logN, int blk) {
     const ulonglong2* g2 = reinterpret_cast<const ulonglong2*>(g);
-    load_first_stage_fn<LB, E>(sm, [g2](int i) { return __ldcs(g2 + i); }, tw_tab, q, logN, blk);
+    auto ld = [g2](int i) { return __ldcs(g2 + i); };
+    load_first_stage_fn<LB, E, decltype(ld), kLoadBatch>(sm, ld, tw_tab, q, logN, blk);
 }
 
 template <int LB, int E = kElems>
@@ -900,7 +901,7 @@ __global__ void __launch_bounds__((1 << LB) / E, MINB) k_ntt_inv3(DevCtx cx, Ntt
     u64* g = jv.ptr + ((size_t)blk << LB);
     const u64* src = jobs.src ? jobs.src[blockIdx.x] + ((size_t)blk << LB) : g;
     fill_tw_cache(cache, pairs(w + 2 * N), logN - LB, blk, kTwCache3);
-    load_first_stage<LB, E>(sm, src, pairs(w + 2 * N), q, logN, blk);
+    load_first_stage<LB, E, (MINB < 3 ? 16 : 8)>(sm, src, pairs(w + 2 * N), q, logN, blk);
     __syncthreads();
     inv_round<LB, 1, LB - 9, false, E>(sm, cache, pairs(w + 2 * N), q, logN, blk);
     __syncthreads();
@@ -1056,6 +1057,14 @@ void launch_inv_io(const DevCtx& cx, const DevParams& hp, const IO& io, u32 jobs
     }
 }
 
+bool ntt_inv2() {
+    static const bool on = [] {
+        const char* v = std::getenv("HGM_NTT_INV2");
+        return v && v[0] == '1';
+    }();
+    return on;
+}
+
 int ntt_elems() {
     static const int e = [] {
         const char* v = std::getenv("HGM_NTT_E");
@@ -1088,7 +1097,7 @@ template <int LB>
 void launch_block3(bool fwd, const DevCtx& cx, const NttJobs& jobs, int sub, cudaStream_t s) {
     if (ntt_elems() == 16)
         launch_block_e<LB, 16, 2>(fwd, cx, jobs, sub, s);
-    else if (ntt_elems() == 322)  // 2 CTAs/SM, 128 registers
+    else if (ntt_elems() == 322 || (!fwd && ntt_inv2()))  // 2 CTAs/SM, 128 registers
         launch_block_e<LB, kElems3, 2>(fwd, cx, jobs, sub, s);
     else
         launch_block_e<LB, kElems3, 3>(fwd, cx, jobs, sub, s);
