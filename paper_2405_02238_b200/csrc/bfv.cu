@@ -41,7 +41,14 @@ constexpr int kChunkEnc = 256, kChunkDec = 1024, kChunkLin = 8192, kChunkKs = 81
 // large batches fill the GPU (3 NTT CTAs per SM, >= 1 wave of limbs per launch)
 constexpr size_t kChunkBytes = (size_t)24 << 30;
 int chunk_for(size_t words_per_item, int cap) {
-    const size_t n = kChunkBytes / (words_per_item * 8);
+    // 24 GB, or a sixth of the device's memory on smaller parts (the stream-ordered
+    // pool keeps freed blocks, so "free" memory is not a useful bound here)
+    static const size_t budget = [] {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || total_b == 0) return kChunkBytes;
+        return std::min(kChunkBytes, total_b / 6);
+    }();
+    const size_t n = budget / (words_per_item * 8);
     return (int)std::max<size_t>(1, std::min<size_t>(n, (size_t)cap));
 }
 

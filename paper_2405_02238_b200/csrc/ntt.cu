@@ -2,6 +2,8 @@
 #include "ntt.cuh"
 
 #include <algorithm>
+#include <mutex>
+#include <utility>
 #include <cstdlib>
 #include <stdexcept>
 
@@ -12,6 +14,14 @@ namespace {
 __constant__ DevParams c_dp[kParamSets];
 
 __device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
+// Runs f once per (call site, device): the dynamic shared-memory opt-in is a
+// per-device function attribute.
+template <typename F>
+void once_per_device(std::once_flag (&flags)[64], F&& f) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::call_once(flags[dev & 63], std::forward<F>(f));
+}
 // pad() of a compile-time offset.  For base = (block << b) + o with b >= 4 and an
 // offset k * 2^s whose bits lie above o's (o < 2^s), pad(base + off) =
 // pad(base) + padc(off): one runtime pad per group, immediates for the rest.
@@ -684,20 +694,19 @@ struct FinishIO : ModDownIO {
 template <typename IO>
 void launch_fwd_io(const DevCtx& cx, const DevParams& hp, const IO& io, u32 jobs, cudaStream_t s) {
     if (jobs == 0) return;
-    static bool configured13 = false, configured12 = false;
     if (hp.logN == 13) {
         const size_t smem = (smem_words<13>() + 2 * kTwCache3) * sizeof(u64);
-        if (!configured13) {
+        static std::once_flag once13[64];
+        once_per_device(once13, [&] {
             cudaFuncSetAttribute(k_ntt_fwd_io<13, IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            configured13 = true;
-        }
+        });
         k_ntt_fwd_io<13, IO><<<jobs, (1 << 13) / kElems3, smem, s>>>(cx, io);
     } else {
         const size_t smem = (smem_words<12>() + 2 * kTwCache3) * sizeof(u64);
-        if (!configured12) {
+        static std::once_flag once12[64];
+        once_per_device(once12, [&] {
             cudaFuncSetAttribute(k_ntt_fwd_io<12, IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            configured12 = true;
-        }
+        });
         k_ntt_fwd_io<12, IO><<<jobs, (1 << 12) / kElems3, smem, s>>>(cx, io);
     }
 }
@@ -840,12 +849,11 @@ int sm_count() {
 template <int LB>
 void launch_block(bool fwd, const DevCtx& cx, const NttJobs& jobs, int sub, cudaStream_t s) {
     const size_t smem = (2 * smem_words<LB>() + 2 * kTwCache) * sizeof(u64);
-    static bool configured = false;
-    if (!configured) {
+    static std::once_flag once[64];
+    once_per_device(once, [&] {
         cudaFuncSetAttribute(k_ntt_fwd<LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_ntt_inv<LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    });
     const u32 items = jobs.count * (u32)sub;
     const u32 grid = std::min<u32>(items, (u32)sm_count());
     if (fwd)
@@ -1039,20 +1047,19 @@ struct TensorIO {
 template <typename IO>
 void launch_inv_io(const DevCtx& cx, const DevParams& hp, const IO& io, u32 jobs, cudaStream_t s) {
     if (jobs == 0) return;
-    static bool configured13 = false, configured12 = false;
     if (hp.logN == 13) {
         const size_t smem = (smem_words<13>() + 2 * kTwCache3) * sizeof(u64);
-        if (!configured13) {
+        static std::once_flag once13[64];
+        once_per_device(once13, [&] {
             cudaFuncSetAttribute(k_ntt_inv_io<13, IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            configured13 = true;
-        }
+        });
         k_ntt_inv_io<13, IO><<<jobs, (1 << 13) / kElems3, smem, s>>>(cx, io);
     } else {
         const size_t smem = (smem_words<12>() + 2 * kTwCache3) * sizeof(u64);
-        if (!configured12) {
+        static std::once_flag once12[64];
+        once_per_device(once12, [&] {
             cudaFuncSetAttribute(k_ntt_inv_io<12, IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            configured12 = true;
-        }
+        });
         k_ntt_inv_io<12, IO><<<jobs, (1 << 12) / kElems3, smem, s>>>(cx, io);
     }
 }
@@ -1077,12 +1084,11 @@ int ntt_elems() {
 template <int LB, int E, int MINB>
 void launch_block_e(bool fwd, const DevCtx& cx, const NttJobs& jobs, int sub, cudaStream_t s) {
     const size_t smem = (smem_words<LB>() + 2 * kTwCache3) * sizeof(u64);
-    static bool configured = false;
-    if (!configured) {
+    static std::once_flag once[64];
+    once_per_device(once, [&] {
         cudaFuncSetAttribute(k_ntt_fwd3<LB, E, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_ntt_inv3<LB, E, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    });
     const dim3 grid(jobs.count, sub);
     if (fwd)
         k_ntt_fwd3<LB, E, MINB><<<grid, (1 << LB) / E, smem, s>>>(cx, jobs);
