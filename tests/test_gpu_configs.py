@@ -84,3 +84,19 @@ def test_cfg5_row_block_sharding(gpu_factory):
     C = np.concatenate([parts[i] for i in range(8)])
     assert sha(C) == g["algos"]["enhanced"]["C_sha256"]
     assert [c for _, c in row_blocks(128, 8)] == [16] * 8
+
+
+@pytest.mark.parametrize("name,algo", [("cfg2", "basic"), ("cfg2", "enhanced"), ("cfg3", "basic"),
+                                       ("cfg5", "enhanced")])
+def test_noise_budget_margin(name, algo, gpu_factory, oracle_factory):
+    """The product ciphertexts keep a healthy invariant-noise budget (oracle's
+    SEAL-convention measure on the exported words), so the parameter sets carry
+    every config's multiplicative depth with room to spare."""
+    import paper_2405_02238_b200 as hb
+
+    m, l, n, lo, hi, pid, _, _ = CONFIGS[name]
+    A, B = splitmix_matrices(GOLD["seed"], 0, m, l, n, lo, hi)
+    C, words = gpu_factory(pid).matmul_batch(A, B, algo=hb.ALGOS[algo], export=True)
+    assert np.array_equal(C[0], (A @ B) % 65537)
+    budget = oracle_factory(pid).noise_budget(words[0])
+    assert budget > 20, f"{name} {algo}: only {budget:.1f} bits of noise budget left"
