@@ -78,3 +78,20 @@ def test_capacity_error_propagates(dropin):
     B = np.ones((64, 64), dtype=np.int64)
     with pytest.raises(RuntimeError, match="rc=2"):
         dropin(A, B, 0, 1)
+
+
+@pytest.mark.parametrize("algo,aid", [("basic", 0), ("enhanced", 1)])
+def test_reference_algorithms_cfg2_dropin(algo, aid, dropin, ref, gpu_factory):
+    """cfg2 (64^3) run op by op by the reference's own basic_mm / enhanced_mm
+    through the adapter: ~250 rotations, ~250 mask products and 64 CC-mults
+    recorded lazily and flushed at decrypt; products, per-phase counts and the
+    final ciphertext equal the batched library path."""
+    m, l, n, lo, hi, pid, _, _ = CONFIGS["cfg2"]
+    A, B = splitmix_matrices(20240404, 0, m, l, n, lo, hi)
+    g = gpu_factory(pid)
+    C, st, words = dropin(A, B, pid, aid, words=g.ct_words)
+    assert np.array_equal(C, (A @ B) % T)
+    Cref, st_ref = ref.mm(A, B, algo, slots=g.slot_count)
+    assert st[:12].astype(int).tolist() == st_ref[:12].astype(int).tolist()
+    _, wb = g.matmul_batch(A, B, algo=aid, counter0=0, export=True)
+    assert np.array_equal(words, wb[0])
