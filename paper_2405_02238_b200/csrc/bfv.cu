@@ -666,8 +666,8 @@ dim3 grid_of(u32 N, u32 n, u32 z = 1) {
 
 u64 mask_hash(const i64* m, size_t S) {
     u64 h = 0x243f6a8885a308d3ULL ^ S;
-    for (size_t i = 0; i < S; ++i) h = mix64(h ^ (u64)m[i]) + 0x9e3779b97f4a7c15ULL;
-    return h;
+    for (size_t i = 0; i < S; ++i) h = (h ^ (u64)m[i]) * 0x100000001b3ULL;  // collisions: content compared
+    return mix64(h);
 }
 
 }  // namespace
@@ -869,12 +869,20 @@ size_t Context::key_count() const {
     return keys_.size();
 }
 
-const u64* Context::mask_plain(const i64* mask, size_t S) {
+const u64* Context::mask_plain(const i64* mask, size_t S, u64 stable_id) {
+    if (stable_id) {
+        std::lock_guard<std::mutex> lk(mask_mu_);
+        auto it = masks_by_id_.find(stable_id);
+        if (it != masks_by_id_.end()) return it->second;
+    }
     const u64 h = mask_hash(mask, S);
     std::lock_guard<std::mutex> lk(mask_mu_);
     auto& bucket = masks_[h];
     for (auto& e : bucket)
-        if (e.content.size() == S && std::equal(e.content.begin(), e.content.end(), mask)) return e.dev;
+        if (e.content.size() == S && std::equal(e.content.begin(), e.content.end(), mask)) {
+            if (stable_id) masks_by_id_.emplace(stable_id, e.dev);
+            return e.dev;
+        }
     const u32 N = hp_.N, L = hp_.L;
     std::vector<u32> padded(N / 2, 0);
     for (size_t j = 0; j < S; ++j) padded[j] = to_slot_residue(mask[j]);
@@ -894,6 +902,7 @@ const u64* Context::mask_plain(const i64* mask, size_t S) {
     release(m);
     HGM_CUDA(cudaGetLastError());
     bucket.push_back(MaskEntry{std::vector<i64>(mask, mask + S), out});
+    if (stable_id) masks_by_id_.emplace(stable_id, out);
     return out;
 }
 

@@ -88,7 +88,7 @@ class Context {
 
     // ---------------------------------------------------------------- masks
     // NTT-domain centred lift of the batch-encoded mask over Q: [L][N].
-    const u64* mask_plain(const i64* mask, size_t S);
+    const u64* mask_plain(const i64* mask, size_t S, u64 stable_id = 0);
 
     // ---------------------------------------------------------------- primitives
     // host_vals[i] holds S[i] values; counters[i] is the encryption counter.
@@ -142,6 +142,7 @@ class Context {
         u64* dev;
     };
     std::unordered_map<u64, std::vector<MaskEntry>> masks_;
+    std::unordered_map<u64, const u64*> masks_by_id_;  // stable MaskData ids
 };
 
 }  // namespace hgm

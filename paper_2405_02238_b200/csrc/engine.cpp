@@ -176,7 +176,7 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
         if (!m) return nullptr;
         auto it = mask_dev.find(m.get());
         if (it != mask_dev.end()) return it->second;
-        const u64* d = ctx.mask_plain(m->v.data(), m->v.size());
+        const u64* d = ctx.mask_plain(m->v.data(), m->v.size(), m->stable ? m->id : 0);
         mask_dev.emplace(m.get(), d);
         return d;
     };

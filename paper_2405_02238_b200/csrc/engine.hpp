@@ -17,6 +17,7 @@
 //     one key read from HBM serves the whole group.
 #pragma once
 #include <functional>
+#include <atomic>
 #include <memory>
 #include <vector>
 
@@ -26,6 +27,14 @@ namespace hgm {
 
 struct MaskData {
     std::vector<i64> v;
+    // masks of cached (never freed) HEGMM programs are `stable`: the device copy is
+    // then found by id, without hashing the content (ids are never reused)
+    bool stable = false;
+    u64 id = next_id();
+    static u64 next_id() {
+        static std::atomic<u64> n{1};
+        return n.fetch_add(1, std::memory_order_relaxed);
+    }
 };
 using MaskRef = std::shared_ptr<const MaskData>;
 

@@ -80,6 +80,7 @@ std::shared_ptr<Plan> plan_from_pairs(const std::vector<std::pair<size_t, size_t
     plan->out_len = out_len;
     for (auto& kv : by) {
         auto md = std::make_shared<MaskData>();
+        md->stable = true;  // owned by a cached program
         md->v = std::move(kv.second);
         plan->entries.push_back(PlanEntry{kv.first, md});
     }
@@ -140,6 +141,7 @@ std::shared_ptr<Plan> embed(const Plan& p, size_t segment) {
     out->in_len = out->out_len = segment;
     for (const auto& e : p.entries) {
         auto md = std::make_shared<MaskData>();
+        md->stable = true;  // owned by a cached program
         md->v.assign(segment, 0);
         std::copy(e.mask->v.begin(), e.mask->v.end(), md->v.begin());
         out->entries.push_back(PlanEntry{e.offset, md});
@@ -339,6 +341,7 @@ void finalize(Strategy& s, size_t l) {
 // reference prefix_mask (algorithms.cpp:119-139)
 MaskRef prefix_mask(size_t kept, Dup dup, size_t p, size_t rows_w, size_t cols_w, Order o, size_t segment) {
     auto md = std::make_shared<MaskData>();
+        md->stable = true;  // owned by a cached program
     md->v.assign(segment, 0);
     for (size_t h = 0; h < kept; ++h) {
         if (dup == Dup::AVertical) {
