@@ -89,6 +89,19 @@ int hgm_apply_plan(hgm_ctx* ctx, const hgm_ct* x, size_t n, const int64_t* offse
 int hgm_flush(hgm_ctx* ctx);
 int hgm_ct_export(hgm_ctx* ctx, const hgm_ct* ct, uint64_t* words);
 int hgm_ct_import(hgm_ctx* ctx, const uint64_t* words, size_t S, size_t depth, hgm_ct** out);
+
+/* Ciphertext wire format (client <-> cloud transport; new): a 48-byte header
+ * { "HGMC", u32 version = 1, u64 key-set fingerprint (primes + key seed),
+ *   u32 N, u32 L, u32 segment, u32 depth, u32 phase, u32 reserved,
+ *   u64 FNV-1a checksum of the payload } followed by the 2*L*N residues
+ * (c0 limbs then c1 limbs, NTT domain, canonical), little endian.
+ * hgm_ct_serialize writes hgm_ct_wire_size() bytes; hgm_ct_deserialize
+ * rejects (HGM_EARG) a wrong magic/version/size, another parameter or key set,
+ * a checksum mismatch or a non-canonical residue, and S > slot_count
+ * (HGM_ECAP) as hgm_encrypt does. */
+size_t hgm_ct_wire_size(const hgm_ctx* ctx);
+int hgm_ct_serialize(hgm_ctx* ctx, const hgm_ct* ct, void* buf, size_t cap);
+int hgm_ct_deserialize(hgm_ctx* ctx, const void* buf, size_t len, hgm_ct** out);
 size_t hgm_ct_segment(const hgm_ct* ct);
 size_t hgm_ct_depth(const hgm_ct* ct);
 int hgm_ct_phase(const hgm_ct* ct);

@@ -24,6 +24,7 @@ EXPORTS = (
     "hgm_ctx_create", "hgm_ctx_destroy", "hgm_last_error", "hgm_ctx_info", "hgm_slot_count",
     "hgm_ct_words", "hgm_encrypt", "hgm_encrypt_at", "hgm_decrypt", "hgm_add", "hgm_mul",
     "hgm_cmul", "hgm_rot", "hgm_apply_plan", "hgm_flush", "hgm_ct_export", "hgm_ct_import",
+    "hgm_ct_wire_size", "hgm_ct_serialize", "hgm_ct_deserialize",
     "hgm_ct_segment", "hgm_ct_depth", "hgm_ct_phase", "hgm_ct_retain", "hgm_ct_release", "hgm_ct_set_pinned",
     "hgm_stats", "hgm_reset_stats", "hgm_peak_live", "hgm_set_phase", "hgm_phase",
     "hgm_matmul_batch", "hgm_matmul_batch_export", "hgm_bench_ntt", "hgm_device_sync",
@@ -163,6 +164,9 @@ def lib() -> ctypes.CDLL:
         "hgm_flush": (_int, [_vp]),
         "hgm_ct_export": (_int, [_vp, _vp, _vp]),
         "hgm_ct_import": (_int, [_vp, _vp, _sz, _sz, _vp]),
+        "hgm_ct_wire_size": (_sz, [_vp]),
+        "hgm_ct_serialize": (_int, [_vp, _vp, _vp, _sz]),
+        "hgm_ct_deserialize": (_int, [_vp, _vp, _sz, _vp]),
         "hgm_ct_segment": (_sz, [_vp]),
         "hgm_ct_depth": (_sz, [_vp]),
         "hgm_ct_phase": (_int, [_vp]),
@@ -346,6 +350,18 @@ class Context:
         w = np.ascontiguousarray(words, dtype=np.uint64)
         out = self._out()
         _check(lib().hgm_ct_import(self._h, _ptr(w), segment, depth, ctypes.byref(out)))
+        return Ciphertext(out.value, self)
+
+    def serialize(self, ct: Ciphertext) -> bytes:
+        """Wire format (header + residues, include/hegmm_b200.h) for transport."""
+        n = lib().hgm_ct_wire_size(self._h)
+        buf = ctypes.create_string_buffer(n)
+        _check(lib().hgm_ct_serialize(self._h, ct._h, buf, n))
+        return buf.raw
+
+    def deserialize(self, data: bytes) -> Ciphertext:
+        out = self._out()
+        _check(lib().hgm_ct_deserialize(self._h, data, len(data), ctypes.byref(out)))
         return Ciphertext(out.value, self)
 
     def matmul_batch(self, A: np.ndarray, B: np.ndarray, algo: int = 0, order: int = -1,

@@ -392,6 +392,79 @@ int hgm_ct_import(hgm_ctx* c, const uint64_t* words, size_t S, size_t depth, hgm
     });
 }
 
+namespace {
+struct WireHeader {
+    char magic[4];
+    uint32_t version;
+    uint64_t keyset;
+    uint32_t N, L, segment, depth, phase, reserved;
+    uint64_t checksum;
+};
+static_assert(sizeof(WireHeader) == 48, "wire header layout");
+uint64_t fnv1a(const void* p, size_t n, uint64_t h = 0xcbf29ce484222325ULL) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001b3ULL;
+    return h;
+}
+uint64_t keyset_fingerprint(const Context& ctx) {
+    const auto& hp = ctx.host();
+    uint64_t h = fnv1a(hp.primes.data(), hp.primes.size() * sizeof(u64));
+    return fnv1a(&hp.seed, sizeof(hp.seed), h);
+}
+}  // namespace
+
+size_t hgm_ct_wire_size(const hgm_ctx* c) { return sizeof(WireHeader) + c->ctx->ct_words() * 8; }
+
+int hgm_ct_serialize(hgm_ctx* c, const hgm_ct* ct, void* buf, size_t cap) {
+    return guarded([&] {
+        if (!ct || !buf) throw std::invalid_argument("null handle or buffer");
+        const size_t W = c->ctx->ct_words();
+        if (cap < sizeof(WireHeader) + W * 8) throw std::invalid_argument("buffer smaller than hgm_ct_wire_size()");
+        uint64_t* words = reinterpret_cast<uint64_t*>(static_cast<char*>(buf) + sizeof(WireHeader));
+        const int rc = hgm_ct_export(c, ct, words);
+        if (rc != HGM_OK) throw std::runtime_error(g_err);
+        WireHeader h{};
+        std::memcpy(h.magic, "HGMC", 4);
+        h.version = 1;
+        h.keyset = keyset_fingerprint(*c->ctx);
+        h.N = c->ctx->host().N;
+        h.L = c->ctx->host().L;
+        h.segment = (uint32_t)ct->node->S;
+        h.depth = (uint32_t)ct->node->depth;
+        h.phase = (uint32_t)ct->node->phase;
+        h.checksum = fnv1a(words, W * 8);
+        std::memcpy(buf, &h, sizeof(h));
+    });
+}
+
+int hgm_ct_deserialize(hgm_ctx* c, const void* buf, size_t len, hgm_ct** out) {
+    return guarded([&] {
+        if (!buf || !out) throw std::invalid_argument("null buffer or output");
+        const size_t W = c->ctx->ct_words();
+        if (len != sizeof(WireHeader) + W * 8) throw std::invalid_argument("wire size mismatch");
+        WireHeader h;
+        std::memcpy(&h, buf, sizeof(h));
+        if (std::memcmp(h.magic, "HGMC", 4) != 0 || h.version != 1) throw std::invalid_argument("not a v1 HGMC ciphertext");
+        if (h.keyset != keyset_fingerprint(*c->ctx) || h.N != c->ctx->host().N || h.L != c->ctx->host().L)
+            throw std::invalid_argument("ciphertext from another parameter or key set");
+        std::vector<uint64_t> words(W);
+        std::memcpy(words.data(), static_cast<const char*>(buf) + sizeof(WireHeader), W * 8);
+        if (fnv1a(words.data(), W * 8) != h.checksum) throw std::invalid_argument("ciphertext checksum mismatch");
+        const auto& hp = c->ctx->host();
+        for (size_t w = 0; w < W; ++w)
+            if (words[w] >= hp.primes[(w / hp.N) % hp.L]) throw std::invalid_argument("non-canonical residue");
+        if (h.segment == 0) throw hgm::DimensionError("empty ciphertext segment");
+        check_values(c, h.segment);  // CapacityError beyond slot_count, as hgm_encrypt
+        auto n = new_node(c, PNode::Input, h.segment, h.depth);
+        n->phase = (int)h.phase;
+        u64* p = c->ctx->alloc(W);
+        n->buf = std::make_shared<DevBuf>(c->ctx.get(), p);
+        HGM_CUDA(cudaMemcpyAsync(p, words.data(), W * 8, cudaMemcpyHostToDevice, c->ctx->stream()));
+        c->ctx->sync();
+        *out = make_handle(c, std::move(n));
+    });
+}
+
 size_t hgm_ct_segment(const hgm_ct* ct) { return ct->node->S; }
 size_t hgm_ct_depth(const hgm_ct* ct) { return ct->node->depth; }
 int hgm_ct_phase(const hgm_ct* ct) { return ct->node->phase; }

@@ -176,3 +176,28 @@ def test_peak_live_tracks_high_water(be):  # :214-226
     peak = be.peak_live_ciphertexts()
     be.encrypt(vec(1))
     assert be.peak_live_ciphertexts() == peak
+
+
+def test_wire_format_round_trip_and_validation(be, gpu_factory):
+    """hgm_ct_serialize / hgm_ct_deserialize: bit-identical round trip that keeps
+    segment, depth and phase; corrupted, truncated or foreign ciphertexts are
+    rejected."""
+    import paper_2405_02238_b200 as hb
+
+    x, y = be.encrypt(vec(1, 2, 3)), be.encrypt(vec(4, 5, 6))
+    prod = be.he_mult(x, y)
+    data = be.serialize(prod)
+    assert len(data) == 48 + 8 * be.ct_words and data[:4] == b"HGMC"
+    back = be.deserialize(data)
+    assert back.segment_length() == 3 and back.depth() == 1
+    assert np.array_equal(be.export(back), be.export(prod))
+    assert np.array_equal(be.decrypt(be.he_add(back, x)), vec(5, 12, 21))
+    bad = bytearray(data)
+    bad[100] ^= 1
+    with pytest.raises(hb.HEError):
+        be.deserialize(bytes(bad))
+    with pytest.raises(hb.HEError):
+        be.deserialize(data[:-8])
+    other = gpu_factory(0, seed=2)  # another key set
+    with pytest.raises(hb.HEError):
+        other.deserialize(data)
