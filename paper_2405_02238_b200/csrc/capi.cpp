@@ -60,7 +60,8 @@ struct SNode {
 
 struct hgm_ctx {
     std::unique_ptr<Context> ctx;
-    std::mutex mu;
+    std::mutex mu;                   // counters, encryption counter
+    std::recursive_mutex exec_mu;    // everything that touches the device (flush, batches, ring)
     std::atomic<int> phase{0};
     Counts counts;
     u64 enc_counter = 0;
@@ -265,6 +266,7 @@ int hgm_encrypt(hgm_ctx* c, const int64_t* values, size_t S, hgm_ct** out) {
 }
 
 int hgm_decrypt(hgm_ctx* c, const hgm_ct* ct, int64_t* out, size_t cap) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
     return guarded([&] {
         bump(c, kDec);
         const size_t S = node_of(ct).S;
@@ -272,8 +274,6 @@ int hgm_decrypt(hgm_ctx* c, const hgm_ct* ct, int64_t* out, size_t cap) {
         flush(c, {ct->node});
         const u64* p = ct->node->buf->p;
         c->ctx->decrypt(1, &p, &S, &out);
-        if (!ct->pinned || ct->node->pins.load() == 0) {
-        }
     });
 }
 
@@ -373,6 +373,7 @@ int hgm_flush(hgm_ctx* c) {
 }
 
 int hgm_ct_export(hgm_ctx* c, const hgm_ct* ct, uint64_t* words) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
     return guarded([&] {
         flush(c, {ct->node});
         c->ctx->sync();
@@ -381,6 +382,7 @@ int hgm_ct_export(hgm_ctx* c, const hgm_ct* ct, uint64_t* words) {
 }
 
 int hgm_ct_import(hgm_ctx* c, const uint64_t* words, size_t S, size_t depth, hgm_ct** out) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
     return guarded([&] {
         check_values(c, S);
         auto n = new_node(c, PNode::Input, S, depth);
@@ -416,6 +418,7 @@ uint64_t keyset_fingerprint(const Context& ctx) {
 size_t hgm_ct_wire_size(const hgm_ctx* c) { return sizeof(WireHeader) + c->ctx->ct_words() * 8; }
 
 int hgm_ct_serialize(hgm_ctx* c, const hgm_ct* ct, void* buf, size_t cap) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
     return guarded([&] {
         if (!ct || !buf) throw std::invalid_argument("null handle or buffer");
         const size_t W = c->ctx->ct_words();
@@ -438,6 +441,7 @@ int hgm_ct_serialize(hgm_ctx* c, const hgm_ct* ct, void* buf, size_t cap) {
 }
 
 int hgm_ct_deserialize(hgm_ctx* c, const void* buf, size_t len, hgm_ct** out) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
     return guarded([&] {
         if (!buf || !out) throw std::invalid_argument("null buffer or output");
         const size_t W = c->ctx->ct_words();
@@ -587,6 +591,7 @@ void put_counts(const MatmulProgram& prog, uint64_t* stats) {
 int matmul_batch_impl(hgm_ctx* c, int algo, int order, int flags, size_t m, size_t l, size_t n, size_t count,
                       const int64_t* A, const int64_t* B, int64_t* C, uint64_t counter0, uint64_t* stats,
                       uint64_t* final_words) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
     return guarded([&] {
         if (order < -1 || order > 1) throw std::invalid_argument("order must be -1, 0 or 1");
         Context& ctx = *c->ctx;
@@ -607,6 +612,7 @@ extern "C" {
 int hgm_blocked_mm(hgm_ctx* c, int algo, size_t m, size_t l, size_t n, const size_t* rows, size_t n_row,
                    const size_t* mids, size_t n_mid, const size_t* cols, size_t n_col, const int64_t* A,
                    const int64_t* B, int64_t* C, uint64_t counter0, int32_t* log) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
     return guarded([&] {
         if (algo < 0 || algo > 2) throw hgm::DimensionError("unknown algorithm id");
         // BlockPlan::validate (algorithms.cpp:412-432)
@@ -720,6 +726,7 @@ extern "C" {
 
 int hgm_batch_encrypt(hgm_ctx* c, int algo, int order, int flags, size_t m, size_t l, size_t n, size_t count,
                       const int64_t* A, const int64_t* B, uint64_t counter0, hgm_batch** out) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
     return guarded([&] {
         if (order < -1 || order > 1) throw std::invalid_argument("order must be -1, 0 or 1");
         Context& ctx = *c->ctx;
@@ -755,6 +762,7 @@ int hgm_batch_encrypt(hgm_ctx* c, int algo, int order, int flags, size_t m, size
 }
 
 int hgm_batch_cloud(hgm_ctx* c, hgm_batch* b, float* device_ms) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
     return guarded([&] {
         Context& ctx = *c->ctx;
         const MatmulProgram& prog = *b->prog;
@@ -792,6 +800,7 @@ uint64_t* hgm_batch_output(hgm_batch* b, size_t i) {
 }
 
 int hgm_batch_decrypt_words(hgm_ctx* c, const uint64_t* dev_words, size_t count, size_t S, int64_t* out) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
     return guarded([&] {
         Context& ctx = *c->ctx;
         if (S == 0 || S > ctx.slots()) throw hgm::DimensionError("bad segment");
@@ -812,6 +821,7 @@ int hgm_batch_decrypt_words(hgm_ctx* c, const uint64_t* dev_words, size_t count,
 }
 
 int hgm_batch_decrypt(hgm_ctx* c, hgm_batch* b, int64_t* C) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
     return guarded([&] {
         const MatmulProgram& prog = *b->prog;
         std::vector<i64> slots(b->count * prog.segment);
@@ -916,6 +926,7 @@ int hgm_matmul_batch_export(hgm_ctx* c, int algo, int order, int flags, size_t m
 }
 
 int hgm_bench_ntt(hgm_ctx* c, int forward, size_t limbs, int iters, float* ms) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
     return guarded([&] {
         Context& ctx = *c->ctx;
         const u32 N = ctx.host().N, L = ctx.host().L;
@@ -941,10 +952,12 @@ int hgm_bench_ntt(hgm_ctx* c, int forward, size_t limbs, int iters, float* ms) {
 }
 
 int hgm_device_sync(hgm_ctx* c) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
     return guarded([&] { c->ctx->sync(); });
 }
 
 int hgm_test_ntt(hgm_ctx* c, int forward, int prime, uint64_t* data, size_t count) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
     return guarded([&] {
         Context& ctx = *c->ctx;
         const u32 N = ctx.host().N;

@@ -201,3 +201,30 @@ def test_wire_format_round_trip_and_validation(be, gpu_factory):
     other = gpu_factory(0, seed=2)  # another key set
     with pytest.raises(hb.HEError):
         other.deserialize(data)
+
+
+def test_concurrent_flushes_on_one_backend(be):
+    """Several threads encrypting, rotating, multiplying and decrypting on one
+    backend at once: device work is serialised inside the library and every
+    thread gets its own correct result."""
+    S = be.slot_count
+    errs = []
+
+    def work(k):
+        try:
+            rng = np.random.default_rng(100 + k)
+            for _ in range(4):
+                v = rng.integers(0, 50, S).astype(np.int64)
+                w = rng.integers(0, 50, S).astype(np.int64)
+                x, y = be.encrypt(v), be.encrypt(w)
+                r = be.he_mult(be.he_rot(x, k + 1), y)
+                got = be.decrypt(r)
+                if not np.array_equal(got, (np.roll(v, -(k + 1)) * w) % T):
+                    errs.append(k)
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(repr(e))
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    [t.start() for t in ts]
+    [t.join() for t in ts]
+    assert not errs, errs
