@@ -468,7 +468,7 @@ __global__ void k_ks_finish(DevCtx cx, u32 n, const u64* const* acc, const u64* 
 // ---------------------------------------------------------------- tensoring
 // oracle q_to_b(): exact centred conversion of 4 polys per item, X: [n][4][L][N]
 template <typename SH>
-__global__ void __launch_bounds__(kThreads, 4) k_q_to_b(DevCtx cx, u32 n, const u64* X, u64* XB) {
+__global__ void __launch_bounds__(kThreads, 6) k_q_to_b(DevCtx cx, u32 n, const u64* X, u64* XB) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = SH::L, K = SH::K, nB = SH::nB;
     ITEM_LOOP {
@@ -538,7 +538,7 @@ template <typename SH>
 // Dg (optional, alpha = 1): component 2 is not stored in E but lifted straight
 // into the relinearisation digits [n][dnum][R][N] (k_modup_lift's output: digit
 // dg = limb dg, centred into every other limb).
-__global__ void __launch_bounds__(kThreads, 4) k_scale_round(DevCtx cx, u32 n, const u64* T, u64* E, u64* Dg) {
+__global__ void __launch_bounds__(kThreads, 6) k_scale_round(DevCtx cx, u32 n, const u64* T, u64* E, u64* Dg) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = SH::L, K = SH::K, nB = SH::nB, D = L + nB;
     ITEM_LOOP {
