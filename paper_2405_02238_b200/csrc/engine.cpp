@@ -228,19 +228,25 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
             std::vector<int> order(rot);
             std::stable_sort(order.begin(), order.end(),
                              [&](int a, int b) { return P.nodes[a].g < P.nodes[b].g; });
+            // items tiled over instances: within a tile of kRotTile instances the
+            // rotations run key by key, so the tile's ModUp digits stay in L2 while
+            // every Galois key streams past them once (instead of re-reading each
+            // instance's digits from HBM for every one of its rotations)
+            constexpr int kRotTile = 8;
             std::vector<const u64*> mu, cts;
             std::vector<u32> gs;
             std::vector<u64*> out;
-            for (int x : order) {
-                const int src = P.nodes[x].in[0];
-                const size_t si = std::lower_bound(srcs.begin(), srcs.end(), src) - srcs.begin();
-                for (int k = 0; k < K; ++k) {
-                    mu.push_back(mbuf + (si * K + k) * MW);
-                    cts.push_back(ptr(src, k));
-                    gs.push_back(P.nodes[x].g);
-                    out.push_back(base[x] + (size_t)k * W);
+            for (int k0 = 0; k0 < K; k0 += kRotTile)
+                for (int x : order) {
+                    const int src = P.nodes[x].in[0];
+                    const size_t si = std::lower_bound(srcs.begin(), srcs.end(), src) - srcs.begin();
+                    for (int k = k0; k < std::min(K, k0 + kRotTile); ++k) {
+                        mu.push_back(mbuf + (si * K + k) * MW);
+                        cts.push_back(ptr(src, k));
+                        gs.push_back(P.nodes[x].g);
+                        out.push_back(base[x] + (size_t)k * W);
+                    }
                 }
-            }
             ctx.rotate((int)mu.size(), mu.data(), cts.data(), gs.data(), out.data());
             g_counters.rot_items += mu.size();
             ctx.release(mbuf);
