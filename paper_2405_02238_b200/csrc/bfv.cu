@@ -345,7 +345,7 @@ __global__ void k_modup_lift(DevCtx cx, u32 n, const u64* C, size_t c_stride,
 // Items are grouped by Galois key (the engine sorts rotations by element): a
 // block serves up to kKeyReuse consecutive items and reads each key element
 // once for all items of the group that share it.
-constexpr int kKeyReuse = 4;
+constexpr int kKeyReuse = 8;
 template <typename SH>
 __global__ void k_ks_inner(DevCtx cx, u32 n, const u64* const* D,
                            const u64* const* key, const u32* g, u64* const* acc) {
