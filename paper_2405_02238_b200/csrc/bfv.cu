@@ -40,6 +40,15 @@ constexpr int kChunkEnc = 256, kChunkDec = 1024, kChunkLin = 8192, kChunkKs = 81
 // key-switch and multiplication batches are also capped by their temporaries:
 // large batches fill the GPU (3 NTT CTAs per SM, >= 1 wave of limbs per launch)
 constexpr size_t kChunkBytes = (size_t)24 << 30;
+// the tensor pass applies the INTT's first stage (HGM_TENSOR_S1=0 disables)
+bool tensor_first_stage() {
+    static const bool on = [] {
+        const char* e = std::getenv("HGM_TENSOR_S1");
+        return !e || e[0] != '0';
+    }();
+    return on;
+}
+
 int chunk_for(size_t words_per_item, int cap) {
     // 24 GB, or a sixth of the device's memory on smaller parts (the stream-ordered
     // pool keeps freed blocks, so "free" memory is not a useful bound here)
@@ -529,6 +538,65 @@ __global__ void k_tensor(DevCtx cx, u32 n, const u64* const* A,
             t0[j] = reduce_acc(s0.fold<SH::S>(), *P);
             t1[j] = reduce_acc(s1.fold<SH::S>(), *P);
             t2[j] = reduce_acc(s2.fold<SH::S>(), *P);
+        }
+    }
+}
+
+// k_tensor with the first Gentleman-Sande stage of the following INTT applied
+// to each output pair (2i, 2i+1): the same arithmetic load_first_stage does,
+// so the INTT (NttJobs::first_done) starts from plain loads.  One thread per
+// coefficient pair, 16-byte loads and stores.
+template <typename SH>
+__global__ void k_tensor_s1(DevCtx cx, u32 n, const u64* const* A, const u64* const* B, const u64* XB, u64* T) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
+    const u32 N = dp->N, L = SH::L, K = SH::K, nB = SH::nB, D = L + nB;
+    ITEM_LOOP {
+        const u32 d = blockIdx.z;
+        const u32 pi = d < L ? d : L + K + (d - L);
+        const ulonglong2 *a0, *a1, *b0, *b1;
+        if (d < L) {
+            a0 = reinterpret_cast<const ulonglong2*>(A[item] + (size_t)d * N);
+            a1 = reinterpret_cast<const ulonglong2*>(A[item] + (size_t)(L + d) * N);
+            b0 = reinterpret_cast<const ulonglong2*>(B[item] + (size_t)d * N);
+            b1 = reinterpret_cast<const ulonglong2*>(B[item] + (size_t)(L + d) * N);
+        } else {
+            const u64* base = XB + (size_t)item * 4 * nB * N + (size_t)(d - L) * N;
+            a0 = reinterpret_cast<const ulonglong2*>(base);
+            a1 = reinterpret_cast<const ulonglong2*>(base + (size_t)nB * N);
+            b0 = reinterpret_cast<const ulonglong2*>(base + (size_t)2 * nB * N);
+            b1 = reinterpret_cast<const ulonglong2*>(base + (size_t)3 * nB * N);
+        }
+        const Prime& P = dp->pr[pi];
+        const u64 q = P.q;
+        const ulonglong2* tw = reinterpret_cast<const ulonglong2*>(cx.tw + (size_t)pi * 4 * N + 2 * N) + (N >> 1);
+        ulonglong2* t0 = reinterpret_cast<ulonglong2*>(T + (((size_t)item * 3 + 0) * D + d) * N);
+        ulonglong2* t1 = reinterpret_cast<ulonglong2*>(T + (((size_t)item * 3 + 1) * D + d) * N);
+        ulonglong2* t2 = reinterpret_cast<ulonglong2*>(T + (((size_t)item * 3 + 2) * D + d) * N);
+        for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < N / 2; i += gridDim.x * blockDim.x) {
+            const ulonglong2 x0 = a0[i], x1 = a1[i], y0 = b0[i], y1 = b1[i];
+            const ulonglong2 w = __ldg(tw + i);
+            u64 r[3][2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const Dig<SH::S> p0 = split<SH::S>(e ? x0.y : x0.x), p1 = split<SH::S>(e ? x1.y : x1.x),
+                                 q0 = split<SH::S>(e ? y0.y : y0.x), q1 = split<SH::S>(e ? y1.y : y1.x);
+                Cols s0, s1, s2;
+                s0.mac(p0, q0);
+                s1.mac(p0, q1);
+                s1.mac(p1, q0);
+                s2.mac(p1, q1);
+                r[0][e] = reduce_acc(s0.fold<SH::S>(), P);
+                r[1][e] = reduce_acc(s1.fold<SH::S>(), P);
+                r[2][e] = reduce_acc(s2.fold<SH::S>(), P);
+            }
+            ulonglong2* outs[3] = {t0, t1, t2};
+#pragma unroll
+            for (int p = 0; p < 3; ++p) {
+                ulonglong2 v;
+                v.x = reduce_once(r[p][0] + r[p][1], q << 1);
+                v.y = shoup_lazy3(r[p][0] - r[p][1] + (q << 1), w.x, w.y, q);
+                outs[p][i] = v;
+            }
         }
     }
 }
@@ -1282,9 +1350,16 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
         ++launches_;
         release(XB);
     } else {
-        if (hp_.L == 3) k_tensor<ShapeQ3><<<grid_of(N, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T); else k_tensor<ShapeQ8><<<grid_of(N, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T); ++launches_;
+        const bool s1 = ntt_inverse_takes_first_stage(hp_.dev) && tensor_first_stage();
+        if (s1) {
+            if (hp_.L == 3) k_tensor_s1<ShapeQ3><<<grid_of(N / 2, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T); else k_tensor_s1<ShapeQ8><<<grid_of(N / 2, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T);
+        } else {
+            if (hp_.L == 3) k_tensor<ShapeQ3><<<grid_of(N, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T); else k_tensor<ShapeQ8><<<grid_of(N, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T);
+        }
+        ++launches_;
         release(XB);
         NttJobs tj = jobs_contig(T, n * 3 * D, 0, D);
+        tj.first_done = s1 ? 1 : 0;
         for (u32 k = 0; k < nB; ++k) tj.prime[L + k] = (unsigned char)(L + K + k);
         tj.unscaled = kLazyOut;  // k_scale_round: Shoup by dhat_inv_n; B limbs reduced, times T_n
         ntt(false, tj);

@@ -909,7 +909,10 @@ __global__ void __launch_bounds__((1 << LB) / E, MINB) k_ntt_inv3(DevCtx cx, Ntt
     u64* g = jv.ptr + ((size_t)blk << LB);
     const u64* src = jobs.src ? jobs.src[blockIdx.x] + ((size_t)blk << LB) : g;
     fill_tw_cache(cache, pairs(w + 2 * N), logN - LB, blk, kTwCache3);
-    load_first_stage<LB, E, (MINB < 3 ? 16 : 8)>(sm, src, pairs(w + 2 * N), q, logN, blk);
+    if (jobs.first_done)
+        load_block<LB, E>(sm, src);
+    else
+        load_first_stage<LB, E, (MINB < 3 ? 16 : 8)>(sm, src, pairs(w + 2 * N), q, logN, blk);
     __syncthreads();
     inv_round<LB, 1, LB - 9, false, E>(sm, cache, pairs(w + 2 * N), q, logN, blk);
     __syncthreads();
@@ -1195,6 +1198,8 @@ void ntt_tensor_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* c
         }
     }
 }
+
+bool ntt_inverse_takes_first_stage(const DevParams& hp) { return hp.logN == 13 && use_ntt3(); }
 
 void ntt_upload_params(int pid, const DevParams& p) {
     cudaMemcpyToSymbol(c_dp, &p, sizeof(DevParams), (size_t)pid * sizeof(DevParams));

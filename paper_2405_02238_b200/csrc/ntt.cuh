@@ -35,6 +35,9 @@ struct NttJobs {
     // (whole-limb transforms; for consumers whose Shoup product takes any
     // 64-bit input -- others get canonical output)
     u32 unscaled = 0;
+    // inverse only: the first Gentleman-Sande stage (t = 1) was applied by the
+    // producer (k_tensor); only honoured where ntt_inverse_takes_first_stage()
+    u32 first_done = 0;
     unsigned char prime[32] = {0};  // host-side pattern
     u64 packed[4] = {0, 0, 0, 0};   // the same pattern, packed for the kernel
     void pack() {
@@ -81,6 +84,8 @@ void ntt_tensor_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* c
 void ntt_upload_params(int pid, const DevParams& p);
 
 constexpr u32 kLazyOut = 2;
+// whether ntt_inverse honours NttJobs::first_done for this parameter set
+bool ntt_inverse_takes_first_stage(const DevParams& hp);
 
 inline NttJobs jobs_contig(u64* base, u32 count, u32 first_prime, u32 period) {
     NttJobs j;
