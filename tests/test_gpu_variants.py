@@ -21,6 +21,7 @@ VARIANTS = {
     "fused-modup": {"HGM_FUSED_KS": "u"},
     "unfused-conv-finish": {"HGM_FUSED_CONV": "0", "HGM_FUSED_FINISH": "0"},
     "fused-tensor": {"HGM_FUSED_TENSOR": "1"},
+    "tensor-without-intt-stage": {"HGM_TENSOR_S1": "0"},
 }
 
 
