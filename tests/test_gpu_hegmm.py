@@ -48,3 +48,23 @@ def test_batch_instances_match_single(gpu_factory, ref):
     C1, w1 = g.matmul_batch(A[2:3], B[2:3], algo=0, counter0=2 * 3, export=True)
     C5, w5 = g.matmul_batch(A, B, algo=0, counter0=0, export=True)
     assert np.array_equal(w1[0], w5[2]), "lockstep batching changed a ciphertext"
+
+
+def test_acceptance_exactness_sweep(gpu_factory):
+    """Acceptance criterion 1 (proj/tests/acceptance/acceptance_main.cpp:36-60):
+    500 random shapes in [1,16]^3, entries in [-9, 9]; basic_mm, enhanced_mm and
+    square_pad_mm on the B200 all equal the integer product (mod t = 65537,
+    which is exact here: |C| <= 16 * 81 < t / 2)."""
+    g = gpu_factory(0)
+    rng = np.random.default_rng(20240101)
+    failures = []
+    for trial in range(500):
+        m, l, n = (int(x) for x in rng.integers(1, 17, 3))
+        A = rng.integers(-9, 10, (m, l)).astype(np.int64)
+        B = rng.integers(-9, 10, (l, n)).astype(np.int64)
+        want = (A @ B) % T
+        for aid in (0, 1, 2):
+            C, _ = g.matmul_batch(A, B, algo=aid, counter0=3 * trial)
+            if not np.array_equal(C[0], want):
+                failures.append((m, l, n, aid))
+    assert not failures, failures[:5]
