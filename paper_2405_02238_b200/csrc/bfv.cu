@@ -36,7 +36,7 @@ struct ShapeQ8 {
     static constexpr int S = 28;  // 55-bit primes
 };
 // items per launch sequence: bounds temporaries and staging uploads
-constexpr int kChunkEnc = 256, kChunkDec = 1024, kChunkLin = 8192, kChunkKs = 8192, kChunkMult = 4096;
+constexpr int kChunkEnc = 1024, kChunkDec = 1024, kChunkLin = 8192, kChunkKs = 8192, kChunkMult = 4096;
 // key-switch and multiplication batches are also capped by their temporaries:
 // large batches fill the GPU (3 NTT CTAs per SM, >= 1 wave of limbs per launch)
 constexpr size_t kChunkBytes = (size_t)24 << 30;
