@@ -257,10 +257,10 @@ void build(orc_ctx& c, int id) {
     c.L = c.spec.L; c.K = c.spec.K; c.nB = c.spec.nB; c.dnum = c.spec.dnum;
     c.alpha = c.L / c.dnum;
     const unsigned N = c.N, L = c.L, K = c.K, nB = c.nB;
-    // primes: descending q = 2^bits - k*2N + 1
+    // primes: descending q = 2^bits - k*2^32 + 1 (= 1 mod 2^32, hence mod 2N)
     const unsigned need = L + K + nB;
     for (u64 k = 1; c.pr.size() < need; ++k) {
-        u64 cand = (1ULL << c.spec.qbits) - k * 2 * N + 1;
+        u64 cand = (1ULL << c.spec.qbits) - (k << 32) + 1;
         if (is_prime(cand)) { Prime p; p.q = cand; c.pr.push_back(p); }
     }
     for (auto& p : c.pr) make_tables(p, c.logN);

@@ -15,7 +15,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhegmm_b200.so")
+LIB_PATH = os.environ.get("HGM_LIB") or os.path.join(_HERE, "libhegmm_b200.so")
 
 HGM_OK, HGM_EDIM, HGM_ECAP, HGM_EINTERNAL, HGM_EOVERFLOW, HGM_ECUDA, HGM_EARG = range(7)
 PHASE_CLIENT, PHASE_CLOUD = 0, 1

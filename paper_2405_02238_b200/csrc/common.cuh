@@ -1,7 +1,7 @@
 // common.cuh -- integer arithmetic and the device-side parameter block.
 //
 // All ciphertext arithmetic is 64-bit RNS modular arithmetic over NTT-friendly
-// primes q < 2^62.  Fixed multiplicands (twiddles, base-conversion constants)
+// primes q = c 2^32 + 1 < 2^60.  Fixed multiplicands (twiddles, base-conversion constants)
 // use Shoup's precomputed quotient; products of two variables use a shifted
 // Barrett reduction.  Nothing here is floating point: the scale-and-round steps
 // use 128-bit fixed-point fractions (see Frac) so that every result is an exact
@@ -120,8 +120,23 @@ HD u64 add_mod(u64 a, u64 b, u64 q) {
 }
 HD u64 sub_mod(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }
 HD u64 neg_mod(u64 a, u64 q) { return a ? q - a : 0; }
+// Every ciphertext prime (Q, P and B) has the form q = c 2^32 + 1 (params.cpp),
+// so the low 64 bits of x q are x + (x_lo c) 2^32: one 32-bit IMAD instead of
+// an IMAD.WIDE and two IMADs.  Every quotient-times-q product of a Shoup or
+// Barrett reduction below goes through this; the plaintext modulus t = 65537 is
+// not of that form and never reaches these helpers (its transforms have their
+// own kernel, ntt.cu k_ntt_t).
+HD u64 mul_lo_q(u64 x, u64 q) {
+#ifdef __CUDA_ARCH__
+    u32 hi;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(hi) : "r"((u32)x), "r"((u32)(q >> 32)), "r"((u32)(x >> 32)));
+    return ((u64)hi << 32) | (u32)x;
+#else
+    return x * q;
+#endif
+}
 // Harvey's lazy Shoup product: a * w mod q in [0, 2q), any a < 2^64
-HD u64 shoup_lazy(u64 a, u64 w, u64 ws, u64 q) { return a * w - mulhi64(a, ws) * q; }
+HD u64 shoup_lazy(u64 a, u64 w, u64 ws, u64 q) { return a * w - mul_lo_q(mulhi64(a, ws), q); }
 // Shoup product whose quotient drops the a_lo*ws_lo partial product: the
 // quotient is low by at most 1, so the result lies in [0, 3q) for any a < 2^64.
 // On sm_100a the quotient is 2 IMAD.WIDE + 1 IMAD.HI instead of 4 IMAD.WIDE
@@ -146,7 +161,58 @@ HD u64 mulhi64_approx(u64 a, u64 b) {
     return a_hi * b_hi + (m1 >> 32) + (m2 >> 32) + (((m1 & 0xffffffffULL) + (m2 & 0xffffffffULL)) >> 32);
 #endif
 }
-HD u64 shoup_lazy3(u64 a, u64 w, u64 ws, u64 q) { return a * w - mulhi64_approx(a, ws) * q; }
+// a * w - qh * q (mod 2^64) for the special primes.  Code-generation variants
+// (same value; they differ in SASS and in register pressure inside the
+// unrolled NTT rounds): 0 generic 64-bit product, 1 qh*q hi word by mad.lo,
+// 2 plain C, 3 whole expression in PTX with mul.lo/mul.hi, 4 the same with
+// mul.wide (IMAD.WIDE + 3 IMAD).
+template <int V>
+HD u64 shoup_rem(u64 a, u64 w, u64 qh, u64 q) {
+#ifdef __CUDA_ARCH__
+    if constexpr (V == 0) {
+        return a * w - qh * q;
+    } else if constexpr (V == 1) {
+        return a * w - mul_lo_q(qh, q);
+    } else if constexpr (V == 2) {
+        return a * w - (qh + ((u64)((u32)qh * (u32)(q >> 32)) << 32));
+    } else if constexpr (V == 3) {
+        u32 r0, r1;
+        asm("{\n\t.reg .u32 t;\n\t"
+            "mul.lo.u32 %0, %2, %4;\n\t"
+            "mul.hi.u32 %1, %2, %4;\n\t"
+            "mad.lo.u32 %1, %2, %5, %1;\n\t"
+            "mad.lo.u32 %1, %3, %4, %1;\n\t"
+            "mad.lo.u32 t, %6, %8, %7;\n\t"
+            "sub.cc.u32 %0, %0, %6;\n\t"
+            "subc.u32 %1, %1, t;\n\t}"
+            : "=&r"(r0), "=&r"(r1)
+            : "r"((u32)a), "r"((u32)(a >> 32)), "r"((u32)w), "r"((u32)(w >> 32)), "r"((u32)qh),
+              "r"((u32)(qh >> 32)), "r"((u32)(q >> 32)));
+        return ((u64)r1 << 32) | r0;
+    } else {
+        u32 r0, r1;
+        asm("{\n\t.reg .u32 t;\n\t.reg .u64 p;\n\t"
+            "mul.wide.u32 p, %2, %4;\n\t"
+            "mov.b64 {%0, %1}, p;\n\t"
+            "mad.lo.u32 %1, %2, %5, %1;\n\t"
+            "mad.lo.u32 %1, %3, %4, %1;\n\t"
+            "mad.lo.u32 t, %6, %8, %7;\n\t"
+            "sub.cc.u32 %0, %0, %6;\n\t"
+            "subc.u32 %1, %1, t;\n\t}"
+            : "=&r"(r0), "=&r"(r1)
+            : "r"((u32)a), "r"((u32)(a >> 32)), "r"((u32)w), "r"((u32)(w >> 32)), "r"((u32)qh),
+              "r"((u32)(qh >> 32)), "r"((u32)(q >> 32)));
+        return ((u64)r1 << 32) | r0;
+    }
+#else
+    return a * w - qh * q;
+#endif
+}
+#ifndef HGM_SHOUP_V
+#define HGM_SHOUP_V 4
+#endif
+template <int V = HGM_SHOUP_V>
+HD u64 shoup_lazy3(u64 a, u64 w, u64 ws, u64 q) { return shoup_rem<V>(a, w, mulhi64_approx(a, ws), q); }
 // a * w mod q with ws = floor(w 2^64 / q); any a < 2^64, result in [0, q)
 HD u64 shoup_mul(u64 a, u64 w, u64 ws, u64 q) {
     u64 r = shoup_lazy3(a, w, ws, q);  // [0, 3q)
@@ -160,7 +226,7 @@ HD u64 mul_mod(u64 a, u64 b, const Prime& p) {
     const u64 lo = a * b, hi = mulhi64(a, b);
     const u64 x = (hi << (66 - p.s)) | (lo >> (p.s - 2));
     const u64 qh = mulhi64_approx(x, p.mu);  // low by at most 3: r < 4q
-    u64 r = lo - qh * p.q;
+    u64 r = lo - mul_lo_q(qh, p.q);
     if (r >= 2 * p.q) r -= 2 * p.q;
     if (r >= p.q) r -= p.q;
     return r;
@@ -185,7 +251,7 @@ struct Acc {
 HD u64 reduce_acc(const Acc& a, const Prime& p) {
     const u64 x = (a.hi << (66 - p.s)) | (a.lo >> (p.s - 2));
     const u64 qh = mulhi64_approx(x, p.mu);
-    u64 r = a.lo - qh * p.q;
+    u64 r = a.lo - mul_lo_q(qh, p.q);
     if (r >= 2 * p.q) r -= 2 * p.q;
     if (r >= p.q) r -= p.q;
     return r;

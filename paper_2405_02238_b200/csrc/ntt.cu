@@ -7,6 +7,14 @@
 #include <cstdlib>
 #include <stdexcept>
 
+// code-generation variant of the register-round butterflies (common.cuh shoup_rem)
+#ifndef HGM_SHOUP_FWD
+#define HGM_SHOUP_FWD HGM_SHOUP_V
+#endif
+#ifndef HGM_SHOUP_INV
+#define HGM_SHOUP_INV HGM_SHOUP_V
+#endif
+
 namespace hgm {
 
 namespace {
@@ -73,7 +81,7 @@ __device__ __forceinline__ void fwd_stage(u64 (&x)[1 << R], u64 q, u64 q4, u64 q
             // lazy butterfly: U < 12q, V = w x mod q in [0, 3q) (shoup_lazy3)
             const int k = c * 2 * h + u;
             const u64 U = kReduce ? reduce_once(x[k], q8) : x[k];
-            const u64 V = shoup_lazy3(x[k + h], w, ws, q);
+            const u64 V = shoup_lazy3<HGM_SHOUP_FWD>(x[k + h], w, ws, q);
             x[k] = U + V;
             x[k + h] = U - V + q4;
         }
@@ -184,7 +192,7 @@ __device__ __forceinline__ void inv_bf(u64 (&x)[1 << R], u64 q, u64 w, u64 ws) {
     constexpr GsAct a = GsPlanOf<R>::v.act[r][k];
     const u64 U = red_by<a.mU>(x[k], q), V = red_by<a.mV>(x[k + h], q);
     x[k] = red_by<a.mS>(U + V, q);
-    x[k + h] = shoup_lazy3(U - V + (q << ilog2c(a.off)), w, ws, q);
+    x[k + h] = shoup_lazy3<HGM_SHOUP_INV>(U - V + (q << ilog2c(a.off)), w, ws, q);
     if constexpr (u + 1 < h) inv_bf<R, r, c, u + 1, Tw>(x, q, w, ws);
 }
 template <int R, int r, int c, typename Tw>
@@ -1205,11 +1213,78 @@ void ntt_upload_params(int pid, const DevParams& p) {
     cudaMemcpyToSymbol(c_dp, &p, sizeof(DevParams), (size_t)pid * sizeof(DevParams));
 }
 
+namespace {
+// Transforms mod the plaintext modulus t = 65537 (encode's INTT and decode's
+// NTT: a few polynomials per product, client path).  t is not of the form
+// c 2^32 + 1 that the ciphertext kernels' reductions assume (common.cuh
+// mul_lo_q), so it has this plain kernel: one CTA per polynomial, residues as
+// u32 in shared memory, one radix-2 stage per barrier, products below 2^34
+// reduced by the compiler's constant-divisor sequence.  Same definition as the
+// ciphertext transforms (natural in / bit-reversed out, inverse scaled by N^-1),
+// canonical inputs and outputs.
+template <bool kFwd>
+__global__ void __launch_bounds__(1024) k_ntt_t(DevCtx cx, NttJobs jobs) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
+    extern __shared__ u32 st[];
+    const u32 N = dp->N, H = N / 2;
+    u64* g = jobs.ptrs ? jobs.ptrs[blockIdx.x] : jobs.base + (size_t)blockIdx.x * N;
+    const ulonglong2* tw = pairs(cx.tw + (size_t)kTIndex * 4 * N) + (kFwd ? 0 : N);
+    for (u32 i = threadIdx.x; i < N; i += blockDim.x) st[i] = (u32)g[i];
+    __syncthreads();
+    if constexpr (kFwd) {
+        for (u32 m = 1, lt = dp->logN - 1; m < N; m <<= 1, --lt) {
+            for (u32 b = threadIdx.x; b < H; b += blockDim.x) {
+                const u32 i = b >> lt, j = (i << (lt + 1)) + (b & ((1u << lt) - 1)), t = 1u << lt;
+                const u32 w = (u32)tw[m + i].x;
+                const u32 U = st[j], V = (u32)((u64)st[j + t] * w % kT);
+                st[j] = U + V >= (u32)kT ? U + V - (u32)kT : U + V;
+                st[j + t] = U >= V ? U - V : U + (u32)kT - V;
+            }
+            __syncthreads();
+        }
+    } else {
+        for (u32 m = H, lt = 0; m >= 1; m >>= 1, ++lt) {
+            for (u32 b = threadIdx.x; b < H; b += blockDim.x) {
+                const u32 i = b >> lt, j = (i << (lt + 1)) + (b & ((1u << lt) - 1)), t = 1u << lt;
+                const u32 w = (u32)tw[m + i].x;
+                const u32 U = st[j], V = st[j + t];
+                st[j] = U + V >= (u32)kT ? U + V - (u32)kT : U + V;
+                st[j + t] = (u32)((u64)(U >= V ? U - V : U + (u32)kT - V) * w % kT);
+            }
+            __syncthreads();
+        }
+    }
+    const u64 sc = kFwd ? 1 : dp->pr[kTIndex].ninv;
+    for (u32 i = threadIdx.x; i < N; i += blockDim.x) g[i] = kFwd ? st[i] : st[i] * sc % kT;
+}
+std::once_flag g_ntt_t_attr[2][64];
+// true if the batch is a transform mod t (all its jobs: t is never mixed with ciphertext primes)
+bool launch_t(bool fwd, const DevCtx& cx, const DevParams& hp, const NttJobs& jobs, cudaStream_t s) {
+    bool any = false, all = true;
+    for (u32 i = 0; i < jobs.period && i < 32; ++i) {
+        const bool t = jobs.prime[i] == kTIndex;
+        any |= t;
+        all &= t;
+    }
+    if (!any) return false;
+    if (!all || jobs.src || jobs.unscaled || jobs.first_done)
+        throw std::logic_error("a transform mod t must be a plain, in-place batch of t jobs only");
+    const int smem = (int)(hp.N * sizeof(u32));
+    auto k = fwd ? k_ntt_t<true> : k_ntt_t<false>;
+    once_per_device(g_ntt_t_attr[fwd], [&] {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
+    });
+    k<<<jobs.count, 1024, smem, s>>>(cx, jobs);
+    return true;
+}
+}  // namespace
+
 void ntt_forward(const DevCtx& cx, const DevParams& hp, const NttJobs& jobs_in, cudaStream_t s) {
     if (jobs_in.count == 0) return;
     if (jobs_in.src && hp.logN > 13) throw std::logic_error("out-of-place NTT needs whole-limb blocks");
     NttJobs jobs = jobs_in;
     jobs.pack();
+    if (launch_t(true, cx, hp, jobs, s)) return;
     if (hp.logN == 13 && use_ntt3()) {
         launch_block3<13>(true, cx, jobs, 1, s);
     } else if (hp.logN == 13) {
@@ -1230,6 +1305,7 @@ void ntt_inverse(const DevCtx& cx, const DevParams& hp, const NttJobs& jobs_in, 
     if (jobs_in.src && hp.logN > 13) throw std::logic_error("out-of-place NTT needs whole-limb blocks");
     NttJobs jobs = jobs_in;
     jobs.pack();
+    if (launch_t(false, cx, hp, jobs, s)) return;
     if (hp.logN == 13 && use_ntt3()) {
         launch_block3<13>(false, cx, jobs, 1, s);
     } else if (hp.logN == 13) {

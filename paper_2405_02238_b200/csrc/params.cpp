@@ -1,7 +1,9 @@
 // params.cpp -- prime selection, NTT tables and RNS conversion constants.
 //
 // Selection rules (shared, by specification, with oracle/bfv_oracle.cpp):
-//  * primes are taken in descending order q = 2^bits - k*2N + 1, k = 1, 2, ...
+//  * primes are taken in descending order q = 2^bits - k*2^32 + 1, k = 1, 2, ...
+//    (q = 1 mod 2^32: NTT-friendly for every N here, and q's low word is 1, so
+//    every quotient-times-q product on the device is one 32-bit IMAD);
 //    first L for Q, next K for P, next nB for the auxiliary base B;
 //  * psi = x^((q-1)/2N) for the smallest x >= 2 with psi^N = -1;
 //  * the NTT is negacyclic, natural order in, bit-reversed order out, so the
@@ -110,9 +112,12 @@ HostParams make_params(int id, u64 seed) {
     const unsigned N = h.N, L = h.L, K = h.K, nB = h.nB, R = h.R, A = h.alpha;
     const unsigned total = L + K + nB;
     for (u64 k = 1; h.primes.size() < total; ++k) {
-        const u64 c = (1ULL << h.spec.qbits) - k * 2 * N + 1;
+        const u64 c = (1ULL << h.spec.qbits) - (k << 32) + 1;  // = 1 mod 2^32, hence mod 2N
         if (is_prime(c)) h.primes.push_back(c);
     }
+    // the device reductions compute quotient * q as x + (x_lo c) 2^32 (common.cuh mul_lo_q)
+    for (u64 q : h.primes)
+        if ((u32)q != 1u) throw std::logic_error("ciphertext primes must be 1 mod 2^32");
     // the lazy NTT butterflies keep values below 16q and the column accumulator
     // splits residues into two digits of at most 30 bits: both need q < 2^60
     for (u64 q : h.primes)
