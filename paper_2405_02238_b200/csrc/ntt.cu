@@ -369,6 +369,33 @@ __device__ __forceinline__ JobView job_of(const NttJobs& jobs, u32 j, u32 N) {
     return v;
 }
 
+// io kernels: 2 (default) prefetches the transform input only, 1 also the store
+// epilogue's streams (measured -1%: 85 MB of prefetches in flight thrash L2), 0 none
+__constant__ int pf_mode = 2;
+// cp.async.bulk L2 prefetch of [p, p + bytes), 16 KB per thread of the calling warp
+__device__ __forceinline__ void pf_l2(const void* p, u32 bytes) {
+    for (u32 o = (threadIdx.x & 31) * 16384u; o < bytes; o += 32 * 16384u) {
+        const u32 n = bytes - o < 16384u ? bytes - o : 16384u;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const char*)p + o), "r"(n) : "memory");
+    }
+}
+
+// One wave ahead: the CTA of job x asks the copy engine (cp.async.bulk
+// prefetch, no registers or issue slots) to stage job x + ahead's block in L2,
+// so that the CTA taking this slot next finds its loads there instead of in HBM.
+template <int LB>
+__device__ __forceinline__ void l2_prefetch_ahead(const NttJobs& jobs, u32 N) {
+    constexpr u32 kParts = 4, kBytes = (8u << LB) / kParts;
+    if (threadIdx.x < kParts && jobs.ahead) {
+        const u32 nx = blockIdx.x + jobs.ahead;
+        if (nx < jobs.count) {
+            const u64* p = jobs.src ? jobs.src[nx] : job_of(jobs, nx, N).ptr;
+            p += ((size_t)blockIdx.y << LB) + (size_t)threadIdx.x * (kBytes / 8);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(kBytes) : "memory");
+        }
+    }
+}
+
 // Forward: the last Cooley-Tukey stage (t = 1, m = N/2) pairs adjacent
 // residues, i.e. exactly the 16-byte vector each thread stores, so it is
 // fused into the coalesced store together with the reduction to [0, q).
@@ -583,13 +610,14 @@ __global__ void __launch_bounds__((1 << LB) / kElems, 1)
 // whose canonical NTT-domain output is CONSUMED by io.store(job, i, v0, v1)
 // (elements 2i, 2i+1): base-conversion passes fused around the NTT.
 template <int LB, typename IO>
-__global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_fwd_io(DevCtx cx, IO io) {
+__global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_fwd_io(DevCtx cx, IO io, u32 ahead) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     extern __shared__ u64 sm[];
     u64* cache = sm + smem_words<LB>();
     const u32 N = dp->N;
     const int logN = (int)dp->logN;
     const u32 job = blockIdx.x;
+    if (ahead && threadIdx.x < 32 && job + ahead < gridDim.x) io.prefetch(job + ahead);
     const int prime = io.prime(job);
     const u64 q = dp->pr[prime].q;
     const u64* w = cx.tw + (size_t)prime * 4 * N;
@@ -623,6 +651,7 @@ struct ModUpIO {
     u64* D;            // [item][dnum][R][N]
     u32 R, dnum, L, A, N;
     __device__ int prime(u32 job) const { return (int)(job % R); }
+    __device__ void prefetch(u32) const {}
     __device__ u64 load(const DevParams* dp, u32 job, u32 j) const {
         const u32 item = job / (dnum * R), dg = (job / R) % dnum, r = job % R;
         const u64* c = C + item * c_stride;
@@ -657,6 +686,13 @@ struct ModDownIO {
     u64* const* out;         // per item [2][L][N]
     u32 L, K, R, N, logN;
     __device__ int prime(u32 job) const { return (int)(job % L); }
+    // the store's streams: acc's limb i and (c = 0) the addend's limb i
+    __device__ void prefetch_store(u32 job) const {
+        const u32 item = job / (2 * L), c = (job / L) & 1, i = job % L;
+        pf_l2(acc[item] + ((size_t)c * R + i) * N, N * 8);
+        if (c == 0 && addn) pf_l2(addn[item] + (size_t)i * N, N * 8);
+    }
+    __device__ void prefetch(u32 job) const { if (pf_mode == 1) prefetch_store(job); }
     __device__ u64 load(const DevParams* dp, u32 job, u32 j) const {
         const u32 item = job / (2 * L), c = (job / L) & 1, i = job % L;
         const u64* a = acc[item] + (size_t)c * R * N;
@@ -696,8 +732,29 @@ struct ModDownIO {
 // the contiguous [n][2][L][N] buffer; the store is ModDownIO's.
 struct FinishIO : ModDownIO {
     const u64* V;
+    __device__ void prefetch(u32 job) const {
+        pf_l2(V + (size_t)job * N, N * 8);
+        if (pf_mode == 1) prefetch_store(job);
+    }
     __device__ u64 load(const DevParams*, u32 job, u32 j) const { return __ldcs(V + (size_t)job * N + j); }
 };
+
+bool ntt_l2_prefetch();
+int sm_count();
+// resident CTAs of the 3-CTA/SM kernels: the one-wave-ahead distance
+u32 io_ahead() {
+    static const bool on = [] {
+        const char* v = std::getenv("HGM_NTT_PFIO");
+        return !(v && v[0] == '0');
+    }();
+    static std::once_flag once[64];
+    once_per_device(once, [] {
+        const char* v = std::getenv("HGM_NTT_PFIO");
+        const int m = v ? std::atoi(v) : 2;
+        cudaMemcpyToSymbol(pf_mode, &m, sizeof(int));
+    });
+    return on && ntt_l2_prefetch() ? (u32)(3 * sm_count()) : 0u;
+}
 
 template <typename IO>
 void launch_fwd_io(const DevCtx& cx, const DevParams& hp, const IO& io, u32 jobs, cudaStream_t s) {
@@ -708,14 +765,14 @@ void launch_fwd_io(const DevCtx& cx, const DevParams& hp, const IO& io, u32 jobs
         once_per_device(once13, [&] {
             cudaFuncSetAttribute(k_ntt_fwd_io<13, IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         });
-        k_ntt_fwd_io<13, IO><<<jobs, (1 << 13) / kElems3, smem, s>>>(cx, io);
+        k_ntt_fwd_io<13, IO><<<jobs, (1 << 13) / kElems3, smem, s>>>(cx, io, io_ahead());
     } else {
         const size_t smem = (smem_words<12>() + 2 * kTwCache3) * sizeof(u64);
         static std::once_flag once12[64];
         once_per_device(once12, [&] {
             cudaFuncSetAttribute(k_ntt_fwd_io<12, IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         });
-        k_ntt_fwd_io<12, IO><<<jobs, (1 << 12) / kElems3, smem, s>>>(cx, io);
+        k_ntt_fwd_io<12, IO><<<jobs, (1 << 12) / kElems3, smem, s>>>(cx, io, io_ahead());
     }
 }
 
@@ -890,6 +947,7 @@ __global__ void __launch_bounds__((1 << LB) / E, MINB) k_ntt_fwd3(DevCtx cx, Ntt
     const u64* w = cx.tw + (size_t)jv.prime * 4 * N;
     u64* g = jv.ptr + ((size_t)blk << LB);
     const u64* src = jobs.src ? jobs.src[blockIdx.x] + ((size_t)blk << LB) : g;
+    l2_prefetch_ahead<LB>(jobs, N);
     fill_tw_cache(cache, pairs(w), pre, blk, kTwCache3);
     __syncthreads();
     auto ld = [src](int j) { return __ldcs(src + j); };
@@ -916,6 +974,7 @@ __global__ void __launch_bounds__((1 << LB) / E, MINB) k_ntt_inv3(DevCtx cx, Ntt
     const u64* w = cx.tw + (size_t)jv.prime * 4 * N;
     u64* g = jv.ptr + ((size_t)blk << LB);
     const u64* src = jobs.src ? jobs.src[blockIdx.x] + ((size_t)blk << LB) : g;
+    l2_prefetch_ahead<LB>(jobs, N);
     fill_tw_cache(cache, pairs(w + 2 * N), logN - LB, blk, kTwCache3);
     if (jobs.first_done)
         load_block<LB, E>(sm, src);
@@ -941,7 +1000,7 @@ __global__ void __launch_bounds__((1 << LB) / E, MINB) k_ntt_inv3(DevCtx cx, Ntt
 // (N * INTT) output, in [0, 4q), is consumed by io.store(job, i, v0, v1)
 // (elements 2i, 2i+1): a base conversion fused behind the INTT.
 template <int LB, typename IO>
-__global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_inv_io(DevCtx cx, IO io) {
+__global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_inv_io(DevCtx cx, IO io, u32 ahead) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     extern __shared__ u64 sm[];
     u64* cache = sm + smem_words<LB>();
@@ -949,6 +1008,7 @@ __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_inv_io(DevCtx cx
     const u32 N = dp->N;
     const int logN = (int)dp->logN;
     const u32 job = blockIdx.x;
+    if (ahead && threadIdx.x < 32 && job + ahead < gridDim.x) io.prefetch(job + ahead);
     const int prime = io.prime(job);
     const u64 q = dp->pr[prime].q;
     const u64* w = cx.tw + (size_t)prime * 4 * N;
@@ -978,6 +1038,10 @@ struct MdConvIO {
     u64* V;                    // [n][2][L][N]
     u32 L, R, N;
     __device__ int prime(u32) const { return (int)L; }
+    __device__ void prefetch(u32 job) const {
+        pf_l2(acc[job >> 1] + ((size_t)(job & 1) * R + L) * N, N * 8);
+        if (ecoef && pf_mode == 1) pf_l2(ecoef[job >> 1] + (size_t)(job & 1) * L * N, L * N * 8);
+    }
     __device__ ulonglong2 load2(const DevParams*, u32 job, u32 i) const {
         return __ldcs(reinterpret_cast<const ulonglong2*>(acc[job >> 1] + ((size_t)(job & 1) * R + L) * N) + i);
     }
@@ -1012,6 +1076,7 @@ struct TensorIO {
     const u64* XB;  // [n][4][nB][N]: a.c0, a.c1, b.c0, b.c1 over B
     u64* T;         // [n][3][D][N]
     u32 L, K, nB, D, N;
+    __device__ void prefetch(u32) const {}
     __device__ int prime(u32 job) const {
         const u32 d = job % D;
         return (int)(d < L ? d : L + K + (d - L));
@@ -1064,14 +1129,14 @@ void launch_inv_io(const DevCtx& cx, const DevParams& hp, const IO& io, u32 jobs
         once_per_device(once13, [&] {
             cudaFuncSetAttribute(k_ntt_inv_io<13, IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         });
-        k_ntt_inv_io<13, IO><<<jobs, (1 << 13) / kElems3, smem, s>>>(cx, io);
+        k_ntt_inv_io<13, IO><<<jobs, (1 << 13) / kElems3, smem, s>>>(cx, io, io_ahead());
     } else {
         const size_t smem = (smem_words<12>() + 2 * kTwCache3) * sizeof(u64);
         static std::once_flag once12[64];
         once_per_device(once12, [&] {
             cudaFuncSetAttribute(k_ntt_inv_io<12, IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         });
-        k_ntt_inv_io<12, IO><<<jobs, (1 << 12) / kElems3, smem, s>>>(cx, io);
+        k_ntt_inv_io<12, IO><<<jobs, (1 << 12) / kElems3, smem, s>>>(cx, io, io_ahead());
     }
 }
 
@@ -1092,6 +1157,15 @@ int ntt_elems() {
     return e;
 }
 
+// L2 prefetch one wave ahead in the block kernels (HGM_NTT_PF=0 disables)
+bool ntt_l2_prefetch() {
+    static const bool on = [] {
+        const char* v = std::getenv("HGM_NTT_PF");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
 template <int LB, int E, int MINB>
 void launch_block_e(bool fwd, const DevCtx& cx, const NttJobs& jobs, int sub, cudaStream_t s) {
     const size_t smem = (smem_words<LB>() + 2 * kTwCache3) * sizeof(u64);
@@ -1101,10 +1175,12 @@ void launch_block_e(bool fwd, const DevCtx& cx, const NttJobs& jobs, int sub, cu
         cudaFuncSetAttribute(k_ntt_inv3<LB, E, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     });
     const dim3 grid(jobs.count, sub);
+    NttJobs j = jobs;
+    if (ntt_l2_prefetch()) j.ahead = (u32)(sm_count() * MINB);
     if (fwd)
-        k_ntt_fwd3<LB, E, MINB><<<grid, (1 << LB) / E, smem, s>>>(cx, jobs);
+        k_ntt_fwd3<LB, E, MINB><<<grid, (1 << LB) / E, smem, s>>>(cx, j);
     else
-        k_ntt_inv3<LB, E, MINB><<<grid, (1 << LB) / E, smem, s>>>(cx, jobs);
+        k_ntt_inv3<LB, E, MINB><<<grid, (1 << LB) / E, smem, s>>>(cx, j);
 }
 
 // shared-memory resident block kernels: 256 threads x 32 residues, 3 CTAs/SM

@@ -38,6 +38,9 @@ struct NttJobs {
     // inverse only: the first Gentleman-Sande stage (t = 1) was applied by the
     // producer (k_tensor); only honoured where ntt_inverse_takes_first_stage()
     u32 first_done = 0;
+    // set by the launcher: CTA x also prefetches job x + ahead's block into L2
+    // (the CTA that will take its slot one wave later); 0 = off
+    u32 ahead = 0;
     unsigned char prime[32] = {0};  // host-side pattern
     u64 packed[4] = {0, 0, 0, 0};   // the same pattern, packed for the kernel
     void pack() {
