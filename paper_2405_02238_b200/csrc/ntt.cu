@@ -228,7 +228,8 @@ struct NoLoad {
 template <int LB, int S0, int R, bool kCached, bool kFromGlobal = false, typename Ld = NoLoad, int E = kElems>
 __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_cache,
                                           const ulonglong2* __restrict__ tw_tab,
-                                          u64 q, int pre, int blk, const Ld& ld = Ld()) {
+                                          u64 q, int pre, int blk, const Ld& ld = Ld(),
+                                          const u64* x0 = nullptr) {
     constexpr int NB = 1 << LB, T = NB / E, G = (NB >> R) / T;
     constexpr int LT_FIRST = LB - 1 - S0, LT_MIN = LT_FIRST - (R - 1);
     const u64 q4 = q << 2, q8 = q << 3;  // lazy bounds (fwd_stage)
@@ -245,7 +246,7 @@ __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_ca
         if constexpr (kCached) {
             if constexpr (kFromGlobal) {
 #pragma unroll
-                for (int k = 0; k < (1 << R); ++k) x[k] = ld(base + (k << LT_MIN));
+                for (int k = 0; k < (1 << R); ++k) x[k] = (x0 && gg == 0) ? x0[k] : ld(base + (k << LT_MIN));
             } else {
 #pragma unroll
                 for (int k = 0; k < (1 << R); ++k) x[k] = sm[at(k)];
@@ -348,6 +349,22 @@ __device__ __forceinline__ void fill_tw_cache(u64* cache, const ulonglong2* __re
         cache[2 * i + 1] = t.y;
     }
 }
+
+// The same fill through cp.async (16-byte copies that bypass the registers): the
+// issuing thread does not wait for the twiddles, so the block's own loads go
+// out behind them.  Visible to the CTA after cp_async_wait_all + barrier.
+__device__ __forceinline__ void fill_tw_cache_async(u64* cache, const ulonglong2* __restrict__ tw_tab, int outer,
+                                                    int blk, int count) {
+    for (int i = threadIdx.x; i < count; i += blockDim.x) {
+        const int s = 31 - __clz(i + 1);
+        const int c = i + 1 - (1 << s);
+        const int g = (1 << (outer + s)) + (blk << s) + c;
+        const unsigned d = (unsigned)__cvta_generic_to_shared(cache + 2 * i);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(tw_tab + g));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 struct JobView {
     u64* ptr;
@@ -948,10 +965,16 @@ __global__ void __launch_bounds__((1 << LB) / E, MINB) k_ntt_fwd3(DevCtx cx, Ntt
     u64* g = jv.ptr + ((size_t)blk << LB);
     const u64* src = jobs.src ? jobs.src[blockIdx.x] + ((size_t)blk << LB) : g;
     l2_prefetch_ahead<LB>(jobs, N);
-    fill_tw_cache(cache, pairs(w), pre, blk, kTwCache3);
-    __syncthreads();
     auto ld = [src](int j) { return __ldcs(src + j); };
-    fwd_round<LB, 0, 4, true, true, decltype(ld), E>(sm, cache, pairs(w), q, pre, blk, ld);
+    // group 0 of the first round is loaded while the twiddle cache fills
+    static_assert((1 << LB) / E <= (1 << (LB - 4)), "first-round group 0 is base = threadIdx.x");
+    u64 x0[16];
+    fill_tw_cache_async(cache, pairs(w), pre, blk, kTwCache3);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x0[k] = ld((int)threadIdx.x + (k << (LB - 4)));
+    cp_async_wait_all();
+    __syncthreads();
+    fwd_round<LB, 0, 4, true, true, decltype(ld), E>(sm, cache, pairs(w), q, pre, blk, ld, x0);
     __syncthreads();
     fwd_round<LB, 4, 4, true, false, NoLoad, E>(sm, cache, pairs(w), q, pre, blk);
     __syncthreads();
@@ -975,11 +998,12 @@ __global__ void __launch_bounds__((1 << LB) / E, MINB) k_ntt_inv3(DevCtx cx, Ntt
     u64* g = jv.ptr + ((size_t)blk << LB);
     const u64* src = jobs.src ? jobs.src[blockIdx.x] + ((size_t)blk << LB) : g;
     l2_prefetch_ahead<LB>(jobs, N);
-    fill_tw_cache(cache, pairs(w + 2 * N), logN - LB, blk, kTwCache3);
+    fill_tw_cache_async(cache, pairs(w + 2 * N), logN - LB, blk, kTwCache3);
     if (jobs.first_done)
         load_block<LB, E>(sm, src);
     else
         load_first_stage<LB, E, (MINB < 3 ? 16 : 8)>(sm, src, pairs(w + 2 * N), q, logN, blk);
+    cp_async_wait_all();
     __syncthreads();
     inv_round<LB, 1, LB - 9, false, E>(sm, cache, pairs(w + 2 * N), q, logN, blk);
     __syncthreads();
@@ -1012,8 +1036,9 @@ __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_inv_io(DevCtx cx
     const int prime = io.prime(job);
     const u64 q = dp->pr[prime].q;
     const u64* w = cx.tw + (size_t)prime * 4 * N;
-    fill_tw_cache(cache, pairs(w + 2 * N), 0, 0, kTwCache3);
+    fill_tw_cache_async(cache, pairs(w + 2 * N), 0, 0, kTwCache3);
     load_first_stage_fn<LB, kElems3>(sm, [&](int i) { return io.load2(dp, job, (u32)i); }, pairs(w + 2 * N), q, logN, 0);
+    cp_async_wait_all();
     __syncthreads();
     inv_round<LB, 1, LB - 9, false, kElems3>(sm, cache, pairs(w + 2 * N), q, logN, 0);
     __syncthreads();
