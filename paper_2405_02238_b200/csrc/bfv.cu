@@ -218,8 +218,14 @@ __global__ void k_copy(u32 n, size_t W, const u64* const* in, u64* const* out) {
 // out[o] = sum_t in[t] (.* mask[t]) : oracle cmult() followed by add()
 // Masks are stored in packed digit form (mask_digits: l | h << 32).  Each
 // thread takes two adjacent words (16-byte loads) of one limb.
+#ifndef HGM_LC_U
+#define HGM_LC_U 2
+#endif
+#ifndef HGM_LC_MINB
+#define HGM_LC_MINB 4
+#endif
 template <typename SH>
-__global__ void k_lincomb(DevCtx cx, u32 n, const u32* off,
+__global__ void __launch_bounds__(kThreads, HGM_LC_MINB) k_lincomb(DevCtx cx, u32 n, const u32* off,
                           const u64* const* in, const u64* const* mask, u64* const* out) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, logN = dp->logN, L = SH::L;
@@ -231,27 +237,45 @@ __global__ void k_lincomb(DevCtx cx, u32 n, const u32* off,
             const size_t wl2 = w2 < LN / 2 ? w2 : w2 - LN / 2;  // pair index within the component
             const Prime& P = dp->pr[(wl2 * 2) >> logN];
             // exact accumulation; reduced after every 3 masked products
-            // (the sum stays below 2^(s+62), reduce_acc's range)
+            // (the sum stays below 2^(s+62), reduce_acc's range).  Terms are
+            // taken kU at a time with all their loads issued first, so a
+            // long plain sum (an add tree of 64 products) is not a chain of
+            // dependent load latencies.
             Cols a0, a1;
             u32 pending = 0;
-            for (u32 t = t0; t < t1; ++t) {
-                const ulonglong2 v = reinterpret_cast<const ulonglong2*>(in[t])[w2];
-                const u64* mt = mask[t];
-                if (mt) {
-                    const ulonglong2 m = __ldg(reinterpret_cast<const ulonglong2*>(mt) + wl2);
-                    a0.mac(split<SH::S>(v.x), packed_dig<SH::S>(m.x));
-                    a1.mac(split<SH::S>(v.y), packed_dig<SH::S>(m.y));
-                    if (++pending == 3) {
-                        const u64 r0 = reduce_acc(a0.fold<SH::S>(), P), r1 = reduce_acc(a1.fold<SH::S>(), P);
-                        a0 = Cols{};
-                        a1 = Cols{};
-                        a0.x = r0;
-                        a1.x = r1;
-                        pending = 0;
+            constexpr u32 kU = HGM_LC_U;
+            for (u32 t = t0; t < t1; t += kU) {
+                const u32 nt = t1 - t < kU ? t1 - t : kU;
+                ulonglong2 v[kU], m[kU];
+                bool hm[kU];
+#pragma unroll
+                for (u32 u = 0; u < kU; ++u) {
+                    hm[u] = false;
+                    if (u < nt) {
+                        const u64* mt = mask[t + u];
+                        hm[u] = mt != nullptr;
+                        v[u] = reinterpret_cast<const ulonglong2*>(in[t + u])[w2];
+                        if (mt) m[u] = __ldg(reinterpret_cast<const ulonglong2*>(mt) + wl2);
                     }
-                } else {
-                    a0.add<SH::S>(v.x);
-                    a1.add<SH::S>(v.y);
+                }
+#pragma unroll
+                for (u32 u = 0; u < kU; ++u) {
+                    if (u >= nt) break;
+                    if (hm[u]) {
+                        a0.mac(split<SH::S>(v[u].x), packed_dig<SH::S>(m[u].x));
+                        a1.mac(split<SH::S>(v[u].y), packed_dig<SH::S>(m[u].y));
+                        if (++pending == 3) {
+                            const u64 r0 = reduce_acc(a0.fold<SH::S>(), P), r1 = reduce_acc(a1.fold<SH::S>(), P);
+                            a0 = Cols{};
+                            a1 = Cols{};
+                            a0.x = r0;
+                            a1.x = r1;
+                            pending = 0;
+                        }
+                    } else {
+                        a0.add<SH::S>(v[u].x);
+                        a1.add<SH::S>(v[u].y);
+                    }
                 }
             }
             ulonglong2 r;
