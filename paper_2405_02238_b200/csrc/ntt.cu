@@ -1077,13 +1077,19 @@ struct MdConvIO {
         const u64 z1 = shoup_mul(v1, dp->phat_inv_n[0], dp->phat_inv_n_sh[0], p);
         const u64* ec = ecoef ? ecoef[item] + (size_t)c * L * N : nullptr;
         u64* out = V + ((size_t)item * 2 + c) * L * N;
+        // K = 1, so P = p: P^-1 centred(z) = P^-1 z - [z > (p-1)/2] (mod q_i), and
+        // V = e - P^-1 centred(z) = e + 3q - lazy(P^-1 z) + [z > (p-1)/2], which lies
+        // in [0, 4q) (the lazy product is never 0 for 0 < z < q_i) -- the same
+        // canonical residue as reducing the centred lift first.
+        const u64 h0 = z0 > (p - 1) / 2, h1 = z1 > (p - 1) / 2;
         for (u32 i = 0; i < L; ++i) {
             const u64 q = dp->pr[i].q, pi = dp->P_inv_q[i], pis = dp->P_inv_q_sh[i];
+            const u64 q2 = q << 1, q3 = 3 * q;
             ulonglong2 b{0, 0};
             if (ec) b = __ldcs(reinterpret_cast<const ulonglong2*>(ec + (size_t)i * N) + i2);
             ulonglong2 v;
-            v.x = sub_mod(b.x, shoup_mul(centred_lift_n(z0, p, q), pi, pis, q), q);
-            v.y = sub_mod(b.y, shoup_mul(centred_lift_n(z1, p, q), pi, pis, q), q);
+            v.x = reduce_once(reduce_once(b.x + h0 + q3 - shoup_lazy3(z0, pi, pis, q), q2), q);
+            v.y = reduce_once(reduce_once(b.y + h1 + q3 - shoup_lazy3(z1, pi, pis, q), q2), q);
             reinterpret_cast<ulonglong2*>(out + (size_t)i * N)[i2] = v;
         }
     }
