@@ -1,5 +1,5 @@
-# Copies the evidence gathered by tools/prof_all.sh + tools/prof_metrics.sh (run
-# under gpurun) from gpurun_out/ into profiles/ (run here, after the call).
+# Copies the evidence gathered by tools/collect_round.sh (run under gpurun) from
+# gpurun_out/ into profiles/ (run here, after the call).
 set -e
 python tools/ncu_summary.py gpurun_out/ntt_full.ncu-rep profiles/r01_ntt_fwd_ncu_full.json 1184 profiles/ntt_traffic.json > /dev/null
 python - <<'PY'
@@ -8,6 +8,9 @@ l = json.load(open('gpurun_out/bench.json'))
 l['roofline']['traffic'] = json.load(open('profiles/ntt_traffic.json'))['bytes_per_limb'] * 1184
 json.dump(l, open('profiles/r01_bench.json', 'w'))
 PY
+cp gpurun_out/bench_ref.json profiles/bench_r01_reference_arm.json
+cp gpurun_out/bench_launches.csv profiles/r01_bench_launches.csv
+python tools/launch_shares.py gpurun_out/bench_launches.csv > profiles/r01_bench_launches_shares.txt
 cp gpurun_out/launches.csv profiles/r01_cloud_step_launches.csv
 python tools/launch_shares.py gpurun_out/launches.csv > profiles/r01_cloud_step_shares.txt
 python tools/metrics_table.py > profiles/r01_cloud_step_metrics.txt
