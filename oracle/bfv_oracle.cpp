@@ -7,7 +7,9 @@
 //   decrypt  : proj/src/backend.cpp:136-139 (returns the S logical slots,
 //              canonical in [0, t) as SlotBackend{N/2, 65537} does)
 //   he_add   : proj/src/backend.cpp:141-153
-//   he_mult  : proj/src/backend.cpp:155-167
+//   he_mult  : proj/src/backend.cpp:155-167 (a PENDING product: the tensor is
+//              scaled, rounded and relinearised when a non-add op reads it,
+//              so he_add chains of products round once -- see XCt below)
 //   he_cmult : proj/src/backend.cpp:169-183 (mask length == segment)
 //   he_rot   : proj/src/backend.cpp:185-197 (left rotation; BFV rotates the
 //              whole N/2-slot row, see backend.hpp:129-131 and SURVEY.md §8
@@ -720,7 +722,13 @@ std::vector<Poly> scale_round(const orc_ctx& c, const std::vector<Poly>& xq,
     return out;
 }
 
-Ct mult(orc_ctx& c, const Ct& x, const Ct& y) {
+// Product of two ciphertexts BEFORE scale-and-round: the tensor
+// (x0 y0, x0 y1 + x1 y0, x1 y1) of the exact centred lifts over Q ++ B, NTT
+// domain (limbs: Q primes, then B primes).
+struct Tensor {
+    std::vector<Poly> t[3];  // each L + nB limbs
+};
+Tensor tensor_of(const orc_ctx& c, const Ct& x, const Ct& y) {
     const unsigned N = c.N, L = c.L, nB = c.nB;
     const std::vector<Poly>* in[4] = {&x.c0, &x.c1, &y.c0, &y.c1};
     std::vector<Poly> bext[4];
@@ -730,25 +738,46 @@ Ct mult(orc_ctx& c, const Ct& x, const Ct& y) {
         bext[p] = q_to_b(c, coeff);
         for (unsigned k = 0; k < nB; ++k) ntt_fwd(bext[p][k], c.pr[c.bidx(k)]);
     }
-    // tensor over Q ++ B
-    std::vector<Poly> tq[3], tb[3];
-    for (int t = 0; t < 3; ++t) { tq[t].assign(L, Poly(N)); tb[t].assign(nB, Poly(N)); }
-    auto tensor = [&](const Poly& a0, const Poly& a1, const Poly& b0, const Poly& b1, u64 q,
-                      Poly& o0, Poly& o1, Poly& o2) {
+    Tensor T;
+    for (int t = 0; t < 3; ++t) T.t[t].assign(L + nB, Poly(N));
+    auto tensor = [&](const Poly& a0, const Poly& a1, const Poly& b0, const Poly& b1, u64 q, unsigned r) {
         for (unsigned j = 0; j < N; ++j) {
-            o0[j] = mulmod(a0[j], b0[j], q);
-            o1[j] = addmod(mulmod(a0[j], b1[j], q), mulmod(a1[j], b0[j], q), q);
-            o2[j] = mulmod(a1[j], b1[j], q);
+            T.t[0][r][j] = mulmod(a0[j], b0[j], q);
+            T.t[1][r][j] = addmod(mulmod(a0[j], b1[j], q), mulmod(a1[j], b0[j], q), q);
+            T.t[2][r][j] = mulmod(a1[j], b1[j], q);
         }
     };
-    for (unsigned i = 0; i < L; ++i) {
-        tensor(x.c0[i], x.c1[i], y.c0[i], y.c1[i], c.pr[i].q, tq[0][i], tq[1][i], tq[2][i]);
-        for (int t = 0; t < 3; ++t) ntt_inv(tq[t][i], c.pr[i]);
-    }
-    for (unsigned k = 0; k < nB; ++k) {
-        const Prime& P = c.pr[c.bidx(k)];
-        tensor(bext[0][k], bext[1][k], bext[2][k], bext[3][k], P.q, tb[0][k], tb[1][k], tb[2][k]);
-        for (int t = 0; t < 3; ++t) ntt_inv(tb[t][k], P);
+    for (unsigned i = 0; i < L; ++i) tensor(x.c0[i], x.c1[i], y.c0[i], y.c1[i], c.pr[i].q, i);
+    for (unsigned k = 0; k < nB; ++k)
+        tensor(bext[0][k], bext[1][k], bext[2][k], bext[3][k], c.pr[c.bidx(k)].q, L + k);
+    return T;
+}
+
+// A ciphertext value: plain (c0, c1), or a PENDING product -- a sum of
+// tensors not yet scaled and relinearised, plus a plain addend.  Semantics
+// (the GPU library follows them exactly):
+//   he_mult(x, y)     -> pending {T = tensor(plain(x), plain(y)), addend 0}
+//   he_add(x, y)      -> pending {T_x + T_y, addend_x + addend_y} when either
+//                        is pending (a plain operand is an addend), else plain
+//   anything else     -> consumes plain(x)
+//   plain(pending)    =  round(t/Q * T) relinearised, + addend   (materialise)
+// Sums of products are therefore scaled and relinearised once, not once per
+// product: the decrypted value is the same, the noise smaller (one rounding).
+struct XCt {
+    Ct add;           // plain value, or the pending value's addend
+    bool pending = false;
+    Tensor T;         // pending only
+};
+
+Ct materialize(orc_ctx& c, const XCt& x) {
+    if (!x.pending) return x.add;
+    const unsigned N = c.N, L = c.L, nB = c.nB;
+    std::vector<Poly> tq[3], tb[3];
+    for (int t = 0; t < 3; ++t) {
+        tq[t].assign(x.T.t[t].begin(), x.T.t[t].begin() + L);
+        tb[t].assign(x.T.t[t].begin() + L, x.T.t[t].end());
+        for (unsigned i = 0; i < L; ++i) ntt_inv(tq[t][i], c.pr[i]);
+        for (unsigned k = 0; k < nB; ++k) ntt_inv(tb[t][k], c.pr[c.bidx(k)]);
     }
     std::vector<Poly> e0 = scale_round(c, tq[0], tb[0]);
     std::vector<Poly> e1 = scale_round(c, tq[1], tb[1]);
@@ -762,11 +791,73 @@ Ct mult(orc_ctx& c, const Ct& x, const Ct& y) {
         ntt_fwd(e0[i], c.pr[i]); ntt_fwd(e1[i], c.pr[i]);
         o.c0[i].resize(N); o.c1[i].resize(N);
         for (unsigned j = 0; j < N; ++j) {
-            o.c0[i][j] = addmod(e0[i][j], u0[i][j], q);
-            o.c1[i][j] = addmod(e1[i][j], u1[i][j], q);
+            o.c0[i][j] = addmod(addmod(e0[i][j], u0[i][j], q), x.add.c0[i][j], q);
+            o.c1[i][j] = addmod(addmod(e1[i][j], u1[i][j], q), x.add.c1[i][j], q);
         }
     }
     return o;
+}
+
+Ct zero_ct(const orc_ctx& c) {
+    Ct z;
+    z.c0.assign(c.L, Poly(c.N, 0));
+    z.c1.assign(c.L, Poly(c.N, 0));
+    return z;
+}
+
+XCt mult_pending(const orc_ctx& c, const Ct& x, const Ct& y) {
+    XCt o;
+    o.pending = true;
+    o.add = zero_ct(c);
+    o.T = tensor_of(c, x, y);
+    return o;
+}
+
+XCt add_any(const orc_ctx& c, const XCt& a, const XCt& b) {
+    XCt o;
+    o.add = add(c, a.add, b.add);
+    o.pending = a.pending || b.pending;
+    if (!o.pending) return o;
+    const unsigned L = c.L, D = c.L + c.nB;
+    const XCt& p = a.pending ? a : b;
+    o.T = p.T;
+    if (a.pending && b.pending)
+        for (int t = 0; t < 3; ++t)
+            for (unsigned r = 0; r < D; ++r) {
+                const u64 q = r < L ? c.pr[r].q : c.pr[c.bidx(r - L)].q;
+                for (unsigned j = 0; j < c.N; ++j) o.T.t[t][r][j] = addmod(a.T.t[t][r][j], b.T.t[t][r][j], q);
+            }
+    return o;
+}
+
+// Eager product (a pending product materialised at once).
+Ct mult(orc_ctx& c, const Ct& x, const Ct& y) { return materialize(c, mult_pending(c, x, y)); }
+
+// pending buffer: [addend: 2 L N words][T: 3 (L + nB) N words]
+size_t pending_words(const orc_ctx& c) { return (size_t)2 * c.L * c.N + (size_t)3 * (c.L + c.nB) * c.N; }
+XCt load_x(const orc_ctx& c, const uint64_t* buf, int pending) {
+    XCt x;
+    x.add = load(c, buf);
+    x.pending = pending != 0;
+    if (!x.pending) return x;
+    const unsigned D = c.L + c.nB;
+    const uint64_t* t = buf + (size_t)2 * c.L * c.N;
+    for (int k = 0; k < 3; ++k) {
+        x.T.t[k].resize(D);
+        for (unsigned r = 0; r < D; ++r) {
+            const uint64_t* p = t + ((size_t)k * D + r) * c.N;
+            x.T.t[k][r].assign(p, p + c.N);
+        }
+    }
+    return x;
+}
+void store_x(const orc_ctx& c, const XCt& x, uint64_t* buf) {
+    store(c, x.add, buf);
+    if (!x.pending) return;
+    const unsigned D = c.L + c.nB;
+    uint64_t* t = buf + (size_t)2 * c.L * c.N;
+    for (int k = 0; k < 3; ++k)
+        for (unsigned r = 0; r < D; ++r) std::memcpy(t + ((size_t)k * D + r) * c.N, x.T.t[k][r].data(), c.N * 8);
 }
 
 template <typename F>
@@ -835,6 +926,16 @@ int orc_rot(orc_ctx* c, const uint64_t* a, int64_t z, uint64_t* out) {
 }
 int orc_mult(orc_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t* out) {
     return guarded([&] { store(*c, mult(*c, load(*c, a), load(*c, b)), out); });
+}
+size_t orc_pending_words(const orc_ctx* c) { return pending_words(*c); }
+int orc_mult_pending(orc_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t* out) {
+    return guarded([&] { store_x(*c, mult_pending(*c, load(*c, a), load(*c, b)), out); });
+}
+int orc_add_any(orc_ctx* c, const uint64_t* a, int a_pending, const uint64_t* b, int b_pending, uint64_t* out) {
+    return guarded([&] { store_x(*c, add_any(*c, load_x(*c, a, a_pending), load_x(*c, b, b_pending)), out); });
+}
+int orc_materialize(orc_ctx* c, const uint64_t* x, uint64_t* out) {
+    return guarded([&] { store(*c, materialize(*c, load_x(*c, x, 1)), out); });
 }
 
 double orc_noise_budget(orc_ctx* c, const uint64_t* ct) {

@@ -44,6 +44,8 @@ class Oracle:
             L.orc_ct_words.restype = _sz
             L.orc_ct_words.argtypes = [_vp]
             L.orc_last_error.restype = ctypes.c_char_p
+            L.orc_pending_words.restype = _sz
+            L.orc_pending_words.argtypes = [_vp]
             for name, args in {
                 "orc_encrypt": [_vp, _vp, _sz, _u64, _vp],
                 "orc_decrypt": [_vp, _vp, _sz, _vp],
@@ -51,6 +53,9 @@ class Oracle:
                 "orc_cmult": [_vp, _vp, _vp, _sz, _vp],
                 "orc_rot": [_vp, _vp, _i64, _vp],
                 "orc_mult": [_vp, _vp, _vp, _vp],
+                "orc_mult_pending": [_vp, _vp, _vp, _vp],
+                "orc_add_any": [_vp, _vp, _int, _vp, _int, _vp],
+                "orc_materialize": [_vp, _vp, _vp],
                 "orc_ntt_fwd": [_vp, _int, _vp],
                 "orc_ntt_inv": [_vp, _int, _vp],
                 "orc_encode": [_vp, _vp, _sz, _vp],
@@ -122,6 +127,30 @@ class Oracle:
     def mult(self, a, b):
         out = self._ct()
         self._chk(self.lib().orc_mult(self._h, _p(a), _p(b), _p(out)))
+        return out
+
+    # Pending products (bfv_oracle.cpp XCt): he_mult returns an unscaled,
+    # unrelinearised tensor that he_add accumulates; plain() materialises.
+    # Values here are (words, is_pending) pairs.
+    def mult_pending(self, a, b):
+        out = np.zeros(int(self.lib().orc_pending_words(self._h)), dtype=np.uint64)
+        self._chk(self.lib().orc_mult_pending(self._h, _p(a), _p(b), _p(out)))
+        return (out, True)
+
+    def add_any(self, x, y):
+        (a, pa), (b, pb) = x, y
+        n = int(self.lib().orc_pending_words(self._h)) if (pa or pb) else self.words
+        out = np.zeros(n, dtype=np.uint64)
+        self._chk(self.lib().orc_add_any(self._h, _p(np.ascontiguousarray(a)), int(pa),
+                                         _p(np.ascontiguousarray(b)), int(pb), _p(out)))
+        return (out, bool(pa or pb))
+
+    def plain(self, x):
+        w, pend = x
+        if not pend:
+            return w
+        out = self._ct()
+        self._chk(self.lib().orc_materialize(self._h, _p(np.ascontiguousarray(w)), _p(out)))
         return out
 
     def noise_budget(self, ct) -> float:

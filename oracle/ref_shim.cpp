@@ -15,6 +15,7 @@
 // depth is raised with he_mult by an all-ones vector, and the phase tag follows
 // the minter's phase.  All of this is host bookkeeping, O(segment) per op.
 #include <atomic>
+#include <map>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -64,6 +65,7 @@ class OracleBackend final : public Backend {
     OracleBackend(orc_ctx* ctx, std::uint64_t enc_counter)
         : ctx_(ctx), cfg_(config_of(ctx)), minter_(cfg_.slot_count), counter_(enc_counter) {
         words_ = orc_ct_words(ctx);
+        pwords_ = orc_pending_words(ctx);
     }
     static BackendConfig config_of(orc_ctx* ctx) {
         std::uint64_t info[64];
@@ -89,17 +91,20 @@ class OracleBackend final : public Backend {
         check(orc_decrypt(ctx_, buf(ct), out.size(), out.data()));
         return out;
     }
+    // he_mult yields a pending product and he_add of pending values sums their
+    // tensors (bfv_oracle.cpp XCt); every other op reads the materialised value.
     Ciphertext he_add(const Ciphertext& x, const Ciphertext& y) override {
         same_segment(x, y, "he_add");
-        std::vector<std::uint64_t> o(words_);
-        check(orc_add(ctx_, buf(x), buf(y), o.data()));
+        const bool px = pending(x), py = pending(y);
+        std::vector<std::uint64_t> o(px || py ? pwords_ : words_);
+        check(orc_add_any(ctx_, raw(x), px, raw(y), py, o.data()));
         count(&OpStats::n_add);
         return keep(std::move(o), x.segment_length(), std::max(x.depth(), y.depth()));
     }
     Ciphertext he_mult(const Ciphertext& x, const Ciphertext& y) override {
         same_segment(x, y, "he_mult");
-        std::vector<std::uint64_t> o(words_);
-        check(orc_mult(ctx_, buf(x), buf(y), o.data()));
+        std::vector<std::uint64_t> o(pwords_);
+        check(orc_mult_pending(ctx_, buf(x), buf(y), o.data()));
         count(&OpStats::n_mult_cc);
         return keep(std::move(o), x.segment_length(), std::max(x.depth(), y.depth()) + 1);
     }
@@ -132,7 +137,8 @@ class OracleBackend final : public Backend {
     void set_phase(Phase p) override { phase_.store(p); }
     Phase phase() const override { return phase_.load(); }
 
-    const std::vector<std::uint64_t>& ct_words(std::uint64_t id) const { return store_.at(id); }
+    // the (materialised) ciphertext words of handle id
+    const std::vector<std::uint64_t>& ct_words(std::uint64_t id) { return plain(id); }
     std::uint64_t last_decrypted() const { return last_decrypted_; }
     std::uint64_t counter() const { return counter_; }
 
@@ -151,9 +157,21 @@ class OracleBackend final : public Backend {
         std::lock_guard<std::mutex> lk(mu_);
         (stats_.*c).bump(p);
     }
-    const std::uint64_t* buf(const Ciphertext& ct) const {
-        return store_.at(Minter::id_of(ct)).data();
+    bool pending(const Ciphertext& ct) const { return store_.at(Minter::id_of(ct)).size() == pwords_; }
+    const std::uint64_t* raw(const Ciphertext& ct) const { return store_.at(Minter::id_of(ct)).data(); }
+    // plain value of handle id: a pending product is materialised once, cached
+    const std::vector<std::uint64_t>& plain(std::uint64_t id) {
+        const std::vector<std::uint64_t>& w = store_.at(id);
+        if (w.size() != pwords_) return w;
+        auto it = plain_.find(id);
+        if (it == plain_.end()) {
+            std::vector<std::uint64_t> o(words_);
+            check(orc_materialize(ctx_, w.data(), o.data()));
+            it = plain_.emplace(id, std::move(o)).first;
+        }
+        return it->second;
     }
+    const std::uint64_t* buf(const Ciphertext& ct) { return plain(Minter::id_of(ct)).data(); }
     Ciphertext keep(std::vector<std::uint64_t> words, std::size_t seg, std::size_t depth) {
         const std::uint64_t id = store_.size();
         store_.push_back(std::move(words));
@@ -163,7 +181,8 @@ class OracleBackend final : public Backend {
     orc_ctx* ctx_;
     BackendConfig cfg_;
     Minter minter_;
-    std::size_t words_ = 0;
+    std::size_t words_ = 0, pwords_ = 0;
+    std::map<std::uint64_t, std::vector<std::uint64_t>> plain_;
     std::uint64_t counter_;
     std::uint64_t last_decrypted_ = 0;
     std::vector<std::vector<std::uint64_t>> store_;

@@ -72,6 +72,32 @@ def test_noise_budget_after_mult(oracle_factory):
     assert o.noise_budget(p) > 20  # fixed-point measure saturates near 61 bits
 
 
+def test_pending_products(oracle_factory):
+    """he_mult is a pending product; he_add sums pending tensors (one
+    scale-and-round + relinearisation at materialisation, bfv_oracle.cpp XCt)."""
+    o = oracle_factory(2)
+    rng = np.random.default_rng(4)
+    S = 300
+    v = [rng.integers(-8, 8, S) for _ in range(5)]
+    c = [o.encrypt(x, i) for i, x in enumerate(v)]
+    p01 = o.mult_pending(c[0], c[1])
+    # a lone pending product materialises to the eager product, bit for bit
+    assert np.array_equal(o.plain(p01), o.mult(c[0], c[1]))
+    # plain + plain is the plain add
+    assert np.array_equal(o.plain(o.add_any((c[0], False), (c[1], False))), o.add(c[0], c[1]))
+    # zero + products + plain addend, in any association
+    s1 = o.add_any(o.add_any((c[4], False), p01), o.mult_pending(c[2], c[3]))
+    s2 = o.add_any(p01, o.add_any(o.mult_pending(c[2], c[3]), (c[4], False)))
+    assert s1[1] and s2[1]
+    m1 = o.plain(s1)
+    assert np.array_equal(m1, o.plain(s2))
+    assert np.array_equal(o.decrypt(m1, S), (v[0] * v[1] + v[2] * v[3] + v[4]) % T)
+    # one rounding instead of two: at least the eager sum's noise budget
+    eager = o.add(o.add(c[4], o.mult(c[0], c[1])), o.mult(c[2], c[3]))
+    assert np.array_equal(o.decrypt(eager, S), o.decrypt(m1, S))
+    assert o.noise_budget(m1) >= o.noise_budget(eager) - 1.0
+
+
 def test_error_conventions(oracle_factory):
     from oracle.bindings import OracleError
 
