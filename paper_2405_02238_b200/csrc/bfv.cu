@@ -625,6 +625,86 @@ __global__ void k_tensor_s1(DevCtx cx, u32 n, const u64* const* A, const u64* co
     }
 }
 
+// Pending products (oracle XCt): T[d] (+)= sum over the items i of
+// d's range [off[d], off[d+1]) of tensor(a_i, b_i) over Q ++ B, NTT domain,
+// T: [3][L+nB][N] per destination.  a_i, b_i give the Q limbs; their B
+// extensions are XB + i * 4 nB N (k_q_to_b's layout).  init[d]: T[d] already
+// holds a partial sum to add to.  One thread per coefficient of one limb;
+// products accumulate in Karatsuba columns, reduced every 2 items (4 products
+// per column, the Cols bound).
+template <typename SH>
+__global__ void __launch_bounds__(kThreads, 4) k_tensor_acc(DevCtx cx, u32 n, const u32* off, const u64* const* A,
+                                                             const u64* const* B, const u64* XB, u64* const* T,
+                                                             const unsigned char* init) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
+    const u32 N = dp->N, L = SH::L, K = SH::K, nB = SH::nB, D = L + nB;
+    ITEM_LOOP {
+        const u32 d = blockIdx.z;
+        const Prime& P = dp->pr[d < L ? d : L + K + (d - L)];
+        const u32 i0 = off[item], i1 = off[item + 1];
+        u64* t0 = T[item] + (size_t)d * N;
+        u64* t1 = t0 + (size_t)D * N;
+        u64* t2 = t1 + (size_t)D * N;
+        const bool acc = init[item] != 0;
+        COEF_LOOP {
+            Cols s0, s1, s2;
+            if (acc) {
+                s0.x = t0[j];
+                s1.x = t1[j];
+                s2.x = t2[j];
+            }
+            u32 since = 0;
+            for (u32 i = i0; i < i1; ++i) {
+                const u64 *a0, *a1, *b0, *b1;
+                if (d < L) {
+                    a0 = A[i] + (size_t)d * N; a1 = A[i] + (size_t)(L + d) * N;
+                    b0 = B[i] + (size_t)d * N; b1 = B[i] + (size_t)(L + d) * N;
+                } else {
+                    a0 = XB + ((size_t)i * 4 * nB + (d - L)) * N; a1 = a0 + (size_t)nB * N;
+                    b0 = a1 + (size_t)nB * N; b1 = b0 + (size_t)nB * N;
+                }
+                const Dig<SH::S> x0 = split<SH::S>(a0[j]), x1 = split<SH::S>(a1[j]), y0 = split<SH::S>(b0[j]),
+                                 y1 = split<SH::S>(b1[j]);
+                s0.mac(x0, y0);
+                s1.mac(x0, y1);
+                s1.mac(x1, y0);
+                s2.mac(x1, y1);
+                if (++since == 2 && i + 1 < i1) {
+                    const u64 r0 = reduce_acc(s0.fold<SH::S>(), P), r1 = reduce_acc(s1.fold<SH::S>(), P),
+                              r2 = reduce_acc(s2.fold<SH::S>(), P);
+                    s0 = Cols{}; s1 = Cols{}; s2 = Cols{};
+                    s0.x = r0; s1.x = r1; s2.x = r2;
+                    since = 0;
+                }
+            }
+            t0[j] = reduce_acc(s0.fold<SH::S>(), P);
+            t1[j] = reduce_acc(s1.fold<SH::S>(), P);
+            t2[j] = reduce_acc(s2.fold<SH::S>(), P);
+        }
+    }
+}
+
+// out[o] (+)= sum over t in [off[o], off[o+1]) of in[t], over the T region of
+// pending buffers ([3][L+nB][N]); init[o]: add to out[o]'s current value.
+template <typename SH>
+__global__ void k_tsum(DevCtx cx, u32 n, const u32* off, const u64* const* in, u64* const* out,
+                       const unsigned char* init) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
+    const u32 N = dp->N, L = SH::L, K = SH::K, nB = SH::nB, D = L + nB;
+    ITEM_LOOP {
+        const u32 r = blockIdx.z;  // limb of [3][D]
+        const u32 d = r % D;
+        const u64 q = dp->pr[d < L ? d : L + K + (d - L)].q;
+        u64* o = out[item] + (size_t)r * N;
+        const bool acc = init[item] != 0;
+        COEF_LOOP {
+            u64 s = acc ? o[j] : 0;
+            for (u32 t = off[item]; t < off[item + 1]; ++t) s = add_mod(s, in[t][(size_t)r * N + j], q);
+            o[j] = s;
+        }
+    }
+}
+
 // oracle scale_round(): round(t x / Q) from Q ++ B residues, then exact B -> Q
 template <typename SH>
 // Dg (optional, alpha = 1): component 2 is not stored in E but lifted straight
@@ -1322,20 +1402,12 @@ void Context::rotate(int n, const u64* const* modup, const u64* const* ct, const
     release(A);
 }
 
-void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* out) {
-    if (n <= 0) return;
-    const u32 Lm = hp_.L, Rm = hp_.R, Dm = hp_.L + hp_.nB;
-    const int chunk = chunk_for((size_t)(7 * Lm + 4 * hp_.nB + 3 * Dm + hp_.dnum * Rm + 2 * Rm) * hp_.N, kChunkMult);
-    if (n > chunk) {
-        for (int c0 = 0; c0 < n; c0 += chunk) {
-            const int cn = std::min(chunk, n - c0);
-            mult(cn, a + c0, b + c0, out + c0);
-        }
-        return;
-    }
-    const u32 N = hp_.N, L = hp_.L, K = hp_.K, R = hp_.R, nB = hp_.nB, dnum = hp_.dnum;
+// Exact B extension of (a.c0, a.c1, b.c0, b.c1), NTT domain over B:
+// returns XB [n][4][nB][N] (k_q_to_b's layout; caller releases).
+u64* Context::b_extend(int n, const u64* const* a, const u64* const* b) {
+    const u32 N = hp_.N, L = hp_.L, K = hp_.K, nB = hp_.nB;
     const size_t LN = (size_t)L * N;
-    // 1. (a.c0, a.c1, b.c0, b.c1) to the coefficient domain (out-of-place INTT)
+    // 1. to the coefficient domain (out-of-place INTT)
     u64* X = alloc((size_t)n * 4 * LN);
     if (ntt_fusable_size(hp_.dev)) {
         std::vector<const u64*> src((size_t)n * 4 * L);
@@ -1365,29 +1437,15 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
     if (hp_.L == 3) k_q_to_b<ShapeQ3><<<grid_of(N, n, 4), kThreads, 0, stream_>>>(cx_, n, X, XB); else k_q_to_b<ShapeQ8><<<grid_of(N, n, 4), kThreads, 0, stream_>>>(cx_, n, X, XB); ++launches_;
     release(X);
     ntt(true, jobs_contig(XB, n * 4 * nB, L + K, nB));
-    // 3. tensor over Q ++ B, INTT
-    const u32 D = L + nB;
-    u64* T = alloc((size_t)n * 3 * D * N);
-    std::vector<const u64*> va(a, a + n), vb(b, b + n);
-    if (ntt_tensor_fusable(hp_.dev)) {  // tensor computed inside its INTT's load
-        ntt_tensor_fused(cx_, hp_.dev, n, upload(va), upload(vb), XB, T, stream_);
-        ++launches_;
-        release(XB);
-    } else {
-        const bool s1 = ntt_inverse_takes_first_stage(hp_.dev) && tensor_first_stage();
-        if (s1) {
-            if (hp_.L == 3) k_tensor_s1<ShapeQ3><<<grid_of(N / 2, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T); else k_tensor_s1<ShapeQ8><<<grid_of(N / 2, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T);
-        } else {
-            if (hp_.L == 3) k_tensor<ShapeQ3><<<grid_of(N, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T); else k_tensor<ShapeQ8><<<grid_of(N, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T);
-        }
-        ++launches_;
-        release(XB);
-        NttJobs tj = jobs_contig(T, n * 3 * D, 0, D);
-        tj.first_done = s1 ? 1 : 0;
-        for (u32 k = 0; k < nB; ++k) tj.prime[L + k] = (unsigned char)(L + K + k);
-        tj.unscaled = kLazyOut;  // k_scale_round: Shoup by dhat_inv_n; B limbs reduced, times T_n
-        ntt(false, tj);
-    }
+    return XB;
+}
+
+// Scale-and-round of n coefficient-domain tensors T [n][3][L+nB][N] (unscaled
+// INTT output, kLazyOut) and relinearisation: out[i] = (e0, e1) + KS(e2).
+// Releases T.
+void Context::scale_relin(int n, u64* T, u64* const* out) {
+    const u32 N = hp_.N, L = hp_.L, R = hp_.R, dnum = hp_.dnum;
+    const size_t LN = (size_t)L * N;
     // 4. scale and round back to Q (coefficient form)
     u64* E = alloc((size_t)n * 3 * LN);
     const bool fused = ntt_fusable(hp_.dev, kFuseModUp);
@@ -1422,6 +1480,140 @@ void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* 
     release(Dg);
     release(A);
     release(E);
+}
+
+void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* out) {
+    if (n <= 0) return;
+    const u32 Lm = hp_.L, Rm = hp_.R, Dm = hp_.L + hp_.nB;
+    const int chunk = chunk_for((size_t)(7 * Lm + 4 * hp_.nB + 3 * Dm + hp_.dnum * Rm + 2 * Rm) * hp_.N, kChunkMult);
+    if (n > chunk) {
+        for (int c0 = 0; c0 < n; c0 += chunk) {
+            const int cn = std::min(chunk, n - c0);
+            mult(cn, a + c0, b + c0, out + c0);
+        }
+        return;
+    }
+    const u32 N = hp_.N, L = hp_.L, K = hp_.K, nB = hp_.nB;
+    u64* XB = b_extend(n, a, b);
+    // 3. tensor over Q ++ B, INTT
+    const u32 D = L + nB;
+    u64* T = alloc((size_t)n * 3 * D * N);
+    std::vector<const u64*> va(a, a + n), vb(b, b + n);
+    if (ntt_tensor_fusable(hp_.dev)) {  // tensor computed inside its INTT's load
+        ntt_tensor_fused(cx_, hp_.dev, n, upload(va), upload(vb), XB, T, stream_);
+        ++launches_;
+        release(XB);
+    } else {
+        const bool s1 = ntt_inverse_takes_first_stage(hp_.dev) && tensor_first_stage();
+        if (s1) {
+            if (hp_.L == 3) k_tensor_s1<ShapeQ3><<<grid_of(N / 2, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T); else k_tensor_s1<ShapeQ8><<<grid_of(N / 2, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T);
+        } else {
+            if (hp_.L == 3) k_tensor<ShapeQ3><<<grid_of(N, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T); else k_tensor<ShapeQ8><<<grid_of(N, n, D), kThreads, 0, stream_>>>(cx_, n, upload(va), upload(vb), XB, T);
+        }
+        ++launches_;
+        release(XB);
+        NttJobs tj = jobs_contig(T, n * 3 * D, 0, D);
+        tj.first_done = s1 ? 1 : 0;
+        for (u32 k = 0; k < nB; ++k) tj.prime[L + k] = (unsigned char)(L + K + k);
+        tj.unscaled = kLazyOut;  // k_scale_round: Shoup by dhat_inv_n; B limbs reduced, times T_n
+        ntt(false, tj);
+    }
+    scale_relin(n, T, out);
+}
+
+void Context::tensor_acc(int n_dest, const u32* off, const u64* const* a, const u64* const* b, u64* const* T,
+                         const unsigned char* init) {
+    if (n_dest <= 0) return;
+    const u32 N = hp_.N, L = hp_.L, nB = hp_.nB, D = L + nB;
+    const int chunk = chunk_for((size_t)(4 * L + 4 * nB) * N, kChunkMult);
+    // segments: (destination, item range) pieces of at most `chunk` items per launch sequence
+    std::vector<const u64*> ca, cb;
+    std::vector<u32> soff{0};
+    std::vector<u64*> sdst;
+    std::vector<unsigned char> sinit;
+    auto run = [&]() {
+        const int n = (int)ca.size();
+        if (n > 0) {
+            u64* XB = b_extend(n, ca.data(), cb.data());
+            const int ns = (int)sdst.size();
+            if (hp_.L == 3) k_tensor_acc<ShapeQ3><<<grid_of(N, ns, D), kThreads, 0, stream_>>>(cx_, ns, upload(soff), upload(ca), upload(cb), XB, upload(sdst), upload(sinit)); else k_tensor_acc<ShapeQ8><<<grid_of(N, ns, D), kThreads, 0, stream_>>>(cx_, ns, upload(soff), upload(ca), upload(cb), XB, upload(sdst), upload(sinit));
+            ++launches_;
+            HGM_CUDA(cudaGetLastError());
+            release(XB);
+        } else if (!sdst.empty()) {  // destinations without items: zero (or unchanged)
+            for (size_t s2 = 0; s2 < sdst.size(); ++s2)
+                if (!sinit[s2]) HGM_CUDA(cudaMemsetAsync(sdst[s2], 0, (size_t)3 * D * N * 8, stream_));
+        }
+        ca.clear(); cb.clear(); sdst.clear(); sinit.clear();
+        soff.assign(1, 0);
+    };
+    for (int d = 0; d < n_dest; ++d) {
+        u32 i = off[d];
+        bool first = true;
+        do {
+            if ((int)ca.size() >= chunk) run();
+            const u32 take = std::min<u32>(off[d + 1] - i, (u32)(chunk - (int)ca.size()));
+            for (u32 t = i; t < i + take; ++t) {
+                ca.push_back(a[t]);
+                cb.push_back(b[t]);
+            }
+            sdst.push_back(T[d]);
+            sinit.push_back(first ? init[d] : 1);
+            soff.push_back((u32)ca.size());
+            first = false;
+            i += take;
+        } while (i < off[d + 1]);
+    }
+    run();
+}
+
+void Context::tsum(int n_out, const u32* off, const u64* const* in, u64* const* out, const unsigned char* init) {
+    if (n_out <= 0) return;
+    const u32 D = hp_.L + hp_.nB;
+    for (int c0 = 0; c0 < n_out; c0 += kChunkLin) {
+        const int cn = std::min(kChunkLin, n_out - c0);
+        std::vector<u32> sub(cn + 1);
+        for (int i = 0; i <= cn; ++i) sub[i] = off[c0 + i] - off[c0];
+        std::vector<const u64*> vin(in + off[c0], in + off[c0 + cn]);
+        std::vector<u64*> vo(out + c0, out + c0 + cn);
+        std::vector<unsigned char> vi(init + c0, init + c0 + cn);
+        if (hp_.L == 3) k_tsum<ShapeQ3><<<grid_of(hp_.N, cn, 3 * D), kThreads, 0, stream_>>>(cx_, cn, upload(sub), upload(vin), upload(vo), upload(vi)); else k_tsum<ShapeQ8><<<grid_of(hp_.N, cn, 3 * D), kThreads, 0, stream_>>>(cx_, cn, upload(sub), upload(vin), upload(vo), upload(vi));
+        ++launches_;
+        HGM_CUDA(cudaGetLastError());
+    }
+}
+
+void Context::materialize(int n, const u64* const* T, const u64* const* addend, u64* const* out) {
+    if (n <= 0) return;
+    const u32 N = hp_.N, L = hp_.L, K = hp_.K, R = hp_.R, nB = hp_.nB, D = L + nB;
+    const int chunk = chunk_for((size_t)(3 * D + 3 * L + hp_.dnum * R + 2 * R) * N, kChunkMult);
+    if (n > chunk) {
+        for (int c0 = 0; c0 < n; c0 += chunk) {
+            const int cn = std::min(chunk, n - c0);
+            materialize(cn, T + c0, addend ? addend + c0 : nullptr, out + c0);
+        }
+        return;
+    }
+    // tensor to the coefficient domain (out of place: the pending value stays valid)
+    u64* Tc = alloc((size_t)n * 3 * D * N);
+    NttJobs tj = jobs_contig(Tc, n * 3 * D, 0, D);
+    for (u32 k = 0; k < nB; ++k) tj.prime[L + k] = (unsigned char)(L + K + k);
+    tj.unscaled = kLazyOut;  // k_scale_round: Shoup by dhat_inv_n; B limbs reduced, times T_n
+    if (ntt_fusable_size(hp_.dev)) {
+        std::vector<const u64*> src((size_t)n * 3 * D);
+        for (int i = 0; i < n; ++i)
+            for (u32 w = 0; w < 3 * D; ++w) src[(size_t)i * 3 * D + w] = T[i] + (size_t)w * N;
+        tj.src = upload(src);
+    } else {
+        std::vector<const u64*> src(T, T + n);
+        std::vector<u64*> dst(n);
+        for (int i = 0; i < n; ++i) dst[i] = Tc + (size_t)i * 3 * D * N;
+        k_copy<<<grid_of(N, n), kThreads, 0, stream_>>>(n, (size_t)3 * D * N, upload(src), upload(dst)); ++launches_;
+    }
+    ntt(false, tj);
+    scale_relin(n, Tc, out);
+    if (addend) add(n, out, addend, out);
+    HGM_CUDA(cudaGetLastError());
 }
 
 }  // namespace hgm

@@ -107,6 +107,17 @@ class Context {
     void rotate(int n, const u64* const* modup, const u64* const* ct, const u32* g,
                 u64* const* out);
     void mult(int n, const u64* const* a, const u64* const* b, u64* const* out);
+    // Pending products (oracle XCt): a pending value is [T: 3 (L+nB) N][addend: 2 L N],
+    // T the unscaled tensor sum over Q ++ B in the NTT domain.
+    size_t pending_words() const { return (size_t)3 * (hp_.L + hp_.nB) * hp_.N + ct_words(); }
+    size_t tensor_words() const { return (size_t)3 * (hp_.L + hp_.nB) * hp_.N; }
+    // T[d] (+= if init[d]) sum of tensor(a[i], b[i]) over i in [off[d], off[d+1])
+    void tensor_acc(int n_dest, const u32* off, const u64* const* a, const u64* const* b, u64* const* T,
+                    const unsigned char* init);
+    // T regions: out[o] (+= if init[o]) sum of in[t], t in [off[o], off[o+1])
+    void tsum(int n_out, const u32* off, const u64* const* in, u64* const* out, const unsigned char* init);
+    // out[i] = scale-and-round + relinearisation of T[i], + addend[i] (optional)
+    void materialize(int n, const u64* const* T, const u64* const* addend, u64* const* out);
     void copy(int n, const u64* const* in, u64* const* out);
 
     // batched NTT helpers (exposed for tests / micro-benchmarks)
@@ -115,6 +126,8 @@ class Context {
 
   private:
     void build_keys();
+    u64* b_extend(int n, const u64* const* a, const u64* const* b);
+    void scale_relin(int n, u64* T, u64* const* out);
     void key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, const u64* const* addn,
                          const u32* g, u64* const* out);
     void inner_product(int n, const u64* const* digits, const u64* const* keys, const u32* g,

@@ -12,6 +12,11 @@
 //     the digit lift uses centred residues and commutes with X -> X^g);
 //   * trees of he_add over he_cmult / he_add become one masked sum
 //     (modular adds are associative and commutative);
+//   * he_mult is a PENDING product (oracle XCt): add trees over products sum
+//     their unscaled tensors, and scale-and-round + relinearisation run once
+//     when a non-add op reads the value (a Mat node); a product whose only
+//     reader is such a sum is accumulated straight into the sum's tensor
+//     (fused: its own tensor is never stored);
 //   * every op of one dependency level is one batched launch sequence over
 //     all (node, instance) pairs; rotations are grouped by Galois key so that
 //     one key read from HBM serves the whole group.
@@ -39,10 +44,12 @@ struct MaskData {
 using MaskRef = std::shared_ptr<const MaskData>;
 
 struct PNode {
-    enum Kind : unsigned char { Input, Enc, Rot, Comb, Mult };
+    enum Kind : unsigned char { Input, Enc, Rot, Comb, Mult, Mat };
     Kind kind = Input;
-    std::vector<int> in;          // Rot: {src}; Mult: {a, b}; Comb: term inputs
+    std::vector<int> in;          // Rot / Mat: {src}; Mult: {a, b}; Comb: term inputs
     std::vector<MaskRef> masks;   // Comb: one per term, null = plain addend
+    std::vector<char> fused;      // Comb (set by optimise): term is a Mult accumulated in place
+    bool pend = false;            // Input: a pending form is supplied (ExecIO::input_pending)
     u32 g = 1;                    // Rot: Galois element
     int slot = -1;                // Input / Enc: external index
     size_t S = 0;                 // logical segment length
@@ -53,7 +60,7 @@ struct Program {
     std::vector<int> outputs;
     int n_inputs = 0;  // Input slots
     int n_enc = 0;     // Enc slots
-    int add_input(size_t S);
+    int add_input(size_t S, bool pending = false);
     int add_enc(size_t S);
     int add_rot(int src, u32 g);
     int add_comb(std::vector<int> in, std::vector<MaskRef> masks);
@@ -66,7 +73,10 @@ struct Schedule {
     std::vector<std::vector<int>> levels;
     std::vector<int> last_use_level;     // -1: never read
     std::vector<char> is_output;
-    size_t rot_count = 0, comb_count = 0, mult_count = 0;
+    std::vector<char> pk;                // node value is a pending product
+    std::vector<int> pending_out;        // per output: node whose pending form is also returned, or -1
+    std::vector<char> is_pending_output;
+    size_t rot_count = 0, comb_count = 0, mult_count = 0, pending_count = 0, mat_count = 0;
 };
 Schedule optimise(const Program& p);
 
@@ -77,6 +87,10 @@ struct ExecIO {
     // Enc slot s of instance k -> host values and encryption counter
     std::function<const i64*(int s, int k)> enc_values;
     std::function<u64(int s, int k)> enc_counter;
+    // Input slot s of instance k -> its pending form (Input nodes with pend set)
+    std::function<const u64*(int s, int k)> input_pending;
+    // if set: receives, per output, a buffer of K pending forms (or nullptr)
+    std::vector<u64*>* pending_out = nullptr;
 };
 
 // Executes `sch` for io.K instances; returns, for each output o, a device
@@ -86,7 +100,7 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io);
 // Kernel-launch accounting of the last execute() on this thread.
 struct ExecCounters {
     size_t levels = 0, launches = 0, rot_items = 0, modup_items = 0, comb_items = 0,
-           mult_items = 0, enc_items = 0;
+           mult_items = 0, enc_items = 0, mat_items = 0;
 };
 ExecCounters last_exec_counters();
 

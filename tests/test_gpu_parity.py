@@ -84,3 +84,44 @@ def test_apply_plan_fused_equals_op_by_op(gpu_factory, oracle_factory):
         term = o.cmult(oa if z == 0 else o.rot(oa, z), m)
         acc = term if acc is None else o.add(acc, term)
     assert np.array_equal(g.export(res), acc)
+
+
+@pytest.mark.parametrize("pid", [2, 0])
+def test_pending_products_bit_exact(pid, gpu_factory, oracle_factory):
+    """he_mult is a pending product and he_add sums pending tensors (oracle
+    XCt): sums of products, mixed with plain addends, materialised in one
+    flush or read back between flushes, masked or rotated afterwards."""
+    g, o = gpu_factory(pid), oracle_factory(pid)
+    rng = np.random.default_rng(40 + pid)
+    S = 257
+    v = [rand_vals(rng, S) for _ in range(6)]
+    gc = [g.encrypt(x, counter=2000 + i) for i, x in enumerate(v)]
+    oc = [(o.encrypt(x, 2000 + i), False) for i, x in enumerate(v)]
+    # one flush: acc = c5 + c0 c1 + c2 c3 + c4 c4
+    gacc, oacc = gc[5], oc[5]
+    for i, j in [(0, 1), (2, 3), (4, 4)]:
+        gacc = g.he_add(gacc, g.he_mult(gc[i], gc[j]))
+        oacc = o.add_any(oacc, o.mult_pending(oc[i][0], oc[j][0]))
+    want = (v[5] + v[0] * v[1] + v[2] * v[3] + v[4] * v[4]) % T
+    assert np.array_equal(g.export(gacc), o.plain(oacc))
+    assert np.array_equal(g.decrypt(gacc), want)
+    # the flushed sum is still pending: adding another product sums tensors
+    p2 = g.he_mult(gc[0], gc[5])
+    gsum = g.he_add(p2, gacc)
+    osum = o.add_any(o.mult_pending(oc[0][0], oc[5][0]), oacc)
+    assert np.array_equal(g.export(gsum), o.plain(osum))
+    # a product read twice: by a sum and by a mask product
+    mask = rng.integers(0, 2, S).astype(np.int64)
+    p01 = g.he_mult(gc[0], gc[1])
+    gmix = g.he_add(g.he_cmult(p01, mask), g.he_add(p01, gc[2]))
+    op01 = o.mult_pending(oc[0][0], oc[1][0])
+    omix = o.add_any((o.cmult(o.plain(op01), mask), False), o.add_any(op01, oc[2]))
+    assert np.array_equal(g.export(gmix), o.plain(omix))
+    assert np.array_equal(g.decrypt(gmix), (v[0] * v[1] * mask + v[0] * v[1] + v[2]) % T)
+    # identity and real rotations of a pending sum read its materialised value
+    for z in (0, 3):
+        r = g.he_rot(gacc, z)
+        assert np.array_equal(g.export(r), o.rot(o.plain(oacc), z))
+    # product of a pending value (materialised operand)
+    m2 = g.he_mult(gacc, gc[1])
+    assert np.array_equal(g.export(m2), o.mult(o.plain(oacc), oc[1][0]))
