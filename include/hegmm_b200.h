@@ -78,6 +78,9 @@ int hgm_encrypt(hgm_ctx* ctx, const int64_t* values, size_t S, hgm_ct** out);
 int hgm_encrypt_at(hgm_ctx* ctx, const int64_t* values, size_t S, uint64_t counter, hgm_ct** out);
 int hgm_decrypt(hgm_ctx* ctx, const hgm_ct* ct, int64_t* out, size_t cap);
 int hgm_add(hgm_ctx* ctx, const hgm_ct* x, const hgm_ct* y, hgm_ct** out);
+/* he_mult's result is a pending product: hgm_add over products sums their
+ * unscaled tensors; scale-and-round and relinearisation run once, when any
+ * other op, decrypt or export reads the value (same slots, counters, depth). */
 int hgm_mul(hgm_ctx* ctx, const hgm_ct* x, const hgm_ct* y, hgm_ct** out);
 int hgm_cmul(hgm_ctx* ctx, const hgm_ct* x, const int64_t* mask, size_t S, hgm_ct** out);
 int hgm_rot(hgm_ctx* ctx, const hgm_ct* x, int64_t offset, hgm_ct** out);
