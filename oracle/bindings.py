@@ -203,6 +203,8 @@ class RefLib:
             L.ref_blocked.restype = _int
             L.ref_blocked.argtypes = [_int, _vp, _sz, _vp, _sz, _vp, _sz, _vp, _sz, _sz, _vp, _sz, _sz, _i64, _vp,
                                       _vp]
+            L.ref_campaign.restype = _int
+            L.ref_campaign.argtypes = [_sz, _sz, _sz, _u64, _int, _sz, _i64, _vp, _vp, _vp, _vp, _vp]
             L.ref_oracle_session_create.restype = _vp
             L.ref_oracle_session_create.argtypes = [_int, _u64]
             L.ref_oracle_session_destroy.argtypes = [_vp]
@@ -227,6 +229,22 @@ class RefLib:
         if rc != 0:
             raise OracleError(f"rc={rc}: {cls._err()}")
         return C, st
+
+    @classmethod
+    def campaign(cls, cases, lo, hi, seed, algos_mask=7, slots=4096, modulus=65537):
+        """The reference's run_campaign over SlotBackend: (shapes[c,3], costs[c,k,2],
+        exact[c,k], stats[c,k,12], resampled), k over the algorithms in mask bit order."""
+        k = bin(algos_mask).count("1")
+        shapes = np.zeros((cases, 3), dtype=np.uint64)
+        costs = np.zeros((cases, k, 2), dtype=np.float64)
+        exact = np.zeros((cases, k), dtype=np.uint8)
+        stats = np.zeros((cases, k, 12), dtype=np.uint64)
+        res = np.zeros(1, dtype=np.uint64)
+        rc = cls.lib().ref_campaign(cases, lo, hi, seed, algos_mask, slots, modulus, _p(shapes), _p(costs),
+                                    _p(exact), _p(stats), _p(res))
+        if rc != 0:
+            raise OracleError(f"rc={rc}: {cls._err()}")
+        return shapes, costs, exact, stats, int(res[0])
 
     @classmethod
     def mm2(cls, A, B, algo="basic", order=-1, flags=0, slots=4096, modulus=65537):

@@ -25,6 +25,7 @@
 
 #include "bfv_oracle.h"
 #include "hegmm/algorithms.hpp"
+#include "hegmm/costmodel.hpp"
 #include "hegmm/backend.hpp"
 #include "hegmm/lintrans.hpp"
 #include "hegmm/matrix.hpp"
@@ -271,6 +272,51 @@ int rc_of(const std::exception& e) {
 extern "C" {
 
 const char* ref_last_error(void) { return g_err.c_str(); }
+
+// The reference's own run_campaign (costmodel.cpp:266-314) over SlotBackend{slots, modulus}:
+// shapes[c*3 + {0,1,2}] = m, l, n; per (case, algo) in algos_mask bit order (0 hegmm,
+// 1 hegmm-en, 2 square-pad): costs[2*k] client_ms, costs[2*k+1] cloud_ms, exact[k],
+// stats[12*k + 2*op + phase].
+int ref_campaign(std::size_t cases, std::size_t lo, std::size_t hi, std::uint64_t seed, int algos_mask,
+                 std::size_t slots, std::int64_t modulus, std::uint64_t* shapes, double* costs,
+                 std::uint8_t* exact, std::uint64_t* stats, std::uint64_t* resampled) {
+    try {
+        CampaignConfig cfg;
+        cfg.cases = cases;
+        cfg.dim_lo = lo;
+        cfg.dim_hi = hi;
+        cfg.seed = seed;
+        cfg.algos.clear();
+        const Algo all[3] = {Algo::Hegmm, Algo::HegmmEn, Algo::SquarePad};
+        for (int i = 0; i < 3; ++i)
+            if (algos_mask & (1 << i)) cfg.algos.push_back(all[i]);
+        cfg.slot_count = slots;
+        if (modulus > 0) cfg.plaintext_modulus = modulus;
+        const CampaignResult r = run_campaign(cfg);
+        std::size_t k = 0;
+        for (const CaseReport& c : r.cases) {
+            shapes[3 * c.index] = c.m;
+            shapes[3 * c.index + 1] = c.l;
+            shapes[3 * c.index + 2] = c.n;
+            for (const AlgoResult& a : c.results) {
+                costs[2 * k] = a.cost.client_ms;
+                costs[2 * k + 1] = a.cost.cloud_ms;
+                exact[k] = a.exact ? 1 : 0;
+                const PhaseCounts* pc[6] = {&a.stats.n_add, &a.stats.n_mult_cc, &a.stats.n_mult_cp,
+                                            &a.stats.n_rot, &a.stats.n_encrypt, &a.stats.n_decrypt};
+                for (int i = 0; i < 6; ++i) {
+                    stats[12 * k + 2 * i] = pc[i]->client;
+                    stats[12 * k + 2 * i + 1] = pc[i]->cloud;
+                }
+                ++k;
+            }
+        }
+        *resampled = r.resampled;
+        return 0;
+    } catch (const std::exception& e) {
+        return rc_of(e);
+    }
+}
 
 // Reference algorithm over the reference SlotBackend. modulus <= 0: none.
 int ref_mm(int algo, int order, const std::int64_t* A, std::size_t m, std::size_t l,
