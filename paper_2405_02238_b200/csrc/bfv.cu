@@ -947,7 +947,8 @@ Context::~Context() {
     cudaStreamSynchronize(stream_);
     for (auto& kv : keys_) cudaFree(kv.second);
     for (auto& kv : masks_)
-        for (auto& e : kv.second) cudaFree(e.dev);
+        for (auto& e : kv.second) cudaFreeAsync(e.dev, stream_);
+    cudaStreamSynchronize(stream_);
     cudaFree(d_sk_);
     cudaFree(d_pk_);
     cudaFree(dp_);
@@ -1045,14 +1046,21 @@ const u64* Context::mask_plain(const i64* mask, size_t S, u64 stable_id) {
     if (stable_id) {
         std::lock_guard<std::mutex> lk(mask_mu_);
         auto it = masks_by_id_.find(stable_id);
-        if (it != masks_by_id_.end()) return it->second;
+        if (it != masks_by_id_.end()) {
+            it->second->tick = ++mask_tick_;
+            return it->second->dev;
+        }
     }
     const u64 h = mask_hash(mask, S);
     std::lock_guard<std::mutex> lk(mask_mu_);
     auto& bucket = masks_[h];
     for (auto& e : bucket)
         if (e.content.size() == S && std::equal(e.content.begin(), e.content.end(), mask)) {
-            if (stable_id) masks_by_id_.emplace(stable_id, e.dev);
+            e.tick = ++mask_tick_;
+            if (stable_id) {
+                masks_by_id_.emplace(stable_id, &e);
+                e.ids.push_back(stable_id);
+            }
             return e.dev;
         }
     const u32 N = hp_.N, L = hp_.L;
@@ -1073,9 +1081,45 @@ const u64* Context::mask_plain(const i64* mask, size_t S, u64 stable_id) {
     ++launches_;
     release(m);
     HGM_CUDA(cudaGetLastError());
-    bucket.push_back(MaskEntry{std::vector<i64>(mask, mask + S), out});
-    if (stable_id) masks_by_id_.emplace(stable_id, out);
+    bucket.push_back(MaskEntry{std::vector<i64>(mask, mask + S), out, ++mask_tick_, {}});
+    mask_bytes_ += (size_t)L * N * 8;
+    if (stable_id) {
+        masks_by_id_.emplace(stable_id, &bucket.back());
+        bucket.back().ids.push_back(stable_id);
+    }
     return out;
+}
+
+size_t Context::mask_budget() const {
+    static const size_t env = [] {
+        const char* e = std::getenv("HGM_MASK_CACHE_MB");
+        return e ? (size_t)std::atoll(e) << 20 : (size_t)0;
+    }();
+    if (env) return env;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || total_b == 0) return (size_t)4 << 30;
+    return std::min<size_t>((size_t)8 << 30, total_b / 16);
+}
+
+void Context::trim_mask_cache() {
+    std::lock_guard<std::mutex> lk(mask_mu_);
+    const size_t budget = mask_budget();
+    if (mask_bytes_ <= budget) return;
+    std::vector<std::pair<u64, std::pair<u64, MaskEntry*>>> all;  // (tick, (hash, entry))
+    for (auto& kv : masks_)
+        for (auto& e : kv.second) all.push_back({e.tick, {kv.first, &e}});
+    std::sort(all.begin(), all.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    const size_t each = (size_t)hp_.L * hp_.N * 8;
+    for (auto& a : all) {
+        if (mask_bytes_ <= budget / 2) break;  // hysteresis: trim to half the budget
+        MaskEntry* e = a.second.second;
+        for (u64 id : e->ids) masks_by_id_.erase(id);
+        HGM_CUDA(cudaFreeAsync(e->dev, stream_));
+        auto& bucket = masks_[a.second.first];
+        bucket.remove_if([e](const MaskEntry& x) { return &x == e; });
+        if (bucket.empty()) masks_.erase(a.second.first);
+        mask_bytes_ -= each;
+    }
 }
 
 // ------------------------------------------------------------------ primitives

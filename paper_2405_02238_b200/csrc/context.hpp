@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <list>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -89,6 +90,11 @@ class Context {
     // ---------------------------------------------------------------- masks
     // NTT-domain centred lift of the batch-encoded mask over Q: [L][N].
     const u64* mask_plain(const i64* mask, size_t S, u64 stable_id = 0);
+    // Bounds the device mask cache (least recently used first) to mask_budget()
+    // bytes; called between programs (execute()), never while one holds mask
+    // pointers -- frees are stream-ordered behind the launches that used them.
+    void trim_mask_cache();
+    size_t mask_budget() const;
 
     // ---------------------------------------------------------------- primitives
     // host_vals[i] holds S[i] values; counters[i] is the encryption counter.
@@ -153,9 +159,13 @@ class Context {
     struct MaskEntry {
         std::vector<i64> content;
         u64* dev;
+        u64 tick = 0;            // last use (LRU)
+        std::vector<u64> ids;    // stable ids aliasing this entry
     };
-    std::unordered_map<u64, std::vector<MaskEntry>> masks_;
-    std::unordered_map<u64, const u64*> masks_by_id_;  // stable MaskData ids
+    std::unordered_map<u64, std::list<MaskEntry>> masks_;
+    std::unordered_map<u64, MaskEntry*> masks_by_id_;  // stable MaskData ids
+    u64 mask_tick_ = 0;
+    size_t mask_bytes_ = 0;
 };
 
 }  // namespace hgm

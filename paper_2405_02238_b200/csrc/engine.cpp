@@ -298,6 +298,7 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
     const size_t W = ctx.ct_words(), MW = ctx.modup_words(), PW = ctx.pending_words(), TW = ctx.tensor_words();
     g_counters = ExecCounters{};
     g_counters.levels = sch.levels.size();
+    ctx.trim_mask_cache();  // between programs: no mask pointer is held here yet
     std::vector<u64*> base(P.nodes.size(), nullptr);   // plain values
     std::vector<u64*> pbase(P.nodes.size(), nullptr);  // pending values [T][addend]
     auto ptr = [&](int node, int k) -> const u64* {

@@ -561,6 +561,7 @@ std::shared_ptr<MatmulProgram> build_enhanced(int order_opt, size_t m, size_t l,
 }
 
 std::mutex g_prog_mu;
+constexpr size_t kProgramCacheCap = 512;
 std::map<std::tuple<int, int, int, size_t, size_t, size_t, size_t, u32>, std::shared_ptr<const MatmulProgram>> g_progs;
 
 // reference square_pad_mm (algorithms.cpp:369-388): basic_mm on d x d operands
@@ -605,6 +606,9 @@ std::shared_ptr<const MatmulProgram> get_matmul_program(int algo, int order, siz
                                              : algo == 1 ? build_enhanced(order, m, l, n, slots, N, enc)
                                                          : build_square_pad(order, m, l, n, slots, N, enc);
     std::lock_guard<std::mutex> lk(g_prog_mu);
+    // bounded: a campaign over thousands of shapes must not keep every program
+    // (and its masks) alive; holders keep theirs through the shared_ptr
+    if (g_progs.size() >= kProgramCacheCap) g_progs.clear();
     return g_progs.emplace(key, p).first->second;
 }
 

@@ -22,6 +22,8 @@ VARIANTS = {
     "unfused-conv-finish": {"HGM_FUSED_CONV": "0", "HGM_FUSED_FINISH": "0"},
     "fused-tensor": {"HGM_FUSED_TENSOR": "1"},
     "tensor-without-intt-stage": {"HGM_TENSOR_S1": "0"},
+    # device mask cache bounded to 4 MB: masks are evicted between programs all the time
+    "small-mask-cache": {"HGM_MASK_CACHE_MB": "4"},
 }
 
 
