@@ -629,30 +629,30 @@ __global__ void k_tensor_s1(DevCtx cx, u32 n, const u64* const* A, const u64* co
 // d's range [off[d], off[d+1]) of tensor(a_i, b_i) over Q ++ B, NTT domain,
 // T: [3][L+nB][N] per destination.  a_i, b_i give the Q limbs; their B
 // extensions are XB + i * 4 nB N (k_q_to_b's layout).  init[d]: T[d] already
-// holds a partial sum to add to.  One thread per coefficient of one limb;
-// products accumulate in Karatsuba columns, reduced every 2 items (4 products
-// per column, the Cols bound).
+// holds a partial sum to add to.  One thread per coefficient of one limb.
+// Karatsuba on the tensor: x0 y1 + x1 y0 = (x0 + x1)(y0 + y1) - x0 y0 - x1 y1,
+// three products per item instead of four; products accumulate in Karatsuba
+// columns, reduced every kGroup items (the Cols / reduce_acc bounds: 4 products
+// of 60-bit residues, 16 of 55-bit ones) into running sums mod q.
 template <typename SH>
 __global__ void __launch_bounds__(kThreads, 4) k_tensor_acc(DevCtx cx, u32 n, const u32* off, const u64* const* A,
                                                              const u64* const* B, const u64* XB, u64* const* T,
                                                              const unsigned char* init) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = SH::L, K = SH::K, nB = SH::nB, D = L + nB;
+    constexpr u32 kGroup = SH::S == 30 ? 4 : 16;
     ITEM_LOOP {
         const u32 d = blockIdx.z;
         const Prime& P = dp->pr[d < L ? d : L + K + (d - L)];
+        const u64 q = P.q;
         const u32 i0 = off[item], i1 = off[item + 1];
         u64* t0 = T[item] + (size_t)d * N;
         u64* t1 = t0 + (size_t)D * N;
         u64* t2 = t1 + (size_t)D * N;
         const bool acc = init[item] != 0;
         COEF_LOOP {
-            Cols s0, s1, s2;
-            if (acc) {
-                s0.x = t0[j];
-                s1.x = t1[j];
-                s2.x = t2[j];
-            }
+            u64 p0 = 0, pm = 0, p2 = 0;
+            Cols s0, sm, s2;
             u32 since = 0;
             for (u32 i = i0; i < i1; ++i) {
                 const u64 *a0, *a1, *b0, *b1;
@@ -663,23 +663,30 @@ __global__ void __launch_bounds__(kThreads, 4) k_tensor_acc(DevCtx cx, u32 n, co
                     a0 = XB + ((size_t)i * 4 * nB + (d - L)) * N; a1 = a0 + (size_t)nB * N;
                     b0 = a1 + (size_t)nB * N; b1 = b0 + (size_t)nB * N;
                 }
-                const Dig<SH::S> x0 = split<SH::S>(a0[j]), x1 = split<SH::S>(a1[j]), y0 = split<SH::S>(b0[j]),
-                                 y1 = split<SH::S>(b1[j]);
-                s0.mac(x0, y0);
-                s1.mac(x0, y1);
-                s1.mac(x1, y0);
-                s2.mac(x1, y1);
-                if (++since == 2 && i + 1 < i1) {
-                    const u64 r0 = reduce_acc(s0.fold<SH::S>(), P), r1 = reduce_acc(s1.fold<SH::S>(), P),
-                              r2 = reduce_acc(s2.fold<SH::S>(), P);
-                    s0 = Cols{}; s1 = Cols{}; s2 = Cols{};
-                    s0.x = r0; s1.x = r1; s2.x = r2;
+                const u64 x0 = a0[j], x1 = a1[j], y0 = b0[j], y1 = b1[j];
+                s0.mac(split<SH::S>(x0), split<SH::S>(y0));
+                s2.mac(split<SH::S>(x1), split<SH::S>(y1));
+                sm.mac(split<SH::S>(add_mod(x0, x1, q)), split<SH::S>(add_mod(y0, y1, q)));
+                if (++since == kGroup && i + 1 < i1) {
+                    p0 = add_mod(p0, reduce_acc(s0.fold<SH::S>(), P), q);
+                    pm = add_mod(pm, reduce_acc(sm.fold<SH::S>(), P), q);
+                    p2 = add_mod(p2, reduce_acc(s2.fold<SH::S>(), P), q);
+                    s0 = Cols{}; sm = Cols{}; s2 = Cols{};
                     since = 0;
                 }
             }
-            t0[j] = reduce_acc(s0.fold<SH::S>(), P);
-            t1[j] = reduce_acc(s1.fold<SH::S>(), P);
-            t2[j] = reduce_acc(s2.fold<SH::S>(), P);
+            p0 = add_mod(p0, reduce_acc(s0.fold<SH::S>(), P), q);
+            pm = add_mod(pm, reduce_acc(sm.fold<SH::S>(), P), q);
+            p2 = add_mod(p2, reduce_acc(s2.fold<SH::S>(), P), q);
+            u64 p1 = sub_mod(sub_mod(pm, p0, q), p2, q);
+            if (acc) {
+                p0 = add_mod(p0, t0[j], q);
+                p1 = add_mod(p1, t1[j], q);
+                p2 = add_mod(p2, t2[j], q);
+            }
+            t0[j] = p0;
+            t1[j] = p1;
+            t2[j] = p2;
         }
     }
 }
