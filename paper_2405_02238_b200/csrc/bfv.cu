@@ -1178,34 +1178,38 @@ void Context::encrypt(int n, const i64* const* host_vals, const size_t* S, const
     HGM_CUDA(cudaGetLastError());
 }
 
+void Context::decrypt_to(int n, const u64* const* in, const size_t* S, u32* host) {
+    if (n <= 0) return;
+    const u32 N = hp_.N, L = hp_.L, H = N / 2;
+    for (int c0 = 0; c0 < n; c0 += kChunkDec) {
+        const int cn = std::min(kChunkDec, n - c0);
+        std::vector<const u64*> ins(in + c0, in + c0 + cn);
+        std::vector<u32> Sv(cn);
+        for (int i = 0; i < cn; ++i) Sv[i] = (u32)S[c0 + i];
+        const u64* const* din = upload(ins);
+        const u32* dS = upload(Sv);
+        u64* X = alloc((size_t)cn * L * N);
+        u64* M = alloc((size_t)cn * N);
+        u32* O = reinterpret_cast<u32*>(alloc(((size_t)cn * H + 1) / 2));
+        if (hp_.L == 3) k_dec_phase<ShapeQ3><<<grid_of(N, cn), kThreads, 0, stream_>>>(cx_, cn, din, d_sk_, X); else k_dec_phase<ShapeQ8><<<grid_of(N, cn), kThreads, 0, stream_>>>(cx_, cn, din, d_sk_, X); ++launches_;
+        ntt(false, jobs_contig(X, cn * L, 0, L));
+        if (hp_.L == 3) k_dec_round<ShapeQ3><<<grid_of(N, cn), kThreads, 0, stream_>>>(cx_, cn, X, M); else k_dec_round<ShapeQ8><<<grid_of(N, cn), kThreads, 0, stream_>>>(cx_, cn, X, M); ++launches_;
+        ntt(true, jobs_contig(M, cn, kTIndex, 1));
+        k_dec_gather<<<grid_of(H, cn), kThreads, 0, stream_>>>(cx_, cn, M, dS, O); ++launches_;
+        HGM_CUDA(cudaMemcpyAsync(host + (size_t)c0 * H, O, (size_t)cn * H * sizeof(u32), cudaMemcpyDeviceToHost,
+                                 stream_));
+        release(X);
+        release(M);
+        release(O);
+    }
+    HGM_CUDA(cudaGetLastError());
+}
+
 void Context::decrypt(int n, const u64* const* in, const size_t* S, i64* const* host_out) {
     if (n <= 0) return;
-    if (n > kChunkDec) {
-        for (int c0 = 0; c0 < n; c0 += kChunkDec) {
-            const int cn = std::min(kChunkDec, n - c0);
-            decrypt(cn, in + c0, S + c0, host_out + c0);
-        }
-        return;
-    }
-    const u32 N = hp_.N, L = hp_.L, H = N / 2;
-    std::vector<const u64*> ins(in, in + n);
-    std::vector<u32> Sv(n);
-    for (int i = 0; i < n; ++i) Sv[i] = (u32)S[i];
-    const u64* const* din = upload(ins);
-    const u32* dS = upload(Sv);
-    u64* X = alloc((size_t)n * L * N);
-    u64* M = alloc((size_t)n * N);
-    u32* O = reinterpret_cast<u32*>(alloc(((size_t)n * H + 1) / 2));
-    if (hp_.L == 3) k_dec_phase<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, din, d_sk_, X); else k_dec_phase<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, din, d_sk_, X); ++launches_;
-    ntt(false, jobs_contig(X, n * L, 0, L));
-    if (hp_.L == 3) k_dec_round<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, X, M); else k_dec_round<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, X, M); ++launches_;
-    ntt(true, jobs_contig(M, n, kTIndex, 1));
-    k_dec_gather<<<grid_of(H, n), kThreads, 0, stream_>>>(cx_, n, M, dS, O); ++launches_;
+    const u32 H = hp_.N / 2;
     const u32* host = static_cast<const u32*>(download_buffer((size_t)n * H * sizeof(u32)));
-    HGM_CUDA(cudaMemcpyAsync((void*)host, O, (size_t)n * H * sizeof(u32), cudaMemcpyDeviceToHost, stream_));
-    release(X);
-    release(M);
-    release(O);
+    decrypt_to(n, in, S, const_cast<u32*>(host));
     sync();
     parallel_for((size_t)n, [&](size_t i) {
         const u32* src = host + i * H;

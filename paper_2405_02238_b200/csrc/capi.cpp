@@ -555,36 +555,77 @@ void run_instances(Context& ctx, const MatmulProgram& prog, size_t count,
         return p;
     };
     std::future<Packed> next = std::async(std::launch::async, pack_chunk, (size_t)0);
-    std::future<void> unpacking;
-    for (size_t c0 = 0; c0 < count; c0 += chunk) {
-        const int K = (int)std::min(chunk, count - c0);
-        Packed packed = next.get();
-        if (c0 + chunk < count) next = std::async(std::launch::async, pack_chunk, c0 + chunk);
-        ExecIO io;
-        io.K = K;
-        io.input = [](int, int) -> const u64* { return nullptr; };
-        io.enc_values = [&](int s, int k) { return (const i64*)packed[k][s].data(); };
-        io.enc_counter = [&](int s, int k) { return base_of(c0 + k) + (u64)s; };
-        std::vector<u64*> res = execute(ctx, prog.sched, io);
-        std::vector<const u64*> cts(K);
-        std::vector<size_t> S(K, prog.segment);
-        std::vector<std::vector<i64>> outv(K, std::vector<i64>(prog.segment));
-        std::vector<i64*> outp(K);
-        for (int k = 0; k < K; ++k) {
-            cts[k] = res[0] + (size_t)k * W;
-            outp[k] = outv[k].data();
-        }
-        ctx.decrypt(K, cts.data(), S.data(), outp.data());
-        if (final_words)
-            HGM_CUDA(cudaMemcpy(final_words + c0 * W, res[0], (size_t)K * W * 8, cudaMemcpyDeviceToHost));
-        for (u64* r : res) ctx.release(r);
-        if (unpacking.valid()) unpacking.get();
-        unpacking = std::async(std::launch::async, [&prog, &c_of, c0, K, outv = std::move(outv)]() {
-            parallel_for((size_t)K, [&](size_t k) { prog.unpack(outv[k], c_of(c0 + k)); }, 4);
-        });
+    // Decrypted slots of chunk i land in pinned slot i % 2 asynchronously; the host
+    // enqueues chunk i + 1 before waiting for them, so the GPU never idles at a
+    // chunk boundary (the export path copies the final words synchronously).
+    const size_t H = ctx.slots();
+    struct Slot {
+        u32* host = nullptr;
+        cudaEvent_t ev = nullptr;
+        std::future<void> unpacking;
+    };
+    Slot slot[2];
+    for (Slot& sl : slot) {
+        HGM_CUDA(cudaMallocHost((void**)&sl.host, std::max<size_t>(1, chunk * H * sizeof(u32))));
+        HGM_CUDA(cudaEventCreateWithFlags(&sl.ev, cudaEventDisableTiming));
     }
-    if (unpacking.valid()) unpacking.get();
+    auto finish = [&](Slot& sl, size_t c0, int K) {
+        sl.unpacking = std::async(std::launch::async, [&prog, &c_of, &sl, c0, K, H, seg = prog.segment]() {
+            HGM_CUDA(cudaEventSynchronize(sl.ev));
+            parallel_for((size_t)K, [&](size_t k) {
+                std::vector<i64> v(seg);
+                const u32* src = sl.host + k * H;
+                for (size_t j = 0; j < seg; ++j) v[j] = (i64)src[j];
+                prog.unpack(v, c_of(c0 + k));
+            }, 4);
+        });
+    };
+    auto drain = [&]() {
+        for (Slot& sl : slot)
+            if (sl.unpacking.valid()) sl.unpacking.get();
+    };
+    try {
+        size_t i = 0;
+        for (size_t c0 = 0; c0 < count; c0 += chunk, ++i) {
+            const int K = (int)std::min(chunk, count - c0);
+            Packed packed = next.get();
+            if (c0 + chunk < count) next = std::async(std::launch::async, pack_chunk, c0 + chunk);
+            ExecIO io;
+            io.K = K;
+            io.input = [](int, int) -> const u64* { return nullptr; };
+            io.enc_values = [&](int s, int k) { return (const i64*)packed[k][s].data(); };
+            io.enc_counter = [&](int s, int k) { return base_of(c0 + k) + (u64)s; };
+            std::vector<u64*> res = execute(ctx, prog.sched, io);
+            std::vector<const u64*> cts(K);
+            std::vector<size_t> S(K, prog.segment);
+            for (int k = 0; k < K; ++k) cts[k] = res[0] + (size_t)k * W;
+            Slot& sl = slot[i % 2];
+            if (sl.unpacking.valid()) sl.unpacking.get();  // chunk i - 2 is out of this slot
+            ctx.decrypt_to(K, cts.data(), S.data(), sl.host);
+            HGM_CUDA(cudaEventRecord(sl.ev, ctx.stream()));
+            if (final_words) {  // stream-ordered (the library stream does not sync with the legacy one)
+                HGM_CUDA(cudaMemcpyAsync(final_words + c0 * W, res[0], (size_t)K * W * 8, cudaMemcpyDeviceToHost,
+                                         ctx.stream()));
+                ctx.sync();
+            }
+            for (u64* r : res) ctx.release(r);
+            finish(sl, c0, K);
+        }
+        drain();
+    } catch (...) {
+        try { drain(); } catch (...) {}
+        ctx.sync();
+        for (Slot& sl : slot) {
+            cudaFreeHost(sl.host);
+            cudaEventDestroy(sl.ev);
+        }
+        throw;
+    }
     ctx.sync();
+    for (Slot& sl : slot) {
+        cudaFreeHost(sl.host);
+        cudaEventDestroy(sl.ev);
+    }
 }
 
 void put_counts(const MatmulProgram& prog, uint64_t* stats) {

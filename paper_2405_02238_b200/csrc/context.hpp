@@ -102,6 +102,9 @@ class Context {
                  u64* const* out);
     // Decrypts n ciphertexts into host buffers (synchronises the stream).
     void decrypt(int n, const u64* const* in, const size_t* S, i64* const* host_out);
+    // Enqueues the decryption of n ciphertexts into pinned host memory (N/2 u32
+    // slots per ciphertext, values in [0, t)); valid once the stream reaches it.
+    void decrypt_to(int n, const u64* const* in, const size_t* S, u32* pinned_host);
     void add(int n, const u64* const* a, const u64* const* b, u64* const* out);
     // out[o] = sum over terms t in [off[o], off[o+1]) of in[t] (.* mask[t] if set)
     void lincomb(int n_out, const u32* off, const u64* const* in, const u64* const* mask,
