@@ -321,8 +321,10 @@ def main():
             e2e_times.append(time.perf_counter() - t0)
         e2e_total = max_over_ranks(sum(e2e_times))
         assert np.array_equal(Ce[0], (A[0] @ B[0]) % 65537)
-        h2d = args.instances * E * (ctx.slot_count * 8)  # packed slot vectors uploaded for encryption
-        d2h = args.instances * facts["segment"] * 8      # decrypted slot vectors read back
+        # bytes the library moves: slot vectors go up as u32 residues mod t (N/2 per
+        # encryption, pinned staging) and decrypted rows come back as N/2 u32 each
+        h2d = args.instances * E * ctx.slot_count * 4
+        d2h = args.instances * ctx.slot_count * 4
         e2e = {"value": args.instances * args.steps / e2e_total, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "path": "hgm_matmul_batch (C ABI): host int64 A,B -> host C, incl. client encrypt/decrypt"}
