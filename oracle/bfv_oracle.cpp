@@ -460,11 +460,12 @@ const KsKey& get_key(orc_ctx& c, u64 kid) {
 
 // Hybrid key switching of a coefficient-domain polynomial d (L limbs, mod Q).
 // Returns (u0, u1) over Q in the NTT domain.
-void key_switch(orc_ctx& c, const std::vector<Poly>& d, u64 kid, std::vector<Poly>& u0,
-                std::vector<Poly>& u1) {
+// The key-switch accumulator before ModDown: (acc0, acc1) over Q ++ P, NTT domain.
+void ks_acc(orc_ctx& c, const std::vector<Poly>& d, u64 kid, std::vector<Poly>& acc0, std::vector<Poly>& acc1) {
     const KsKey& key = get_key(c, kid);
-    const unsigned N = c.N, L = c.L, K = c.K, R = c.R(), A = c.alpha;
-    std::vector<Poly> acc0(R, Poly(N, 0)), acc1(R, Poly(N, 0));
+    const unsigned N = c.N, L = c.L, R = c.R(), A = c.alpha;
+    acc0.assign(R, Poly(N, 0));
+    acc1.assign(R, Poly(N, 0));
     for (unsigned dg = 0; dg < c.dnum; ++dg) {
         // centred digit residues y_i = [d_i (Q_d/q_i)^-1]_{q_i}
         std::vector<std::vector<i64>> y(A, std::vector<i64>(N));
@@ -493,7 +494,12 @@ void key_switch(orc_ctx& c, const std::vector<Poly>& d, u64 kid, std::vector<Pol
             }
         }
     }
-    auto moddown = [&](std::vector<Poly>& acc, std::vector<Poly>& out) {
+}
+
+// ModDown: round(acc / P) over Q, NTT domain in and out.
+void moddown(const orc_ctx& c, const std::vector<Poly>& acc, std::vector<Poly>& out) {
+    const unsigned N = c.N, L = c.L, K = c.K;
+    {
         std::vector<Poly> w(K);
         for (unsigned k = 0; k < K; ++k) { w[k] = acc[L + k]; ntt_inv(w[k], c.pr[L + k]); }
         out.assign(L, Poly(N));
@@ -513,9 +519,17 @@ void key_switch(orc_ctx& c, const std::vector<Poly>& d, u64 kid, std::vector<Pol
             for (unsigned j = 0; j < N; ++j)
                 out[i][j] = mulmod(submod(acc[i][j], conv[j], q), c.P_inv_q[i], q);
         }
-    };
-    moddown(acc0, u0);
-    moddown(acc1, u1);
+    }
+}
+
+// Hybrid key switching of a coefficient-domain polynomial d (L limbs, mod Q).
+// Returns (u0, u1) over Q in the NTT domain.
+void key_switch(orc_ctx& c, const std::vector<Poly>& d, u64 kid, std::vector<Poly>& u0,
+                std::vector<Poly>& u1) {
+    std::vector<Poly> acc0, acc1;
+    ks_acc(c, d, kid, acc0, acc1);
+    moddown(c, acc0, u0);
+    moddown(c, acc1, u1);
 }
 
 struct Ct {
@@ -637,31 +651,6 @@ Ct cmult(const orc_ctx& c, const Ct& a, const int64_t* mask, size_t S) {
     return o;
 }
 
-Ct rot(orc_ctx& c, const Ct& a, i64 z) {
-    const i64 H = c.N / 2;
-    i64 zz = ((z % H) + H) % H;
-    if (zz == 0) return a;
-    const u64 g = powmod(3, (u64)zz, 2 * (u64)c.N);
-    std::vector<Poly> c0(c.L), c1(c.L);
-    for (unsigned i = 0; i < c.L; ++i) {
-        Poly t0 = a.c0[i], t1 = a.c1[i];
-        ntt_inv(t0, c.pr[i]); ntt_inv(t1, c.pr[i]);
-        c0[i] = automorph_coeff(t0, g, c.pr[i].q);
-        c1[i] = automorph_coeff(t1, g, c.pr[i].q);
-        ntt_fwd(c0[i], c.pr[i]);
-    }
-    std::vector<Poly> u0, u1;
-    key_switch(c, c1, g, u0, u1);
-    Ct o;
-    o.c0.resize(c.L); o.c1 = u1;
-    for (unsigned i = 0; i < c.L; ++i) {
-        const u64 q = c.pr[i].q;
-        o.c0[i].resize(c.N);
-        for (unsigned j = 0; j < c.N; ++j) o.c0[i][j] = addmod(c0[i][j], u0[i][j], q);
-    }
-    return o;
-}
-
 // exact Q -> B conversion of a coefficient-domain polynomial (centred lift)
 std::vector<Poly> q_to_b(const orc_ctx& c, const std::vector<Poly>& x) {
     const unsigned N = c.N, L = c.L, nB = c.nB;
@@ -753,56 +742,82 @@ Tensor tensor_of(const orc_ctx& c, const Ct& x, const Ct& y) {
     return T;
 }
 
-// A ciphertext value: plain (c0, c1), or a PENDING product -- a sum of
-// tensors not yet scaled and relinearised, plus a plain addend.  Semantics
-// (the GPU library follows them exactly):
-//   he_mult(x, y)     -> pending {T = tensor(plain(x), plain(y)), addend 0}
-//   he_add(x, y)      -> pending {T_x + T_y, addend_x + addend_y} when either
-//                        is pending (a plain operand is an addend), else plain
-//   anything else     -> consumes plain(x)
-//   plain(pending)    =  round(t/Q * T) relinearised, + addend   (materialise)
-// Sums of products are therefore scaled and relinearised once, not once per
-// product: the decrypted value is the same, the noise smaller (one rounding).
+// A ciphertext value has up to three parts, and its plain value is their sum:
+//   X  a plain (c0, c1) over Q                         (always present, may be 0)
+//   T  a PENDING PRODUCT: a sum of unscaled tensors over Q ++ B; its plain value
+//      is round(t/Q * T) relinearised
+//   A  a PENDING KEY SWITCH: a sum of key-switch accumulators over Q ++ P (NTT
+//      domain) of rotations, P phi(c0) folded in; its plain value is ModDown(A)
+// Semantics (the GPU library follows them exactly):
+//   he_mult(x, y)  -> {T = tensor(plain(x), plain(y))}
+//   he_rot(x, z)   -> {A = KS_g(phi(plain(x).c1)) + P phi(plain(x).c0)}  (z = 0: {X = plain(x)})
+//   he_cmult(x, m) -> {X = m X, A = m A}; if x has T: {X = m plain(x)}
+//   he_add(x, y)   -> partwise sum
+//   decrypt, export, and every other reader use plain(x).
+// A lone rotation or product materialises to exactly the eager result (ModDown
+// of A + P y is ModDown(A) + y), while sums of products and masked sums of
+// rotations are scaled, relinearised or moded down once instead of per term.
+enum : int { kPartT = 1, kPartA = 2 };
 struct XCt {
-    Ct add;           // plain value, or the pending value's addend
-    bool pending = false;
-    Tensor T;         // pending only
+    Ct add;                  // X
+    bool pending = false;    // T present
+    Tensor T;
+    bool ks = false;         // A present
+    std::vector<Poly> A0, A1;  // R limbs each
+    int kind() const { return (pending ? kPartT : 0) | (ks ? kPartA : 0); }
 };
-
-Ct materialize(orc_ctx& c, const XCt& x) {
-    if (!x.pending) return x.add;
-    const unsigned N = c.N, L = c.L, nB = c.nB;
-    std::vector<Poly> tq[3], tb[3];
-    for (int t = 0; t < 3; ++t) {
-        tq[t].assign(x.T.t[t].begin(), x.T.t[t].begin() + L);
-        tb[t].assign(x.T.t[t].begin() + L, x.T.t[t].end());
-        for (unsigned i = 0; i < L; ++i) ntt_inv(tq[t][i], c.pr[i]);
-        for (unsigned k = 0; k < nB; ++k) ntt_inv(tb[t][k], c.pr[c.bidx(k)]);
-    }
-    std::vector<Poly> e0 = scale_round(c, tq[0], tb[0]);
-    std::vector<Poly> e1 = scale_round(c, tq[1], tb[1]);
-    std::vector<Poly> e2 = scale_round(c, tq[2], tb[2]);
-    std::vector<Poly> u0, u1;
-    key_switch(c, e2, 0, u0, u1);
-    Ct o;
-    o.c0.resize(L); o.c1.resize(L);
-    for (unsigned i = 0; i < L; ++i) {
-        const u64 q = c.pr[i].q;
-        ntt_fwd(e0[i], c.pr[i]); ntt_fwd(e1[i], c.pr[i]);
-        o.c0[i].resize(N); o.c1[i].resize(N);
-        for (unsigned j = 0; j < N; ++j) {
-            o.c0[i][j] = addmod(addmod(e0[i][j], u0[i][j], q), x.add.c0[i][j], q);
-            o.c1[i][j] = addmod(addmod(e1[i][j], u1[i][j], q), x.add.c1[i][j], q);
-        }
-    }
-    return o;
-}
 
 Ct zero_ct(const orc_ctx& c) {
     Ct z;
     z.c0.assign(c.L, Poly(c.N, 0));
     z.c1.assign(c.L, Poly(c.N, 0));
     return z;
+}
+
+Ct materialize(orc_ctx& c, const XCt& x) {
+    const unsigned N = c.N, L = c.L, nB = c.nB;
+    Ct o = x.add;
+    if (x.pending) {
+        std::vector<Poly> tq[3], tb[3];
+        for (int t = 0; t < 3; ++t) {
+            tq[t].assign(x.T.t[t].begin(), x.T.t[t].begin() + L);
+            tb[t].assign(x.T.t[t].begin() + L, x.T.t[t].end());
+            for (unsigned i = 0; i < L; ++i) ntt_inv(tq[t][i], c.pr[i]);
+            for (unsigned k = 0; k < nB; ++k) ntt_inv(tb[t][k], c.pr[c.bidx(k)]);
+        }
+        std::vector<Poly> e0 = scale_round(c, tq[0], tb[0]);
+        std::vector<Poly> e1 = scale_round(c, tq[1], tb[1]);
+        std::vector<Poly> e2 = scale_round(c, tq[2], tb[2]);
+        std::vector<Poly> u0, u1;
+        key_switch(c, e2, 0, u0, u1);
+        for (unsigned i = 0; i < L; ++i) {
+            const u64 q = c.pr[i].q;
+            ntt_fwd(e0[i], c.pr[i]); ntt_fwd(e1[i], c.pr[i]);
+            for (unsigned j = 0; j < N; ++j) {
+                o.c0[i][j] = addmod(addmod(e0[i][j], u0[i][j], q), o.c0[i][j], q);
+                o.c1[i][j] = addmod(addmod(e1[i][j], u1[i][j], q), o.c1[i][j], q);
+            }
+        }
+    }
+    if (x.ks) {
+        std::vector<Poly> m0, m1;
+        moddown(c, x.A0, m0);
+        moddown(c, x.A1, m1);
+        for (unsigned i = 0; i < L; ++i) {
+            const u64 q = c.pr[i].q;
+            for (unsigned j = 0; j < N; ++j) {
+                o.c0[i][j] = addmod(o.c0[i][j], m0[i][j], q);
+                o.c1[i][j] = addmod(o.c1[i][j], m1[i][j], q);
+            }
+        }
+    }
+    return o;
+}
+
+XCt plain_x(const Ct& v) {
+    XCt o;
+    o.add = v;
+    return o;
 }
 
 XCt mult_pending(const orc_ctx& c, const Ct& x, const Ct& y) {
@@ -813,51 +828,147 @@ XCt mult_pending(const orc_ctx& c, const Ct& x, const Ct& y) {
     return o;
 }
 
+// rotation as a pending key switch (z = 0: the plain operand)
+XCt rot_x(orc_ctx& c, const Ct& a, i64 z) {
+    const i64 H = c.N / 2;
+    const i64 zz = ((z % H) + H) % H;
+    if (zz == 0) return plain_x(a);
+    const u64 g = powmod(3, (u64)zz, 2 * (u64)c.N);
+    std::vector<Poly> c0(c.L), c1(c.L);
+    for (unsigned i = 0; i < c.L; ++i) {
+        Poly t0 = a.c0[i], t1 = a.c1[i];
+        ntt_inv(t0, c.pr[i]); ntt_inv(t1, c.pr[i]);
+        c0[i] = automorph_coeff(t0, g, c.pr[i].q);
+        c1[i] = automorph_coeff(t1, g, c.pr[i].q);
+        ntt_fwd(c0[i], c.pr[i]);
+    }
+    XCt o;
+    o.add = zero_ct(c);
+    o.ks = true;
+    ks_acc(c, c1, g, o.A0, o.A1);
+    for (unsigned i = 0; i < c.L; ++i) {  // + P phi(c0): ModDown(A + P y) = ModDown(A) + y
+        const u64 q = c.pr[i].q;
+        for (unsigned j = 0; j < c.N; ++j) o.A0[i][j] = addmod(o.A0[i][j], mulmod(c.P_mod_r[i], c0[i][j], q), q);
+    }
+    return o;
+}
+
+// mask over Q ++ P (NTT domain) for masking pending key switches
+std::vector<Poly> mask_qp(const orc_ctx& c, const int64_t* mask, size_t S) {
+    Poly m = encode(c, mask, S);
+    std::vector<Poly> out(c.R());
+    for (unsigned r = 0; r < c.R(); ++r) {
+        const u64 q = c.pr[r].q;
+        out[r].resize(c.N);
+        for (unsigned j = 0; j < c.N; ++j) out[r][j] = from_signed(centred(m[j], kT), q);
+        ntt_fwd(out[r], c.pr[r]);
+    }
+    return out;
+}
+
+XCt cmult_x(orc_ctx& c, const XCt& v, const int64_t* mask, size_t S) {
+    XCt o;
+    if (v.pending) {  // a pending product is materialised (with every other part) first
+        o.add = cmult(c, materialize(c, v), mask, S);
+        return o;
+    }
+    o.add = cmult(c, v.add, mask, S);
+    if (v.ks) {
+        const std::vector<Poly> m = mask_qp(c, mask, S);
+        o.ks = true;
+        o.A0 = v.A0;
+        o.A1 = v.A1;
+        for (unsigned r = 0; r < c.R(); ++r) {
+            const u64 q = c.pr[r].q;
+            for (unsigned j = 0; j < c.N; ++j) {
+                o.A0[r][j] = mulmod(o.A0[r][j], m[r][j], q);
+                o.A1[r][j] = mulmod(o.A1[r][j], m[r][j], q);
+            }
+        }
+    }
+    return o;
+}
+
 XCt add_any(const orc_ctx& c, const XCt& a, const XCt& b) {
     XCt o;
     o.add = add(c, a.add, b.add);
     o.pending = a.pending || b.pending;
-    if (!o.pending) return o;
-    const unsigned L = c.L, D = c.L + c.nB;
-    const XCt& p = a.pending ? a : b;
-    o.T = p.T;
-    if (a.pending && b.pending)
-        for (int t = 0; t < 3; ++t)
-            for (unsigned r = 0; r < D; ++r) {
-                const u64 q = r < L ? c.pr[r].q : c.pr[c.bidx(r - L)].q;
-                for (unsigned j = 0; j < c.N; ++j) o.T.t[t][r][j] = addmod(a.T.t[t][r][j], b.T.t[t][r][j], q);
+    if (o.pending) {
+        const unsigned L = c.L, D = c.L + c.nB;
+        const XCt& p = a.pending ? a : b;
+        o.T = p.T;
+        if (a.pending && b.pending)
+            for (int t = 0; t < 3; ++t)
+                for (unsigned r = 0; r < D; ++r) {
+                    const u64 q = r < L ? c.pr[r].q : c.pr[c.bidx(r - L)].q;
+                    for (unsigned j = 0; j < c.N; ++j) o.T.t[t][r][j] = addmod(a.T.t[t][r][j], b.T.t[t][r][j], q);
+                }
+    }
+    o.ks = a.ks || b.ks;
+    if (o.ks) {
+        const XCt& p = a.ks ? a : b;
+        o.A0 = p.A0;
+        o.A1 = p.A1;
+        if (a.ks && b.ks)
+            for (unsigned r = 0; r < c.R(); ++r) {
+                const u64 q = c.pr[r].q;
+                for (unsigned j = 0; j < c.N; ++j) {
+                    o.A0[r][j] = addmod(a.A0[r][j], b.A0[r][j], q);
+                    o.A1[r][j] = addmod(a.A1[r][j], b.A1[r][j], q);
+                }
             }
+    }
     return o;
 }
 
-// Eager product (a pending product materialised at once).
+// Eager product / rotation (a pending value materialised at once).
 Ct mult(orc_ctx& c, const Ct& x, const Ct& y) { return materialize(c, mult_pending(c, x, y)); }
+Ct rot(orc_ctx& c, const Ct& a, i64 z) { return materialize(c, rot_x(c, a, z)); }
 
-// pending buffer: [addend: 2 L N words][T: 3 (L + nB) N words]
-size_t pending_words(const orc_ctx& c) { return (size_t)2 * c.L * c.N + (size_t)3 * (c.L + c.nB) * c.N; }
-XCt load_x(const orc_ctx& c, const uint64_t* buf, int pending) {
+// value buffer: [X: 2 L N][T: 3 (L + nB) N][A: 2 R N], parts valid per kind bits
+size_t pending_words(const orc_ctx& c) {
+    return (size_t)2 * c.L * c.N + (size_t)3 * (c.L + c.nB) * c.N + (size_t)2 * c.R() * c.N;
+}
+XCt load_x(const orc_ctx& c, const uint64_t* buf, int kind) {
     XCt x;
     x.add = load(c, buf);
-    x.pending = pending != 0;
-    if (!x.pending) return x;
-    const unsigned D = c.L + c.nB;
+    x.pending = (kind & kPartT) != 0;
+    x.ks = (kind & kPartA) != 0;
+    const unsigned D = c.L + c.nB, R = c.R();
     const uint64_t* t = buf + (size_t)2 * c.L * c.N;
-    for (int k = 0; k < 3; ++k) {
-        x.T.t[k].resize(D);
-        for (unsigned r = 0; r < D; ++r) {
-            const uint64_t* p = t + ((size_t)k * D + r) * c.N;
-            x.T.t[k][r].assign(p, p + c.N);
+    if (x.pending)
+        for (int k = 0; k < 3; ++k) {
+            x.T.t[k].resize(D);
+            for (unsigned r = 0; r < D; ++r) {
+                const uint64_t* p = t + ((size_t)k * D + r) * c.N;
+                x.T.t[k][r].assign(p, p + c.N);
+            }
+        }
+    const uint64_t* a = t + (size_t)3 * D * c.N;
+    if (x.ks) {
+        x.A0.resize(R);
+        x.A1.resize(R);
+        for (unsigned r = 0; r < R; ++r) {
+            x.A0[r].assign(a + (size_t)r * c.N, a + (size_t)(r + 1) * c.N);
+            x.A1[r].assign(a + (size_t)(R + r) * c.N, a + (size_t)(R + r + 1) * c.N);
         }
     }
     return x;
 }
 void store_x(const orc_ctx& c, const XCt& x, uint64_t* buf) {
     store(c, x.add, buf);
-    if (!x.pending) return;
-    const unsigned D = c.L + c.nB;
+    if (!x.pending && !x.ks) return;
+    const unsigned D = c.L + c.nB, R = c.R();
     uint64_t* t = buf + (size_t)2 * c.L * c.N;
-    for (int k = 0; k < 3; ++k)
-        for (unsigned r = 0; r < D; ++r) std::memcpy(t + ((size_t)k * D + r) * c.N, x.T.t[k][r].data(), c.N * 8);
+    if (x.pending)
+        for (int k = 0; k < 3; ++k)
+            for (unsigned r = 0; r < D; ++r) std::memcpy(t + ((size_t)k * D + r) * c.N, x.T.t[k][r].data(), c.N * 8);
+    uint64_t* a = t + (size_t)3 * D * c.N;
+    if (x.ks)
+        for (unsigned r = 0; r < R; ++r) {
+            std::memcpy(a + (size_t)r * c.N, x.A0[r].data(), c.N * 8);
+            std::memcpy(a + (size_t)(R + r) * c.N, x.A1[r].data(), c.N * 8);
+        }
 }
 
 template <typename F>
@@ -931,12 +1042,29 @@ size_t orc_pending_words(const orc_ctx* c) { return pending_words(*c); }
 int orc_mult_pending(orc_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t* out) {
     return guarded([&] { store_x(*c, mult_pending(*c, load(*c, a), load(*c, b)), out); });
 }
-int orc_add_any(orc_ctx* c, const uint64_t* a, int a_pending, const uint64_t* b, int b_pending, uint64_t* out) {
-    return guarded([&] { store_x(*c, add_any(*c, load_x(*c, a, a_pending), load_x(*c, b, b_pending)), out); });
+int orc_add_any(orc_ctx* c, const uint64_t* a, int a_kind, const uint64_t* b, int b_kind, uint64_t* out) {
+    return guarded([&] { store_x(*c, add_any(*c, load_x(*c, a, a_kind), load_x(*c, b, b_kind)), out); });
 }
-int orc_materialize(orc_ctx* c, const uint64_t* x, uint64_t* out) {
-    return guarded([&] { store(*c, materialize(*c, load_x(*c, x, 1)), out); });
+int orc_rot_x(orc_ctx* c, const uint64_t* a, int64_t z, uint64_t* out, int* out_kind) {
+    return guarded([&] {
+        const XCt x = rot_x(*c, load(*c, a), z);
+        store_x(*c, x, out);
+        *out_kind = x.kind();
+    });
 }
+int orc_cmult_x(orc_ctx* c, const uint64_t* a, int a_kind, const int64_t* mask, size_t S, uint64_t* out,
+                int* out_kind) {
+    return guarded([&] {
+        check_segment(*c, S);
+        const XCt x = cmult_x(*c, load_x(*c, a, a_kind), mask, S);
+        store_x(*c, x, out);
+        *out_kind = x.kind();
+    });
+}
+int orc_materialize_kind(orc_ctx* c, const uint64_t* x, int kind, uint64_t* out) {
+    return guarded([&] { store(*c, materialize(*c, load_x(*c, x, kind)), out); });
+}
+int orc_materialize(orc_ctx* c, const uint64_t* x, uint64_t* out) { return orc_materialize_kind(c, x, kPartT, out); }
 
 double orc_noise_budget(orc_ctx* c, const uint64_t* ct) {
     std::vector<u128> ph = scaled_phase(*c, load(*c, ct));

@@ -56,6 +56,9 @@ class Oracle:
                 "orc_mult_pending": [_vp, _vp, _vp, _vp],
                 "orc_add_any": [_vp, _vp, _int, _vp, _int, _vp],
                 "orc_materialize": [_vp, _vp, _vp],
+                "orc_materialize_kind": [_vp, _vp, _int, _vp],
+                "orc_rot_x": [_vp, _vp, _i64, _vp, _vp],
+                "orc_cmult_x": [_vp, _vp, _int, _vp, _sz, _vp, _vp],
                 "orc_ntt_fwd": [_vp, _int, _vp],
                 "orc_ntt_inv": [_vp, _int, _vp],
                 "orc_encode": [_vp, _vp, _sz, _vp],
@@ -129,28 +132,45 @@ class Oracle:
         self._chk(self.lib().orc_mult(self._h, _p(a), _p(b), _p(out)))
         return out
 
-    # Pending products (bfv_oracle.cpp XCt): he_mult returns an unscaled,
-    # unrelinearised tensor that he_add accumulates; plain() materialises.
-    # Values here are (words, is_pending) pairs.
+    # Values with parts (bfv_oracle.cpp XCt): (words, kind), kind bits 1 = pending
+    # product, 2 = pending key switch (0: plain words).  he_mult / he_rot /
+    # he_cmult / he_add in this form are mult_pending / rot_x / cmult_x / add_any;
+    # plain() materialises.
+    def _full(self):
+        return np.zeros(int(self.lib().orc_pending_words(self._h)), dtype=np.uint64)
+
     def mult_pending(self, a, b):
-        out = np.zeros(int(self.lib().orc_pending_words(self._h)), dtype=np.uint64)
+        out = self._full()
         self._chk(self.lib().orc_mult_pending(self._h, _p(a), _p(b), _p(out)))
-        return (out, True)
+        return (out, 1)
 
     def add_any(self, x, y):
-        (a, pa), (b, pb) = x, y
-        n = int(self.lib().orc_pending_words(self._h)) if (pa or pb) else self.words
-        out = np.zeros(n, dtype=np.uint64)
-        self._chk(self.lib().orc_add_any(self._h, _p(np.ascontiguousarray(a)), int(pa),
-                                         _p(np.ascontiguousarray(b)), int(pb), _p(out)))
-        return (out, bool(pa or pb))
+        (a, ka), (b, kb) = x, y
+        k = int(ka) | int(kb)
+        out = self._full() if k else self._ct()
+        self._chk(self.lib().orc_add_any(self._h, _p(np.ascontiguousarray(a)), int(ka),
+                                         _p(np.ascontiguousarray(b)), int(kb), _p(out)))
+        return (out, k)
+
+    def rot_x(self, a, z: int):
+        out, k = self._full(), ctypes.c_int(0)
+        self._chk(self.lib().orc_rot_x(self._h, _p(np.ascontiguousarray(a)), int(z), _p(out), ctypes.byref(k)))
+        return (out if k.value else out[: self.words].copy(), k.value)
+
+    def cmult_x(self, x, mask):
+        a, ka = x
+        m = np.ascontiguousarray(mask, dtype=np.int64)
+        out, k = self._full(), ctypes.c_int(0)
+        self._chk(self.lib().orc_cmult_x(self._h, _p(np.ascontiguousarray(a)), int(ka), _p(m), m.size, _p(out),
+                                         ctypes.byref(k)))
+        return (out if k.value else out[: self.words].copy(), k.value)
 
     def plain(self, x):
-        w, pend = x
-        if not pend:
-            return w
+        w, k = x
+        if not k:
+            return w[: self.words]
         out = self._ct()
-        self._chk(self.lib().orc_materialize(self._h, _p(np.ascontiguousarray(w)), _p(out)))
+        self._chk(self.lib().orc_materialize_kind(self._h, _p(np.ascontiguousarray(w)), int(k), _p(out)))
         return out
 
     def noise_budget(self, ct) -> float:

@@ -83,7 +83,7 @@ class OracleBackend final : public Backend {
         std::vector<std::uint64_t> buf(words_);
         check(orc_encrypt(ctx_, values.data(), values.size(), counter_++, buf.data()));
         count(&OpStats::n_encrypt);
-        return keep(std::move(buf), values.size(), 0);
+        return keep(std::move(buf), 0, values.size(), 0);
     }
     std::vector<value_t> decrypt(const Ciphertext& ct) override {
         count(&OpStats::n_decrypt);
@@ -92,38 +92,43 @@ class OracleBackend final : public Backend {
         check(orc_decrypt(ctx_, buf(ct), out.size(), out.data()));
         return out;
     }
-    // he_mult yields a pending product and he_add of pending values sums their
-    // tensors (bfv_oracle.cpp XCt); every other op reads the materialised value.
+    // Values carry parts (bfv_oracle.cpp XCt): he_mult yields a pending product,
+    // he_rot a pending key switch, he_cmult masks a value's plain and key-switch
+    // parts, he_add sums parts; every other reader uses the materialised value.
     Ciphertext he_add(const Ciphertext& x, const Ciphertext& y) override {
         same_segment(x, y, "he_add");
-        const bool px = pending(x), py = pending(y);
-        std::vector<std::uint64_t> o(px || py ? pwords_ : words_);
-        check(orc_add_any(ctx_, raw(x), px, raw(y), py, o.data()));
+        const int kx = kind(x), ky = kind(y);
+        std::vector<std::uint64_t> o((kx | ky) ? pwords_ : words_);
+        check(orc_add_any(ctx_, raw(x), kx, raw(y), ky, o.data()));
         count(&OpStats::n_add);
-        return keep(std::move(o), x.segment_length(), std::max(x.depth(), y.depth()));
+        return keep(std::move(o), kx | ky, x.segment_length(), std::max(x.depth(), y.depth()));
     }
     Ciphertext he_mult(const Ciphertext& x, const Ciphertext& y) override {
         same_segment(x, y, "he_mult");
         std::vector<std::uint64_t> o(pwords_);
         check(orc_mult_pending(ctx_, buf(x), buf(y), o.data()));
         count(&OpStats::n_mult_cc);
-        return keep(std::move(o), x.segment_length(), std::max(x.depth(), y.depth()) + 1);
+        return keep(std::move(o), 1, x.segment_length(), std::max(x.depth(), y.depth()) + 1);
     }
     Ciphertext he_cmult(const Ciphertext& x, std::span<const value_t> mask) override {
         if (mask.size() != x.segment_length())
             throw DimensionError("he_cmult mask length " + std::to_string(mask.size()) +
                                  " does not match segment " +
                                  std::to_string(x.segment_length()));
-        std::vector<std::uint64_t> o(words_);
-        check(orc_cmult(ctx_, buf(x), mask.data(), mask.size(), o.data()));
+        std::vector<std::uint64_t> o(pwords_);
+        int k = 0;
+        check(orc_cmult_x(ctx_, raw(x), kind(x), mask.data(), mask.size(), o.data(), &k));
+        if (k == 0) o.resize(words_);
         count(&OpStats::n_mult_cp);
-        return keep(std::move(o), x.segment_length(), x.depth());
+        return keep(std::move(o), k, x.segment_length(), x.depth());
     }
     Ciphertext he_rot(const Ciphertext& x, std::ptrdiff_t offset) override {
-        std::vector<std::uint64_t> o(words_);
-        check(orc_rot(ctx_, buf(x), offset, o.data()));
+        std::vector<std::uint64_t> o(pwords_);
+        int k = 0;
+        check(orc_rot_x(ctx_, buf(x), offset, o.data(), &k));
+        if (k == 0) o.resize(words_);
         count(&OpStats::n_rot);
-        return keep(std::move(o), x.segment_length(), x.depth());
+        return keep(std::move(o), k, x.segment_length(), x.depth());
     }
     OpStats stats() const override {
         std::lock_guard<std::mutex> lk(mu_);
@@ -158,24 +163,25 @@ class OracleBackend final : public Backend {
         std::lock_guard<std::mutex> lk(mu_);
         (stats_.*c).bump(p);
     }
-    bool pending(const Ciphertext& ct) const { return store_.at(Minter::id_of(ct)).size() == pwords_; }
+    int kind(const Ciphertext& ct) const { return kinds_.at(Minter::id_of(ct)); }
     const std::uint64_t* raw(const Ciphertext& ct) const { return store_.at(Minter::id_of(ct)).data(); }
     // plain value of handle id: a pending product is materialised once, cached
     const std::vector<std::uint64_t>& plain(std::uint64_t id) {
         const std::vector<std::uint64_t>& w = store_.at(id);
-        if (w.size() != pwords_) return w;
+        if (kinds_.at(id) == 0) return w;
         auto it = plain_.find(id);
         if (it == plain_.end()) {
             std::vector<std::uint64_t> o(words_);
-            check(orc_materialize(ctx_, w.data(), o.data()));
+            check(orc_materialize_kind(ctx_, w.data(), kinds_.at(id), o.data()));
             it = plain_.emplace(id, std::move(o)).first;
         }
         return it->second;
     }
     const std::uint64_t* buf(const Ciphertext& ct) { return plain(Minter::id_of(ct)).data(); }
-    Ciphertext keep(std::vector<std::uint64_t> words, std::size_t seg, std::size_t depth) {
+    Ciphertext keep(std::vector<std::uint64_t> words, int kind, std::size_t seg, std::size_t depth) {
         const std::uint64_t id = store_.size();
         store_.push_back(std::move(words));
+        kinds_.push_back(kind);
         return minter_.mint(seg, depth, id, phase());
     }
 
@@ -187,6 +193,7 @@ class OracleBackend final : public Backend {
     std::uint64_t counter_;
     std::uint64_t last_decrypted_ = 0;
     std::vector<std::vector<std::uint64_t>> store_;
+    std::vector<int> kinds_;
     mutable std::mutex mu_;
     OpStats stats_;
     std::atomic<Phase> phase_{Phase::Client};

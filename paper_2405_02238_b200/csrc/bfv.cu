@@ -224,11 +224,13 @@ __global__ void k_copy(u32 n, size_t W, const u64* const* in, u64* const* out) {
 #ifndef HGM_LC_MINB
 #define HGM_LC_MINB 4
 #endif
-template <typename SH>
+// RL = limbs per component: L (ciphertexts), or R = L + K for pending key
+// switches over Q ++ P (the masks hold R limbs; limb r uses prime r).
+template <typename SH, u32 RL = SH::L>
 __global__ void __launch_bounds__(kThreads, HGM_LC_MINB) k_lincomb(DevCtx cx, u32 n, const u32* off,
                           const u64* const* in, const u64* const* mask, u64* const* out) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, logN = dp->logN, L = SH::L;
+    const u32 N = dp->N, logN = dp->logN, L = RL;
     const size_t LN = (size_t)L * N, W2 = LN;  // word pairs per ciphertext
     ITEM_LOOP {
         const u32 t0 = off[item], t1 = off[item + 1];
@@ -305,7 +307,7 @@ __global__ void k_mask_lift(DevCtx cx, const u64* m, u64* out) {
     ITEM_LOOP {
         COEF_LOOP {
             const u64 v = m[j];
-            for (u32 i = 0; i < L; ++i) out[(size_t)i * N + j] = centred_lift(v, kT, dp->pr[i].q);
+            for (u32 i = 0; i < SH::R; ++i) out[(size_t)i * N + j] = centred_lift(v, kT, dp->pr[i].q);
         }
     }
 }
@@ -380,8 +382,11 @@ __global__ void k_modup_lift(DevCtx cx, u32 n, const u64* C, size_t c_stride,
 // once for all items of the group that share it.
 constexpr int kKeyReuse = 8;
 template <typename SH>
+// c0 (optional, per item): NTT-domain c0 of the rotated ciphertext; P phi_g(c0)
+// is folded into acc's component 0 over Q (a pending key switch, oracle rot_x:
+// ModDown(acc + P y) = ModDown(acc) + y).
 __global__ void k_ks_inner(DevCtx cx, u32 n, const u64* const* D,
-                           const u64* const* key, const u32* g, u64* const* acc) {
+                           const u64* const* key, const u32* g, u64* const* acc, const u64* const* c0) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, R = SH::R, dnum = SH::dnum, logN = dp->logN;
     for (u32 grp = blockIdx.y; grp * kKeyReuse < n; grp += gridDim.y) {
@@ -408,6 +413,8 @@ __global__ void k_ks_inner(DevCtx cx, u32 n, const u64* const* D,
                         a0.mac(x, k0[dg]);
                         a1.mac(x, k1[dg]);
                     }
+                    if (c0 && r < SH::L)
+                        a0.mac(split<SH::S>(c0[i0 + u][(size_t)r * N + src]), split<SH::S>(dp->P_mod_q[r]));
                     u64* a = acc[i0 + u];
                     a[(size_t)r * N + j] = reduce_acc(a0.fold<SH::S>(), P);
                     a[((size_t)R + r) * N + j] = reduce_acc(a1.fold<SH::S>(), P);
@@ -426,6 +433,8 @@ __global__ void k_ks_inner(DevCtx cx, u32 n, const u64* const* D,
                         a0.mac(x, packed_dig<SH::S>(__ldg(kk + (((size_t)dg * 2 + 0) * R + r) * N + j)));
                         a1.mac(x, packed_dig<SH::S>(__ldg(kk + (((size_t)dg * 2 + 1) * R + r) * N + j)));
                     }
+                    if (c0 && r < SH::L)
+                        a0.mac(split<SH::S>(c0[i0 + u][(size_t)r * N + su]), split<SH::S>(dp->P_mod_q[r]));
                     a[(size_t)r * N + j] = reduce_acc(a0.fold<SH::S>(), dp->pr[r]);
                     a[((size_t)R + r) * N + j] = reduce_acc(a1.fold<SH::S>(), dp->pr[r]);
                 }
@@ -1081,15 +1090,17 @@ const u64* Context::mask_plain(const i64* mask, size_t S, u64 stable_id) {
     NttJobs tj = jobs_contig(m, 1, kTIndex, 1);
     ntt(false, tj);
     u64* out = nullptr;
-    HGM_CUDA(cudaMallocAsync((void**)&out, (size_t)L * N * 8, stream_));
+    // over Q ++ P: the P limbs mask pending key switches (k_lincomb over R limbs)
+    const u32 R = hp_.R;
+    HGM_CUDA(cudaMallocAsync((void**)&out, (size_t)R * N * 8, stream_));
     if (hp_.L == 3) k_mask_lift<ShapeQ3><<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, m, out); else k_mask_lift<ShapeQ8><<<grid_of(N, 1), kThreads, 0, stream_>>>(cx_, m, out); ++launches_;
-    ntt(true, jobs_contig(out, L, 0, L));
-    if (hp_.L == 3) k_mask_digits<ShapeQ3><<<grid_of(N, 1), kThreads, 0, stream_>>>(out, (size_t)L * N); else k_mask_digits<ShapeQ8><<<grid_of(N, 1), kThreads, 0, stream_>>>(out, (size_t)L * N);
+    ntt(true, jobs_contig(out, R, 0, R));
+    if (hp_.L == 3) k_mask_digits<ShapeQ3><<<grid_of(N, 1), kThreads, 0, stream_>>>(out, (size_t)R * N); else k_mask_digits<ShapeQ8><<<grid_of(N, 1), kThreads, 0, stream_>>>(out, (size_t)R * N);
     ++launches_;
     release(m);
     HGM_CUDA(cudaGetLastError());
     bucket.push_back(MaskEntry{std::vector<i64>(mask, mask + S), out, ++mask_tick_, {}});
-    mask_bytes_ += (size_t)L * N * 8;
+    mask_bytes_ += (size_t)R * N * 8;
     if (stable_id) {
         masks_by_id_.emplace(stable_id, &bucket.back());
         bucket.back().ids.push_back(stable_id);
@@ -1116,7 +1127,7 @@ void Context::trim_mask_cache() {
     for (auto& kv : masks_)
         for (auto& e : kv.second) all.push_back({e.tick, {kv.first, &e}});
     std::sort(all.begin(), all.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-    const size_t each = (size_t)hp_.L * hp_.N * 8;
+    const size_t each = (size_t)hp_.R * hp_.N * 8;
     for (auto& a : all) {
         if (mask_bytes_ <= budget / 2) break;  // hysteresis: trim to half the budget
         MaskEntry* e = a.second.second;
@@ -1364,13 +1375,18 @@ void Context::modup(int n, const u64* const* ct, u64* const* out) {
 }
 
 void Context::inner_product(int n, const u64* const* digits, const u64* const* keys, const u32* g,
-                            u64* const* acc) {
+                            u64* const* acc, const u64* const* c0) {
     std::vector<const u64*> vd(digits, digits + n), vk(keys, keys + n);
     std::vector<u32> vg(g, g + n);
     std::vector<u64*> va(acc, acc + n);
+    const u64* const* dc0 = nullptr;
+    if (c0) {
+        std::vector<const u64*> v(c0, c0 + n);
+        dc0 = upload(v);
+    }
     if (hp_.L == 3) k_ks_inner<ShapeQ3><<<grid_of(hp_.N, (n + kKeyReuse - 1) / kKeyReuse), kThreads, 0, stream_>>>(cx_, n, upload(vd), upload(vk), upload(vg),
-                                                           upload(va)); else k_ks_inner<ShapeQ8><<<grid_of(hp_.N, (n + kKeyReuse - 1) / kKeyReuse), kThreads, 0, stream_>>>(cx_, n, upload(vd), upload(vk), upload(vg),
-                                                           upload(va)); ++launches_;
+                                                           upload(va), dc0); else k_ks_inner<ShapeQ8><<<grid_of(hp_.N, (n + kKeyReuse - 1) / kKeyReuse), kThreads, 0, stream_>>>(cx_, n, upload(vd), upload(vk), upload(vg),
+                                                           upload(va), dc0); ++launches_;
     HGM_CUDA(cudaGetLastError());
 }
 
@@ -1535,6 +1551,56 @@ void Context::scale_relin(int n, u64* T, u64* const* out) {
     release(Dg);
     release(A);
     release(E);
+}
+
+void Context::rotate_acc(int n, const u64* const* modup, const u64* const* ct, const u32* g, u64* const* acc) {
+    if (n <= 0) return;
+    for (int c0 = 0; c0 < n; c0 += kChunkKs) {
+        const int cn = std::min(kChunkKs, n - c0);
+        std::vector<const u64*> keys(cn);
+        for (int i = 0; i < cn; ++i) keys[i] = ks_key(g[c0 + i]);
+        inner_product(cn, modup + c0, keys.data(), g + c0, acc + c0, ct + c0);
+    }
+}
+
+void Context::moddown(int n, const u64* const* acc, u64* const* out) {
+    if (n <= 0) return;
+    const int chunk = chunk_for((size_t)(2 * hp_.R + 2 * hp_.L) * hp_.N, kChunkKs);
+    for (int c0 = 0; c0 < n; c0 += chunk) {
+        const int cn = std::min(chunk, n - c0);
+        std::vector<u32> ones(cn, 1);
+        const bool in_place = !(ntt_conv_fusable(hp_.dev) && !ntt_fusable(hp_.dev, kFuseModDown));
+        if (in_place) {  // this key_switch_tail path inverse-transforms acc's P limbs in place: work on a copy
+            u64* A = alloc((size_t)cn * ks_words());
+            std::vector<const u64*> src(acc + c0, acc + c0 + cn);
+            std::vector<u64*> dst(cn);
+            for (int i = 0; i < cn; ++i) dst[i] = A + (size_t)i * ks_words();
+            k_copy<<<grid_of(hp_.N, cn), kThreads, 0, stream_>>>(cn, ks_words(), upload(src), upload(dst)); ++launches_;
+            key_switch_tail(cn, dst.data(), nullptr, nullptr, ones.data(), out + c0);
+            release(A);
+        } else {
+            std::vector<u64*> va(cn);
+            for (int i = 0; i < cn; ++i) va[i] = const_cast<u64*>(acc[c0 + i]);
+            key_switch_tail(cn, va.data(), nullptr, nullptr, ones.data(), out + c0);
+        }
+    }
+}
+
+void Context::lincomb_qp(int n_out, const u32* off, const u64* const* in, const u64* const* mask, u64* const* out) {
+    if (n_out <= 0) return;
+    for (int c0 = 0; c0 < n_out; c0 += kChunkLin) {
+        const int cn = std::min(kChunkLin, n_out - c0);
+        std::vector<u32> sub(cn + 1);
+        for (int i = 0; i <= cn; ++i) sub[i] = off[c0 + i] - off[c0];
+        std::vector<const u64*> vin(in + off[c0], in + off[c0 + cn]), vm(mask + off[c0], mask + off[c0 + cn]);
+        std::vector<u64*> vo(out + c0, out + c0 + cn);
+        if (hp_.L == 3)
+            k_lincomb<ShapeQ3, ShapeQ3::R><<<grid_of(hp_.N, cn, 1), kThreads, 0, stream_>>>(cx_, cn, upload(sub), upload(vin), upload(vm), upload(vo));
+        else
+            k_lincomb<ShapeQ8, ShapeQ8::R><<<grid_of(hp_.N, cn, 1), kThreads, 0, stream_>>>(cx_, cn, upload(sub), upload(vin), upload(vm), upload(vo));
+        ++launches_;
+        HGM_CUDA(cudaGetLastError());
+    }
 }
 
 void Context::mult(int n, const u64* const* a, const u64* const* b, u64* const* out) {

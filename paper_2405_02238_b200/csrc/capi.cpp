@@ -53,7 +53,8 @@ struct SNode {
     std::vector<i64> values;  // Enc
     u64 counter = 0;          // Enc
     std::shared_ptr<DevBuf> buf;
-    std::shared_ptr<DevBuf> pbuf;  // pending product form (engine.hpp), when the value is one
+    std::shared_ptr<DevBuf> pbuf;  // the value's parts (engine.hpp), when it is not plain
+    int pkind = 0;
     std::atomic<int> pins{0};
 };
 
@@ -162,7 +163,7 @@ void flush(hgm_ctx* c, const std::vector<std::shared_ptr<SNode>>& targets) {
             }
             int id;
             if (n->buf) {
-                id = prog.add_input(n->S, n->pbuf != nullptr);
+                id = prog.add_input(n->S, n->pbuf ? n->pkind : 0);
                 inputs.push_back(f.n);
             } else {
                 std::vector<int> in;
@@ -206,12 +207,17 @@ void flush(hgm_ctx* c, const std::vector<std::shared_ptr<SNode>>& targets) {
     io.enc_counter = [&](int s, int) { return encs[s]->counter; };
     io.input_pending = [&](int s, int) { return (const u64*)inputs[s]->pbuf->p; };
     std::vector<u64*> pres;
+    std::vector<int> pkinds;
     io.pending_out = &pres;
+    io.pending_kind = &pkinds;
     std::vector<u64*> res = execute(*c->ctx, sch, io);
     for (size_t i = 0; i < uniq.size(); ++i) {
         uniq[i]->buf = std::make_shared<DevBuf>(c->ctx.get(), res[i]);
-        // a pending product keeps its pending form: later he_adds sum its tensor
-        if (pres[i]) uniq[i]->pbuf = std::make_shared<DevBuf>(c->ctx.get(), pres[i]);
+        // a non-plain value keeps its parts: later he_adds / he_cmults work on them
+        if (pres[i]) {
+            uniq[i]->pbuf = std::make_shared<DevBuf>(c->ctx.get(), pres[i]);
+            uniq[i]->pkind = pkinds[i];
+        }
         uniq[i]->in.clear();  // materialised: history no longer needed
     }
 }
@@ -540,8 +546,8 @@ void run_instances(Context& ctx, const MatmulProgram& prog, size_t count,
                    uint64_t* final_words) {
     const size_t W = ctx.ct_words();
     // instances per lockstep chunk: bounded by the rotated working set
-    const size_t per_inst = (prog.sched.rot_count + prog.sched.comb_count / 2 + 8) * W * 8 +
-                            prog.sched.pending_count * ctx.pending_words() * 8;
+    const size_t per_inst = (prog.sched.rot_count * ctx.ks_words() + (prog.sched.comb_count / 2 + 8) * W +
+                             prog.sched.pending_count * ctx.pending_words()) * 8;
     size_t free_b = 0, total_b = 0;
     HGM_CUDA(cudaMemGetInfo(&free_b, &total_b));
     size_t chunk = std::max<size_t>(1, (size_t)(0.45 * (double)free_b) / per_inst);
@@ -761,8 +767,8 @@ namespace {
 
 size_t lockstep_chunk(Context& ctx, const MatmulProgram& prog) {
     const size_t W = ctx.ct_words();
-    const size_t per_inst = (prog.cloud_sched.rot_count + prog.cloud_sched.comb_count / 2 + 8) * W * 8 +
-                            prog.cloud_sched.pending_count * ctx.pending_words() * 8;
+    const size_t per_inst = (prog.cloud_sched.rot_count * ctx.ks_words() + (prog.cloud_sched.comb_count / 2 + 8) * W +
+                             prog.cloud_sched.pending_count * ctx.pending_words()) * 8;
     size_t free_b = 0, total_b = 0;
     HGM_CUDA(cudaMemGetInfo(&free_b, &total_b));
     size_t chunk = std::max<size_t>(1, (size_t)(0.45 * (double)free_b) / per_inst);

@@ -116,6 +116,14 @@ class Context {
     void rotate(int n, const u64* const* modup, const u64* const* ct, const u32* g,
                 u64* const* out);
     void mult(int n, const u64* const* a, const u64* const* b, u64* const* out);
+    // Pending key switches (oracle rot_x): acc [2][R][N] over Q ++ P, NTT domain,
+    // P phi_g(c0) folded in; their plain value is ModDown(acc).
+    size_t ks_words() const { return (size_t)2 * hp_.R * hp_.N; }
+    void rotate_acc(int n, const u64* const* modup, const u64* const* ct, const u32* g, u64* const* acc);
+    // out = ModDown(acc) (acc is left intact)
+    void moddown(int n, const u64* const* acc, u64* const* out);
+    // lincomb over pending key switches ([2][R][N] inputs, masks over Q ++ P)
+    void lincomb_qp(int n_out, const u32* off, const u64* const* in, const u64* const* mask, u64* const* out);
     // Pending products (oracle XCt): a pending value is [T: 3 (L+nB) N][addend: 2 L N],
     // T the unscaled tensor sum over Q ++ B in the NTT domain.
     size_t pending_words() const { return (size_t)3 * (hp_.L + hp_.nB) * hp_.N + ct_words(); }
@@ -140,7 +148,7 @@ class Context {
     void key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, const u64* const* addn,
                          const u32* g, u64* const* out);
     void inner_product(int n, const u64* const* digits, const u64* const* keys, const u32* g,
-                       u64* const* acc);
+                       u64* const* acc, const u64* const* c0 = nullptr);
 
     HostParams hp_;
     std::atomic<u64> launches_{0};

@@ -9,10 +9,10 @@
 
 namespace hgm {
 
-int Program::add_input(size_t S, bool pending) {
+int Program::add_input(size_t S, int kind) {
     PNode n;
     n.kind = PNode::Input;
-    n.pend = pending;
+    n.pend = kind;
     n.slot = n_inputs++;
     n.S = S;
     nodes.push_back(std::move(n));
@@ -75,55 +75,78 @@ thread_local ExecCounters g_counters;
 
 ExecCounters last_exec_counters() { return g_counters; }
 
+PartLayout part_layout(const Context& ctx, int kind) {
+    PartLayout l;
+    size_t o = 0;
+    if (kind & kPartT) { l.t = o; o += ctx.tensor_words(); }
+    if (kind & kPartA) { l.a = o; o += ctx.ks_words(); }
+    if (kind & kPartX) { l.x = o; o += ctx.ct_words(); }
+    l.words = o;
+    return l;
+}
+
+namespace {
+// the parts a Comb term contributes (oracle cmult_x / add_any): a masked value
+// with a pending product is read materialised
+int term_kind(int in_kind, bool masked) {
+    if (masked && (in_kind & kPartT)) return kPartX;
+    return in_kind;
+}
+}  // namespace
+
 Schedule optimise(const Program& p) {
     Schedule s;
     Program& q = s.prog;
     q = p;
     const size_t n0 = q.nodes.size();
-    // 1. rotation aliases: identity rotations and duplicate (src, g) pairs.  An
-    //    identity rotation of a pending product still reads its materialised
-    //    value (oracle rot() of a pending operand), so it becomes a Mat node.
+    // 1. value kinds, rotation aliases (identity rotations and duplicate (src, g)
+    //    pairs).  An identity rotation of a non-plain value reads its materialised
+    //    value (oracle rot_x), so it becomes a Mat node.
     std::vector<int> alias(n0);
     for (size_t i = 0; i < n0; ++i) alias[i] = (int)i;
     auto root = [&](int x) {
         while (alias[x] != x) x = alias[x];
         return x;
     };
-    std::vector<char> pk(n0, 0);
+    std::vector<int> kind(n0, kPartX);
     std::map<std::pair<int, u32>, int> rots;
     std::map<int, int> mats;
     for (size_t i = 0; i < n0; ++i) {
         PNode& nd = q.nodes[i];
         for (int& x : nd.in) x = root(x);
         switch (nd.kind) {
-            case PNode::Input: pk[i] = nd.pend; break;
-            case PNode::Mult: pk[i] = 1; break;
-            case PNode::Comb:
-                for (size_t t = 0; t < nd.in.size(); ++t)
-                    if (!nd.masks[t] && pk[nd.in[t]]) pk[i] = 1;
+            case PNode::Input: kind[i] = nd.pend ? nd.pend : kPartX; break;
+            case PNode::Mult: kind[i] = kPartT; break;
+            case PNode::Comb: {
+                int k = 0;
+                for (size_t t = 0; t < nd.in.size(); ++t) k |= term_kind(kind[nd.in[t]], nd.masks[t] != nullptr);
+                kind[i] = k;
                 break;
-            default: break;
-        }
-        if (nd.kind == PNode::Rot) {
-            const int src = nd.in[0];
-            if (nd.g == 1 && !pk[src]) {
-                alias[i] = src;
-            } else if (nd.g == 1) {
-                auto it = mats.find(src);
-                if (it != mats.end()) {
-                    alias[i] = it->second;
-                } else {
-                    nd.kind = PNode::Mat;
-                    mats.emplace(src, (int)i);
-                }
-            } else {
-                auto key = std::make_pair(src, nd.g);
-                auto it = rots.find(key);
-                if (it != rots.end())
-                    alias[i] = it->second;
-                else
-                    rots.emplace(key, (int)i);
             }
+            case PNode::Rot: {
+                const int src = nd.in[0];
+                if (nd.g == 1 && kind[src] == kPartX) {
+                    alias[i] = src;
+                } else if (nd.g == 1) {
+                    auto it = mats.find(src);
+                    if (it != mats.end()) {
+                        alias[i] = it->second;
+                    } else {
+                        nd.kind = PNode::Mat;
+                        mats.emplace(src, (int)i);
+                    }
+                } else {
+                    kind[i] = kPartA;
+                    auto key = std::make_pair(src, nd.g);
+                    auto it = rots.find(key);
+                    if (it != rots.end())
+                        alias[i] = it->second;
+                    else
+                        rots.emplace(key, (int)i);
+                }
+                break;
+            }
+            default: break;
         }
     }
     for (int& o : q.outputs) o = root(o);
@@ -136,8 +159,7 @@ Schedule optimise(const Program& p) {
         if (live[i])
             for (int x : q.nodes[i].in) ++uses[x];
     // 3. fold single-use plain addends that are masked sums into their consumer
-    //    (a pending child's tensor and addend join the parent's: he_add is
-    //    associative on pending values too)
+    //    (he_add is partwise, so a non-plain child's parts join the parent's)
     for (size_t i = 0; i < n0; ++i) {
         PNode& nd = q.nodes[i];
         if (!live[i] || nd.kind != PNode::Comb) continue;
@@ -157,8 +179,9 @@ Schedule optimise(const Program& p) {
         nd.in = std::move(in);
         nd.masks = std::move(masks);
     }
-    // 4. every read of a pending value other than a plain sum term reads its
-    //    materialised form (one Mat node per value); pending outputs return both
+    // 4. every read of a non-plain value that is not a Comb term taking its parts
+    //    reads its materialised form (one Mat node per value); non-plain outputs
+    //    return both
     auto mat_of = [&](int x) {
         auto it = mats.find(x);
         if (it != mats.end()) return it->second;
@@ -167,7 +190,7 @@ Schedule optimise(const Program& p) {
         m.in = {x};
         m.S = q.nodes[x].S;
         q.nodes.push_back(std::move(m));
-        pk.push_back(0);
+        kind.push_back(kPartX);
         const int id = (int)q.nodes.size() - 1;
         mats.emplace(x, id);
         return id;
@@ -177,23 +200,26 @@ Schedule optimise(const Program& p) {
         if (!live[i] || q.nodes[i].kind == PNode::Mat) continue;
         for (size_t t = 0; t < q.nodes[i].in.size(); ++t) {  // (mat_of appends: no references held)
             const int x = q.nodes[i].in[t];
-            const bool sum_term = q.nodes[i].kind == PNode::Comb && !q.nodes[i].masks[t];
-            if (pk[x] && !sum_term) {
-                const int m = mat_of(x);
-                q.nodes[i].in[t] = m;
-            }
+            if (kind[x] == kPartX) continue;
+            const bool comb = q.nodes[i].kind == PNode::Comb, masked = comb && q.nodes[i].masks[t];
+            if (comb && (!masked || !(kind[x] & kPartT))) continue;  // the term takes x's parts
+            // a non-plain Input's materialised form is supplied (ExecIO::input), except
+            // where a Comb term would read it: there it needs a plain node
+            if (q.nodes[x].kind == PNode::Input && !comb) continue;
+            const int m = mat_of(x);
+            q.nodes[i].in[t] = m;
         }
     }
     s.pending_out.assign(q.outputs.size(), -1);
     for (size_t o = 0; o < q.outputs.size(); ++o) {
         const int x = q.outputs[o];
-        if (pk[x]) {
+        if (kind[x] != kPartX) {
             s.pending_out[o] = x;
-            q.outputs[o] = mat_of(x);
+            if (q.nodes[x].kind != PNode::Input) q.outputs[o] = mat_of(x);
         }
     }
     const size_t n = q.nodes.size();
-    // liveness from the outputs and the pending outputs
+    // liveness from the outputs and the non-plain outputs
     {
         std::vector<int> stack(q.outputs.begin(), q.outputs.end());
         for (int x : s.pending_out)
@@ -212,8 +238,8 @@ Schedule optimise(const Program& p) {
     s.is_pending_output.assign(n, 0);
     for (int x : s.pending_out)
         if (x >= 0) s.is_pending_output[x] = 1;
-    // 5. fusion: a product read only by one plain term of a pending sum is
-    //    accumulated straight into that sum's tensor
+    // 5. fusion: a product read only by one plain term of a sum is accumulated
+    //    straight into that sum's tensor
     uses.assign(n, 0);
     for (size_t i = 0; i < n; ++i)
         if (live[i])
@@ -276,7 +302,7 @@ Schedule optimise(const Program& p) {
         if (nd.kind == PNode::Rot) ++s.rot_count;
         if (nd.kind == PNode::Comb) ++s.comb_count;
         if (nd.kind == PNode::Mat) ++s.mat_count;
-        if (pk[i]) ++s.pending_count;
+        if (kind[i] & kPartT) ++s.pending_count;
         for (size_t t = 0; t < nd.in.size(); ++t) {
             const int x = nd.in[t];
             if (nd.kind == PNode::Comb && nd.fused[t]) {
@@ -288,28 +314,41 @@ Schedule optimise(const Program& p) {
         }
         if (nd.kind == PNode::Mult) ++s.mult_count;
     }
-    s.pk = pk;
+    s.kind = kind;
     return s;
 }
 
 std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
     const Program& P = sch.prog;
     const int K = io.K;
-    const size_t W = ctx.ct_words(), MW = ctx.modup_words(), PW = ctx.pending_words(), TW = ctx.tensor_words();
+    const size_t MW = ctx.modup_words();
     g_counters = ExecCounters{};
     g_counters.levels = sch.levels.size();
     ctx.trim_mask_cache();  // between programs: no mask pointer is held here yet
-    std::vector<u64*> base(P.nodes.size(), nullptr);   // plain values
-    std::vector<u64*> pbase(P.nodes.size(), nullptr);  // pending values [T][addend]
-    auto ptr = [&](int node, int k) -> const u64* {
+    std::vector<u64*> buf(P.nodes.size(), nullptr);
+    std::vector<PartLayout> lay(P.nodes.size());
+    for (size_t x = 0; x < P.nodes.size(); ++x) lay[x] = part_layout(ctx, sch.kind[x]);
+    // pointer to a part of node `node`'s value for instance k
+    auto part = [&](int node, int k, int which) -> const u64* {
+        const PNode& nd = P.nodes[node];
+        const PartLayout& l = lay[node];
+        const size_t off = which == kPartT ? l.t : which == kPartA ? l.a : l.x;
+        if (nd.kind == PNode::Input)
+            return (nd.pend ? io.input_pending(nd.slot, k) : io.input(nd.slot, k)) + off;
+        return buf[node] + (size_t)k * l.words + off;
+    };
+    auto wpart = [&](int node, int k, int which) { return const_cast<u64*>(part(node, k, which)); };
+    // the value's start (all parts), and its plain (materialised) form: plain nodes,
+    // or an Input's supplied materialised form
+    auto whole = [&](int node, int k) -> const u64* {
+        const PNode& nd = P.nodes[node];
+        if (nd.kind == PNode::Input) return nd.pend ? io.input_pending(nd.slot, k) : io.input(nd.slot, k);
+        return buf[node] + (size_t)k * lay[node].words;
+    };
+    auto plain = [&](int node, int k) -> const u64* {
         const PNode& nd = P.nodes[node];
         if (nd.kind == PNode::Input) return io.input(nd.slot, k);
-        return base[node] + (size_t)k * W;
-    };
-    auto pptr = [&](int node, int k) -> const u64* {
-        const PNode& nd = P.nodes[node];
-        if (nd.kind == PNode::Input) return io.input_pending(nd.slot, k);
-        return pbase[node] + (size_t)k * PW;
+        return part(node, k, kPartX);
     };
     std::unordered_map<const MaskData*, const u64*> mask_dev;
     auto resolve = [&](const MaskRef& m) -> const u64* {
@@ -322,16 +361,13 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
     };
     for (size_t lv = 0; lv < sch.levels.size(); ++lv) {
         const std::vector<int>& nodes = sch.levels[lv];
-        std::vector<int> enc, rot, comb, pcomb, mult, mat;
+        std::vector<int> enc, rot, comb, mult, mat;
         for (int x : nodes) {
-            if (sch.pk[x])
-                pbase[x] = ctx.alloc((size_t)K * PW);
-            else
-                base[x] = ctx.alloc((size_t)K * W);
+            buf[x] = ctx.alloc((size_t)K * lay[x].words);
             switch (P.nodes[x].kind) {
                 case PNode::Enc: enc.push_back(x); break;
                 case PNode::Rot: rot.push_back(x); break;
-                case PNode::Comb: (sch.pk[x] ? pcomb : comb).push_back(x); break;
+                case PNode::Comb: comb.push_back(x); break;
                 case PNode::Mult: mult.push_back(x); break;
                 case PNode::Mat: mat.push_back(x); break;
                 default: throw std::logic_error("input node scheduled");
@@ -347,7 +383,7 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
                     vals.push_back(io.enc_values(P.nodes[x].slot, k));
                     S.push_back(P.nodes[x].S);
                     ctr.push_back(io.enc_counter(P.nodes[x].slot, k));
-                    out.push_back(base[x] + (size_t)k * W);
+                    out.push_back(wpart(x, k, kPartX));
                 }
             ctx.encrypt((int)vals.size(), vals.data(), S.data(), ctr.data(), out.data());
             g_counters.enc_items += vals.size();
@@ -363,7 +399,7 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
             std::vector<u64*> mout;
             for (size_t si = 0; si < srcs.size(); ++si)
                 for (int k = 0; k < K; ++k) {
-                    mct.push_back(ptr(srcs[si], k));
+                    mct.push_back(plain(srcs[si], k));
                     mout.push_back(mbuf + (si * K + k) * MW);
                 }
             ctx.modup((int)mct.size(), mct.data(), mout.data());
@@ -386,61 +422,73 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
                     const size_t si = std::lower_bound(srcs.begin(), srcs.end(), src) - srcs.begin();
                     for (int k = k0; k < std::min(K, k0 + kRotTile); ++k) {
                         mu.push_back(mbuf + (si * K + k) * MW);
-                        cts.push_back(ptr(src, k));
+                        cts.push_back(plain(src, k));
                         gs.push_back(P.nodes[x].g);
-                        out.push_back(base[x] + (size_t)k * W);
+                        out.push_back(wpart(x, k, kPartA));
                     }
                 }
-            ctx.rotate((int)mu.size(), mu.data(), cts.data(), gs.data(), out.data());
+            // a pending key switch: the accumulator, P phi(c0) folded in (no ModDown)
+            ctx.rotate_acc((int)mu.size(), mu.data(), cts.data(), gs.data(), out.data());
             g_counters.rot_items += mu.size();
             ctx.release(mbuf);
         }
-        // plain masked sums, and the addends of pending sums (plain terms, masked
-        // terms, and the addends of pending non-fused terms)
-        if (!comb.empty() || !pcomb.empty()) {
-            std::vector<u32> off{0};
-            std::vector<const u64*> in, masks;
-            std::vector<u64*> out;
-            for (int pass = 0; pass < 2; ++pass)
-                for (int x : pass == 0 ? comb : pcomb) {
-                    const PNode& nd = P.nodes[x];
-                    std::vector<const u64*> md(nd.in.size());
-                    for (size_t t = 0; t < nd.in.size(); ++t) md[t] = resolve(nd.masks[t]);
-                    for (int k = 0; k < K; ++k) {
-                        for (size_t t = 0; t < nd.in.size(); ++t) {
-                            const int y = nd.in[t];
-                            if (pass == 1 && !nd.masks[t] && sch.pk[y]) {
-                                if (nd.fused[t]) continue;
-                                in.push_back(pptr(y, k) + TW);  // its addend
-                            } else {
-                                in.push_back(ptr(y, k));
-                            }
-                            masks.push_back(md[t]);
+        // sums: plain parts (masked or not), key-switch parts over Q ++ P, tensors
+        if (!comb.empty()) {
+            std::vector<u32> xoff{0}, aoff{0};
+            std::vector<const u64*> xin, xmask, ain, amask;
+            std::vector<u64*> xout, aout;
+            for (int x : comb) {
+                const PNode& nd = P.nodes[x];
+                const int kx = sch.kind[x];
+                std::vector<const u64*> md(nd.in.size());
+                for (size_t t = 0; t < nd.in.size(); ++t) md[t] = resolve(nd.masks[t]);
+                for (int k = 0; k < K; ++k) {
+                    for (size_t t = 0; t < nd.in.size(); ++t) {
+                        const int y = nd.in[t];
+                        const int ky = sch.kind[y];
+                        if (!nd.fused.empty() && nd.fused[t]) continue;
+                        if (ky & kPartX) {
+                            xin.push_back(part(y, k, kPartX));
+                            xmask.push_back(md[t]);
                         }
-                        off.push_back((u32)in.size());
-                        out.push_back(pass == 0 ? base[x] + (size_t)k * W : pbase[x] + (size_t)k * PW + TW);
+                        if (ky & kPartA) {
+                            ain.push_back(part(y, k, kPartA));
+                            amask.push_back(md[t]);
+                        }
+                    }
+                    if (kx & kPartX) {
+                        xoff.push_back((u32)xin.size());
+                        xout.push_back(wpart(x, k, kPartX));
+                    }
+                    if (kx & kPartA) {
+                        aoff.push_back((u32)ain.size());
+                        aout.push_back(wpart(x, k, kPartA));
                     }
                 }
-            ctx.lincomb((int)out.size(), off.data(), in.data(), masks.data(), out.data());
-            g_counters.comb_items += out.size();
+            }
+            if (!xout.empty()) ctx.lincomb((int)xout.size(), xoff.data(), xin.data(), xmask.data(), xout.data());
+            if (!aout.empty()) ctx.lincomb_qp((int)aout.size(), aoff.data(), ain.data(), amask.data(), aout.data());
+            g_counters.comb_items += xout.size() + aout.size();
         }
-        // tensors of pending sums: stored pending terms summed, fused products
-        // accumulated; non-fused products get their own tensor (addend zero)
-        if (!pcomb.empty() || !mult.empty()) {
+        // tensors: stored tensor terms summed, fused products accumulated;
+        // non-fused products get their own tensor
+        {
             std::vector<u32> toff{0}, moff{0};
             std::vector<const u64*> tin, ma, mb;
             std::vector<u64*> tout, mout;
             std::vector<unsigned char> tinit, minit;
-            for (int x : pcomb) {
+            for (int x : comb) {
+                if (!(sch.kind[x] & kPartT)) continue;
                 const PNode& nd = P.nodes[x];
                 bool has_t = false;
                 for (size_t t = 0; t < nd.in.size(); ++t)
-                    if (!nd.masks[t] && sch.pk[nd.in[t]] && !nd.fused[t]) has_t = true;
+                    if (!nd.masks[t] && (sch.kind[nd.in[t]] & kPartT) && !nd.fused[t]) has_t = true;
                 for (int k = 0; k < K; ++k) {
-                    u64* T = pbase[x] + (size_t)k * PW;
+                    u64* T = wpart(x, k, kPartT);
                     if (has_t) {
                         for (size_t t = 0; t < nd.in.size(); ++t)
-                            if (!nd.masks[t] && sch.pk[nd.in[t]] && !nd.fused[t]) tin.push_back(pptr(nd.in[t], k));
+                            if (!nd.masks[t] && (sch.kind[nd.in[t]] & kPartT) && !nd.fused[t])
+                                tin.push_back(part(nd.in[t], k, kPartT));
                         toff.push_back((u32)tin.size());
                         tout.push_back(T);
                         tinit.push_back(0);
@@ -449,8 +497,8 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
                     for (size_t t = 0; t < nd.in.size(); ++t)
                         if (!nd.masks[t] && nd.fused[t]) {
                             const PNode& m = P.nodes[nd.in[t]];
-                            ma.push_back(ptr(m.in[0], k));
-                            mb.push_back(ptr(m.in[1], k));
+                            ma.push_back(plain(m.in[0], k));
+                            mb.push_back(plain(m.in[1], k));
                             any = true;
                         }
                     if (any) {
@@ -462,14 +510,12 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
             }
             for (int x : mult) {
                 const PNode& nd = P.nodes[x];
-                std::vector<u64*> addends;
                 for (int k = 0; k < K; ++k) {
-                    ma.push_back(ptr(nd.in[0], k));
-                    mb.push_back(ptr(nd.in[1], k));
+                    ma.push_back(plain(nd.in[0], k));
+                    mb.push_back(plain(nd.in[1], k));
                     moff.push_back((u32)ma.size());
-                    mout.push_back(pbase[x] + (size_t)k * PW);
+                    mout.push_back(wpart(x, k, kPartT));
                     minit.push_back(0);
-                    HGM_CUDA(cudaMemsetAsync(pbase[x] + (size_t)k * PW + TW, 0, W * 8, ctx.stream()));
                 }
             }
             if (!tout.empty()) ctx.tsum((int)tout.size(), toff.data(), tin.data(), tout.data(), tinit.data());
@@ -478,71 +524,118 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
             g_counters.mult_items += ma.size();
         }
         if (!mat.empty()) {
-            std::vector<const u64*> T, A;
-            std::vector<u64*> out;
-            for (int x : mat)
+            // products (+ plain part), then ModDown of key-switch parts, added
+            std::vector<const u64*> T, Xp, A1, A2;
+            std::vector<u64*> outT, outA1, outA2;
+            std::vector<const u64*> addx_a, addx_b;
+            std::vector<u64*> addx_o;
+            for (int x : mat) {
+                const int src = P.nodes[x].in[0];
+                const int ks = sch.kind[src];
                 for (int k = 0; k < K; ++k) {
-                    const u64* p = pptr(P.nodes[x].in[0], k);
-                    T.push_back(p);
-                    A.push_back(p + TW);
-                    out.push_back(base[x] + (size_t)k * W);
+                    u64* o = wpart(x, k, kPartX);
+                    if (ks & kPartT) {
+                        T.push_back(part(src, k, kPartT));
+                        Xp.push_back((ks & kPartX) ? part(src, k, kPartX) : nullptr);
+                        outT.push_back(o);
+                        if (ks & kPartA) {
+                            A2.push_back(part(src, k, kPartA));
+                            outA2.push_back(o);
+                        }
+                    } else {  // key switch part (+ plain part)
+                        A1.push_back(part(src, k, kPartA));
+                        outA1.push_back(o);
+                        if (ks & kPartX) {
+                            addx_a.push_back(o);
+                            addx_b.push_back(part(src, k, kPartX));
+                            addx_o.push_back(o);
+                        }
+                    }
                 }
-            ctx.materialize((int)out.size(), T.data(), A.data(), out.data());
-            g_counters.mat_items += out.size();
+            }
+            if (!T.empty()) {
+                bool any_x = false;
+                for (auto* p : Xp) any_x |= p != nullptr;
+                if (any_x) {
+                    // materialize() adds one addend per item: split the items by presence
+                    std::vector<const u64*> T1, X1, T0;
+                    std::vector<u64*> O1, O0;
+                    for (size_t i = 0; i < T.size(); ++i) {
+                        if (Xp[i]) { T1.push_back(T[i]); X1.push_back(Xp[i]); O1.push_back(outT[i]); }
+                        else { T0.push_back(T[i]); O0.push_back(outT[i]); }
+                    }
+                    ctx.materialize((int)O1.size(), T1.data(), X1.data(), O1.data());
+                    ctx.materialize((int)O0.size(), T0.data(), nullptr, O0.data());
+                } else {
+                    ctx.materialize((int)outT.size(), T.data(), nullptr, outT.data());
+                }
+            }
+            if (!A1.empty()) ctx.moddown((int)A1.size(), A1.data(), outA1.data());
+            if (!addx_o.empty()) ctx.add((int)addx_o.size(), addx_a.data(), addx_b.data(), addx_o.data());
+            if (!A2.empty()) {  // T and A together: ModDown into a temporary, added
+                u64* tmp = ctx.alloc(A2.size() * ctx.ct_words());
+                std::vector<u64*> to(A2.size());
+                std::vector<const u64*> tc(A2.size());
+                for (size_t i = 0; i < A2.size(); ++i) tc[i] = to[i] = tmp + i * ctx.ct_words();
+                ctx.moddown((int)A2.size(), A2.data(), to.data());
+                std::vector<const u64*> oa(outA2.begin(), outA2.end());
+                ctx.add((int)A2.size(), oa.data(), tc.data(), outA2.data());
+                ctx.release(tmp);
+            }
+            g_counters.mat_items += mat.size() * (size_t)K;
         }
         // release buffers whose last reader ran at this level
         for (size_t x = 0; x < P.nodes.size(); ++x)
-            if (sch.last_use_level[x] == (int)lv) {
-                if (base[x] && !sch.is_output[x]) {
-                    ctx.release(base[x]);
-                    base[x] = nullptr;
-                }
-                if (pbase[x] && !sch.is_pending_output[x]) {
-                    ctx.release(pbase[x]);
-                    pbase[x] = nullptr;
-                }
+            if (buf[x] && sch.last_use_level[x] == (int)lv && !sch.is_output[x] && !sch.is_pending_output[x]) {
+                ctx.release(buf[x]);
+                buf[x] = nullptr;
             }
     }
+    const size_t W = ctx.ct_words();
     std::vector<u64*> outs;
     std::vector<char> handed(P.nodes.size(), 0);
-    for (int o : P.outputs) {
-        if (P.nodes[o].kind == PNode::Input || handed[o] || !base[o]) {
+    for (int o : P.outputs) {  // outputs are plain (Mat nodes for non-plain values)
+        if (P.nodes[o].kind == PNode::Input || handed[o] || !buf[o]) {
             u64* c = ctx.alloc((size_t)K * W);
             std::vector<const u64*> src;
             std::vector<u64*> dst;
             for (int k = 0; k < K; ++k) {
-                src.push_back(ptr(o, k));
+                src.push_back(plain(o, k));
                 dst.push_back(c + (size_t)k * W);
             }
             ctx.copy(K, src.data(), dst.data());
             outs.push_back(c);
         } else {
-            outs.push_back(base[o]);
+            outs.push_back(buf[o]);
             handed[o] = 1;
         }
     }
-    // outputs that were never handed over (e.g. duplicates) are released
-    for (size_t x = 0; x < P.nodes.size(); ++x)
-        if (base[x] && sch.is_output[x] && !handed[x]) ctx.release(base[x]);
-    // pending forms of pending outputs
+    // parts of non-plain outputs
     std::vector<char> phanded(P.nodes.size(), 0);
     if (io.pending_out) io.pending_out->assign(P.outputs.size(), nullptr);
+    if (io.pending_kind) io.pending_kind->assign(P.outputs.size(), 0);
     for (size_t o = 0; o < sch.pending_out.size() && io.pending_out; ++o) {
         const int x = sch.pending_out[o];
         if (x < 0) continue;
-        if (P.nodes[x].kind == PNode::Input || phanded[x] || !pbase[x]) {
+        const size_t PW = lay[x].words;
+        if (io.pending_kind) (*io.pending_kind)[o] = sch.kind[x];
+        if (P.nodes[x].kind == PNode::Input || phanded[x] || !buf[x]) {
             u64* c = ctx.alloc((size_t)K * PW);
             for (int k = 0; k < K; ++k)
-                HGM_CUDA(cudaMemcpyAsync(c + (size_t)k * PW, pptr(x, k), PW * 8, cudaMemcpyDeviceToDevice,
+                HGM_CUDA(cudaMemcpyAsync(c + (size_t)k * PW, whole(x, k), PW * 8, cudaMemcpyDeviceToDevice,
                                          ctx.stream()));
             (*io.pending_out)[o] = c;
         } else {
-            (*io.pending_out)[o] = pbase[x];
+            (*io.pending_out)[o] = buf[x];
             phanded[x] = 1;
         }
     }
-    for (size_t x = 0; x < P.nodes.size(); ++x)
-        if (pbase[x] && sch.is_pending_output[x] && !phanded[x]) ctx.release(pbase[x]);
+    for (size_t x = 0; x < P.nodes.size(); ++x) {
+        if (!buf[x]) continue;
+        const bool keep_plain = sch.is_output[x] && handed[x];
+        const bool keep_parts = sch.is_pending_output[x] && phanded[x];
+        if (!keep_plain && !keep_parts) ctx.release(buf[x]);
+    }
     return outs;
 }
 

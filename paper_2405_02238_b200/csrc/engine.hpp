@@ -12,11 +12,12 @@
 //     the digit lift uses centred residues and commutes with X -> X^g);
 //   * trees of he_add over he_cmult / he_add become one masked sum
 //     (modular adds are associative and commutative);
-//   * he_mult is a PENDING product (oracle XCt): add trees over products sum
-//     their unscaled tensors, and scale-and-round + relinearisation run once
-//     when a non-add op reads the value (a Mat node); a product whose only
-//     reader is such a sum is accumulated straight into the sum's tensor
-//     (fused: its own tensor is never stored);
+//   * he_mult is a PENDING product and he_rot a PENDING key switch (oracle
+//     XCt): add trees and masked sums work on the parts (tensors, Q ++ P
+//     accumulators, plain ciphertexts), and scale-and-round + relinearisation
+//     or ModDown run once when another op reads the value (a Mat node); a
+//     product whose only reader is such a sum is accumulated straight into the
+//     sum's tensor (fused: its own tensor is never stored);
 //   * every op of one dependency level is one batched launch sequence over
 //     all (node, instance) pairs; rotations are grouped by Galois key so that
 //     one key read from HBM serves the whole group.
@@ -49,7 +50,8 @@ struct PNode {
     std::vector<int> in;          // Rot / Mat: {src}; Mult: {a, b}; Comb: term inputs
     std::vector<MaskRef> masks;   // Comb: one per term, null = plain addend
     std::vector<char> fused;      // Comb (set by optimise): term is a Mult accumulated in place
-    bool pend = false;            // Input: a pending form is supplied (ExecIO::input_pending)
+    int pend = 0;                 // Input: kind of the supplied value (0: plain, ExecIO::input;
+                                  // else parts, ExecIO::input_pending)
     u32 g = 1;                    // Rot: Galois element
     int slot = -1;                // Input / Enc: external index
     size_t S = 0;                 // logical segment length
@@ -60,12 +62,22 @@ struct Program {
     std::vector<int> outputs;
     int n_inputs = 0;  // Input slots
     int n_enc = 0;     // Enc slots
-    int add_input(size_t S, bool pending = false);
+    int add_input(size_t S, int kind = 0);
     int add_enc(size_t S);
     int add_rot(int src, u32 g);
     int add_comb(std::vector<int> in, std::vector<MaskRef> masks);
     int add_mult(int a, int b);
 };
+
+// A value's parts (oracle XCt): T a pending product (unscaled tensor over
+// Q ++ B), A a pending key switch (accumulator over Q ++ P), X a plain
+// ciphertext; plain nodes have kind kPartX.  A non-plain value is stored as
+// [T][A][X] with only its parts present (part_layout).
+enum : int { kPartT = 1, kPartA = 2, kPartX = 4 };
+struct PartLayout {
+    size_t t = 0, a = 0, x = 0, words = 0;
+};
+PartLayout part_layout(const Context& ctx, int kind);
 
 // Optimised, levelised form of a Program (built once, reused for every batch).
 struct Schedule {
@@ -73,8 +85,8 @@ struct Schedule {
     std::vector<std::vector<int>> levels;
     std::vector<int> last_use_level;     // -1: never read
     std::vector<char> is_output;
-    std::vector<char> pk;                // node value is a pending product
-    std::vector<int> pending_out;        // per output: node whose pending form is also returned, or -1
+    std::vector<int> kind;               // value parts per node (kPartT | kPartA | kPartX)
+    std::vector<int> pending_out;        // per output: node whose parts are also returned, or -1
     std::vector<char> is_pending_output;
     size_t rot_count = 0, comb_count = 0, mult_count = 0, pending_count = 0, mat_count = 0;
 };
@@ -89,8 +101,9 @@ struct ExecIO {
     std::function<u64(int s, int k)> enc_counter;
     // Input slot s of instance k -> its pending form (Input nodes with pend set)
     std::function<const u64*(int s, int k)> input_pending;
-    // if set: receives, per output, a buffer of K pending forms (or nullptr)
+    // if set: receives, per output, a buffer of K non-plain values (or nullptr) and their kind
     std::vector<u64*>* pending_out = nullptr;
+    std::vector<int>* pending_kind = nullptr;
 };
 
 // Executes `sch` for io.K instances; returns, for each output o, a device

@@ -125,3 +125,45 @@ def test_pending_products_bit_exact(pid, gpu_factory, oracle_factory):
     # product of a pending value (materialised operand)
     m2 = g.he_mult(gacc, gc[1])
     assert np.array_equal(g.export(m2), o.mult(o.plain(oacc), oc[1][0]))
+
+
+@pytest.mark.parametrize("pid", [2, 0])
+def test_pending_key_switches_bit_exact(pid, gpu_factory, oracle_factory):
+    """he_rot is a pending key switch (oracle XCt part A): masked sums of
+    rotations are moded down once; values mixing plain, key-switch and product
+    parts; reads between flushes; rotations and products of such values."""
+    g, o = gpu_factory(pid), oracle_factory(pid)
+    rng = np.random.default_rng(60 + pid)
+    S = 300
+    a, b = rand_vals(rng, S), rand_vals(rng, S)
+    ga, gb = g.encrypt(a, counter=3000), g.encrypt(b, counter=3001)
+    oa, ob = o.encrypt(a, 3000), o.encrypt(b, 3001)
+    m = [rng.integers(0, 2, S).astype(np.int64) for _ in range(4)]
+    # eps = m0 rot(a, 1) + m1 rot(a, 7) + m2 rot(a, -2)   (an apply_plan-like masked sum)
+    geps, oeps = None, None
+    for z, mk in [(1, m[0]), (7, m[1]), (-2, m[2])]:
+        gt = g.he_cmult(g.he_rot(ga, z), mk)
+        ot = o.cmult_x(o.rot_x(oa, z), mk)
+        geps = gt if geps is None else g.he_add(geps, gt)
+        oeps = ot if oeps is None else o.add_any(oeps, ot)
+    assert oeps[1] == 2
+    assert np.array_equal(g.export(geps), o.plain(oeps))
+    full = np.zeros(g.slot_count, np.int64)
+    full[:S] = a
+    want = sum(np.roll(full, -z)[:S] * mk for z, mk in [(1, m[0]), (7, m[1]), (-2, m[2])]) % T
+    assert np.array_equal(g.decrypt(geps), want)
+    # the flushed sum keeps its parts: mask it again, add a plain value and a product
+    gmix = g.he_add(g.he_add(g.he_cmult(geps, m[3]), gb), g.he_mult(ga, gb))
+    omix = o.add_any(o.add_any(o.cmult_x(oeps, m[3]), (ob, 0)), o.mult_pending(oa, ob))
+    assert omix[1] == 3
+    assert np.array_equal(g.export(gmix), o.plain(omix))
+    # masking a value with a product part reads it materialised
+    gmm = g.he_cmult(gmix, m[0])
+    assert np.array_equal(g.export(gmm), o.plain(o.cmult_x(omix, m[0])))
+    # rotating / multiplying a non-plain value reads it materialised
+    r = g.he_rot(gmix, 3)
+    assert np.array_equal(g.export(r), o.rot(o.plain(omix), 3))
+    r0 = g.he_add(g.he_rot(geps, 0), ga)  # identity rotation: the plain value
+    assert np.array_equal(g.export(r0), o.add(o.plain(oeps), oa))
+    pm = g.he_mult(geps, gb)
+    assert np.array_equal(g.export(pm), o.mult(o.plain(oeps), ob))

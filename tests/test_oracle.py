@@ -98,6 +98,37 @@ def test_pending_products(oracle_factory):
     assert o.noise_budget(m1) >= o.noise_budget(eager) - 1.0
 
 
+def test_pending_key_switches(oracle_factory):
+    """he_rot is a pending key switch (bfv_oracle.cpp XCt part A): masked sums of
+    rotations are moded down once; a lone rotation materialises to the eager one."""
+    o = oracle_factory(2)
+    H = o.N // 2
+    rng = np.random.default_rng(5)
+    S = 200
+    a, b = rng.integers(-8, 8, S), rng.integers(-8, 8, S)
+    ca, cb = o.encrypt(a, 0), o.encrypt(b, 1)
+    full = np.zeros(H, dtype=np.int64)
+    full[:S] = a
+    r1, r5 = o.rot_x(ca, 1), o.rot_x(ca, 5)
+    assert r1[1] == 2 and o.rot_x(ca, 0)[1] == 0
+    assert np.array_equal(o.plain(r1), o.rot(ca, 1))
+    m1, m2 = rng.integers(0, 2, S), rng.integers(0, 2, S)
+    s = o.add_any(o.cmult_x(r1, m1), o.cmult_x(r5, m2))
+    want = (np.roll(full, -1)[:S] * m1 + np.roll(full, -5)[:S] * m2) % T
+    assert np.array_equal(o.decrypt(o.plain(s), S), want)
+    # masks distribute exactly over pending sums
+    assert np.array_equal(o.plain(o.cmult_x(o.add_any(r1, r5), m1)),
+                          o.plain(o.add_any(o.cmult_x(r1, m1), o.cmult_x(r5, m1))))
+    # all three parts at once: plain + pending key switch + pending product
+    mix = o.add_any(o.add_any((cb, 0), r1), o.mult_pending(ca, cb))
+    assert mix[1] == 3
+    assert np.array_equal(o.decrypt(o.plain(mix), S), (b + np.roll(full, -1)[:S] + a * b) % T)
+    # masking a value with a pending product materialises it first
+    mm = o.cmult_x(mix, m1)
+    assert mm[1] == 0
+    assert np.array_equal(o.decrypt(o.plain(mm), S), ((b + np.roll(full, -1)[:S] + a * b) * m1) % T)
+
+
 def test_error_conventions(oracle_factory):
     from oracle.bindings import OracleError
 
