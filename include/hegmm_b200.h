@@ -83,6 +83,9 @@ int hgm_add(hgm_ctx* ctx, const hgm_ct* x, const hgm_ct* y, hgm_ct** out);
  * other op, decrypt or export reads the value (same slots, counters, depth). */
 int hgm_mul(hgm_ctx* ctx, const hgm_ct* x, const hgm_ct* y, hgm_ct** out);
 int hgm_cmul(hgm_ctx* ctx, const hgm_ct* x, const int64_t* mask, size_t S, hgm_ct** out);
+/* he_rot's result is a pending key switch (the accumulator over Q and the
+ * special primes): hgm_cmul / hgm_add of rotations work on it and ModDown runs
+ * once, when any other op, decrypt or export reads the value. */
 int hgm_rot(hgm_ctx* ctx, const hgm_ct* x, int64_t offset, hgm_ct** out);
 /* offsets[n], masks[n][S] (row-major); counts n cmult, n-1 add and one rot
  * per non-zero offset, as apply_plan does. */
