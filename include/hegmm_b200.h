@@ -174,7 +174,9 @@ int hgm_batch_decrypt_words(hgm_ctx* ctx, const uint64_t* dev_words, size_t coun
 void hgm_batch_free(hgm_batch* b);
 /* Program facts of a product shape (no GPU needed): stats[12] as hgm_stats,
  * facts[0]=segment [1]=encryptions [2]=rotations after CSE [3]=masked sums
- * [4]=CC-mults [5]=levels [6]=flatten order used. */
+ * [4]=CC-mults [5]=levels [6]=flatten order used [7]=ModDowns (values with a
+ * pending key switch read) [8]=scale-and-round + relinearisations (values with
+ * a pending product read); facts holds 9 entries. */
 int hgm_program_info(int algo, int order, int flags, size_t m, size_t l, size_t n, size_t slots,
                      uint32_t N, uint64_t* stats, uint64_t* facts);
 /* Op stream of a product shape in call order (no GPU needed), same layout as

@@ -50,9 +50,10 @@ def program_info(algo: int, m: int, l: int, n: int, slots: int = 4096, N: int = 
                  flags: int = 0):
     """Op counts (stats[12]) and facts of a compiled HEGMM program (CPU only)."""
     st = np.zeros(12, dtype=np.uint64)
-    facts = np.zeros(7, dtype=np.uint64)
+    facts = np.zeros(9, dtype=np.uint64)
     _check(lib().hgm_program_info(algo, order, flags, m, l, n, slots, N, _ptr(st), _ptr(facts)))
-    keys = ("segment", "encryptions", "rotations", "masked_sums", "cc_mults", "levels", "order")
+    keys = ("segment", "encryptions", "rotations", "masked_sums", "cc_mults", "levels", "order", "moddowns",
+            "rescales")
     return st, dict(zip(keys, (int(x) for x in facts)))
 
 

@@ -914,6 +914,8 @@ int hgm_program_info(int algo, int order, int flags, size_t m, size_t l, size_t 
             facts[4] = p->cloud_sched.mult_count;
             facts[5] = p->cloud_sched.levels.size();
             facts[6] = (u64)p->order;
+            facts[7] = p->cloud_sched.moddown_count;
+            facts[8] = p->cloud_sched.rescale_count;
         }
     });
 }

@@ -301,7 +301,11 @@ Schedule optimise(const Program& p) {
         const PNode& nd = q.nodes[i];
         if (nd.kind == PNode::Rot) ++s.rot_count;
         if (nd.kind == PNode::Comb) ++s.comb_count;
-        if (nd.kind == PNode::Mat) ++s.mat_count;
+        if (nd.kind == PNode::Mat) {
+            ++s.mat_count;
+            if (kind[nd.in[0]] & kPartA) ++s.moddown_count;
+            if (kind[nd.in[0]] & kPartT) ++s.rescale_count;
+        }
         if (kind[i] & kPartT) ++s.pending_count;
         for (size_t t = 0; t < nd.in.size(); ++t) {
             const int x = nd.in[t];

@@ -89,6 +89,7 @@ struct Schedule {
     std::vector<int> pending_out;        // per output: node whose parts are also returned, or -1
     std::vector<char> is_pending_output;
     size_t rot_count = 0, comb_count = 0, mult_count = 0, pending_count = 0, mat_count = 0;
+    size_t moddown_count = 0, rescale_count = 0;  // Mat nodes reading a key-switch / product part
 };
 Schedule optimise(const Program& p);
 

@@ -125,3 +125,16 @@ def test_encrypted_client_transforms_and_square_pad_streams(ref):
                 assert st.astype(int).tolist() == st_ref[:12].astype(int).tolist()
                 if flags:
                     assert st[4] > 0  # client-phase cmults (test_algorithms.cpp:84-94)
+
+
+def test_schedule_defers_moddown_and_rescale():
+    """The compiled 64^3 and cfg3 programs (CPU only): rotations after CSE, and
+    one ModDown per masked sum of rotations / one scale-and-round +
+    relinearisation per product sum (pending key switches and products)."""
+    import paper_2405_02238_b200 as hb
+
+    for algo in (0, 1):
+        _, f = hb.program_info(algo, 64, 64, 64)
+        assert (f["rotations"], f["cc_mults"], f["moddowns"], f["rescales"]) == (189, 64, 126, 1)
+    _, f = hb.program_info(0, 32, 128, 16)
+    assert (f["rotations"], f["cc_mults"], f["moddowns"], f["rescales"]) == (1725, 128, 255, 1)
