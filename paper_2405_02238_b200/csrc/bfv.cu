@@ -973,6 +973,8 @@ Context::~Context() {
     cudaFree(d_cdt_);
     ring_.reset();
     if (dl_host_) cudaFreeHost(dl_host_);
+    for (u32* p : slot_host_)
+        if (p) cudaFreeHost(p);
     cudaStreamDestroy(stream_);
 }
 
@@ -1114,9 +1116,13 @@ size_t Context::mask_budget() const {
         return e ? (size_t)std::atoll(e) << 20 : (size_t)0;
     }();
     if (env) return env;
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || total_b == 0) return (size_t)4 << 30;
-    return std::min<size_t>((size_t)8 << 30, total_b / 16);
+    if (mask_budget_ == 0) {  // once per context (cudaMemGetInfo is not free)
+        size_t free_b = 0, total_b = 0;
+        mask_budget_ = (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || total_b == 0)
+                           ? (size_t)4 << 30
+                           : std::min<size_t>((size_t)8 << 30, total_b / 16);
+    }
+    return mask_budget_;
 }
 
 void Context::trim_mask_cache() {
@@ -1227,6 +1233,16 @@ void Context::decrypt(int n, const u64* const* in, const size_t* S, i64* const* 
         i64* dst = host_out[i];
         for (size_t j = 0; j < S[i]; ++j) dst[j] = (i64)src[j];
     });
+}
+
+u32* Context::pinned_slot(int i, size_t bytes) {
+    if (bytes > slot_cap_[i]) {
+        if (slot_host_[i]) HGM_CUDA(cudaFreeHost(slot_host_[i]));
+        slot_host_[i] = nullptr;
+        HGM_CUDA(cudaMallocHost((void**)&slot_host_[i], bytes));
+        slot_cap_[i] = bytes;
+    }
+    return slot_host_[i];
 }
 
 void* Context::download_buffer(size_t bytes) {

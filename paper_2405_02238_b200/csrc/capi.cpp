@@ -571,9 +571,9 @@ void run_instances(Context& ctx, const MatmulProgram& prog, size_t count,
         std::future<void> unpacking;
     };
     Slot slot[2];
-    for (Slot& sl : slot) {
-        HGM_CUDA(cudaMallocHost((void**)&sl.host, std::max<size_t>(1, chunk * H * sizeof(u32))));
-        HGM_CUDA(cudaEventCreateWithFlags(&sl.ev, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+        slot[i].host = ctx.pinned_slot(i, std::max<size_t>(1, std::min(chunk, count) * H * sizeof(u32)));
+        HGM_CUDA(cudaEventCreateWithFlags(&slot[i].ev, cudaEventDisableTiming));
     }
     auto finish = [&](Slot& sl, size_t c0, int K) {
         sl.unpacking = std::async(std::launch::async, [&prog, &c_of, &sl, c0, K, H, seg = prog.segment]() {
@@ -621,17 +621,11 @@ void run_instances(Context& ctx, const MatmulProgram& prog, size_t count,
     } catch (...) {
         try { drain(); } catch (...) {}
         ctx.sync();
-        for (Slot& sl : slot) {
-            cudaFreeHost(sl.host);
-            cudaEventDestroy(sl.ev);
-        }
+        for (Slot& sl : slot) cudaEventDestroy(sl.ev);
         throw;
     }
     ctx.sync();
-    for (Slot& sl : slot) {
-        cudaFreeHost(sl.host);
-        cudaEventDestroy(sl.ev);
-    }
+    for (Slot& sl : slot) cudaEventDestroy(sl.ev);
 }
 
 void put_counts(const MatmulProgram& prog, uint64_t* stats) {

@@ -80,6 +80,9 @@ class Context {
     }
     // pinned host buffer for result downloads (grown on demand, reused)
     void* download_buffer(size_t bytes);
+    // pinned double buffers of the pipelined batch decrypt (grown on demand, reused:
+    // cudaMallocHost / cudaFreeHost per call cost milliseconds)
+    u32* pinned_slot(int i, size_t bytes);
 
     // ---------------------------------------------------------------- keys
     const u64* ks_key(u32 kid);  // [dnum][2][R][N]; kid = Galois element, 0 = relin
@@ -164,6 +167,8 @@ class Context {
     std::unique_ptr<PinnedRing> ring_;
     void* dl_host_ = nullptr;
     size_t dl_cap_ = 0;
+    u32* slot_host_[2] = {nullptr, nullptr};
+    size_t slot_cap_[2] = {0, 0};
     mutable std::mutex key_mu_;
     std::unordered_map<u32, u64*> keys_;
     std::mutex mask_mu_;
@@ -177,6 +182,7 @@ class Context {
     std::unordered_map<u64, MaskEntry*> masks_by_id_;  // stable MaskData ids
     u64 mask_tick_ = 0;
     size_t mask_bytes_ = 0;
+    mutable size_t mask_budget_ = 0;
 };
 
 }  // namespace hgm
