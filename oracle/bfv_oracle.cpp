@@ -10,10 +10,12 @@
 //   he_mult  : proj/src/backend.cpp:155-167 (a PENDING product: the tensor is
 //              scaled, rounded and relinearised when a non-add op reads it,
 //              so he_add chains of products round once -- see XCt below)
-//   he_cmult : proj/src/backend.cpp:169-183 (mask length == segment)
+//   he_cmult : proj/src/backend.cpp:169-183 (mask length == segment; masks a
+//              value's plain and key-switch parts, see XCt below)
 //   he_rot   : proj/src/backend.cpp:185-197 (left rotation; BFV rotates the
 //              whole N/2-slot row, see backend.hpp:129-131 and SURVEY.md §8
-//              "Row semantics verified")
+//              "Row semantics verified"; a PENDING key switch: ModDown runs
+//              when a non-add, non-mask op reads it, once per masked sum)
 // The arithmetic below is the spec the GPU library reproduces bit-exactly:
 // integer-only scale-and-round, centred (symmetric) digit lifting in ModUp,
 // Galois element g = 3^z mod 2N, and a counter-based sampler.  The oracle's
