@@ -537,6 +537,16 @@ int hgm_phase(const hgm_ctx* c) { return c->phase.load(); }
 
 namespace {
 
+// share of free device memory a lockstep chunk may plan for (HGM_LOCKSTEP_FRAC)
+double lockstep_fraction() {
+    static const double f = [] {
+        const char* e = std::getenv("HGM_LOCKSTEP_FRAC");
+        const double v = e ? std::atof(e) : 0.45;
+        return v > 0.05 && v < 0.95 ? v : 0.45;
+    }();
+    return f;
+}
+
 // Runs `count` instances of one compiled program in lockstep chunks: instance k
 // reads A_k / B_k, encrypts with counters base(k) + s, and writes C_k (and its
 // final ciphertext words when requested).
@@ -550,7 +560,7 @@ void run_instances(Context& ctx, const MatmulProgram& prog, size_t count,
                              prog.sched.pending_count * ctx.pending_words()) * 8;
     size_t free_b = 0, total_b = 0;
     HGM_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    size_t chunk = std::max<size_t>(1, (size_t)(0.45 * (double)free_b) / per_inst);
+    size_t chunk = std::max<size_t>(1, (size_t)(lockstep_fraction() * (double)free_b) / per_inst);
     chunk = std::min<size_t>(chunk, 1024);
     // host packing of chunk i+1 and unpacking of chunk i-1 overlap chunk i's GPU work
     using Packed = std::vector<std::vector<std::vector<i64>>>;
@@ -765,7 +775,7 @@ size_t lockstep_chunk(Context& ctx, const MatmulProgram& prog) {
                              prog.cloud_sched.pending_count * ctx.pending_words()) * 8;
     size_t free_b = 0, total_b = 0;
     HGM_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    size_t chunk = std::max<size_t>(1, (size_t)(0.45 * (double)free_b) / per_inst);
+    size_t chunk = std::max<size_t>(1, (size_t)(lockstep_fraction() * (double)free_b) / per_inst);
     return std::min<size_t>(chunk, 1024);
 }
 
