@@ -26,6 +26,7 @@
 
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -217,6 +218,10 @@ struct orc_ctx {
     std::vector<Poly> s_ntt;  // over Q ++ P
     std::vector<Poly> pk0, pk1;  // over Q
     std::map<u64, std::unique_ptr<KsKey>> keys;
+    // NTT-domain lifts of masks over Q ++ P, by content (a cache: the values are
+    // exactly what cmult / mask_qp would compute again)
+    mutable std::mutex mask_mu;
+    mutable std::map<std::vector<int64_t>, std::shared_ptr<const std::vector<Poly>>> masks;
 
     // constants
     std::vector<u64> delta;            // floor(Q/t) mod q_i
@@ -637,14 +642,34 @@ Ct add(const orc_ctx& c, const Ct& a, const Ct& b) {
     return o;
 }
 
-Ct cmult(const orc_ctx& c, const Ct& a, const int64_t* mask, size_t S) {
+// The batch-encoded mask, centred mod t, lifted to every prime of Q ++ P and
+// NTT'd (cached by content).
+std::shared_ptr<const std::vector<Poly>> mask_ntt(const orc_ctx& c, const int64_t* mask, size_t S) {
+    std::vector<int64_t> key(mask, mask + S);
+    {
+        std::lock_guard<std::mutex> lk(c.mask_mu);
+        auto it = c.masks.find(key);
+        if (it != c.masks.end()) return it->second;
+    }
     Poly m = encode(c, mask, S);
+    auto out = std::make_shared<std::vector<Poly>>(c.R());
+    for (unsigned r = 0; r < c.R(); ++r) {
+        const u64 q = c.pr[r].q;
+        Poly& mm = (*out)[r];
+        mm.resize(c.N);
+        for (unsigned j = 0; j < c.N; ++j) mm[j] = from_signed(centred(m[j], kT), q);
+        ntt_fwd(mm, c.pr[r]);
+    }
+    std::lock_guard<std::mutex> lk(c.mask_mu);
+    return c.masks.emplace(std::move(key), std::move(out)).first->second;
+}
+
+Ct cmult(const orc_ctx& c, const Ct& a, const int64_t* mask, size_t S) {
+    const auto mp = mask_ntt(c, mask, S);
     Ct o = a;
     for (unsigned i = 0; i < c.L; ++i) {
         const u64 q = c.pr[i].q;
-        Poly mm(c.N);
-        for (unsigned j = 0; j < c.N; ++j) mm[j] = from_signed(centred(m[j], kT), q);
-        ntt_fwd(mm, c.pr[i]);
+        const Poly& mm = (*mp)[i];
         for (unsigned j = 0; j < c.N; ++j) {
             o.c0[i][j] = mulmod(a.c0[i][j], mm[j], q);
             o.c1[i][j] = mulmod(a.c1[i][j], mm[j], q);
@@ -856,17 +881,7 @@ XCt rot_x(orc_ctx& c, const Ct& a, i64 z) {
 }
 
 // mask over Q ++ P (NTT domain) for masking pending key switches
-std::vector<Poly> mask_qp(const orc_ctx& c, const int64_t* mask, size_t S) {
-    Poly m = encode(c, mask, S);
-    std::vector<Poly> out(c.R());
-    for (unsigned r = 0; r < c.R(); ++r) {
-        const u64 q = c.pr[r].q;
-        out[r].resize(c.N);
-        for (unsigned j = 0; j < c.N; ++j) out[r][j] = from_signed(centred(m[j], kT), q);
-        ntt_fwd(out[r], c.pr[r]);
-    }
-    return out;
-}
+std::vector<Poly> mask_qp(const orc_ctx& c, const int64_t* mask, size_t S) { return *mask_ntt(c, mask, S); }
 
 XCt cmult_x(orc_ctx& c, const XCt& v, const int64_t* mask, size_t S) {
     XCt o;
@@ -927,9 +942,13 @@ XCt add_any(const orc_ctx& c, const XCt& a, const XCt& b) {
 Ct mult(orc_ctx& c, const Ct& x, const Ct& y) { return materialize(c, mult_pending(c, x, y)); }
 Ct rot(orc_ctx& c, const Ct& a, i64 z) { return materialize(c, rot_x(c, a, z)); }
 
-// value buffer: [X: 2 L N][T: 3 (L + nB) N][A: 2 R N], parts valid per kind bits
+// value buffer: [X: 2 L N][T: 3 (L + nB) N, if kind & 1][A: 2 R N, if kind & 2]
 size_t pending_words(const orc_ctx& c) {
     return (size_t)2 * c.L * c.N + (size_t)3 * (c.L + c.nB) * c.N + (size_t)2 * c.R() * c.N;
+}
+size_t kind_words(const orc_ctx& c, int kind) {
+    return (size_t)2 * c.L * c.N + ((kind & kPartT) ? (size_t)3 * (c.L + c.nB) * c.N : 0) +
+           ((kind & kPartA) ? (size_t)2 * c.R() * c.N : 0);
 }
 XCt load_x(const orc_ctx& c, const uint64_t* buf, int kind) {
     XCt x;
@@ -946,7 +965,7 @@ XCt load_x(const orc_ctx& c, const uint64_t* buf, int kind) {
                 x.T.t[k][r].assign(p, p + c.N);
             }
         }
-    const uint64_t* a = t + (size_t)3 * D * c.N;
+    const uint64_t* a = t + (x.pending ? (size_t)3 * D * c.N : 0);
     if (x.ks) {
         x.A0.resize(R);
         x.A1.resize(R);
@@ -965,7 +984,7 @@ void store_x(const orc_ctx& c, const XCt& x, uint64_t* buf) {
     if (x.pending)
         for (int k = 0; k < 3; ++k)
             for (unsigned r = 0; r < D; ++r) std::memcpy(t + ((size_t)k * D + r) * c.N, x.T.t[k][r].data(), c.N * 8);
-    uint64_t* a = t + (size_t)3 * D * c.N;
+    uint64_t* a = t + (x.pending ? (size_t)3 * D * c.N : 0);
     if (x.ks)
         for (unsigned r = 0; r < R; ++r) {
             std::memcpy(a + (size_t)r * c.N, x.A0[r].data(), c.N * 8);
@@ -1041,6 +1060,7 @@ int orc_mult(orc_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t* out) {
     return guarded([&] { store(*c, mult(*c, load(*c, a), load(*c, b)), out); });
 }
 size_t orc_pending_words(const orc_ctx* c) { return pending_words(*c); }
+size_t orc_kind_words(const orc_ctx* c, int kind) { return kind_words(*c, kind); }
 int orc_mult_pending(orc_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t* out) {
     return guarded([&] { store_x(*c, mult_pending(*c, load(*c, a), load(*c, b)), out); });
 }

@@ -46,6 +46,8 @@ class Oracle:
             L.orc_last_error.restype = ctypes.c_char_p
             L.orc_pending_words.restype = _sz
             L.orc_pending_words.argtypes = [_vp]
+            L.orc_kind_words.restype = _sz
+            L.orc_kind_words.argtypes = [_vp, _int]
             for name, args in {
                 "orc_encrypt": [_vp, _vp, _sz, _u64, _vp],
                 "orc_decrypt": [_vp, _vp, _sz, _vp],
@@ -136,34 +138,34 @@ class Oracle:
     # product, 2 = pending key switch (0: plain words).  he_mult / he_rot /
     # he_cmult / he_add in this form are mult_pending / rot_x / cmult_x / add_any;
     # plain() materialises.
-    def _full(self):
-        return np.zeros(int(self.lib().orc_pending_words(self._h)), dtype=np.uint64)
+    def _buf(self, kind):
+        return np.zeros(int(self.lib().orc_kind_words(self._h, int(kind))), dtype=np.uint64)
 
     def mult_pending(self, a, b):
-        out = self._full()
+        out = self._buf(1)
         self._chk(self.lib().orc_mult_pending(self._h, _p(a), _p(b), _p(out)))
         return (out, 1)
 
     def add_any(self, x, y):
         (a, ka), (b, kb) = x, y
         k = int(ka) | int(kb)
-        out = self._full() if k else self._ct()
+        out = self._buf(k)
         self._chk(self.lib().orc_add_any(self._h, _p(np.ascontiguousarray(a)), int(ka),
                                          _p(np.ascontiguousarray(b)), int(kb), _p(out)))
         return (out, k)
 
     def rot_x(self, a, z: int):
-        out, k = self._full(), ctypes.c_int(0)
+        out, k = self._buf(2), ctypes.c_int(0)
         self._chk(self.lib().orc_rot_x(self._h, _p(np.ascontiguousarray(a)), int(z), _p(out), ctypes.byref(k)))
-        return (out if k.value else out[: self.words].copy(), k.value)
+        return (out[: int(self.lib().orc_kind_words(self._h, k.value))].copy(), k.value)
 
     def cmult_x(self, x, mask):
         a, ka = x
         m = np.ascontiguousarray(mask, dtype=np.int64)
-        out, k = self._full(), ctypes.c_int(0)
+        out, k = self._buf(int(ka) & 2), ctypes.c_int(0)
         self._chk(self.lib().orc_cmult_x(self._h, _p(np.ascontiguousarray(a)), int(ka), _p(m), m.size, _p(out),
                                          ctypes.byref(k)))
-        return (out if k.value else out[: self.words].copy(), k.value)
+        return (out[: int(self.lib().orc_kind_words(self._h, k.value))].copy(), k.value)
 
     def plain(self, x):
         w, k = x

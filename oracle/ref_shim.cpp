@@ -98,14 +98,14 @@ class OracleBackend final : public Backend {
     Ciphertext he_add(const Ciphertext& x, const Ciphertext& y) override {
         same_segment(x, y, "he_add");
         const int kx = kind(x), ky = kind(y);
-        std::vector<std::uint64_t> o((kx | ky) ? pwords_ : words_);
+        std::vector<std::uint64_t> o(orc_kind_words(ctx_, kx | ky));
         check(orc_add_any(ctx_, raw(x), kx, raw(y), ky, o.data()));
         count(&OpStats::n_add);
         return keep(std::move(o), kx | ky, x.segment_length(), std::max(x.depth(), y.depth()));
     }
     Ciphertext he_mult(const Ciphertext& x, const Ciphertext& y) override {
         same_segment(x, y, "he_mult");
-        std::vector<std::uint64_t> o(pwords_);
+        std::vector<std::uint64_t> o(orc_kind_words(ctx_, 1));
         check(orc_mult_pending(ctx_, buf(x), buf(y), o.data()));
         count(&OpStats::n_mult_cc);
         return keep(std::move(o), 1, x.segment_length(), std::max(x.depth(), y.depth()) + 1);
@@ -115,18 +115,18 @@ class OracleBackend final : public Backend {
             throw DimensionError("he_cmult mask length " + std::to_string(mask.size()) +
                                  " does not match segment " +
                                  std::to_string(x.segment_length()));
-        std::vector<std::uint64_t> o(pwords_);
+        std::vector<std::uint64_t> o(orc_kind_words(ctx_, kind(x) & 2));
         int k = 0;
         check(orc_cmult_x(ctx_, raw(x), kind(x), mask.data(), mask.size(), o.data(), &k));
-        if (k == 0) o.resize(words_);
+        o.resize(orc_kind_words(ctx_, k));
         count(&OpStats::n_mult_cp);
         return keep(std::move(o), k, x.segment_length(), x.depth());
     }
     Ciphertext he_rot(const Ciphertext& x, std::ptrdiff_t offset) override {
-        std::vector<std::uint64_t> o(pwords_);
+        std::vector<std::uint64_t> o(orc_kind_words(ctx_, 2));
         int k = 0;
         check(orc_rot_x(ctx_, buf(x), offset, o.data(), &k));
-        if (k == 0) o.resize(words_);
+        o.resize(orc_kind_words(ctx_, k));
         count(&OpStats::n_rot);
         return keep(std::move(o), k, x.segment_length(), x.depth());
     }
