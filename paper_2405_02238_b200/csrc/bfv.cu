@@ -405,6 +405,7 @@ __global__ void k_ks_inner(DevCtx cx, u32 n, const u64* const* D,
                     k0[dg] = packed_dig<SH::S>(__ldg(k + (((size_t)dg * 2 + 0) * R + r) * N + j));
                     k1[dg] = packed_dig<SH::S>(__ldg(k + (((size_t)dg * 2 + 1) * R + r) * N + j));
                 }
+                const Dig<SH::S> pm = split<SH::S>(dp->P_mod_q[r < SH::L ? r : 0]);
                 for (u32 u = 0; u < same; ++u) {
                     const u64* d = D[i0 + u];
                     Cols a0, a1;  // column accumulation, one reduction per output
@@ -413,8 +414,7 @@ __global__ void k_ks_inner(DevCtx cx, u32 n, const u64* const* D,
                         a0.mac(x, k0[dg]);
                         a1.mac(x, k1[dg]);
                     }
-                    if (c0 && r < SH::L)
-                        a0.mac(split<SH::S>(c0[i0 + u][(size_t)r * N + src]), split<SH::S>(dp->P_mod_q[r]));
+                    if (c0 && r < SH::L) a0.mac(split<SH::S>(c0[i0 + u][(size_t)r * N + src]), pm);
                     u64* a = acc[i0 + u];
                     a[(size_t)r * N + j] = reduce_acc(a0.fold<SH::S>(), P);
                     a[((size_t)R + r) * N + j] = reduce_acc(a1.fold<SH::S>(), P);
@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_q_to_b(DevCtx cx, u32 n, const 
             for (u32 k = 0; k < nB; ++k) {
                 // sum_i y_i (Q/q_i) - v Q  (mod b_k), one reduction
                 Cols a;
-                for (u32 i = 0; i < L; ++i) a.mac(yd[i], split<SH::S>(dp->qhat_mod_b[i][k]));
+                for (u32 i = 0; i < L; ++i) a.mac(yd[i], packed_dig<SH::S>(dp->qhat_mod_b_pk[i][k]));
                 a.add<SH::S>(v * dp->neg_Q_mod_b[k]);  // v <= L: < 2^63, a plain addend
                 xb[(size_t)k * N + j] = reduce_acc(a.fold<SH::S>(), dp->pr[L + K + k]);
             }

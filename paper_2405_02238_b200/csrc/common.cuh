@@ -62,6 +62,7 @@ struct DevParams {
     // exact Q -> B
     Frac one_over_q[kMaxL];
     u64 qhat_mod_b[kMaxL][kMaxB], qhat_mod_b_sh[kMaxL][kMaxB];
+    u64 qhat_mod_b_pk[kMaxL][kMaxB];  // packed digits (l | h << 32) at the set's digit width
     u64 Q_mod_b[kMaxB], Q_mod_b_sh[kMaxB];
     u64 neg_Q_mod_b[kMaxB];  // b_j - (Q mod b_j)
     // scale-and-round Q++B -> B

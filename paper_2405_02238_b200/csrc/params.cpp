@@ -193,6 +193,11 @@ HostParams make_params(int id, u64 seed) {
             d.W_sh[i][j] = shoup_of(d.W[i][j], b);
             d.qhat_mod_b[i][j] = prod_mod(without(Qs, i), b);
             d.qhat_mod_b_sh[i][j] = shoup_of(d.qhat_mod_b[i][j], b);
+            {  // digit width of the kernels' shape for this set (bfv.cu: L = 3 -> ShapeQ3, else ShapeQ8)
+                const unsigned S = L == 3 ? 30 : 28;
+                const u64 v = d.qhat_mod_b[i][j];
+                d.qhat_mod_b_pk[i][j] = (v & ((1ULL << S) - 1)) | ((v >> S) << 32);
+            }
         }
         d.B_mod_q[i] = Bq;
         d.B_mod_q_sh[i] = shoup_of(Bq, q);
