@@ -35,3 +35,22 @@ def test_variant_parity(name):
                         "-k", "not acceptance", "tests/test_gpu_parity.py", "tests/test_gpu_hegmm.py"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, f"{name}: {VARIANTS[name]}\n{r.stdout[-3000:]}\n{r.stderr[-2000:]}"
+
+
+def test_many_lockstep_chunks_exact():
+    """hgm_matmul_batch over many lockstep chunks (a small memory share forces
+    several): the pipelined decrypt's pinned double buffers are reused across
+    chunks, and every product must still come back exact and in order."""
+    code = (
+        "import numpy as np, paper_2405_02238_b200 as hb\n"
+        "from paper_2405_02238_b200.workload import batch\n"
+        "ctx = hb.Context(0, 1, 0)\n"
+        "A, B = batch(7, 0, 300, 64, 64, 64, -8, 7)\n"
+        "C, _ = ctx.matmul_batch(A, B, algo=0)\n"
+        "bad = [i for i in range(300) if not np.array_equal(C[i], (A[i] @ B[i]) % 65537)]\n"
+        "assert not bad, bad\n"
+        "print('ok')\n")
+    env = dict(os.environ)
+    env["HGM_LOCKSTEP_FRAC"] = "0.06"
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
