@@ -29,8 +29,7 @@
  *   HGM_EOVERFLOW -> OverflowError, anything else -> Error.
  * Ciphertexts are immutable, reference counted handles owned by the caller
  * (hgm_ct_release).  Operations are recorded and executed lazily on the GPU;
- * hgm_decrypt / hgm_ct_export / hgm_flush force execution.  A handle must be
- * released before its context is destroyed.
+ * hgm_decrypt / hgm_ct_export / hgm_flush force execution.
  * Slot semantics: slot_count = N/2 values per ciphertext row, values mod
  * t = 65537, decrypted values canonical in [0, t); rotation is cyclic over the
  * full N/2-slot row ("Row semantics").
@@ -63,19 +62,63 @@ enum { HGM_PHASE_CLIENT = 0, HGM_PHASE_CLOUD = 1 };
 typedef struct hgm_ctx hgm_ctx;
 typedef struct hgm_ct hgm_ct;
 
+/* Sessions are reference counted: every live handle and batch keeps its
+ * context alive, so hgm_ctx_destroy with handles outstanding only drops the
+ * creator's reference (the device memory goes with the last handle).  Every
+ * entry point makes the context's device current for its duration and
+ * restores the caller's current device.
+ *
+ * Randomness.  Keys and encryption noise come from a counter-based generator
+ * keyed by `seed` (splitmix64 finalisers, shared bit for bit with the CPU
+ * oracle).  A caller-chosen seed is a TEST / PARITY mode: anyone who knows
+ * the seed can regenerate the secret key.  HGM_CTX_OS_SEED draws the seed
+ * from the OS CSPRNG instead and never exports it (hgm_ctx_info reports 0);
+ * for keys held outside the library, create the cloud context with
+ * HGM_CTX_KEYLESS and upload them (hgm_key_upload), and encrypt with
+ * host-sampled noise (hgm_encrypt_noise). */
+#define HGM_CTX_KEYLESS 1 /* no keys are generated: upload sk / pk / switching keys */
+#define HGM_CTX_OS_SEED 2 /* seed from /dev/urandom, not exported */
 hgm_ctx* hgm_ctx_create(int param_id, uint64_t seed, int device);
+hgm_ctx* hgm_ctx_create_ex(int param_id, uint64_t seed, int device, int flags);
 void hgm_ctx_destroy(hgm_ctx* ctx);
 const char* hgm_last_error(void);
 
-/* info[0]=N [1]=L [2]=K [3]=nB [4]=dnum [5]=t [6]=alpha [7]=seed, then primes */
+/* info[0]=N [1]=L [2]=K [3]=nB [4]=dnum [5]=t [6]=alpha [7]=seed (0 if OS seeded), then primes */
 int hgm_ctx_info(const hgm_ctx* ctx, uint64_t* info, size_t cap);
 size_t hgm_slot_count(const hgm_ctx* ctx);
 size_t hgm_ct_words(const hgm_ctx* ctx);
 
-/* encrypt uses (and advances) the session's encryption counter; the
- * _at variant takes it explicitly (the counter selects u, e0, e1). */
+/* Key material (SURVEY.md 8b hgm_keys_upload), canonical residues in the NTT
+ * domain, words = hgm_key_words(kind):
+ *   kind 0 secret key [R][N] (s over Q ++ P, R = L + K primes)
+ *   kind 1 public key [2][L][N] (pk0 = -a s + e, pk1 = a)
+ *   kind 2 switching key of Galois element `elt` (0 = relinearisation, s^2)
+ *          [dnum][2][R][N] (row dg: -a s + e + [r in digit dg] P s', a)
+ * Upload replaces the context's copy; export of a switching key the context
+ * lacks generates it (needs the secret key).  A context without the secret
+ * key cannot decrypt (HGM_EARG) and fails on a rotation / product whose key was
+ * not uploaded (HGM_EARG, naming the Galois element). */
+size_t hgm_key_words(const hgm_ctx* ctx, int kind);
+int hgm_key_export(hgm_ctx* ctx, int kind, uint32_t elt, uint64_t* words, size_t n);
+int hgm_key_upload(hgm_ctx* ctx, int kind, uint32_t elt, const uint64_t* words, size_t n);
+int hgm_key_drop_secret(hgm_ctx* ctx);
+int hgm_key_has(const hgm_ctx* ctx, int kind); /* kind 0 / 1 */
+/* Galois element of a left rotation by `offset` slots: 3^(offset mod N/2) mod 2N */
+uint32_t hgm_galois_element(const hgm_ctx* ctx, int64_t offset);
+
+/* encrypt reserves (atomically) and uses the next session encryption counter;
+ * the _at variant takes it explicitly (the counter selects u, e0, e1). */
 int hgm_encrypt(hgm_ctx* ctx, const int64_t* values, size_t S, hgm_ct** out);
 int hgm_encrypt_at(hgm_ctx* ctx, const int64_t* values, size_t S, uint64_t counter, hgm_ct** out);
+/* Encryption with host-sampled randomness: u (ternary), e0, e1 are N signed
+ * coefficients each (SURVEY.md 8b hgm_rand).  Counts as one encrypt. */
+int hgm_encrypt_noise(hgm_ctx* ctx, const int64_t* values, size_t S, const int64_t* u, const int64_t* e0,
+                      const int64_t* e1, hgm_ct** out);
+/* Reserves n consecutive session counters; returns the first. */
+uint64_t hgm_reserve_counters(hgm_ctx* ctx, uint64_t n);
+/* counter0 value for the batch entry points: take count * E counters from the
+ * session (hgm_reserve_counters) instead of an explicit range */
+#define HGM_COUNTER_AUTO UINT64_MAX
 int hgm_decrypt(hgm_ctx* ctx, const hgm_ct* ct, int64_t* out, size_t cap);
 int hgm_add(hgm_ctx* ctx, const hgm_ct* x, const hgm_ct* y, hgm_ct** out);
 /* he_mult's result is a pending product: hgm_add over products sums their
@@ -92,6 +135,8 @@ int hgm_rot(hgm_ctx* ctx, const hgm_ct* x, int64_t offset, hgm_ct** out);
 int hgm_apply_plan(hgm_ctx* ctx, const hgm_ct* x, size_t n, const int64_t* offsets,
                    const int64_t* masks, size_t S, hgm_ct** out);
 
+/* Executes every pending operation whose result a pinned handle still
+ * refers to (unpinned handles stay lazy); synchronous. */
 int hgm_flush(hgm_ctx* ctx);
 int hgm_ct_export(hgm_ctx* ctx, const hgm_ct* ct, uint64_t* words);
 int hgm_ct_import(hgm_ctx* ctx, const uint64_t* words, size_t S, size_t depth, hgm_ct** out);
@@ -179,6 +224,10 @@ void hgm_batch_free(hgm_batch* b);
  * a pending product read); facts holds 9 entries. */
 int hgm_program_info(int algo, int order, int flags, size_t m, size_t l, size_t n, size_t slots,
                      uint32_t N, uint64_t* stats, uint64_t* facts);
+/* Switching keys a product shape needs (no GPU): sorted Galois elements, 0
+ * (relinearisation) first when it multiplies; returns the count (or -error). */
+long hgm_program_keys(int algo, int order, int flags, size_t m, size_t l, size_t n, size_t slots, uint32_t N,
+                      uint32_t* elements, size_t cap);
 /* Op stream of a product shape in call order (no GPU needed), same layout as
  * the reference trace: hdr[3*i] = kind (0 enc 1 dec 2 add 3 mult 4 cmult 5 rot),
  * hdr[3*i+1] = rotation offset / segment, hdr[3*i+2] = data length; data = the

@@ -46,9 +46,19 @@ BfvGpuBackend::~BfvGpuBackend() {
 }
 
 Ciphertext BfvGpuBackend::wrap(hgm_ct* h, std::size_t segment, std::size_t depth) {
-    // the caller's Ciphertext lifetime is not observable: keep the recipe only
+    // the caller's Ciphertext lifetime is not observable per handle: keep the recipe only
     hgm_ct_set_pinned(h, 0);
     std::lock_guard<std::mutex> lk(mu_);
+    // ... but the minter's live count is (LiveTracker, backend.cpp:50-90; reset_stats
+    // sets peak = current): when no ciphertext this backend handed out is alive any
+    // more -- e.g. between two basic_mm calls on one session -- every GPU handle is
+    // dead and is released, so a long-lived backend does not grow without bound.
+    minter_.reset_stats();
+    if (minter_.peak_live_ciphertexts() <= ones_.size() && !handles_.empty()) {
+        for (hgm_ct* old : handles_) hgm_ct_release(old);
+        handles_.clear();
+        ++epoch_;
+    }
     const std::uint64_t id = handles_.size();
     handles_.push_back(h);
     minter_.set_phase(phase());

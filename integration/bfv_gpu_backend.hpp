@@ -55,6 +55,15 @@ class BfvGpuBackend final : public Backend {
     // GPU words (2*L*N, NTT domain) of a ciphertext produced by this backend
     std::vector<std::uint64_t> export_words(const Ciphertext& ct);
     hgm_ctx* raw() const { return ctx_; }
+    // GPU handles currently held / handle sets released (no minted ciphertext alive)
+    std::size_t held_handles() const {
+        std::lock_guard<std::mutex> lk(mu_);
+        return handles_.size();
+    }
+    std::size_t epochs() const {
+        std::lock_guard<std::mutex> lk(mu_);
+        return epoch_;
+    }
 
   private:
     Ciphertext wrap(hgm_ct* h, std::size_t segment, std::size_t depth);
@@ -65,7 +74,8 @@ class BfvGpuBackend final : public Backend {
     BackendConfig cfg_;
     SlotBackend minter_;
     mutable std::mutex mu_;
-    std::vector<hgm_ct*> handles_;                 // id -> GPU handle
+    std::vector<hgm_ct*> handles_;                 // id -> GPU handle (this epoch)
+    std::size_t epoch_ = 0;                        // handle sets released so far
     std::map<std::size_t, Ciphertext> ones_;       // per segment, for depth minting
 };
 

@@ -1,6 +1,7 @@
 // dropin_capi.cpp -- test entry: the REFERENCE's own algorithms (compiled from
 // /root/reference sources into oracle/_ref/libhegmm_ref.so) driving the B200
 // through hegmm::BfvGpuBackend.  Used by tests/test_gpu_dropin.py.
+#include <algorithm>
 #include <cstring>
 #include <optional>
 
@@ -75,6 +76,31 @@ int dropin_mm(int param_id, std::uint64_t seed, int algo, int order, const std::
     } catch (const CapacityError& e) {
         g_err = e.what();
         return 2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 3;
+    }
+}
+
+// `reps` products on ONE long-lived backend session (the handle table must
+// not grow across products): info[0] = handle sets released, info[1] = handles
+// held at the end, info[2] = most handles held at once.
+int dropin_repeat(int param_id, int algo, const std::int64_t* A, std::size_t m, std::size_t l,
+                  const std::int64_t* B, std::size_t n, int reps, std::int64_t* C, std::uint64_t* info) {
+    try {
+        BfvGpuBackend gpu(param_id, 1, 0);
+        Matrix a(m, l, std::vector<value_t>(A, A + m * l));
+        Matrix b(l, n, std::vector<value_t>(B, B + l * n));
+        std::size_t most = 0;
+        for (int r = 0; r < reps; ++r) {
+            Matrix c = algo == 0 ? basic_mm(a, b, gpu) : enhanced_mm(a, b, gpu);
+            std::memcpy(C + (std::size_t)r * m * n, c.data().data(), m * n * 8);
+            most = std::max(most, gpu.held_handles());
+        }
+        info[0] = gpu.epochs();
+        info[1] = gpu.held_handles();
+        info[2] = most;
+        return 0;
     } catch (const std::exception& e) {
         g_err = e.what();
         return 3;

@@ -574,15 +574,25 @@ Poly encode(const orc_ctx& c, const int64_t* v, size_t S) {
     return slots;
 }
 
+// encryption with given randomness: c0 = pk0 u + e0 + Delta m, c1 = pk1 u + e1
+Ct encrypt_with(orc_ctx& c, const int64_t* v, size_t S, const std::vector<i64>& u, const std::vector<i64>& e0,
+                const std::vector<i64>& e1);
+
 Ct encrypt(orc_ctx& c, const int64_t* v, size_t S, u64 ctr) {
     const unsigned N = c.N;
-    Poly m = encode(c, v, S);
     std::vector<i64> u(N), e0(N), e1(N);
     for (unsigned j = 0; j < N; ++j) {
         u[j] = ternary(c.seed, kStreamEncU | ctr, j);
         e0[j] = gauss(c.seed, kStreamEncE0 | ctr, j);
         e1[j] = gauss(c.seed, kStreamEncE1 | ctr, j);
     }
+    return encrypt_with(c, v, S, u, e0, e1);
+}
+
+Ct encrypt_with(orc_ctx& c, const int64_t* v, size_t S, const std::vector<i64>& u, const std::vector<i64>& e0,
+                const std::vector<i64>& e1) {
+    const unsigned N = c.N;
+    Poly m = encode(c, v, S);
     Ct ct;
     ct.c0.resize(c.L); ct.c1.resize(c.L);
     for (unsigned i = 0; i < c.L; ++i) {
@@ -1125,6 +1135,86 @@ int orc_encode(orc_ctx* c, const int64_t* values, size_t S, uint64_t* m_out) {
         std::memcpy(m_out, m.data(), c->N * 8);
     });
 }
+size_t orc_key_words(const orc_ctx* c, int kind) {
+    switch (kind) {
+        case 0: return (size_t)c->R() * c->N;
+        case 1: return (size_t)2 * c->L * c->N;
+        case 2: return (size_t)c->dnum * 2 * c->R() * c->N;
+        default: return 0;
+    }
+}
+
+int orc_key_export(orc_ctx* c, int kind, uint32_t elt, uint64_t* w) {
+    return guarded([&] {
+        const size_t N = c->N;
+        if (kind == 0) {
+            for (unsigned r = 0; r < c->R(); ++r) std::memcpy(w + r * N, c->s_ntt[r].data(), N * 8);
+        } else if (kind == 1) {
+            for (unsigned i = 0; i < c->L; ++i) {
+                std::memcpy(w + i * N, c->pk0[i].data(), N * 8);
+                std::memcpy(w + (c->L + i) * N, c->pk1[i].data(), N * 8);
+            }
+        } else if (kind == 2) {
+            const KsKey& k = get_key(*c, elt);
+            const unsigned R = c->R();
+            for (unsigned d = 0; d < c->dnum; ++d)
+                for (unsigned r = 0; r < R; ++r) {
+                    std::memcpy(w + (((size_t)d * 2 + 0) * R + r) * N, k.k0[d][r].data(), N * 8);
+                    std::memcpy(w + (((size_t)d * 2 + 1) * R + r) * N, k.k1[d][r].data(), N * 8);
+                }
+        } else {
+            throw std::invalid_argument("key kind");
+        }
+    });
+}
+
+// Installs key material produced elsewhere (the layouts of orc_key_export).
+// An imported secret key also replaces the coefficient form the oracle derives
+// Galois and relinearisation keys from (centred INTT of its first limb).
+int orc_key_import(orc_ctx* c, int kind, uint32_t elt, const uint64_t* w) {
+    return guarded([&] {
+        const size_t N = c->N;
+        if (kind == 0) {
+            for (unsigned r = 0; r < c->R(); ++r) c->s_ntt[r].assign(w + r * N, w + (r + 1) * N);
+            Poly s0 = c->s_ntt[0];
+            ntt_inv(s0, c->pr[0]);
+            const u64 q = c->pr[0].q;
+            for (size_t j = 0; j < N; ++j) c->s_coeff[j] = s0[j] > q / 2 ? -(i64)(q - s0[j]) : (i64)s0[j];
+            c->keys.clear();  // keys derived from the old secret
+        } else if (kind == 1) {
+            for (unsigned i = 0; i < c->L; ++i) {
+                c->pk0[i].assign(w + i * N, w + (i + 1) * N);
+                c->pk1[i].assign(w + (c->L + i) * N, w + (c->L + i + 1) * N);
+            }
+        } else if (kind == 2) {
+            const unsigned R = c->R();
+            auto k = std::make_unique<KsKey>();
+            k->k0.assign(c->dnum, std::vector<Poly>(R));
+            k->k1.assign(c->dnum, std::vector<Poly>(R));
+            for (unsigned d = 0; d < c->dnum; ++d)
+                for (unsigned r = 0; r < R; ++r) {
+                    const uint64_t* a = w + (((size_t)d * 2 + 0) * R + r) * N;
+                    const uint64_t* b = w + (((size_t)d * 2 + 1) * R + r) * N;
+                    k->k0[d][r].assign(a, a + N);
+                    k->k1[d][r].assign(b, b + N);
+                }
+            c->keys[elt] = std::move(k);
+        } else {
+            throw std::invalid_argument("key kind");
+        }
+    });
+}
+
+int orc_encrypt_noise(orc_ctx* c, const int64_t* values, size_t S, const int64_t* u, const int64_t* e0,
+                      const int64_t* e1, uint64_t* out) {
+    return guarded([&] {
+        check_segment(*c, S);
+        const size_t N = c->N;
+        std::vector<i64> U(u, u + N), E0(e0, e0 + N), E1(e1, e1 + N);
+        store(*c, encrypt_with(*c, values, S, U, E0, E1), out);
+    });
+}
+
 uint64_t orc_prng(uint64_t seed, uint64_t stream, uint64_t idx) { return prng(seed, stream, idx); }
 int64_t orc_gauss(uint64_t seed, uint64_t stream, uint64_t idx) { return gauss(seed, stream, idx); }
 

@@ -64,10 +64,15 @@ class Oracle:
                 "orc_ntt_fwd": [_vp, _int, _vp],
                 "orc_ntt_inv": [_vp, _int, _vp],
                 "orc_encode": [_vp, _vp, _sz, _vp],
+                "orc_key_export": [_vp, _int, ctypes.c_uint32, _vp],
+                "orc_key_import": [_vp, _int, ctypes.c_uint32, _vp],
+                "orc_encrypt_noise": [_vp, _vp, _sz, _vp, _vp, _vp, _vp],
             }.items():
                 fn = getattr(L, name)
                 fn.restype = _int
                 fn.argtypes = args
+            L.orc_key_words.restype = _sz
+            L.orc_key_words.argtypes = [_vp, _int]
             L.orc_noise_budget.restype = ctypes.c_double
             L.orc_noise_budget.argtypes = [_vp, _vp]
             L.orc_prng.restype = _u64
@@ -101,6 +106,23 @@ class Oracle:
 
     def _ct(self):
         return np.zeros(self.words, dtype=np.uint64)
+
+    def export_key(self, kind: int, elt: int = 0) -> np.ndarray:
+        w = np.zeros(self.lib().orc_key_words(self._h, kind), dtype=np.uint64)
+        self._chk(self.lib().orc_key_export(self._h, kind, elt, _p(w)))
+        return w
+
+    def import_key(self, kind: int, words, elt: int = 0) -> None:
+        w = np.ascontiguousarray(words, dtype=np.uint64)
+        assert w.size == self.lib().orc_key_words(self._h, kind)
+        self._chk(self.lib().orc_key_import(self._h, kind, elt, _p(w)))
+
+    def encrypt_noise(self, values, u, e0, e1) -> np.ndarray:
+        v = np.ascontiguousarray(values, dtype=np.int64)
+        uu, a, b = (np.ascontiguousarray(x, dtype=np.int64) for x in (u, e0, e1))
+        out = self._ct()
+        self._chk(self.lib().orc_encrypt_noise(self._h, _p(v), v.size, _p(uu), _p(a), _p(b), _p(out)))
+        return out
 
     def encrypt(self, values, counter: int) -> np.ndarray:
         v = np.ascontiguousarray(values, dtype=np.int64)

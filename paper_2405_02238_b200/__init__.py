@@ -31,7 +31,12 @@ EXPORTS = (
     "hgm_test_ntt", "hgm_launch_count", "hgm_batch_encrypt", "hgm_batch_cloud", "hgm_batch_output",
     "hgm_batch_decrypt", "hgm_batch_decrypt_words", "hgm_batch_free", "hgm_program_info",
     "hgm_program_stream", "hgm_plan_info", "hgm_blocked_mm",
+    "hgm_ctx_create_ex", "hgm_key_words", "hgm_key_export", "hgm_key_upload", "hgm_key_drop_secret",
+    "hgm_key_has", "hgm_galois_element", "hgm_encrypt_noise", "hgm_reserve_counters", "hgm_program_keys",
 )
+CTX_KEYLESS, CTX_OS_SEED = 1, 2
+COUNTER_AUTO = (1 << 64) - 1
+KEY_SECRET, KEY_PUBLIC, KEY_SWITCH = 0, 1, 2
 FLAG_ENCRYPTED_CLIENT_TRANSFORMS = 1
 ALGOS = {"basic": 0, "enhanced": 1, "square_pad": 2}
 
@@ -57,6 +62,16 @@ def program_info(algo: int, m: int, l: int, n: int, slots: int = 4096, N: int = 
     return st, dict(zip(keys, (int(x) for x in facts)))
 
 
+def program_keys(algo: int, m: int, l: int, n: int, slots: int = 4096, N: int = 8192, order: int = -1,
+                 flags: int = 0):
+    """Switching keys a product shape needs: Galois elements, 0 = relinearisation."""
+    out = np.zeros(8192, dtype=np.uint32)
+    cnt = lib().hgm_program_keys(algo, order, flags, m, l, n, slots, N, _ptr(out), out.size)
+    if cnt < 0:
+        _check(-cnt)
+    return [int(x) for x in out[:cnt]]
+
+
 def program_stream(algo: int, m: int, l: int, n: int, slots: int = 4096, N: int = 8192, order: int = -1,
                    flags: int = 0):
     """The recorded op stream (reference trace layout): (hdr[k,3], mask data)."""
@@ -77,7 +92,7 @@ class Batch:
     """Encrypted inputs of `count` instances resident in HBM (client phase done)."""
 
     def __init__(self, ctx: "Context", A: np.ndarray, B: np.ndarray, algo: int = 0, order: int = -1,
-                 counter0: int = 0, flags: int = 0):
+                 counter0: Optional[int] = None, flags: int = 0):
         A = _as_i64(A)
         B = _as_i64(B)
         if A.ndim == 2:
@@ -87,7 +102,7 @@ class Batch:
         self.n = B.shape[2]
         h = ctypes.c_void_p()
         _check(lib().hgm_batch_encrypt(ctx._h, algo, order, flags, self.m, self.l, self.n, self.count,
-                                       _ptr(A), _ptr(B), counter0, ctypes.byref(h)))
+                                       _ptr(A), _ptr(B), _counter(counter0), ctypes.byref(h)))
         self._h = h.value
 
     def cloud(self) -> float:
@@ -196,6 +211,16 @@ def lib() -> ctypes.CDLL:
         "hgm_program_stream": (ctypes.c_long, [_int, _int, _int, _sz, _sz, _sz, _sz, ctypes.c_uint32, _vp,
                                                _sz, _vp, _sz, _vp]),
         "hgm_plan_info": (ctypes.c_long, [_int, _sz, _sz, _sz, _sz, _int, _sz, _vp, _vp, _sz]),
+        "hgm_ctx_create_ex": (_vp, [_int, _u64, _int, _int]),
+        "hgm_key_words": (_sz, [_vp, _int]),
+        "hgm_key_export": (_int, [_vp, _int, ctypes.c_uint32, _vp, _sz]),
+        "hgm_key_upload": (_int, [_vp, _int, ctypes.c_uint32, _vp, _sz]),
+        "hgm_key_drop_secret": (_int, [_vp]),
+        "hgm_key_has": (_int, [_vp, _int]),
+        "hgm_galois_element": (ctypes.c_uint32, [_vp, _i64]),
+        "hgm_encrypt_noise": (_int, [_vp, _vp, _sz, _vp, _vp, _vp, _vp]),
+        "hgm_reserve_counters": (_u64, [_vp, _u64]),
+        "hgm_program_keys": (ctypes.c_long, [_int, _int, _int, _sz, _sz, _sz, _sz, ctypes.c_uint32, _vp, _sz]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -217,6 +242,11 @@ def _ptr(a: np.ndarray) -> ctypes.c_void_p:
 
 def _as_i64(v) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(v, dtype=np.int64))
+
+
+def _counter(c: Optional[int]) -> int:
+    """None -> COUNTER_AUTO: the library reserves fresh counters from the session."""
+    return COUNTER_AUTO if c is None else int(c)
 
 
 class Ciphertext:
@@ -252,9 +282,12 @@ class Ciphertext:
 class Context:
     """One backend session on one GPU (reference SlotBackend, backend.hpp:132-163)."""
 
-    def __init__(self, param_id: int = 0, seed: int = 1, device: int = 0):
+    def __init__(self, param_id: int = 0, seed: int = 1, device: int = 0, flags: int = 0):
+        """seed: a TEST / PARITY seed (keys and noise are derived from it, shared
+        with the CPU oracle); flags: CTX_KEYLESS (keys are uploaded), CTX_OS_SEED
+        (the seed comes from the OS CSPRNG and is never exported)."""
         L = lib()
-        h = L.hgm_ctx_create(param_id, seed, device)
+        h = L.hgm_ctx_create_ex(param_id, seed, device, flags)
         if not h:
             raise HEError(L.hgm_last_error().decode(errors="replace"))
         self._h = h
@@ -266,9 +299,49 @@ class Context:
         self.ct_words = 2 * self.L * self.N
 
     def close(self) -> None:
+        """Drops this object's reference; the native context lives on until its
+        last Ciphertext / Batch is released (the library reference counts it)."""
         if self._h:
             lib().hgm_ctx_destroy(self._h)
             self._h = None
+
+    # -- key material (include/hegmm_b200.h, hgm_key_*) --------------------------
+    def key_words(self, kind: int) -> int:
+        return int(lib().hgm_key_words(self._h, kind))
+
+    def export_key(self, kind: int, elt: int = 0) -> np.ndarray:
+        w = np.zeros(self.key_words(kind), dtype=np.uint64)
+        _check(lib().hgm_key_export(self._h, kind, elt, _ptr(w), w.size))
+        return w
+
+    def upload_key(self, kind: int, words: np.ndarray, elt: int = 0) -> None:
+        w = np.ascontiguousarray(words, dtype=np.uint64)
+        _check(lib().hgm_key_upload(self._h, kind, elt, _ptr(w), w.size))
+
+    def drop_secret(self) -> None:
+        _check(lib().hgm_key_drop_secret(self._h))
+
+    def has_key(self, kind: int) -> bool:
+        return bool(lib().hgm_key_has(self._h, kind))
+
+    def galois_element(self, offset: int) -> int:
+        return int(lib().hgm_galois_element(self._h, int(offset)))
+
+    def reserve_counters(self, n: int) -> int:
+        return int(lib().hgm_reserve_counters(self._h, n))
+
+    def encrypt_noise(self, values: Sequence[int], u, e0, e1) -> Ciphertext:
+        """Encryption with host-sampled randomness (u ternary, e0 / e1 small; N each)."""
+        v = _as_i64(values)
+        uu, a, b = (_as_i64(x) for x in (u, e0, e1))
+        if not uu.size == a.size == b.size == self.N:
+            raise DimensionError(f"noise vectors must have N = {self.N} coefficients")
+        out = self._out()
+        _check(lib().hgm_encrypt_noise(self._h, _ptr(v), v.size, _ptr(uu), _ptr(a), _ptr(b), ctypes.byref(out)))
+        return Ciphertext(out.value, self)
+
+    def flush(self) -> None:
+        _check(lib().hgm_flush(self._h))
 
     def __del__(self):
         try:
@@ -366,7 +439,7 @@ class Context:
         return Ciphertext(out.value, self)
 
     def matmul_batch(self, A: np.ndarray, B: np.ndarray, algo: int = 0, order: int = -1,
-                     counter0: int = 0, export: bool = False, flags: int = 0):
+                     counter0: Optional[int] = None, export: bool = False, flags: int = 0):
         """C_i = A_i B_i mod t for a batch (count, m, l) x (count, l, n)."""
         A = _as_i64(A)
         B = _as_i64(B)
@@ -380,14 +453,15 @@ class Context:
         if export:
             words = np.zeros((cnt, self.ct_words), dtype=np.uint64)
             _check(lib().hgm_matmul_batch_export(self._h, algo, order, flags, m, l, n, cnt, _ptr(A), _ptr(B),
-                                                 _ptr(C), counter0, _ptr(words)))
+                                                 _ptr(C), _counter(counter0), _ptr(words)))
             return C, words
         stats = np.zeros(12, dtype=np.uint64)
         _check(lib().hgm_matmul_batch(self._h, algo, order, flags, m, l, n, cnt, _ptr(A), _ptr(B), _ptr(C),
-                                      counter0, _ptr(stats)))
+                                      _counter(counter0), _ptr(stats)))
         return C, stats
 
-    def blocked_mm(self, A: np.ndarray, B: np.ndarray, rows, mids, cols, algo: int = 1, counter0: int = 0):
+    def blocked_mm(self, A: np.ndarray, B: np.ndarray, rows, mids, cols, algo: int = 1,
+                   counter0: Optional[int] = None):
         """blocked_mm (algorithms.cpp:434-498): returns (C mod t, per-block log
         rows of (algo used, fell_back, block m, block l))."""
         A = _as_i64(A)
@@ -398,7 +472,7 @@ class Context:
         C = np.zeros((m, n), dtype=np.int64)
         log = np.zeros((r.size * md.size * c.size, 4), dtype=np.int32)
         _check(lib().hgm_blocked_mm(self._h, algo, m, l, n, _ptr(r), r.size, _ptr(md), md.size, _ptr(c), c.size,
-                                    _ptr(A), _ptr(B), _ptr(C), counter0, _ptr(log)))
+                                    _ptr(A), _ptr(B), _ptr(C), _counter(counter0), _ptr(log)))
         return C, log
 
     def decrypt_words(self, words, segment: int) -> np.ndarray:

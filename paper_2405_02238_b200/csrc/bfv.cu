@@ -98,19 +98,22 @@ inline u32 to_slot_residue(i64 x) {
 }
 
 // oracle encrypt(): sample u, e0, e1; c0 = e0 + Delta m, c1 = e1 (coefficient form)
+// noise (optional): host-sampled [n][3][N] signed coefficients (u, e0, e1) in
+// place of the counter PRNG (hgm_encrypt_noise)
 template <typename SH>
 __global__ void __launch_bounds__(kThreads, 4) k_enc_lift(DevCtx cx, u32 n, const u64* m, const u64* ctr,
-                           u64* U, u64* const* out) {
+                           const i64* noise, u64* U, u64* const* out) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = SH::L;
     const u64 seed = cx.seed;
     ITEM_LOOP {
-        const u64 c = ctr[item];
+        const u64 c = noise ? 0 : ctr[item];
+        const i64* nz = noise ? noise + (size_t)item * 3 * N : nullptr;
         u64* o = out[item];
         COEF_LOOP {
-            const i64 u = ternary(seed, kStreamEncU | c, j);
-            const i64 e0 = gauss(seed, kStreamEncE0 | c, j, cx.cdt);
-            const i64 e1 = gauss(seed, kStreamEncE1 | c, j, cx.cdt);
+            const i64 u = nz ? nz[j] : ternary(seed, kStreamEncU | c, j);
+            const i64 e0 = nz ? nz[N + j] : gauss(seed, kStreamEncE0 | c, j, cx.cdt);
+            const i64 e1 = nz ? nz[2 * N + j] : gauss(seed, kStreamEncE1 | c, j, cx.cdt);
             const u64 mj = m[(size_t)item * N + j];
             for (u32 i = 0; i < L; ++i) {
                 const u64 q = dp->pr[i].q;
@@ -920,7 +923,21 @@ void* PinnedRing::upload(const void* src, size_t bytes, cudaStream_t s) {
 }
 
 // ==================================================================== Context
-Context::Context(int param_id, u64 seed, int device) : device_(device) {
+namespace {
+// Makes the context's device current for a scope and restores the caller's.
+struct DeviceScope {
+    int prev = -1, want;
+    explicit DeviceScope(int d) : want(d) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != want) cudaSetDevice(want);
+    }
+    ~DeviceScope() {
+        if (prev >= 0 && prev != want) cudaSetDevice(prev);
+    }
+};
+}  // namespace
+
+Context::Context(int param_id, u64 seed, int device, bool keyless) : device_(device), keyless_(keyless) {
     hp_ = make_params(param_id, seed);
     // all primes of one set share their bit length (centred_lift relies on it)
     for (size_t r = 1; r < hp_.primes.size(); ++r)
@@ -955,11 +972,11 @@ Context::Context(int param_id, u64 seed, int device) : device_(device) {
     cx_.cdt = d_cdt_;
     cx_.seed = seed;
     cx_.pid = (u32)param_id;
-    build_keys();
+    if (!keyless_) build_keys();
 }
 
 Context::~Context() {
-    cudaSetDevice(device_);
+    DeviceScope dev(device_);
     cudaStreamSynchronize(stream_);
     for (auto& kv : keys_) cudaFree(kv.second);
     for (auto& kv : masks_)
@@ -1027,6 +1044,10 @@ const u64* Context::ks_key(u32 kid) {
         auto it = keys_.find(kid);
         if (it != keys_.end()) return it->second;
     }
+    if (!d_sk_)
+        throw std::invalid_argument("no key-switching key for Galois element " + std::to_string(kid) +
+                                    (kid == 0 ? " (relinearisation)" : "") +
+                                    " and no secret key to generate it: upload it with hgm_key_upload");
     const u32 N = hp_.N, R = hp_.R, dnum = hp_.dnum;
     u64* key = nullptr;
     HGM_CUDA(cudaMallocAsync((void**)&key, (size_t)dnum * 2 * R * N * 8, stream_));
@@ -1053,6 +1074,79 @@ const u64* Context::ks_key(u32 kid) {
 void Context::ensure_galois_keys(const std::vector<u32>& elements) {
     for (u32 g : elements)
         if (g != 1) ks_key(g);
+}
+
+size_t Context::key_words(int kind) const {
+    const size_t N = hp_.N;
+    switch (kind) {
+        case 0: return (size_t)hp_.R * N;
+        case 1: return (size_t)2 * hp_.L * N;
+        case 2: return (size_t)hp_.dnum * 2 * hp_.R * N;
+        default: throw std::invalid_argument("key kind must be 0 (secret), 1 (public) or 2 (switching)");
+    }
+}
+
+namespace {
+// every word of a [..][limbs][N] key image canonical under its limb's prime
+void check_canonical(const HostParams& hp, const u64* w, size_t words, u32 limbs) {
+    for (size_t i = 0; i < words; ++i)
+        if (w[i] >= hp.primes[(i / hp.N) % limbs]) throw std::invalid_argument("non-canonical key residue");
+}
+}  // namespace
+
+void Context::upload_key(int kind, u32 elt, const u64* host, size_t words) {
+    const size_t W = key_words(kind);
+    if (words != W) throw std::invalid_argument("key size mismatch: " + std::to_string(words) + " words, expected " +
+                                                std::to_string(W));
+    if (kind == 2 && elt != 0 && (elt % 2 == 0 || elt >= 2 * hp_.N))
+        throw std::invalid_argument("Galois element must be odd and below 2N (0 = relinearisation)");
+    check_canonical(hp_, host, W, kind == 1 ? hp_.L : hp_.R);
+    u64* dst = nullptr;
+    HGM_CUDA(cudaMalloc((void**)&dst, W * 8));
+    HGM_CUDA(cudaMemcpyAsync(dst, host, W * 8, cudaMemcpyHostToDevice, stream_));
+    if (kind == 2) {  // k_ks_inner reads keys in packed digit form
+        const dim3 kg((unsigned)((W + 4 * kThreads - 1) / (4 * kThreads)));
+        if (hp_.L == 3) k_mask_digits<ShapeQ3><<<kg, kThreads, 0, stream_>>>(dst, W); else k_mask_digits<ShapeQ8><<<kg, kThreads, 0, stream_>>>(dst, W);
+        ++launches_;
+    }
+    HGM_CUDA(cudaGetLastError());
+    sync();
+    u64* old = nullptr;
+    if (kind == 0) {
+        old = d_sk_;
+        d_sk_ = dst;
+    } else if (kind == 1) {
+        old = d_pk_;
+        d_pk_ = dst;
+    } else {
+        std::lock_guard<std::mutex> lk(key_mu_);
+        auto it = keys_.find(elt);
+        if (it != keys_.end()) old = it->second;
+        keys_[elt] = dst;
+    }
+    if (old) HGM_CUDA(cudaFree(old));
+}
+
+void Context::export_key(int kind, u32 elt, u64* host) {
+    const size_t W = key_words(kind);
+    const u64* src = kind == 0 ? d_sk_ : kind == 1 ? d_pk_ : ks_key(elt);
+    if (!src) throw std::invalid_argument(kind == 0 ? "context holds no secret key" : "context holds no public key");
+    sync();
+    HGM_CUDA(cudaMemcpy(host, src, W * 8, cudaMemcpyDeviceToHost));
+    if (kind == 2) {  // unpack the digit form: v = l + h 2^S
+        const int S = hp_.L == 3 ? ShapeQ3::S : ShapeQ8::S;
+        for (size_t i = 0; i < W; ++i) host[i] = (host[i] & 0xffffffffULL) + ((host[i] >> 32) << S);
+    }
+}
+
+void Context::drop_secret() {
+    sync();
+    if (d_sk_) {
+        // overwrite before freeing: the allocation may be handed out again
+        HGM_CUDA(cudaMemset(d_sk_, 0, (size_t)hp_.R * hp_.N * 8));
+        HGM_CUDA(cudaFree(d_sk_));
+    }
+    d_sk_ = nullptr;
 }
 
 size_t Context::key_count() const {
@@ -1149,17 +1243,37 @@ void Context::trim_mask_cache() {
 // ------------------------------------------------------------------ primitives
 void Context::encrypt(int n, const i64* const* host_vals, const size_t* S, const u64* counters,
                       u64* const* out) {
+    encrypt_impl(n, host_vals, S, counters, nullptr, out);
+}
+
+void Context::encrypt_noise(int n, const i64* const* host_vals, const size_t* S, const i64* noise,
+                            u64* const* out) {
+    const size_t N = hp_.N;
+    for (size_t i = 0; i < (size_t)n * 3 * N; ++i) {
+        const bool is_u = (i / N) % 3 == 0;
+        const i64 v = noise[i];
+        if (is_u ? (v < -1 || v > 1) : (v < -(i64)1e9 || v > (i64)1e9))
+            throw std::invalid_argument(is_u ? "u must be ternary" : "noise coefficient out of range");
+    }
+    encrypt_impl(n, host_vals, S, nullptr, noise, out);
+}
+
+void Context::encrypt_impl(int n, const i64* const* host_vals, const size_t* S, const u64* counters,
+                           const i64* noise, u64* const* out) {
     if (n <= 0) return;
+    if (!d_pk_) throw std::invalid_argument("context holds no public key: upload it with hgm_key_upload");
     if (n > kChunkEnc) {
         for (int c0 = 0; c0 < n; c0 += kChunkEnc) {
             const int cn = std::min(kChunkEnc, n - c0);
-            encrypt(cn, host_vals + c0, S + c0, counters + c0, out + c0);
+            encrypt_impl(cn, host_vals + c0, S + c0, counters ? counters + c0 : nullptr,
+                         noise ? noise + (size_t)c0 * 3 * hp_.N : nullptr, out + c0);
         }
         return;
     }
     const u32 N = hp_.N, L = hp_.L, H = N / 2;
     std::vector<u32> Sv(n);
-    std::vector<u64> ctr(counters, counters + n);
+    std::vector<u64> ctr(n, 0);
+    if (counters) std::copy(counters, counters + n, ctr.begin());
     std::vector<u64*> outs(out, out + n);
     for (int i = 0; i < n; ++i) Sv[i] = (u32)S[i];
     // slot values -> residues mod t, written straight into pinned staging
@@ -1176,9 +1290,14 @@ void Context::encrypt(int n, const i64* const* host_vals, const size_t* S, const
     u64* const* dout = upload(outs);
     u64* M = alloc((size_t)n * N);
     u64* U = alloc((size_t)n * L * N);
+    i64* dnoise = nullptr;
+    if (noise) {
+        dnoise = reinterpret_cast<i64*>(alloc((size_t)n * 3 * N));
+        HGM_CUDA(cudaMemcpyAsync(dnoise, noise, (size_t)n * 3 * N * 8, cudaMemcpyHostToDevice, stream_));
+    }
     k_encode_scatter<<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, dvals, dS, M); ++launches_;
     ntt(false, jobs_contig(M, n, kTIndex, 1));
-    if (hp_.L == 3) k_enc_lift<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, M, dctr, U, dout); else k_enc_lift<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, M, dctr, U, dout); ++launches_;
+    if (hp_.L == 3) k_enc_lift<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, M, dctr, dnoise, U, dout); else k_enc_lift<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, M, dctr, dnoise, U, dout); ++launches_;
     ntt(true, jobs_contig(U, n * L, 0, L));
     NttJobs cj;
     std::vector<u64*> limbs((size_t)n * 2 * L);
@@ -1192,11 +1311,16 @@ void Context::encrypt(int n, const i64* const* host_vals, const size_t* S, const
     if (hp_.L == 3) k_enc_finish<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, U, d_pk_, dout); else k_enc_finish<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, U, d_pk_, dout); ++launches_;
     release(M);
     release(U);
+    if (dnoise) {
+        release(dnoise);
+        sync();  // the caller's noise buffer was copied from pageable memory; keep the call synchronous
+    }
     HGM_CUDA(cudaGetLastError());
 }
 
 void Context::decrypt_to(int n, const u64* const* in, const size_t* S, u32* host) {
     if (n <= 0) return;
+    if (!d_sk_) throw std::invalid_argument("context holds no secret key (a cloud context cannot decrypt)");
     const u32 N = hp_.N, L = hp_.L, H = N / 2;
     for (int c0 = 0; c0 < n; c0 += kChunkDec) {
         const int cn = std::min(kChunkDec, n - c0);

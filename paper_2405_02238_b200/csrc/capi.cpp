@@ -13,7 +13,9 @@
 #include <future>
 #include <map>
 #include <tuple>
+#include <algorithm>
 #include <cstring>
+#include <fstream>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -60,14 +62,24 @@ struct SNode {
 
 }  // namespace
 
+// A session.  It is reference counted: the creator holds one reference and
+// every live handle and batch holds one, so hgm_ctx_destroy with handles still
+// alive only drops the creator's reference and the context (its device memory
+// and keys) goes away with the last handle (no use-after-free from late
+// releases, e.g. Python finalisers running after Context.close()).
 struct hgm_ctx {
     std::unique_ptr<Context> ctx;
-    std::mutex mu;                   // counters, encryption counter
+    int device = 0;
+    bool os_seed = false;            // seed drawn from the OS CSPRNG: never exported
+    std::mutex mu;                   // counters, encryption counter, pending registry
     std::recursive_mutex exec_mu;    // everything that touches the device (flush, batches, ring)
     std::atomic<int> phase{0};
+    std::atomic<int> refs{1};
     Counts counts;
     u64 enc_counter = 0;
     std::atomic<size_t> live{0}, peak{0};
+    // nodes handed out unmaterialised (hgm_flush materialises the pinned ones)
+    std::vector<std::weak_ptr<SNode>> pending;
 };
 
 struct hgm_ct {
@@ -83,6 +95,30 @@ int fail(int code, const std::string& msg) {
     g_err = msg;
     return code;
 }
+
+void ctx_retain(hgm_ctx* c) { c->refs.fetch_add(1, std::memory_order_relaxed); }
+void ctx_release(hgm_ctx* c) {
+    if (c->refs.fetch_sub(1, std::memory_order_acq_rel) == 1) {
+        c->pending.clear();
+        c->ctx.reset();  // Context's destructor sets and restores its own device
+        delete c;
+    }
+}
+
+// Makes the context's device current for the duration of an entry point and
+// restores the caller's current device afterwards (the library may be called
+// from any thread, and a process may hold contexts on several GPUs).
+struct DeviceScope {
+    int prev = -1, want;
+    explicit DeviceScope(const hgm_ctx* c) : want(c ? c->device : -1) {
+        if (want < 0) return;
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != want) cudaSetDevice(want);
+    }
+    ~DeviceScope() {
+        if (want >= 0 && prev >= 0 && prev != want) cudaSetDevice(prev);
+    }
+};
 
 template <typename F>
 int guarded(F&& f) {
@@ -102,6 +138,27 @@ int guarded(F&& f) {
     }
 }
 
+// Reserves n consecutive encryption counters of the session (atomically, so
+// concurrent and repeated calls never reuse (u, e0, e1)).
+u64 reserve_counters(hgm_ctx* c, u64 n) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    const u64 first = c->enc_counter;
+    c->enc_counter += n;
+    return first;
+}
+
+// counter0 == HGM_COUNTER_AUTO: the next count * E counters of the session
+u64 resolve_counter0(hgm_ctx* c, uint64_t counter0, u64 n) {
+    return counter0 == HGM_COUNTER_AUTO ? reserve_counters(c, n) : counter0;
+}
+
+u64 os_random_u64() {
+    u64 v = 0;
+    std::ifstream f("/dev/urandom", std::ios::binary);
+    if (!f.read(reinterpret_cast<char*>(&v), sizeof(v))) throw std::runtime_error("cannot read /dev/urandom");
+    return v;
+}
+
 void bump(hgm_ctx* c, int op) {
     std::lock_guard<std::mutex> lk(c->mu);
     c->counts.at(op, c->phase.load())++;
@@ -110,6 +167,18 @@ void bump(hgm_ctx* c, int op) {
 hgm_ct* make_handle(hgm_ctx* c, std::shared_ptr<SNode> n) {
     auto* h = new hgm_ct;
     h->owner = c;
+    ctx_retain(c);
+    if (!n->buf) {
+        std::lock_guard<std::mutex> lk(c->mu);
+        if (c->pending.size() >= 1024)  // prune released / materialised entries now and then
+            c->pending.erase(std::remove_if(c->pending.begin(), c->pending.end(),
+                                            [](const std::weak_ptr<SNode>& w) {
+                                                auto p = w.lock();
+                                                return !p || p->buf;
+                                            }),
+                             c->pending.end());
+        c->pending.push_back(n);
+    }
     h->node = std::move(n);
     h->node->pins++;
     const size_t now = ++c->live;
@@ -230,25 +299,87 @@ extern "C" {
 
 const char* hgm_last_error(void) { return g_err.c_str(); }
 
-hgm_ctx* hgm_ctx_create(int param_id, uint64_t seed, int device) {
+hgm_ctx* hgm_ctx_create_ex(int param_id, uint64_t seed, int device, int flags) {
     hgm_ctx* c = nullptr;
     const int rc = guarded([&] {
+        if (flags & ~(HGM_CTX_KEYLESS | HGM_CTX_OS_SEED)) throw std::invalid_argument("unknown context flags");
+        if (device < 0) throw std::invalid_argument("negative device ordinal");
         auto h = std::make_unique<hgm_ctx>();
-        h->ctx = std::make_unique<Context>(param_id, seed, device);
+        h->device = device;
+        if (flags & HGM_CTX_OS_SEED) {
+            h->os_seed = true;
+            seed = os_random_u64();
+        }
+        int prev = -1;
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        try {
+            h->ctx = std::make_unique<Context>(param_id, seed, device, (flags & HGM_CTX_KEYLESS) != 0);
+        } catch (...) {
+            if (prev >= 0) cudaSetDevice(prev);
+            throw;
+        }
+        if (prev >= 0 && prev != device) cudaSetDevice(prev);  // the constructor made `device` current
         c = h.release();
     });
     return rc == HGM_OK ? c : nullptr;
 }
 
-void hgm_ctx_destroy(hgm_ctx* c) { delete c; }
+hgm_ctx* hgm_ctx_create(int param_id, uint64_t seed, int device) {
+    return hgm_ctx_create_ex(param_id, seed, device, 0);
+}
+
+void hgm_ctx_destroy(hgm_ctx* c) {
+    if (c) ctx_release(c);
+}
 
 int hgm_ctx_info(const hgm_ctx* c, uint64_t* info, size_t cap) {
     const HostParams& h = c->ctx->host();
     if (cap < 8 + h.primes.size()) return fail(HGM_EARG, "info buffer too small");
     info[0] = h.N; info[1] = h.L; info[2] = h.K; info[3] = h.nB; info[4] = h.dnum;
-    info[5] = kT; info[6] = h.alpha; info[7] = h.seed;
+    info[5] = kT; info[6] = h.alpha; info[7] = c->os_seed ? 0 : h.seed;
     for (size_t i = 0; i < h.primes.size(); ++i) info[8 + i] = h.primes[i];
     return HGM_OK;
+}
+
+size_t hgm_key_words(const hgm_ctx* c, int kind) {
+    try {
+        return c->ctx->key_words(kind);
+    } catch (...) {
+        return 0;
+    }
+}
+
+int hgm_key_export(hgm_ctx* c, int kind, uint32_t elt, uint64_t* words, size_t n) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);
+    DeviceScope dev(c);
+    return guarded([&] {
+        if (!words) throw std::invalid_argument("null output buffer");
+        if (n < c->ctx->key_words(kind)) throw std::invalid_argument("key buffer too small");
+        c->ctx->export_key(kind, elt, words);
+    });
+}
+
+int hgm_key_upload(hgm_ctx* c, int kind, uint32_t elt, const uint64_t* words, size_t n) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);
+    DeviceScope dev(c);
+    return guarded([&] {
+        if (!words) throw std::invalid_argument("null key buffer");
+        c->ctx->upload_key(kind, elt, words, n);
+    });
+}
+
+int hgm_key_drop_secret(hgm_ctx* c) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);
+    DeviceScope dev(c);
+    return guarded([&] { c->ctx->drop_secret(); });
+}
+
+int hgm_key_has(const hgm_ctx* c, int kind) {
+    return kind == 0 ? c->ctx->has_secret() : kind == 1 ? c->ctx->has_public() : 0;
+}
+
+uint32_t hgm_galois_element(const hgm_ctx* c, int64_t offset) {
+    return Context::galois_of(offset, (u32)c->ctx->host().N);
 }
 size_t hgm_slot_count(const hgm_ctx* c) { return c->ctx->slots(); }
 size_t hgm_ct_words(const hgm_ctx* c) { return c->ctx->ct_words(); }
@@ -256,6 +387,7 @@ size_t hgm_ct_words(const hgm_ctx* c) { return c->ctx->ct_words(); }
 int hgm_encrypt_at(hgm_ctx* c, const int64_t* values, size_t S, uint64_t counter, hgm_ct** out) {
     return guarded([&] {
         check_values(c, S);
+        if (!c->ctx->has_public()) throw std::invalid_argument("context holds no public key: upload it with hgm_key_upload");
         auto n = new_node(c, PNode::Enc, S, 0);
         n->values.assign(values, values + S);
         n->counter = counter;
@@ -264,21 +396,43 @@ int hgm_encrypt_at(hgm_ctx* c, const int64_t* values, size_t S, uint64_t counter
     });
 }
 int hgm_encrypt(hgm_ctx* c, const int64_t* values, size_t S, hgm_ct** out) {
-    u64 ctr;
-    {
-        std::lock_guard<std::mutex> lk(c->mu);
-        ctr = c->enc_counter;
-    }
-    const int rc = hgm_encrypt_at(c, values, S, ctr, out);
-    if (rc == HGM_OK) {
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->enc_counter++;
-    }
-    return rc;
+    // the counter is reserved atomically BEFORE encrypting: concurrent callers
+    // never share (u, e0, e1); a failed call leaves a harmless gap
+    return hgm_encrypt_at(c, values, S, reserve_counters(c, 1), out);
 }
+
+int hgm_encrypt_noise(hgm_ctx* c, const int64_t* values, size_t S, const int64_t* u, const int64_t* e0,
+                      const int64_t* e1, hgm_ct** out) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);
+    DeviceScope dev(c);
+    return guarded([&] {
+        check_values(c, S);
+        if (!u || !e0 || !e1 || !out) throw std::invalid_argument("null noise or output buffer");
+        const size_t N = c->ctx->host().N, W = c->ctx->ct_words();
+        std::vector<i64> noise(3 * N);
+        std::copy(u, u + N, noise.begin());
+        std::copy(e0, e0 + N, noise.begin() + N);
+        std::copy(e1, e1 + N, noise.begin() + 2 * N);
+        const i64* vals = values;
+        u64* p = c->ctx->alloc(W);
+        try {
+            c->ctx->encrypt_noise(1, &vals, &S, noise.data(), &p);
+        } catch (...) {
+            c->ctx->release(p);
+            throw;
+        }
+        auto n = new_node(c, PNode::Input, S, 0);
+        n->buf = std::make_shared<DevBuf>(c->ctx.get(), p);
+        bump(c, kEnc);
+        *out = make_handle(c, std::move(n));
+    });
+}
+
+uint64_t hgm_reserve_counters(hgm_ctx* c, uint64_t n) { return reserve_counters(c, n); }
 
 int hgm_decrypt(hgm_ctx* c, const hgm_ct* ct, int64_t* out, size_t cap) {
     std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
+    DeviceScope dev(c);
     return guarded([&] {
         bump(c, kDec);
         const size_t S = node_of(ct).S;
@@ -380,12 +534,31 @@ int hgm_apply_plan(hgm_ctx* c, const hgm_ct* x, size_t n_entries, const int64_t*
 }
 
 int hgm_flush(hgm_ctx* c) {
-    (void)c;
-    return HGM_OK;
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
+    DeviceScope dev(c);
+    return guarded([&] {
+        // every node some caller still holds a pinned handle to, not yet computed
+        std::vector<std::shared_ptr<SNode>> targets;
+        {
+            std::lock_guard<std::mutex> lk(c->mu);
+            std::vector<std::weak_ptr<SNode>> keep;
+            for (auto& w : c->pending) {
+                auto p = w.lock();
+                if (!p || p->buf) continue;
+                if (p->pins.load() > 0) targets.push_back(p);
+                else keep.push_back(w);  // unpinned: stays lazy (recomputed on demand)
+            }
+            c->pending.swap(keep);
+        }
+        if (targets.empty()) return;
+        flush(c, targets);
+        c->ctx->sync();
+    });
 }
 
 int hgm_ct_export(hgm_ctx* c, const hgm_ct* ct, uint64_t* words) {
     std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
+    DeviceScope dev(c);
     return guarded([&] {
         flush(c, {ct->node});
         c->ctx->sync();
@@ -395,6 +568,7 @@ int hgm_ct_export(hgm_ctx* c, const hgm_ct* ct, uint64_t* words) {
 
 int hgm_ct_import(hgm_ctx* c, const uint64_t* words, size_t S, size_t depth, hgm_ct** out) {
     std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
+    DeviceScope dev(c);
     return guarded([&] {
         check_values(c, S);
         auto n = new_node(c, PNode::Input, S, depth);
@@ -431,6 +605,7 @@ size_t hgm_ct_wire_size(const hgm_ctx* c) { return sizeof(WireHeader) + c->ctx->
 
 int hgm_ct_serialize(hgm_ctx* c, const hgm_ct* ct, void* buf, size_t cap) {
     std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
+    DeviceScope dev(c);
     return guarded([&] {
         if (!ct || !buf) throw std::invalid_argument("null handle or buffer");
         const size_t W = c->ctx->ct_words();
@@ -454,6 +629,7 @@ int hgm_ct_serialize(hgm_ctx* c, const hgm_ct* ct, void* buf, size_t cap) {
 
 int hgm_ct_deserialize(hgm_ctx* c, const void* buf, size_t len, hgm_ct** out) {
     std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
+    DeviceScope dev(c);
     return guarded([&] {
         if (!buf || !out) throw std::invalid_argument("null buffer or output");
         const size_t W = c->ctx->ct_words();
@@ -504,9 +680,14 @@ int hgm_ct_set_pinned(hgm_ct* ct, int pinned) {
 void hgm_ct_release(hgm_ct* ct) {
     if (!ct) return;
     if (--ct->refs == 0) {
-        if (ct->pinned) ct->node->pins--;
-        ct->owner->live--;
-        delete ct;
+        hgm_ctx* c = ct->owner;
+        {
+            DeviceScope dev(c);  // freeing the last reference to a node frees device memory
+            if (ct->pinned) ct->node->pins--;
+            c->live--;
+            delete ct;
+        }
+        ctx_release(c);
     }
 }
 
@@ -650,6 +831,7 @@ int matmul_batch_impl(hgm_ctx* c, int algo, int order, int flags, size_t m, size
                       const int64_t* A, const int64_t* B, int64_t* C, uint64_t counter0, uint64_t* stats,
                       uint64_t* final_words) {
     std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
+    DeviceScope dev(c);
     return guarded([&] {
         if (order < -1 || order > 1) throw std::invalid_argument("order must be -1, 0 or 1");
         Context& ctx = *c->ctx;
@@ -657,6 +839,7 @@ int matmul_batch_impl(hgm_ctx* c, int algo, int order, int flags, size_t m, size
         put_counts(*prog, stats);
         if (count == 0) return;
         const u64 E = (u64)prog->n_enc;
+        counter0 = resolve_counter0(c, counter0, count * E);
         run_instances(
             ctx, *prog, count, [&](size_t k) { return A + k * m * l; }, [&](size_t k) { return B + k * l * n; },
             [&](size_t k) { return counter0 + k * E; }, [&](size_t k) { return C + k * m * n; }, final_words);
@@ -671,6 +854,7 @@ int hgm_blocked_mm(hgm_ctx* c, int algo, size_t m, size_t l, size_t n, const siz
                    const size_t* mids, size_t n_mid, const size_t* cols, size_t n_col, const int64_t* A,
                    const int64_t* B, int64_t* C, uint64_t counter0, int32_t* log) {
     std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
+    DeviceScope dev(c);
     return guarded([&] {
         if (algo < 0 || algo > 2) throw hgm::DimensionError("unknown algorithm id");
         // BlockPlan::validate (algorithms.cpp:412-432)
@@ -704,7 +888,7 @@ int hgm_blocked_mm(hgm_ctx* c, int algo, size_t m, size_t l, size_t n, const siz
             std::vector<i64> a, b, cprod;
         };
         std::vector<Blk> blocks;
-        u64 ctr = counter0;
+        u64 ctr = 0;  // relative counters; the base is resolved once the total is known
         for (size_t bi = 0; bi < n_row; ++bi)
             for (size_t bj = 0; bj < n_col; ++bj)
                 for (size_t bk = 0; bk < n_mid; ++bk) {  // the reference loop order (algorithms.cpp:472-492)
@@ -725,6 +909,8 @@ int hgm_blocked_mm(hgm_ctx* c, int algo, size_t m, size_t l, size_t n, const siz
                         for (size_t q = 0; q < k.nn; ++q) k.b[r * k.nn + q] = B[(mo[bk] + r) * n + co[bj] + q];
                     blocks.push_back(std::move(k));
                 }
+        const u64 base = resolve_counter0(c, counter0, ctr);
+        for (Blk& k : blocks) k.base += base;
         // one lockstep batch per distinct (algorithm, shape)
         std::map<std::tuple<int, size_t, size_t, size_t>, std::vector<size_t>> groups;
         for (size_t i = 0; i < blocks.size(); ++i)
@@ -760,11 +946,18 @@ int hgm_blocked_mm(hgm_ctx* c, int algo, size_t m, size_t l, size_t n, const siz
 }  // extern "C"
 
 struct hgm_batch {
-    hgm_ctx* owner = nullptr;
+    hgm_ctx* owner = nullptr;  // holds a context reference once fully built
     std::shared_ptr<const MatmulProgram> prog;
     size_t count = 0;
     u64* in = nullptr;   // [count][n_enc][W]
     u64* out = nullptr;  // [count][W]
+    Context* dctx = nullptr;
+    ~hgm_batch() {
+        if (dctx) {
+            dctx->release(in);
+            dctx->release(out);
+        }
+    }
 };
 
 namespace {
@@ -786,14 +979,16 @@ extern "C" {
 int hgm_batch_encrypt(hgm_ctx* c, int algo, int order, int flags, size_t m, size_t l, size_t n, size_t count,
                       const int64_t* A, const int64_t* B, uint64_t counter0, hgm_batch** out) {
     std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
+    DeviceScope dev(c);
     return guarded([&] {
         if (order < -1 || order > 1) throw std::invalid_argument("order must be -1, 0 or 1");
         Context& ctx = *c->ctx;
         auto b = std::make_unique<hgm_batch>();
-        b->owner = c;
         b->prog = get_matmul_program(algo, order, m, l, n, ctx.slots(), ctx.host().N, flags);
         b->count = count;
         const size_t W = ctx.ct_words(), E = b->prog->n_enc;
+        counter0 = resolve_counter0(c, counter0, count * E);
+        b->dctx = &ctx;
         b->in = ctx.alloc(std::max<size_t>(1, count * E) * W);
         b->out = ctx.alloc(std::max<size_t>(1, count) * W);
         const size_t chunk = 1024;
@@ -816,12 +1011,15 @@ int hgm_batch_encrypt(hgm_ctx* c, int algo, int order, int flags, size_t m, size
             ctx.encrypt((int)vals.size(), vals.data(), S.data(), ctr.data(), dst.data());
             ctx.sync();  // `packed` is host staging for this chunk
         }
+        b->owner = c;
+        ctx_retain(c);
         *out = b.release();
     });
 }
 
 int hgm_batch_cloud(hgm_ctx* c, hgm_batch* b, float* device_ms) {
     std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
+    DeviceScope dev(c);
     return guarded([&] {
         Context& ctx = *c->ctx;
         const MatmulProgram& prog = *b->prog;
@@ -860,6 +1058,7 @@ uint64_t* hgm_batch_output(hgm_batch* b, size_t i) {
 
 int hgm_batch_decrypt_words(hgm_ctx* c, const uint64_t* dev_words, size_t count, size_t S, int64_t* out) {
     std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
+    DeviceScope dev(c);
     return guarded([&] {
         Context& ctx = *c->ctx;
         if (S == 0 || S > ctx.slots()) throw hgm::DimensionError("bad segment");
@@ -881,6 +1080,7 @@ int hgm_batch_decrypt_words(hgm_ctx* c, const uint64_t* dev_words, size_t count,
 
 int hgm_batch_decrypt(hgm_ctx* c, hgm_batch* b, int64_t* C) {
     std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
+    DeviceScope dev(c);
     return guarded([&] {
         const MatmulProgram& prog = *b->prog;
         std::vector<i64> slots(b->count * prog.segment);
@@ -895,10 +1095,18 @@ int hgm_batch_decrypt(hgm_ctx* c, hgm_batch* b, int64_t* C) {
 
 void hgm_batch_free(hgm_batch* b) {
     if (!b) return;
-    b->owner->ctx->release(b->in);
-    b->owner->ctx->release(b->out);
-    b->owner->ctx->sync();
-    delete b;
+    hgm_ctx* c = b->owner;
+    {
+        std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);
+        DeviceScope dev(c);
+        try {
+            delete b;  // stream-ordered frees
+            c->ctx->sync();
+        } catch (const std::exception& e) {
+            g_err = e.what();
+        }
+    }
+    ctx_release(c);
 }
 
 int hgm_program_info(int algo, int order, int flags, size_t m, size_t l, size_t n, size_t slots, uint32_t N,
@@ -922,6 +1130,26 @@ int hgm_program_info(int algo, int order, int flags, size_t m, size_t l, size_t 
             facts[8] = p->cloud_sched.rescale_count;
         }
     });
+}
+
+long hgm_program_keys(int algo, int order, int flags, size_t m, size_t l, size_t n, size_t slots, uint32_t N,
+                      uint32_t* elements, size_t cap) {
+    long result = 0;
+    const int rc = guarded([&] {
+        auto p = get_matmul_program(algo, order, m, l, n, slots, N, flags);
+        std::vector<u32> els;
+        bool relin = false;
+        for (const auto& nd : p->sched.prog.nodes) {
+            if (nd.kind == PNode::Rot && nd.g != 1) els.push_back(nd.g);
+            if (nd.kind == PNode::Mult) relin = true;
+        }
+        std::sort(els.begin(), els.end());
+        els.erase(std::unique(els.begin(), els.end()), els.end());
+        if (relin) els.insert(els.begin(), 0u);
+        result = (long)els.size();
+        if (elements) std::copy(els.begin(), els.begin() + std::min(cap, els.size()), elements);
+    });
+    return rc == HGM_OK ? result : -rc;
 }
 
 long hgm_program_stream(int algo, int order, int flags, size_t m, size_t l, size_t n, size_t slots, uint32_t N,
@@ -988,6 +1216,7 @@ int hgm_matmul_batch_export(hgm_ctx* c, int algo, int order, int flags, size_t m
 
 int hgm_bench_ntt(hgm_ctx* c, int forward, size_t limbs, int iters, float* ms) {
     std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
+    DeviceScope dev(c);
     return guarded([&] {
         Context& ctx = *c->ctx;
         const u32 N = ctx.host().N, L = ctx.host().L;
@@ -1014,11 +1243,13 @@ int hgm_bench_ntt(hgm_ctx* c, int forward, size_t limbs, int iters, float* ms) {
 
 int hgm_device_sync(hgm_ctx* c) {
     std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
+    DeviceScope dev(c);
     return guarded([&] { c->ctx->sync(); });
 }
 
 int hgm_test_ntt(hgm_ctx* c, int forward, int prime, uint64_t* data, size_t count) {
     std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
+    DeviceScope dev(c);
     return guarded([&] {
         Context& ctx = *c->ctx;
         const u32 N = ctx.host().N;

@@ -58,7 +58,9 @@ class PinnedRing {
 
 class Context {
   public:
-    Context(int param_id, u64 seed, int device);
+    // keyless: no secret, public or switching keys are generated; they must be
+    // uploaded (upload_key) before the operations that need them
+    Context(int param_id, u64 seed, int device, bool keyless = false);
     ~Context();
     Context(const Context&) = delete;
     Context& operator=(const Context&) = delete;
@@ -88,6 +90,19 @@ class Context {
     const u64* ks_key(u32 kid);  // [dnum][2][R][N]; kid = Galois element, 0 = relin
     void ensure_galois_keys(const std::vector<u32>& elements);
     size_t key_count() const;
+    // Key material at the boundary (canonical residues, NTT domain):
+    //   kind 0 secret key   [R][N]  (s over Q ++ P)
+    //   kind 1 public key   [2][L][N]
+    //   kind 2 switching key for Galois element `elt` (0 = relinearisation)
+    //                       [dnum][2][R][N]
+    size_t key_words(int kind) const;
+    void upload_key(int kind, u32 elt, const u64* host, size_t words);
+    void export_key(int kind, u32 elt, u64* host);
+    // Forget the secret key (a cloud context keeps only evaluation keys):
+    // decryption and generation of new switching keys then fail.
+    void drop_secret();
+    bool has_secret() const { return d_sk_ != nullptr; }
+    bool has_public() const { return d_pk_ != nullptr; }
     static u32 galois_of(i64 z, u32 N);  // 3^(z mod N/2) mod 2N; 1 for z = 0
 
     // ---------------------------------------------------------------- masks
@@ -103,6 +118,10 @@ class Context {
     // host_vals[i] holds S[i] values; counters[i] is the encryption counter.
     void encrypt(int n, const i64* const* host_vals, const size_t* S, const u64* counters,
                  u64* const* out);
+    // Same with host-sampled randomness: noise = n x [u | e0 | e1] x N signed
+    // coefficients (u ternary, e0 / e1 small), instead of the counter PRNG.
+    void encrypt_noise(int n, const i64* const* host_vals, const size_t* S, const i64* noise,
+                       u64* const* out);
     // Decrypts n ciphertexts into host buffers (synchronises the stream).
     void decrypt(int n, const u64* const* in, const size_t* S, i64* const* host_out);
     // Enqueues the decryption of n ciphertexts into pinned host memory (N/2 u32
@@ -146,6 +165,8 @@ class Context {
 
   private:
     void build_keys();
+    void encrypt_impl(int n, const i64* const* host_vals, const size_t* S, const u64* counters,
+                      const i64* noise, u64* const* out);
     u64* b_extend(int n, const u64* const* a, const u64* const* b);
     void scale_relin(int n, u64* T, u64* const* out);
     void key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, const u64* const* addn,
@@ -156,6 +177,7 @@ class Context {
     HostParams hp_;
     std::atomic<u64> launches_{0};
     int device_ = 0;
+    bool keyless_ = false;
     cudaStream_t stream_ = nullptr;
     DevParams* dp_ = nullptr;
     DevCtx cx_{};

@@ -95,3 +95,26 @@ def test_reference_algorithms_cfg2_dropin(algo, aid, dropin, ref, gpu_factory):
     assert st[:12].astype(int).tolist() == st_ref[:12].astype(int).tolist()
     _, wb = g.matmul_batch(A, B, algo=aid, counter0=0, export=True)
     assert np.array_equal(words, wb[0])
+
+
+def test_long_lived_backend_releases_dead_handles(dropin):
+    """A drop-in backend session reused for several products releases its GPU
+    handles whenever no ciphertext it handed out is alive (between products),
+    so its handle table (device buffers and op recipes) stays bounded."""
+    L = ctypes.CDLL(SO)
+    vp, sz = ctypes.c_void_p, ctypes.c_size_t
+    L.dropin_repeat.restype = ctypes.c_int
+    L.dropin_repeat.argtypes = [ctypes.c_int, ctypes.c_int, vp, sz, sz, vp, sz, ctypes.c_int, vp, vp]
+    m, l, n, lo, hi, pid, _, _ = CONFIGS["cfg1"]
+    A, B = splitmix_matrices(20240101, 0, m, l, n, lo, hi)
+    reps = 4
+    C = np.zeros((reps, m, n), dtype=np.int64)
+    info = np.zeros(3, dtype=np.uint64)
+    rc = L.dropin_repeat(pid, 1, A.ctypes.data, m, l, B.ctypes.data, n, reps, C.ctypes.data, info.ctypes.data)
+    assert rc == 0, L.dropin_last_error()
+    for r in range(reps):
+        assert np.array_equal(C[r], (A @ B) % T)
+    epochs, held, most = (int(x) for x in info)
+    assert epochs >= reps - 1, f"handles were released only {epochs} times over {reps} products"
+    per_product = most
+    assert held <= per_product
