@@ -271,11 +271,13 @@ def main():
     barrier()
     total_ms = max_over_ranks(sum(step_ms))
     value = args.instances * args.steps / (total_ms / 1e3)
-    # correctness of what was timed (decrypt outside the timed region)
+    # correctness of what was timed (decrypt outside the timed region): every product
+    want = np.einsum("kij,kjl->kil", A, B) % 65537
     C = bt.decrypt()
-    ok = all(np.array_equal(C[i], (A[i] @ B[i]) % 65537) for i in range(0, count, max(1, count // 16)))
-    if not ok:
-        raise RuntimeError("timed cloud phase produced a wrong product")
+    wrong = int(np.count_nonzero(~np.all(C == want, axis=(1, 2))))
+    if wrong:
+        raise RuntimeError(f"timed cloud phase produced {wrong} wrong products")
+    verified = {"value": f"{count} of {count} products decrypted and checked"}
     # gather result ciphertexts to rank 0 over NCCL (the only collective)
     gather_ms = None
     if dist:
@@ -320,7 +322,10 @@ def main():
             barrier()
             e2e_times.append(time.perf_counter() - t0)
         e2e_total = max_over_ranks(sum(e2e_times))
-        assert np.array_equal(Ce[0], (A[0] @ B[0]) % 65537)
+        wrong = int(np.count_nonzero(~np.all(Ce == want, axis=(1, 2))))  # outside the timed region
+        if wrong:
+            raise RuntimeError(f"e2e path produced {wrong} wrong products")
+        verified["e2e"] = f"{count} of {count} products of the last step checked
         # bytes the library moves: slot vectors go up as u32 residues mod t (N/2 per
         # encryption, pinned staging) and decrypted rows come back as N/2 u32 each
         h2d = args.instances * E * ctx.slot_count * 4
@@ -379,6 +384,7 @@ def main():
             "roofline": roofline,
             "cpu_baseline": None if args.no_cpu_baseline or world > 1 else cpu_baseline(),
         }
+        line["verified"] = verified
         if gather_ms is not None:
             line["nccl_gather_ms"] = round(gather_ms, 3)
         print(json.dumps(line))
