@@ -325,7 +325,7 @@ def main():
         wrong = int(np.count_nonzero(~np.all(Ce == want, axis=(1, 2))))  # outside the timed region
         if wrong:
             raise RuntimeError(f"e2e path produced {wrong} wrong products")
-        verified["e2e"] = f"{count} of {count} products of the last step checked
+        verified["e2e"] = f"{count} of {count} products of the last step checked"
         # bytes the library moves: slot vectors go up as u32 residues mod t (N/2 per
         # encryption, pinned staging) and decrypted rows come back as N/2 u32 each
         h2d = args.instances * E * ctx.slot_count * 4
