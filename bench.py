@@ -110,7 +110,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-from paper_2405_02238_b200.dist import counter_base, gather_ciphertexts, shard  # noqa: E402
+from paper_2405_02238_b200.dist import comm_from_env, counter_base, env_rank, shard  # noqa: E402
 
 
 def cpu_baseline(seconds_budget: float = 20.0):
@@ -134,7 +134,28 @@ def cpu_baseline(seconds_budget: float = 20.0):
     return {"value": done / dt, "unit": UNIT, "cores": 1, "kind": "port",
             "sample": f"{done} x cfg4 instance(s) through the reference basic_mm (compiled from "
                       f"/root/reference sources) over the CPU RNS-BFV restatement (oracle/), "
-                      f"1 thread, {dt:.1f} s"}
+                      f"1 thread, {dt:.1f} s",
+            "cleartext_emulator": cleartext_emulator_rate()}
+
+
+def cleartext_emulator_rate(seconds_budget: float = 3.0):
+    """BASELINE.md's literal reference CPU path: the reference's own basic_mm on
+    its cleartext slot emulator (SlotBackend{4096, 65537}), 1 thread.  Not an
+    encrypted product -- reported for context only."""
+    from oracle.bindings import RefLib  # CPU baseline leg only
+    from paper_2405_02238_b200.workload import batch
+
+    A, B = batch(SEED, 0, 64, M, L_, N_, LO, HI)
+    RefLib.mm(A[0], B[0], "basic", slots=4096)
+    done, t0 = 0, time.perf_counter()
+    while done < len(A) and (done == 0 or time.perf_counter() - t0 < seconds_budget):
+        C, _ = RefLib.mm(A[done], B[done], "basic", slots=4096)
+        assert np.array_equal(C, (A[done] @ B[done]) % 65537)
+        done += 1
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": UNIT, "cores": 1,
+            "sample": f"{done} x cfg4 instance(s), reference basic_mm on SlotBackend{{4096, 65537}} "
+                      f"(cleartext slot emulator, NOT homomorphic), 1 thread, {dt:.1f} s"}
 
 
 def run_reference(args):
@@ -187,7 +208,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(step_times),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (reference campaign splitmix64 draws)",
         "config": {"workload": "cfg4: 64x64x64 HEGMM (basic_mm) instances, BFV N=8192 t=65537 3x60b",
                    "per_step": f"{threads} instances (1 per host thread)"},
@@ -209,8 +230,12 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--algo", default="basic", choices=["basic", "enhanced"])
-    ap.add_argument("--instances", type=int, default=TOTAL_INSTANCES)
+    ap.add_argument("--config", default="cfg4", choices=["cfg4", "cfg5"])
+    ap.add_argument("--algo", default=None, choices=["basic", "enhanced"])
+    ap.add_argument("--instances", type=int, default=None,
+                    help="products per GPU per step (cfg4: 4096 instances; cfg5: 128^3 products)")
+    ap.add_argument("--strong", action="store_true",
+                    help="split --instances across the GPUs instead of giving every GPU that many")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -218,96 +243,115 @@ def main():
         args.warmup = 3  # timing rules: >= 3 warm-up steps
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "cfg5":
+        return run_cfg5(args)
+    return run_cfg4(args)
 
+
+def ntt_roofline(ctx, limb_bytes, label):
+    """Forward / inverse NTT and the key-switch inner product timed live (CUDA
+    events on the library stream), inputs larger than L2 with canonical random
+    residues; algorithmic bytes per unit from SURVEY.md 8(d) / DESIGN.md."""
+    peak, peak_src = load_peaks()
+    limbs = 148 * 8 * 4  # 4736 limbs: > 126 MB L2 at N = 8192, several waves of 444 resident CTAs
+    if ctx.N > 8192:
+        limbs = 148 * 8
+    ntt_ms = ctx.bench_ntt(limbs, 20, True)
+    intt_ms = ctx.bench_ntt(limbs, 20, False)
+    achieved = limbs * limb_bytes / (ntt_ms / 1e3) / 1e9
+    # key switch: per rotation read dnum (L+K) digit limbs + dnum 2 (L+K) key limbs + L c0 limbs,
+    # write 2 (L+K) accumulator limbs (DESIGN.md, roofline table)
+    R = ctx.L + ctx.K
+    ks_items = 2048 if ctx.N == 8192 else 256
+    ks_bytes = (ctx.dnum * R + ctx.dnum * 2 * R + ctx.L + 2 * R) * ctx.N * 8
+    ks_ms = ctx.bench_keyswitch(ks_items, 10)
+    ks_gbs = ks_items * ks_bytes / (ks_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ntt_traffic.json")
+    if os.path.exists(prof):
+        try:
+            rec = json.load(open(prof))
+            if rec.get("N", 8192) == ctx.N and rec.get("bytes_per_limb"):
+                traffic = rec["bytes_per_limb"] * limbs
+        except Exception:
+            traffic = None
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "kernel": label, "algorithmic_bytes_per_launch": limbs * limb_bytes, "limbs_per_launch": limbs,
+            "ms_per_launch": round(ntt_ms, 4),
+            "inverse_frac": round(limbs * limb_bytes / (intt_ms / 1e3) / 1e9 / peak, 4),
+            "peak_source": peak_src, "frac_vs_spec_8tbs": round(achieved / 8000.0, 4),
+            "keyswitch": {"kernel": "k_ks_inner (key inner product, Galois gather fused, 8 rotations per key read)",
+                          "rotations_per_launch": ks_items, "algorithmic_bytes_per_rotation": ks_bytes,
+                          "ms_per_launch": round(ks_ms, 4), "achieved": round(ks_gbs, 1),
+                          "frac": round(ks_gbs / peak, 4)}}
+
+
+def run_cfg4(args):
     import paper_2405_02238_b200 as hb
     from paper_2405_02238_b200.workload import batch
 
-    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
-    dist = None
-    if world > 1:
-        import torch
-        import torch.distributed as tdist
-
-        torch.cuda.set_device(local)
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        dist = tdist
-
-    algo = hb.ALGOS[args.algo]
-    first, count = shard(rank, world, args.instances)
+    rank, world, local = env_rank()
+    algo_name = args.algo or "basic"
+    algo = hb.ALGOS[algo_name]
+    per_gpu = args.instances or TOTAL_INSTANCES
+    total = per_gpu if args.strong else per_gpu * world
+    first, count = shard(rank, world, total)
     ctx = hb.Context(PARAM_ID, 1, local)
+    comm = comm_from_env(ctx)  # the library's NCCL communicator (no torch)
     A, B = batch(SEED, first, count, M, L_, N_, LO, HI)
     st, facts = hb.program_info(algo, M, L_, N_, ctx.slot_count, ctx.N)
     E = facts["encryptions"]
 
     def barrier():
-        if dist:
-            import torch
-
-            torch.cuda.synchronize()
-            dist.barrier()
+        ctx.sync()
+        if comm:
+            comm.barrier()
 
     def max_over_ranks(x: float) -> float:
-        if not dist:
-            return x
-        import torch
-
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return comm.max(x) if comm else x
 
     # ---------------------------------------------------------------- value: cloud phase
     bt = hb.Batch(ctx, A, B, algo=algo, counter0=counter_base(first, E))  # client phase (not timed)
     for _ in range(args.warmup):
         bt.cloud()
     barrier()
-    ctx.sync()
     launches0 = ctx.launch_count()
     step_ms = []
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             step_ms.append(bt.cloud())
     launches = ctx.launch_count() - launches0
-    ctx.sync()
     barrier()
     total_ms = max_over_ranks(sum(step_ms))
-    value = args.instances * args.steps / (total_ms / 1e3)
+    value = total * args.steps / (total_ms / 1e3)
     # correctness of what was timed (decrypt outside the timed region): every product
     want = np.einsum("kij,kjl->kil", A, B) % 65537
     C = bt.decrypt()
     wrong = int(np.count_nonzero(~np.all(C == want, axis=(1, 2))))
     if wrong:
         raise RuntimeError(f"timed cloud phase produced {wrong} wrong products")
-    verified = {"value": f"{count} of {count} products decrypted and checked"}
-    # gather result ciphertexts to rank 0 over NCCL (the only collective)
+    verified = {"value": f"{count} of {count} products decrypted and checked (rank {rank})"}
+    # gather every rank's result ciphertexts to rank 0 over the library's NCCL
+    # communicator (the only collective, SURVEY 8e); rank 0 decrypts all of them
     gather_ms = None
-    if dist:
-        import torch
-
-        W = ctx.ct_words
-
-        class _View:
-            def __init__(self, ptr, n):
-                self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr, False),
-                                                 "version": 3}
-
-        mine = torch.as_tensor(_View(bt.output_ptr(0), count * W), device="cuda")
-        ctx.sync()
-        torch.cuda.synchronize()
+    if comm:
+        barrier()
         t0 = time.perf_counter()
-        got = gather_ciphertexts(dist, mine, count, W, args.instances, world, rank, device="cuda")
-        torch.cuda.synchronize()
+        ptr, n = comm.gather_batch(bt, root=0)
         gather_ms = 1e3 * (time.perf_counter() - t0)
-        if rank == 0:  # rank 0 (the client side) decrypts a sample of every shard
-            for r, part in enumerate(got):
-                f, c = shard(r, world, args.instances)
-                if c:  # check the shard's first product from its gathered ciphertext
-                    slots = ctx.decrypt_words(part[: W], facts["segment"])[0]
-                    Ar, Br = batch(SEED, f, 1, M, L_, N_, LO, HI)
-                    col = facts["order"] == 0
-                    C0 = np.array([[slots[(i + j * M) if col else (i * N_ + j)] for j in range(N_)]
-                                   for i in range(M)])
-                    if not np.array_equal(C0, (Ar[0] @ Br[0]) % 65537):
-                        raise RuntimeError(f"gathered ciphertext of rank {r} decrypts wrongly")
+        gather_ms = max_over_ranks(gather_ms)
+        if rank == 0:
+            try:
+                Cg = ctx.decrypt_products(ptr, n, M, L_, N_, algo=algo)
+            finally:
+                comm.free_buffer(ptr)
+            Ag, Bg = batch(SEED, 0, total, M, L_, N_, LO, HI)
+            wantg = np.einsum("kij,kjl->kil", Ag, Bg) % 65537
+            wrong = int(np.count_nonzero(~np.all(Cg == wantg, axis=(1, 2))))
+            if n != total or wrong:
+                raise RuntimeError(f"gathered {n} of {total} ciphertexts, {wrong} decrypt wrongly")
+            verified["gather"] = f"{n} of {total} ciphertexts gathered to rank 0 over NCCL, all decrypted and checked"
     bt.free()
 
     # ---------------------------------------------------------------- e2e through the C ABI
@@ -319,68 +363,46 @@ def main():
             barrier()
             t0 = time.perf_counter()
             Ce, _ = ctx.matmul_batch(A, B, algo=algo, counter0=first * E)
-            barrier()
             e2e_times.append(time.perf_counter() - t0)
+        barrier()
         e2e_total = max_over_ranks(sum(e2e_times))
         wrong = int(np.count_nonzero(~np.all(Ce == want, axis=(1, 2))))  # outside the timed region
         if wrong:
             raise RuntimeError(f"e2e path produced {wrong} wrong products")
-        verified["e2e"] = f"{count} of {count} products of the last step checked"
+        verified["e2e"] = f"{count} of {count} products of the last step checked (rank {rank})"
         # bytes the library moves: slot vectors go up as u32 residues mod t (N/2 per
         # encryption, pinned staging) and decrypted rows come back as N/2 u32 each
-        h2d = args.instances * E * ctx.slot_count * 4
-        d2h = args.instances * ctx.slot_count * 4
-        e2e = {"value": args.instances * args.steps / e2e_total, "unit": UNIT,
+        h2d = total * E * ctx.slot_count * 4
+        d2h = total * ctx.slot_count * 4
+        e2e = {"value": total * args.steps / e2e_total, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "path": "hgm_matmul_batch (C ABI): host int64 A,B -> host C, incl. client encrypt/decrypt"}
 
-    # ---------------------------------------------------------------- roofline: NTT kernel
-    limbs = 148 * 8
-    ntt_ms = ctx.bench_ntt(limbs, 20, True)
-    intt_ms = ctx.bench_ntt(limbs, 20, False)
-    peak, peak_src = load_peaks()
-    achieved = limbs * LIMB_BYTES / (ntt_ms / 1e3) / 1e9
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ntt_traffic.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("bytes_per_limb")
-            traffic = traffic * limbs if traffic else None
-        except Exception:
-            traffic = None
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": "k_ntt_fwd3<13> (forward NTT, N=8192, 64-bit Shoup, 3 CTAs/SM)",
-                "algorithmic_bytes_per_launch": limbs * LIMB_BYTES, "limbs_per_launch": limbs,
-                "inverse_frac": round(limbs * LIMB_BYTES / (intt_ms / 1e3) / 1e9 / peak, 4),
-                "peak_source": peak_src,
-                "frac_vs_spec_8tbs": round(achieved / 8000.0, 4),
-                # op-level bytes of one cfg2/cfg4 basic_mm matmul
-                # (every primitive's compulsory ciphertext/key/mask traffic x the reference op
-                # counts); fused, deduplicated execution may move fewer, so frac may exceed 1
-                "op_level": {"bytes_per_matmul": OP_BYTES_PER_MATMUL,
-                             "achieved": round(value * OP_BYTES_PER_MATMUL / 1e9 / world, 1),
-                             "unit": "GB/s per GPU",
-                             "frac": round(value * OP_BYTES_PER_MATMUL / 1e9 / world / peak, 4)}}
+    roofline = ntt_roofline(ctx, LIMB_BYTES, "k_ntt_fwd3<13> (forward NTT, N=8192, 64-bit Shoup, 3 CTAs/SM)")
+    roofline["op_level"] = {"bytes_per_matmul": OP_BYTES_PER_MATMUL,
+                            "achieved": round(value * OP_BYTES_PER_MATMUL / 1e9 / world, 1),
+                            "unit": "GB/s per GPU",
+                            "frac": round(value * OP_BYTES_PER_MATMUL / 1e9 / world / roofline["peak"], 4)}
 
     if rank == 0:
-        clocks = clk.summary()
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 3), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+            "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (reference campaign splitmix64 draws, seed %d)" % SEED,
-            "config": {"workload": f"cfg4: {args.instances} x A(64x64).B(64x64) {args.algo}_mm instances, "
-                                   f"BFV N=8192 t=65537 Q=3x60b P=1x60b dnum=3",
-                       "instances_per_step": args.instances, "algo": args.algo,
+            "config": {"workload": f"cfg4: {per_gpu} x A(64x64).B(64x64) {algo_name}_mm instances "
+                                   f"{'in total' if args.strong else 'per GPU'}, BFV N=8192 t=65537 "
+                                   f"Q=3x60b P=1x60b dnum=3 (log2 PQ ~ 240: above the 128-bit bound for N=8192, "
+                                   f"as BASELINE.json's 3x60-bit Q prescribes)",
+                       "instances_per_step": total, "instances_per_gpu": count, "algo": algo_name,
                        "cloud_ops_per_instance": {"rot": int(st[7]), "cmult": int(st[5]), "add": int(st[1]),
                                                   "mult": int(st[3])},
                        "rotations_after_cse": facts["rotations"], "parallelism": f"instances x{world}",
-                       "l2": "inputs larger than L2 (%.1f GB of ciphertexts per step)" %
-                             (args.instances * E * ctx.ct_words * 8 / 1e9)},
+                       "l2": "inputs larger than L2 (%.1f GB of ciphertexts per GPU per step)" %
+                             (count * E * ctx.ct_words * 8 / 1e9)},
             "e2e": e2e,
             "gpu_launches": int(launches),
-            "clocks": clocks,
+            "clocks": clk.summary(),
             "roofline": roofline,
             "cpu_baseline": None if args.no_cpu_baseline or world > 1 else cpu_baseline(),
         }
@@ -388,9 +410,123 @@ def main():
         if gather_ms is not None:
             line["nccl_gather_ms"] = round(gather_ms, 3)
         print(json.dumps(line))
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
+    if comm:
+        comm.barrier()
+        comm.close()
+    ctx.close()
+    return 0
+
+
+CFG5 = dict(m=128, l=128, n=128, lo=-4, hi=3, param_id=1, parts=8, seed=20240505)
+
+
+def run_cfg5(args):
+    """Config 5: A(128x128).B(128x128) at N=32768 (8 x ~55-bit Q, 4 special
+    primes, dnum 2), HEGMM-Enhanced over 8 row blocks of 16 rows:
+    a step runs `--instances` such products (default 4) -- 8 row-block
+    products each, sharded over the ranks -- and gathers the result ciphertexts
+    to rank 0 over the library's NCCL communicator."""
+    import paper_2405_02238_b200 as hb
+    from paper_2405_02238_b200.dist import row_blocks
+    from paper_2405_02238_b200.workload import splitmix_matrices
+
+    rank, world, local = env_rank()
+    c = CFG5
+    algo_name = args.algo or "enhanced"
+    algo = hb.ALGOS[algo_name]
+    products = args.instances or 4
+    total_blocks = products * c["parts"]
+    first, count = shard(rank, world, total_blocks)
+    h = c["m"] // c["parts"]
+    ctx = hb.Context(c["param_id"], 1, local)
+    comm = comm_from_env(ctx)
+    mats = [splitmix_matrices(c["seed"], p, c["m"], c["l"], c["n"], c["lo"], c["hi"]) for p in range(products)]
+    blocks = row_blocks(c["m"], c["parts"])
+    As = np.stack([mats[b // c["parts"]][0][blocks[b % c["parts"]][0]: blocks[b % c["parts"]][0] + h]
+                   for b in range(first, first + count)])
+    Bs = np.stack([mats[b // c["parts"]][1] for b in range(first, first + count)])
+    st, facts = hb.program_info(algo, h, c["l"], c["n"], ctx.slot_count, ctx.N)
+    E = facts["encryptions"]
+
+    def barrier():
+        ctx.sync()
+        if comm:
+            comm.barrier()
+
+    bt = hb.Batch(ctx, As, Bs, algo=algo, counter0=first * E)
+    for _ in range(args.warmup):
+        bt.cloud()
+    barrier()
+    launches0 = ctx.launch_count()
+    step_ms = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            step_ms.append(bt.cloud())
+    launches = ctx.launch_count() - launches0
+    barrier()
+    total_ms = comm.max(sum(step_ms)) if comm else sum(step_ms)
+    value = products * args.steps / (total_ms / 1e3)
+    # gather to rank 0, decrypt, stitch and check every product (outside the timed region)
+    verified = {}
+    if comm:
+        ptr, n = comm.gather_batch(bt, root=0)
+        if rank == 0:
+            try:
+                Cb = ctx.decrypt_products(ptr, n, h, c["l"], c["n"], algo=algo)
+            finally:
+                comm.free_buffer(ptr)
+    else:
+        Cb = bt.decrypt()
+    if rank == 0:
+        for p in range(products):
+            Cp = np.concatenate(list(Cb[p * c["parts"]:(p + 1) * c["parts"]]))
+            if not np.array_equal(Cp, (mats[p][0] @ mats[p][1]) % 65537):
+                raise RuntimeError(f"cfg5 product {p} decrypts wrongly")
+        verified["value"] = f"{products} of {products} 128^3 products (gathered to rank 0) decrypted and checked"
+    bt.free()
+    e2e = None
+    if not args.no_e2e:
+        ctx.matmul_batch(As[:1], Bs[:1], algo=algo)
+        times = []
+        for _ in range(args.steps):
+            barrier()
+            t0 = time.perf_counter()
+            Ce, _ = ctx.matmul_batch(As, Bs, algo=algo, counter0=first * E)
+            times.append(time.perf_counter() - t0)
+        barrier()
+        tot = comm.max(sum(times)) if comm else sum(times)
+        want = np.einsum("kij,kjl->kil", As, Bs) % 65537
+        if not np.array_equal(Ce, want):
+            raise RuntimeError("cfg5 e2e path produced wrong row blocks")
+        verified["e2e"] = f"{count} of {count} row blocks of the last step checked (rank {rank})"
+        e2e = {"value": products * args.steps / tot, "unit": "matmuls/s",
+               "h2d_bytes_per_step": total_blocks * E * ctx.slot_count * 4,
+               "d2h_bytes_per_step": total_blocks * ctx.slot_count * 4,
+               "path": "hgm_matmul_batch (C ABI) over the rank's row blocks: host int64 in -> host C"}
+    roofline = ntt_roofline(ctx, 2 * 8 * ctx.N,
+                            "k_ntt_fwd_outer2 + k_ntt_fwd3<13> (forward NTT, N=32768, 64-bit Shoup)")
+    if rank == 0:
+        line = {
+            "metric": "encrypted 128x128x128 matmuls/sec (BFV N=32768)", "value": round(value, 3),
+            "unit": "matmuls/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(total_ms / args.steps, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (reference campaign splitmix64 draws, seed %d)" % c["seed"],
+            "config": {"workload": f"cfg5: {products} x A(128x128).B(128x128) {algo_name}_mm per step as "
+                                   f"{total_blocks} row-block products 16x128.128x128, BFV N=32768 t=65537 "
+                                   f"Q=8x55b P=4x55b dnum=2", "row_blocks_per_gpu": count,
+                       "cloud_ops_per_row_block": {"rot": int(st[7]), "cmult": int(st[5]), "add": int(st[1]),
+                                                   "mult": int(st[3])},
+                       "parallelism": f"row blocks x{world}",
+                       "l2": "inputs larger than L2 (%.2f GB of ciphertexts per GPU)" %
+                             (count * E * ctx.ct_words * 8 / 1e9)},
+            "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(), "roofline": roofline,
+            "cpu_baseline": None, "verified": verified,
+        }
+        print(json.dumps(line))
+    if comm:
+        comm.barrier()
+        comm.close()
     ctx.close()
     return 0
 

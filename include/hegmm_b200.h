@@ -217,6 +217,45 @@ int hgm_batch_decrypt(hgm_ctx* ctx, hgm_batch* b, int64_t* C);
 int hgm_batch_decrypt_words(hgm_ctx* ctx, const uint64_t* dev_words, size_t count, size_t S,
                             int64_t* out);
 void hgm_batch_free(hgm_batch* b);
+/* Decrypts and unpacks `count` result ciphertexts of a product shape held in
+ * device memory (e.g. gathered from other ranks by hgm_comm_gather_batch) into
+ * host C[count][m][n]: the client-side decrypt of algorithms.cpp:244-247. */
+int hgm_decrypt_products(hgm_ctx* ctx, int algo, int order, int flags, size_t m, size_t l, size_t n,
+                         const uint64_t* dev_words, size_t count, int64_t* C);
+
+/* Multi-GPU (reference analogue: the std::async pool over
+ * independent cases, costmodel.cpp:273-296).  One process per GPU, one NCCL
+ * communicator per session over NVLink / NVSwitch.  Work shards by independent
+ * products or output blocks with keys replicated per GPU; the communicator
+ * only MOVES result ciphertexts (never reduces them: NCCL sums wrap mod 2^64,
+ * not mod q) and carries control values.  Every call is collective over the
+ * communicator and stream-ordered after the session's queued work.
+ *   hgm_comm_unique_id / hgm_comm_init   NCCL bootstrap with a caller-distributed id
+ *   hgm_comm_init_file                   the same, rank 0 publishing the id at `path`
+ *                                        (atomic rename; other ranks poll, timeout_s)
+ *   hgm_comm_barrier                     after every rank's queued work
+ *   hgm_comm_max                         host double, max over ranks (timings)
+ *   hgm_comm_gather                      variable-size gather of device words to `root`
+ *                                        (rank order); recv / recv_cap_words used on root
+ *   hgm_comm_gather_batch                every rank's batch results to `root`, in rank
+ *                                        order, into a device buffer the library allocates
+ *                                        (free with hgm_comm_buffer_free); b may be NULL
+ *                                        on a rank without instances */
+typedef struct hgm_comm hgm_comm;
+#define HGM_COMM_ID_BYTES 128
+int hgm_comm_unique_id(uint8_t* id);
+int hgm_comm_init(hgm_ctx* ctx, int rank, int world, const uint8_t* id, hgm_comm** out);
+int hgm_comm_init_file(hgm_ctx* ctx, int rank, int world, const char* path, double timeout_s, hgm_comm** out);
+void hgm_comm_destroy(hgm_comm* comm);
+int hgm_comm_rank(const hgm_comm* comm);
+int hgm_comm_size(const hgm_comm* comm);
+int hgm_comm_barrier(hgm_comm* comm);
+int hgm_comm_max(hgm_comm* comm, double* value);
+int hgm_comm_gather(hgm_comm* comm, const uint64_t* send, size_t send_words, uint64_t* recv,
+                    size_t recv_cap_words, int root, size_t* recv_words);
+int hgm_comm_gather_batch(hgm_comm* comm, hgm_batch* b, int root, uint64_t** dev_out, size_t* total_count);
+int hgm_comm_buffer_free(hgm_comm* comm, uint64_t* p);
+
 /* Program facts of a product shape (no GPU needed): stats[12] as hgm_stats,
  * facts[0]=segment [1]=encryptions [2]=rotations after CSE [3]=masked sums
  * [4]=CC-mults [5]=levels [6]=flatten order used [7]=ModDowns (values with a
@@ -245,6 +284,8 @@ long hgm_plan_info(int kind, size_t k, size_t a, size_t b, size_t c, int order, 
 
 /* Kernel-level timing hooks for bench.py (CUDA events on the library stream). */
 int hgm_bench_ntt(hgm_ctx* ctx, int forward, size_t limbs, int iters, float* ms_per_iter);
+/* key-switch inner product (k_ks_inner) over `items` rotations, 8 per Galois key */
+int hgm_bench_keyswitch(hgm_ctx* ctx, size_t items, int iters, float* ms_per_iter);
 int hgm_device_sync(hgm_ctx* ctx);
 /* Test hook: in-place NTT of `count` host limbs (count*N words) under one
  * prime (index into Q ++ P ++ B, or -1 for t). */

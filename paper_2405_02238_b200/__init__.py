@@ -17,6 +17,28 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HGM_LIB") or os.path.join(_HERE, "libhegmm_b200.so")
 
+
+def _nccl_wheel() -> Optional[str]:
+    """The nvidia-nccl wheel's libnccl.so.2 when installed (the build torch also
+    loads): the library binds NCCL lazily and prefers one copy per process."""
+    import importlib.util
+
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return None
+    for base in (spec.submodule_search_locations or []) if spec else []:
+        cand = os.path.join(base, "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            return cand
+    return None
+
+
+if not os.environ.get("HGM_NCCL_LIB"):
+    _w = _nccl_wheel()
+    if _w:
+        os.environ["HGM_NCCL_LIB"] = _w
+
 HGM_OK, HGM_EDIM, HGM_ECAP, HGM_EINTERNAL, HGM_EOVERFLOW, HGM_ECUDA, HGM_EARG = range(7)
 PHASE_CLIENT, PHASE_CLOUD = 0, 1
 # C ABI symbols declared in include/hegmm_b200.h
@@ -33,6 +55,9 @@ EXPORTS = (
     "hgm_program_stream", "hgm_plan_info", "hgm_blocked_mm",
     "hgm_ctx_create_ex", "hgm_key_words", "hgm_key_export", "hgm_key_upload", "hgm_key_drop_secret",
     "hgm_key_has", "hgm_galois_element", "hgm_encrypt_noise", "hgm_reserve_counters", "hgm_program_keys",
+    "hgm_decrypt_products", "hgm_comm_unique_id", "hgm_comm_init", "hgm_comm_init_file", "hgm_comm_destroy",
+    "hgm_comm_rank", "hgm_comm_size", "hgm_comm_barrier", "hgm_comm_max", "hgm_comm_gather",
+    "hgm_comm_gather_batch", "hgm_comm_buffer_free", "hgm_bench_keyswitch",
 )
 CTX_KEYLESS, CTX_OS_SEED = 1, 2
 COUNTER_AUTO = (1 << 64) - 1
@@ -131,6 +156,63 @@ class Batch:
             pass
 
 
+class Comm:
+    """The session's NCCL communicator (include/hegmm_b200.h, hgm_comm_*): one
+    process per GPU; moves result ciphertexts and control values only."""
+
+    def __init__(self, ctx: "Context", rank: int, world: int, id_file: Optional[str] = None,
+                 unique_id: Optional[bytes] = None, timeout_s: float = 120.0):
+        self.ctx = ctx
+        h = ctypes.c_void_p()
+        if unique_id is not None:
+            buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+            _check(lib().hgm_comm_init(ctx._h, rank, world, buf, ctypes.byref(h)))
+        else:
+            if id_file is None:
+                raise ValueError("Comm needs id_file or unique_id")
+            _check(lib().hgm_comm_init_file(ctx._h, rank, world, id_file.encode(), timeout_s, ctypes.byref(h)))
+        self._h = h.value
+        self.rank, self.world = rank, world
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(lib().hgm_comm_unique_id(buf))
+        return buf.raw
+
+    def barrier(self) -> None:
+        _check(lib().hgm_comm_barrier(self._h))
+
+    def max(self, x: float) -> float:
+        v = ctypes.c_double(float(x))
+        _check(lib().hgm_comm_max(self._h, ctypes.byref(v)))
+        return v.value
+
+    def gather_batch(self, batch: Optional["Batch"], root: int = 0):
+        """Every rank's batch results to `root` (rank order): (device pointer,
+        count) on the root -- free with free_buffer -- and (None, 0) elsewhere."""
+        p = ctypes.c_void_p()
+        n = ctypes.c_size_t()
+        _check(lib().hgm_comm_gather_batch(self._h, batch._h if batch is not None else None, root,
+                                           ctypes.byref(p), ctypes.byref(n)))
+        return (p.value, n.value) if p.value else (None, 0)
+
+    def free_buffer(self, ptr: Optional[int]) -> None:
+        if ptr:
+            _check(lib().hgm_comm_buffer_free(self._h, ptr))
+
+    def close(self) -> None:
+        if self._h:
+            lib().hgm_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class HEError(RuntimeError):
     """Base error (reference hegmm::Error, errors.hpp:10-14)."""
 
@@ -199,6 +281,7 @@ def lib() -> ctypes.CDLL:
         "hgm_blocked_mm": (_int, [_vp, _int, _sz, _sz, _sz, _vp, _sz, _vp, _sz, _vp, _sz, _vp, _vp, _vp, _u64, _vp]),
         "hgm_bench_ntt": (_int, [_vp, _int, _sz, _int, _vp]),
         "hgm_device_sync": (_int, [_vp]),
+        "hgm_bench_keyswitch": (_int, [_vp, _sz, _int, _vp]),
         "hgm_test_ntt": (_int, [_vp, _int, _int, _vp, _sz]),
         "hgm_launch_count": (_u64, [_vp]),
         "hgm_batch_encrypt": (_int, [_vp, _int, _int, _int, _sz, _sz, _sz, _sz, _vp, _vp, _u64, _vp]),
@@ -221,6 +304,18 @@ def lib() -> ctypes.CDLL:
         "hgm_encrypt_noise": (_int, [_vp, _vp, _sz, _vp, _vp, _vp, _vp]),
         "hgm_reserve_counters": (_u64, [_vp, _u64]),
         "hgm_program_keys": (ctypes.c_long, [_int, _int, _int, _sz, _sz, _sz, _sz, ctypes.c_uint32, _vp, _sz]),
+        "hgm_decrypt_products": (_int, [_vp, _int, _int, _int, _sz, _sz, _sz, _vp, _sz, _vp]),
+        "hgm_comm_unique_id": (_int, [_vp]),
+        "hgm_comm_init": (_int, [_vp, _int, _int, _vp, _vp]),
+        "hgm_comm_init_file": (_int, [_vp, _int, _int, ctypes.c_char_p, ctypes.c_double, _vp]),
+        "hgm_comm_destroy": (None, [_vp]),
+        "hgm_comm_rank": (_int, [_vp]),
+        "hgm_comm_size": (_int, [_vp]),
+        "hgm_comm_barrier": (_int, [_vp]),
+        "hgm_comm_max": (_int, [_vp, _vp]),
+        "hgm_comm_gather": (_int, [_vp, _vp, _sz, _vp, _sz, _int, _vp]),
+        "hgm_comm_gather_batch": (_int, [_vp, _vp, _int, _vp, _vp]),
+        "hgm_comm_buffer_free": (_int, [_vp, _vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -475,6 +570,14 @@ class Context:
                                     _ptr(A), _ptr(B), _ptr(C), _counter(counter0), _ptr(log)))
         return C, log
 
+    def decrypt_products(self, dev_ptr: int, count: int, m: int, l: int, n: int, algo: int = 0, order: int = -1,
+                         flags: int = 0) -> np.ndarray:
+        """Decrypts and unpacks `count` result ciphertexts of an (m, l, n) product
+        held in device memory at dev_ptr (e.g. a Comm.gather_batch buffer)."""
+        C = np.zeros((count, m, n), dtype=np.int64)
+        _check(lib().hgm_decrypt_products(self._h, algo, order, flags, m, l, n, dev_ptr, count, _ptr(C)))
+        return C
+
     def decrypt_words(self, words, segment: int) -> np.ndarray:
         """Decrypts ciphertexts held in a device buffer (a torch CUDA tensor, e.g.
         one gathered over NCCL, or a raw device pointer for one ciphertext)."""
@@ -494,6 +597,12 @@ class Context:
     def bench_ntt(self, limbs: int, iters: int = 20, forward: bool = True) -> float:
         ms = ctypes.c_float()
         _check(lib().hgm_bench_ntt(self._h, 1 if forward else 0, limbs, iters, ctypes.byref(ms)))
+        return ms.value
+
+    def bench_keyswitch(self, items: int, iters: int = 10) -> float:
+        """ms per k_ks_inner launch over `items` rotations (8 per Galois key)."""
+        ms = ctypes.c_float()
+        _check(lib().hgm_bench_keyswitch(self._h, items, iters, ctypes.byref(ms)))
         return ms.value
 
     def sync(self) -> None:

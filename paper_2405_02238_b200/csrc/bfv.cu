@@ -1514,6 +1514,64 @@ void Context::modup(int n, const u64* const* ct, u64* const* out) {
     HGM_CUDA(cudaGetLastError());
 }
 
+__global__ void k_fill_residues(DevCtx cx, u64* p, u32 limbs, u32 first_prime, u32 period, u64 seed) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
+    const size_t N = dp->N, words = (size_t)limbs * N;
+    for (size_t w = (size_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (size_t)gridDim.x * blockDim.x) {
+        const u64 q = dp->pr[first_prime + (u32)((w / N) % period)].q;
+        p[w] = prng(seed, 0, w) % q;
+    }
+}
+
+void Context::fill_residues(u64* p, u32 limbs, u32 first_prime, u32 period, u64 seed) {
+    k_fill_residues<<<148 * 8, 256, 0, stream_>>>(cx_, p, limbs, first_prime, period, seed); ++launches_;
+    HGM_CUDA(cudaGetLastError());
+}
+
+float Context::bench_inner_product(int items, int iters) {
+    const u32 N = hp_.N, R = hp_.R, dnum = hp_.dnum;
+    const size_t dw = (size_t)dnum * R * N, aw = ks_words();
+    u64* D = alloc((size_t)items * dw);
+    u64* A = alloc((size_t)items * aw);
+    u64* C0 = alloc((size_t)items * ct_words());
+    for (int i = 0; i < items; ++i) {
+        fill_residues(D + i * dw, dnum * R, 0, R, 11 + i);
+        fill_residues(C0 + i * ct_words(), 2 * hp_.L, 0, hp_.L, 7 + i);
+    }
+    // groups of kKeyReuse rotations share one Galois key (the engine's order)
+    std::vector<u32> elts;
+    for (int i = 0; i < (items + kKeyReuse - 1) / kKeyReuse; ++i) elts.push_back(galois_of(1 + i % 64, N));
+    ensure_galois_keys(elts);
+    std::vector<const u64*> dig(items), keys(items), c0(items);
+    std::vector<u64*> acc(items);
+    std::vector<u32> g(items);
+    for (int i = 0; i < items; ++i) {
+        dig[i] = D + i * dw;
+        g[i] = elts[i / kKeyReuse];
+        keys[i] = ks_key(g[i]);
+        acc[i] = A + i * aw;
+        c0[i] = C0 + i * ct_words();
+    }
+    inner_product(items, dig.data(), keys.data(), g.data(), acc.data(), c0.data());  // warm-up
+    cudaEvent_t e0, e1;
+    HGM_CUDA(cudaEventCreate(&e0));
+    HGM_CUDA(cudaEventCreate(&e1));
+    HGM_CUDA(cudaEventRecord(e0, stream_));
+    for (int it = 0; it < iters; ++it)
+        inner_product(items, dig.data(), keys.data(), g.data(), acc.data(), c0.data());
+    HGM_CUDA(cudaEventRecord(e1, stream_));
+    HGM_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    HGM_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    release(D);
+    release(A);
+    release(C0);
+    sync();
+    return ms / iters;
+}
+
 void Context::inner_product(int n, const u64* const* digits, const u64* const* keys, const u32* g,
                             u64* const* acc, const u64* const* c0) {
     std::vector<const u64*> vd(digits, digits + n), vk(keys, keys + n);

@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "../../include/hegmm_b200.h"
+#include "capi_internal.hpp"
 #include "context.hpp"
 #include "engine.hpp"
 #include "parallel.hpp"
@@ -960,6 +961,22 @@ struct hgm_batch {
     }
 };
 
+namespace hgm {
+
+Context& session_context(hgm_ctx* c) { return *c->ctx; }
+int session_device(const hgm_ctx* c) { return c->device; }
+std::recursive_mutex& session_exec_mutex(hgm_ctx* c) { return c->exec_mu; }
+void session_retain(hgm_ctx* c) { ctx_retain(c); }
+void session_release(hgm_ctx* c) { ctx_release(c); }
+hgm_ctx* batch_session(hgm_batch* b) { return b ? b->owner : nullptr; }
+const u64* batch_results(const hgm_batch* b, size_t* count) {
+    if (count) *count = b ? b->count : 0;
+    return b ? b->out : nullptr;
+}
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+
+}  // namespace hgm
+
 namespace {
 
 size_t lockstep_chunk(Context& ctx, const MatmulProgram& prog) {
@@ -1075,6 +1092,23 @@ int hgm_batch_decrypt_words(hgm_ctx* c, const uint64_t* dev_words, size_t count,
             }
             ctx.decrypt((int)K, cts.data(), Sv.data(), outp.data());
         }
+    });
+}
+
+int hgm_decrypt_products(hgm_ctx* c, int algo, int order, int flags, size_t m, size_t l, size_t n,
+                         const uint64_t* dev_words, size_t count, int64_t* C) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
+    DeviceScope dev(c);
+    return guarded([&] {
+        if (order < -1 || order > 1) throw std::invalid_argument("order must be -1, 0 or 1");
+        auto prog = get_matmul_program(algo, order, m, l, n, c->ctx->slots(), c->ctx->host().N, flags);
+        std::vector<i64> slots(count * prog->segment);
+        const int rc = hgm_batch_decrypt_words(c, dev_words, count, prog->segment, slots.data());
+        if (rc != HGM_OK) throw std::runtime_error(g_err);
+        parallel_for(count, [&](size_t k) {
+            std::vector<i64> v(slots.begin() + k * prog->segment, slots.begin() + (k + 1) * prog->segment);
+            prog->unpack(v, C + k * m * n);
+        });
     });
 }
 
@@ -1221,7 +1255,7 @@ int hgm_bench_ntt(hgm_ctx* c, int forward, size_t limbs, int iters, float* ms) {
         Context& ctx = *c->ctx;
         const u32 N = ctx.host().N, L = ctx.host().L;
         u64* buf = ctx.alloc(limbs * N);
-        HGM_CUDA(cudaMemsetAsync(buf, 0, limbs * N * 8, ctx.stream()));
+        ctx.fill_residues(buf, (u32)limbs, 0, L, 0x6e7474);  // canonical operands, not zeros
         NttJobs j = jobs_contig(buf, (u32)limbs, 0, L);
         ctx.ntt(forward != 0, j);  // warm-up
         cudaEvent_t e0, e1;
@@ -1238,6 +1272,15 @@ int hgm_bench_ntt(hgm_ctx* c, int forward, size_t limbs, int iters, float* ms) {
         cudaEventDestroy(e1);
         ctx.release(buf);
         ctx.sync();
+    });
+}
+
+int hgm_bench_keyswitch(hgm_ctx* c, size_t items, int iters, float* ms) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
+    DeviceScope dev(c);
+    return guarded([&] {
+        if (items == 0 || iters <= 0 || !ms) throw std::invalid_argument("bad benchmark arguments");
+        *ms = c->ctx->bench_inner_product((int)items, iters);
     });
 }
 

@@ -161,6 +161,13 @@ class Context {
 
     // batched NTT helpers (exposed for tests / micro-benchmarks)
     void ntt(bool forward, const NttJobs& jobs);
+    // micro-benchmark inputs: limb l gets pseudo-random residues of prime
+    // first_prime + l % period (canonical, so the kernels see real operands)
+    void fill_residues(u64* p, u32 limbs, u32 first_prime, u32 period, u64 seed);
+    // micro-benchmark of the key-switch inner product (k_ks_inner) over `items`
+    // rotations in groups of 8 sharing a Galois key, as the engine orders them;
+    // returns ms per launch (CUDA events on the library stream)
+    float bench_inner_product(int items, int iters);
     u64 launches() const { return launches_.load(); }
 
   private:

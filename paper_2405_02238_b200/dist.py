@@ -1,11 +1,16 @@
-"""Multi-GPU plumbing: instances are sharded across ranks with
-no data-path collective; the only exchange is gathering each rank's result
-ciphertexts to rank 0 (one process per GPU, torch.distributed over NCCL on the
-B200 box, gloo in the CPU tests).  NCCL never reduces ciphertexts: its sums
-wrap mod 2^64, not mod q, so results are moved, never added, in transit."""
+"""Multi-GPU plumbing, torch-free: one process per GPU, the
+library's own NCCL communicator (``hgm_comm_*``, ``paper_2405_02238_b200.Comm``).
+
+Work shards by independent products (config 4: instance ranges) or output row
+blocks (config 5); keys are replicated per GPU, so a rank's shard needs no
+data-path collective.  The only exchange is the gather of each rank's result
+ciphertexts to rank 0, which decrypts (NCCL never reduces ciphertexts: its sums
+wrap mod 2^64, not mod q).  Reference analogue: the std::async pool over
+independent cases, /root/reference/proj/src/costmodel.cpp:273-296."""
 from __future__ import annotations
 
-from typing import List, Optional, Tuple
+import os
+from typing import Dict, List, Optional, Tuple
 
 
 def shard(rank: int, world: int, total: int) -> Tuple[int, int]:
@@ -23,24 +28,37 @@ def counter_base(first_instance: int, encryptions_per_instance: int) -> int:
     return first_instance * encryptions_per_instance
 
 
-def gather_ciphertexts(dist, local, count: int, words: int, total: int, world: int, rank: int,
-                       device=None) -> Optional[List]:
-    """Gathers `count` ciphertexts of `words` uint64 words (as an int64 tensor
-    `local` of count*words elements) from every rank to rank 0.  Returns, on
-    rank 0, the list of per-rank tensors trimmed to their true counts (instance
-    order = rank order); None elsewhere.  Shards may differ by one instance, so
-    each rank sends a buffer padded to the largest shard."""
-    import torch
+def gather_layout(world: int, total: int) -> List[Tuple[int, int]]:
+    """(first, count) of every rank's shard: the order and sizes in which
+    Comm.gather_batch lays the gathered ciphertexts out on the root."""
+    return [shard(r, world, total) for r in range(world)]
 
-    maxc = max(shard(r, world, total)[1] for r in range(world))
-    send = torch.zeros(maxc * words, dtype=torch.int64, device=device)
-    if count:
-        send[: count * words] = local[: count * words]
-    outs = [torch.empty_like(send) for _ in range(world)] if rank == 0 else None
-    dist.gather(send, outs, dst=0)
-    if rank != 0:
+
+def env_rank() -> Tuple[int, int, int]:
+    """(rank, world, local_rank) from the torchrun / launcher environment."""
+    g = os.environ.get
+    return int(g("RANK", 0)), int(g("WORLD_SIZE", 1)), int(g("LOCAL_RANK", 0))
+
+
+def id_file_path() -> str:
+    """Where rank 0 publishes the NCCL id for this launch: unique per launcher
+    process (all ranks of one torchrun share its pid) and master port."""
+    explicit = os.environ.get("HGM_COMM_ID_FILE")
+    if explicit:
+        return explicit
+    port = os.environ.get("MASTER_PORT", "0")
+    run = os.environ.get("TORCHELASTIC_RUN_ID", "none")
+    return f"/tmp/hgm_comm_{port}_{run}_{os.getppid()}.id"
+
+
+def comm_from_env(ctx) -> Optional["object"]:
+    """The session's communicator for a multi-rank launch (None at world 1)."""
+    import paper_2405_02238_b200 as hb
+
+    rank, world, _ = env_rank()
+    if world <= 1:
         return None
-    return [outs[r][: shard(r, world, total)[1] * words] for r in range(world)]
+    return hb.Comm(ctx, rank, world, id_file=id_file_path())
 
 
 def row_blocks(m: int, parts: int) -> List[Tuple[int, int]]:
@@ -50,23 +68,45 @@ def row_blocks(m: int, parts: int) -> List[Tuple[int, int]]:
     return [shard(r, parts, m) for r in range(parts)]
 
 
-def sharded_matmul(ctx, A, B, parts: int, algo: int = 1, rank: int = 0, world: int = 1, counter0: int = 0):
-    """Runs this rank's share of the row blocks of A.B as one lockstep batch on
-    its GPU (blocks of equal height share one compiled program).  Returns
-    {block index: C block} for the blocks this rank owns."""
+def sharded_matmul(ctx, A, B, parts: int, algo: int = 1, comm=None, counter0: int = 0,
+                   timings: Optional[Dict[str, float]] = None):
+    """Config-5 decomposition: the `parts` row blocks of A.B, rank r running its
+    share as one lockstep batch on its GPU (block b encrypts from counter
+    counter0 + 2 b, as a single GPU would), the result ciphertexts gathered to
+    rank 0 over the library's NCCL communicator and decrypted there.
+    Returns C (m x n, mod t) on rank 0 and None elsewhere.  Row blocks must be
+    of equal height (one compiled program)."""
     import numpy as np
 
+    import paper_2405_02238_b200 as hb
+
+    rank, world = (comm.rank, comm.world) if comm is not None else (0, 1)
     blocks = row_blocks(A.shape[0], parts)
+    heights = {h for _, h in blocks}
+    if len(heights) != 1:
+        raise ValueError("row blocks of unequal height: use parts dividing m")
+    h = heights.pop()
     first, count = shard(rank, world, parts)
-    mine = list(range(first, first + count))
-    out = {}
-    by_height = {}
-    for bi in mine:
-        by_height.setdefault(blocks[bi][1], []).append(bi)
-    for height, ids in by_height.items():
-        As = np.stack([A[blocks[bi][0]: blocks[bi][0] + height] for bi in ids])
-        Bs = np.stack([B for _ in ids])
-        C, _ = ctx.matmul_batch(As, Bs, algo=algo, counter0=counter0 + ids[0] * 2)
-        for k, bi in enumerate(ids):
-            out[bi] = C[k]
-    return out
+    E = hb.program_info(algo, h, A.shape[1], B.shape[1], ctx.slot_count, ctx.N)[1]["encryptions"]
+    bt = None
+    if count:
+        As = np.stack([A[blocks[b][0]: blocks[b][0] + h] for b in range(first, first + count)])
+        Bs = np.stack([B] * count)
+        bt = hb.Batch(ctx, As, Bs, algo=algo, counter0=counter0 + first * E)
+        ms = bt.cloud()
+        if timings is not None:
+            timings["cloud_ms"] = ms
+    try:
+        if comm is None:
+            return np.concatenate(list(bt.decrypt()))
+        ptr, n = comm.gather_batch(bt, root=0)
+        if rank != 0:
+            return None
+        try:
+            C = ctx.decrypt_products(ptr, n, h, A.shape[1], B.shape[1], algo=algo)
+        finally:
+            comm.free_buffer(ptr)
+        return np.concatenate(list(C))
+    finally:
+        if bt is not None:
+            bt.free()

@@ -49,3 +49,9 @@ def test_no_gpu_context_fails_loudly():
         pass
     with pytest.raises(hb.HEError):
         hb.Context(2, 1, 0)
+
+
+def test_nccl_unique_id_without_gpu():
+    """The communicator bootstrap id is produced by the library (NCCL, no torch)."""
+    a, b = hb.Comm.unique_id(), hb.Comm.unique_id()
+    assert len(a) == 128 and a != b

@@ -3,16 +3,18 @@
 Each rank encrypts and multiplies its shard of instances with the reference
 algorithms over the CPU BFV oracle (the stand-in for its GPU), using the same
 encryption counters a single-GPU run would use; rank 0 gathers the result
-ciphertexts with the same paper_2405_02238_b200.dist.gather_ciphertexts that
-bench.py runs over NCCL, decrypts them, and checks every product and that the
-gathered words equal a single-process run of the same instances."""
+ciphertexts in the layout the library's NCCL gather uses
+(paper_2405_02238_b200.dist.gather_layout: rank order, variable-size shards;
+gloo stands in for hgm_comm_gather_batch here), decrypts them, and checks every
+product and that the gathered words equal a single-process run of the same
+instances."""
 import os
 import socket
 
 import numpy as np
 import pytest
 
-from paper_2405_02238_b200.dist import counter_base, gather_ciphertexts, shard
+from paper_2405_02238_b200.dist import counter_base, gather_layout, id_file_path, shard
 
 TOTAL, M, L, N = 5, 3, 4, 2
 
@@ -23,6 +25,23 @@ def free_port():
     p = s.getsockname()[1]
     s.close()
     return p
+
+
+def gather_ciphertexts(dist, local, count, words, total, world, rank):
+    """gloo stand-in for hgm_comm_gather_batch: pads every shard to the largest
+    and trims on the root to gather_layout's counts."""
+    import torch
+
+    layout = gather_layout(world, total)
+    maxc = max(c for _, c in layout)
+    send = torch.zeros(maxc * words, dtype=torch.int64)
+    if count:
+        send[: count * words] = local[: count * words]
+    outs = [torch.empty_like(send) for _ in range(world)] if rank == 0 else None
+    dist.gather(send, outs, dst=0)
+    if rank != 0:
+        return None
+    return [outs[r][: layout[r][1] * words] for r in range(world)]
 
 
 def worker(rank, world, port, q):
@@ -67,6 +86,16 @@ def test_sharding_is_a_partition():
         assert spans[0][0] == 0 and sum(c for _, c in spans) == 4096
         for (f0, c0), (f1, _) in zip(spans, spans[1:]):
             assert f0 + c0 == f1
+
+
+def test_gather_layout_and_id_path(monkeypatch):
+    assert gather_layout(3, 8) == [(0, 2), (2, 3), (5, 3)]
+    monkeypatch.setenv("MASTER_PORT", "29511")
+    monkeypatch.delenv("HGM_COMM_ID_FILE", raising=False)
+    p = id_file_path()
+    assert p.startswith("/tmp/hgm_comm_29511_") and p.endswith(f"_{os.getppid()}.id")
+    monkeypatch.setenv("HGM_COMM_ID_FILE", "/tmp/x.id")
+    assert id_file_path() == "/tmp/x.id"
 
 
 def test_gloo_world2_gather_and_decrypt(ref):
