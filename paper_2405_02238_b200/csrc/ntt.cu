@@ -1,6 +1,8 @@
 // ntt.cu -- see ntt.cuh for the design.
 #include "ntt.cuh"
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <mutex>
 #include <utility>
@@ -1214,6 +1216,180 @@ void launch_block_e(bool fwd, const DevCtx& cx, const NttJobs& jobs, int sub, cu
         k_ntt_inv3<LB, E, MINB><<<grid, (1 << LB) / E, smem, s>>>(cx, j);
 }
 
+// ---------------------------------------------------------------- N = 2^15: 4-CTA clusters
+// One limb of 2^15 residues (256 KiB) crosses HBM once: a cluster of four CTAs
+// holds it in their shared memories (one 2^13 quarter each, the same 72 KB image
+// as k_ntt_fwd3), and the two outermost stages, which pair elements j, j + N/4,
+// j + N/2, j + 3N/4 of different quarters, exchange them through distributed
+// shared memory instead of an extra HBM pass.
+//
+// Forward: CTA r loads columns j in [r N/16, (r+1) N/16) of all four quarters
+// straight from HBM (coalesced), applies the two outer stages in registers and
+// stores each result into the owning quarter's shared memory (three of the four
+// remotely); after a cluster barrier every CTA runs the 13 block stages of its
+// quarter (twiddle offset pre = 2, blk = r) and stores it.
+// Inverse: every CTA runs the 13 block stages of its quarter (first stage fused
+// into its load), then after a cluster barrier CTA r reads its columns of the
+// four quarters (three remotely), applies the two outer stages (+ N^-1) and
+// writes them to HBM; a final barrier keeps the shared memories alive until
+// every remote read is done.
+// 32-bit shared::cluster addresses (mapa): four quarters cost four registers
+__device__ __forceinline__ u32 dsmem_base(const u64* local, u32 rank) {
+    u32 r;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((u32)__cvta_generic_to_shared(local)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void dsmem_st(u32 base, int i, u64 v) {
+    asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(base + 8u * (u32)i), "l"(v) : "memory");
+}
+__device__ __forceinline__ u64 dsmem_ld(u32 base, int i) {
+    u64 v;
+    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(base + 8u * (u32)i) : "memory");
+    return v;
+}
+
+template <int LB>
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__((1 << LB) / kElems3, 3)
+    k_ntt_fwd_c4(DevCtx cx, NttJobs jobs) {
+    namespace cg = cooperative_groups;
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
+    extern __shared__ u64 sm[];
+    u64* cache = sm + smem_words<LB>();
+    constexpr int NB = 1 << LB, T = NB / kElems3, COLS = NB / 4;
+    const u32 N = dp->N;
+    const int logN = (int)dp->logN;
+    const int blk = (int)(blockIdx.x & 3);
+    const JobView jv = job_of(jobs, blockIdx.x >> 2, N);
+    const u64 q = dp->pr[jv.prime].q;
+    const u64* w = cx.tw + (size_t)jv.prime * 4 * N;
+    fill_tw_cache_async(cache, pairs(w), 2, blk, kTwCache3);
+    const ulonglong2* t = pairs(w);
+    const u64 w1 = t[1].x, w1s = t[1].y, w2 = t[2].x, w2s = t[2].y, w3 = t[3].x, w3s = t[3].y;
+    u32 quarter[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) quarter[r] = dsmem_base(sm, r);
+    const u64* a = jv.ptr;
+    constexpr int kBatch = 4;  // columns per batch: 16 loads in flight per thread
+#pragma unroll 1
+    for (int c0 = 0; c0 < COLS / T; c0 += kBatch) {
+        u64 x[kBatch][4];
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            const int j = blk * COLS + (c0 + b) * T + (int)threadIdx.x;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) x[b][k] = __ldcs(a + j + k * NB);
+        }
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            const int j = blk * COLS + (c0 + b) * T + (int)threadIdx.x;
+            u64 V = shoup_mul(x[b][2], w1, w1s, q);
+            const u64 y0 = add_mod(x[b][0], V, q), y2 = sub_mod(x[b][0], V, q);
+            V = shoup_mul(x[b][3], w1, w1s, q);
+            const u64 y1 = add_mod(x[b][1], V, q), y3 = sub_mod(x[b][1], V, q);
+            V = shoup_mul(y1, w2, w2s, q);
+            const int p = pad(j);
+            dsmem_st(quarter[0], p, add_mod(y0, V, q));
+            dsmem_st(quarter[1], p, sub_mod(y0, V, q));
+            V = shoup_mul(y3, w3, w3s, q);
+            dsmem_st(quarter[2], p, add_mod(y2, V, q));
+            dsmem_st(quarter[3], p, sub_mod(y2, V, q));
+        }
+    }
+    cp_async_wait_all();
+    cg::this_cluster().sync();  // every quarter complete (and the twiddle caches)
+    fwd_round<LB, 0, 4, true, false, NoLoad, kElems3>(sm, cache, pairs(w), q, 2, blk);
+    __syncthreads();
+    fwd_round<LB, 4, 4, true, false, NoLoad, kElems3>(sm, cache, pairs(w), q, 2, blk);
+    __syncthreads();
+    fwd_round<LB, 8, LB - 9, false, false, NoLoad, kElems3>(sm, cache, pairs(w), q, 2, blk);
+    __syncthreads();
+    store_last_stage<LB, kElems3>(sm, jv.ptr + ((size_t)blk << LB), pairs(w), q, logN, blk);
+}
+
+template <int LB>
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__((1 << LB) / kElems3, 3)
+    k_ntt_inv_c4(DevCtx cx, NttJobs jobs) {
+    namespace cg = cooperative_groups;
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
+    extern __shared__ u64 sm[];
+    u64* cache = sm + smem_words<LB>();
+    constexpr int NB = 1 << LB, T = NB / kElems3, COLS = NB / 4;
+    const u32 N = dp->N;
+    const int logN = (int)dp->logN;
+    const int blk = (int)(blockIdx.x & 3);
+    const JobView jv = job_of(jobs, blockIdx.x >> 2, N);
+    const Prime& P = dp->pr[jv.prime];
+    const u64 q = P.q;
+    const u64* w = cx.tw + (size_t)jv.prime * 4 * N;
+    fill_tw_cache_async(cache, pairs(w + 2 * N), logN - LB, blk, kTwCache3);
+    load_first_stage<LB, kElems3, 8>(sm, jv.ptr + ((size_t)blk << LB), pairs(w + 2 * N), q, logN, blk);
+    cp_async_wait_all();
+    __syncthreads();
+    inv_round<LB, 1, LB - 9, false, kElems3>(sm, cache, pairs(w + 2 * N), q, logN, blk);
+    __syncthreads();
+    inv_round<LB, LB - 8, 4, true, kElems3>(sm, cache, pairs(w + 2 * N), q, logN, blk);
+    __syncthreads();
+    inv_round<LB, LB - 4, 4, true, kElems3>(sm, cache, pairs(w + 2 * N), q, logN, blk);
+    cg::this_cluster().sync();  // all four quarters transformed
+    const ulonglong2* t = pairs(w + 2 * N);
+    const u64 w1 = t[1].x, w1s = t[1].y, w2 = t[2].x, w2s = t[2].y, w3 = t[3].x, w3s = t[3].y;
+    const bool scale = !jobs.unscaled;
+    u32 quarter[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) quarter[r] = dsmem_base(sm, r);
+    u64* a = jv.ptr;
+    const u64 q2 = q << 1;
+    constexpr int kBatch = 4;
+#pragma unroll 1
+    for (int c0 = 0; c0 < COLS / T; c0 += kBatch) {
+        u64 x[kBatch][4];
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            const int p = pad(blk * COLS + (c0 + b) * T + (int)threadIdx.x);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) x[b][k] = reduce_once(reduce_once(dsmem_ld(quarter[k], p), q2), q);  // [0, 4q) -> [0, q)
+        }
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            const int j = blk * COLS + (c0 + b) * T + (int)threadIdx.x;
+            // t = N/4: pairs (0,1) with w[2], (2,3) with w[3]; t = N/2: (0,2), (1,3) with w[1]
+            const u64 y0 = add_mod(x[b][0], x[b][1], q), y1 = shoup_mul(sub_mod(x[b][0], x[b][1], q), w2, w2s, q);
+            const u64 y2 = add_mod(x[b][2], x[b][3], q), y3 = shoup_mul(sub_mod(x[b][2], x[b][3], q), w3, w3s, q);
+            u64 z[4];
+            z[0] = add_mod(y0, y2, q);
+            z[2] = shoup_mul(sub_mod(y0, y2, q), w1, w1s, q);
+            z[1] = add_mod(y1, y3, q);
+            z[3] = shoup_mul(sub_mod(y1, y3, q), w1, w1s, q);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) __stcs(a + j + k * NB, scale ? shoup_mul(z[k], P.ninv, P.ninv_sh, q) : z[k]);
+        }
+    }
+    cg::this_cluster().sync();  // keep this CTA's shared memory until every remote read is done
+}
+
+bool ntt_cluster4() {
+    static const bool on = [] {
+        const char* e = std::getenv("HGM_NTT_CLUSTER");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <int LB>
+void launch_c4(bool fwd, const DevCtx& cx, const NttJobs& jobs, cudaStream_t s) {
+    const size_t smem = (smem_words<LB>() + 2 * kTwCache3) * sizeof(u64);
+    static std::once_flag once[64];
+    once_per_device(once, [&] {
+        cudaFuncSetAttribute(k_ntt_fwd_c4<LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_ntt_inv_c4<LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    const dim3 grid(jobs.count * 4);
+    if (fwd)
+        k_ntt_fwd_c4<LB><<<grid, (1 << LB) / kElems3, smem, s>>>(cx, jobs);
+    else
+        k_ntt_inv_c4<LB><<<grid, (1 << LB) / kElems3, smem, s>>>(cx, jobs);
+}
+
 // shared-memory resident block kernels: 256 threads x 32 residues, 3 CTAs/SM
 // (default), 512 x 16 at 2 CTAs/SM (HGM_NTT_E=16: spills, -8%), or 256 x 32 at
 // 2 CTAs/SM (HGM_NTT_E=322: no spills, forward -4%, inverse +2%)
@@ -1398,6 +1574,8 @@ void ntt_forward(const DevCtx& cx, const DevParams& hp, const NttJobs& jobs_in, 
         launch_block<13>(true, cx, jobs, 1, s);
     } else if (hp.logN == 12) {
         launch_block<12>(true, cx, jobs, 1, s);
+    } else if (hp.logN == 15 && ntt_cluster4()) {  // one HBM pass: 4-CTA cluster per limb
+        launch_c4<13>(true, cx, jobs, s);
     } else {  // 2^15: two outer stages, then four 2^13 blocks
         k_ntt_fwd_outer2<<<dim3(16, jobs.count), 512, 0, s>>>(cx, jobs);
         if (use_ntt3())
@@ -1419,6 +1597,8 @@ void ntt_inverse(const DevCtx& cx, const DevParams& hp, const NttJobs& jobs_in, 
         launch_block<13>(false, cx, jobs, 1, s);
     } else if (hp.logN == 12) {
         launch_block<12>(false, cx, jobs, 1, s);
+    } else if (hp.logN == 15 && ntt_cluster4()) {
+        launch_c4<13>(false, cx, jobs, s);
     } else {
         if (use_ntt3())
             launch_block3<13>(false, cx, jobs, 4, s);

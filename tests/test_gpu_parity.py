@@ -27,6 +27,24 @@ def test_ntt_matches_oracle(pid, gpu_factory, oracle_factory):
         assert np.array_equal(i_gpu, data), f"inverse NTT prime {prime}"
 
 
+@pytest.mark.parametrize("pid", [0, 1])
+def test_ntt_many_limbs(pid, gpu_factory, oracle_factory):
+    """A launch of several waves (N = 32768: 4-CTA clusters, DSMEM outer stages):
+    every limb's forward transform equals the oracle's, and inverse o forward
+    is the identity on all of them."""
+    g, o = gpu_factory(pid), oracle_factory(pid)
+    rng = np.random.default_rng(77 + pid)
+    count = 1500 if g.N == 8192 else 600
+    prime = g.L - 1
+    q = g.primes[prime]
+    data = (rng.integers(0, 2**63, count * g.N, dtype=np.uint64) % np.uint64(q)).astype(np.uint64)
+    f_gpu = g.test_ntt(data, prime, True)
+    for k in (0, count // 2, count - 1):
+        sl = slice(k * g.N, (k + 1) * g.N)
+        assert np.array_equal(f_gpu[sl], o.ntt(data[sl], prime, True)), f"limb {k}"
+    assert np.array_equal(g.test_ntt(f_gpu, prime, False), data)
+
+
 @pytest.mark.parametrize("pid", [2, 0])
 def test_encrypt_bit_exact(pid, gpu_factory, oracle_factory):
     g, o = gpu_factory(pid), oracle_factory(pid)

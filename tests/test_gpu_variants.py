@@ -2,7 +2,7 @@
 
 The library picks its NTT layout and kernel fusions once per process from the
 environment (csrc/ntt.cu: HGM_NTT3, HGM_FUSED_KS, HGM_FUSED_CONV,
-HGM_FUSED_FINISH, HGM_FUSED_TENSOR).  Each variant re-runs the primitive
+HGM_FUSED_FINISH, HGM_FUSED_TENSOR, HGM_NTT_CLUSTER).  Each variant re-runs the primitive
 parity tests (every op against the CPU oracle, ciphertext words bit-exact) and
 the HEGMM product tests in a fresh process with that environment."""
 import os
@@ -17,6 +17,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 VARIANTS = {
     "one-cta-ntt": {"HGM_NTT3": "0"},
+    # N = 32768 as two HBM passes (outer 2-stage kernel + 2^13 blocks) instead of 4-CTA clusters
+    "two-pass-n32768-ntt": {"HGM_NTT_CLUSTER": "0"},
     "fused-modup-moddown": {"HGM_FUSED_KS": "1"},
     "fused-modup": {"HGM_FUSED_KS": "u"},
     "unfused-conv-finish": {"HGM_FUSED_CONV": "0", "HGM_FUSED_FINISH": "0"},
