@@ -259,11 +259,12 @@ def ntt_roofline(ctx, limb_bytes, label):
     ntt_ms = ctx.bench_ntt(limbs, 20, True)
     intt_ms = ctx.bench_ntt(limbs, 20, False)
     achieved = limbs * limb_bytes / (ntt_ms / 1e3) / 1e9
-    # key switch: per rotation read dnum (L+K) digit limbs + dnum 2 (L+K) key limbs + L c0 limbs,
-    # write 2 (L+K) accumulator limbs (roofline table)
+    # key switch, compulsory bytes per rotation: read dnum (L+K) digit limbs + L c0 limbs, write
+    # 2 (L+K) accumulator limbs, and the dnum 2 (L+K)-limb Galois key once per group of 8
+    # rotations that share it (the kernel's key reuse; DESIGN.md roofline table)
     R = ctx.L + ctx.K
     ks_items = 2048 if ctx.N == 8192 else 256
-    ks_bytes = (ctx.dnum * R + ctx.dnum * 2 * R + ctx.L + 2 * R) * ctx.N * 8
+    ks_bytes = (ctx.dnum * R + ctx.L + 2 * R + ctx.dnum * 2 * R / 8) * ctx.N * 8
     ks_ms = ctx.bench_keyswitch(ks_items, 10)
     ks_gbs = ks_items * ks_bytes / (ks_ms / 1e3) / 1e9
     traffic = None
@@ -282,9 +283,23 @@ def ntt_roofline(ctx, limb_bytes, label):
             "inverse_frac": round(limbs * limb_bytes / (intt_ms / 1e3) / 1e9 / peak, 4),
             "peak_source": peak_src, "frac_vs_spec_8tbs": round(achieved / 8000.0, 4),
             "keyswitch": {"kernel": "k_ks_inner (key inner product, Galois gather fused, 8 rotations per key read)",
-                          "rotations_per_launch": ks_items, "algorithmic_bytes_per_rotation": ks_bytes,
+                          "rotations_per_launch": ks_items, "algorithmic_bytes_per_rotation": int(ks_bytes),
+                          "traffic": ks_traffic(ctx.N, ks_items),
                           "ms_per_launch": round(ks_ms, 4), "achieved": round(ks_gbs, 1),
                           "frac": round(ks_gbs / peak, 4)}}
+
+
+def ks_traffic(N, items):
+    """DRAM bytes per k_ks_inner launch from the committed ncu --set full capture
+    (profiles/ks_traffic.json), scaled to `items` rotations; None if absent."""
+    prof = os.path.join(ROOT, "profiles", "ks_traffic.json")
+    try:
+        rec = json.load(open(prof))
+        if rec.get("N") == N and rec.get("bytes_per_rotation"):
+            return rec["bytes_per_rotation"] * items
+    except Exception:
+        pass
+    return None
 
 
 def run_cfg4(args):

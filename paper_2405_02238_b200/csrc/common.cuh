@@ -214,23 +214,38 @@ HD u64 shoup_rem(u64 a, u64 w, u64 qh, u64 q) {
 #endif
 template <int V = HGM_SHOUP_V>
 HD u64 shoup_lazy3(u64 a, u64 w, u64 ws, u64 q) { return shoup_rem<V>(a, w, mulhi64_approx(a, ws), q); }
+// x in [0, 2m) -> [0, m)   (m = q or 2q).  On the device the subtraction's
+// borrow selects the result: IADD3 + IADD3.X (carry out) + 2 SEL, where the
+// compare-then-subtract form costs two ISETP, two SEL and the subtraction.
+#ifndef HGM_RED_BORROW
+#define HGM_RED_BORROW 1
+#endif
+HD u64 reduce_once(u64 x, u64 m) {
+#if defined(__CUDA_ARCH__) && HGM_RED_BORROW
+    u32 lo, hi, b;
+    asm("sub.cc.u32 %0, %3, %5;\n\t"
+        "subc.cc.u32 %1, %4, %6;\n\t"
+        "subc.u32 %2, 0, 0;"
+        : "=r"(lo), "=r"(hi), "=r"(b)
+        : "r"((u32)x), "r"((u32)(x >> 32)), "r"((u32)m), "r"((u32)(m >> 32)));
+    return b ? x : ((u64)hi << 32) | lo;
+#else
+    return x >= m ? x - m : x;
+#endif
+}
 // a * w mod q with ws = floor(w 2^64 / q); any a < 2^64, result in [0, q)
 HD u64 shoup_mul(u64 a, u64 w, u64 ws, u64 q) {
     u64 r = shoup_lazy3(a, w, ws, q);  // [0, 3q)
-    r = r >= q ? r - q : r;
-    return r >= q ? r - q : r;
+    r = reduce_once(r, q);
+    return reduce_once(r, q);
 }
-// x in [0, 2m) -> [0, m)   (m = q or 2q)
-HD u64 reduce_once(u64 x, u64 m) { return x >= m ? x - m : x; }
 // a * b mod q for a, b < q < 2^61 (shifted Barrett, two corrections)
 HD u64 mul_mod(u64 a, u64 b, const Prime& p) {
     const u64 lo = a * b, hi = mulhi64(a, b);
     const u64 x = (hi << (66 - p.s)) | (lo >> (p.s - 2));
     const u64 qh = mulhi64_approx(x, p.mu);  // low by at most 3: r < 4q
-    u64 r = lo - mul_lo_q(qh, p.q);
-    if (r >= 2 * p.q) r -= 2 * p.q;
-    if (r >= p.q) r -= p.q;
-    return r;
+    const u64 r = lo - mul_lo_q(qh, p.q);
+    return reduce_once(reduce_once(r, 2 * p.q), p.q);
 }
 // 128-bit lazy accumulator of products of residues, reduced once; valid while
 // the sum stays below 2^(s+62) (4 products of 60-bit residues, 9 of 55-bit).
@@ -252,10 +267,8 @@ struct Acc {
 HD u64 reduce_acc(const Acc& a, const Prime& p) {
     const u64 x = (a.hi << (66 - p.s)) | (a.lo >> (p.s - 2));
     const u64 qh = mulhi64_approx(x, p.mu);
-    u64 r = a.lo - mul_lo_q(qh, p.q);
-    if (r >= 2 * p.q) r -= 2 * p.q;
-    if (r >= p.q) r -= p.q;
-    return r;
+    const u64 r = a.lo - mul_lo_q(qh, p.q);
+    return reduce_once(reduce_once(r, 2 * p.q), p.q);
 }
 // Column accumulator for sums of residue products.  Operands are split into
 // S-bit digits (residues < 2^(2S): S = 30 for 60-bit primes, 28 for 55-bit)

@@ -13,4 +13,4 @@ for f in ntt bfv; do
 done
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o variants/lib_$1.so variants/ntt_$1.o variants/bfv_$1.o \
-    $B/params.cpp.o $B/engine.cpp.o $B/hegmm_algos.cpp.o $B/capi.cpp.o -lcudart
+    $B/params.cpp.o $B/engine.cpp.o $B/hegmm_algos.cpp.o $B/capi.cpp.o $B/comm.cpp.o -lcudart -ldl

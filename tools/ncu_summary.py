@@ -1,6 +1,6 @@
 """Summarise one kernel of an `ncu --set full` report into profiles/ JSON.
 
-usage: python tools/ncu_summary.py REPORT.ncu-rep OUT.json [limbs] [traffic.json]
+usage: python tools/ncu_summary.py REPORT.ncu-rep OUT.json [limbs] [traffic.json] [bytes_per_unit]
 Reads the raw page (ncu -i ... --page raw --csv) of the first captured kernel,
 keeps the metrics DESIGN.md argues from, the PC-sampling stall histogram and,
 given the limb count of the launch, the DRAM bytes per limb (written also to
@@ -32,7 +32,10 @@ def main():
     limbs = int(sys.argv[3]) if len(sys.argv) > 3 else None
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr, units, val = rows[0], rows[1], rows[2]
+    hdr, units = rows[0], rows[1]
+    gi = hdr.index("launch__grid_size")
+    # several launches may be captured: summarise the largest (the benchmarked one)
+    val = max(rows[2:], key=lambda r: int(float(r[gi].replace(",", "") or 0)))
     col = {k: i for i, k in enumerate(hdr)}
     res = {}
     for k in KEYS:
@@ -47,7 +50,7 @@ def main():
         wr = to_bytes(val[col["dram__bytes_write.sum"]], units[col["dram__bytes_write.sum"]])
         res["limbs"] = limbs
         res["dram_bytes_per_limb"] = (rd + wr) / limbs
-        res["algorithmic_bytes_per_limb"] = 2 * 8 * 8192
+        res["algorithmic_bytes_per_limb"] = int(sys.argv[5]) if len(sys.argv) > 5 else 2 * 8 * 8192
     json.dump(res, open(out, "w"), indent=1)
     if limbs and len(sys.argv) > 4:
         name = res["Kernel Name"].split("::")[-1].split("(")[0]
