@@ -17,7 +17,7 @@ fi
 if [ -n "$NCU" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/bench_launches.csv \
       python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1; echo "ncu launches rc $?"
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_ntt_fwd3 -c 40 -o gpurun_out/ntt_full -f \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_ntt_fwd3 -s 4 -c 1 -o gpurun_out/ntt_full -f \
       python tools/ntt_once.py > gpurun_out/ncu_ntt_full.log 2>&1; echo "ncu ntt rc $?"
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_ks_inner -s 1 -c 1 -o gpurun_out/ks_full -f \
       python tools/ntt_once.py > gpurun_out/ncu_ks_full.log 2>&1; echo "ncu ks rc $?"
