@@ -201,6 +201,33 @@ int hgm_blocked_mm(hgm_ctx* ctx, int algo, size_t m, size_t l, size_t n, const s
                    size_t n_col, const int64_t* A, const int64_t* B, int64_t* C, uint64_t counter0,
                    int32_t* log);
 
+/* blocked_mm with ENCRYPTED accumulation (new): every block
+ * product of an output block stays a ciphertext on the GPU; the products of
+ * one output block that share a slot layout (working rows / cols and flatten
+ * order -- all of them unless the enhanced -> basic fallback mixes layouts)
+ * are summed over the mid dimension (mod q, one add launch per depth level),
+ * and each sum is decrypted ONCE -- where the reference decrypts every block
+ * product and adds in cleartext (algorithms.cpp:485-490), so the decrypt
+ * count differs (n_decrypts).  Products, log and encryption counters are those
+ * of hgm_blocked_mm; a sum decrypts to the sum of its products mod t.
+ *   out_first / out_count  output blocks (row-major bi * n_col + bj) this call
+ *                          computes -- a shard for multi-GPU; C entries of other
+ *                          blocks are left untouched; counters stay those of the
+ *                          whole product, so shards are bit-identical to one run
+ *   acc_words / acc_meta   optional host outputs, acc_cap entries: each summed
+ *                          ciphertext ([ct_words]) and its meta (8 int64: output
+ *                          block, algo used, block m, l, n, flatten order, terms,
+ *                          segment); *n_acc = number of sums
+ * flags 0 gives hgm_blocked_mm exactly (out range must then cover all blocks). */
+#define HGM_BLOCKED_ENCRYPTED_ACCUMULATION 1
+/* with it: export the sums only, decrypt nothing (the decrypting rank gathers them) */
+#define HGM_BLOCKED_NO_DECRYPT 2
+int hgm_blocked_mm_ex(hgm_ctx* ctx, int algo, size_t m, size_t l, size_t n, const size_t* row_blocks,
+                      size_t n_row, const size_t* mid_blocks, size_t n_mid, const size_t* col_blocks,
+                      size_t n_col, const int64_t* A, const int64_t* B, int64_t* C, uint64_t counter0, int flags,
+                      size_t out_first, size_t out_count, int32_t* log, uint64_t* acc_words, int64_t* acc_meta,
+                      size_t acc_cap, size_t* n_acc, size_t* n_decrypts);
+
 /* The same pipeline split at the reference's phase boundaries
  * (algorithms.cpp:216-247: Client encrypt / Cloud loop / Client decrypt):
  *   hgm_batch_encrypt  packs and encrypts `count` instances (ciphertexts stay in HBM)
@@ -218,7 +245,7 @@ int hgm_batch_decrypt_words(hgm_ctx* ctx, const uint64_t* dev_words, size_t coun
                             int64_t* out);
 void hgm_batch_free(hgm_batch* b);
 /* Decrypts and unpacks `count` result ciphertexts of a product shape held in
- * device memory (e.g. gathered from other ranks by hgm_comm_gather_batch) into
+ * device (or host) memory (e.g. gathered from other ranks by hgm_comm_gather_batch) into
  * host C[count][m][n]: the client-side decrypt of algorithms.cpp:244-247. */
 int hgm_decrypt_products(hgm_ctx* ctx, int algo, int order, int flags, size_t m, size_t l, size_t n,
                          const uint64_t* dev_words, size_t count, int64_t* C);
@@ -235,8 +262,9 @@ int hgm_decrypt_products(hgm_ctx* ctx, int algo, int order, int flags, size_t m,
  *                                        (atomic rename; other ranks poll, timeout_s)
  *   hgm_comm_barrier                     after every rank's queued work
  *   hgm_comm_max                         host double, max over ranks (timings)
- *   hgm_comm_gather                      variable-size gather of device words to `root`
- *                                        (rank order); recv / recv_cap_words used on root
+ *   hgm_comm_gather                      variable-size gather of words to `root` (rank
+ *                                        order); recv / recv_cap_words used on root; host
+ *                                        buffers are staged through device memory
  *   hgm_comm_gather_batch                every rank's batch results to `root`, in rank
  *                                        order, into a device buffer the library allocates
  *                                        (free with hgm_comm_buffer_free); b may be NULL

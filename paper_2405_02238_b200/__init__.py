@@ -57,7 +57,7 @@ EXPORTS = (
     "hgm_key_has", "hgm_galois_element", "hgm_encrypt_noise", "hgm_reserve_counters", "hgm_program_keys",
     "hgm_decrypt_products", "hgm_comm_unique_id", "hgm_comm_init", "hgm_comm_init_file", "hgm_comm_destroy",
     "hgm_comm_rank", "hgm_comm_size", "hgm_comm_barrier", "hgm_comm_max", "hgm_comm_gather",
-    "hgm_comm_gather_batch", "hgm_comm_buffer_free", "hgm_bench_keyswitch",
+    "hgm_comm_gather_batch", "hgm_comm_buffer_free", "hgm_bench_keyswitch", "hgm_blocked_mm_ex",
 )
 CTX_KEYLESS, CTX_OS_SEED = 1, 2
 COUNTER_AUTO = (1 << 64) - 1
@@ -197,6 +197,17 @@ class Comm:
                                            ctypes.byref(p), ctypes.byref(n)))
         return (p.value, n.value) if p.value else (None, 0)
 
+    def gather_words(self, words: np.ndarray, total_cap: int = 0, root: int = 0) -> Optional[np.ndarray]:
+        """Host uint64 words of every rank to `root` in rank order (staged through
+        device memory by the library); total_cap = receive capacity on the root."""
+        w = np.ascontiguousarray(words, dtype=np.uint64).ravel()
+        recv = np.zeros(max(1, total_cap), dtype=np.uint64) if self.rank == root else None
+        got = ctypes.c_size_t()
+        _check(lib().hgm_comm_gather(self._h, _ptr(w) if w.size else None, w.size,
+                                     _ptr(recv) if recv is not None else None, total_cap if recv is not None else 0,
+                                     root, ctypes.byref(got)))
+        return recv[: got.value] if self.rank == root else None
+
     def free_buffer(self, ptr: Optional[int]) -> None:
         if ptr:
             _check(lib().hgm_comm_buffer_free(self._h, ptr))
@@ -279,6 +290,8 @@ def lib() -> ctypes.CDLL:
         "hgm_matmul_batch": (_int, [_vp, _int, _int, _int, _sz, _sz, _sz, _sz, _vp, _vp, _vp, _u64, _vp]),
         "hgm_matmul_batch_export": (_int, [_vp, _int, _int, _int, _sz, _sz, _sz, _sz, _vp, _vp, _vp, _u64, _vp]),
         "hgm_blocked_mm": (_int, [_vp, _int, _sz, _sz, _sz, _vp, _sz, _vp, _sz, _vp, _sz, _vp, _vp, _vp, _u64, _vp]),
+        "hgm_blocked_mm_ex": (_int, [_vp, _int, _sz, _sz, _sz, _vp, _sz, _vp, _sz, _vp, _sz, _vp, _vp, _vp, _u64,
+                                     _int, _sz, _sz, _vp, _vp, _vp, _sz, _vp, _vp]),
         "hgm_bench_ntt": (_int, [_vp, _int, _sz, _int, _vp]),
         "hgm_device_sync": (_int, [_vp]),
         "hgm_bench_keyswitch": (_int, [_vp, _sz, _int, _vp]),
@@ -569,6 +582,36 @@ class Context:
         _check(lib().hgm_blocked_mm(self._h, algo, m, l, n, _ptr(r), r.size, _ptr(md), md.size, _ptr(c), c.size,
                                     _ptr(A), _ptr(B), _ptr(C), _counter(counter0), _ptr(log)))
         return C, log
+
+    def blocked_mm_acc(self, A: np.ndarray, B: np.ndarray, rows, mids, cols, algo: int = 1,
+                       counter0: Optional[int] = None, out_range=None, export: bool = False):
+        """blocked_mm with encrypted accumulation (hgm_blocked_mm_ex): returns
+        (C, log, n_decrypts[, acc_words, acc_meta]).  out_range = (first, count)
+        of output blocks (row-major) computes a shard; C holds only those blocks.
+        export=True also returns the summed ciphertexts; export="only" returns
+        them without decrypting (HGM_BLOCKED_NO_DECRYPT)."""
+        A = _as_i64(A)
+        B = _as_i64(B)
+        m, l = A.shape
+        n = B.shape[1]
+        r, md, c = (np.ascontiguousarray(x, dtype=np.uint64) for x in (rows, mids, cols))
+        nblk = r.size * c.size
+        first, count = out_range if out_range is not None else (0, nblk)
+        C = np.zeros((m, n), dtype=np.int64)
+        log = np.zeros((r.size * md.size * c.size, 4), dtype=np.int32)
+        cap = max(1, count * md.size) if export else 0
+        flags = 1 | (2 if export == "only" else 0)
+        words = np.zeros((cap, self.ct_words), dtype=np.uint64) if export else None
+        meta = np.zeros((cap, 8), dtype=np.int64) if export else None
+        n_acc = ctypes.c_size_t()
+        n_dec = ctypes.c_size_t()
+        _check(lib().hgm_blocked_mm_ex(self._h, algo, m, l, n, _ptr(r), r.size, _ptr(md), md.size, _ptr(c), c.size,
+                                       _ptr(A), _ptr(B), _ptr(C), _counter(counter0), flags, first, count, _ptr(log),
+                                       _ptr(words) if export else None, _ptr(meta) if export else None, cap,
+                                       ctypes.byref(n_acc), ctypes.byref(n_dec)))
+        if export:
+            return C, log, n_dec.value, words[: n_acc.value], meta[: n_acc.value]
+        return C, log, n_dec.value
 
     def decrypt_products(self, dev_ptr: int, count: int, m: int, l: int, n: int, algo: int = 0, order: int = -1,
                          flags: int = 0) -> np.ndarray:

@@ -854,10 +854,24 @@ extern "C" {
 int hgm_blocked_mm(hgm_ctx* c, int algo, size_t m, size_t l, size_t n, const size_t* rows, size_t n_row,
                    const size_t* mids, size_t n_mid, const size_t* cols, size_t n_col, const int64_t* A,
                    const int64_t* B, int64_t* C, uint64_t counter0, int32_t* log) {
+    return hgm_blocked_mm_ex(c, algo, m, l, n, rows, n_row, mids, n_mid, cols, n_col, A, B, C, counter0, 0, 0,
+                             (size_t)-1, log, nullptr, nullptr, 0, nullptr, nullptr);
+}
+
+int hgm_blocked_mm_ex(hgm_ctx* c, int algo, size_t m, size_t l, size_t n, const size_t* rows, size_t n_row,
+                      const size_t* mids, size_t n_mid, const size_t* cols, size_t n_col, const int64_t* A,
+                      const int64_t* B, int64_t* C, uint64_t counter0, int flags, size_t out_first,
+                      size_t out_count, int32_t* log, uint64_t* acc_words, int64_t* acc_meta, size_t acc_cap,
+                      size_t* n_acc, size_t* n_decrypts) {
     std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
     DeviceScope dev(c);
     return guarded([&] {
         if (algo < 0 || algo > 2) throw hgm::DimensionError("unknown algorithm id");
+        if (flags & ~(HGM_BLOCKED_ENCRYPTED_ACCUMULATION | HGM_BLOCKED_NO_DECRYPT))
+            throw std::invalid_argument("unknown blocked_mm flag");
+        const bool enc_acc = (flags & HGM_BLOCKED_ENCRYPTED_ACCUMULATION) != 0;
+        const bool no_dec = (flags & HGM_BLOCKED_NO_DECRYPT) != 0;
+        if (no_dec && !enc_acc) throw std::invalid_argument("HGM_BLOCKED_NO_DECRYPT needs encrypted accumulation");
         // BlockPlan::validate (algorithms.cpp:412-432)
         auto check = [](const size_t* p, size_t np, size_t total, const char* name) {
             if (np == 0) throw hgm::DimensionError(std::string("empty ") + name + " partition");
@@ -873,8 +887,13 @@ int hgm_blocked_mm(hgm_ctx* c, int algo, size_t m, size_t l, size_t n, const siz
         check(rows, n_row, m, "row");
         check(mids, n_mid, l, "mid");
         check(cols, n_col, n, "col");
+        const size_t n_out = n_row * n_col;
+        if (out_first > n_out) throw std::invalid_argument("output block range starts past the last block");
+        out_count = std::min(out_count, n_out - out_first);
+        if (!enc_acc && (out_first != 0 || out_count != n_out))
+            throw std::invalid_argument("an output block range needs HGM_BLOCKED_ENCRYPTED_ACCUMULATION");
         Context& ctx = *c->ctx;
-        const size_t slots = ctx.slots();
+        const size_t slots = ctx.slots(), W = ctx.ct_words();
         auto offs = [](const size_t* p, size_t np) {
             std::vector<size_t> o(np + 1, 0);
             for (size_t i = 0; i < np; ++i) o[i + 1] = o[i] + p[i];
@@ -887,20 +906,27 @@ int hgm_blocked_mm(hgm_ctx* c, int algo, size_t m, size_t l, size_t n, const siz
             bool fell;
             u64 base;
             std::vector<i64> a, b, cprod;
+            std::shared_ptr<const MatmulProgram> prog;
+            u64* ct = nullptr;  // encrypted accumulation: the product's ciphertext on the device
         };
         std::vector<Blk> blocks;
-        u64 ctr = 0;  // relative counters; the base is resolved once the total is known
+        u64 ctr = 0;  // relative counters over ALL blocks (a shard encrypts exactly as a full run)
         for (size_t bi = 0; bi < n_row; ++bi)
             for (size_t bj = 0; bj < n_col; ++bj)
                 for (size_t bk = 0; bk < n_mid; ++bk) {  // the reference loop order (algorithms.cpp:472-492)
-                    Blk k{bi, bj, bk, rows[bi], mids[bk], cols[bj], algo, false, 0, {}, {}, {}};
+                    Blk k{bi, bj, bk, rows[bi], mids[bk], cols[bj], algo, false, 0, {}, {}, {}, nullptr, nullptr};
                     if (algo == 1 && !hgm::fits(1, k.mm, k.ll, k.nn, slots)) {
                         k.used = 0;  // duplicated working set outgrows the slots (algorithms.cpp:456-466)
                         k.fell = true;
                     }
-                    auto prog = get_matmul_program(k.used, -1, k.mm, k.ll, k.nn, slots, ctx.host().N);
+                    k.prog = get_matmul_program(k.used, -1, k.mm, k.ll, k.nn, slots, ctx.host().N);
                     k.base = ctr;
-                    ctr += (u64)prog->n_enc;
+                    ctr += (u64)k.prog->n_enc;
+                    const size_t ob = bi * n_col + bj;
+                    if (ob < out_first || ob >= out_first + out_count) {
+                        blocks.push_back(std::move(k));  // kept for the log and the counters only
+                        continue;
+                    }
                     k.a.resize(k.mm * k.ll);
                     k.b.resize(k.ll * k.nn);
                     k.cprod.resize(k.mm * k.nn);
@@ -912,34 +938,186 @@ int hgm_blocked_mm(hgm_ctx* c, int algo, size_t m, size_t l, size_t n, const siz
                 }
         const u64 base = resolve_counter0(c, counter0, ctr);
         for (Blk& k : blocks) k.base += base;
+        auto mine = [&](const Blk& k) {
+            const size_t ob = k.bi * n_col + k.bj;
+            return ob >= out_first && ob < out_first + out_count;
+        };
         // one lockstep batch per distinct (algorithm, shape)
         std::map<std::tuple<int, size_t, size_t, size_t>, std::vector<size_t>> groups;
         for (size_t i = 0; i < blocks.size(); ++i)
-            groups[std::make_tuple(blocks[i].used, blocks[i].mm, blocks[i].ll, blocks[i].nn)].push_back(i);
-        for (auto& kv : groups) {
-            const auto& ids = kv.second;
-            const Blk& f = blocks[ids[0]];
-            auto prog = get_matmul_program(f.used, -1, f.mm, f.ll, f.nn, slots, ctx.host().N);
-            run_instances(
-                ctx, *prog, ids.size(), [&](size_t k) { return (const i64*)blocks[ids[k]].a.data(); },
-                [&](size_t k) { return (const i64*)blocks[ids[k]].b.data(); },
-                [&](size_t k) { return blocks[ids[k]].base; }, [&](size_t k) { return blocks[ids[k]].cprod.data(); },
-                nullptr);
+            if (mine(blocks[i]))
+                groups[std::make_tuple(blocks[i].used, blocks[i].mm, blocks[i].ll, blocks[i].nn)].push_back(i);
+        std::vector<u64*> owned;  // device ciphertexts of the encrypted path
+        size_t decrypts = 0;
+        try {
+            for (auto& kv : groups) {
+                const auto& ids = kv.second;
+                const Blk& f = blocks[ids[0]];
+                const MatmulProgram& prog = *f.prog;
+                if (!enc_acc) {
+                    run_instances(
+                        ctx, prog, ids.size(), [&](size_t k) { return (const i64*)blocks[ids[k]].a.data(); },
+                        [&](size_t k) { return (const i64*)blocks[ids[k]].b.data(); },
+                        [&](size_t k) { return blocks[ids[k]].base; },
+                        [&](size_t k) { return blocks[ids[k]].cprod.data(); }, nullptr);
+                    decrypts += ids.size();
+                    continue;
+                }
+                // client encrypt + cloud program; the products stay on the device
+                u64* out = ctx.alloc(ids.size() * W);
+                owned.push_back(out);
+                for (size_t c0 = 0; c0 < ids.size(); c0 += 256) {
+                    const int K = (int)std::min<size_t>(256, ids.size() - c0);
+                    std::vector<std::vector<std::vector<i64>>> packed(K);
+                    parallel_for((size_t)K, [&](size_t k) {
+                        const Blk& b = blocks[ids[c0 + k]];
+                        packed[k] = prog.pack(b.a.data(), b.b.data());
+                    }, 4);
+                    ExecIO io;
+                    io.K = K;
+                    io.input = [](int, int) -> const u64* { return nullptr; };
+                    io.enc_values = [&](int s, int k) { return (const i64*)packed[k][s].data(); };
+                    io.enc_counter = [&](int s, int k) { return blocks[ids[c0 + k]].base + (u64)s; };
+                    std::vector<u64*> res = execute(ctx, prog.sched, io);
+                    HGM_CUDA(cudaMemcpyAsync(out + c0 * W, res[0], (size_t)K * W * 8, cudaMemcpyDeviceToDevice,
+                                             ctx.stream()));
+                    for (u64* r : res) ctx.release(r);
+                    ctx.sync();  // `packed` is host staging
+                }
+                for (size_t k = 0; k < ids.size(); ++k) blocks[ids[k]].ct = out + k * W;
+            }
+            if (n_acc) *n_acc = 0;
+            if (enc_acc) {
+                // per output block and slot layout (working rows, cols, flatten order): sum the
+                // block products' ciphertexts over the mid dimension on the GPU
+                struct Cls {
+                    size_t ob;
+                    size_t rep;                 // index of the class's first block product
+                    std::vector<size_t> terms;  // its block products, mid-dimension order
+                };
+                std::vector<Cls> classes;
+                std::map<std::tuple<size_t, size_t, size_t, int>, size_t> cidx;
+                for (size_t bidx = 0; bidx < blocks.size(); ++bidx) {
+                    const Blk& k = blocks[bidx];
+                    if (!mine(k)) continue;
+                    const MatmulProgram& p = *k.prog;
+                    const size_t rw = p.algo == Algo::Enhanced ? p.strat.rows_w : p.m;
+                    const size_t cw = p.algo == Algo::Enhanced ? p.strat.cols_w : p.n;
+                    const auto key = std::make_tuple(k.bi * n_col + k.bj, rw, cw, (int)p.order);
+                    auto it = cidx.find(key);
+                    if (it == cidx.end()) {
+                        it = cidx.emplace(key, classes.size()).first;
+                        classes.push_back(Cls{k.bi * n_col + k.bj, bidx, {}});
+                    }
+                    classes[it->second].terms.push_back(bidx);
+                }
+                u64* acc = ctx.alloc(std::max<size_t>(1, classes.size()) * W);
+                owned.push_back(acc);
+                size_t depth = 0;
+                for (const Cls& cl : classes) depth = std::max(depth, cl.terms.size());
+                std::vector<const u64*> sa, sb;
+                std::vector<u64*> so;
+                for (size_t i = 0; i < classes.size(); ++i) {  // acc = term 0 + term 1
+                    const auto& t = classes[i].terms;
+                    if (t.size() == 1) {
+                        HGM_CUDA(cudaMemcpyAsync(acc + i * W, blocks[t[0]].ct, W * 8, cudaMemcpyDeviceToDevice,
+                                                 ctx.stream()));
+                    } else {
+                        sa.push_back(blocks[t[0]].ct);
+                        sb.push_back(blocks[t[1]].ct);
+                        so.push_back(acc + i * W);
+                    }
+                }
+                ctx.add((int)so.size(), sa.data(), sb.data(), so.data());
+                for (size_t d = 2; d < depth; ++d) {  // acc += term d, one launch per depth level
+                    sa.clear();
+                    sb.clear();
+                    so.clear();
+                    for (size_t i = 0; i < classes.size(); ++i)
+                        if (classes[i].terms.size() > d) {
+                            sa.push_back(acc + i * W);
+                            sb.push_back(blocks[classes[i].terms[d]].ct);
+                            so.push_back(acc + i * W);
+                        }
+                    ctx.add((int)so.size(), sa.data(), sb.data(), so.data());
+                }
+                // one decrypt per accumulated class (the reference: one per block product)
+                std::vector<const u64*> cts(classes.size());
+                std::vector<size_t> S(classes.size());
+                std::vector<std::vector<i64>> slotv(classes.size());
+                std::vector<i64*> outp(classes.size());
+                for (size_t i = 0; i < classes.size(); ++i) {
+                    cts[i] = acc + i * W;
+                    S[i] = blocks[classes[i].rep].prog->segment;
+                    slotv[i].resize(S[i]);
+                    outp[i] = slotv[i].data();
+                }
+                if (!classes.empty() && !no_dec) ctx.decrypt((int)classes.size(), cts.data(), S.data(), outp.data());
+                decrypts = no_dec ? 0 : classes.size();
+                // the class's decrypted sum lands in its first product's slot of C; the
+                // other products of the class contribute nothing more
+                for (const Cls& cl : classes) {
+                    if (no_dec) {
+                        for (size_t t : cl.terms) std::fill(blocks[t].cprod.begin(), blocks[t].cprod.end(), 0);
+                        continue;
+                    }
+                    Blk& r = blocks[cl.rep];
+                    r.prog->unpack(slotv[&cl - classes.data()], r.cprod.data());
+                    for (size_t t : cl.terms)
+                        if (t != cl.rep) std::fill(blocks[t].cprod.begin(), blocks[t].cprod.end(), 0);
+                }
+                if (acc_words || acc_meta || n_acc) {
+                    if (classes.size() > acc_cap && (acc_words || acc_meta))
+                        throw std::invalid_argument("accumulated ciphertexts (" + std::to_string(classes.size()) +
+                                                    ") exceed acc_cap");
+                    for (size_t i = 0; i < classes.size() && (acc_words || acc_meta); ++i) {
+                        const Blk& r = blocks[classes[i].rep];
+                        if (acc_words)
+                            HGM_CUDA(cudaMemcpyAsync(acc_words + i * W, acc + i * W, W * 8, cudaMemcpyDeviceToHost,
+                                                     ctx.stream()));
+                        if (acc_meta) {
+                            int64_t* mt = acc_meta + 8 * i;
+                            mt[0] = (int64_t)classes[i].ob;
+                            mt[1] = r.used;
+                            mt[2] = (int64_t)r.mm;
+                            mt[3] = (int64_t)r.ll;
+                            mt[4] = (int64_t)r.nn;
+                            mt[5] = (int64_t)r.prog->order;
+                            mt[6] = (int64_t)classes[i].terms.size();
+                            mt[7] = (int64_t)r.prog->segment;
+                        }
+                    }
+                    if (n_acc) *n_acc = classes.size();
+                    ctx.sync();
+                }
+            }
+        } catch (...) {
+            ctx.sync();
+            for (u64* p : owned) ctx.release(p);
+            throw;
         }
-        std::fill(C, C + m * n, 0);
+        for (u64* p : owned) ctx.release(p);
+        ctx.sync();
+        if (n_decrypts) *n_decrypts = decrypts;
+        for (size_t ob = out_first; ob < out_first + out_count; ++ob) {  // the blocks this call computes
+            const size_t bi = ob / n_col, bj = ob % n_col;
+            for (size_t r = 0; r < rows[bi]; ++r)
+                std::fill(C + (ro[bi] + r) * n + co[bj], C + (ro[bi] + r) * n + co[bj] + cols[bj], 0);
+        }
         for (size_t i = 0; i < blocks.size(); ++i) {
             const Blk& k = blocks[i];
-            for (size_t r = 0; r < k.mm; ++r)
-                for (size_t q = 0; q < k.nn; ++q) {
-                    i64& dst = C[(ro[k.bi] + r) * n + co[k.bj] + q];
-                    dst = (dst + k.cprod[r * k.nn + q]) % (i64)kT;
-                }
             if (log) {
                 log[4 * i] = k.used;
                 log[4 * i + 1] = k.fell ? 1 : 0;
                 log[4 * i + 2] = (int32_t)k.mm;
                 log[4 * i + 3] = (int32_t)k.ll;
             }
+            if (!mine(k)) continue;
+            for (size_t r = 0; r < k.mm; ++r)
+                for (size_t q = 0; q < k.nn; ++q) {
+                    i64& dst = C[(ro[k.bi] + r) * n + co[k.bj] + q];
+                    dst = (dst + k.cprod[r * k.nn + q]) % (i64)kT;
+                }
         }
     });
 }
@@ -974,6 +1152,14 @@ const u64* batch_results(const hgm_batch* b, size_t* count) {
     return b ? b->out : nullptr;
 }
 int set_error(int code, const std::string& msg) { return fail(code, msg); }
+bool is_device_pointer(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();  // unregistered host memory on older runtimes
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
 
 }  // namespace hgm
 
@@ -1103,7 +1289,20 @@ int hgm_decrypt_products(hgm_ctx* c, int algo, int order, int flags, size_t m, s
         if (order < -1 || order > 1) throw std::invalid_argument("order must be -1, 0 or 1");
         auto prog = get_matmul_program(algo, order, m, l, n, c->ctx->slots(), c->ctx->host().N, flags);
         std::vector<i64> slots(count * prog->segment);
-        const int rc = hgm_batch_decrypt_words(c, dev_words, count, prog->segment, slots.data());
+        // host words (e.g. a host gather) are staged through the device
+        const u64* words = dev_words;
+        u64* staged = nullptr;
+        if (count && !is_device_pointer(dev_words)) {
+            staged = c->ctx->alloc(count * c->ctx->ct_words());
+            HGM_CUDA(cudaMemcpyAsync(staged, dev_words, count * c->ctx->ct_words() * 8, cudaMemcpyHostToDevice,
+                                     c->ctx->stream()));
+            words = staged;
+        }
+        const int rc = hgm_batch_decrypt_words(c, words, count, prog->segment, slots.data());
+        if (staged) {
+            c->ctx->release(staged);
+            c->ctx->sync();
+        }
         if (rc != HGM_OK) throw std::runtime_error(g_err);
         parallel_for(count, [&](size_t k) {
             std::vector<i64> v(slots.begin() + k * prog->segment, slots.begin() + (k + 1) * prog->segment);

@@ -18,6 +18,8 @@ hgm_ctx* batch_session(hgm_batch* b);
 const u64* batch_results(const hgm_batch* b, size_t* count);
 // records the thread-local message behind hgm_last_error and returns `code`
 int set_error(int code, const std::string& msg);
+// device (or managed) memory, as opposed to host memory that must be staged
+bool is_device_pointer(const void* p);
 
 // Makes a device current for a scope and restores the caller's afterwards.
 struct DeviceGuard {

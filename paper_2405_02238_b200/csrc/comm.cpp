@@ -295,6 +295,34 @@ int hgm_comm_gather(hgm_comm* cm, const uint64_t* send, size_t send_words, uint6
         if (root < 0 || root >= cm->world) throw std::invalid_argument("bad root rank");
         if (send_words && !send) throw std::invalid_argument("null send buffer");
         Context& ctx = session_context(cm->owner);
+        // host buffers are staged through device memory (NCCL moves device memory only)
+        u64* st_send = nullptr;
+        u64* st_recv = nullptr;
+        uint64_t* host_recv = nullptr;
+        struct Staging {
+            Context& ctx;
+            u64*& a;
+            u64*& b;
+            ~Staging() {
+                try {
+                    ctx.sync();
+                    if (a) ctx.release(a);
+                    if (b) ctx.release(b);
+                    ctx.sync();
+                } catch (...) {
+                }
+            }
+        } staging{ctx, st_send, st_recv};
+        if (send_words && !is_device_pointer(send)) {
+            st_send = ctx.alloc(send_words);
+            HGM_CUDA(cudaMemcpyAsync(st_send, send, send_words * 8, cudaMemcpyHostToDevice, ctx.stream()));
+            send = st_send;
+        }
+        if (cm->rank == root && recv && recv_cap_words && !is_device_pointer(recv)) {
+            st_recv = ctx.alloc(recv_cap_words);
+            host_recv = recv;
+            recv = st_recv;
+        }
         const std::vector<u64> cnt = allgather_u64(cm, send_words);  // also orders after the producing work
         size_t total = 0;
         for (u64 x : cnt) total += x;
@@ -321,6 +349,8 @@ int hgm_comm_gather(hgm_comm* cm, const uint64_t* send, size_t send_words, uint6
         } else if (send_words) {
             HGM_NCCL(nccl().Send(send, send_words, ncclUint64, root, cm->nc, ctx.stream()));
         }
+        if (host_recv && total)
+            HGM_CUDA(cudaMemcpyAsync(host_recv, recv, total * 8, cudaMemcpyDeviceToHost, ctx.stream()));
         HGM_CUDA(cudaStreamSynchronize(ctx.stream()));
         if (recv_words) *recv_words = cm->rank == root ? total : 0;
     });

@@ -110,3 +110,38 @@ def sharded_matmul(ctx, A, B, parts: int, algo: int = 1, comm=None, counter0: in
     finally:
         if bt is not None:
             bt.free()
+
+
+def blocked_mm_sharded(ctx, A, B, rows, mids, cols, algo: int = 1, comm=None, counter0: int = 0):
+    """blocked_mm (algorithms.cpp:434-498) with encrypted accumulation, output
+    blocks sharded over the ranks: rank r sums its output
+    blocks' products over the mid dimension as ciphertexts on its GPU
+    (hgm_blocked_mm_ex, no decryption), the sums travel to rank 0 over the
+    library's NCCL communicator, and rank 0 decrypts each sum once.  Counters
+    are those of a single-GPU run, so every sum is bit-identical to it.
+    Returns (C mod t, number of decrypts) on rank 0 and (None, 0) elsewhere."""
+    import numpy as np
+
+    rank, world = (comm.rank, comm.world) if comm is not None else (0, 1)
+    n_out = len(rows) * len(cols)
+    first, count = shard(rank, world, n_out)
+    _, _, _, words, meta = ctx.blocked_mm_acc(A, B, rows, mids, cols, algo=algo, counter0=counter0,
+                                              out_range=(first, count), export="only")
+    if comm is not None:
+        cap_entries = n_out * len(mids)
+        all_words = comm.gather_words(words, cap_entries * ctx.ct_words)
+        all_meta = comm.gather_words(meta.view(np.uint64), cap_entries * 8)
+        if rank != 0:
+            return None, 0
+        words = all_words.reshape(-1, ctx.ct_words)
+        meta = all_meta.view(np.int64).reshape(-1, 8)
+    m, n = A.shape[0], B.shape[1]
+    ro = np.concatenate([[0], np.cumsum(rows)])
+    co = np.concatenate([[0], np.cumsum(cols)])
+    C = np.zeros((m, n), dtype=np.int64)
+    for k in range(meta.shape[0]):
+        ob, used, bm, bl, bn, order = (int(x) for x in meta[k][:6])
+        blk = ctx.decrypt_products(words[k].ctypes.data, 1, bm, bl, bn, algo=used, order=order)[0]
+        bi, bj = divmod(ob, len(cols))
+        C[ro[bi]:ro[bi] + bm, co[bj]:co[bj] + bn] = (C[ro[bi]:ro[bi] + bm, co[bj]:co[bj] + bn] + blk) % 65537
+    return C, int(meta.shape[0])
