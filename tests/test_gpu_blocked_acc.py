@@ -125,15 +125,17 @@ def test_plain_blocked_mm_unchanged_and_flags_checked(gpu_factory):
     C, log = g.blocked_mm(A, B, [3], [2, 2], [2], algo=0)
     assert np.array_equal(C, (A @ B) % T)
     A64, B64 = (np.ascontiguousarray(x, dtype=np.int64) for x in (A, B))
-    r, md, c = (np.array(x, dtype=np.uint64) for x in ([3], [2, 2], [2]))
+    r, md, c = (np.array(x, dtype=np.uint64) for x in ([3], [2, 2], [1, 1]))
     Cout = np.zeros((3, 2), dtype=np.int64)
     P = hb._ptr
 
     def call(flags, first, count):
-        return hb.lib().hgm_blocked_mm_ex(g._h, 0, 3, 4, 2, P(r), 1, P(md), 2, P(c), 1, P(A64), P(B64), P(Cout),
+        return hb.lib().hgm_blocked_mm_ex(g._h, 0, 3, 4, 2, P(r), 1, P(md), 2, P(c), 2, P(A64), P(B64), P(Cout),
                                           0, flags, first, count, None, None, None, 0, None, None)
 
     assert call(0, 0, 1) == hb.HGM_EARG  # an output block range needs encrypted accumulation
     assert call(2, 0, 1) == hb.HGM_EARG  # export-only needs encrypted accumulation
     assert call(8, 0, 1) == hb.HGM_EARG  # unknown flag
-    assert call(1, 0, 1) == hb.HGM_OK and np.array_equal(Cout, (A @ B) % T)
+    assert call(1, 0, 1) == hb.HGM_OK and np.array_equal(Cout[:, :1], ((A @ B) % T)[:, :1])
+    assert not Cout[:, 1:].any()  # the other output block is left untouched
+    assert call(1, 0, 2) == hb.HGM_OK and np.array_equal(Cout, (A @ B) % T)
