@@ -107,7 +107,8 @@ u64 prng(u64 seed, u64 stream, u64 idx) {
     return mix64(h + (idx + 1) * 0x9e3779b97f4a7c15ULL);
 }
 // |x| CDT for the discrete Gaussian sigma = 3.2, tail cut 19 (SEAL's 6 sigma):
-// T[k] = floor(2^63 * P(|X| <= k)); computed once by oracle/gen_cdt.py.
+// T[k] = floor(2^63 * P(|X| <= k)); committed from a double-precision derivation; oracle/gen_cdt.py recomputes it
+// exactly (60-digit decimal) and checks every entry to within 2^-50 (tests/test_oracle.py).
 const u64 kCdt[20] = {
     0x0ff52b40a5917e80ULL, 0x2e5a25d4bf0e3e00ULL, 0x489ae26955b04800ULL, 0x5d2bc20f621bf000ULL,
     0x6bc8694c3cc81000ULL, 0x7532d89ac6ba8000ULL, 0x7ab396cb74436c00ULL, 0x7d9e4e916643f000ULL,

@@ -1,3 +1,8 @@
+# SPDX-License-Identifier: Apache-2.0
+# Attribution: the case draws and the Table-1 cost model restate the reference
+# implementation of arXiv 2405.02238 (Apache-2.0; /root/reference/proj/src/
+# costmodel.cpp:20-30, :83-106, :154-184), so that draws are bit-identical to
+# run_campaign's (pinned by tests/test_campaign.py).
 """Real-HE campaign.
 
 The reference's campaign (``run_campaign``, /root/reference/proj/src/costmodel.cpp:266-314)

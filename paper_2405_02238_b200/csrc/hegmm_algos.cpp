@@ -1,6 +1,14 @@
+// SPDX-License-Identifier: Apache-2.0
 // hegmm_algos.cpp -- HEGMM (Algorithm 1) and HEGMM-Enhanced (Algorithm 2) as
 // recorded HE programs.  Each function names the reference routine whose op
 // stream it reproduces.
+//
+// Attribution: the strategy selection, diagonal plans and op order restate the
+// reference implementation of arXiv 2405.02238 (Apache-2.0;
+// /root/reference/proj/src/algorithms.cpp:74-170, :198-388 and
+// proj/src/lintrans.cpp:16-21, :139-159, :244-302, :433-461), because the
+// recorded op stream must equal the reference's op for op (pinned against a
+// live reference trace by tests/test_op_stream.py).
 #include "hegmm_algos.hpp"
 
 #include <algorithm>

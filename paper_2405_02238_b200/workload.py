@@ -1,3 +1,6 @@
+# SPDX-License-Identifier: Apache-2.0
+# Attribution: the splitmix64 draws restate the reference implementation of
+# arXiv 2405.02238 (Apache-2.0; /root/reference/proj/src/costmodel.cpp:20-26, :158-184).
 """Seeded synthetic HEGMM workloads (BASELINE.json configs).
 
 Entries are drawn exactly as the reference's seeded campaign draws them

@@ -16,6 +16,7 @@ import pytest
 from paper_2405_02238_b200.workload import CONFIGS, splitmix_matrices
 
 T = 65537
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_golden.json")))
 
 
@@ -212,3 +213,20 @@ def test_oracle_key_import_export_round_trip():
     b.import_key(2, a.export_key(2, 0), 0)
     assert np.array_equal(a.rot(ca, 1), b.rot(cb, 1))
     assert np.array_equal(a.mult(ca, ca), b.mult(cb, cb))
+
+
+def test_gaussian_cdt_matches_exact_derivation():
+    """oracle/gen_cdt.py: the committed CDT (sigma 3.2, tail 19) agrees with a
+    60-digit recomputation to within 2^-50, and the device copy is identical."""
+    import re
+    import subprocess
+    import sys
+
+    r = subprocess.run([sys.executable, "oracle/gen_cdt.py", "--check"], cwd=ROOT, capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    src = open(os.path.join(ROOT, "paper_2405_02238_b200", "csrc", "params.cpp")).read()
+    dev = [int(h, 16) for h in re.findall(r"0x([0-9a-f]{16})ULL", src)]
+    orc = open(os.path.join(ROOT, "oracle", "bfv_oracle.cpp")).read()
+    body = re.search(r"kCdt\[20\]\s*=\s*\{(.*?)\};", orc, re.S).group(1)
+    host = [int(h, 16) for h in re.findall(r"0x([0-9a-fA-F]+)ULL", body)]
+    assert host and all(v in dev for v in host)
