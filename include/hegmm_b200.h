@@ -288,7 +288,9 @@ int hgm_comm_buffer_free(hgm_comm* comm, uint64_t* p);
  * facts[0]=segment [1]=encryptions [2]=rotations after CSE [3]=masked sums
  * [4]=CC-mults [5]=levels [6]=flatten order used [7]=ModDowns (values with a
  * pending key switch read) [8]=scale-and-round + relinearisations (values with
- * a pending product read); facts holds 9 entries. */
+ * a pending product read) [9]=rows [10]=cols of the product's slot layout
+ * (entry (r, c) at r + c rows column-major / r cols + c row-major, by [6]);
+ * facts holds 11 entries. */
 int hgm_program_info(int algo, int order, int flags, size_t m, size_t l, size_t n, size_t slots,
                      uint32_t N, uint64_t* stats, uint64_t* facts);
 /* Switching keys a product shape needs (no GPU): sorted Galois elements, 0

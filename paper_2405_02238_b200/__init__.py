@@ -80,10 +80,10 @@ def program_info(algo: int, m: int, l: int, n: int, slots: int = 4096, N: int = 
                  flags: int = 0):
     """Op counts (stats[12]) and facts of a compiled HEGMM program (CPU only)."""
     st = np.zeros(12, dtype=np.uint64)
-    facts = np.zeros(9, dtype=np.uint64)
+    facts = np.zeros(11, dtype=np.uint64)
     _check(lib().hgm_program_info(algo, order, flags, m, l, n, slots, N, _ptr(st), _ptr(facts)))
     keys = ("segment", "encryptions", "rotations", "masked_sums", "cc_mults", "levels", "order", "moddowns",
-            "rescales")
+            "rescales", "layout_rows", "layout_cols")
     return st, dict(zip(keys, (int(x) for x in facts)))
 
 

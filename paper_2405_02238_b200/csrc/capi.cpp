@@ -1361,6 +1361,9 @@ int hgm_program_info(int algo, int order, int flags, size_t m, size_t l, size_t 
             facts[6] = (u64)p->order;
             facts[7] = p->cloud_sched.moddown_count;
             facts[8] = p->cloud_sched.rescale_count;
+            // slot layout of the decrypted product: working rows, cols (flat_index with facts[6])
+            facts[9] = p->algo == Algo::Enhanced ? p->strat.rows_w : p->m;
+            facts[10] = p->algo == Algo::Enhanced ? p->strat.cols_w : p->n;
         }
     });
 }

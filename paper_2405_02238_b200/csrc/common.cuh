@@ -115,11 +115,6 @@ HD u64 mulhi64(u64 a, u64 b) {
 inline u64 mulhi64(u64 a, u64 b) { return (u64)(((unsigned __int128)a * b) >> 64); }
 #endif
 
-HD u64 add_mod(u64 a, u64 b, u64 q) {
-    u64 s = a + b;
-    return s >= q ? s - q : s;
-}
-HD u64 sub_mod(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }
 HD u64 neg_mod(u64 a, u64 q) { return a ? q - a : 0; }
 // Every ciphertext prime (Q, P and B) has the form q = c 2^32 + 1 (params.cpp),
 // so the low 64 bits of x q are x + (x_lo c) 2^32: one 32-bit IMAD instead of
@@ -233,6 +228,9 @@ HD u64 reduce_once(u64 x, u64 m) {
     return x >= m ? x - m : x;
 #endif
 }
+// a + b, a - b mod q for a, b < q (q < 2^63), through the borrow-select reduction
+HD u64 add_mod(u64 a, u64 b, u64 q) { return reduce_once(a + b, q); }
+HD u64 sub_mod(u64 a, u64 b, u64 q) { return reduce_once(a + q - b, q); }
 // a * w mod q with ws = floor(w 2^64 / q); any a < 2^64, result in [0, q)
 HD u64 shoup_mul(u64 a, u64 w, u64 ws, u64 q) {
     u64 r = shoup_lazy3(a, w, ws, q);  // [0, 3q)

@@ -66,19 +66,25 @@ def test_summed_ciphertexts_match_oracle(algo, gpu_factory, oracle_factory, ref)
     ro, mo, co = (np.concatenate([[0], np.cumsum(x)]) for x in (rows, mids, cols))
     names = {0: "basic", 1: "enhanced"}
     seen = 0
+    def layout(used, bm, bl, bn):
+        f = hb.program_info(used, bm, bl, bn, g.slot_count, g.N)[1]
+        return used, f["layout_rows"], f["layout_cols"], f["order"]
+
     for k in range(meta.shape[0]):
         ob, used, bm, bl, bn, order, terms, seg = (int(x) for x in meta[k])
         bi, bj = divmod(ob, len(cols))
-        want = None
+        want, members = None, 0
         for bk in range(len(mids)):
             base, u = ctrs[(bi, bj, bk)]
-            if u != used:
-                continue
+            if layout(u, bm, mids[bk], bn) != layout(used, bm, bl, bn):
+                continue  # another slot layout: another sum
+            members += 1
             Ab = A[ro[bi]:ro[bi + 1], mo[bk]:mo[bk + 1]]
             Bb = B[mo[bk]:mo[bk + 1], co[bj]:co[bj + 1]]
             _, _, ct, _ = ref.mm_oracle(Ab, Bb, param_id=2, seed=1, counter0=base, algo=names[u], words=o.words)
             want = ct if want is None else o.add(want, ct)
             seen += 1
+        assert members == terms
         assert np.array_equal(words[k], want), f"summed ciphertext of output block {ob} differs from the oracle"
     assert seen == len(rows) * len(cols) * len(mids)
     assert ndec == meta.shape[0] <= len(rows) * len(cols) * len(mids)
