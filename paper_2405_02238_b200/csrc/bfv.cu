@@ -291,6 +291,54 @@ __global__ void __launch_bounds__(kThreads, HGM_LC_MINB) k_lincomb(DevCtx cx, u3
     }
 }
 
+// The same sum when every term carries a mask (the masked sums of rotations of
+// an apply_plan / eps / omega plan): terms are taken three at a time -- the
+// most masked products the 128-bit column sum holds with the running residue
+// (3 q^2 + q < 2^(s+62)) -- with all their loads issued first, the chunk's
+// columns start from its first product (no zeroed accumulators to carry
+// through the loop) and each chunk folds the previous chunk's residue in.
+template <typename SH, u32 RL = SH::L>
+__global__ void __launch_bounds__(kThreads, HGM_LC_MINB) k_lincomb_masked(DevCtx cx, u32 n, const u32* off,
+                          const u64* const* in, const u64* const* mask, u64* const* out) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
+    const u32 N = dp->N, logN = dp->logN, L = RL;
+    const size_t LN = (size_t)L * N, W2 = LN;  // word pairs per output
+    ITEM_LOOP {
+        const u32 t0 = off[item], t1 = off[item + 1];
+        ulonglong2* o = reinterpret_cast<ulonglong2*>(out[item]);
+        for (size_t w2 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; w2 < W2; w2 += (size_t)gridDim.x * blockDim.x) {
+            const size_t wl2 = w2 < LN / 2 ? w2 : w2 - LN / 2;  // pair index within the component
+            const Prime& P = dp->pr[(wl2 * 2) >> logN];
+            u64 r0 = 0, r1 = 0;
+            for (u32 t = t0; t < t1; t += 3) {
+                const u32 nt = t1 - t < 3 ? t1 - t : 3;
+                ulonglong2 v[3], m[3];
+#pragma unroll
+                for (u32 u = 0; u < 3; ++u)
+                    if (u < nt) {
+                        v[u] = reinterpret_cast<const ulonglong2*>(in[t + u])[w2];
+                        m[u] = __ldg(reinterpret_cast<const ulonglong2*>(mask[t + u]) + wl2);
+                    }
+                Cols a0, a1;
+                a0.x = r0;
+                a1.x = r1;
+#pragma unroll
+                for (u32 u = 0; u < 3; ++u)
+                    if (u < nt) {
+                        a0.mac(split<SH::S>(v[u].x), packed_dig<SH::S>(m[u].x));
+                        a1.mac(split<SH::S>(v[u].y), packed_dig<SH::S>(m[u].y));
+                    }
+                r0 = reduce_acc(a0.fold<SH::S>(), P);
+                r1 = reduce_acc(a1.fold<SH::S>(), P);
+            }
+            ulonglong2 r;
+            r.x = r0;
+            r.y = r1;
+            o[w2] = r;
+        }
+    }
+}
+
 // canonical residues -> packed digit form (l | h << 32) for k_lincomb (masks) and
 // k_ks_inner (keys); launch on a 1-D grid (every word converted exactly once)
 template <typename SH>
@@ -1409,6 +1457,20 @@ void Context::copy(int n, const u64* const* in, u64* const* out) {
     HGM_CUDA(cudaGetLastError());
 }
 
+namespace {
+// every term of every output has a mask (k_lincomb_masked applies); HGM_LC_MASKED=0 disables
+bool all_masked(const std::vector<const u64*>& masks) {
+    static const bool on = [] {
+        const char* e = std::getenv("HGM_LC_MASKED");
+        return !(e && e[0] == '0');
+    }();
+    if (!on || masks.empty()) return false;
+    for (const u64* m : masks)
+        if (!m) return false;
+    return true;
+}
+}  // namespace
+
 void Context::lincomb(int n_out, const u32* off, const u64* const* in, const u64* const* mask,
                       u64* const* out) {
     if (n_out <= 0) return;
@@ -1425,6 +1487,15 @@ void Context::lincomb(int n_out, const u32* off, const u64* const* in, const u64
     std::vector<u32> voff(off, off + n_out + 1);
     std::vector<const u64*> vin(in, in + nt), vm(mask, mask + nt);
     std::vector<u64*> vo(out, out + n_out);
+    if (all_masked(vm)) {
+        if (hp_.L == 3)
+            k_lincomb_masked<ShapeQ3><<<grid_of(hp_.N, n_out, 1), kThreads, 0, stream_>>>(cx_, n_out, upload(voff), upload(vin), upload(vm), upload(vo));
+        else
+            k_lincomb_masked<ShapeQ8><<<grid_of(hp_.N, n_out, 1), kThreads, 0, stream_>>>(cx_, n_out, upload(voff), upload(vin), upload(vm), upload(vo));
+        ++launches_;
+        HGM_CUDA(cudaGetLastError());
+        return;
+    }
     if (hp_.L == 3) k_lincomb<ShapeQ3><<<grid_of(hp_.N, n_out, 1), kThreads, 0, stream_>>>(cx_, n_out, upload(voff), upload(vin),
                                                                   upload(vm), upload(vo)); else k_lincomb<ShapeQ8><<<grid_of(hp_.N, n_out, 1), kThreads, 0, stream_>>>(cx_, n_out, upload(voff), upload(vin),
                                                                   upload(vm), upload(vo)); ++launches_;
@@ -1792,7 +1863,12 @@ void Context::lincomb_qp(int n_out, const u32* off, const u64* const* in, const 
         for (int i = 0; i <= cn; ++i) sub[i] = off[c0 + i] - off[c0];
         std::vector<const u64*> vin(in + off[c0], in + off[c0 + cn]), vm(mask + off[c0], mask + off[c0 + cn]);
         std::vector<u64*> vo(out + c0, out + c0 + cn);
-        if (hp_.L == 3)
+        if (all_masked(vm)) {
+            if (hp_.L == 3)
+                k_lincomb_masked<ShapeQ3, ShapeQ3::R><<<grid_of(hp_.N, cn, 1), kThreads, 0, stream_>>>(cx_, cn, upload(sub), upload(vin), upload(vm), upload(vo));
+            else
+                k_lincomb_masked<ShapeQ8, ShapeQ8::R><<<grid_of(hp_.N, cn, 1), kThreads, 0, stream_>>>(cx_, cn, upload(sub), upload(vin), upload(vm), upload(vo));
+        } else if (hp_.L == 3)
             k_lincomb<ShapeQ3, ShapeQ3::R><<<grid_of(hp_.N, cn, 1), kThreads, 0, stream_>>>(cx_, cn, upload(sub), upload(vin), upload(vm), upload(vo));
         else
             k_lincomb<ShapeQ8, ShapeQ8::R><<<grid_of(hp_.N, cn, 1), kThreads, 0, stream_>>>(cx_, cn, upload(sub), upload(vin), upload(vm), upload(vo));

@@ -215,6 +215,12 @@ HD u64 shoup_lazy3(u64 a, u64 w, u64 ws, u64 q) { return shoup_rem<V>(a, w, mulh
 #ifndef HGM_RED_BORROW
 #define HGM_RED_BORROW 1
 #endif
+#ifndef HGM_ADD128_PTX
+#define HGM_ADD128_PTX 1
+#endif
+#ifndef HGM_MAC_PTX
+#define HGM_MAC_PTX 1
+#endif
 HD u64 reduce_once(u64 x, u64 m) {
 #if defined(__CUDA_ARCH__) && HGM_RED_BORROW
     u32 lo, hi, b;
@@ -247,17 +253,21 @@ HD u64 mul_mod(u64 a, u64 b, const Prime& p) {
 }
 // 128-bit lazy accumulator of products of residues, reduced once; valid while
 // the sum stays below 2^(s+62) (4 products of 60-bit residues, 9 of 55-bit).
+// (hi:lo) += (bh:bl): on the device one carry chain (add.cc / addc: IADD3 +
+// IADD3.X with carry-out), where the C form derives the carry by a 64-bit
+// compare and a select.
+HD void add128(u64& lo, u64& hi, u64 bl, u64 bh) {
+#if defined(__CUDA_ARCH__) && HGM_ADD128_PTX
+    asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(bl), "l"(bh));
+#else
+    lo += bl;
+    hi += bh + (lo < bl);
+#endif
+}
 struct Acc {
     u64 lo = 0, hi = 0;
-    HD void add(u64 v) {
-        lo += v;
-        hi += (lo < v);
-    }
-    HD void mac(u64 a, u64 b) {
-        const u64 pl = a * b, ph = mulhi64(a, b);
-        lo += pl;
-        hi += ph + (lo < pl);
-    }
+    HD void add(u64 v) { add128(lo, hi, v, 0); }
+    HD void mac(u64 a, u64 b) { add128(lo, hi, a * b, mulhi64(a, b)); }
 };
 // Shifted Barrett on x < 2^(s+62) (s = bit length of q <= 60): x >> (s-2)
 // fits 64 bits; the quotient estimate is low by at most 2 (+1 for the
@@ -296,28 +306,34 @@ struct Cols {
     u64 c0 = 0, c1 = 0, c2 = 0, x = 0, xh = 0;
     template <int S>
     HD void mac(Dig<S> a, Dig<S> b) {
+#if defined(__CUDA_ARCH__) && HGM_MAC_PTX
+        // one IMAD.WIDE.U32 per column with the 64-bit accumulator as its addend
+        asm("mad.wide.u32 %0, %3, %4, %0;\n\t"
+            "mad.wide.u32 %1, %5, %6, %1;\n\t"
+            "mad.wide.u32 %2, %7, %8, %2;"
+            : "+l"(c0), "+l"(c1), "+l"(c2)
+            : "r"(a.l), "r"(b.l), "r"(a.s), "r"(b.s), "r"(a.h), "r"(b.h));
+#else
         c0 += (u64)a.l * b.l;
         c1 += (u64)a.s * b.s;
         c2 += (u64)a.h * b.h;
+#endif
     }
     // adds a full 64-bit value
     template <int S>
     HD void add(u64 v) {
-        x += v;
-        xh += (x < v);
+        add128(x, xh, v, 0);
     }
     // x + c0 + (c1 - c0 - c2) 2^S + c2 2^(2S) as a 128-bit accumulator
     template <int S>
     HD Acc fold() const {
         const u64 mid = c1 - c0 - c2;
         Acc a;
-        a.lo = c0 + x;
-        a.hi = xh + (a.lo < x);
-        const u64 t1 = mid << S, t2 = c2 << (2 * S);
-        a.lo += t1;
-        a.hi += (mid >> (64 - S)) + (a.lo < t1);
-        a.lo += t2;
-        a.hi += (c2 >> (64 - 2 * S)) + (a.lo < t2);
+        a.lo = x;
+        a.hi = xh;
+        add128(a.lo, a.hi, c0, 0);
+        add128(a.lo, a.hi, mid << S, mid >> (64 - S));
+        add128(a.lo, a.hi, c2 << (2 * S), c2 >> (64 - 2 * S));
         return a;
     }
 };
@@ -341,30 +357,23 @@ struct Acc128 {
 HD void fx_add(Acc128& s, u64 y, const Frac& f) {
     // y*f.hi (128 bit) + mulhi(y, f.lo)
     u64 plo = y * f.hi, phi = mulhi64(y, f.hi);
-    u64 t = mulhi64(y, f.lo);
-    u64 lo1 = plo + t;
-    phi += (lo1 < plo);
-    u64 lo2 = s.lo + lo1;
-    s.hi += phi + (lo2 < lo1);
-    s.lo = lo2;
+    add128(plo, phi, mulhi64(y, f.lo), 0);
+    add128(s.lo, s.hi, plo, phi);
 }
 // fx_add for a fraction whose integer part f.hi < 2^32 (1/q, 1/b: f.hi = 2^64/q):
 // y * f.hi from two 32x32 products instead of a full 64x64 one; same sum exactly
 HD void fx_add_small(Acc128& s, u64 y, const Frac& f) {
     const u64 p0 = (u64)(u32)y * f.hi, p1 = (y >> 32) * f.hi;  // f.hi < 2^32
-    const u64 plo = p0 + (p1 << 32);
-    u64 phi = (p1 >> 32) + (plo < p0);
-    const u64 t = mulhi64(y, f.lo);
-    const u64 lo1 = plo + t;
-    phi += (lo1 < plo);
-    const u64 lo2 = s.lo + lo1;
-    s.hi += phi + (lo2 < lo1);
-    s.lo = lo2;
+    u64 plo = p0, phi = 0;
+    add128(plo, phi, p1 << 32, p1 >> 32);
+    add128(plo, phi, mulhi64(y, f.lo), 0);
+    add128(s.lo, s.hi, plo, phi);
 }
 HD u64 fx_round(const Acc128& s) {
     // (s + 2^63) >> 64
-    u64 lo = s.lo + (1ULL << 63);
-    return s.hi + (lo < s.lo);
+    u64 lo = s.lo, hi = s.hi;
+    add128(lo, hi, 1ULL << 63, 0);
+    return hi;
 }
 
 // ------------------------------------------------------------------ sampler
