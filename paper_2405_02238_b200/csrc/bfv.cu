@@ -711,33 +711,36 @@ __global__ void __launch_bounds__(kThreads, 4) k_tensor_acc(DevCtx cx, u32 n, co
         u64* t2 = t1 + (size_t)D * N;
         const bool acc = init[item] != 0;
         COEF_LOOP {
+            // chunks of kGroup products (the column sums' range), each chunk's
+            // columns starting from the running residues (folded in as x)
             u64 p0 = 0, pm = 0, p2 = 0;
-            Cols s0, sm, s2;
-            u32 since = 0;
-            for (u32 i = i0; i < i1; ++i) {
-                const u64 *a0, *a1, *b0, *b1;
-                if (d < L) {
-                    a0 = A[i] + (size_t)d * N; a1 = A[i] + (size_t)(L + d) * N;
-                    b0 = B[i] + (size_t)d * N; b1 = B[i] + (size_t)(L + d) * N;
-                } else {
-                    a0 = XB + ((size_t)i * 4 * nB + (d - L)) * N; a1 = a0 + (size_t)nB * N;
-                    b0 = a1 + (size_t)nB * N; b1 = b0 + (size_t)nB * N;
+            for (u32 ic = i0; ic < i1; ic += kGroup) {
+                const u32 ni = i1 - ic < kGroup ? i1 - ic : kGroup;
+                Cols s0, sm, s2;
+                s0.x = p0;
+                sm.x = pm;
+                s2.x = p2;
+#pragma unroll
+                for (u32 u = 0; u < kGroup; ++u) {
+                    if (u >= ni) break;
+                    const u32 i = ic + u;
+                    const u64 *a0, *a1, *b0, *b1;
+                    if (d < L) {
+                        a0 = A[i] + (size_t)d * N; a1 = A[i] + (size_t)(L + d) * N;
+                        b0 = B[i] + (size_t)d * N; b1 = B[i] + (size_t)(L + d) * N;
+                    } else {
+                        a0 = XB + ((size_t)i * 4 * nB + (d - L)) * N; a1 = a0 + (size_t)nB * N;
+                        b0 = a1 + (size_t)nB * N; b1 = b0 + (size_t)nB * N;
+                    }
+                    const u64 x0 = a0[j], x1 = a1[j], y0 = b0[j], y1 = b1[j];
+                    s0.mac(split<SH::S>(x0), split<SH::S>(y0));
+                    s2.mac(split<SH::S>(x1), split<SH::S>(y1));
+                    sm.mac(split<SH::S>(add_mod(x0, x1, q)), split<SH::S>(add_mod(y0, y1, q)));
                 }
-                const u64 x0 = a0[j], x1 = a1[j], y0 = b0[j], y1 = b1[j];
-                s0.mac(split<SH::S>(x0), split<SH::S>(y0));
-                s2.mac(split<SH::S>(x1), split<SH::S>(y1));
-                sm.mac(split<SH::S>(add_mod(x0, x1, q)), split<SH::S>(add_mod(y0, y1, q)));
-                if (++since == kGroup && i + 1 < i1) {
-                    p0 = add_mod(p0, reduce_acc(s0.fold<SH::S>(), P), q);
-                    pm = add_mod(pm, reduce_acc(sm.fold<SH::S>(), P), q);
-                    p2 = add_mod(p2, reduce_acc(s2.fold<SH::S>(), P), q);
-                    s0 = Cols{}; sm = Cols{}; s2 = Cols{};
-                    since = 0;
-                }
+                p0 = reduce_acc(s0.fold<SH::S>(), P);
+                pm = reduce_acc(sm.fold<SH::S>(), P);
+                p2 = reduce_acc(s2.fold<SH::S>(), P);
             }
-            p0 = add_mod(p0, reduce_acc(s0.fold<SH::S>(), P), q);
-            pm = add_mod(pm, reduce_acc(sm.fold<SH::S>(), P), q);
-            p2 = add_mod(p2, reduce_acc(s2.fold<SH::S>(), P), q);
             u64 p1 = sub_mod(sub_mod(pm, p0, q), p2, q);
             if (acc) {
                 p0 = add_mod(p0, t0[j], q);
