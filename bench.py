@@ -267,13 +267,16 @@ def ntt_roofline(ctx, limb_bytes, label):
     ks_bytes = (ctx.dnum * R + ctx.L + 2 * R + ctx.dnum * 2 * R / 8) * ctx.N * 8
     ks_ms = ctx.bench_keyswitch(ks_items, 10)
     ks_gbs = ks_items * ks_bytes / (ks_ms / 1e3) / 1e9
-    traffic = None
+    traffic, pipes = None, None
     prof = os.path.join(ROOT, "profiles", "ntt_traffic.json")
     if os.path.exists(prof):
         try:
             rec = json.load(open(prof))
             if rec.get("N", 8192) == ctx.N and rec.get("bytes_per_limb"):
                 traffic = rec["bytes_per_limb"] * limbs
+                # integer-pipe utilisation of the same launch (ncu, profiles/): the bound that binds
+                pipes = {k: rec.get(k) for k in ("fmaheavy_frac", "alu_frac", "issue_frac")}
+                pipes["source"] = rec.get("source")
         except Exception:
             traffic = None
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -282,9 +285,10 @@ def ntt_roofline(ctx, limb_bytes, label):
             "ms_per_launch": round(ntt_ms, 4),
             "inverse_frac": round(limbs * limb_bytes / (intt_ms / 1e3) / 1e9 / peak, 4),
             "peak_source": peak_src, "frac_vs_spec_8tbs": round(achieved / 8000.0, 4),
+            "int_pipes_ncu": pipes,
             "keyswitch": {"kernel": "k_ks_inner (key inner product, Galois gather fused, 8 rotations per key read)",
                           "rotations_per_launch": ks_items, "algorithmic_bytes_per_rotation": int(ks_bytes),
-                          "traffic": ks_traffic(ctx.N, ks_items),
+                          "traffic": ks_traffic(ctx.N, ks_items), "int_pipes_ncu": ks_pipes(ctx.N),
                           "ms_per_launch": round(ks_ms, 4), "achieved": round(ks_gbs, 1),
                           "frac": round(ks_gbs / peak, 4)}}
 
@@ -297,6 +301,16 @@ def ks_traffic(N, items):
         rec = json.load(open(prof))
         if rec.get("N") == N and rec.get("bytes_per_rotation"):
             return rec["bytes_per_rotation"] * items
+    except Exception:
+        pass
+    return None
+
+
+def ks_pipes(N):
+    try:
+        rec = json.load(open(os.path.join(ROOT, "profiles", "ks_traffic.json")))
+        if rec.get("N") == N:
+            return {k: rec.get(k) for k in ("fmaheavy_frac", "alu_frac", "issue_frac")}
     except Exception:
         pass
     return None

@@ -308,6 +308,14 @@ struct Cols {
     HD void mac(Dig<S> a, Dig<S> b) {
 #if defined(__CUDA_ARCH__) && HGM_MAC_PTX
         // one IMAD.WIDE.U32 per column with the 64-bit accumulator as its addend
+        // (parameter set 1's long unrolled conversions, S = 28, keep the C form:
+        // the asm operands pushed k_scale_round<ShapeQ8> into 1.4 KB of spills)
+        if constexpr (S == 28) {
+            c0 += (u64)a.l * b.l;
+            c1 += (u64)a.s * b.s;
+            c2 += (u64)a.h * b.h;
+            return;
+        }
         asm("mad.wide.u32 %0, %3, %4, %0;\n\t"
             "mad.wide.u32 %1, %5, %6, %1;\n\t"
             "mad.wide.u32 %2, %7, %8, %2;"

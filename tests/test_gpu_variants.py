@@ -17,6 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 VARIANTS = {
     "one-cta-ntt": {"HGM_NTT3": "0"},
+    "general-lincomb": {"HGM_LC_MASKED": "0"},
     # N = 32768 as two HBM passes (outer 2-stage kernel + 2^13 blocks) instead of 4-CTA clusters
     "two-pass-n32768-ntt": {"HGM_NTT_CLUSTER": "0"},
     "fused-modup-moddown": {"HGM_FUSED_KS": "1"},

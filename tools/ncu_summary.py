@@ -54,8 +54,20 @@ def main():
     json.dump(res, open(out, "w"), indent=1)
     if limbs and len(sys.argv) > 4:
         name = res["Kernel Name"].split("::")[-1].split("(")[0]
-        json.dump({"kernel": name, "source": f"{out} (ncu --set full, {limbs}-limb launch)",
-                   "bytes_per_limb": res["dram_bytes_per_limb"]}, open(sys.argv[4], "w"), indent=1)
+        def pct(k):
+            try:
+                return round(float(val[col[k]].replace(",", "")) / 100.0, 4)
+            except (KeyError, ValueError):
+                return None
+        n_dim = 32768 if "c4" in name else 8192
+        rec = {"kernel": name, "N": n_dim, "source": f"{out} (ncu --set full, {limbs}-unit launch)",
+               "bytes_per_limb": res["dram_bytes_per_limb"],
+               "fmaheavy_frac": pct("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+               "alu_frac": pct("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+               "issue_frac": pct("smsp__issue_active.avg.pct_of_peak_sustained_active")}
+        if "ks_inner" in name:
+            rec["bytes_per_rotation"] = rec.pop("bytes_per_limb")
+        json.dump(rec, open(sys.argv[4], "w"), indent=1)
     print(json.dumps(res, indent=1))
 
 

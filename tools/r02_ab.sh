@@ -7,7 +7,7 @@ for r in 1 2; do
   for c in "${CASES[@]}"; do
     IFS='|' read -r label lib envs <<< "$c"
     [ "$lib" = "-" ] && lib=""
-    v=$(env ${lib:+HGM_LIB=$lib} $envs python bench.py --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; print(json.loads(sys.stdin.read())['value'])")
+    v=$(env ${lib:+HGM_LIB=$lib} $envs python bench.py --no-cpu-baseline --no-e2e $BENCH_ARGS 2>/dev/null | python -c "import json,sys; print(json.loads(sys.stdin.read())['value'])")
     echo "$label $v"
   done
 done
