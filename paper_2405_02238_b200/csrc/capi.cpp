@@ -9,6 +9,8 @@
 // ModUps.  Nodes still referenced by a pinned handle keep their ciphertext;
 // every other intermediate is recomputed on demand (all ops are deterministic).
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <functional>
 #include <future>
 #include <map>
@@ -782,11 +784,23 @@ void run_instances(Context& ctx, const MatmulProgram& prog, size_t count,
         for (Slot& sl : slot)
             if (sl.unpacking.valid()) sl.unpacking.get();
     };
+    // HGM_TRACE=1: per-chunk host timeline on stderr (where the end-to-end path waits)
+    static const bool trace = [] {
+        const char* e = std::getenv("HGM_TRACE");
+        return e && e[0] == '1';
+    }();
+    const auto t_start = std::chrono::steady_clock::now();
+    auto ms_since = [&]() {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    };
     try {
         size_t i = 0;
         for (size_t c0 = 0; c0 < count; c0 += chunk, ++i) {
             const int K = (int)std::min(chunk, count - c0);
+            const double tw0 = trace ? ms_since() : 0;
             Packed packed = next.get();
+            if (trace) std::fprintf(stderr, "hgm_trace chunk %zu (K=%d): pack wait %.1f ms at %.1f\n", i, K,
+                                    ms_since() - tw0, ms_since());
             if (c0 + chunk < count) next = std::async(std::launch::async, pack_chunk, c0 + chunk);
             ExecIO io;
             io.K = K;
@@ -808,8 +822,10 @@ void run_instances(Context& ctx, const MatmulProgram& prog, size_t count,
             }
             for (u64* r : res) ctx.release(r);
             finish(sl, c0, K);
+            if (trace) std::fprintf(stderr, "hgm_trace chunk %zu enqueued at %.1f\n", i, ms_since());
         }
         drain();
+        if (trace) std::fprintf(stderr, "hgm_trace drained at %.1f (chunk %zu instances)\n", ms_since(), chunk);
     } catch (...) {
         try { drain(); } catch (...) {}
         ctx.sync();
