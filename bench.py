@@ -326,6 +326,7 @@ def run_cfg4(args):
     per_gpu = args.instances or TOTAL_INSTANCES
     total = per_gpu if args.strong else per_gpu * world
     first, count = shard(rank, world, total)
+    local = env_int("HGM_DEVICE", local)  # test hook: several ranks on one GPU (tests/test_gpu_multirank.py)
     ctx = hb.Context(PARAM_ID, 1, local)
     comm = comm_from_env(ctx)  # the library's NCCL communicator (no torch)
     A, B = batch(SEED, first, count, M, L_, N_, LO, HI)
@@ -467,6 +468,7 @@ def run_cfg5(args):
     total_blocks = products * c["parts"]
     first, count = shard(rank, world, total_blocks)
     h = c["m"] // c["parts"]
+    local = env_int("HGM_DEVICE", local)
     ctx = hb.Context(c["param_id"], 1, local)
     comm = comm_from_env(ctx)
     mats = [splitmix_matrices(c["seed"], p, c["m"], c["l"], c["n"], c["lo"], c["hi"]) for p in range(products)]
