@@ -329,6 +329,15 @@ int hgm_comm_gather(hgm_comm* cm, const uint64_t* send, size_t send_words, uint6
         // every rank checks the root's capacity, so no rank enqueues a transfer the root will refuse
         const std::vector<u64> caps = allgather_u64(cm, cm->rank == root ? (u64)recv_cap_words : 0);
         if (cm->rank == root && total && !recv) throw std::invalid_argument("null receive buffer on the root");
+        static const bool trace = [] {
+            const char* e = std::getenv("HGM_TRACE");
+            return e && e[0] == '1';
+        }();
+        if (trace) {
+            std::fprintf(stderr, "hgm_comm_gather rank %d: send %zu words, counts", cm->rank, send_words);
+            for (u64 x : cnt) std::fprintf(stderr, " %llu", (unsigned long long)x);
+            std::fprintf(stderr, ", root cap %llu\n", (unsigned long long)caps[root]);
+        }
         if (total > caps[root])
             throw std::invalid_argument("gather of " + std::to_string(total) + " words exceeds the root's buffer of " +
                                         std::to_string(caps[root]));

@@ -48,6 +48,11 @@ size_t type_size(ncclDataType_t t) {
     }
 }
 ncclResult_t sync(cudaStream_t s) { return cudaStreamSynchronize(s) == cudaSuccess ? ncclSuccess : ncclUnhandledCudaError; }
+// copies ordered on the communicator's stream and complete on return (a plain
+// cudaMemcpy from pageable memory may return before its DMA lands)
+bool copy(void* dst, const void* src, size_t n, cudaMemcpyKind k, cudaStream_t s) {
+    return cudaMemcpyAsync(dst, src, n, k, s) == cudaSuccess && cudaStreamSynchronize(s) == cudaSuccess;
+}
 
 }  // namespace
 
@@ -119,7 +124,7 @@ ncclResult_t ncclSend(const void* buf, size_t count, ncclDataType_t t, int peer,
     if (c->rank != 0 && peer != 0) return ncclInvalidUsage;
     if (sync(s) != ncclSuccess) return ncclUnhandledCudaError;
     std::vector<char> h(count * type_size(t));
-    cudaMemcpy(h.data(), buf, h.size(), cudaMemcpyDeviceToHost);
+    if (!copy(h.data(), buf, h.size(), cudaMemcpyDeviceToHost, s)) return ncclUnhandledCudaError;
     return io_all(c->fd[peer], h.data(), h.size(), true) ? ncclSuccess : ncclSystemError;
 }
 ncclResult_t ncclRecv(void* buf, size_t count, ncclDataType_t t, int peer, ncclComm_t c, cudaStream_t s) {
@@ -127,8 +132,7 @@ ncclResult_t ncclRecv(void* buf, size_t count, ncclDataType_t t, int peer, ncclC
     if (sync(s) != ncclSuccess) return ncclUnhandledCudaError;
     std::vector<char> h(count * type_size(t));
     if (!io_all(c->fd[peer], h.data(), h.size(), false)) return ncclSystemError;
-    return cudaMemcpy(buf, h.data(), h.size(), cudaMemcpyHostToDevice) == cudaSuccess ? ncclSuccess
-                                                                                     : ncclUnhandledCudaError;
+    return copy(buf, h.data(), h.size(), cudaMemcpyHostToDevice, s) ? ncclSuccess : ncclUnhandledCudaError;
 }
 // all-gather / all-reduce(max) through rank 0
 ncclResult_t ncclAllGather(const void* send, void* recv, size_t count, ncclDataType_t t, ncclComm_t c,
@@ -136,7 +140,7 @@ ncclResult_t ncclAllGather(const void* send, void* recv, size_t count, ncclDataT
     if (sync(s) != ncclSuccess) return ncclUnhandledCudaError;
     const size_t b = count * type_size(t);
     std::vector<char> all(b * c->world);
-    cudaMemcpy(all.data() + b * c->rank, send, b, cudaMemcpyDeviceToHost);
+    if (!copy(all.data() + b * c->rank, send, b, cudaMemcpyDeviceToHost, s)) return ncclUnhandledCudaError;
     if (c->rank == 0) {
         for (int r = 1; r < c->world; ++r)
             if (!io_all(c->fd[r], all.data() + b * r, b, false)) return ncclSystemError;
@@ -146,21 +150,20 @@ ncclResult_t ncclAllGather(const void* send, void* recv, size_t count, ncclDataT
         if (!io_all(c->fd[0], all.data() + b * c->rank, b, true) || !io_all(c->fd[0], all.data(), all.size(), false))
             return ncclSystemError;
     }
-    cudaMemcpy(recv, all.data(), all.size(), cudaMemcpyHostToDevice);
-    return ncclSuccess;
+    return copy(recv, all.data(), all.size(), cudaMemcpyHostToDevice, s) ? ncclSuccess : ncclUnhandledCudaError;
 }
 ncclResult_t ncclAllReduce(const void* send, void* recv, size_t count, ncclDataType_t t, ncclRedOp_t op,
                            ncclComm_t c, cudaStream_t s) {
     if (t != ncclFloat64 || op != ncclMax || count != 1) return ncclInvalidUsage;
     std::vector<double> all(c->world);
     double* tmp = nullptr;
-    cudaMalloc(&tmp, sizeof(double) * c->world);
+    if (cudaMalloc(&tmp, sizeof(double) * c->world) != cudaSuccess) return ncclUnhandledCudaError;
     const ncclResult_t r = ncclAllGather(send, tmp, 1, ncclFloat64, c, s);
-    cudaMemcpy(all.data(), tmp, sizeof(double) * c->world, cudaMemcpyDeviceToHost);
+    const bool ok = copy(all.data(), tmp, sizeof(double) * c->world, cudaMemcpyDeviceToHost, s);
     cudaFree(tmp);
     double m = all[0];
     for (double v : all) m = v > m ? v : m;
-    cudaMemcpy(recv, &m, sizeof(m), cudaMemcpyHostToDevice);
+    if (!ok || !copy(recv, &m, sizeof(m), cudaMemcpyHostToDevice, s)) return ncclUnhandledCudaError;
     return r;
 }
 

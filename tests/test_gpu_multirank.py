@@ -30,20 +30,24 @@ def free_port():
     return p
 
 
-def launch(world, argv, tmp_path, timeout=600):
+def launch(world, argv, tmp_path, timeout=600, id_file=True):
     if not os.path.exists(SHIM):
         pytest.skip("tests/shim/libnccl_tcp_shim.so not built")
     port = free_port()
     procs = []
     for r in range(world):
         env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), LOCAL_RANK=str(r), MASTER_ADDR="127.0.0.1",
-                   MASTER_PORT=str(port), HGM_NCCL_LIB=SHIM, HGM_DEVICE="0",
-                   HGM_COMM_ID_FILE=str(tmp_path / f"id_{port}"))
+                   MASTER_PORT=str(port), HGM_NCCL_LIB=SHIM, HGM_DEVICE="0")
+        if id_file:
+            env["HGM_COMM_ID_FILE"] = str(tmp_path / f"id_{port}")
+        else:  # the launcher default: /tmp/hgm_comm_<port>_<run>_<parent pid>.id (dist.id_file_path)
+            env.pop("HGM_COMM_ID_FILE", None)
         procs.append(subprocess.Popen([sys.executable] + argv, cwd=ROOT, env=env, stdout=subprocess.PIPE,
                                       stderr=subprocess.PIPE, text=True))
     outs = [p.communicate(timeout=timeout) for p in procs]
-    for p, (o, e) in zip(procs, outs):
-        assert p.returncode == 0, f"rank failed:\n{o[-2000:]}\n{e[-4000:]}"
+    bad = [r for r, p in enumerate(procs) if p.returncode != 0]
+    assert not bad, "\n".join(f"rank {r} rc {procs[r].returncode}:\n{outs[r][0][-1500:]}\n{outs[r][1][-3000:]}"
+                               for r in range(world))
     return outs
 
 
@@ -60,7 +64,7 @@ def test_bench_cfg4_two_ranks(tmp_path):
 
 def test_bench_cfg5_two_ranks(tmp_path):
     outs = launch(2, ["bench.py", "--gpus", "2", "--config", "cfg5", "--instances", "1", "--steps", "1",
-                      "--warmup", "3", "--no-e2e"], tmp_path)
+                      "--warmup", "3", "--no-e2e"], tmp_path, id_file=False)
     line = json.loads(outs[0][0].strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["config"]["row_blocks_per_gpu"] == 4
     assert line["verified"]["value"].startswith("1 of 1 128^3 products")
