@@ -9,6 +9,8 @@
 #include <stdexcept>
 
 #include "context.hpp"
+
+#include <type_traits>
 #include "parallel.hpp"
 
 namespace hgm {
@@ -310,26 +312,37 @@ __global__ void __launch_bounds__(kThreads, HGM_LC_MINB) k_lincomb_masked(DevCtx
             const size_t wl2 = w2 < LN / 2 ? w2 : w2 - LN / 2;  // pair index within the component
             const Prime& P = dp->pr[(wl2 * 2) >> logN];
             u64 r0 = 0, r1 = 0;
-            for (u32 t = t0; t < t1; t += 3) {
-                const u32 nt = t1 - t < 3 ? t1 - t : 3;
-                ulonglong2 v[3], m[3];
+            // one straight-line block per chunk size: with the term count a
+            // compile-time constant the column accumulators stay in aligned
+            // register pairs and every product is a single IMAD.WIDE (a shared,
+            // predicated block split each into IMAD.WIDE + IADD3 + IMAD.X + moves)
+            auto chunk = [&](auto nt_c, u32 t) {
+                constexpr u32 NT = decltype(nt_c)::value;
+                ulonglong2 v[NT], m[NT];
 #pragma unroll
-                for (u32 u = 0; u < 3; ++u)
-                    if (u < nt) {
-                        v[u] = reinterpret_cast<const ulonglong2*>(in[t + u])[w2];
-                        m[u] = __ldg(reinterpret_cast<const ulonglong2*>(mask[t + u]) + wl2);
-                    }
+                for (u32 u = 0; u < NT; ++u) {
+                    v[u] = reinterpret_cast<const ulonglong2*>(in[t + u])[w2];
+                    m[u] = __ldg(reinterpret_cast<const ulonglong2*>(mask[t + u]) + wl2);
+                }
                 Cols a0, a1;
                 a0.x = r0;
                 a1.x = r1;
 #pragma unroll
-                for (u32 u = 0; u < 3; ++u)
-                    if (u < nt) {
-                        a0.mac(split<SH::S>(v[u].x), packed_dig<SH::S>(m[u].x));
-                        a1.mac(split<SH::S>(v[u].y), packed_dig<SH::S>(m[u].y));
-                    }
+                for (u32 u = 0; u < NT; ++u) {
+                    a0.mac(split<SH::S>(v[u].x), packed_dig<SH::S>(m[u].x));
+                    a1.mac(split<SH::S>(v[u].y), packed_dig<SH::S>(m[u].y));
+                }
                 r0 = reduce_acc(a0.fold<SH::S>(), P);
                 r1 = reduce_acc(a1.fold<SH::S>(), P);
+            };
+            for (u32 t = t0; t < t1; t += 3) {
+                const u32 nt = t1 - t;
+                if (nt >= 3)
+                    chunk(std::integral_constant<u32, 3>{}, t);
+                else if (nt == 2)
+                    chunk(std::integral_constant<u32, 2>{}, t);
+                else
+                    chunk(std::integral_constant<u32, 1>{}, t);
             }
             ulonglong2 r;
             r.x = r0;
