@@ -397,14 +397,14 @@ __global__ void k_gather_c1(DevCtx cx, u32 n, const u64* const* ct, u64* C) {
 // copies them from the NTT-domain ciphertext, so they need no forward NTT).
 template <typename SH>
 __global__ void k_modup_lift(DevCtx cx, u32 n, const u64* C, size_t c_stride,
-                             u64* D, int from_intt) {
+                             u64* D, int from_intt, u64* const* Dp = nullptr) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = SH::L, R = SH::R, A = SH::A, dnum = SH::dnum;
     const u64* ghi = from_intt ? dp->dg_hat_inv_n : dp->dg_hat_inv;
     const u64* ghs = from_intt ? dp->dg_hat_inv_n_sh : dp->dg_hat_inv_sh;
     ITEM_LOOP {
         const u64* c = C + item * c_stride;
-        u64* d = D + (size_t)item * dnum * R * N;
+        u64* d = Dp ? Dp[item] : D + (size_t)item * dnum * R * N;  // per-item outputs, or one block
         COEF_LOOP {
             u64 x[kMaxL];
             for (u32 i = 0; i < L; ++i) x[i] = c[(size_t)i * N + j];
@@ -1546,16 +1546,26 @@ void Context::modup(int n, const u64* const* ct, u64* const* out) {
         if (hp_.L == 3) k_gather_c1<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, upload(vc), C); else k_gather_c1<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, upload(vc), C); ++launches_;
         ntt(false, jobs_contig(C, n * L, 0, L));
     }
-    // lift into a contiguous staging area, then scatter-copy to the outputs
+    // the digits go straight to the per-item outputs (only the opt-in fused
+    // ModUp needs one contiguous block, staged and scattered afterwards)
+    const bool fused = ntt_fusable(hp_.dev, kFuseModUp);
+    const size_t W = modup_words();
     bool contiguous = true;
     for (int i = 1; i < n; ++i)
-        if (out[i] != out[0] + (size_t)i * dnum * R * N) contiguous = false;
-    u64* D = contiguous ? out[0] : alloc((size_t)n * dnum * R * N);
-    if (ntt_fusable(hp_.dev, kFuseModUp)) {
+        if (out[i] != out[0] + (size_t)i * W) contiguous = false;
+    u64* const* dpd = upload(std::vector<u64*>(out, out + n));
+    if (fused) {
+        u64* D = contiguous ? out[0] : alloc((size_t)n * W);
         ntt_modup_fused(cx_, hp_.dev, n, C, (size_t)L * N, D, stream_);
         ++launches_;
+        if (!contiguous) {
+            std::vector<const u64*> src(n);
+            for (int i = 0; i < n; ++i) src[i] = D + (size_t)i * W;
+            k_copy<<<grid_of(N, n), kThreads, 0, stream_>>>(n, W, upload(src), dpd); ++launches_;
+            release(D);
+        }
     } else if (own_copy) {
-        if (hp_.L == 3) k_modup_lift<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, C, (size_t)L * N, D, 1); else k_modup_lift<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, C, (size_t)L * N, D, 1); ++launches_;
+        if (hp_.L == 3) k_modup_lift<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, C, (size_t)L * N, nullptr, 1, dpd); else k_modup_lift<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, C, (size_t)L * N, nullptr, 1, dpd); ++launches_;
         // forward NTT of the lifted (non-own) limbs only; own limbs copied from c1
         const u32 A = hp_.alpha, per = dnum * R - L;
         NttJobs dj;
@@ -1567,7 +1577,7 @@ void Context::modup(int n, const u64* const* ct, u64* const* out) {
             for (u32 r = 0; r < R; ++r)
                 if (!(r < L && r / A == dg)) dj.prime[k++] = (unsigned char)r;
         for (int i = 0; i < n; ++i) {
-            u64* base = D + (size_t)i * dnum * R * N;
+            u64* base = out[i];
             u32 t = 0;
             for (u32 dg = 0; dg < dnum; ++dg)
                 for (u32 r = 0; r < R; ++r) {
@@ -1586,16 +1596,13 @@ void Context::modup(int n, const u64* const* ct, u64* const* out) {
         ntt(true, dj);
         k_copy<<<grid_of(N, n * L), kThreads, 0, stream_>>>(n * L, N, upload(csrc), upload(cdst)); ++launches_;
     } else {
-        if (hp_.L == 3) k_modup_lift<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, C, (size_t)L * N, D, 0); else k_modup_lift<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, C, (size_t)L * N, D, 0); ++launches_;
-        ntt(true, jobs_contig(D, n * dnum * R, 0, R));
-    }
-    if (!contiguous) {
-        std::vector<const u64*> src(n);
-        std::vector<u64*> dst(out, out + n);
-        for (int i = 0; i < n; ++i) src[i] = D + (size_t)i * dnum * R * N;
-        const size_t W = modup_words();
-        k_copy<<<grid_of(N, n), kThreads, 0, stream_>>>(n, W, upload(src), upload(dst)); ++launches_;
-        release(D);
+        if (hp_.L == 3) k_modup_lift<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, C, (size_t)L * N, nullptr, 0, dpd); else k_modup_lift<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, C, (size_t)L * N, nullptr, 0, dpd); ++launches_;
+        NttJobs dj = jobs_contig(nullptr, n * dnum * R, 0, R);
+        std::vector<u64*> dl((size_t)n * dnum * R);
+        for (int i = 0; i < n; ++i)
+            for (u32 w = 0; w < dnum * R; ++w) dl[(size_t)i * dnum * R + w] = out[i] + (size_t)w * N;
+        dj.ptrs = upload(dl);
+        ntt(true, dj);
     }
     release(C);
     HGM_CUDA(cudaGetLastError());

@@ -1268,7 +1268,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__((1 << LB) / kElems3,
     u32 quarter[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) quarter[r] = dsmem_base(sm, r);
-    const u64* a = jv.ptr;
+    const u64* a = jobs.src ? jobs.src[blockIdx.x >> 2] : jv.ptr;  // out-of-place: read the source limb
     constexpr int kBatch = 4;  // columns per batch: 16 loads in flight per thread
 #pragma unroll 1
     for (int c0 = 0; c0 < COLS / T; c0 += kBatch) {
@@ -1322,7 +1322,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__((1 << LB) / kElems3,
     const u64 q = P.q;
     const u64* w = cx.tw + (size_t)jv.prime * 4 * N;
     fill_tw_cache_async(cache, pairs(w + 2 * N), logN - LB, blk, kTwCache3);
-    load_first_stage<LB, kElems3, 8>(sm, jv.ptr + ((size_t)blk << LB), pairs(w + 2 * N), q, logN, blk);
+    const u64* src = jobs.src ? jobs.src[blockIdx.x >> 2] : jv.ptr;  // every read precedes the first write
+    load_first_stage<LB, kElems3, 8>(sm, src + ((size_t)blk << LB), pairs(w + 2 * N), q, logN, blk);
     cp_async_wait_all();
     __syncthreads();
     inv_round<LB, 1, LB - 9, false, kElems3>(sm, cache, pairs(w + 2 * N), q, logN, blk);
@@ -1492,6 +1493,8 @@ void ntt_tensor_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* c
 
 bool ntt_inverse_takes_first_stage(const DevParams& hp) { return hp.logN == 13 && use_ntt3(); }
 
+bool ntt_out_of_place_ok(const DevParams& hp) { return hp.logN <= 13 || (hp.logN == 15 && ntt_cluster4()); }
+
 void ntt_upload_params(int pid, const DevParams& p) {
     cudaMemcpyToSymbol(c_dp, &p, sizeof(DevParams), (size_t)pid * sizeof(DevParams));
 }
@@ -1564,7 +1567,7 @@ bool launch_t(bool fwd, const DevCtx& cx, const DevParams& hp, const NttJobs& jo
 
 void ntt_forward(const DevCtx& cx, const DevParams& hp, const NttJobs& jobs_in, cudaStream_t s) {
     if (jobs_in.count == 0) return;
-    if (jobs_in.src && hp.logN > 13) throw std::logic_error("out-of-place NTT needs whole-limb blocks");
+    if (jobs_in.src && !ntt_out_of_place_ok(hp)) throw std::logic_error("out-of-place NTT needs whole-limb blocks");
     NttJobs jobs = jobs_in;
     jobs.pack();
     if (launch_t(true, cx, hp, jobs, s)) return;
@@ -1587,7 +1590,7 @@ void ntt_forward(const DevCtx& cx, const DevParams& hp, const NttJobs& jobs_in, 
 
 void ntt_inverse(const DevCtx& cx, const DevParams& hp, const NttJobs& jobs_in, cudaStream_t s) {
     if (jobs_in.count == 0) return;
-    if (jobs_in.src && hp.logN > 13) throw std::logic_error("out-of-place NTT needs whole-limb blocks");
+    if (jobs_in.src && !ntt_out_of_place_ok(hp)) throw std::logic_error("out-of-place NTT needs whole-limb blocks");
     NttJobs jobs = jobs_in;
     jobs.pack();
     if (launch_t(false, cx, hp, jobs, s)) return;

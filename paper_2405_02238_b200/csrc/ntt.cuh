@@ -61,7 +61,9 @@ void ntt_inverse(const DevCtx& cx, const DevParams& hp, const NttJobs& jobs, cud
 constexpr int kFuseModUp = 1, kFuseModDown = 2;
 bool ntt_fusable(const DevParams& hp, int which);
 // whole-limb transforms (N <= 8192): out-of-place jobs allowed
-inline bool ntt_fusable_size(const DevParams& hp) { return hp.logN <= 13; }
+// (N = 32768 too while its transforms run as 4-CTA clusters, which read any source)
+bool ntt_out_of_place_ok(const DevParams& hp);
+inline bool ntt_fusable_size(const DevParams& hp) { return ntt_out_of_place_ok(hp); }
 void ntt_modup_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* C, size_t c_stride, u64* D,
                      cudaStream_t s);
 void ntt_moddown_fused(const DevCtx& cx, const DevParams& hp, int n, u64* const* acc, const u64* const* addc,
