@@ -24,6 +24,21 @@ namespace {
 __constant__ DevParams c_dp[kParamSets];
 
 __device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
+// 32-bit shared::cluster addresses (mapa): four quarters cost four registers
+__device__ __forceinline__ u32 dsmem_base(const u64* local, u32 rank) {
+    u32 r;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((u32)__cvta_generic_to_shared(local)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void dsmem_st(u32 base, int i, u64 v) {
+    asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(base + 8u * (u32)i), "l"(v) : "memory");
+}
+__device__ __forceinline__ u64 dsmem_ld(u32 base, int i) {
+    u64 v;
+    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(base + 8u * (u32)i) : "memory");
+    return v;
+}
+
 // Runs f once per (call site, device): the dynamic shared-memory opt-in is a
 // per-device function attribute.
 template <typename F>
@@ -775,9 +790,81 @@ u32 io_ahead() {
     return on && ntt_l2_prefetch() ? (u32)(3 * sm_count()) : 0u;
 }
 
+// k_ntt_fwd_c4 with its input read through io.load and its output handed to
+// io.store (pair index over the whole 2^15 limb): N = 32768's fused epilogues
+// (ModDown's finishing pass) in the one-HBM-pass cluster transform.
+template <int LB, typename IO>
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__((1 << LB) / kElems3, 3)
+    k_ntt_fwd_c4_io(DevCtx cx, IO io) {
+    namespace cg = cooperative_groups;
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
+    extern __shared__ u64 sm[];
+    u64* cache = sm + smem_words<LB>();
+    constexpr int NB = 1 << LB, T = NB / kElems3, COLS = NB / 4;
+    const u32 N = dp->N;
+    const int logN = (int)dp->logN;
+    const int blk = (int)(blockIdx.x & 3);
+    const u32 job = blockIdx.x >> 2;
+    const int prime = io.prime(job);
+    const u64 q = dp->pr[prime].q;
+    const u64* w = cx.tw + (size_t)prime * 4 * N;
+    fill_tw_cache_async(cache, pairs(w), 2, blk, kTwCache3);
+    const ulonglong2* t = pairs(w);
+    const u64 w1 = t[1].x, w1s = t[1].y, w2 = t[2].x, w2s = t[2].y, w3 = t[3].x, w3s = t[3].y;
+    u32 quarter[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) quarter[r] = dsmem_base(sm, r);
+    constexpr int kBatch = 4;
+#pragma unroll 1
+    for (int c0 = 0; c0 < COLS / T; c0 += kBatch) {
+        u64 x[kBatch][4];
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            const int j = blk * COLS + (c0 + b) * T + (int)threadIdx.x;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) x[b][k] = io.load(dp, job, (u32)(j + k * NB));
+        }
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            const int j = blk * COLS + (c0 + b) * T + (int)threadIdx.x;
+            u64 V = shoup_mul(x[b][2], w1, w1s, q);
+            const u64 y0 = add_mod(x[b][0], V, q), y2 = sub_mod(x[b][0], V, q);
+            V = shoup_mul(x[b][3], w1, w1s, q);
+            const u64 y1 = add_mod(x[b][1], V, q), y3 = sub_mod(x[b][1], V, q);
+            V = shoup_mul(y1, w2, w2s, q);
+            const int p = pad(j);
+            dsmem_st(quarter[0], p, add_mod(y0, V, q));
+            dsmem_st(quarter[1], p, sub_mod(y0, V, q));
+            V = shoup_mul(y3, w3, w3s, q);
+            dsmem_st(quarter[2], p, add_mod(y2, V, q));
+            dsmem_st(quarter[3], p, sub_mod(y2, V, q));
+        }
+    }
+    cp_async_wait_all();
+    cg::this_cluster().sync();
+    fwd_round<LB, 0, 4, true, false, NoLoad, kElems3>(sm, cache, pairs(w), q, 2, blk);
+    __syncthreads();
+    fwd_round<LB, 4, 4, true, false, NoLoad, kElems3>(sm, cache, pairs(w), q, 2, blk);
+    __syncthreads();
+    fwd_round<LB, 8, LB - 9, false, false, NoLoad, kElems3>(sm, cache, pairs(w), q, 2, blk);
+    __syncthreads();
+    const u32 pair0 = (u32)blk << (LB - 1);
+    auto st = [&](int i, u64 v0, u64 v1) { io.store(dp, job, pair0 + (u32)i, v0, v1); };
+    store_last_stage_io<LB, decltype(st), kElems3>(sm, st, pairs(w), q, logN, blk);
+}
+
 template <typename IO>
 void launch_fwd_io(const DevCtx& cx, const DevParams& hp, const IO& io, u32 jobs, cudaStream_t s) {
     if (jobs == 0) return;
+    if (hp.logN == 15) {
+        const size_t smem = (smem_words<13>() + 2 * kTwCache3) * sizeof(u64);
+        static std::once_flag once15[64];
+        once_per_device(once15, [&] {
+            cudaFuncSetAttribute(k_ntt_fwd_c4_io<13, IO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        });
+        k_ntt_fwd_c4_io<13, IO><<<jobs * 4, (1 << 13) / kElems3, smem, s>>>(cx, io);
+        return;
+    }
     if (hp.logN == 13) {
         const size_t smem = (smem_words<13>() + 2 * kTwCache3) * sizeof(u64);
         static std::once_flag once13[64];
@@ -1233,21 +1320,6 @@ void launch_block_e(bool fwd, const DevCtx& cx, const NttJobs& jobs, int sub, cu
 // four quarters (three remotely), applies the two outer stages (+ N^-1) and
 // writes them to HBM; a final barrier keeps the shared memories alive until
 // every remote read is done.
-// 32-bit shared::cluster addresses (mapa): four quarters cost four registers
-__device__ __forceinline__ u32 dsmem_base(const u64* local, u32 rank) {
-    u32 r;
-    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((u32)__cvta_generic_to_shared(local)), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void dsmem_st(u32 base, int i, u64 v) {
-    asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(base + 8u * (u32)i), "l"(v) : "memory");
-}
-__device__ __forceinline__ u64 dsmem_ld(u32 base, int i) {
-    u64 v;
-    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(base + 8u * (u32)i) : "memory");
-    return v;
-}
-
 template <int LB>
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__((1 << LB) / kElems3, 3)
     k_ntt_fwd_c4(DevCtx cx, NttJobs jobs) {
@@ -1444,7 +1516,7 @@ bool ntt_finish_fusable(const DevParams& hp) {
         const char* e = std::getenv("HGM_FUSED_FINISH");
         return !e || e[0] != '0';
     }();
-    return on && hp.logN <= 13;
+    return on && (hp.logN <= 13 || (hp.logN == 15 && ntt_cluster4()));
 }
 
 void ntt_finish_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* V, u64* const* acc,
