@@ -512,19 +512,23 @@ __global__ void k_ks_inner(DevCtx cx, u32 n, const u64* const* D,
 // so that NTT(V) + P^-1 acc = (acc - NTT(conv)) P^-1 + NTT(ecoef) exactly (the NTT
 // is linear mod q_i): relinearisation adds e0, e1 without transforming them apart.
 template <typename SH>
-__global__ void __launch_bounds__(kThreads, 4) k_moddown_conv(DevCtx cx, u32 n, const u64* const* acc, const u64* const* ecoef, u64* V) {
+// Pc (optional): the P limbs' coefficients [n][2][K][N] (an out-of-place INTT, acc
+// left intact); otherwise they are read from acc's P limbs, inverse-transformed in place.
+__global__ void __launch_bounds__(kThreads, 4) k_moddown_conv(DevCtx cx, u32 n, const u64* const* acc, const u64* const* ecoef, u64* V,
+                                                               const u64* Pc) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = SH::L, K = SH::K, R = SH::R;
     ITEM_LOOP {
         const u32 c = blockIdx.z;
-        const u64* a = acc[item] + (size_t)c * R * N;
+        // P limb k: Pc's [item][c][k], or acc's limb L + k
+        const u64* pl = Pc ? Pc + ((size_t)item * 2 + c) * K * N : acc[item] + ((size_t)c * R + L) * N;
         const u64* ec = ecoef ? ecoef[item] + (size_t)c * L * N : nullptr;
         u64* v = V + ((size_t)item * 2 + c) * L * N;
         COEF_LOOP {
             u64 z[kMaxK];
             for (u32 k = 0; k < K; ++k) {
                 const u64 p = dp->pr[L + k].q;
-                z[k] = shoup_mul(a[(size_t)(L + k) * N + j], dp->phat_inv_n[k], dp->phat_inv_n_sh[k], p);
+                z[k] = shoup_mul(pl[(size_t)k * N + j], dp->phat_inv_n[k], dp->phat_inv_n_sh[k], p);
             }
             for (u32 i = 0; i < L; ++i) {
                 const u64 q = dp->pr[i].q;
@@ -1687,6 +1691,13 @@ void Context::inner_product(int n, const u64* const* digits, const u64* const* k
 //   out = (acc - NTT(conv)) P^-1 + NTT(ecoef) + addn[galois]   (ecoef/addn optional)
 // ecoef: per item [2][L][N] coefficient-domain addend (relinearisation's e0, e1);
 // addn: per item NTT-domain c0 limbs added to component 0 (rotation's phi(c0)).
+// key_switch_tail leaves acc intact: its P limbs are read by the fused
+// conversion (MdConvIO), or inverse-transformed out of place for k_moddown_conv
+bool Context::tail_keeps_acc() const {
+    if (ntt_fusable(hp_.dev, kFuseModDown)) return false;  // opt-in ModDownIO: P limbs transformed in place
+    return ntt_conv_fusable(hp_.dev) || ntt_out_of_place_ok(hp_.dev);
+}
+
 void Context::key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, const u64* const* addn,
                               const u32* g, u64* const* out) {
     const u32 N = hp_.N, L = hp_.L, K = hp_.K, R = hp_.R;
@@ -1705,7 +1716,20 @@ void Context::key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, c
         dec = upload(v);
     }
     const bool conv_fused = ntt_conv_fusable(hp_.dev) && !ntt_fusable(hp_.dev, kFuseModDown);
-    if (!conv_fused) {  // P limbs back to the coefficient domain (N^-1 left to the conversion)
+    // out of place where the transform allows it: acc's P limbs stay in the NTT domain,
+    // so a pending key switch survives its own ModDown without a copy (moddown())
+    u64* Pc = nullptr;
+    if (!conv_fused && tail_keeps_acc()) {
+        Pc = alloc((size_t)n * 2 * K * N);
+        std::vector<const u64*> src((size_t)n * 2 * K);
+        for (int i = 0; i < n; ++i)
+            for (u32 c = 0; c < 2; ++c)
+                for (u32 k = 0; k < K; ++k) src[((size_t)i * 2 + c) * K + k] = acc[i] + ((size_t)c * R + L + k) * N;
+        NttJobs pj = jobs_contig(Pc, n * 2 * K, L, K);
+        pj.src = upload(src);
+        pj.unscaled = kLazyOut;  // k_moddown_conv: Shoup by phat_inv_n (N^-1 folded in)
+        ntt(false, pj);
+    } else if (!conv_fused) {  // P limbs back to the coefficient domain (N^-1 left to the conversion)
         NttJobs pj;
         std::vector<u64*> plimbs((size_t)n * 2 * K);
         for (int i = 0; i < n; ++i)
@@ -1730,7 +1754,8 @@ void Context::key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, c
         ntt_moddown_conv_fused(cx_, hp_.dev, n, dacc, dec, V, stream_);
         ++launches_;
     } else {
-        if (hp_.L == 3) k_moddown_conv<ShapeQ3><<<grid_of(N, n, 2), kThreads, 0, stream_>>>(cx_, n, dacc, dec, V); else k_moddown_conv<ShapeQ8><<<grid_of(N, n, 2), kThreads, 0, stream_>>>(cx_, n, dacc, dec, V); ++launches_;
+        if (hp_.L == 3) k_moddown_conv<ShapeQ3><<<grid_of(N, n, 2), kThreads, 0, stream_>>>(cx_, n, dacc, dec, V, Pc); else k_moddown_conv<ShapeQ8><<<grid_of(N, n, 2), kThreads, 0, stream_>>>(cx_, n, dacc, dec, V, Pc); ++launches_;
+        if (Pc) release(Pc);
     }
     if (ntt_finish_fusable(hp_.dev)) {
         ntt_finish_fused(cx_, hp_.dev, n, V, dacc, dadd, upload(vg), upload(vo), stream_);
@@ -1861,7 +1886,7 @@ void Context::moddown(int n, const u64* const* acc, u64* const* out) {
     for (int c0 = 0; c0 < n; c0 += chunk) {
         const int cn = std::min(chunk, n - c0);
         std::vector<u32> ones(cn, 1);
-        const bool in_place = !(ntt_conv_fusable(hp_.dev) && !ntt_fusable(hp_.dev, kFuseModDown));
+        const bool in_place = !tail_keeps_acc();
         if (in_place) {  // this key_switch_tail path inverse-transforms acc's P limbs in place: work on a copy
             u64* A = alloc((size_t)cn * ks_words());
             std::vector<const u64*> src(acc + c0, acc + c0 + cn);

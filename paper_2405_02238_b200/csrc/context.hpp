@@ -178,6 +178,7 @@ class Context {
     void scale_relin(int n, u64* T, u64* const* out);
     void key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, const u64* const* addn,
                          const u32* g, u64* const* out);
+    bool tail_keeps_acc() const;
     void inner_product(int n, const u64* const* digits, const u64* const* keys, const u32* g,
                        u64* const* acc, const u64* const* c0 = nullptr);
 
