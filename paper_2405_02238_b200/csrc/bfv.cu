@@ -606,6 +606,54 @@ __global__ void __launch_bounds__(kThreads, 6) k_q_to_b(DevCtx cx, u32 n, const 
     }
 }
 
+// The same with two adjacent coefficients per thread: 16-byte loads and stores,
+// and the conversion constants (uniform loads) and addressing shared by both.
+#ifndef HGM_QTOB_PAIR
+#define HGM_QTOB_PAIR 1
+#endif
+template <typename SH>
+__global__ void __launch_bounds__(kThreads, 4) k_q_to_b2(DevCtx cx, u32 n, const u64* X, u64* XB) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
+    const u32 N = dp->N, L = SH::L, K = SH::K, nB = SH::nB;
+    ITEM_LOOP {
+        const u32 p = blockIdx.z;
+        const ulonglong2* x = reinterpret_cast<const ulonglong2*>(X + ((size_t)item * 4 + p) * L * N);
+        ulonglong2* xb = reinterpret_cast<ulonglong2*>(XB + ((size_t)item * 4 + p) * nB * N);
+        const u32 N2 = N / 2;
+        for (u32 j = blockIdx.x * blockDim.x + threadIdx.x; j < N2; j += gridDim.x * blockDim.x) {
+            ulonglong2 xv[kMaxL];
+            for (u32 i = 0; i < L; ++i) xv[i] = x[(size_t)i * N2 + j];
+            u64 y0[kMaxL], y1[kMaxL];
+            Acc128 s0{0, 0}, s1{0, 0};
+            for (u32 i = 0; i < L; ++i) {
+                const u64 qi = dp->pr[i].q, hi = dp->qhat_inv_n[i], hs = dp->qhat_inv_n_sh[i];
+                const Frac f = dp->one_over_q[i];
+                y0[i] = shoup_mul(xv[i].x, hi, hs, qi);
+                y1[i] = shoup_mul(xv[i].y, hi, hs, qi);
+                fx_add_small(s0, y0[i], f);
+                fx_add_small(s1, y1[i], f);
+            }
+            const u64 v0 = fx_round(s0), v1 = fx_round(s1);
+            for (u32 k = 0; k < nB; ++k) {
+                Cols a0, a1;
+                for (u32 i = 0; i < L; ++i) {
+                    const Dig<SH::S> c = packed_dig<SH::S>(dp->qhat_mod_b_pk[i][k]);
+                    a0.mac(split<SH::S>(y0[i]), c);
+                    a1.mac(split<SH::S>(y1[i]), c);
+                }
+                const u64 nq = dp->neg_Q_mod_b[k];
+                a0.add<SH::S>(v0 * nq);
+                a1.add<SH::S>(v1 * nq);
+                const Prime& P = dp->pr[L + K + k];
+                ulonglong2 r;
+                r.x = reduce_acc(a0.fold<SH::S>(), P);
+                r.y = reduce_acc(a1.fold<SH::S>(), P);
+                xb[(size_t)k * N2 + j] = r;
+            }
+        }
+    }
+}
+
 // tensor over Q ++ B in the NTT domain; T: [n][3][L+nB][N]
 template <typename SH>
 __global__ void k_tensor(DevCtx cx, u32 n, const u64* const* A,
@@ -1822,7 +1870,12 @@ u64* Context::b_extend(int n, const u64* const* a, const u64* const* b) {
     }
     // 2. exact Q -> B and NTT over B
     u64* XB = alloc((size_t)n * 4 * nB * N);
-    if (hp_.L == 3) k_q_to_b<ShapeQ3><<<grid_of(N, n, 4), kThreads, 0, stream_>>>(cx_, n, X, XB); else k_q_to_b<ShapeQ8><<<grid_of(N, n, 4), kThreads, 0, stream_>>>(cx_, n, X, XB); ++launches_;
+    if (HGM_QTOB_PAIR && hp_.L == 3) {  // (ShapeQ8's pair kernel spills: parameter set 1 keeps one per thread)
+        k_q_to_b2<ShapeQ3><<<grid_of(N / 2, n, 4), kThreads, 0, stream_>>>(cx_, n, X, XB);
+    } else {
+        if (hp_.L == 3) k_q_to_b<ShapeQ3><<<grid_of(N, n, 4), kThreads, 0, stream_>>>(cx_, n, X, XB); else k_q_to_b<ShapeQ8><<<grid_of(N, n, 4), kThreads, 0, stream_>>>(cx_, n, X, XB);
+    }
+    ++launches_;
     release(X);
     ntt(true, jobs_contig(XB, n * 4 * nB, L + K, nB));
     return XB;
