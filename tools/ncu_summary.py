@@ -53,7 +53,7 @@ def main():
         res["algorithmic_bytes_per_limb"] = int(sys.argv[5]) if len(sys.argv) > 5 else 2 * 8 * 8192
     json.dump(res, open(out, "w"), indent=1)
     if limbs and len(sys.argv) > 4:
-        name = res["Kernel Name"].split("::")[-1].split("(")[0]
+        name = res["Kernel Name"].replace("void ", "").replace("unnamed>::", "").split("(")[0]
         def pct(k):
             try:
                 return round(float(val[col[k]].replace(",", "")) / 100.0, 4)
