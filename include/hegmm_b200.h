@@ -71,8 +71,11 @@ typedef struct hgm_ct hgm_ct;
  * Randomness.  Keys and encryption noise come from a counter-based generator
  * keyed by `seed` (splitmix64 finalisers, shared bit for bit with the CPU
  * oracle).  A caller-chosen seed is a TEST / PARITY mode: anyone who knows
- * the seed can regenerate the secret key.  HGM_CTX_OS_SEED draws the seed
- * from the OS CSPRNG instead and never exports it (hgm_ctx_info reports 0);
+ * the seed can regenerate the secret key (and since that generator is a public
+ * bijection chain, one sample such as a public key's uniform `a` gives the seed
+ * back).  HGM_CTX_OS_SEED sessions draw every key and noise sample from ChaCha12
+ * keyed with 256 bits from the OS CSPRNG instead, never exported (hgm_ctx_info
+ * reports seed 0);
  * for keys held outside the library, create the cloud context with
  * HGM_CTX_KEYLESS and upload them (hgm_key_upload), and encrypt with
  * host-sampled noise (hgm_encrypt_noise). */
@@ -314,6 +317,9 @@ long hgm_plan_info(int kind, size_t k, size_t a, size_t b, size_t c, int order, 
 
 /* Kernel-level timing hooks for bench.py (CUDA events on the library stream). */
 int hgm_bench_ntt(hgm_ctx* ctx, int forward, size_t limbs, int iters, float* ms_per_iter);
+/* Test hook (no GPU): the ChaCha block function of OS-seeded sessions (key 8
+ * words, 64-bit nonce and block counter, `rounds` rounds) into out[16]. */
+int hgm_test_chacha(const uint32_t* key, uint64_t nonce, uint64_t counter, int rounds, uint32_t* out);
 /* key-switch inner product (k_ks_inner) over `items` rotations, 8 per Galois key */
 int hgm_bench_keyswitch(hgm_ctx* ctx, size_t items, int iters, float* ms_per_iter);
 int hgm_device_sync(hgm_ctx* ctx);

@@ -58,6 +58,7 @@ EXPORTS = (
     "hgm_decrypt_products", "hgm_comm_unique_id", "hgm_comm_init", "hgm_comm_init_file", "hgm_comm_destroy",
     "hgm_comm_rank", "hgm_comm_size", "hgm_comm_barrier", "hgm_comm_max", "hgm_comm_gather",
     "hgm_comm_gather_batch", "hgm_comm_buffer_free", "hgm_bench_keyswitch", "hgm_blocked_mm_ex",
+    "hgm_test_chacha",
 )
 CTX_KEYLESS, CTX_OS_SEED = 1, 2
 COUNTER_AUTO = (1 << 64) - 1
@@ -74,6 +75,14 @@ def plan_info(kind: int, k: int, a: int, b: int, c: int, order: int, segment: in
     if cnt < 0:
         _check(-cnt)
     return off[:cnt].tolist(), w[:cnt].astype(int).tolist()
+
+
+def chacha_block(key, nonce: int, counter: int, rounds: int = 20) -> np.ndarray:
+    """The ChaCha block function OS-seeded sessions sample from (test hook, CPU)."""
+    k = np.ascontiguousarray(key, dtype=np.uint32)
+    out = np.zeros(16, dtype=np.uint32)
+    _check(lib().hgm_test_chacha(_ptr(k), nonce, counter, rounds, _ptr(out)))
+    return out
 
 
 def program_info(algo: int, m: int, l: int, n: int, slots: int = 4096, N: int = 8192, order: int = -1,
@@ -295,6 +304,7 @@ def lib() -> ctypes.CDLL:
         "hgm_bench_ntt": (_int, [_vp, _int, _sz, _int, _vp]),
         "hgm_device_sync": (_int, [_vp]),
         "hgm_bench_keyswitch": (_int, [_vp, _sz, _int, _vp]),
+        "hgm_test_chacha": (_int, [_vp, _u64, _u64, _int, _vp]),
         "hgm_test_ntt": (_int, [_vp, _int, _int, _vp, _sz]),
         "hgm_launch_count": (_u64, [_vp]),
         "hgm_batch_encrypt": (_int, [_vp, _int, _int, _int, _sz, _sz, _sz, _sz, _vp, _vp, _u64, _vp]),

@@ -107,15 +107,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_enc_lift(DevCtx cx, u32 n, cons
                            const i64* noise, u64* U, u64* const* out) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = SH::L;
-    const u64 seed = cx.seed;
     ITEM_LOOP {
         const u64 c = noise ? 0 : ctr[item];
         const i64* nz = noise ? noise + (size_t)item * 3 * N : nullptr;
         u64* o = out[item];
         COEF_LOOP {
-            const i64 u = nz ? nz[j] : ternary(seed, kStreamEncU | c, j);
-            const i64 e0 = nz ? nz[N + j] : gauss(seed, kStreamEncE0 | c, j, cx.cdt);
-            const i64 e1 = nz ? nz[2 * N + j] : gauss(seed, kStreamEncE1 | c, j, cx.cdt);
+            const i64 u = nz ? nz[j] : ternary(cx, kStreamEncU | c, j);
+            const i64 e0 = nz ? nz[N + j] : gauss(cx, kStreamEncE0 | c, j, cx.cdt);
+            const i64 e1 = nz ? nz[2 * N + j] : gauss(cx, kStreamEncE1 | c, j, cx.cdt);
             const u64 mj = m[(size_t)item * N + j];
             for (u32 i = 0; i < L; ++i) {
                 const u64 q = dp->pr[i].q;
@@ -904,7 +903,7 @@ __global__ void k_keygen_sk(DevCtx cx, u64* S) {
     const u32 n = 1;
     ITEM_LOOP {
         COEF_LOOP {
-            const i64 s = ternary(cx.seed, kStreamSk, j);
+            const i64 s = ternary(cx, kStreamSk, j);
             for (u32 r = 0; r < R; ++r) S[(size_t)r * N + j] = small_to_mod(s, dp->pr[r].q);
         }
     }
@@ -917,7 +916,7 @@ __global__ void k_keygen_err(DevCtx cx, u64 stream, u32 limbs, u64* E) {
     const u32 n = 1;
     ITEM_LOOP {
         COEF_LOOP {
-            const i64 e = gauss(cx.seed, stream, j, cx.cdt);
+            const i64 e = gauss(cx, stream, j, cx.cdt);
             for (u32 r = 0; r < limbs; ++r) E[(size_t)r * N + j] = small_to_mod(e, dp->pr[r].q);
         }
     }
@@ -932,7 +931,7 @@ __global__ void k_keygen_pk(DevCtx cx, const u64* S, const u64* E, u64* pk) {
         COEF_LOOP {
             for (u32 i = 0; i < L; ++i) {
                 const Prime& P = dp->pr[i];
-                const u64 a = uniform(cx.seed, kStreamPkA, (u64)i * N + j, P.q);
+                const u64 a = uniform(cx, kStreamPkA, (u64)i * N + j, P.q);
                 pk[(size_t)i * N + j] = sub_mod(E[(size_t)i * N + j], mul_mod(a, S[(size_t)i * N + j], P), P.q);
                 pk[(size_t)(L + i) * N + j] = a;
             }
@@ -954,7 +953,7 @@ __global__ void k_keygen_ks(DevCtx cx, u32 kid, u32 g, const u64* S,
         for (u32 r = 0; r < R; ++r) {
             const Prime& P = dp->pr[r];
             const u64 sr = S[(size_t)r * N + j];
-            const u64 a = uniform(cx.seed, kStreamKsA | ((u64)kid << 8) | dg, (u64)r * N + j, P.q);
+            const u64 a = uniform(cx, kStreamKsA | ((u64)kid << 8) | dg, (u64)r * N + j, P.q);
             u64 v = sub_mod(E[((size_t)dg * R + r) * N + j], mul_mod(a, sr, P), P.q);
             if (r < L && r / A == dg) {
                 const u64 sp = kid == 0 ? mul_mod(sr, sr, P) : S[(size_t)r * N + src];
@@ -1053,7 +1052,8 @@ struct DeviceScope {
 };
 }  // namespace
 
-Context::Context(int param_id, u64 seed, int device, bool keyless) : device_(device), keyless_(keyless) {
+Context::Context(int param_id, u64 seed, int device, bool keyless, const u32* csprng_key)
+    : device_(device), keyless_(keyless) {
     hp_ = make_params(param_id, seed);
     // all primes of one set share their bit length (centred_lift relies on it)
     for (size_t r = 1; r < hp_.primes.size(); ++r)
@@ -1088,6 +1088,10 @@ Context::Context(int param_id, u64 seed, int device, bool keyless) : device_(dev
     cx_.cdt = d_cdt_;
     cx_.seed = seed;
     cx_.pid = (u32)param_id;
+    if (csprng_key) {
+        cx_.csprng = 1;
+        for (int i = 0; i < 8; ++i) cx_.ck[i] = csprng_key[i];
+    }
     if (!keyless_) build_keys();
 }
 

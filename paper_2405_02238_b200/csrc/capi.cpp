@@ -309,14 +309,21 @@ hgm_ctx* hgm_ctx_create_ex(int param_id, uint64_t seed, int device, int flags) {
         if (device < 0) throw std::invalid_argument("negative device ordinal");
         auto h = std::make_unique<hgm_ctx>();
         h->device = device;
-        if (flags & HGM_CTX_OS_SEED) {
+        u32 key[8];
+        if (flags & HGM_CTX_OS_SEED) {  // ChaCha12 keyed from the OS CSPRNG (never exported)
             h->os_seed = true;
-            seed = os_random_u64();
+            seed = os_random_u64();  // only the wire format's key-set fingerprint uses it
+            for (int i = 0; i < 4; ++i) {
+                const u64 v = os_random_u64();
+                key[2 * i] = (u32)v;
+                key[2 * i + 1] = (u32)(v >> 32);
+            }
         }
         int prev = -1;
         if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
         try {
-            h->ctx = std::make_unique<Context>(param_id, seed, device, (flags & HGM_CTX_KEYLESS) != 0);
+            h->ctx = std::make_unique<Context>(param_id, seed, device, (flags & HGM_CTX_KEYLESS) != 0,
+                                               h->os_seed ? key : nullptr);
         } catch (...) {
             if (prev >= 0) cudaSetDevice(prev);
             throw;
@@ -1490,6 +1497,13 @@ int hgm_bench_ntt(hgm_ctx* c, int forward, size_t limbs, int iters, float* ms) {
         cudaEventDestroy(e1);
         ctx.release(buf);
         ctx.sync();
+    });
+}
+
+int hgm_test_chacha(const uint32_t* key, uint64_t nonce, uint64_t counter, int rounds, uint32_t* out) {
+    return guarded([&] {
+        if (!key || !out || rounds <= 0 || rounds % 2) throw std::invalid_argument("bad ChaCha test arguments");
+        chacha_block(key, nonce, counter, rounds, out);
     });
 }
 

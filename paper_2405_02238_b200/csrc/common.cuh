@@ -100,6 +100,8 @@ struct DevCtx {
     const u64* cdt;       // Gaussian CDT
     u64 seed;
     u32 pid;              // parameter-set slot in c_dp
+    u32 csprng;           // 1: keys and noise from ChaCha (OS-seeded sessions), 0: the parity PRF
+    u32 ck[8];            // ChaCha key (256 bits from the OS CSPRNG), csprng == 1
 };
 
 // ------------------------------------------------------------------ scalar ops
@@ -395,10 +397,46 @@ HD u64 prng(u64 seed, u64 stream, u64 idx) {
     h = mix64(h ^ stream);
     return mix64(h + (idx + 1) * 0x9e3779b97f4a7c15ULL);
 }
-HD i64 ternary(u64 seed, u64 stream, u64 idx) { return (i64)mulhi64(prng(seed, stream, idx), 3) - 1; }
-HD u64 uniform(u64 seed, u64 stream, u64 idx, u64 q) { return mulhi64(prng(seed, stream, idx), q); }
-HD i64 gauss(u64 seed, u64 stream, u64 idx, const u64* cdt) {
-    u64 r = prng(seed, stream, idx);
+// ChaCha block function (Bernstein's original layout: 64-bit block counter,
+// 64-bit nonce), `rounds` rounds.  OS-seeded sessions draw every secret-key,
+// key-switching and encryption sample from ChaCha12(key, nonce = stream,
+// counter = index): the parity PRF above is a public bijection chain, so one
+// output (e.g. a public key's uniform `a`) would give back its 64-bit seed.
+HD u32 rotl32(u32 x, int r) { return (x << r) | (x >> (32 - r)); }
+#define HGM_QR(a, b, c, d) \
+    a += b; d = rotl32(d ^ a, 16); c += d; b = rotl32(b ^ c, 12); \
+    a += b; d = rotl32(d ^ a, 8);  c += d; b = rotl32(b ^ c, 7);
+HD void chacha_block(const u32 key[8], u64 nonce, u64 counter, int rounds, u32 out[16]) {
+    u32 x[16] = {0x61707865u, 0x3320646eu, 0x79622d32u, 0x6b206574u,
+                 key[0], key[1], key[2], key[3], key[4], key[5], key[6], key[7],
+                 (u32)counter, (u32)(counter >> 32), (u32)nonce, (u32)(nonce >> 32)};
+    u32 in[16];
+    for (int i = 0; i < 16; ++i) in[i] = x[i];
+    for (int r = 0; r < rounds; r += 2) {
+        HGM_QR(x[0], x[4], x[8], x[12]) HGM_QR(x[1], x[5], x[9], x[13])
+        HGM_QR(x[2], x[6], x[10], x[14]) HGM_QR(x[3], x[7], x[11], x[15])
+        HGM_QR(x[0], x[5], x[10], x[15]) HGM_QR(x[1], x[6], x[11], x[12])
+        HGM_QR(x[2], x[7], x[8], x[13]) HGM_QR(x[3], x[4], x[9], x[14])
+    }
+    for (int i = 0; i < 16; ++i) out[i] = x[i] + in[i];
+}
+#undef HGM_QR
+constexpr int kChachaRounds = 12;
+// one 64-bit sample of (stream, idx): the first two words of its block
+HD u64 chacha_u64(const u32 key[8], u64 stream, u64 idx) {
+    u32 b[16];
+    chacha_block(key, stream, idx, kChachaRounds, b);
+    return (u64)b[0] | ((u64)b[1] << 32);
+}
+// the session's sampler: ChaCha for OS-seeded sessions, the parity PRF (shared
+// bit for bit with the CPU oracle) for caller-seeded ones
+HD u64 draw(const DevCtx& cx, u64 stream, u64 idx) {
+    return cx.csprng ? chacha_u64(cx.ck, stream, idx) : prng(cx.seed, stream, idx);
+}
+HD i64 ternary(const DevCtx& cx, u64 stream, u64 idx) { return (i64)mulhi64(draw(cx, stream, idx), 3) - 1; }
+HD u64 uniform(const DevCtx& cx, u64 stream, u64 idx, u64 q) { return mulhi64(draw(cx, stream, idx), q); }
+HD i64 gauss(const DevCtx& cx, u64 stream, u64 idx, const u64* cdt) {
+    u64 r = draw(cx, stream, idx);
     u64 mag = r & 0x7fffffffffffffffULL;
     i64 k = 0;
     while (mag >= cdt[k]) ++k;

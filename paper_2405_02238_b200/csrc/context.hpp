@@ -60,7 +60,9 @@ class Context {
   public:
     // keyless: no secret, public or switching keys are generated; they must be
     // uploaded (upload_key) before the operations that need them
-    Context(int param_id, u64 seed, int device, bool keyless = false);
+    // csprng_key (optional, 8 words from the OS CSPRNG): keys and noise from ChaCha12
+    // instead of the seeded parity PRF (HGM_CTX_OS_SEED sessions)
+    Context(int param_id, u64 seed, int device, bool keyless = false, const u32* csprng_key = nullptr);
     ~Context();
     Context(const Context&) = delete;
     Context& operator=(const Context&) = delete;

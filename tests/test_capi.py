@@ -55,3 +55,17 @@ def test_nccl_unique_id_without_gpu():
     """The communicator bootstrap id is produced by the library (NCCL, no torch)."""
     a, b = hb.Comm.unique_id(), hb.Comm.unique_id()
     assert len(a) == 128 and a != b
+
+
+def test_chacha20_known_answer():
+    """The OS-seeded sampler's block function: ChaCha20 with an all-zero key,
+    nonce and counter gives the published keystream 76 b8 e0 ad a0 f1 3d 90 ..."""
+    import numpy as np
+
+    out = hb.chacha_block(np.zeros(8, dtype=np.uint32), 0, 0, 20)
+    stream = out.astype("<u4").tobytes()
+    assert stream[:16].hex() == "76b8e0ada0f13d90405d6ae55386bd28"
+    assert stream[16:32].hex() == "bdd219b8a08ded1aa836efcc8b770dc7"
+    # block 1 differs, 12 rounds differ from 20
+    assert not np.array_equal(hb.chacha_block(np.zeros(8, np.uint32), 0, 1, 20), out)
+    assert not np.array_equal(hb.chacha_block(np.zeros(8, np.uint32), 0, 0, 12), out)

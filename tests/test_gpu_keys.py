@@ -207,3 +207,38 @@ def test_flush_materialises_pinned_pending_values(gpu_factory, oracle_factory):
     assert g.launch_count() == n1, "export recomputed a flushed value"
     assert np.array_equal(w, o.rot(o.encrypt(a, 50), 3))
     g.close()
+
+
+def test_os_seeded_sessions_sample_from_chacha():
+    """HGM_CTX_OS_SEED: keys and noise come from ChaCha12 keyed by the OS CSPRNG.
+    Two sessions get independent keys, neither equals the parity PRF's keys for
+    any small seed, the seed is not exported, and products stay exact."""
+    import numpy as np
+
+    import paper_2405_02238_b200 as hb
+    from paper_2405_02238_b200.workload import batch
+
+    a = hb.Context(2, 0, 0, flags=hb.CTX_OS_SEED)
+    b = hb.Context(2, 0, 0, flags=hb.CTX_OS_SEED)
+    try:
+        info = np.zeros(64, dtype=np.uint64)
+        hb._check(hb.lib().hgm_ctx_info(a._h, hb._ptr(info), 64))
+        assert int(info[7]) == 0  # the seed is never exported
+        pa, pb = a.export_key(hb.KEY_PUBLIC), b.export_key(hb.KEY_PUBLIC)
+        assert not np.array_equal(pa, pb)
+        for seed in (0, 1):  # not the splitmix parity keys of the seeds a caller might guess
+            ref = hb.Context(2, seed, 0)
+            try:
+                assert not np.array_equal(ref.export_key(hb.KEY_PUBLIC), pa)
+            finally:
+                ref.close()
+        A, B = batch(3, 0, 4, 8, 16, 4, -8, 7)
+        C, _ = a.matmul_batch(A, B, algo=1)
+        assert np.array_equal(C, np.einsum("kij,kjl->kil", A, B) % 65537)
+        v = np.arange(-20, 20)
+        ct1, ct2 = a.encrypt(v), a.encrypt(v)
+        assert not np.array_equal(a.export(ct1), a.export(ct2))  # fresh noise per encryption
+        assert np.array_equal(a.decrypt(ct1), v % 65537)
+    finally:
+        a.close()
+        b.close()
