@@ -1146,11 +1146,13 @@ __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_inv_io(DevCtx cx
 // ModDown conversion fused behind the INTT of acc's P limb (K = 1, so P/p = 1):
 // job = (item, component c);  V[item][c][i] = ecoef[c][i] - P^-1 centred(N^-1 * INTT_p)
 // -- k_moddown_conv's output, from the unscaled INTT (N^-1 folded into phat_inv_n).
+template <u32 kL>  // the Q limb count, compile-time so the conversion loop unrolls
 struct MdConvIO {
+    static constexpr u32 L = kL;
     u64* const* acc;           // per item [2][R][N]; the P limb in the NTT domain
     const u64* const* ecoef;   // per item [2][L][N] coefficient-domain addend, or null
     u64* V;                    // [n][2][L][N]
-    u32 L, R, N;
+    u32 R, N;
     __device__ int prime(u32) const { return (int)L; }
     __device__ void prefetch(u32 job) const {
         pf_l2(acc[job >> 1] + ((size_t)(job & 1) * R + L) * N, N * 8);
@@ -1171,6 +1173,7 @@ struct MdConvIO {
         // in [0, 4q) (the lazy product is never 0 for 0 < z < q_i) -- the same
         // canonical residue as reducing the centred lift first.
         const u64 h0 = z0 > (p - 1) / 2, h1 = z1 > (p - 1) / 2;
+#pragma unroll
         for (u32 i = 0; i < L; ++i) {
             const u64 q = dp->pr[i].q, pi = dp->P_inv_q[i], pis = dp->P_inv_q_sh[i];
             const u64 q2 = q << 1, q3 = 3 * q;
@@ -1532,12 +1535,13 @@ bool ntt_conv_fusable(const DevParams& hp) {
         const char* e = std::getenv("HGM_FUSED_CONV");
         return !e || e[0] != '0';
     }();
-    return on && hp.logN <= 13 && hp.K == 1;
+    return on && hp.logN <= 13 && hp.K == 1 && hp.L == 3;
 }
 
 void ntt_moddown_conv_fused(const DevCtx& cx, const DevParams& hp, int n, u64* const* acc, const u64* const* ecoef,
                             u64* V, cudaStream_t s) {
-    MdConvIO io{acc, ecoef, V, hp.L, hp.R, hp.N};
+    if (hp.L != 3) throw std::logic_error("the fused ModDown conversion is built for 3 ciphertext primes");
+    MdConvIO<3> io{acc, ecoef, V, hp.R, hp.N};
     launch_inv_io(cx, hp, io, (u32)n * 2, s);
 }
 
