@@ -438,7 +438,11 @@ __device__ __forceinline__ void store_last_stage(const u64* sm, u64* g, const ul
     constexpr int NB = 1 << LB, T = NB / E;
     ulonglong2* g2 = reinterpret_cast<ulonglong2*>(g);
     const int tw0 = (1 << (logN - 1)) + (blk << (LB - 1));
-#pragma unroll 4
+#ifndef HGM_LAST_UNROLL
+#define HGM_LAST_UNROLL 8
+#endif
+    constexpr int kLastUnroll = HGM_LAST_UNROLL;
+#pragma unroll kLastUnroll
     for (int i = threadIdx.x; i < NB / 2; i += T) {
         const ulonglong2 t = __ldg(tw_tab + tw0 + i);
         const u64 w = t.x, ws = t.y;
