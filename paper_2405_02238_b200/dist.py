@@ -58,6 +58,11 @@ def comm_from_env(ctx) -> Optional["object"]:
     rank, world, _ = env_rank()
     if world <= 1:
         return None
+    # NCCL's own init lines (ranks, transports) for the launcher's logs, on stderr so
+    # that rank 0's stdout stays one JSON line; NCCL is bound lazily, after this
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     return hb.Comm(ctx, rank, world, id_file=id_file_path())
 
 
