@@ -506,6 +506,105 @@ __global__ void k_ks_inner(DevCtx cx, u32 n, const u64* const* D,
     }
 }
 
+// Masked key of one term of a masked sum of rotations:
+//   mk[dg][c][r][j] = key_g[dg][c][r][j] * m[r][j] mod q_r     (packed digits)
+//   mp[r][j]        = (P mod q_r) * m[r][j] mod q_r, r < L     (packed digits)
+// with m = the sum mod q_r of the term's NTT-domain mask lifts (several masks
+// on one rotation add up: a x m1 + a x m2 = a x (m1 + m2) mod q).  Since
+// mask (.) (sum_dg D_dg key_dg + P phi(c0)) = sum_dg D_dg (mask (.) key_dg) + phi(c0) (mask P),
+// k_ks_plan computes a whole masked sum of rotations as one longer inner
+// product, with neither the rotations' accumulators nor a separate masked sum.
+template <typename SH>
+__global__ void k_mask_key(DevCtx cx, const u64* key, const u64* const* masks, u32 n_masks, u64* out) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
+    const u32 N = dp->N, R = SH::R, L = SH::L, dnum = SH::dnum;
+    auto unpack = [](u64 p) { return (u64)(u32)p + ((p >> 32) << SH::S); };
+    auto pack = [](u64 v) {
+        const Dig<SH::S> d = split<SH::S>(v);
+        return (u64)d.l | ((u64)d.h << 32);
+    };
+    for (u32 w = blockIdx.x * blockDim.x + threadIdx.x; w < R * N; w += gridDim.x * blockDim.x) {
+        const u32 r = w / N, j = w - r * N;
+        const Prime& P = dp->pr[r];
+        u64 m = 0;
+        for (u32 i = 0; i < n_masks; ++i) m = add_mod(m, unpack(masks[i][w]), P.q);
+        for (u32 dg = 0; dg < dnum; ++dg)
+            for (u32 c = 0; c < 2; ++c) {
+                const size_t o = (((size_t)dg * 2 + c) * R + r) * N + j;
+                out[o] = pack(mul_mod(unpack(key[o]), m, P));
+            }
+        if (r < L) out[(size_t)dnum * 2 * R * N + w] = pack(mul_mod(dp->P_mod_q[r], m, P));
+    }
+}
+
+// out[c][r][j] = sum_t ( sum_dg D_t[dg][r][src_t(j)] mk_t[dg][c][r][j]
+//                        + [c = 0, r < L] c0_t[r][src_t(j)] mp_t[r][j] )   over Q ++ P
+// = sum_t mask_t (.) RotAcc(ct_t, g_t): the value k_ks_inner + k_lincomb_masked
+// produce, bit for bit (canonical residues of the same sum mod q_r).
+// A group is up to kKeyReuse instances of one sum: each masked-key element is
+// read once per group.  Terms are taken one at a time with the running residues
+// of the group's instances in registers (4 products + a residue stay inside the
+// 128-bit column sum: 4 q^2 + q < 2^(s+62) for every prime of the sets).
+template <typename SH>
+__global__ void __launch_bounds__(kThreads, 2) k_ks_plan(DevCtx cx, u32 n_groups, const PlanGroup* groups,
+                                                         const u64* const* mkey, const u32* g,
+                                                         const u64* const* D, const u64* const* c0,
+                                                         u64* const* out) {
+    const DevParams* __restrict__ dp = &c_dp[cx.pid];
+    const u32 N = dp->N, R = SH::R, dnum = SH::dnum, logN = dp->logN;
+    for (u32 grp = blockIdx.y; grp < n_groups; grp += gridDim.y) {
+        const PlanGroup G = groups[grp];
+        COEF_LOOP {
+            for (u32 r = 0; r < R; ++r) {
+                const Prime& P = dp->pr[r];
+                u64 r0[kKeyReuse], r1[kKeyReuse];
+#pragma unroll
+                for (u32 u = 0; u < (u32)kKeyReuse; ++u) r0[u] = r1[u] = 0;
+                for (u32 t = 0; t < G.nterms; ++t) {
+                    const u64* k = mkey[G.term0 + t];
+                    const u32 ge = g[G.term0 + t];
+                    const u32 src = ge == 1 ? j : galois_src(j, ge, logN);
+                    u64 k0[SH::dnum], k1[SH::dnum];
+#pragma unroll
+                    for (u32 dg = 0; dg < dnum; ++dg) {
+                        k0[dg] = __ldg(k + (((size_t)dg * 2 + 0) * R + r) * N + j);
+                        k1[dg] = __ldg(k + (((size_t)dg * 2 + 1) * R + r) * N + j);
+                    }
+                    const u64 pm = r < SH::L ? __ldg(k + ((size_t)dnum * 2 * R + r) * N + j) : 0;
+                    const u64* const* Dt = D + G.dbase + t;
+                    const u64* const* Ct = c0 + G.dbase + t;
+#pragma unroll
+                    for (u32 u = 0; u < (u32)kKeyReuse; ++u) {
+                        if (u < G.cnt) {
+                            const u64* d = Dt[(size_t)u * G.nterms];
+                            Cols a0, a1;
+                            a0.x = r0[u];
+                            a1.x = r1[u];
+#pragma unroll
+                            for (u32 dg = 0; dg < dnum; ++dg) {
+                                const Dig<SH::S> x = split<SH::S>(d[((size_t)dg * R + r) * N + src]);
+                                a0.mac(x, packed_dig<SH::S>(k0[dg]));
+                                a1.mac(x, packed_dig<SH::S>(k1[dg]));
+                            }
+                            if (r < SH::L)
+                                a0.mac(split<SH::S>(Ct[(size_t)u * G.nterms][(size_t)r * N + src]), packed_dig<SH::S>(pm));
+                            r0[u] = reduce_acc(a0.fold<SH::S>(), P);
+                            r1[u] = reduce_acc(a1.fold<SH::S>(), P);
+                        }
+                    }
+                }
+#pragma unroll
+                for (u32 u = 0; u < (u32)kKeyReuse; ++u)
+                    if (u < G.cnt) {
+                        u64* a = out[G.item0 + u];
+                        a[(size_t)r * N + j] = r0[u];
+                        a[((size_t)R + r) * N + j] = r1[u];
+                    }
+            }
+        }
+    }
+}
+
 // ModDown correction: V[c][i] = sum_k centred([w_k (P/p_k)^-1]_{p_k}) (P/p_k) mod q_i
 // V[c][i] = ecoef[c][i] - P^-1 conv[c][i]  (coefficient domain; ecoef optional)
 // so that NTT(V) + P^-1 acc = (acc - NTT(conv)) P^-1 + NTT(ecoef) exactly (the NTT
@@ -1101,6 +1200,7 @@ Context::~Context() {
     for (auto& kv : keys_) cudaFree(kv.second);
     for (auto& kv : masks_)
         for (auto& e : kv.second) cudaFreeAsync(e.dev, stream_);
+    for (auto& kv : mkeys_) cudaFreeAsync(kv.second.dev, stream_);
     cudaStreamSynchronize(stream_);
     cudaFree(d_sk_);
     cudaFree(d_pk_);
@@ -1244,6 +1344,7 @@ void Context::upload_key(int kind, u32 elt, const u64* host, size_t words) {
         if (it != keys_.end()) old = it->second;
         keys_[elt] = dst;
     }
+    if (kind == 2 && old) drop_masked_keys();  // masked keys derive from the replaced key
     if (old) HGM_CUDA(cudaFree(old));
 }
 
@@ -1935,6 +2036,88 @@ void Context::rotate_acc(int n, const u64* const* modup, const u64* const* ct, c
         for (int i = 0; i < cn; ++i) keys[i] = ks_key(g[c0 + i]);
         inner_product(cn, modup + c0, keys.data(), g + c0, acc + c0, ct + c0);
     }
+}
+
+size_t Context::masked_key_budget() const {
+    static const size_t env = [] {
+        const char* e = std::getenv("HGM_MASKED_KEY_MB");
+        return e ? (size_t)std::atoll(e) << 20 : (size_t)0;
+    }();
+    if (env) return env;
+    return 2 * mask_budget();  // min(16 GB, an eighth of the device)
+}
+
+void Context::drop_masked_keys() {
+    std::lock_guard<std::mutex> lk(mask_mu_);
+    for (auto& kv : mkeys_) HGM_CUDA(cudaFreeAsync(kv.second.dev, stream_));
+    mkeys_.clear();
+}
+
+void Context::trim_masked_keys(size_t needed) {
+    std::lock_guard<std::mutex> lk(mask_mu_);
+    const size_t each = masked_key_words() * 8, budget = masked_key_budget();
+    if ((mkeys_.size() + needed) * each <= budget) return;
+    // least recently used first, down to half the budget (or room for `needed`)
+    std::vector<std::pair<u64, const std::vector<u64>*>> all;
+    for (auto& kv : mkeys_) all.push_back({kv.second.tick, &kv.first});
+    std::sort(all.begin(), all.end());
+    const size_t keep = std::min(budget / 2, budget - std::min(budget, needed * each)) / each;
+    std::vector<std::vector<u64>> victims;
+    for (size_t i = 0; i < all.size() && mkeys_.size() - victims.size() > keep; ++i) victims.push_back(*all[i].second);
+    for (auto& v : victims) {
+        auto it = mkeys_.find(v);
+        HGM_CUDA(cudaFreeAsync(it->second.dev, stream_));
+        mkeys_.erase(it);
+    }
+}
+
+const u64* Context::masked_key(u32 g, const std::vector<u64>& ids, const std::vector<const u64*>* mask_dev) {
+    std::vector<u64> id(ids);
+    std::sort(id.begin(), id.end());
+    id.insert(id.begin(), (u64)g);
+    {
+        std::lock_guard<std::mutex> lk(mask_mu_);
+        auto it = mkeys_.find(id);
+        if (it != mkeys_.end()) {
+            it->second.tick = ++mask_tick_;
+            return it->second.dev;
+        }
+        if (!mask_dev || (mkeys_.size() + 1) * masked_key_words() * 8 > masked_key_budget()) return nullptr;
+    }
+    const u64* key = ks_key(g);
+    u64* out = nullptr;
+    HGM_CUDA(cudaMallocAsync((void**)&out, masked_key_words() * 8, stream_));
+    const u64* const* dm = upload(*mask_dev);
+    const u32 words = hp_.R * hp_.N;
+    const dim3 grid((words + kThreads - 1) / kThreads);
+    if (hp_.L == 3)
+        k_mask_key<ShapeQ3><<<grid, kThreads, 0, stream_>>>(cx_, key, dm, (u32)mask_dev->size(), out);
+    else
+        k_mask_key<ShapeQ8><<<grid, kThreads, 0, stream_>>>(cx_, key, dm, (u32)mask_dev->size(), out);
+    ++launches_;
+    HGM_CUDA(cudaGetLastError());
+    std::lock_guard<std::mutex> lk(mask_mu_);
+    mkeys_.emplace(std::move(id), MaskedKey{out, ++mask_tick_});
+    return out;
+}
+
+void Context::rotate_plan(const std::vector<PlanGroup>& groups, const std::vector<const u64*>& mkey,
+                          const std::vector<u32>& g, const std::vector<const u64*>& digits,
+                          const std::vector<const u64*>& c0, const std::vector<u64*>& out) {
+    if (groups.empty()) return;
+    const u64* const* dk = upload(mkey);
+    const u32* dg = upload(g);
+    const u64* const* dd = upload(digits);
+    const u64* const* dc = upload(c0);
+    u64* const* dout = upload(out);
+    const PlanGroup* dgrp = upload(groups);
+    const u32 n = (u32)groups.size();
+    if (hp_.L == 3)
+        k_ks_plan<ShapeQ3><<<grid_of(hp_.N, n), kThreads, 0, stream_>>>(cx_, n, dgrp, dk, dg, dd, dc, dout);
+    else
+        k_ks_plan<ShapeQ8><<<grid_of(hp_.N, n), kThreads, 0, stream_>>>(cx_, n, dgrp, dk, dg, dd, dc, dout);
+    ++launches_;
+    HGM_CUDA(cudaGetLastError());
 }
 
 void Context::moddown(int n, const u64* const* acc, u64* const* out) {

@@ -1190,7 +1190,10 @@ namespace {
 
 size_t lockstep_chunk(Context& ctx, const MatmulProgram& prog) {
     const size_t W = ctx.ct_words();
-    const size_t per_inst = (prog.cloud_sched.rot_count * ctx.ks_words() + (prog.cloud_sched.comb_count / 2 + 8) * W +
+    // stored rotation accumulators; sums computed straight from the ModUp digits
+    // (Schedule::ks_terms) store their own accumulator instead
+    const size_t accs = prog.cloud_sched.stored_rot_count + prog.cloud_sched.ks_comb_count;
+    const size_t per_inst = (accs * ctx.ks_words() + (prog.cloud_sched.comb_count / 2 + 8) * W +
                              prog.cloud_sched.pending_count * ctx.pending_words()) * 8;
     size_t free_b = 0, total_b = 0;
     HGM_CUDA(cudaMemGetInfo(&free_b, &total_b));

@@ -11,6 +11,7 @@
 
 #include <atomic>
 #include <list>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -54,6 +55,14 @@ class PinnedRing {
     };
     std::vector<Mark> marks_;
     std::vector<cudaEvent_t> free_events_;
+};
+
+// One group of k_ks_plan (a masked sum of rotations computed straight from the
+// ModUp digits): up to 8 lockstep instances of one sum, sharing its masked keys.
+struct PlanGroup {
+    u32 item0, cnt;     // outputs item0 .. item0 + cnt - 1
+    u32 term0, nterms;  // masked keys / Galois elements term0 .. term0 + nterms - 1
+    u32 dbase, pad;     // digits / c0 of instance u, term t at dbase + u * nterms + t
 };
 
 class Context {
@@ -146,6 +155,23 @@ class Context {
     void rotate_acc(int n, const u64* const* modup, const u64* const* ct, const u32* g, u64* const* acc);
     // out = ModDown(acc) (acc is left intact)
     void moddown(int n, const u64* const* acc, u64* const* out);
+    // Masked sums of rotations straight from the ModUp digits (k_ks_plan).
+    // masked_key: key_g (.) (sum of the masks) over Q ++ P followed by (P mod q) (.)
+    // (that sum) over Q, packed digits, cached per (g, mask ids) -- the ids are the
+    // stable ids of cached programs' masks, mask_dev their device lifts
+    // (mask_plain; null = look up only); nullptr when absent / the cache budget
+    // cannot take another entry.
+    size_t masked_key_words() const { return ((size_t)hp_.dnum * 2 * hp_.R + hp_.L) * hp_.N; }
+    const u64* masked_key(u32 g, const std::vector<u64>& ids, const std::vector<const u64*>* mask_dev);
+    size_t masked_key_budget() const;
+    bool masked_keys_fit(size_t count) const { return count * masked_key_words() * 8 <= masked_key_budget(); }
+    void trim_masked_keys(size_t needed);  // between programs: room for `needed` more entries
+    void drop_masked_keys();               // keys changed
+    // out[i] = sum over the terms of i's group of mask (.) RotAcc: mkey / g per
+    // term, digits / c0 per (instance, term) as PlanGroup lays them out
+    void rotate_plan(const std::vector<PlanGroup>& groups, const std::vector<const u64*>& mkey,
+                     const std::vector<u32>& g, const std::vector<const u64*>& digits,
+                     const std::vector<const u64*>& c0, const std::vector<u64*>& out);
     // lincomb over pending key switches ([2][R][N] inputs, masks over Q ++ P)
     void lincomb_qp(int n_out, const u32* off, const u64* const* in, const u64* const* mask, u64* const* out);
     // Pending products (oracle XCt): a pending value is [T: 3 (L+nB) N][addend: 2 L N],
@@ -212,6 +238,11 @@ class Context {
     };
     std::unordered_map<u64, std::list<MaskEntry>> masks_;
     std::unordered_map<u64, MaskEntry*> masks_by_id_;  // stable MaskData ids
+    struct MaskedKey {
+        u64* dev;
+        u64 tick;
+    };
+    std::map<std::vector<u64>, MaskedKey> mkeys_;  // {g, sorted mask ids} -> masked key
     u64 mask_tick_ = 0;
     size_t mask_bytes_ = 0;
     mutable size_t mask_budget_ = 0;

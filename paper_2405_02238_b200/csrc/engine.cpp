@@ -258,6 +258,82 @@ Schedule optimise(const Program& p) {
             }
         }
     }
+    // 5b. masked sums of rotations: a sum whose key-switch terms are all masked
+    //     (stable masks) Rot nodes takes them as one inner product over masked
+    //     keys; Rot nodes read only by such sums are never stored.
+    s.ks_terms.assign(n, {});
+    s.virt.assign(n, 0);
+    {
+        static const bool on = [] {
+            const char* e = std::getenv("HGM_KS_PLAN");
+            return !(e && e[0] == '0');
+        }();
+        std::vector<char> fus(n, 0);
+        for (size_t i = 0; i < n && on; ++i) {
+            const PNode& nd = q.nodes[i];
+            if (!live[i] || nd.kind != PNode::Comb || !(kind[i] & kPartA)) continue;
+            bool ok = true;
+            for (size_t t = 0; t < nd.in.size() && ok; ++t) {
+                const int x = nd.in[t];
+                if (!(term_kind(kind[x], nd.masks[t] != nullptr) & kPartA)) continue;
+                ok = nd.masks[t] && nd.masks[t]->stable && q.nodes[x].kind == PNode::Rot && kind[x] == kPartA &&
+                     !s.is_output[x] && !s.is_pending_output[x];
+            }
+            fus[i] = ok;
+        }
+        for (bool changed = on; changed;) {
+            changed = false;
+            std::vector<char> v(n, 0);
+            for (size_t x = 0; x < n; ++x)
+                v[x] = live[x] && q.nodes[x].kind == PNode::Rot && kind[x] == kPartA && !s.is_output[x] &&
+                       !s.is_pending_output[x];
+            for (size_t i = 0; i < n; ++i) {
+                if (!live[i]) continue;
+                const PNode& nd = q.nodes[i];
+                for (size_t t = 0; t < nd.in.size(); ++t)
+                    if (!(nd.kind == PNode::Comb && fus[i] && nd.masks[t])) v[nd.in[t]] = 0;
+            }
+            for (size_t i = 0; i < n; ++i) {
+                if (!fus[i]) continue;
+                const PNode& nd = q.nodes[i];
+                for (size_t t = 0; t < nd.in.size(); ++t)
+                    if ((kind[nd.in[t]] & kPartA) && !v[nd.in[t]]) {
+                        fus[i] = 0;
+                        changed = true;
+                        break;
+                    }
+            }
+            if (!changed) s.virt = v;
+        }
+        std::map<std::pair<u32, std::vector<u64>>, int> distinct;
+        for (size_t i = 0; i < n; ++i) {
+            if (!fus[i]) continue;
+            const PNode& nd = q.nodes[i];
+            std::vector<KsTerm>& kt = s.ks_terms[i];
+            for (size_t t = 0; t < nd.in.size(); ++t) {
+                const int x = nd.in[t];
+                if (!s.virt[x]) continue;
+                auto it = std::find_if(kt.begin(), kt.end(), [&](const KsTerm& k) { return k.rot == x; });
+                if (it == kt.end()) {
+                    KsTerm k;
+                    k.rot = x;
+                    k.src = q.nodes[x].in[0];
+                    k.g = q.nodes[x].g;
+                    kt.push_back(std::move(k));
+                    it = kt.end() - 1;
+                }
+                it->masks.push_back(nd.masks[t]);
+            }
+            for (const KsTerm& k : kt) {
+                std::vector<u64> ids;
+                for (const MaskRef& m : k.masks) ids.push_back(m->id);
+                std::sort(ids.begin(), ids.end());
+                distinct.emplace(std::make_pair(k.g, std::move(ids)), 0);
+            }
+            ++s.ks_comb_count;
+        }
+        s.masked_key_count = distinct.size();
+    }
     // 6. levels.  Inputs precede their readers, except Mat nodes appended in
     //    step 4, whose source does precede the reader: computed on first use.
     std::vector<int> level(n, -1);
@@ -280,7 +356,7 @@ Schedule optimise(const Program& p) {
             lv = 0;
             for (size_t t = 0; t < nd.in.size(); ++t) {
                 const int x = nd.in[t];
-                if (nd.kind == PNode::Comb && nd.fused[t]) {
+                if (nd.kind == PNode::Comb && (nd.fused[t] || s.virt[x])) {
                     for (int y : q.nodes[x].in) lv = std::max(lv, get(y) + 1);
                 } else {
                     lv = std::max(lv, get(x) + 1);
@@ -292,15 +368,17 @@ Schedule optimise(const Program& p) {
         return lv;
     };
     for (size_t i = 0; i < n; ++i)
-        if (live[i] && !fused_node[i]) max_level = std::max(max_level, level_of((int)i));
+        if (live[i] && !fused_node[i] && !s.virt[i]) max_level = std::max(max_level, level_of((int)i));
     s.levels.assign(max_level + 1, {});
     s.last_use_level.assign(n, -1);
     for (size_t i = 0; i < n; ++i) {
-        if (!live[i] || fused_node[i] || level[i] < 0) continue;
+        if (live[i] && s.virt[i]) ++s.rot_count;  // executed inside the sums that read it
+        if (!live[i] || fused_node[i] || s.virt[i] || level[i] < 0) continue;
         s.levels[level[i]].push_back((int)i);
         const PNode& nd = q.nodes[i];
-        if (nd.kind == PNode::Rot) ++s.rot_count;
+        if (nd.kind == PNode::Rot) { ++s.rot_count; ++s.stored_rot_count; }
         if (nd.kind == PNode::Comb) ++s.comb_count;
+        if (nd.kind == PNode::Comb && (kind[i] & kPartA)) ++s.acc_comb_count;
         if (nd.kind == PNode::Mat) {
             ++s.mat_count;
             if (kind[nd.in[0]] & kPartA) ++s.moddown_count;
@@ -311,6 +389,8 @@ Schedule optimise(const Program& p) {
             const int x = nd.in[t];
             if (nd.kind == PNode::Comb && nd.fused[t]) {
                 ++s.mult_count;
+                for (int y : q.nodes[x].in) s.last_use_level[y] = std::max(s.last_use_level[y], level[i]);
+            } else if (s.virt[x]) {
                 for (int y : q.nodes[x].in) s.last_use_level[y] = std::max(s.last_use_level[y], level[i]);
             } else {
                 s.last_use_level[x] = std::max(s.last_use_level[x], level[i]);
@@ -329,6 +409,8 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
     g_counters = ExecCounters{};
     g_counters.levels = sch.levels.size();
     ctx.trim_mask_cache();  // between programs: no mask pointer is held here yet
+    const bool masked_keys_ok = sch.masked_key_count > 0 && ctx.masked_keys_fit(sch.masked_key_count);
+    if (masked_keys_ok) ctx.trim_masked_keys(sch.masked_key_count);
     std::vector<u64*> buf(P.nodes.size(), nullptr);
     std::vector<PartLayout> lay(P.nodes.size());
     for (size_t x = 0; x < P.nodes.size(); ++x) lay[x] = part_layout(ctx, sch.kind[x]);
@@ -392,10 +474,16 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
             ctx.encrypt((int)vals.size(), vals.data(), S.data(), ctr.data(), out.data());
             g_counters.enc_items += vals.size();
         }
-        if (!rot.empty()) {
+        // masked sums of rotations taken straight from the ModUp digits (Schedule::ks_terms)
+        std::vector<int> kcomb;
+        for (int x : comb)
+            if (!sch.ks_terms[x].empty()) kcomb.push_back(x);
+        if (!rot.empty() || !kcomb.empty()) {
             // hoisting: one ModUp per distinct source (and instance)
             std::vector<int> srcs;
             for (int x : rot) srcs.push_back(P.nodes[x].in[0]);
+            for (int x : kcomb)
+                for (const KsTerm& kt : sch.ks_terms[x]) srcs.push_back(kt.src);
             std::sort(srcs.begin(), srcs.end());
             srcs.erase(std::unique(srcs.begin(), srcs.end()), srcs.end());
             u64* mbuf = ctx.alloc(srcs.size() * (size_t)K * MW);
@@ -408,32 +496,155 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
                 }
             ctx.modup((int)mct.size(), mct.data(), mout.data());
             g_counters.modup_items += mct.size();
-            // rotations grouped by Galois element: one key serves the group
-            std::vector<int> order(rot);
-            std::stable_sort(order.begin(), order.end(),
-                             [&](int a, int b) { return P.nodes[a].g < P.nodes[b].g; });
-            // items tiled over instances: within a tile of kRotTile instances the
-            // rotations run key by key, so the tile's ModUp digits stay in L2 while
-            // every Galois key streams past them once (instead of re-reading each
-            // instance's digits from HBM for every one of its rotations)
-            constexpr int kRotTile = 8;
-            std::vector<const u64*> mu, cts;
-            std::vector<u32> gs;
-            std::vector<u64*> out;
-            for (int k0 = 0; k0 < K; k0 += kRotTile)
-                for (int x : order) {
-                    const int src = P.nodes[x].in[0];
-                    const size_t si = std::lower_bound(srcs.begin(), srcs.end(), src) - srcs.begin();
-                    for (int k = k0; k < std::min(K, k0 + kRotTile); ++k) {
-                        mu.push_back(mbuf + (si * K + k) * MW);
-                        cts.push_back(plain(src, k));
-                        gs.push_back(P.nodes[x].g);
-                        out.push_back(wpart(x, k, kPartA));
+            auto digits_of = [&](int src, int k) -> const u64* {
+                const size_t si = std::lower_bound(srcs.begin(), srcs.end(), src) - srcs.begin();
+                return mbuf + (si * K + k) * MW;
+            };
+            if (!rot.empty()) {
+                // rotations grouped by Galois element: one key serves the group
+                std::vector<int> order(rot);
+                std::stable_sort(order.begin(), order.end(),
+                                 [&](int a, int b) { return P.nodes[a].g < P.nodes[b].g; });
+                // items tiled over instances: within a tile of kRotTile instances the
+                // rotations run key by key, so the tile's ModUp digits stay in L2 while
+                // every Galois key streams past them once (instead of re-reading each
+                // instance's digits from HBM for every one of its rotations)
+                constexpr int kRotTile = 8;
+                std::vector<const u64*> mu, cts;
+                std::vector<u32> gs;
+                std::vector<u64*> out;
+                for (int k0 = 0; k0 < K; k0 += kRotTile)
+                    for (int x : order) {
+                        const int src = P.nodes[x].in[0];
+                        for (int k = k0; k < std::min(K, k0 + kRotTile); ++k) {
+                            mu.push_back(digits_of(src, k));
+                            cts.push_back(plain(src, k));
+                            gs.push_back(P.nodes[x].g);
+                            out.push_back(wpart(x, k, kPartA));
+                        }
+                    }
+                // a pending key switch: the accumulator, P phi(c0) folded in (no ModDown)
+                ctx.rotate_acc((int)mu.size(), mu.data(), cts.data(), gs.data(), out.data());
+                g_counters.rot_items += mu.size();
+            }
+            if (!kcomb.empty()) {
+                // masked keys of every sum (cached per context); a sum whose keys the
+                // cache cannot hold runs rotation by rotation (same value)
+                std::vector<std::vector<const u64*>> mk(kcomb.size());
+                std::vector<int> slow;
+                for (size_t ci = 0; ci < kcomb.size(); ++ci) {
+                    const std::vector<KsTerm>& kts = sch.ks_terms[kcomb[ci]];
+                    bool ok = masked_keys_ok;
+                    for (size_t t = 0; t < kts.size() && ok; ++t) {
+                        std::vector<u64> ids;
+                        std::vector<const u64*> devs;
+                        for (const MaskRef& m : kts[t].masks) ids.push_back(m->id);
+                        const u64* d = ctx.masked_key(kts[t].g, ids, nullptr);  // cached?
+                        if (!d) {
+                            for (const MaskRef& m : kts[t].masks) devs.push_back(resolve(m));
+                            d = ctx.masked_key(kts[t].g, ids, &devs);
+                        }
+                        if (!d) ok = false;
+                        mk[ci].push_back(d);
+                    }
+                    if (!ok) {
+                        mk[ci].clear();
+                        slow.push_back(kcomb[ci]);
                     }
                 }
-            // a pending key switch: the accumulator, P phi(c0) folded in (no ModDown)
-            ctx.rotate_acc((int)mu.size(), mu.data(), cts.data(), gs.data(), out.data());
-            g_counters.rot_items += mu.size();
+                // groups of up to 8 instances of one sum; tiles of instances, sum by sum
+                // inside a tile, so the tile's ModUp digits stay in L2 while the masked
+                // keys stream past them, and a key's second group finds it in L2
+                static const int tile = [] {
+                    const char* e = std::getenv("HGM_PLAN_TILE");
+                    const int v = e ? std::atoi(e) : 16;
+                    return v < 8 ? 8 : v;
+                }();
+                std::vector<PlanGroup> groups;
+                std::vector<const u64*> mkey, dig, c0;
+                std::vector<u32> gs;
+                std::vector<u64*> out;
+                auto flush = [&]() {
+                    ctx.rotate_plan(groups, mkey, gs, dig, c0, out);
+                    g_counters.plan_items += out.size();
+                    groups.clear(); mkey.clear(); dig.clear(); c0.clear(); gs.clear(); out.clear();
+                };
+                for (int k0 = 0; k0 < K; k0 += tile) {
+                    for (size_t ci = 0; ci < kcomb.size(); ++ci) {
+                        if (mk[ci].empty()) continue;
+                        const int x = kcomb[ci];
+                        const std::vector<KsTerm>& kts = sch.ks_terms[x];
+                        for (int k1 = k0; k1 < std::min(K, k0 + tile); k1 += 8) {
+                            PlanGroup G{};
+                            G.item0 = (u32)out.size();
+                            G.cnt = (u32)(std::min(std::min(K, k0 + tile), k1 + 8) - k1);
+                            G.term0 = (u32)mkey.size();
+                            G.nterms = (u32)kts.size();
+                            G.dbase = (u32)dig.size();
+                            for (size_t t = 0; t < kts.size(); ++t) {
+                                mkey.push_back(mk[ci][t]);
+                                gs.push_back(kts[t].g);
+                            }
+                            for (u32 u = 0; u < G.cnt; ++u) {
+                                for (size_t t = 0; t < kts.size(); ++t) {
+                                    dig.push_back(digits_of(kts[t].src, k1 + (int)u));
+                                    c0.push_back(plain(kts[t].src, k1 + (int)u));
+                                }
+                                out.push_back(wpart(x, k1 + (int)u, kPartA));
+                            }
+                            groups.push_back(G);
+                        }
+                    }
+                    if (out.size() >= 8192) flush();
+                }
+                flush();
+                // the same sums rotation by rotation: accumulators in temporaries, then the masked sum
+                const size_t AW = ctx.ks_words();
+                for (size_t s0 = 0; s0 < slow.size();) {
+                    size_t s1 = s0, terms = 0;
+                    while (s1 < slow.size() && (s1 == s0 || (terms + P.nodes[slow[s1]].in.size()) * K * AW * 8 <= ((size_t)8 << 30))) {
+                        terms += P.nodes[slow[s1]].in.size();
+                        ++s1;
+                    }
+                    u64* tmp = ctx.alloc(terms * (size_t)K * AW);
+                    std::vector<const u64*> mu, cts, ain, amask;
+                    std::vector<u32> rg, aoff{0};
+                    std::vector<u64*> racc, aout;
+                    size_t slot = 0;
+                    for (size_t si = s0; si < s1; ++si) {
+                        const int x = slow[si];
+                        const PNode& nd = P.nodes[x];
+                        std::map<int, size_t> rot_slot;  // each distinct rotation once
+                        for (size_t t = 0; t < nd.in.size(); ++t)
+                            if (sch.virt[nd.in[t]] && !rot_slot.count(nd.in[t])) {
+                                const int y = nd.in[t];
+                                rot_slot.emplace(y, slot);
+                                for (int k = 0; k < K; ++k) {
+                                    mu.push_back(digits_of(P.nodes[y].in[0], k));
+                                    cts.push_back(plain(P.nodes[y].in[0], k));
+                                    rg.push_back(P.nodes[y].g);
+                                    racc.push_back(tmp + (slot * K + k) * AW);
+                                }
+                                ++slot;
+                            }
+                        for (int k = 0; k < K; ++k) {
+                            for (size_t t = 0; t < nd.in.size(); ++t)
+                                if (sch.virt[nd.in[t]]) {
+                                    ain.push_back(tmp + (rot_slot[nd.in[t]] * K + k) * AW);
+                                    amask.push_back(resolve(nd.masks[t]));
+                                }
+                            aoff.push_back((u32)ain.size());
+                            aout.push_back(wpart(x, k, kPartA));
+                        }
+                    }
+                    ctx.rotate_acc((int)mu.size(), mu.data(), cts.data(), rg.data(), racc.data());
+                    ctx.lincomb_qp((int)aout.size(), aoff.data(), ain.data(), amask.data(), aout.data());
+                    g_counters.rot_items += mu.size();
+                    g_counters.comb_items += aout.size();
+                    ctx.release(tmp);
+                    s0 = s1;
+                }
+            }
             ctx.release(mbuf);
         }
         // sums: plain parts (masked or not), key-switch parts over Q ++ P, tensors
@@ -445,7 +656,8 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
                 const PNode& nd = P.nodes[x];
                 const int kx = sch.kind[x];
                 std::vector<const u64*> md(nd.in.size());
-                for (size_t t = 0; t < nd.in.size(); ++t) md[t] = resolve(nd.masks[t]);
+                for (size_t t = 0; t < nd.in.size(); ++t)
+                    md[t] = sch.virt[nd.in[t]] ? nullptr : resolve(nd.masks[t]);  // virtual: masked keys
                 for (int k = 0; k < K; ++k) {
                     for (size_t t = 0; t < nd.in.size(); ++t) {
                         const int y = nd.in[t];
@@ -455,7 +667,7 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
                             xin.push_back(part(y, k, kPartX));
                             xmask.push_back(md[t]);
                         }
-                        if (ky & kPartA) {
+                        if ((ky & kPartA) && !sch.virt[y]) {
                             ain.push_back(part(y, k, kPartA));
                             amask.push_back(md[t]);
                         }
@@ -464,7 +676,7 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
                         xoff.push_back((u32)xin.size());
                         xout.push_back(wpart(x, k, kPartX));
                     }
-                    if (kx & kPartA) {
+                    if ((kx & kPartA) && sch.ks_terms[x].empty()) {
                         aoff.push_back((u32)ain.size());
                         aout.push_back(wpart(x, k, kPartA));
                     }

@@ -18,6 +18,10 @@
 //     or ModDown run once when another op reads the value (a Mat node); a
 //     product whose only reader is such a sum is accumulated straight into the
 //     sum's tensor (fused: its own tensor is never stored);
+//   * a masked sum of rotations sum_t m_t (.) Rot(x_t, g_t) whose masks belong to a
+//     cached program is ONE key inner product over masked keys m_t (.) key_{g_t}
+//     (mask multiplication distributes over the inner product mod q: the same
+//     canonical residues as rotating, masking and adding);
 //   * every op of one dependency level is one batched launch sequence over
 //     all (node, instance) pairs; rotations are grouped by Galois key so that
 //     one key read from HBM serves the whole group.
@@ -79,6 +83,14 @@ struct PartLayout {
 };
 PartLayout part_layout(const Context& ctx, int kind);
 
+// One rotation of a masked sum whose key-switch part is computed straight from
+// the ModUp digits (k_ks_plan): the masks of every term reading that rotation.
+struct KsTerm {
+    int rot = -1, src = -1;  // the (never stored) Rot node and its source
+    u32 g = 1;
+    std::vector<MaskRef> masks;
+};
+
 // Optimised, levelised form of a Program (built once, reused for every batch).
 struct Schedule {
     Program prog;                        // rewritten program
@@ -90,6 +102,13 @@ struct Schedule {
     std::vector<char> is_pending_output;
     size_t rot_count = 0, comb_count = 0, mult_count = 0, pending_count = 0, mat_count = 0;
     size_t moddown_count = 0, rescale_count = 0;  // Mat nodes reading a key-switch / product part
+    // Masked sums of rotations (stable masks only): ks_terms[x] non-empty = Comb x's
+    // key-switch part is one inner product over its rotations' masked keys; a Rot
+    // read only by such sums is virtual (no level, no buffer).
+    std::vector<std::vector<KsTerm>> ks_terms;
+    std::vector<char> virt;
+    size_t ks_comb_count = 0, masked_key_count = 0, acc_comb_count = 0;
+    size_t stored_rot_count = 0;  // rot_count counts every rotation after CSE, stored or not
 };
 Schedule optimise(const Program& p);
 
@@ -114,7 +133,7 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io);
 // Kernel-launch accounting of the last execute() on this thread.
 struct ExecCounters {
     size_t levels = 0, launches = 0, rot_items = 0, modup_items = 0, comb_items = 0,
-           mult_items = 0, enc_items = 0, mat_items = 0;
+           mult_items = 0, enc_items = 0, mat_items = 0, plan_items = 0;
 };
 ExecCounters last_exec_counters();
 

@@ -40,6 +40,28 @@ def test_variant_parity(name):
     assert r.returncode == 0, f"{name}: {VARIANTS[name]}\n{r.stdout[-3000:]}\n{r.stderr[-2000:]}"
 
 
+# Masked sums of rotations (csrc/engine.cpp, Schedule::ks_terms) run as one inner
+# product over masked keys; the same sums rotation by rotation (k_ks_inner +
+# k_lincomb_masked) must give the same ciphertext words: with the rewrite off, and
+# with a masked-key cache too small for any program (the executor's fallback).
+PLAN_VARIANTS = {
+    "plan-sums-off": {"HGM_KS_PLAN": "0"},
+    "masked-key-cache-too-small": {"HGM_MASKED_KEY_MB": "8"},
+    "plan-tile-8": {"HGM_PLAN_TILE": "8"},
+}
+
+
+@pytest.mark.parametrize("name", sorted(PLAN_VARIANTS))
+def test_plan_sum_variants(name):
+    env = dict(os.environ)
+    env.update(PLAN_VARIANTS[name])
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        "-k", "not acceptance", "tests/test_gpu_hegmm.py", "tests/test_gpu_ct_golden.py",
+                        "tests/test_gpu_widen.py"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, f"{name}: {PLAN_VARIANTS[name]}\n{r.stdout[-3000:]}\n{r.stderr[-2000:]}"
+
+
 def test_many_lockstep_chunks_exact():
     """hgm_matmul_batch over many lockstep chunks (a small memory share forces
     several): the pipelined decrypt's pinned double buffers are reused across
