@@ -541,65 +541,90 @@ __global__ void k_mask_key(DevCtx cx, const u64* key, const u64* const* masks, u
 //                        + [c = 0, r < L] c0_t[r][src_t(j)] mp_t[r][j] )   over Q ++ P
 // = sum_t mask_t (.) RotAcc(ct_t, g_t): the value k_ks_inner + k_lincomb_masked
 // produce, bit for bit (canonical residues of the same sum mod q_r).
-// A group is up to kKeyReuse instances of one sum: each masked-key element is
-// read once per group.  Terms are taken one at a time with the running residues
-// of the group's instances in registers (4 products + a residue stay inside the
-// 128-bit column sum: 4 q^2 + q < 2^(s+62) for every prime of the sets).
+// A group is a tile of lockstep instances of one sum: each thread keeps its
+// coefficient's masked-key elements of up to kPlanTerms terms in shared memory
+// (its own slots: no barrier) and walks the group's instances, so a masked key
+// is read once per group.  Terms are taken one at a time on top of the running
+// residue (4 products + a residue stay inside the 128-bit column sum:
+// 4 q^2 + q < 2^(s+62) for every prime of the sets); sums of more than
+// kPlanTerms terms continue from the stored output.
+constexpr u32 kPlanTerms = 2;
+template <typename SH, u32 NT>
+__device__ __forceinline__ void plan_terms(const Prime& P, const u64* sk, u32 tid, u32 r, u32 N, const u32* src,
+                                           const u64* const* Dt, const u64* const* Ct, u64& r0, u64& r1) {
+    constexpr u32 dnum = SH::dnum, R = SH::R, E = 2 * SH::dnum + 1;
+    u64 x[NT][SH::dnum], c[NT];
+#pragma unroll
+    for (u32 t = 0; t < NT; ++t) {  // every load of the chunk first
+        const u64* d = Dt[t];
+#pragma unroll
+        for (u32 dg = 0; dg < dnum; ++dg) x[t][dg] = d[((size_t)dg * R + r) * N + src[t]];
+        c[t] = r < SH::L ? Ct[t][(size_t)r * N + src[t]] : 0;
+    }
+#pragma unroll
+    for (u32 t = 0; t < NT; ++t) {
+        Cols a0, a1;
+        a0.x = r0;
+        a1.x = r1;
+#pragma unroll
+        for (u32 dg = 0; dg < dnum; ++dg) {
+            const Dig<SH::S> xd = split<SH::S>(x[t][dg]);
+            a0.mac(xd, packed_dig<SH::S>(sk[((t * E) + 2 * dg) * kThreads + tid]));
+            a1.mac(xd, packed_dig<SH::S>(sk[((t * E) + 2 * dg + 1) * kThreads + tid]));
+        }
+        if (r < SH::L) a0.mac(split<SH::S>(c[t]), packed_dig<SH::S>(sk[((t * E) + 2 * dnum) * kThreads + tid]));
+        r0 = reduce_acc(a0.fold<SH::S>(), P);
+        r1 = reduce_acc(a1.fold<SH::S>(), P);
+    }
+}
 template <typename SH>
-__global__ void __launch_bounds__(kThreads, 2) k_ks_plan(DevCtx cx, u32 n_groups, const PlanGroup* groups,
+__global__ void __launch_bounds__(kThreads, 4) k_ks_plan(DevCtx cx, u32 n_groups, const PlanGroup* groups,
                                                          const u64* const* mkey, const u32* g,
                                                          const u64* const* D, const u64* const* c0,
                                                          u64* const* out) {
+    extern __shared__ u64 sk[];  // [chunk terms][2 dnum + 1][kThreads]
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
-    const u32 N = dp->N, R = SH::R, dnum = SH::dnum, logN = dp->logN;
+    const u32 N = dp->N, R = SH::R, dnum = SH::dnum, logN = dp->logN, tid = threadIdx.x;
+    constexpr u32 E = 2 * SH::dnum + 1;
     for (u32 grp = blockIdx.y; grp < n_groups; grp += gridDim.y) {
         const PlanGroup G = groups[grp];
         COEF_LOOP {
-            for (u32 r = 0; r < R; ++r) {
-                const Prime& P = dp->pr[r];
-                u64 r0[kKeyReuse], r1[kKeyReuse];
+            for (u32 t0 = 0; t0 < G.nterms; t0 += kPlanTerms) {
+                const u32 nt = min(kPlanTerms, G.nterms - t0);
+                u32 src[kPlanTerms];
 #pragma unroll
-                for (u32 u = 0; u < (u32)kKeyReuse; ++u) r0[u] = r1[u] = 0;
-                for (u32 t = 0; t < G.nterms; ++t) {
-                    const u64* k = mkey[G.term0 + t];
-                    const u32 ge = g[G.term0 + t];
-                    const u32 src = ge == 1 ? j : galois_src(j, ge, logN);
-                    u64 k0[SH::dnum], k1[SH::dnum];
+                for (u32 t = 0; t < kPlanTerms; ++t) {
+                    const u32 ge = t < nt ? g[G.term0 + t0 + t] : 1;
+                    src[t] = ge == 1 ? j : galois_src(j, ge, logN);
+                }
+                for (u32 r = 0; r < R; ++r) {
+                    const Prime& P = dp->pr[r];
+                    for (u32 t = 0; t < nt; ++t) {
+                        const u64* k = mkey[G.term0 + t0 + t];
 #pragma unroll
-                    for (u32 dg = 0; dg < dnum; ++dg) {
-                        k0[dg] = __ldg(k + (((size_t)dg * 2 + 0) * R + r) * N + j);
-                        k1[dg] = __ldg(k + (((size_t)dg * 2 + 1) * R + r) * N + j);
-                    }
-                    const u64 pm = r < SH::L ? __ldg(k + ((size_t)dnum * 2 * R + r) * N + j) : 0;
-                    const u64* const* Dt = D + G.dbase + t;
-                    const u64* const* Ct = c0 + G.dbase + t;
-#pragma unroll
-                    for (u32 u = 0; u < (u32)kKeyReuse; ++u) {
-                        if (u < G.cnt) {
-                            const u64* d = Dt[(size_t)u * G.nterms];
-                            Cols a0, a1;
-                            a0.x = r0[u];
-                            a1.x = r1[u];
-#pragma unroll
-                            for (u32 dg = 0; dg < dnum; ++dg) {
-                                const Dig<SH::S> x = split<SH::S>(d[((size_t)dg * R + r) * N + src]);
-                                a0.mac(x, packed_dig<SH::S>(k0[dg]));
-                                a1.mac(x, packed_dig<SH::S>(k1[dg]));
-                            }
-                            if (r < SH::L)
-                                a0.mac(split<SH::S>(Ct[(size_t)u * G.nterms][(size_t)r * N + src]), packed_dig<SH::S>(pm));
-                            r0[u] = reduce_acc(a0.fold<SH::S>(), P);
-                            r1[u] = reduce_acc(a1.fold<SH::S>(), P);
+                        for (u32 dg = 0; dg < dnum; ++dg) {
+                            sk[((t * E) + 2 * dg) * kThreads + tid] = __ldg(k + (((size_t)dg * 2 + 0) * R + r) * N + j);
+                            sk[((t * E) + 2 * dg + 1) * kThreads + tid] = __ldg(k + (((size_t)dg * 2 + 1) * R + r) * N + j);
                         }
+                        if (r < SH::L) sk[((t * E) + 2 * dnum) * kThreads + tid] = __ldg(k + ((size_t)dnum * 2 * R + r) * N + j);
+                    }
+                    for (u32 u = 0; u < G.cnt; ++u) {
+                        u64* a = out[G.item0 + u];
+                        u64 r0 = 0, r1 = 0;
+                        if (t0) {
+                            r0 = a[(size_t)r * N + j];
+                            r1 = a[((size_t)R + r) * N + j];
+                        }
+                        const u64* const* Dt = D + G.dbase + (size_t)u * G.nterms + t0;
+                        const u64* const* Ct = c0 + G.dbase + (size_t)u * G.nterms + t0;
+                        if (nt == 1)
+                            plan_terms<SH, 1>(P, sk, tid, r, N, src, Dt, Ct, r0, r1);
+                        else
+                            plan_terms<SH, 2>(P, sk, tid, r, N, src, Dt, Ct, r0, r1);
+                        a[(size_t)r * N + j] = r0;
+                        a[((size_t)R + r) * N + j] = r1;
                     }
                 }
-#pragma unroll
-                for (u32 u = 0; u < (u32)kKeyReuse; ++u)
-                    if (u < G.cnt) {
-                        u64* a = out[G.item0 + u];
-                        a[(size_t)r * N + j] = r0[u];
-                        a[((size_t)R + r) * N + j] = r1[u];
-                    }
             }
         }
     }
@@ -2112,10 +2137,20 @@ void Context::rotate_plan(const std::vector<PlanGroup>& groups, const std::vecto
     u64* const* dout = upload(out);
     const PlanGroup* dgrp = upload(groups);
     const u32 n = (u32)groups.size();
+    u32 tmax = 1;
+    for (const PlanGroup& G : groups) tmax = std::max(tmax, std::min(G.nterms, kPlanTerms));
+    const size_t smem = (size_t)tmax * (2 * hp_.dnum + 1) * kThreads * 8;
+    static const bool attr = [] {
+        const int cap = (int)(kPlanTerms * (2 * 3 + 1) * kThreads * 8);
+        HGM_CUDA(cudaFuncSetAttribute(k_ks_plan<ShapeQ3>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+        HGM_CUDA(cudaFuncSetAttribute(k_ks_plan<ShapeQ8>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+        return true;
+    }();
+    (void)attr;
     if (hp_.L == 3)
-        k_ks_plan<ShapeQ3><<<grid_of(hp_.N, n), kThreads, 0, stream_>>>(cx_, n, dgrp, dk, dg, dd, dc, dout);
+        k_ks_plan<ShapeQ3><<<grid_of(hp_.N, n), kThreads, smem, stream_>>>(cx_, n, dgrp, dk, dg, dd, dc, dout);
     else
-        k_ks_plan<ShapeQ8><<<grid_of(hp_.N, n), kThreads, 0, stream_>>>(cx_, n, dgrp, dk, dg, dd, dc, dout);
+        k_ks_plan<ShapeQ8><<<grid_of(hp_.N, n), kThreads, smem, stream_>>>(cx_, n, dgrp, dk, dg, dd, dc, dout);
     ++launches_;
     HGM_CUDA(cudaGetLastError());
 }

@@ -58,7 +58,7 @@ class PinnedRing {
 };
 
 // One group of k_ks_plan (a masked sum of rotations computed straight from the
-// ModUp digits): up to 8 lockstep instances of one sum, sharing its masked keys.
+// ModUp digits): a tile of lockstep instances of one sum, sharing its masked keys.
 struct PlanGroup {
     u32 item0, cnt;     // outputs item0 .. item0 + cnt - 1
     u32 term0, nterms;  // masked keys / Galois elements term0 .. term0 + nterms - 1

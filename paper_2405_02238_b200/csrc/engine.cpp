@@ -552,13 +552,13 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
                         slow.push_back(kcomb[ci]);
                     }
                 }
-                // groups of up to 8 instances of one sum; tiles of instances, sum by sum
-                // inside a tile, so the tile's ModUp digits stay in L2 while the masked
-                // keys stream past them, and a key's second group finds it in L2
+                // one group per (tile of instances, sum); tiles in order, sum by sum inside a
+                // tile, so the tile's ModUp digits stay in L2 while the masked keys stream
+                // past them, each read once per tile
                 static const int tile = [] {
                     const char* e = std::getenv("HGM_PLAN_TILE");
                     const int v = e ? std::atoi(e) : 16;
-                    return v < 8 ? 8 : v;
+                    return v < 1 ? 1 : v;
                 }();
                 std::vector<PlanGroup> groups;
                 std::vector<const u64*> mkey, dig, c0;
@@ -574,10 +574,11 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
                         if (mk[ci].empty()) continue;
                         const int x = kcomb[ci];
                         const std::vector<KsTerm>& kts = sch.ks_terms[x];
-                        for (int k1 = k0; k1 < std::min(K, k0 + tile); k1 += 8) {
+                        {
+                            const int k1 = k0;
                             PlanGroup G{};
                             G.item0 = (u32)out.size();
-                            G.cnt = (u32)(std::min(std::min(K, k0 + tile), k1 + 8) - k1);
+                            G.cnt = (u32)(std::min(K, k0 + tile) - k0);
                             G.term0 = (u32)mkey.size();
                             G.nterms = (u32)kts.size();
                             G.dbase = (u32)dig.size();
