@@ -64,6 +64,16 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def sm_max_mhz(device: int = 0) -> float:
+    """The GPU's maximum SM clock (nvidia-smi clocks.max.sm); 1965 MHz (B200) if unreadable."""
+    try:
+        out = subprocess.run(["nvidia-smi", "--query-gpu=clocks.max.sm", "--format=csv,noheader,nounits", "-i",
+                              str(device)], capture_output=True, text=True, timeout=5).stdout
+        return float(out.strip().splitlines()[0])
+    except Exception:
+        return 1965.0
+
+
 class ClockSampler:
     """nvidia-smi clocks and throttle reasons sampled DURING the timed region."""
 
@@ -267,6 +277,25 @@ def ntt_roofline(ctx, limb_bytes, label):
     ks_bytes = (ctx.dnum * R + ctx.L + 2 * R + ctx.dnum * 2 * R / 8) * ctx.N * 8
     ks_ms = ctx.bench_keyswitch(ks_items, 10)
     ks_gbs = ks_items * ks_bytes / (ks_ms / 1e3) / 1e9
+    # the in-step key-switch kernel: masked sums of rotations straight from the ModUp digits
+    # (k_ks_plan), as the cloud step lays them out -- tiles of 16 instances, every sum of an
+    # instance reading that instance's digits, masked keys read once per tile.  Compulsory
+    # bytes per sum: 2 (L+K) limbs written, terms (2 dnum (L+K) + L) masked-key limbs per
+    # tile, the instance's dnum (L+K) + L digit / c0 limbs once per `sums` sums.
+    pl_inst, pl_sums, pl_terms, pl_tile = (128, 63, 2, 16) if ctx.N == 8192 else (16, 16, 2, 16)
+    pl_bytes = (2 * R + pl_terms * (2 * ctx.dnum * R + ctx.L) / pl_tile
+                + (ctx.dnum * R + ctx.L) / pl_sums) * ctx.N * 8
+    pl_ms = ctx.bench_keyswitch_plan(pl_inst, pl_sums, pl_terms, pl_tile, 5)
+    pl_n = pl_inst * pl_sums
+    pl_gbs = pl_n * pl_bytes / (pl_ms / 1e3) / 1e9
+    # what the same sums cost as separate kernels (one k_ks_inner per rotation, then the
+    # masked sum of the accumulators): the bytes k_ks_plan no longer moves
+    unfused = pl_terms * ks_bytes + (pl_terms * (2 * R + R) + 2 * R) * ctx.N * 8
+    # integer-multiply ceiling of the butterfly: 22 fmaheavy cycles per warp-butterfly
+    # (3 IMAD.WIDE + IMAD.HI at 4, 3 IMAD at 2), 4 SMSPs x 148 SMs
+    logn = ctx.N.bit_length() - 1
+    SM_MAX_MHZ = sm_max_mhz()
+    warp_bf = limbs * (ctx.N // 2) * logn / 32
     traffic, pipes = None, None
     prof = os.path.join(ROOT, "profiles", "ntt_traffic.json")
     if os.path.exists(prof):
@@ -286,7 +315,20 @@ def ntt_roofline(ctx, limb_bytes, label):
             "inverse_frac": round(limbs * limb_bytes / (intt_ms / 1e3) / 1e9 / peak, 4),
             "peak_source": peak_src, "frac_vs_spec_8tbs": round(achieved / 8000.0, 4),
             "int_pipes_ncu": pipes,
-            "keyswitch": {"kernel": "k_ks_inner (key inner product, Galois gather fused, 8 rotations per key read)",
+            "int_multiply_ceiling": {"pipe": "fmaheavy (IMAD / IMAD.WIDE / IMAD.HI)",
+                                     "cycles_per_warp_butterfly": 22,
+                                     "min_ms_at_max_clock": round(warp_bf * 22 / (148 * 4) / (SM_MAX_MHZ * 1e3), 4),
+                                     "frac_of_ceiling": round(warp_bf * 22 / (148 * 4) / (SM_MAX_MHZ * 1e3) / ntt_ms, 4),
+                                     "ceiling_as_hbm_frac": round(limbs * limb_bytes / (warp_bf * 22 / (148 * 4) / (SM_MAX_MHZ * 1e6)) / 1e9 / peak, 4)},
+            "keyswitch_plan": {"kernel": "k_ks_plan (masked sum of rotations as one key inner product over masked "
+                                         "keys; the cloud step's key-switch kernel for cached programs)",
+                               "sums_per_launch": pl_n, "terms_per_sum": pl_terms, "tile": pl_tile,
+                               "algorithmic_bytes_per_sum": int(pl_bytes), "ms_per_launch": round(pl_ms, 4),
+                               "achieved": round(pl_gbs, 1), "frac": round(pl_gbs / peak, 4),
+                               "unfused_bytes_per_sum": int(unfused),
+                               "unfused_equivalent_gbs": round(pl_n * unfused / (pl_ms / 1e3) / 1e9, 1),
+                               "int_pipes_ncu": plan_pipes(ctx.N)},
+            "keyswitch": {"kernel": "k_ks_inner (key inner product of one rotation, Galois gather fused, 8 rotations per key read; relinearisation and uncached programs)",
                           "rotations_per_launch": ks_items, "algorithmic_bytes_per_rotation": int(ks_bytes),
                           "traffic": ks_traffic(ctx.N, ks_items), "int_pipes_ncu": ks_pipes(ctx.N),
                           "ms_per_launch": round(ks_ms, 4), "achieved": round(ks_gbs, 1),
@@ -301,6 +343,16 @@ def ks_traffic(N, items):
         rec = json.load(open(prof))
         if rec.get("N") == N and rec.get("bytes_per_rotation"):
             return rec["bytes_per_rotation"] * items
+    except Exception:
+        pass
+    return None
+
+
+def plan_pipes(N):
+    try:
+        rec = json.load(open(os.path.join(ROOT, "profiles", "ks_plan_traffic.json")))
+        if rec.get("N") == N:
+            return {k: rec.get(k) for k in ("fmaheavy_frac", "alu_frac", "issue_frac", "dram_frac", "source")}
     except Exception:
         pass
     return None
@@ -535,7 +587,7 @@ def run_cfg5(args):
                "d2h_bytes_per_step": total_blocks * ctx.slot_count * 4,
                "path": "hgm_matmul_batch (C ABI) over the rank's row blocks: host int64 in -> host C"}
     roofline = ntt_roofline(ctx, 2 * 8 * ctx.N,
-                            "k_ntt_fwd_outer2 + k_ntt_fwd3<13> (forward NTT, N=32768, 64-bit Shoup)")
+                            "k_ntt_fwd_c4<13> (forward NTT, N=32768, one HBM pass: 4-CTA clusters, outer stages through DSMEM, 64-bit Shoup)")
     if rank == 0:
         line = {
             "metric": "encrypted 128x128x128 matmuls/sec (BFV N=32768)", "value": round(value, 3),

@@ -322,6 +322,11 @@ int hgm_bench_ntt(hgm_ctx* ctx, int forward, size_t limbs, int iters, float* ms_
 int hgm_test_chacha(const uint32_t* key, uint64_t nonce, uint64_t counter, int rounds, uint32_t* out);
 /* key-switch inner product (k_ks_inner) over `items` rotations, 8 per Galois key */
 int hgm_bench_keyswitch(hgm_ctx* ctx, size_t items, int iters, float* ms_per_iter);
+/* masked sums of rotations straight from the ModUp digits (k_ks_plan), laid out as
+ * the cloud step launches them: tiles of `tile` instances, `sums` sums of `terms`
+ * rotations per instance, all reading that instance's digits */
+int hgm_bench_keyswitch_plan(hgm_ctx* ctx, size_t instances, size_t sums, size_t terms, size_t tile, int iters,
+                             float* ms_per_iter);
 int hgm_device_sync(hgm_ctx* ctx);
 /* Test hook: in-place NTT of `count` host limbs (count*N words) under one
  * prime (index into Q ++ P ++ B, or -1 for t). */

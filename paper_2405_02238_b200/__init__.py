@@ -58,7 +58,7 @@ EXPORTS = (
     "hgm_decrypt_products", "hgm_comm_unique_id", "hgm_comm_init", "hgm_comm_init_file", "hgm_comm_destroy",
     "hgm_comm_rank", "hgm_comm_size", "hgm_comm_barrier", "hgm_comm_max", "hgm_comm_gather",
     "hgm_comm_gather_batch", "hgm_comm_buffer_free", "hgm_bench_keyswitch", "hgm_blocked_mm_ex",
-    "hgm_test_chacha",
+    "hgm_test_chacha", "hgm_bench_keyswitch_plan",
 )
 CTX_KEYLESS, CTX_OS_SEED = 1, 2
 COUNTER_AUTO = (1 << 64) - 1
@@ -304,6 +304,7 @@ def lib() -> ctypes.CDLL:
         "hgm_bench_ntt": (_int, [_vp, _int, _sz, _int, _vp]),
         "hgm_device_sync": (_int, [_vp]),
         "hgm_bench_keyswitch": (_int, [_vp, _sz, _int, _vp]),
+        "hgm_bench_keyswitch_plan": (_int, [_vp, _sz, _sz, _sz, _sz, _int, _vp]),
         "hgm_test_chacha": (_int, [_vp, _u64, _u64, _int, _vp]),
         "hgm_test_ntt": (_int, [_vp, _int, _int, _vp, _sz]),
         "hgm_launch_count": (_u64, [_vp]),
@@ -656,6 +657,14 @@ class Context:
         """ms per k_ks_inner launch over `items` rotations (8 per Galois key)."""
         ms = ctypes.c_float()
         _check(lib().hgm_bench_keyswitch(self._h, items, iters, ctypes.byref(ms)))
+        return ms.value
+
+    def bench_keyswitch_plan(self, instances: int, sums: int, terms: int = 2, tile: int = 16,
+                             iters: int = 5) -> float:
+        """ms per k_ks_plan launch: `sums` masked sums of `terms` rotations for each of
+        `instances` lockstep instances (tiles of `tile` sharing the masked keys)."""
+        ms = ctypes.c_float()
+        _check(lib().hgm_bench_keyswitch_plan(self._h, instances, sums, terms, tile, iters, ctypes.byref(ms)))
         return ms.value
 
     def sync(self) -> None:

@@ -549,6 +549,9 @@ __global__ void k_mask_key(DevCtx cx, const u64* key, const u64* const* masks, u
 // 4 q^2 + q < 2^(s+62) for every prime of the sets); sums of more than
 // kPlanTerms terms continue from the stored output.
 constexpr u32 kPlanTerms = 2;
+#ifndef HGM_PLAN_WIDE
+#define HGM_PLAN_WIDE 1
+#endif
 template <typename SH, u32 NT>
 __device__ __forceinline__ void plan_terms(const Prime& P, const u64* sk, u32 tid, u32 r, u32 N, const u32* src,
                                            const u64* const* Dt, const u64* const* Ct, u64& r0, u64& r1) {
@@ -561,6 +564,31 @@ __device__ __forceinline__ void plan_terms(const Prime& P, const u64* sk, u32 ti
         for (u32 dg = 0; dg < dnum; ++dg) x[t][dg] = d[((size_t)dg * R + r) * N + src[t]];
         c[t] = r < SH::L ? Ct[t][(size_t)r * N + src[t]] : 0;
     }
+#if HGM_PLAN_WIDE
+    if constexpr (NT == 2) {
+        // both terms' column sums folded into one 128-bit sum, reduced once
+        // (8 q^2 + q < 2^(s+63), reduce_acc_wide): one Barrett reduction per output
+        // instead of one per term
+        Acc s0{r0, 0}, s1{r1, 0};
+#pragma unroll
+        for (u32 t = 0; t < NT; ++t) {
+            Cols a0, a1;
+#pragma unroll
+            for (u32 dg = 0; dg < dnum; ++dg) {
+                const Dig<SH::S> xd = split<SH::S>(x[t][dg]);
+                a0.mac(xd, packed_dig<SH::S>(sk[((t * E) + 2 * dg) * kThreads + tid]));
+                a1.mac(xd, packed_dig<SH::S>(sk[((t * E) + 2 * dg + 1) * kThreads + tid]));
+            }
+            if (r < SH::L) a0.mac(split<SH::S>(c[t]), packed_dig<SH::S>(sk[((t * E) + 2 * dnum) * kThreads + tid]));
+            const Acc f0 = a0.fold<SH::S>(), f1 = a1.fold<SH::S>();
+            add128(s0.lo, s0.hi, f0.lo, f0.hi);
+            add128(s1.lo, s1.hi, f1.lo, f1.hi);
+        }
+        r0 = reduce_acc_wide(s0, P);
+        r1 = reduce_acc_wide(s1, P);
+        return;
+    }
+#endif
 #pragma unroll
     for (u32 t = 0; t < NT; ++t) {
         Cols a0, a1;
@@ -1844,6 +1872,77 @@ float Context::bench_inner_product(int items, int iters) {
     release(D);
     release(A);
     release(C0);
+    sync();
+    return ms / iters;
+}
+
+// k_ks_plan in the arrangement the cloud step launches it: tiles of `tile`
+// lockstep instances, `sums` masked sums of `terms` rotations per tile, every sum
+// of an instance reading that instance's ModUp digits and c0 (one source
+// ciphertext, as basic_mm's shifts of sigma(A)), masked keys shared by the tile.
+float Context::bench_plan(int instances, int sums, int terms, int tile, int iters) {
+    const u32 N = hp_.N, R = hp_.R, dnum = hp_.dnum;
+    const size_t dw = (size_t)dnum * R * N, aw = ks_words(), kw = masked_key_words();
+    u64* D = alloc((size_t)instances * dw);
+    u64* C0 = alloc((size_t)instances * ct_words());
+    u64* MK = alloc((size_t)sums * terms * kw);
+    u64* A = alloc((size_t)instances * sums * aw);
+    for (int i = 0; i < instances; ++i) {
+        fill_residues(D + i * dw, dnum * R, 0, R, 11 + i);
+        fill_residues(C0 + i * ct_words(), 2 * hp_.L, 0, hp_.L, 7 + i);
+    }
+    for (int k = 0; k < sums * terms; ++k) {  // random residues in packed digit form
+        fill_residues(MK + k * kw, dnum * 2 * R, 0, R, 1000 + k);
+        fill_residues(MK + k * kw + (size_t)dnum * 2 * R * N, hp_.L, 0, hp_.L, 5000 + k);
+    }
+    {
+        const size_t words = (size_t)sums * terms * kw;
+        const dim3 kg((unsigned)((words + 4 * kThreads - 1) / (4 * kThreads)));
+        if (hp_.L == 3) k_mask_digits<ShapeQ3><<<kg, kThreads, 0, stream_>>>(MK, words);
+        else k_mask_digits<ShapeQ8><<<kg, kThreads, 0, stream_>>>(MK, words);
+        ++launches_;
+    }
+    std::vector<PlanGroup> groups;
+    std::vector<const u64*> mkey, dig, c0;
+    std::vector<u32> gs;
+    std::vector<u64*> out;
+    for (int k0 = 0; k0 < instances; k0 += tile)
+        for (int s = 0; s < sums; ++s) {
+            PlanGroup G{};
+            G.item0 = (u32)out.size();
+            G.cnt = (u32)(std::min(instances, k0 + tile) - k0);
+            G.term0 = (u32)mkey.size();
+            G.nterms = (u32)terms;
+            G.dbase = (u32)dig.size();
+            for (int t = 0; t < terms; ++t) {
+                mkey.push_back(MK + ((size_t)s * terms + t) * kw);
+                gs.push_back(galois_of(1 + (s * terms + t) % 2047, N));
+            }
+            for (u32 u = 0; u < G.cnt; ++u) {
+                for (int t = 0; t < terms; ++t) {
+                    dig.push_back(D + (size_t)(k0 + u) * dw);
+                    c0.push_back(C0 + (size_t)(k0 + u) * ct_words());
+                }
+                out.push_back(A + ((size_t)(k0 + u) * sums + s) * aw);
+            }
+            groups.push_back(G);
+        }
+    rotate_plan(groups, mkey, gs, dig, c0, out);  // warm-up
+    cudaEvent_t e0, e1;
+    HGM_CUDA(cudaEventCreate(&e0));
+    HGM_CUDA(cudaEventCreate(&e1));
+    HGM_CUDA(cudaEventRecord(e0, stream_));
+    for (int it = 0; it < iters; ++it) rotate_plan(groups, mkey, gs, dig, c0, out);
+    HGM_CUDA(cudaEventRecord(e1, stream_));
+    HGM_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    HGM_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    release(D);
+    release(C0);
+    release(MK);
+    release(A);
     sync();
     return ms / iters;
 }

@@ -1519,6 +1519,17 @@ int hgm_bench_keyswitch(hgm_ctx* c, size_t items, int iters, float* ms) {
     });
 }
 
+int hgm_bench_keyswitch_plan(hgm_ctx* c, size_t instances, size_t sums, size_t terms, size_t tile, int iters,
+                             float* ms) {
+    std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
+    DeviceScope dev(c);
+    return guarded([&] {
+        if (instances == 0 || sums == 0 || terms == 0 || tile == 0 || iters <= 0 || !ms)
+            throw std::invalid_argument("bad benchmark arguments");
+        *ms = c->ctx->bench_plan((int)instances, (int)sums, (int)terms, (int)tile, iters);
+    });
+}
+
 int hgm_device_sync(hgm_ctx* c) {
     std::lock_guard<std::recursive_mutex> exec_lk(c->exec_mu);  // one device user at a time
     DeviceScope dev(c);

@@ -280,6 +280,16 @@ HD u64 reduce_acc(const Acc& a, const Prime& p) {
     const u64 r = a.lo - mul_lo_q(qh, p.q);
     return reduce_once(reduce_once(r, 2 * p.q), p.q);
 }
+// The same on x < 2^(s+63) (8 products of 60-bit residues and a residue): x >> (s-1)
+// fits 64 bits and 2 mu stands in for floor(2^(63+s) / q) (low by less than 2), so the
+// quotient estimate is low by less than 3 (+1 for the 3-partial-product high half):
+// r < 5q, three corrections.
+HD u64 reduce_acc_wide(const Acc& a, const Prime& p) {
+    const u64 x = (a.hi << (65 - p.s)) | (a.lo >> (p.s - 1));
+    const u64 qh = mulhi64_approx(x, p.mu << 1);
+    const u64 r = a.lo - mul_lo_q(qh, p.q);
+    return reduce_once(reduce_once(reduce_once(r, 4 * p.q), 2 * p.q), p.q);
+}
 // Column accumulator for sums of residue products.  Operands are split into
 // S-bit digits (residues < 2^(2S): S = 30 for 60-bit primes, 28 for 55-bit)
 // and multiplied Karatsuba-style: c0 += a_l b_l, c2 += a_h b_h,

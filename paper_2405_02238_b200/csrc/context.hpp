@@ -196,6 +196,7 @@ class Context {
     // rotations in groups of 8 sharing a Galois key, as the engine orders them;
     // returns ms per launch (CUDA events on the library stream)
     float bench_inner_product(int items, int iters);
+    float bench_plan(int instances, int sums, int terms, int tile, int iters);  // k_ks_plan, ms per launch
     u64 launches() const { return launches_.load(); }
 
   private:

@@ -456,6 +456,75 @@ __device__ __forceinline__ void store_last_stage(const u64* sm, u64* g, const ul
     }
 }
 
+// x < 16q -> [0, q) in one table step and one conditional subtraction: every
+// prime lies so close below 2^s (16 (2^s - q) < q, checked in params.cpp) that
+// x - floor(x / 2^s) q falls in [0, 2q).  tab[i] = i q, 16 entries in shared
+// memory (no multiply: the transforms are bound by the integer multiply pipe).
+// HGM_LAST_TAB: 1 table (default), 2 the product by IMAD instead, 0 the chain of
+// conditional subtractions (previous form).
+#ifndef HGM_LAST_TAB
+#define HGM_LAST_TAB 1
+#endif
+struct Canon {
+    const u64* tab;
+    u32 sh32;  // s - 32
+    u64 q;
+    __device__ __forceinline__ u64 operator()(u64 x) const {
+        const u32 k = (u32)(x >> 32) >> sh32;
+#if HGM_LAST_TAB == 2
+        return reduce_once(x - mul_lo_q((u64)k, q), q);
+#else
+        return reduce_once(x - tab[k], q);
+#endif
+    }
+};
+__device__ __forceinline__ Canon make_canon(u64* tab, const Prime& P) {
+    if (threadIdx.x < 16) tab[threadIdx.x] = (u64)threadIdx.x * P.q;  // visible after the next barrier
+    return Canon{tab, P.s - 32, P.q};
+}
+
+// Last stage with the table reduction: U < kU q (reduced by 8q once where the
+// round bounds allow more), V = w x in [0, 3q), outputs U + V and U - V + 3q
+// below (kU + 3) q canonicalised by `cn`.
+template <int LB, int E = kElems>
+__device__ __forceinline__ void store_last_stage_tab(const u64* sm, u64* g, const ulonglong2* __restrict__ tw_tab, u64 q,
+                                                     int logN, int blk, const Canon& cn) {
+    constexpr int NB = 1 << LB, T = NB / E;
+    constexpr bool kRedU = fwd_bound(LB - 1) > 12;  // U + V must stay below 16q
+    ulonglong2* g2 = reinterpret_cast<ulonglong2*>(g);
+    const int tw0 = (1 << (logN - 1)) + (blk << (LB - 1));
+    const u64 q3 = q + (q << 1), q8 = q << 3;
+#pragma unroll 8
+    for (int i = threadIdx.x; i < NB / 2; i += T) {
+        const ulonglong2 t = __ldg(tw_tab + tw0 + i);
+        const u64 u = sm[pad(2 * i)];
+        const u64 U = kRedU ? reduce_once(u, q8) : u;
+        const u64 V = shoup_lazy3(sm[pad(2 * i + 1)], t.x, t.y, q);
+        ulonglong2 v;
+        v.x = cn(U + V);
+        v.y = cn(U - V + q3);
+        g2[i] = v;
+    }
+}
+// The same handing (U + V, U - V + 3q), both below 11q, to `st`: the consumer may
+// add up to 4q more before canonicalising with the same table.
+template <int LB, typename St, int E = kElems>
+__device__ __forceinline__ void store_last_stage_io_tab(const u64* sm, const St& st, const ulonglong2* __restrict__ tw_tab,
+                                                        u64 q, int logN, int blk) {
+    constexpr int NB = 1 << LB, T = NB / E;
+    constexpr bool kRedU = fwd_bound(LB - 1) > 8;
+    const int tw0 = (1 << (logN - 1)) + (blk << (LB - 1));
+    const u64 q3 = q + (q << 1), q8 = q << 3;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < NB / 2; i += T) {
+        const ulonglong2 t = __ldg(tw_tab + tw0 + i);
+        const u64 u = sm[pad(2 * i)];
+        const u64 U = kRedU ? reduce_once(u, q8) : u;
+        const u64 V = shoup_lazy3(sm[pad(2 * i + 1)], t.x, t.y, q);
+        st(i, U + V, U - V + q3);
+    }
+}
+
 // Same, handing each finished pair (elements 2i, 2i+1, in [0, 4q)) to `st`.
 template <int LB, typename St, int E = kElems>
 __device__ __forceinline__ void store_last_stage_io(const u64* sm, const St& st, const ulonglong2* __restrict__ tw_tab, u64 q, int logN, int blk) {
@@ -659,6 +728,10 @@ __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_fwd_io(DevCtx cx
     const int prime = io.prime(job);
     const u64 q = dp->pr[prime].q;
     const u64* w = cx.tw + (size_t)prime * 4 * N;
+#if HGM_LAST_TAB
+    __shared__ u64 qtab[16];
+    const Canon cn = make_canon(qtab, dp->pr[prime]);
+#endif
     fill_tw_cache(cache, pairs(w), 0, 0, kTwCache3);
     __syncthreads();
     auto ld = [&](int j) { return io.load(dp, job, (u32)j); };
@@ -668,8 +741,13 @@ __global__ void __launch_bounds__((1 << LB) / kElems3, 3) k_ntt_fwd_io(DevCtx cx
     __syncthreads();
     fwd_round<LB, 8, LB - 9, false, false, NoLoad, kElems3>(sm, cache, pairs(w), q, 0, 0);
     __syncthreads();
+#if HGM_LAST_TAB
+    auto st = [&](int i, u64 v0, u64 v1) { io.store_lazy(dp, job, (u32)i, v0, v1, cn); };
+    store_last_stage_io_tab<LB, decltype(st), kElems3>(sm, st, pairs(w), q, logN, 0);
+#else
     auto st = [&](int i, u64 v0, u64 v1) { io.store(dp, job, (u32)i, v0, v1); };
     store_last_stage_io<LB, decltype(st), kElems3>(sm, st, pairs(w), q, logN, 0);
+#endif
 }
 
 // y < src < 2*dst (one bit length per prime set): centred y mod dst
@@ -708,6 +786,13 @@ struct ModUpIO {
         ulonglong2 v;
         v.x = reduce_once(reduce_once(v0, q << 1), q);
         v.y = reduce_once(reduce_once(v1, q << 1), q);
+        reinterpret_cast<ulonglong2*>(D + (size_t)job * N)[i] = v;
+    }
+    // v0, v1 < 11q (store_last_stage_io_tab)
+    __device__ void store_lazy(const DevParams*, u32 job, u32 i, u64 v0, u64 v1, const Canon& cn) const {
+        ulonglong2 v;
+        v.x = cn(v0);
+        v.y = cn(v1);
         reinterpret_cast<ulonglong2*>(D + (size_t)job * N)[i] = v;
     }
 };
@@ -763,6 +848,25 @@ struct ModDownIO {
         v.y = reduce_once(reduce_once(reduce_once(r1, q4), q2), q);
         reinterpret_cast<ulonglong2*>(out[item] + ((size_t)c * L + i) * N)[i2] = v;
     }
+    // v0, v1 < 11q (store_last_stage_io_tab): + Shoup < 3q + addend < q stays below 15q,
+    // canonicalised by the table step
+    __device__ void store_lazy(const DevParams* dp, u32 job, u32 i2, u64 v0, u64 v1, const Canon& cn) const {
+        const u32 item = job / (2 * L), c = (job / L) & 1, i = job % L;
+        const u64 q = dp->pr[i].q, pi = dp->P_inv_q[i], pis = dp->P_inv_q_sh[i];
+        const ulonglong2 av = __ldcs(reinterpret_cast<const ulonglong2*>(acc[item] + ((size_t)c * R + i) * N) + i2);
+        u64 r0 = v0 + shoup_lazy3(av.x, pi, pis, q);
+        u64 r1 = v1 + shoup_lazy3(av.y, pi, pis, q);
+        if (c == 0 && addn) {
+            const u64* x = addn[item] + (size_t)i * N;
+            const u32 ge = g[item];
+            r0 += x[ge == 1 ? 2 * i2 : galois_src(2 * i2, ge, logN)];
+            r1 += x[ge == 1 ? 2 * i2 + 1 : galois_src(2 * i2 + 1, ge, logN)];
+        }
+        ulonglong2 v;
+        v.x = cn(r0);
+        v.y = cn(r1);
+        reinterpret_cast<ulonglong2*>(out[item] + ((size_t)c * L + i) * N)[i2] = v;
+    }
 };
 
 // ModDown's forward NTT with the finishing pass fused into its store: input is
@@ -812,6 +916,10 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__((1 << LB) / kElems3,
     const int prime = io.prime(job);
     const u64 q = dp->pr[prime].q;
     const u64* w = cx.tw + (size_t)prime * 4 * N;
+#if HGM_LAST_TAB
+    __shared__ u64 qtab[16];
+    const Canon cn = make_canon(qtab, dp->pr[prime]);
+#endif
     fill_tw_cache_async(cache, pairs(w), 2, blk, kTwCache3);
     const ulonglong2* t = pairs(w);
     const u64 w1 = t[1].x, w1s = t[1].y, w2 = t[2].x, w2s = t[2].y, w3 = t[3].x, w3s = t[3].y;
@@ -853,8 +961,13 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__((1 << LB) / kElems3,
     fwd_round<LB, 8, LB - 9, false, false, NoLoad, kElems3>(sm, cache, pairs(w), q, 2, blk);
     __syncthreads();
     const u32 pair0 = (u32)blk << (LB - 1);
+#if HGM_LAST_TAB
+    auto st = [&](int i, u64 v0, u64 v1) { io.store_lazy(dp, job, pair0 + (u32)i, v0, v1, cn); };
+    store_last_stage_io_tab<LB, decltype(st), kElems3>(sm, st, pairs(w), q, logN, blk);
+#else
     auto st = [&](int i, u64 v0, u64 v1) { io.store(dp, job, pair0 + (u32)i, v0, v1); };
     store_last_stage_io<LB, decltype(st), kElems3>(sm, st, pairs(w), q, logN, blk);
+#endif
 }
 
 template <typename IO>
@@ -1057,6 +1170,10 @@ __global__ void __launch_bounds__((1 << LB) / E, MINB) k_ntt_fwd3(DevCtx cx, Ntt
     const u64* w = cx.tw + (size_t)jv.prime * 4 * N;
     u64* g = jv.ptr + ((size_t)blk << LB);
     const u64* src = jobs.src ? jobs.src[blockIdx.x] + ((size_t)blk << LB) : g;
+#if HGM_LAST_TAB
+    __shared__ u64 qtab[16];
+    const Canon cn = make_canon(qtab, dp->pr[jv.prime]);
+#endif
     l2_prefetch_ahead<LB>(jobs, N);
     auto ld = [src](int j) { return __ldcs(src + j); };
     // group 0 of the first round is loaded while the twiddle cache fills
@@ -1073,7 +1190,11 @@ __global__ void __launch_bounds__((1 << LB) / E, MINB) k_ntt_fwd3(DevCtx cx, Ntt
     __syncthreads();
     fwd_round<LB, 8, LB - 9, false, false, NoLoad, E>(sm, cache, pairs(w), q, pre, blk);
     __syncthreads();
+#if HGM_LAST_TAB
+    store_last_stage_tab<LB, E>(sm, g, pairs(w), q, logN, blk, cn);
+#else
     store_last_stage<LB, E>(sm, g, pairs(w), q, logN, blk);
+#endif
 }
 
 template <int LB, int E = kElems3, int MINB = 3>
@@ -1341,6 +1462,10 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__((1 << LB) / kElems3,
     const JobView jv = job_of(jobs, blockIdx.x >> 2, N);
     const u64 q = dp->pr[jv.prime].q;
     const u64* w = cx.tw + (size_t)jv.prime * 4 * N;
+#if HGM_LAST_TAB
+    __shared__ u64 qtab[16];
+    const Canon cn = make_canon(qtab, dp->pr[jv.prime]);
+#endif
     fill_tw_cache_async(cache, pairs(w), 2, blk, kTwCache3);
     const ulonglong2* t = pairs(w);
     const u64 w1 = t[1].x, w1s = t[1].y, w2 = t[2].x, w2s = t[2].y, w3 = t[3].x, w3s = t[3].y;
@@ -1382,7 +1507,11 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__((1 << LB) / kElems3,
     __syncthreads();
     fwd_round<LB, 8, LB - 9, false, false, NoLoad, kElems3>(sm, cache, pairs(w), q, 2, blk);
     __syncthreads();
+#if HGM_LAST_TAB
+    store_last_stage_tab<LB, kElems3>(sm, jv.ptr + ((size_t)blk << LB), pairs(w), q, logN, blk, cn);
+#else
     store_last_stage<LB, kElems3>(sm, jv.ptr + ((size_t)blk << LB), pairs(w), q, logN, blk);
+#endif
 }
 
 template <int LB>

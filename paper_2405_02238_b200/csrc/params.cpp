@@ -75,6 +75,10 @@ Prime prime_of(u64 q, unsigned N) {
     p.q = q;
     p.s = 64 - __builtin_clzll(q);
     p.mu = (u64)(((u128)1 << (62 + p.s)) / q);
+    // ntt.cu Canon: x < 16q is canonicalised as x - floor(x / 2^s) q, then one
+    // conditional subtraction; that needs 16 (2^s - q) < q (t = 65537 has its own kernel)
+    if (q != kT && (p.s < 33 || (((u128)1 << p.s) - q) * 16 >= q))
+        throw std::invalid_argument("prime too far below a power of two for the table reduction");
     p.ninv = invmod(N % q, q);
     p.ninv_sh = shoup_of(p.ninv, q);
     return p;

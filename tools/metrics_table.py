@@ -5,6 +5,7 @@ import sys
 
 KEYS = ["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_elapsed",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active"]
 
 
@@ -29,7 +30,7 @@ def main(path):
         a["regs"] = m["launch__registers_per_thread"]
     tot = sum(a["t"] for a in agg.values())
     print(f"total {tot / 1e6:.2f} ms over {sum(int(a['n']) for a in agg.values())} launches")
-    print(f"{'kernel':30s} {'n':>4s} {'share':>6s} {'avg_us':>8s} {'GB/s':>7s} {'dram%':>6s} {'fmaH%':>6s} "
+    print(f"{'kernel':30s} {'n':>4s} {'share':>6s} {'avg_us':>8s} {'GB/s':>7s} {'dram%':>6s} {'fmaH%':>6s} {'alu%':>6s} "
           f"{'issue%':>6s} {'warps%':>6s} regs")
     for k, a in sorted(agg.items(), key=lambda kv: -kv[1]["t"]):
         t = a["t"]

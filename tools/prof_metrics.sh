@@ -4,6 +4,6 @@ set -e
 python tools/profile_step.py ${K:-256} > gpurun_out/prof_plain.txt 2>&1
 SKIP=$(sed -n 's/.*skip=\([0-9]*\).*/\1/p' gpurun_out/prof_plain.txt)
 CNT=$(sed -n 's/.*count=\([0-9]*\).*/\1/p' gpurun_out/prof_plain.txt)
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__warps_active.avg.pct_of_peak_sustained_active,launch__registers_per_thread,launch__grid_size \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_elapsed,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__warps_active.avg.pct_of_peak_sustained_active,launch__registers_per_thread,launch__grid_size \
   --clock-control none -s $SKIP -c $CNT --csv --log-file gpurun_out/metrics.csv python tools/profile_step.py ${K:-256} > gpurun_out/ncu_metrics.log 2>&1
 echo ncu_rc=$?
