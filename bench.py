@@ -327,7 +327,7 @@ def ntt_roofline(ctx, limb_bytes, label):
                                "achieved": round(pl_gbs, 1), "frac": round(pl_gbs / peak, 4),
                                "unfused_bytes_per_sum": int(unfused),
                                "unfused_equivalent_gbs": round(pl_n * unfused / (pl_ms / 1e3) / 1e9, 1),
-                               "int_pipes_ncu": plan_pipes(ctx.N)},
+                               "traffic": plan_traffic(ctx.N, pl_n), "int_pipes_ncu": plan_pipes(ctx.N)},
             "keyswitch": {"kernel": "k_ks_inner (key inner product of one rotation, Galois gather fused, 8 rotations per key read; relinearisation and uncached programs)",
                           "rotations_per_launch": ks_items, "algorithmic_bytes_per_rotation": int(ks_bytes),
                           "traffic": ks_traffic(ctx.N, ks_items), "int_pipes_ncu": ks_pipes(ctx.N),
@@ -343,6 +343,18 @@ def ks_traffic(N, items):
         rec = json.load(open(prof))
         if rec.get("N") == N and rec.get("bytes_per_rotation"):
             return rec["bytes_per_rotation"] * items
+    except Exception:
+        pass
+    return None
+
+
+def plan_traffic(N, sums):
+    """DRAM bytes per k_ks_plan launch from the committed ncu --set full capture of the
+    same launch (profiles/ks_plan_traffic.json); None if absent."""
+    try:
+        rec = json.load(open(os.path.join(ROOT, "profiles", "ks_plan_traffic.json")))
+        if rec.get("N") == N and rec.get("bytes_per_sum"):
+            return rec["bytes_per_sum"] * sums
     except Exception:
         pass
     return None
