@@ -515,7 +515,10 @@ __global__ void k_ks_inner(DevCtx cx, u32 n, const u64* const* D,
 // k_ks_plan computes a whole masked sum of rotations as one longer inner
 // product, with neither the rotations' accumulators nor a separate masked sum.
 template <typename SH>
-__global__ void k_mask_key(DevCtx cx, const u64* key, const u64* const* masks, u32 n_masks, u64* out) {
+// pre: the Q limbs' mask is multiplied by P^-1 mod q_r first, so the sum k_ks_plan
+// computes over Q is P^-1 (acc + P phi(c0)) and ModDown's finishing pass adds it
+// without its Shoup product (exact: the same canonical residue).
+__global__ void k_mask_key(DevCtx cx, const u64* key, const u64* const* masks, u32 n_masks, u64* out, u32 pre) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, R = SH::R, L = SH::L, dnum = SH::dnum;
     auto unpack = [](u64 p) { return (u64)(u32)p + ((p >> 32) << SH::S); };
@@ -528,6 +531,7 @@ __global__ void k_mask_key(DevCtx cx, const u64* key, const u64* const* masks, u
         const Prime& P = dp->pr[r];
         u64 m = 0;
         for (u32 i = 0; i < n_masks; ++i) m = add_mod(m, unpack(masks[i][w]), P.q);
+        if (pre && r < L) m = mul_mod(m, dp->P_inv_q[r], P);
         for (u32 dg = 0; dg < dnum; ++dg)
             for (u32 c = 0; c < 2; ++c) {
                 const size_t o = (((size_t)dg * 2 + c) * R + r) * N + j;
@@ -702,7 +706,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_moddown_conv(DevCtx cx, u32 n, 
 // out_c = NTT(V_c) + P^-1 acc_c  (+ addn[galois_src] for c = 0)
 template <typename SH>
 __global__ void k_ks_finish(DevCtx cx, u32 n, const u64* const* acc, const u64* V, const u64* const* addn,
-                            const u32* g, u64* const* out) {
+                            const u32* g, u64* const* out, u32 pre) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = SH::L, R = SH::R, logN = dp->logN;
     ITEM_LOOP {
@@ -716,8 +720,9 @@ __global__ void k_ks_finish(DevCtx cx, u32 n, const u64* const* acc, const u64* 
             for (u32 i = 0; i < L; ++i) {
                 const u64 q = dp->pr[i].q;
                 const u64 pi = dp->P_inv_q[i], pis = dp->P_inv_q_sh[i];
-                u64 r0 = add_mod(v[(size_t)i * N + j], shoup_mul(a[(size_t)i * N + j], pi, pis, q), q);
-                const u64 r1 = add_mod(v[((size_t)L + i) * N + j], shoup_mul(a[((size_t)R + i) * N + j], pi, pis, q), q);
+                const u64 a0 = a[(size_t)i * N + j], a1 = a[((size_t)R + i) * N + j];
+                u64 r0 = add_mod(v[(size_t)i * N + j], pre ? a0 : shoup_mul(a0, pi, pis, q), q);
+                const u64 r1 = add_mod(v[((size_t)L + i) * N + j], pre ? a1 : shoup_mul(a1, pi, pis, q), q);
                 if (x0) r0 = add_mod(r0, x0[(size_t)i * N + src], q);
                 o[(size_t)i * N + j] = r0;
                 o[((size_t)L + i) * N + j] = r1;
@@ -1976,7 +1981,9 @@ bool Context::tail_keeps_acc() const {
 }
 
 void Context::key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, const u64* const* addn,
-                              const u32* g, u64* const* out) {
+                              const u32* g, u64* const* out, bool prescaled) {
+    if (prescaled && ntt_fusable(hp_.dev, kFuseModDown))
+        throw std::logic_error("prescaled accumulators need the split ModDown path");
     const u32 N = hp_.N, L = hp_.L, K = hp_.K, R = hp_.R;
     std::vector<u64*> va(acc, acc + n);
     u64* const* dacc = upload(va);
@@ -2035,11 +2042,11 @@ void Context::key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, c
         if (Pc) release(Pc);
     }
     if (ntt_finish_fusable(hp_.dev)) {
-        ntt_finish_fused(cx_, hp_.dev, n, V, dacc, dadd, upload(vg), upload(vo), stream_);
+        ntt_finish_fused(cx_, hp_.dev, n, V, dacc, dadd, upload(vg), upload(vo), stream_, prescaled);
         ++launches_;
     } else {
         ntt(true, jobs_contig(V, n * 2 * L, 0, L));
-        if (hp_.L == 3) k_ks_finish<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, dacc, V, dadd, upload(vg), upload(vo)); else k_ks_finish<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, dacc, V, dadd, upload(vg), upload(vo)); ++launches_;
+        if (hp_.L == 3) k_ks_finish<ShapeQ3><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, dacc, V, dadd, upload(vg), upload(vo), prescaled ? 1u : 0u); else k_ks_finish<ShapeQ8><<<grid_of(N, n), kThreads, 0, stream_>>>(cx_, n, dacc, V, dadd, upload(vg), upload(vo), prescaled ? 1u : 0u); ++launches_;
     }
     release(V);
     HGM_CUDA(cudaGetLastError());
@@ -2195,10 +2202,11 @@ void Context::trim_masked_keys(size_t needed) {
     }
 }
 
-const u64* Context::masked_key(u32 g, const std::vector<u64>& ids, const std::vector<const u64*>* mask_dev) {
+const u64* Context::masked_key(u32 g, const std::vector<u64>& ids, const std::vector<const u64*>* mask_dev,
+                               bool prescaled) {
     std::vector<u64> id(ids);
     std::sort(id.begin(), id.end());
-    id.insert(id.begin(), (u64)g);
+    id.insert(id.begin(), (u64)g | ((u64)(prescaled ? 1 : 0) << 32));
     {
         std::lock_guard<std::mutex> lk(mask_mu_);
         auto it = mkeys_.find(id);
@@ -2215,9 +2223,9 @@ const u64* Context::masked_key(u32 g, const std::vector<u64>& ids, const std::ve
     const u32 words = hp_.R * hp_.N;
     const dim3 grid((words + kThreads - 1) / kThreads);
     if (hp_.L == 3)
-        k_mask_key<ShapeQ3><<<grid, kThreads, 0, stream_>>>(cx_, key, dm, (u32)mask_dev->size(), out);
+        k_mask_key<ShapeQ3><<<grid, kThreads, 0, stream_>>>(cx_, key, dm, (u32)mask_dev->size(), out, prescaled ? 1u : 0u);
     else
-        k_mask_key<ShapeQ8><<<grid, kThreads, 0, stream_>>>(cx_, key, dm, (u32)mask_dev->size(), out);
+        k_mask_key<ShapeQ8><<<grid, kThreads, 0, stream_>>>(cx_, key, dm, (u32)mask_dev->size(), out, prescaled ? 1u : 0u);
     ++launches_;
     HGM_CUDA(cudaGetLastError());
     std::lock_guard<std::mutex> lk(mask_mu_);
@@ -2254,7 +2262,15 @@ void Context::rotate_plan(const std::vector<PlanGroup>& groups, const std::vecto
     HGM_CUDA(cudaGetLastError());
 }
 
-void Context::moddown(int n, const u64* const* acc, u64* const* out) {
+bool Context::can_prescale() const {
+    static const bool on = [] {
+        const char* e = std::getenv("HGM_PRESCALE");
+        return !(e && e[0] == '0');
+    }();
+    return on && !ntt_fusable(hp_.dev, kFuseModDown);
+}
+
+void Context::moddown(int n, const u64* const* acc, u64* const* out, bool prescaled) {
     if (n <= 0) return;
     const int chunk = chunk_for((size_t)(2 * hp_.R + 2 * hp_.L) * hp_.N, kChunkKs);
     for (int c0 = 0; c0 < n; c0 += chunk) {
@@ -2267,12 +2283,12 @@ void Context::moddown(int n, const u64* const* acc, u64* const* out) {
             std::vector<u64*> dst(cn);
             for (int i = 0; i < cn; ++i) dst[i] = A + (size_t)i * ks_words();
             k_copy<<<grid_of(hp_.N, cn), kThreads, 0, stream_>>>(cn, ks_words(), upload(src), upload(dst)); ++launches_;
-            key_switch_tail(cn, dst.data(), nullptr, nullptr, ones.data(), out + c0);
+            key_switch_tail(cn, dst.data(), nullptr, nullptr, ones.data(), out + c0, prescaled);
             release(A);
         } else {
             std::vector<u64*> va(cn);
             for (int i = 0; i < cn; ++i) va[i] = const_cast<u64*>(acc[c0 + i]);
-            key_switch_tail(cn, va.data(), nullptr, nullptr, ones.data(), out + c0);
+            key_switch_tail(cn, va.data(), nullptr, nullptr, ones.data(), out + c0, prescaled);
         }
     }
 }

@@ -154,7 +154,7 @@ class Context {
     size_t ks_words() const { return (size_t)2 * hp_.R * hp_.N; }
     void rotate_acc(int n, const u64* const* modup, const u64* const* ct, const u32* g, u64* const* acc);
     // out = ModDown(acc) (acc is left intact)
-    void moddown(int n, const u64* const* acc, u64* const* out);
+    void moddown(int n, const u64* const* acc, u64* const* out, bool prescaled = false);
     // Masked sums of rotations straight from the ModUp digits (k_ks_plan).
     // masked_key: key_g (.) (sum of the masks) over Q ++ P followed by (P mod q) (.)
     // (that sum) over Q, packed digits, cached per (g, mask ids) -- the ids are the
@@ -162,7 +162,11 @@ class Context {
     // (mask_plain; null = look up only); nullptr when absent / the cache budget
     // cannot take another entry.
     size_t masked_key_words() const { return ((size_t)hp_.dnum * 2 * hp_.R + hp_.L) * hp_.N; }
-    const u64* masked_key(u32 g, const std::vector<u64>& ids, const std::vector<const u64*>* mask_dev);
+    // prescaled: the Q limbs' masks carry P^-1, so the sum over Q is P^-1 (acc + P phi(c0))
+    // and moddown(..., prescaled) adds it without the Shoup product (can_prescale())
+    const u64* masked_key(u32 g, const std::vector<u64>& ids, const std::vector<const u64*>* mask_dev,
+                          bool prescaled = false);
+    bool can_prescale() const;
     size_t masked_key_budget() const;
     bool masked_keys_fit(size_t count) const { return count * masked_key_words() * 8 <= masked_key_budget(); }
     void trim_masked_keys(size_t needed);  // between programs: room for `needed` more entries
@@ -206,7 +210,7 @@ class Context {
     u64* b_extend(int n, const u64* const* a, const u64* const* b);
     void scale_relin(int n, u64* T, u64* const* out);
     void key_switch_tail(int n, u64* const* acc, const u64* const* ecoef, const u64* const* addn,
-                         const u32* g, u64* const* out);
+                         const u32* g, u64* const* out, bool prescaled = false);
     bool tail_keeps_acc() const;
     void inner_product(int n, const u64* const* digits, const u64* const* keys, const u32* g,
                        u64* const* acc, const u64* const* c0 = nullptr);

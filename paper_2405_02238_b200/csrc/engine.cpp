@@ -305,7 +305,18 @@ Schedule optimise(const Program& p) {
             }
             if (!changed) s.virt = v;
         }
-        std::map<std::pair<u32, std::vector<u64>>, int> distinct;
+        // a sum with only a key-switch part whose every reader is a ModDown (Mat) and
+        // that is no output itself: its accumulator may be kept as P^-1 acc over Q
+        s.prescale.assign(n, 0);
+        for (size_t i = 0; i < n; ++i)
+            s.prescale[i] = fus[i] && kind[i] == kPartA && !s.is_output[i] && !s.is_pending_output[i];
+        for (size_t j = 0; j < n; ++j) {
+            if (!live[j]) continue;
+            const PNode& rd = q.nodes[j];
+            for (int x : rd.in)
+                if (rd.kind != PNode::Mat) s.prescale[x] = 0;
+        }
+        std::map<std::pair<u64, std::vector<u64>>, int> distinct;
         for (size_t i = 0; i < n; ++i) {
             if (!fus[i]) continue;
             const PNode& nd = q.nodes[i];
@@ -328,7 +339,7 @@ Schedule optimise(const Program& p) {
                 std::vector<u64> ids;
                 for (const MaskRef& m : k.masks) ids.push_back(m->id);
                 std::sort(ids.begin(), ids.end());
-                distinct.emplace(std::make_pair(k.g, std::move(ids)), 0);
+                distinct.emplace(std::make_pair((u64)k.g | ((u64)s.prescale[i] << 32), std::move(ids)), 0);
             }
             ++s.ks_comb_count;
         }
@@ -410,6 +421,8 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
     g_counters.levels = sch.levels.size();
     ctx.trim_mask_cache();  // between programs: no mask pointer is held here yet
     const bool masked_keys_ok = sch.masked_key_count > 0 && ctx.masked_keys_fit(sch.masked_key_count);
+    const bool prescale_ok = ctx.can_prescale();
+    std::vector<char> prescaled_now(P.nodes.size(), 0);  // set when a sum ran over P^-1-scaled masked keys
     if (masked_keys_ok) ctx.trim_masked_keys(sch.masked_key_count);
     std::vector<u64*> buf(P.nodes.size(), nullptr);
     std::vector<PartLayout> lay(P.nodes.size());
@@ -535,14 +548,15 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
                 for (size_t ci = 0; ci < kcomb.size(); ++ci) {
                     const std::vector<KsTerm>& kts = sch.ks_terms[kcomb[ci]];
                     bool ok = masked_keys_ok;
+                    const bool pre = prescale_ok && sch.prescale[kcomb[ci]];
                     for (size_t t = 0; t < kts.size() && ok; ++t) {
                         std::vector<u64> ids;
                         std::vector<const u64*> devs;
                         for (const MaskRef& m : kts[t].masks) ids.push_back(m->id);
-                        const u64* d = ctx.masked_key(kts[t].g, ids, nullptr);  // cached?
+                        const u64* d = ctx.masked_key(kts[t].g, ids, nullptr, pre);  // cached?
                         if (!d) {
                             for (const MaskRef& m : kts[t].masks) devs.push_back(resolve(m));
-                            d = ctx.masked_key(kts[t].g, ids, &devs);
+                            d = ctx.masked_key(kts[t].g, ids, &devs, pre);
                         }
                         if (!d) ok = false;
                         mk[ci].push_back(d);
@@ -550,6 +564,8 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
                     if (!ok) {
                         mk[ci].clear();
                         slow.push_back(kcomb[ci]);
+                    } else if (pre) {
+                        prescaled_now[kcomb[ci]] = 1;  // its accumulators hold P^-1 acc over Q
                     }
                 }
                 // one group per (tile of instances, sum); tiles in order, sum by sum inside a
@@ -742,8 +758,8 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
         }
         if (!mat.empty()) {
             // products (+ plain part), then ModDown of key-switch parts, added
-            std::vector<const u64*> T, Xp, A1, A2;
-            std::vector<u64*> outT, outA1, outA2;
+            std::vector<const u64*> T, Xp, A1, A1p, A2;
+            std::vector<u64*> outT, outA1, outA1p, outA2;
             std::vector<const u64*> addx_a, addx_b;
             std::vector<u64*> addx_o;
             for (int x : mat) {
@@ -760,8 +776,8 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
                             outA2.push_back(o);
                         }
                     } else {  // key switch part (+ plain part)
-                        A1.push_back(part(src, k, kPartA));
-                        outA1.push_back(o);
+                        (prescaled_now[src] ? A1p : A1).push_back(part(src, k, kPartA));
+                        (prescaled_now[src] ? outA1p : outA1).push_back(o);
                         if (ks & kPartX) {
                             addx_a.push_back(o);
                             addx_b.push_back(part(src, k, kPartX));
@@ -788,6 +804,7 @@ std::vector<u64*> execute(Context& ctx, const Schedule& sch, const ExecIO& io) {
                 }
             }
             if (!A1.empty()) ctx.moddown((int)A1.size(), A1.data(), outA1.data());
+            if (!A1p.empty()) ctx.moddown((int)A1p.size(), A1p.data(), outA1p.data(), true);
             if (!addx_o.empty()) ctx.add((int)addx_o.size(), addx_a.data(), addx_b.data(), addx_o.data());
             if (!A2.empty()) {  // T and A together: ModDown into a temporary, added
                 u64* tmp = ctx.alloc(A2.size() * ctx.ct_words());

@@ -107,6 +107,9 @@ struct Schedule {
     // read only by such sums is virtual (no level, no buffer).
     std::vector<std::vector<KsTerm>> ks_terms;
     std::vector<char> virt;
+    // prescale[x]: masked sum x (ks_terms) is read only by its own ModDown, so its
+    // masked keys may carry P^-1 over Q and that ModDown skips the product
+    std::vector<char> prescale;
     size_t ks_comb_count = 0, masked_key_count = 0, acc_comb_count = 0;
     size_t stored_rot_count = 0;  // rot_count counts every rotation after CSE, stored or not
 };

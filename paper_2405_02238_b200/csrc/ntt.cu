@@ -801,7 +801,10 @@ struct ModUpIO {
 //   out_c,i = NTT(addc_c,i - P^-1 conv_c,i) + P^-1 acc_c,i + [c = 0] addn_i[galois_src]
 // which equals the oracle's (acc - NTT(conv)) P^-1 (+ NTT(addc)) (+ phi(c0)) by
 // linearity of the NTT mod q_i -- exact.
-struct ModDownIO {
+// kPre: acc's Q limbs already hold P^-1 acc (k_ks_plan over masked keys scaled by
+// P^-1, Context::masked_key): the store adds them as they are.
+template <bool kPre>
+struct ModDownIOT {
     u64* const* acc;         // per item [2][R][N]; P limbs already inverse-transformed
     const u64* const* addc;  // per item [2][L][N] coefficient-domain addend, or null
     const u64* const* addn;  // per item [L][N] NTT-domain addend for c = 0, or null
@@ -834,8 +837,8 @@ struct ModDownIO {
         const u64 q = dp->pr[i].q, pi = dp->P_inv_q[i], pis = dp->P_inv_q_sh[i];
         const ulonglong2 av = __ldcs(reinterpret_cast<const ulonglong2*>(acc[item] + ((size_t)c * R + i) * N) + i2);
         // lazy sums (v < 4q, Shoup < 3q, addend < q), one reduction chain from [0, 8q)
-        u64 r0 = v0 + shoup_lazy3(av.x, pi, pis, q);
-        u64 r1 = v1 + shoup_lazy3(av.y, pi, pis, q);
+        u64 r0 = v0 + (kPre ? av.x : shoup_lazy3(av.x, pi, pis, q));
+        u64 r1 = v1 + (kPre ? av.y : shoup_lazy3(av.y, pi, pis, q));
         if (c == 0 && addn) {
             const u64* x = addn[item] + (size_t)i * N;
             const u32 ge = g[item];
@@ -854,8 +857,8 @@ struct ModDownIO {
         const u32 item = job / (2 * L), c = (job / L) & 1, i = job % L;
         const u64 q = dp->pr[i].q, pi = dp->P_inv_q[i], pis = dp->P_inv_q_sh[i];
         const ulonglong2 av = __ldcs(reinterpret_cast<const ulonglong2*>(acc[item] + ((size_t)c * R + i) * N) + i2);
-        u64 r0 = v0 + shoup_lazy3(av.x, pi, pis, q);
-        u64 r1 = v1 + shoup_lazy3(av.y, pi, pis, q);
+        u64 r0 = v0 + (kPre ? av.x : shoup_lazy3(av.x, pi, pis, q));
+        u64 r1 = v1 + (kPre ? av.y : shoup_lazy3(av.y, pi, pis, q));
         if (c == 0 && addn) {
             const u64* x = addn[item] + (size_t)i * N;
             const u32 ge = g[item];
@@ -872,14 +875,17 @@ struct ModDownIO {
 // ModDown's forward NTT with the finishing pass fused into its store: input is
 // V = ecoef - P^-1 conv (k_moddown_conv), job = (item, component c, limb i) over
 // the contiguous [n][2][L][N] buffer; the store is ModDownIO's.
-struct FinishIO : ModDownIO {
+using ModDownIO = ModDownIOT<false>;
+template <bool kPre>
+struct FinishIOT : ModDownIOT<kPre> {
     const u64* V;
     __device__ void prefetch(u32 job) const {
-        pf_l2(V + (size_t)job * N, N * 8);
-        if (pf_mode == 1) prefetch_store(job);
+        pf_l2(V + (size_t)job * this->N, this->N * 8);
+        if (pf_mode == 1) this->prefetch_store(job);
     }
-    __device__ u64 load(const DevParams*, u32 job, u32 j) const { return __ldcs(V + (size_t)job * N + j); }
+    __device__ u64 load(const DevParams*, u32 job, u32 j) const { return __ldcs(V + (size_t)job * this->N + j); }
 };
+using FinishIO = FinishIOT<false>;
 
 bool ntt_l2_prefetch();
 int sm_count();
@@ -1656,7 +1662,14 @@ bool ntt_finish_fusable(const DevParams& hp) {
 }
 
 void ntt_finish_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* V, u64* const* acc,
-                      const u64* const* addn, const u32* g, u64* const* out, cudaStream_t s) {
+                      const u64* const* addn, const u32* g, u64* const* out, cudaStream_t s, bool prescaled) {
+    if (prescaled) {
+        FinishIOT<true> io;
+        static_cast<ModDownIOT<true>&>(io) = ModDownIOT<true>{acc, nullptr, addn, g, out, hp.L, hp.K, hp.R, hp.N, hp.logN};
+        io.V = V;
+        launch_fwd_io(cx, hp, io, (u32)n * 2 * hp.L, s);
+        return;
+    }
     FinishIO io;
     static_cast<ModDownIO&>(io) = ModDownIO{acc, nullptr, addn, g, out, hp.L, hp.K, hp.R, hp.N, hp.logN};
     io.V = V;

@@ -73,7 +73,8 @@ void ntt_moddown_fused(const DevCtx& cx, const DevParams& hp, int n, u64* const*
 // (HGM_FUSED_FINISH=0 disables) for whole-limb transforms.
 bool ntt_finish_fusable(const DevParams& hp);
 void ntt_finish_fused(const DevCtx& cx, const DevParams& hp, int n, const u64* V, u64* const* acc,
-                      const u64* const* addn, const u32* g, u64* const* out, cudaStream_t s);
+                      const u64* const* addn, const u32* g, u64* const* out, cudaStream_t s,
+                      bool prescaled = false);  // prescaled: acc's Q limbs hold P^-1 acc already
 // INTT of acc's P limb with k_moddown_conv fused into its store (K = 1, whole
 // limbs; default on, HGM_FUSED_CONV=0 disables): writes V = ecoef - P^-1 conv.
 bool ntt_conv_fusable(const DevParams& hp);
