@@ -63,6 +63,9 @@ constexpr int smem_words() {
 // twiddles per thread) prefetch the 15 pairs of their group into registers
 // before the butterflies, so no global load sits on the critical path.
 constexpr int kTwCache = 511;
+#ifndef HGM_TWFILL_ROLLED
+#define HGM_TWFILL_ROLLED 1
+#endif
 // residues per thread: NB / kElems threads per CTA
 constexpr int kElems = 16;
 // 3-CTA/SM variant: 256 threads x 32 residues, 255 cached twiddle pairs
@@ -357,6 +360,11 @@ __device__ __forceinline__ void inv_round(u64* sm, const u64* __restrict__ tw_ca
 // with m-offset 2^s inside the block).
 __device__ __forceinline__ void fill_tw_cache(u64* cache, const ulonglong2* __restrict__ tw_tab, int outer, int blk,
                                               int count = kTwCache) {
+    // (not unrolled: an unrolled strided loop derives its trip count by an integer
+    // division in every thread, for what is a single pass at count <= blockDim)
+#if HGM_TWFILL_ROLLED
+#pragma unroll 1
+#endif
     for (int i = threadIdx.x; i < count; i += blockDim.x) {
         const int s = 31 - __clz(i + 1);  // i + 1 in [2^s, 2^(s+1))
         const int c = i + 1 - (1 << s);
@@ -372,6 +380,9 @@ __device__ __forceinline__ void fill_tw_cache(u64* cache, const ulonglong2* __re
 // out behind them.  Visible to the CTA after cp_async_wait_all + barrier.
 __device__ __forceinline__ void fill_tw_cache_async(u64* cache, const ulonglong2* __restrict__ tw_tab, int outer,
                                                     int blk, int count) {
+#if HGM_TWFILL_ROLLED
+#pragma unroll 1
+#endif
     for (int i = threadIdx.x; i < count; i += blockDim.x) {
         const int s = 31 - __clz(i + 1);
         const int c = i + 1 - (1 << s);
