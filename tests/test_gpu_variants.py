@@ -48,6 +48,10 @@ PLAN_VARIANTS = {
     "plan-sums-off": {"HGM_KS_PLAN": "0"},
     "masked-key-cache-too-small": {"HGM_MASKED_KEY_MB": "8"},
     "plan-tile-8": {"HGM_PLAN_TILE": "8"},
+    # sums read only by their ModDown keep P^-1 acc over Q (masked keys scaled by P^-1):
+    # off, and on with the unfused finishing pass (k_ks_finish's own prescaled path)
+    "prescale-off": {"HGM_PRESCALE": "0"},
+    "prescale-unfused-finish": {"HGM_FUSED_FINISH": "0"},
 }
 
 
