@@ -8,9 +8,12 @@
 // The smem image is padded one word per 16 (pad()) so that the stride-16 and
 // contiguous-16 access patterns of the three rounds are bank-conflict free.
 // Twiddles are Shoup pairs read through the read-only path; every twiddle is
-// loaded once per group and stage.  For N = 2^15 the two outermost stages run
-// in a separate coalesced pass (pre-pass for the forward transform, post-pass
-// with the N^-1 scaling for the inverse).
+// loaded once per group and stage.  For N = 2^15 a limb is held by a cluster of
+// four CTAs that exchange the two outermost stages through distributed shared
+// memory, one HBM pass per limb (k_ntt_fwd_c4 / k_ntt_inv_c4); HGM_NTT_CLUSTER=0
+// runs those two stages as a separate coalesced pass instead.  The forward
+// transform's fused last stage canonicalises through a 16-entry k*q table in
+// shared memory (Canon, ntt.cu).
 #pragma once
 #include <cuda_runtime.h>
 
