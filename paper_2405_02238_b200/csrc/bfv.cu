@@ -552,6 +552,17 @@ __global__ void k_mask_key(DevCtx cx, const u64* key, const u64* const* masks, u
 // residue (4 products + a residue stay inside the 128-bit column sum:
 // 4 q^2 + q < 2^(s+62) for every prime of the sets); sums of more than
 // kPlanTerms terms continue from the stored output.
+// resident CTAs per SM the register allocation of the three largest elementwise kernels
+// is bounded for (A/B knobs; 4 measured best)
+#ifndef HGM_PLAN_MINB
+#define HGM_PLAN_MINB 4
+#endif
+#ifndef HGM_QTOB2_MINB
+#define HGM_QTOB2_MINB 4
+#endif
+#ifndef HGM_TACC_MINB
+#define HGM_TACC_MINB 4
+#endif
 constexpr u32 kPlanTerms = 2;
 #ifndef HGM_PLAN_WIDE
 #define HGM_PLAN_WIDE 1
@@ -610,7 +621,7 @@ __device__ __forceinline__ void plan_terms(const Prime& P, const u64* sk, u32 ti
     }
 }
 template <typename SH>
-__global__ void __launch_bounds__(kThreads, 4) k_ks_plan(DevCtx cx, u32 n_groups, const PlanGroup* groups,
+__global__ void __launch_bounds__(kThreads, HGM_PLAN_MINB) k_ks_plan(DevCtx cx, u32 n_groups, const PlanGroup* groups,
                                                          const u64* const* mkey, const u32* g,
                                                          const u64* const* D, const u64* const* c0,
                                                          u64* const* out) {
@@ -768,7 +779,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_q_to_b(DevCtx cx, u32 n, const 
 #define HGM_QTOB_PAIR 1
 #endif
 template <typename SH>
-__global__ void __launch_bounds__(kThreads, 4) k_q_to_b2(DevCtx cx, u32 n, const u64* X, u64* XB) {
+__global__ void __launch_bounds__(kThreads, HGM_QTOB2_MINB) k_q_to_b2(DevCtx cx, u32 n, const u64* X, u64* XB) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
     const u32 N = dp->N, L = SH::L, K = SH::K, nB = SH::nB;
     ITEM_LOOP {
@@ -916,7 +927,7 @@ __global__ void k_tensor_s1(DevCtx cx, u32 n, const u64* const* A, const u64* co
 // columns, reduced every kGroup items (the Cols / reduce_acc bounds: 4 products
 // of 60-bit residues, 16 of 55-bit ones) into running sums mod q.
 template <typename SH>
-__global__ void __launch_bounds__(kThreads, 4) k_tensor_acc(DevCtx cx, u32 n, const u32* off, const u64* const* A,
+__global__ void __launch_bounds__(kThreads, HGM_TACC_MINB) k_tensor_acc(DevCtx cx, u32 n, const u32* off, const u64* const* A,
                                                              const u64* const* B, const u64* XB, u64* const* T,
                                                              const unsigned char* init) {
     const DevParams* __restrict__ dp = &c_dp[cx.pid];
