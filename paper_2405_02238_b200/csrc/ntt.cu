@@ -1559,12 +1559,12 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__((1 << LB) / kElems3,
     cg::this_cluster().sync();  // all four quarters transformed
     const ulonglong2* t = pairs(w + 2 * N);
     const u64 w1 = t[1].x, w1s = t[1].y, w2 = t[2].x, w2s = t[2].y, w3 = t[3].x, w3s = t[3].y;
-    const bool scale = !jobs.unscaled;
+    const u32 mode = jobs.unscaled;  // 0: scaled by N^-1, 1: canonical, kLazyOut: [0, 4q)
     u32 quarter[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) quarter[r] = dsmem_base(sm, r);
     u64* a = jv.ptr;
-    const u64 q2 = q << 1;
+    const u64 q2 = q << 1, q3 = q2 + q, q4 = q << 2, q8 = q << 3;
     constexpr int kBatch = 4;
 #pragma unroll 1
     for (int c0 = 0; c0 < COLS / T; c0 += kBatch) {
@@ -1573,21 +1573,35 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__((1 << LB) / kElems3,
         for (int b = 0; b < kBatch; ++b) {
             const int p = pad(blk * COLS + (c0 + b) * T + (int)threadIdx.x);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) x[b][k] = reduce_once(reduce_once(dsmem_ld(quarter[k], p), q2), q);  // [0, 4q) -> [0, q)
+            for (int k = 0; k < 4; ++k) x[b][k] = dsmem_ld(quarter[k], p);  // [0, 4q) (the rounds' bound kGsIn)
         }
 #pragma unroll
         for (int b = 0; b < kBatch; ++b) {
             const int j = blk * COLS + (c0 + b) * T + (int)threadIdx.x;
-            // t = N/4: pairs (0,1) with w[2], (2,3) with w[3]; t = N/2: (0,2), (1,3) with w[1]
-            const u64 y0 = add_mod(x[b][0], x[b][1], q), y1 = shoup_mul(sub_mod(x[b][0], x[b][1], q), w2, w2s, q);
-            const u64 y2 = add_mod(x[b][2], x[b][3], q), y3 = shoup_mul(sub_mod(x[b][2], x[b][3], q), w3, w3s, q);
+            // t = N/4: pairs (0,1) with w[2], (2,3) with w[3]; t = N/2: (0,2), (1,3) with w[1].
+            // Lazy: sums grow to 8q and 16q < 2^64, differences are offset by the
+            // subtrahend's bound and go straight into the Shoup product ([0, 3q), any
+            // 64-bit input); one reduction chain at the end, as short as the output allows.
+            const u64 y0 = x[b][0] + x[b][1], y1 = shoup_lazy3(x[b][0] - x[b][1] + q4, w2, w2s, q);
+            const u64 y2 = x[b][2] + x[b][3], y3 = shoup_lazy3(x[b][2] - x[b][3] + q4, w3, w3s, q);
             u64 z[4];
-            z[0] = add_mod(y0, y2, q);
-            z[2] = shoup_mul(sub_mod(y0, y2, q), w1, w1s, q);
-            z[1] = add_mod(y1, y3, q);
-            z[3] = shoup_mul(sub_mod(y1, y3, q), w1, w1s, q);
+            z[0] = y0 + y2;                                    // < 16q
+            z[2] = shoup_lazy3(y0 - y2 + q8, w1, w1s, q);      // < 3q
+            z[1] = y1 + y3;                                    // < 6q
+            z[3] = shoup_lazy3(y1 - y3 + q3, w1, w1s, q);      // < 3q
+            if (mode == 0) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) __stcs(a + j + k * NB, scale ? shoup_mul(z[k], P.ninv, P.ninv_sh, q) : z[k]);
+                for (int k = 0; k < 4; ++k) z[k] = shoup_mul(z[k], P.ninv, P.ninv_sh, q);
+            } else {
+                z[0] = reduce_once(reduce_once(z[0], q8), q4);
+                z[1] = reduce_once(z[1], q4);
+                if (mode != kLazyOut) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) z[k] = reduce_once(reduce_once(z[k], q2), q);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) __stcs(a + j + k * NB, z[k]);
         }
     }
     cg::this_cluster().sync();  // keep this CTA's shared memory until every remote read is done
