@@ -78,20 +78,32 @@ __device__ __forceinline__ const ulonglong2* pairs(const u64* t) { return reinte
 // A stage maps inputs < b q to outputs < (b + 4) q (U + V with V < 3q, and
 // U - V + 4q); values must stay below 16q <= 2^64 (q < 2^60), so U is reduced
 // by 8q only where b > 12: about every other stage instead of every stage.
-constexpr int fwd_bound(int s) {
-    int b = 1;
+// b0: the bound of the transform's inputs (1 = canonical; 8 for the block stages of the
+// N = 2^15 cluster transform, whose outer stages hand over sums below 7q -- starting
+// at 8 moves the reductions to the even stages without adding one).
+constexpr int fwd_bound(int s, int b0 = 1) {
+    int b = b0;
     for (int i = 0; i < s; ++i) b = (b > 12 ? 8 : b) + 4;
     return b;
 }
-constexpr bool fwd_reduce(int s) { return fwd_bound(s) > 12; }
+constexpr bool fwd_reduce(int s, int b0 = 1) { return fwd_bound(s, b0) > 12; }
+// N = 2^15 forward cluster transform: HGM_C4_LAZY=1 runs its outer stages lazily (no
+// reductions, block stages from the bound 8); exact, measured -1% on the forward
+// transform (the phase is bound by its loads and remote stores, and the last stage
+// then needs one more reduction), so the canonical form stays the default.  The
+// inverse's outer stages are lazy (+7.6%: they sit behind remote loads).
+#ifndef HGM_C4_LAZY
+#define HGM_C4_LAZY 0
+#endif
+constexpr int kC4B0 = HGM_C4_LAZY ? 8 : 1;
 
 // Cooley-Tukey stage r (global stage SG + r) of an R-stage register round
 // (compile-time bounds so the round unrolls and x[] stays in registers).
 // tw(r, c) yields (w, w') for the c-th twiddle of stage r within this group.
-template <int R, int r, int SG, typename Tw>
+template <int R, int r, int SG, int B0, typename Tw>
 __device__ __forceinline__ void fwd_stage(u64 (&x)[1 << R], u64 q, u64 q4, u64 q8, const Tw& tw) {
     constexpr int h = 1 << (R - 1 - r);
-    constexpr bool kReduce = fwd_reduce(SG + r);
+    constexpr bool kReduce = fwd_reduce(SG + r, B0);
 #pragma unroll
     for (int c = 0; c < (1 << r); ++c) {
         u64 w, ws;
@@ -106,7 +118,7 @@ __device__ __forceinline__ void fwd_stage(u64 (&x)[1 << R], u64 q, u64 q4, u64 q
             x[k + h] = U - V + q4;
         }
     }
-    if constexpr (r + 1 < R) fwd_stage<R, r + 1, SG>(x, q, q4, q8, tw);
+    if constexpr (r + 1 < R) fwd_stage<R, r + 1, SG, B0>(x, q, q4, q8, tw);
 }
 
 // Gentleman-Sande rounds track a compile-time bound (units of q) per register
@@ -245,7 +257,8 @@ struct NoLoad {
     __device__ u64 operator()(int) const { return 0; }
 };
 
-template <int LB, int S0, int R, bool kCached, bool kFromGlobal = false, typename Ld = NoLoad, int E = kElems>
+template <int LB, int S0, int R, bool kCached, bool kFromGlobal = false, typename Ld = NoLoad, int E = kElems,
+          int B0 = 1>
 __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_cache,
                                           const ulonglong2* __restrict__ tw_tab,
                                           u64 q, int pre, int blk, const Ld& ld = Ld(),
@@ -276,7 +289,7 @@ __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_ca
                 w = tw_cache[2 * i];
                 ws = tw_cache[2 * i + 1];
             };
-            fwd_stage<R, 0, S0>(x, q, q4, q8, tw);
+            fwd_stage<R, 0, S0, B0>(x, q, q4, q8, tw);
         } else {
             u64 pw[(1 << R) - 1], pws[(1 << R) - 1];
 #pragma unroll
@@ -294,7 +307,7 @@ __device__ __forceinline__ void fwd_round(u64* sm, const u64* __restrict__ tw_ca
                 w = pw[(1 << r) - 1 + c];
                 ws = pws[(1 << r) - 1 + c];
             };
-            fwd_stage<R, 0, S0>(x, q, q4, q8, tw);
+            fwd_stage<R, 0, S0, B0>(x, q, q4, q8, tw);
         }
 #pragma unroll
         for (int k = 0; k < (1 << R); ++k) sm[at(k)] = x[k];
@@ -497,11 +510,11 @@ __device__ __forceinline__ Canon make_canon(u64* tab, const Prime& P) {
 // Last stage with the table reduction: U < kU q (reduced by 8q once where the
 // round bounds allow more), V = w x in [0, 3q), outputs U + V and U - V + 3q
 // below (kU + 3) q canonicalised by `cn`.
-template <int LB, int E = kElems>
+template <int LB, int E = kElems, int B0 = 1>
 __device__ __forceinline__ void store_last_stage_tab(const u64* sm, u64* g, const ulonglong2* __restrict__ tw_tab, u64 q,
                                                      int logN, int blk, const Canon& cn) {
     constexpr int NB = 1 << LB, T = NB / E;
-    constexpr bool kRedU = fwd_bound(LB - 1) > 12;  // U + V must stay below 16q
+    constexpr bool kRedU = fwd_bound(LB - 1, B0) > 12;  // U + V must stay below 16q
     ulonglong2* g2 = reinterpret_cast<ulonglong2*>(g);
     const int tw0 = (1 << (logN - 1)) + (blk << (LB - 1));
     const u64 q3 = q + (q << 1), q8 = q << 3;
@@ -519,11 +532,11 @@ __device__ __forceinline__ void store_last_stage_tab(const u64* sm, u64* g, cons
 }
 // The same handing (U + V, U - V + 3q), both below 11q, to `st`: the consumer may
 // add up to 4q more before canonicalising with the same table.
-template <int LB, typename St, int E = kElems>
+template <int LB, typename St, int E = kElems, int B0 = 1>
 __device__ __forceinline__ void store_last_stage_io_tab(const u64* sm, const St& st, const ulonglong2* __restrict__ tw_tab,
                                                         u64 q, int logN, int blk) {
     constexpr int NB = 1 << LB, T = NB / E;
-    constexpr bool kRedU = fwd_bound(LB - 1) > 8;
+    constexpr bool kRedU = fwd_bound(LB - 1, B0) > 8;
     const int tw0 = (1 << (logN - 1)) + (blk << (LB - 1));
     const u64 q3 = q + (q << 1), q8 = q << 3;
 #pragma unroll 4
@@ -956,31 +969,48 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__((1 << LB) / kElems3,
 #pragma unroll
         for (int b = 0; b < kBatch; ++b) {
             const int j = blk * COLS + (c0 + b) * T + (int)threadIdx.x;
+            const int p = pad(j);
+#if HGM_C4_LAZY
+            // lazy: Shoup products in [0, 3q), differences offset by 3q, no reduction --
+            // the quarters receive values below 7q and the block stages start from the
+            // bound 8 (kC4B0), which costs them no extra reduction
+            const u64 q3 = q + (q << 1);
+            u64 V = shoup_lazy3(x[b][2], w1, w1s, q);
+            const u64 y0 = x[b][0] + V, y2 = x[b][0] - V + q3;  // < 4q
+            V = shoup_lazy3(x[b][3], w1, w1s, q);
+            const u64 y1 = x[b][1] + V, y3 = x[b][1] - V + q3;  // < 4q
+            V = shoup_lazy3(y1, w2, w2s, q);
+            dsmem_st(quarter[0], p, y0 + V);                    // < 7q
+            dsmem_st(quarter[1], p, y0 - V + q3);
+            V = shoup_lazy3(y3, w3, w3s, q);
+            dsmem_st(quarter[2], p, y2 + V);
+            dsmem_st(quarter[3], p, y2 - V + q3);
+#else
             u64 V = shoup_mul(x[b][2], w1, w1s, q);
             const u64 y0 = add_mod(x[b][0], V, q), y2 = sub_mod(x[b][0], V, q);
             V = shoup_mul(x[b][3], w1, w1s, q);
             const u64 y1 = add_mod(x[b][1], V, q), y3 = sub_mod(x[b][1], V, q);
             V = shoup_mul(y1, w2, w2s, q);
-            const int p = pad(j);
             dsmem_st(quarter[0], p, add_mod(y0, V, q));
             dsmem_st(quarter[1], p, sub_mod(y0, V, q));
             V = shoup_mul(y3, w3, w3s, q);
             dsmem_st(quarter[2], p, add_mod(y2, V, q));
             dsmem_st(quarter[3], p, sub_mod(y2, V, q));
+#endif
         }
     }
     cp_async_wait_all();
     cg::this_cluster().sync();
-    fwd_round<LB, 0, 4, true, false, NoLoad, kElems3>(sm, cache, pairs(w), q, 2, blk);
+    fwd_round<LB, 0, 4, true, false, NoLoad, kElems3, kC4B0>(sm, cache, pairs(w), q, 2, blk);
     __syncthreads();
-    fwd_round<LB, 4, 4, true, false, NoLoad, kElems3>(sm, cache, pairs(w), q, 2, blk);
+    fwd_round<LB, 4, 4, true, false, NoLoad, kElems3, kC4B0>(sm, cache, pairs(w), q, 2, blk);
     __syncthreads();
-    fwd_round<LB, 8, LB - 9, false, false, NoLoad, kElems3>(sm, cache, pairs(w), q, 2, blk);
+    fwd_round<LB, 8, LB - 9, false, false, NoLoad, kElems3, kC4B0>(sm, cache, pairs(w), q, 2, blk);
     __syncthreads();
     const u32 pair0 = (u32)blk << (LB - 1);
 #if HGM_LAST_TAB
     auto st = [&](int i, u64 v0, u64 v1) { io.store_lazy(dp, job, pair0 + (u32)i, v0, v1, cn); };
-    store_last_stage_io_tab<LB, decltype(st), kElems3>(sm, st, pairs(w), q, logN, blk);
+    store_last_stage_io_tab<LB, decltype(st), kElems3, kC4B0>(sm, st, pairs(w), q, logN, blk);
 #else
     auto st = [&](int i, u64 v0, u64 v1) { io.store(dp, job, pair0 + (u32)i, v0, v1); };
     store_last_stage_io<LB, decltype(st), kElems3>(sm, st, pairs(w), q, logN, blk);
@@ -1503,29 +1533,46 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__((1 << LB) / kElems3,
 #pragma unroll
         for (int b = 0; b < kBatch; ++b) {
             const int j = blk * COLS + (c0 + b) * T + (int)threadIdx.x;
+            const int p = pad(j);
+#if HGM_C4_LAZY
+            // lazy: Shoup products in [0, 3q), differences offset by 3q, no reduction --
+            // the quarters receive values below 7q and the block stages start from the
+            // bound 8 (kC4B0), which costs them no extra reduction
+            const u64 q3 = q + (q << 1);
+            u64 V = shoup_lazy3(x[b][2], w1, w1s, q);
+            const u64 y0 = x[b][0] + V, y2 = x[b][0] - V + q3;  // < 4q
+            V = shoup_lazy3(x[b][3], w1, w1s, q);
+            const u64 y1 = x[b][1] + V, y3 = x[b][1] - V + q3;  // < 4q
+            V = shoup_lazy3(y1, w2, w2s, q);
+            dsmem_st(quarter[0], p, y0 + V);                    // < 7q
+            dsmem_st(quarter[1], p, y0 - V + q3);
+            V = shoup_lazy3(y3, w3, w3s, q);
+            dsmem_st(quarter[2], p, y2 + V);
+            dsmem_st(quarter[3], p, y2 - V + q3);
+#else
             u64 V = shoup_mul(x[b][2], w1, w1s, q);
             const u64 y0 = add_mod(x[b][0], V, q), y2 = sub_mod(x[b][0], V, q);
             V = shoup_mul(x[b][3], w1, w1s, q);
             const u64 y1 = add_mod(x[b][1], V, q), y3 = sub_mod(x[b][1], V, q);
             V = shoup_mul(y1, w2, w2s, q);
-            const int p = pad(j);
             dsmem_st(quarter[0], p, add_mod(y0, V, q));
             dsmem_st(quarter[1], p, sub_mod(y0, V, q));
             V = shoup_mul(y3, w3, w3s, q);
             dsmem_st(quarter[2], p, add_mod(y2, V, q));
             dsmem_st(quarter[3], p, sub_mod(y2, V, q));
+#endif
         }
     }
     cp_async_wait_all();
     cg::this_cluster().sync();  // every quarter complete (and the twiddle caches)
-    fwd_round<LB, 0, 4, true, false, NoLoad, kElems3>(sm, cache, pairs(w), q, 2, blk);
+    fwd_round<LB, 0, 4, true, false, NoLoad, kElems3, kC4B0>(sm, cache, pairs(w), q, 2, blk);
     __syncthreads();
-    fwd_round<LB, 4, 4, true, false, NoLoad, kElems3>(sm, cache, pairs(w), q, 2, blk);
+    fwd_round<LB, 4, 4, true, false, NoLoad, kElems3, kC4B0>(sm, cache, pairs(w), q, 2, blk);
     __syncthreads();
-    fwd_round<LB, 8, LB - 9, false, false, NoLoad, kElems3>(sm, cache, pairs(w), q, 2, blk);
+    fwd_round<LB, 8, LB - 9, false, false, NoLoad, kElems3, kC4B0>(sm, cache, pairs(w), q, 2, blk);
     __syncthreads();
 #if HGM_LAST_TAB
-    store_last_stage_tab<LB, kElems3>(sm, jv.ptr + ((size_t)blk << LB), pairs(w), q, logN, blk, cn);
+    store_last_stage_tab<LB, kElems3, kC4B0>(sm, jv.ptr + ((size_t)blk << LB), pairs(w), q, logN, blk, cn);
 #else
     store_last_stage<LB, kElems3>(sm, jv.ptr + ((size_t)blk << LB), pairs(w), q, logN, blk);
 #endif
