@@ -1612,7 +1612,10 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__((1 << LB) / kElems3,
     for (int r = 0; r < 4; ++r) quarter[r] = dsmem_base(sm, r);
     u64* a = jv.ptr;
     const u64 q2 = q << 1, q3 = q2 + q, q4 = q << 2, q8 = q << 3;
-    constexpr int kBatch = 4;
+#ifndef HGM_C4_INV_BATCH
+#define HGM_C4_INV_BATCH 2
+#endif
+    constexpr int kBatch = HGM_C4_INV_BATCH;  // columns (4 remote loads each) in flight per thread
 #pragma unroll 1
     for (int c0 = 0; c0 < COLS / T; c0 += kBatch) {
         u64 x[kBatch][4];
